@@ -1,0 +1,178 @@
+/*
+ * freqcache_b200 — C ABI of the B200-native frequency-aware embedding cache.
+ *
+ * Drop-in boundary for the reference's cached-embedding path
+ * (/root/reference/pkg/src/freqcache, a pure-Python/numpy package with no FFI of
+ * its own). Each entry point replaces one reference call; the citation is the
+ * reference function whose semantics it reproduces bit-for-bit. The Python host
+ * package `paper_2208_05321_b200` binds these with ctypes and keeps the reference
+ * names, argument meanings and exception classes.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. "dev" pointers are CUDA device pointers,
+ *    "host" pointers are host memory. Streams are cudaStream_t passed as void*.
+ *  - Every call returns an fc_status (0 = OK). Validation errors are reported
+ *    BEFORE any state mutation, like the reference (cache_manager.py:261-282).
+ *  - Calls that must hand scalars back (prepare, flush, warmup) synchronise the
+ *    given stream; everything else is stream-ordered and asynchronous.
+ *  - One handle is single-writer; independent handles may run
+ *    concurrently on different streams/devices.
+ */
+#ifndef FREQCACHE_B200_H
+#define FREQCACHE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum fc_status {
+  FC_OK = 0,
+  FC_ERR_BATCH_EXCEEDS_CAPACITY = 1, /* BatchExceedsCapacity   cache_manager.py:35-40,278-282 */
+  FC_ERR_ID_OUT_OF_RANGE = 2,        /* ValueError("id out of range: ...")  :272-275 */
+  FC_ERR_INSUFFICIENT_EVICTABLE = 3, /* InsufficientEvictable  :43-44,67-72 */
+  FC_ERR_INSUFFICIENT_FREE_SLOTS = 4,/* InsufficientFreeSlots  :47-52,313-317 */
+  FC_ERR_BUFFER_TOO_SMALL = 5,       /* BufferTooSmall         transmitter.py:28-29,85-88 */
+  FC_ERR_CUDA = 6,
+  FC_ERR_BAD_ARG = 7,                /* ValueError for bad modes / sizes */
+  FC_ERR_SLOT_OUT_OF_RANGE = 8,      /* IndexError             cache_manager.py:397-399 */
+  FC_ERR_NOT_EMPTY = 9,              /* ValueError("warmup requires an empty cache") :365-366 */
+  FC_ERR_NO_SLOW_TIER = 10
+} fc_status;
+
+typedef enum fc_write_back { FC_WB_DIRTY_ONLY = 0, FC_WB_ALWAYS = 1 } fc_write_back;     /* :31 */
+typedef enum fc_evict_mode { FC_EVICT_OCCUPANCY_AWARE = 0, FC_EVICT_PAPER_LITERAL = 1 } fc_evict_mode; /* :32 */
+typedef enum fc_pool_mode { FC_POOL_SUM = 0, FC_POOL_MEAN = 1 } fc_pool_mode;
+typedef enum fc_optim { FC_OPT_SGD = 0, FC_OPT_ADAGRAD = 1 } fc_optim;
+
+typedef struct fc_cache fc_cache;   /* opaque handle: one CacheStack (cache_manager.py:441-562) */
+
+/* Outcome of one prepare call (PrepareResult, cache_manager.py:173-194, plus the
+ * two TransferReports' row counts, transmitter.py:62-72). */
+typedef struct fc_prepare_info {
+  int64_t unique;        /* |U| */
+  int64_t hits;
+  int64_t misses;        /* rows admitted slow -> fast */
+  int64_t evictions;     /* victims chosen */
+  int64_t rows_to_slow;  /* victims written back (dirty_only filters by dirty bit) */
+  int64_t free_count;    /* free slots after the call */
+  int64_t bad_id;        /* offending id for FC_ERR_ID_OUT_OF_RANGE */
+  int64_t candidates;    /* evictable rows seen when eviction ran (diagnostic) */
+} fc_prepare_info;
+
+/* Device pointers of the handle-owned state, for zero-copy views (torch tensors). */
+typedef struct fc_views {
+  float* fast_rows;       /* [capacity, row_width] fp32 fast tier (FastTierStore.slots)  */
+  int32_t* slot_to_rank;  /* [capacity]   (CacheState.slot_to_rank, int64 in reference)  */
+  int32_t* rank_to_slot;  /* [num_ids]    (CacheState.rank_to_slot)                      */
+  uint8_t* dirty;         /* [capacity]   (CacheState.dirty)                             */
+  int32_t* rank_of;       /* [num_ids]    (IdxMap.rank_of on device)                     */
+  float* fast_state;      /* [capacity, state_width] optimizer state or NULL             */
+  int64_t capacity, num_ids, dim, state_width;
+} fc_views;
+
+/* ---- lifecycle ------------------------------------------------------------ */
+/* CacheState(capacity, num_ids) + FastTierStore + Transmitter(buffer_bytes)
+ * (cache_manager.py:129-139, store.py:62-87, transmitter.py:75-94).
+ * state_width: optimizer-state columns cached with each row (0 = none,
+ * dim = element-wise Adagrad). buffer_bytes only drives message accounting and
+ * the staged engine's chunk size (chunk = floor(buffer/row_bytes) rows). */
+int fc_create(int64_t num_ids, int64_t capacity, int32_t dim, int32_t state_width,
+              int32_t write_back, int32_t evict_mode, int64_t buffer_bytes, int32_t device,
+              fc_cache** out);
+int fc_destroy(fc_cache* h);
+const char* fc_last_error(void);
+int fc_get_views(fc_cache* h, fc_views* out);
+
+/* Pinned, device-mapped host memory for the slow tier (page-locked once). */
+int fc_host_alloc(int64_t bytes, void** out);
+int fc_host_free(void* p);
+
+/* IdxMap.rank_of (freq_stats.py:52-73), host int64[num_ids] -> device int32. */
+int fc_set_idx_map(fc_cache* h, const int64_t* rank_of_host, void* stream);
+
+/* SlowTierStore (store.py:39-59): rank-indexed rows [num_ids, dim] (+ optional
+ * state rows [num_ids, state_width]) in pinned mapped host memory from
+ * fc_host_alloc (or any cudaHostRegister-ed range). Row strides in floats. */
+int fc_attach_slow_tier(fc_cache* h, float* rows_host, int64_t row_stride,
+                        float* state_host, int64_t state_stride);
+
+/* Per-call modes of prepare_cache (write_back, evict_mode kwargs, cache_manager.py:241-245). */
+int fc_set_modes(fc_cache* h, int32_t write_back, int32_t evict_mode);
+/* CacheState.free_count after the last synchronising call. */
+int64_t fc_free_count(fc_cache* h);
+
+/* ---- the cache verbs ------------------------------------------------------- */
+/* warmup (cache_manager.py:351-390): ranks 0..k-1 -> slots 0..k-1; empty cache only. */
+int fc_warmup(fc_cache* h, int64_t k, void* stream);
+
+/* prepare_cache (cache_manager.py:234-348), the per-batch hot path.
+ * ids_dev: n ids (int64 if ids_bytes==8, int32 if 4). Outputs (device, caller
+ * allocated, capacity >= min(n, capacity) entries; `inverse` n entries):
+ * unique ids ascending, their counts, ranks and final slots, and for every id
+ * its position in the unique list (PrepareResult.slots_for_ids, :187-190).
+ * Synchronises `stream`; fills `info`. On error nothing was mutated. */
+int fc_prepare(fc_cache* h, const void* ids_dev, int32_t ids_bytes, int64_t n, int64_t batch_seq,
+               int32_t* unique_ids, int32_t* unique_counts, int32_t* unique_ranks,
+               int32_t* unique_slots, int32_t* inverse, void* stream, fc_prepare_info* info);
+
+/* Event-log payload of the last prepare (CacheEvent, cache_manager.py:78-99):
+ * evicted ranks (descending) and admitted ranks (ascending), device -> host. */
+int fc_last_events(fc_cache* h, int64_t* evicted_host, int64_t* admitted_host, void* stream);
+
+/* flush (cache_manager.py:403-415): every dirty slot written back; rows stay. */
+int fc_flush(fc_cache* h, void* stream, int64_t* rows_written);
+
+/* mark_dirty (cache_manager.py:393-400). */
+int fc_mark_dirty(fc_cache* h, const int64_t* slots_dev, int64_t n, void* stream);
+
+/* select_evictions (cache_manager.py:205-216): slots of the `needed` largest
+ * occupied ranks outside `protected`, in descending-rank order. */
+int fc_select_evictions(fc_cache* h, int64_t needed, const int64_t* protected_dev, int64_t n_protected,
+                        int64_t* slots_host, void* stream);
+
+/* ---- lookups and updates ---------------------------------------------------- */
+/* Pooled EmbeddingBag forward over cached rows (north star; semantics of
+ * torch.nn.functional.embedding_bag; mean+psw = sum(w*row)/L, empty bag -> 0).
+ * occurrence j uses row fast[unique_slots[inverse[j]]]. offsets == NULL means
+ * one occurrence per bag (gather, cache_manager.py:418-420).
+ * out: [n_bags, dim] fp32. offsets are int64 if offsets_bytes==8 else int32. */
+int fc_pooled_forward(fc_cache* h, const int32_t* unique_slots, const int32_t* inverse, int64_t n,
+                      const void* offsets, int32_t offsets_bytes, int64_t n_bags,
+                      int32_t include_last_offset, const float* per_sample_weights, int32_t mode,
+                      float* out, void* stream);
+
+/* Rows of the unique ids (CacheStack.gather_unique, cache_manager.py:509-510). */
+int fc_gather_rows(fc_cache* h, const int32_t* slots, int64_t n, float* out, void* stream);
+
+/* apply_unique_update (cache_manager.py:517-523): fast[slot[p]] += add[p]; dirty. */
+int fc_apply_unique_update(fc_cache* h, const int32_t* unique_slots, int64_t u, const float* add,
+                           void* stream);
+
+/* The simulator's deterministic update fused on device (simulator.py:246-260,433):
+ * add[p][c] = ((hash24(id_p, salt)*2^-24 - 0.5) * count_p) * colw[c]. */
+int fc_apply_synthetic_update(fc_cache* h, const int32_t* unique_ids, const int32_t* unique_counts,
+                              const int32_t* unique_slots, int64_t u, uint64_t salt,
+                              const float* colw, void* stream);
+
+/* scatter_update (cache_manager.py:423-438): per-occurrence deltas accumulated in
+ * batch order (bit-exact with np.add.at), every unique slot dirtied. */
+int fc_scatter_update(fc_cache* h, const int32_t* unique_slots, const int32_t* inverse,
+                      const int32_t* unique_counts, int64_t u, int64_t n, const float* deltas,
+                      void* stream);
+
+/* Fused backward of the pooled forward + sparse optimizer row update (north star
+ * item 6): sort occurrences by unique row, segmented reduction of
+ * grad_out[bag(j)] * coef_j, then SGD (w -= lr*g) or Adagrad
+ * (G += g^2; w -= lr*g/(sqrt(G)+eps)) on the cached rows; rows dirtied. */
+int fc_backward_update(fc_cache* h, const int32_t* unique_slots, const int32_t* inverse,
+                       const int32_t* unique_counts, int64_t u, int64_t n,
+                       const void* offsets, int32_t offsets_bytes, int64_t n_bags,
+                       int32_t include_last_offset, const float* per_sample_weights, int32_t mode,
+                       const float* grad_out, int32_t optim, float lr, float eps, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FREQCACHE_B200_H */

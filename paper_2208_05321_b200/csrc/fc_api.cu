@@ -1,0 +1,459 @@
+// C ABI entry points (include/freqcache_b200.h). Each call validates on the host
+// what the reference validates before mutation, launches the device sequence on
+// the caller's stream and, where the reference returns scalars, synchronises.
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "fc_internal.cuh"
+
+namespace fc {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error("CUDA error %s (%s) in %s", cudaGetErrorName(e), cudaGetErrorString(e), what);
+  return FC_ERR_CUDA;
+}
+
+int ensure_scratch(fc_cache* h, size_t bytes) {
+  if (bytes <= h->scratch_bytes) return FC_OK;
+  size_t nb = std::max(bytes, h->scratch_bytes + h->scratch_bytes / 2);
+  if (h->scratch) FC_CUDA(cudaFree(h->scratch));
+  h->scratch = nullptr;
+  h->scratch_bytes = 0;
+  FC_CUDA(cudaMalloc(&h->scratch, nb));
+  h->scratch_bytes = nb;
+  return FC_OK;
+}
+
+// sync the stream through the handle's event and pull the counters
+static int sync_counters(fc_cache* h, cudaStream_t st) {
+  FC_CUDA(cudaMemcpyAsync(h->ctr_host, h->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  FC_CUDA(cudaEventRecord(h->done, st));
+  FC_CUDA(cudaEventSynchronize(h->done));
+  h->host_free = h->ctr_host->free_count;
+  return FC_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+static int dalloc(T** p, size_t count) {
+  FC_CUDA(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
+  return FC_OK;
+}
+
+static void release(fc_cache* h) {
+  void* dev[] = {h->rank_of, h->rank_to_slot, h->slot_to_rank, h->dirty, h->fast, h->fast_state,
+                 h->res_bits, h->free_bits, h->id_bits, h->miss_bits, h->prot_bits, h->aux,
+                 h->evicted_ranks, h->victim_slots, h->wb_ranks, h->wb_stage, h->wb_stage_state,
+                 h->admitted_ranks, h->target_slots, h->block_cnt, h->block_cnt2, h->ctr, h->scratch};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (h->ctr_host) cudaFreeHost(h->ctr_host);
+  if (h->done) cudaEventDestroy(h->done);
+  delete h;
+}
+
+}  // namespace fc
+
+using namespace fc;
+
+#define FC_TRY(expr)          \
+  do {                        \
+    int rc__ = (expr);        \
+    if (rc__) return rc__;    \
+  } while (0)
+
+extern "C" {
+
+const char* fc_last_error(void) { return g_err; }
+
+int fc_host_alloc(int64_t bytes, void** out) {
+  if (!out || bytes < 0) return FC_ERR_BAD_ARG;
+  *out = nullptr;
+  FC_CUDA(cudaHostAlloc(out, std::max<int64_t>(bytes, 16), cudaHostAllocMapped | cudaHostAllocPortable));
+  return FC_OK;
+}
+
+int fc_host_free(void* p) {
+  if (p) FC_CUDA(cudaFreeHost(p));
+  return FC_OK;
+}
+
+int fc_create(int64_t num_ids, int64_t capacity, int32_t dim, int32_t state_width, int32_t write_back,
+              int32_t evict_mode, int64_t buffer_bytes, int32_t device, fc_cache** out) {
+  if (!out) return FC_ERR_BAD_ARG;
+  *out = nullptr;
+  if (capacity < 1) {
+    set_error("capacity must be >= 1");
+    return FC_ERR_BAD_ARG;
+  }
+  if (capacity > num_ids) {
+    set_error("capacity %lld exceeds num_ids %lld", (long long)capacity, (long long)num_ids);
+    return FC_ERR_BAD_ARG;
+  }
+  if (num_ids > INT32_MAX - 64 || dim < 1 || state_width < 0 || buffer_bytes < 1 ||
+      (write_back != FC_WB_DIRTY_ONLY && write_back != FC_WB_ALWAYS) ||
+      (evict_mode != FC_EVICT_OCCUPANCY_AWARE && evict_mode != FC_EVICT_PAPER_LITERAL)) {
+    set_error("bad geometry or mode");
+    return FC_ERR_BAD_ARG;
+  }
+  DeviceGuard dg(device);
+  fc_cache* h = new fc_cache();
+  std::memset(h, 0, sizeof(*h));
+  h->num_ids = num_ids;
+  h->capacity = (int32_t)capacity;
+  h->dim = dim;
+  h->sw = state_width;
+  h->write_back = write_back;
+  h->evict_mode = evict_mode;
+  h->buffer_bytes = buffer_bytes;
+  h->device = device;
+  h->nw_ids = ((num_ids + 31) / 32 + 3) / 4 * 4;
+  h->nw_slots = ((capacity + 31) / 32 + 3) / 4 * 4;
+  const size_t C = (size_t)capacity;
+  int rc = FC_OK;
+#define A(ptr, n)                  \
+  if ((rc = dalloc(&(ptr), (n)))) { \
+    release(h);                    \
+    return rc;                     \
+  }
+  A(h->rank_of, num_ids);
+  A(h->rank_to_slot, num_ids);
+  A(h->aux, num_ids);
+  A(h->slot_to_rank, C);
+  A(h->dirty, C);
+  A(h->fast, C * dim);
+  if (state_width) A(h->fast_state, C * state_width);
+  A(h->res_bits, h->nw_ids);
+  A(h->id_bits, h->nw_ids);
+  A(h->miss_bits, h->nw_ids);
+  A(h->prot_bits, h->nw_ids);
+  A(h->free_bits, h->nw_slots);
+  A(h->evicted_ranks, C);
+  A(h->victim_slots, C);
+  A(h->wb_ranks, C);
+  A(h->wb_stage, C * dim);
+  if (state_width) A(h->wb_stage_state, C * state_width);
+  A(h->admitted_ranks, C);
+  A(h->target_slots, C);
+  A(h->block_cnt, kMaxScanBlocks + 1);
+  A(h->block_cnt2, kMaxScanBlocks + 1);
+  A(h->ctr, 1);
+#undef A
+  cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&h->ctr_host), sizeof(Counters), cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->done, cudaEventDisableTiming);
+  if (e == cudaSuccess) e = cudaMemset(h->rank_to_slot, 0xff, num_ids * 4);
+  if (e == cudaSuccess) e = cudaMemset(h->slot_to_rank, 0xff, C * 4);
+  if (e == cudaSuccess) e = cudaMemset(h->aux, 0, num_ids * 4);
+  if (e == cudaSuccess) e = cudaMemset(h->dirty, 0, C);
+  if (e == cudaSuccess) e = cudaMemset(h->fast, 0, C * dim * 4);
+  if (e == cudaSuccess && state_width) e = cudaMemset(h->fast_state, 0, C * state_width * 4);
+  for (uint32_t* b : {h->res_bits, h->id_bits, h->miss_bits, h->prot_bits})
+    if (e == cudaSuccess) e = cudaMemset(b, 0, h->nw_ids * 4);
+  if (e == cudaSuccess) {  // every slot starts free
+    std::vector<uint32_t> fb(h->nw_slots, 0u);
+    for (int64_t s = 0; s < capacity; ++s) fb[s >> 5] |= 1u << (s & 31);
+    e = cudaMemcpy(h->free_bits, fb.data(), fb.size() * 4, cudaMemcpyHostToDevice);
+  }
+  if (e == cudaSuccess) {
+    Counters c0;
+    std::memset(&c0, 0, sizeof(c0));
+    c0.free_count = (int32_t)capacity;
+    e = cudaMemcpy(h->ctr, &c0, sizeof(c0), cudaMemcpyHostToDevice);
+  }
+  if (e != cudaSuccess) {
+    rc = cuda_fail(e, "fc_create");
+    release(h);
+    return rc;
+  }
+  h->host_free = (int32_t)capacity;
+  *out = h;
+  return FC_OK;
+}
+
+int fc_destroy(fc_cache* h) {
+  if (!h) return FC_OK;
+  DeviceGuard dg(h->device);
+  cudaDeviceSynchronize();
+  release(h);
+  return FC_OK;
+}
+
+int fc_get_views(fc_cache* h, fc_views* v) {
+  if (!h || !v) return FC_ERR_BAD_ARG;
+  v->fast_rows = h->fast;
+  v->slot_to_rank = h->slot_to_rank;
+  v->rank_to_slot = h->rank_to_slot;
+  v->dirty = h->dirty;
+  v->rank_of = h->rank_of;
+  v->fast_state = h->fast_state;
+  v->capacity = h->capacity;
+  v->num_ids = h->num_ids;
+  v->dim = h->dim;
+  v->state_width = h->sw;
+  return FC_OK;
+}
+
+int fc_set_modes(fc_cache* h, int32_t write_back, int32_t evict_mode) {
+  if (!h || (write_back != FC_WB_DIRTY_ONLY && write_back != FC_WB_ALWAYS) ||
+      (evict_mode != FC_EVICT_OCCUPANCY_AWARE && evict_mode != FC_EVICT_PAPER_LITERAL))
+    return FC_ERR_BAD_ARG;
+  h->write_back = write_back;
+  h->evict_mode = evict_mode;
+  return FC_OK;
+}
+
+int64_t fc_free_count(fc_cache* h) { return h ? h->host_free : -1; }
+
+int fc_set_idx_map(fc_cache* h, const int64_t* rank_of_host, void* stream) {
+  if (!h || !rank_of_host) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  std::vector<int32_t> r((size_t)h->num_ids);
+  for (int64_t i = 0; i < h->num_ids; ++i) {
+    const int64_t v = rank_of_host[i];
+    if (v < 0 || v >= h->num_ids) {
+      set_error("rank_of[%lld]=%lld outside [0, %lld)", (long long)i, (long long)v, (long long)h->num_ids);
+      return FC_ERR_BAD_ARG;
+    }
+    r[(size_t)i] = (int32_t)v;
+  }
+  cudaStream_t st = as_stream(stream);
+  FC_CUDA(cudaMemcpyAsync(h->rank_of, r.data(), r.size() * 4, cudaMemcpyHostToDevice, st));
+  FC_CUDA(cudaStreamSynchronize(st));
+  return FC_OK;
+}
+
+int fc_attach_slow_tier(fc_cache* h, float* rows_host, int64_t row_stride, float* state_host, int64_t state_stride) {
+  if (!h || !rows_host || row_stride < h->dim) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  void* dptr = nullptr;
+  cudaError_t e = cudaHostGetDevicePointer(&dptr, rows_host, 0);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    set_error("slow tier must live in pinned mapped host memory (fc_host_alloc): %s", cudaGetErrorString(e));
+    return FC_ERR_BAD_ARG;
+  }
+  h->slow = static_cast<float*>(dptr);
+  h->slow_ld = row_stride;
+  if (h->sw) {
+    if (!state_host || state_stride < h->sw) {
+      set_error("optimizer-state rows required (state_width=%d)", h->sw);
+      return FC_ERR_BAD_ARG;
+    }
+    e = cudaHostGetDevicePointer(&dptr, state_host, 0);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      set_error("slow state must be pinned mapped host memory");
+      return FC_ERR_BAD_ARG;
+    }
+    h->slow_state = static_cast<float*>(dptr);
+    h->state_ld = state_stride;
+  }
+  return FC_OK;
+}
+
+int fc_warmup(fc_cache* h, int64_t k, void* stream) {
+  if (!h) return FC_ERR_BAD_ARG;
+  if (k < 0 || k > h->capacity) {
+    set_error("warmup k must be in [0, capacity=%d], got %lld", h->capacity, (long long)k);
+    return FC_ERR_BAD_ARG;
+  }
+  if (h->host_free != h->capacity) {
+    set_error("warmup requires an empty cache");
+    return FC_ERR_NOT_EMPTY;
+  }
+  if (k == 0) return FC_OK;
+  if (!h->slow) return FC_ERR_NO_SLOW_TIER;
+  if ((int64_t)h->dim * 4 > h->buffer_bytes) {
+    set_error("row of %d B cannot fit in a %lld B buffer", h->dim * 4, (long long)h->buffer_bytes);
+    return FC_ERR_BUFFER_TOO_SMALL;
+  }
+  DeviceGuard dg(h->device);
+  cudaStream_t st = as_stream(stream);
+  // ranks 0..k-1 are contiguous in the slow tier: one DMA copy, no gather
+  FC_CUDA(cudaMemcpy2DAsync(h->fast, (size_t)h->dim * 4, h->slow, (size_t)h->slow_ld * 4, (size_t)h->dim * 4, (size_t)k,
+                            cudaMemcpyDefault, st));
+  if (h->sw)
+    FC_CUDA(cudaMemcpy2DAsync(h->fast_state, (size_t)h->sw * 4, h->slow_state, (size_t)h->state_ld * 4,
+                              (size_t)h->sw * 4, (size_t)k, cudaMemcpyDefault, st));
+  FC_TRY(launch_warmup_state(h, k, st));
+  return sync_counters(h, st);
+}
+
+int fc_prepare(fc_cache* h, const void* ids, int32_t ids_bytes, int64_t n, int64_t batch_seq, int32_t* uids,
+               int32_t* ucnt, int32_t* uranks, int32_t* uslots, int32_t* inverse, void* stream, fc_prepare_info* info) {
+  (void)batch_seq;
+  if (!h || !info || (ids_bytes != 4 && ids_bytes != 8) || n < 0 || n > INT32_MAX) return FC_ERR_BAD_ARG;
+  std::memset(info, 0, sizeof(*info));
+  info->free_count = h->host_free;
+  if (n == 0) return FC_OK;
+  if (!h->slow) return FC_ERR_NO_SLOW_TIER;
+  DeviceGuard dg(h->device);
+  cudaStream_t st = as_stream(stream);
+  FC_TRY(launch_prepare(h, ids, ids_bytes, n, uids, ucnt, uranks, uslots, inverse, st));
+  FC_TRY(sync_counters(h, st));
+  const Counters& c = *h->ctr_host;
+  info->unique = c.unique;
+  info->free_count = c.free_count;
+  info->candidates = c.candidates;
+  h->last_needed = 0;
+  h->last_misses = 0;
+  switch (c.err) {
+    case FC_OK:
+      break;
+    case FC_ERR_ID_OUT_OF_RANGE:
+      info->bad_id = (c.lo != LLONG_MAX) ? c.lo : c.hi;
+      set_error("id out of range: %lld not in [0, %lld)", (long long)info->bad_id, (long long)h->num_ids);
+      return c.err;
+    case FC_ERR_BATCH_EXCEEDS_CAPACITY:
+      set_error("batch has %d unique ids but the fast tier holds %d; the cache ratio is too small for this batch",
+                c.unique, h->capacity);
+      return c.err;
+    case FC_ERR_INSUFFICIENT_FREE_SLOTS:
+      set_error("%d rows to admit but only %d free slots (evict_mode='paper_literal' left the tier over-full)",
+                c.misses, c.free_count + c.needed);
+      return c.err;
+    case FC_ERR_INSUFFICIENT_EVICTABLE:
+      set_error("need %d victims but only %d evictable rows", c.needed, c.candidates);
+      return c.err;
+    case FC_ERR_BUFFER_TOO_SMALL:
+      set_error("row of %d B cannot fit in a %lld B buffer", h->dim * 4, (long long)h->buffer_bytes);
+      return c.err;
+    default:
+      set_error("internal error %d in prepare", c.err);
+      return c.err;
+  }
+  info->misses = c.misses;
+  info->hits = c.unique - c.misses;
+  info->evictions = c.needed;
+  info->rows_to_slow = c.wb_rows;
+  h->last_needed = c.needed;
+  h->last_misses = c.misses;
+  return FC_OK;
+}
+
+int fc_last_events(fc_cache* h, int64_t* evicted_host, int64_t* admitted_host, void* stream) {
+  if (!h) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  cudaStream_t st = as_stream(stream);
+  std::vector<int32_t> a((size_t)h->last_needed), b((size_t)h->last_misses);
+  if (!a.empty()) FC_CUDA(cudaMemcpyAsync(a.data(), h->evicted_ranks, a.size() * 4, cudaMemcpyDeviceToHost, st));
+  if (!b.empty()) FC_CUDA(cudaMemcpyAsync(b.data(), h->admitted_ranks, b.size() * 4, cudaMemcpyDeviceToHost, st));
+  FC_CUDA(cudaStreamSynchronize(st));
+  for (size_t i = 0; i < a.size(); ++i) evicted_host[i] = a[i];
+  for (size_t i = 0; i < b.size(); ++i) admitted_host[i] = b[i];
+  return FC_OK;
+}
+
+int fc_flush(fc_cache* h, void* stream, int64_t* rows_written) {
+  if (!h) return FC_ERR_BAD_ARG;
+  if (!h->slow) return FC_ERR_NO_SLOW_TIER;
+  DeviceGuard dg(h->device);
+  cudaStream_t st = as_stream(stream);
+  FC_TRY(launch_reset_counters(h, st));
+  FC_TRY(launch_flush(h, st));
+  FC_TRY(sync_counters(h, st));
+  if (rows_written) *rows_written = h->ctr_host->flush_rows;
+  return FC_OK;
+}
+
+int fc_mark_dirty(fc_cache* h, const int64_t* slots, int64_t n, void* stream) {
+  if (!h || n < 0) return FC_ERR_BAD_ARG;
+  if (n == 0) return FC_OK;
+  DeviceGuard dg(h->device);
+  cudaStream_t st = as_stream(stream);
+  FC_TRY(launch_mark_dirty(h, slots, n, st));
+  FC_TRY(sync_counters(h, st));
+  if (h->ctr_host->err) {
+    set_error("slot out of range [0, %d)", h->capacity);
+    return FC_ERR_SLOT_OUT_OF_RANGE;
+  }
+  return FC_OK;
+}
+
+int fc_select_evictions(fc_cache* h, int64_t needed, const int64_t* prot, int64_t nprot, int64_t* slots_host,
+                        void* stream) {
+  if (!h || needed < 0 || nprot < 0) return FC_ERR_BAD_ARG;
+  if (needed == 0) return FC_OK;
+  DeviceGuard dg(h->device);
+  cudaStream_t st = as_stream(stream);
+  FC_TRY(launch_select_evictions(h, needed, prot, nprot, st));
+  FC_TRY(sync_counters(h, st));
+  if (h->ctr_host->err) {
+    set_error("need %lld victims but only %d evictable rows", (long long)needed, h->ctr_host->candidates);
+    return h->ctr_host->err;
+  }
+  std::vector<int32_t> v((size_t)needed);
+  FC_CUDA(cudaMemcpy(v.data(), h->victim_slots, v.size() * 4, cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < v.size(); ++i) slots_host[i] = v[i];
+  return FC_OK;
+}
+
+int fc_pooled_forward(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const void* offsets,
+                      int32_t off_bytes, int64_t nbags, int32_t include_last, const float* psw, int32_t mode,
+                      float* out, void* stream) {
+  if (!h || (mode != FC_POOL_SUM && mode != FC_POOL_MEAN) || (offsets && off_bytes != 4 && off_bytes != 8))
+    return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  return launch_pool(h, uslots, inv, n, offsets, off_bytes, nbags, include_last, psw, mode, out, as_stream(stream));
+}
+
+int fc_gather_rows(fc_cache* h, const int32_t* slots, int64_t n, float* out, void* stream) {
+  if (!h) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  return launch_gather_rows(h, slots, n, out, as_stream(stream));
+}
+
+int fc_apply_unique_update(fc_cache* h, const int32_t* uslots, int64_t u, const float* add, void* stream) {
+  if (!h) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  return launch_unique_add(h, uslots, u, add, as_stream(stream));
+}
+
+int fc_apply_synthetic_update(fc_cache* h, const int32_t* uids, const int32_t* ucnt, const int32_t* uslots, int64_t u,
+                              uint64_t salt, const float* colw, void* stream) {
+  if (!h) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  return launch_synthetic(h, uids, ucnt, uslots, u, salt, colw, as_stream(stream));
+}
+
+int fc_scatter_update(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u, int64_t n,
+                      const float* deltas, void* stream) {
+  if (!h) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  return launch_scatter_update(h, uslots, inv, ucnt, u, n, deltas, as_stream(stream));
+}
+
+int fc_backward_update(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u, int64_t n,
+                       const void* offsets, int32_t off_bytes, int64_t nbags, int32_t include_last, const float* psw,
+                       int32_t mode, const float* grad, int32_t optim, float lr, float eps, void* stream) {
+  if (!h || (optim != FC_OPT_SGD && optim != FC_OPT_ADAGRAD) || (offsets && off_bytes != 4 && off_bytes != 8))
+    return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  return launch_backward(h, uslots, inv, ucnt, u, n, offsets, off_bytes, nbags, include_last, psw, mode, grad, optim, lr,
+                         eps, as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,418 @@
+// Index-space kernels of prepare_cache (/root/reference/pkg/src/freqcache/cache_manager.py:234-348).
+//
+// Every ordered list the reference builds with a sort is produced here by an
+// ordered compaction of a bitmap (count -> scan -> emit):
+//
+//   np.unique(ids, return_counts=True)      (:277)  -> id_bits   (id space, ascending)
+//   np.sort(unique_ranks[miss_mask])        (:310)  -> miss_bits (rank space, ascending)
+//   StaticFreqLfu.victim_ranks top-k        (:67-75,298-303) -> res_bits & ~prot_bits, last k set
+//                                                    bits, emitted in descending order
+//   state.free_slots()[:misses]             (:312-318) -> free_bits (slot space, first M)
+//
+// All kernels read their sizes from device counters, so one prepare is a fixed
+// sequence of launches with a single host synchronisation at the end.
+#include <algorithm>
+#include <climits>
+#include <cstddef>
+
+#include "fc_internal.cuh"
+
+namespace fc {
+
+// ------------------------------------------------------------------ word sources
+struct ArrWords {
+  uint32_t* w;
+  __device__ __forceinline__ uint32_t operator()(int64_t i) const { return w[i]; }
+  __device__ __forceinline__ void clear(int64_t i) const { w[i] = 0u; }
+};
+
+struct CandWords {  // resident and not protected by the current batch
+  const uint32_t* res;
+  const uint32_t* prot;
+  __device__ __forceinline__ uint32_t operator()(int64_t i) const { return res[i] & ~prot[i]; }
+  __device__ __forceinline__ void clear(int64_t) const {}
+};
+
+// ------------------------------------------------------------------ the primitive
+template <class WF>
+__global__ void __launch_bounds__(kNT) k_bits_count(WF wf, int64_t nwords, int64_t chunk, int32_t* cnt,
+                                                    const Counters* ctr, int gate) {
+  __shared__ int sm[kNT / 32 + 1];
+  if (!gate_open(ctr, gate)) return;
+  const int64_t b0 = (int64_t)blockIdx.x * chunk;
+  const int64_t b1 = min(nwords, b0 + chunk);
+  int c = 0;
+  for (int64_t w = b0 + threadIdx.x; w < b1; w += kNT) c += __popc(wf(w));
+  c = block_sum<kNT>(c, sm);
+  if (threadIdx.x == 0) cnt[blockIdx.x] = c;
+}
+
+template <class FIN>
+__global__ void __launch_bounds__(1024) k_bits_scan(int32_t* cnt, int nb, FIN fin, Counters* ctr, int gate) {
+  __shared__ int sm[1024 / 32 + 1];
+  if (!gate_open(ctr, gate)) return;
+  const int per = (nb + 1023) / 1024;
+  const int beg = threadIdx.x * per;
+  int s = 0;
+  for (int k = 0; k < per; ++k)
+    if (beg + k < nb) s += cnt[beg + k];
+  int tot;
+  int off = block_excl_scan<1024>(s, sm, tot);
+  for (int k = 0; k < per; ++k)
+    if (beg + k < nb) {
+      int v = cnt[beg + k];
+      cnt[beg + k] = off;
+      off += v;
+    }
+  if (threadIdx.x == 0) {
+    cnt[nb] = tot;
+    fin(tot, ctr);
+  }
+}
+
+template <class WF, class EM>
+__global__ void __launch_bounds__(kNT) k_bits_emit(WF wf, EM em, int64_t nwords, int64_t chunk, const int32_t* off,
+                                                   const int32_t* win, Counters* ctr, int gate) {
+  __shared__ int sm[kNT / 32 + 1];
+  if (!gate_open(ctr, gate)) return;
+  int lo = 0, hi = INT_MAX;
+  if (win != nullptr) {
+    lo = win[0];
+    hi = win[1];
+  }
+  const int base = off[blockIdx.x];
+  const int bend = off[blockIdx.x + 1];
+  if (!EM::kVisitAll && (bend <= lo || base >= hi)) return;
+  EM e = em;
+  e.init(ctr);
+  const int64_t b0 = (int64_t)blockIdx.x * chunk;
+  const int64_t b1 = min(nwords, b0 + chunk);
+  int run = base;
+  int acc = 0;
+  for (int64_t t0 = b0; t0 < b1; t0 += kNT) {
+    const int64_t w = t0 + threadIdx.x;
+    uint32_t x = (w < b1) ? wf(w) : 0u;
+    int tot;
+    int idx = run + block_excl_scan<kNT>(__popc(x), sm, tot);
+    while (x) {
+      const int bit = __ffs(x) - 1;
+      x &= x - 1;
+      if (idx >= lo && idx < hi) acc += e(w * 32 + bit, idx);
+      ++idx;
+    }
+    if (EM::kClear && w < b1) wf.clear(w);
+    run += tot;
+  }
+  if (EM::kCount) {
+    acc = block_sum<kNT>(acc, sm);
+    if (threadIdx.x == 0 && acc) atomicAdd(e.counter(ctr), acc);
+  }
+}
+
+template <class WF, class FIN, class EM>
+static void compact(WF wf, FIN fin, EM em, int64_t nwords, int32_t* cnt, const int32_t* win, Counters* ctr,
+                    int gate, cudaStream_t st) {
+  const int nb = grid_for(nwords, 1024, kMaxScanBlocks);
+  const int64_t chunk = (nwords + nb - 1) / nb;
+  k_bits_count<WF><<<nb, kNT, 0, st>>>(wf, nwords, chunk, cnt, ctr, gate);
+  k_bits_scan<FIN><<<1, 1024, 0, st>>>(cnt, nb, fin, ctr, gate);
+  k_bits_emit<WF, EM><<<nb, kNT, 0, st>>>(wf, em, nwords, chunk, cnt, win, ctr, gate);
+}
+
+// ------------------------------------------------------------------ unique ids (:268-289)
+template <typename IdT>
+__global__ void __launch_bounds__(kNT) k_mark_ids(const IdT* __restrict__ ids, int64_t n, int64_t num_ids,
+                                                  uint32_t* id_bits, int32_t* aux, Counters* c) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    const bool valid = i < n;
+    const long long id = valid ? (long long)ids[i] : 0;
+    const bool inr = valid && id >= 0 && id < num_ids;
+    if (valid && !inr) {
+      if (id < 0) atomicMin(&c->lo, id);
+      else atomicMax(&c->hi, id);
+    }
+    // duplicates inside a warp are aggregated before touching global memory
+    const unsigned peers = __match_any_sync(FC_FULL, inr ? (int)id : -1);
+    if (inr && lane == __ffs(peers) - 1) {
+      atomicAdd(&aux[id], __popc(peers));
+      const uint32_t m = 1u << (id & 31);
+      uint32_t* wp = &id_bits[id >> 5];
+      if (!(*wp & m)) atomicOr(wp, m);
+    }
+  }
+}
+
+struct IdFin {
+  int32_t cap;
+  __device__ void operator()(int total, Counters* c) const {
+    c->unique = total;
+    if (c->lo != LLONG_MAX || c->hi != LLONG_MIN) c->err = FC_ERR_ID_OUT_OF_RANGE;        // :272-275
+    else if (total > cap) c->err = FC_ERR_BATCH_EXCEEDS_CAPACITY;                          // :278-282
+    c->emitted = (c->err == 0);
+  }
+};
+
+struct IdEmit {
+  static constexpr bool kVisitAll = true, kClear = true, kCount = true;
+  int32_t* aux;
+  const int32_t* rank_of;
+  const int32_t* rank_to_slot;
+  uint32_t* prot;
+  uint32_t* miss;
+  int32_t* uids;
+  int32_t* ucnt;
+  int32_t* uranks;
+  int32_t* uslots;
+  int ok;
+  __device__ void init(const Counters* c) { ok = c->emitted; }
+  __device__ int* counter(Counters* c) const { return &c->misses; }
+  __device__ __forceinline__ int operator()(int64_t id, int p) const {
+    if (!ok) {  // validation failed: undo the per-id counts, touch nothing else
+      aux[id] = 0;
+      return 0;
+    }
+    const int cnt = aux[id];
+    aux[id] = p;  // position in the unique list, read by k_inverse
+    const int r = rank_of[id];             // :283
+    const int s = rank_to_slot[r];         // :286
+    uids[p] = (int32_t)id;
+    ucnt[p] = cnt;
+    uranks[p] = r;
+    uslots[p] = s;
+    atomicOr(&prot[r >> 5], 1u << (r & 31));  // every batch rank is protected (:299)
+    if (s < 0) {                              // miss (:287)
+      atomicOr(&miss[r >> 5], 1u << (r & 31));
+      return 1;
+    }
+    return 0;
+  }
+};
+
+template <typename IdT>
+__global__ void __launch_bounds__(kNT) k_inverse(const IdT* __restrict__ ids, int64_t n, const int32_t* __restrict__ aux,
+                                                 int32_t* __restrict__ inv, const Counters* c) {
+  if (!c->emitted) return;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT)
+    inv[i] = aux[(int64_t)ids[i]];
+}
+
+// ------------------------------------------------------------------ eviction count (:293-296)
+__global__ void k_plan(Counters* c, int cap, int evict_mode, int row_fits) {
+  if (c->err) return;
+  const int m = c->misses, u = c->unique, fr = c->free_count;
+  const int needed = evict_mode == FC_EVICT_OCCUPANCY_AWARE ? max(0, m - fr) : max(0, u - cap);
+  c->needed = needed;
+  if (fr + needed < m) c->err = FC_ERR_INSUFFICIENT_FREE_SLOTS;  // paper_literal (:313-317)
+  // a row larger than the staging buffer cannot move (transmitter.py:85-88); refuse
+  // before any mutation whenever this batch has rows to move
+  if (!row_fits && (m > 0 || needed > 0)) c->err = FC_ERR_BUFFER_TOO_SMALL;
+  c->win_admit[0] = 0;
+  c->win_admit[1] = m;
+}
+
+// ------------------------------------------------------------------ victims (:298-303)
+struct EvictFin {
+  __device__ void operator()(int total, Counters* c) const {
+    c->candidates = total;
+    const int need = c->needed;
+    if (need > total) {
+      c->err = FC_ERR_INSUFFICIENT_EVICTABLE;
+      return;
+    }
+    c->win_evict[0] = total - need;  // the `need` largest candidate ranks
+    c->win_evict[1] = total;
+  }
+};
+
+struct EvictEmit {
+  static constexpr bool kVisitAll = false, kClear = false, kCount = false;
+  int32_t* evicted;
+  int32_t* vslots;
+  const int32_t* rank_to_slot;
+  int total;
+  __device__ void init(const Counters* c) { total = c->candidates; }
+  __device__ int* counter(Counters*) const { return nullptr; }
+  __device__ __forceinline__ int operator()(int64_t r, int a) const {
+    const int v = total - 1 - a;  // descending, like np.sort(top)[::-1] (:75)
+    evicted[v] = (int32_t)r;
+    vslots[v] = rank_to_slot[r];
+    return 0;
+  }
+};
+
+// ------------------------------------------------------------------ admission (:310-323)
+struct AdmitFin {
+  __device__ void operator()(int total, Counters* c) const {
+    if (total != c->misses) c->err = FC_ERR_CUDA;  // internal inconsistency guard
+  }
+};
+
+struct RankEmit {
+  static constexpr bool kVisitAll = false, kClear = false, kCount = false;
+  int32_t* out;
+  __device__ void init(const Counters*) {}
+  __device__ int* counter(Counters*) const { return nullptr; }
+  __device__ __forceinline__ int operator()(int64_t r, int a) const {
+    out[a] = (int32_t)r;
+    return 0;
+  }
+};
+
+struct FreeFin {
+  __device__ void operator()(int total, Counters* c) const {
+    if (total < c->misses) c->err = FC_ERR_INSUFFICIENT_FREE_SLOTS;
+  }
+};
+
+__global__ void k_begin(Counters* c) {
+  c->err = 0;
+  c->emitted = 0;
+  c->lo = LLONG_MAX;
+  c->hi = LLONG_MIN;
+  c->unique = 0;
+  c->misses = 0;
+  c->needed = 0;
+  c->wb_rows = 0;
+  c->candidates = 0;
+  c->win_evict[0] = c->win_evict[1] = 0;
+  c->win_admit[0] = c->win_admit[1] = 0;
+  c->flush_rows = 0;
+  c->bad_slot = -1;
+}
+
+// unique_slots after admission + clear every per-batch bitmap / aux entry
+__global__ void __launch_bounds__(kNT) k_finish(const int32_t* __restrict__ uids, const int32_t* __restrict__ uranks,
+                                                int32_t* __restrict__ uslots, int32_t* aux,
+                                                const int32_t* __restrict__ rank_to_slot, uint32_t* prot,
+                                                uint32_t* miss, const Counters* c) {
+  if (!c->emitted) return;
+  const int u = c->unique;
+  const bool ok = c->err == 0;
+  for (int p = blockIdx.x * kNT + threadIdx.x; p < u; p += gridDim.x * kNT) {
+    aux[uids[p]] = 0;
+    const int r = uranks[p];
+    prot[r >> 5] = 0u;
+    miss[r >> 5] = 0u;
+    if (ok) uslots[p] = rank_to_slot[r];  // :325
+  }
+}
+
+// device addresses of the order-index windows inside the (device) counters
+static const int32_t* win_evict(Counters* c) {
+  return reinterpret_cast<const int32_t*>(reinterpret_cast<char*>(c) + offsetof(Counters, win_evict));
+}
+static const int32_t* win_admit(Counters* c) {
+  return reinterpret_cast<const int32_t*>(reinterpret_cast<char*>(c) + offsetof(Counters, win_admit));
+}
+
+int launch_reset_counters(fc_cache* h, cudaStream_t st) {
+  k_begin<<<1, 1, 0, st>>>(h->ctr);
+  return FC_OK;
+}
+
+int launch_prepare(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt,
+                   int32_t* uranks, int32_t* uslots, int32_t* inverse, cudaStream_t st) {
+  Counters* c = h->ctr;
+  k_begin<<<1, 1, 0, st>>>(c);
+  const int gn = grid_for(n, kNT, kSMs * 8);
+  if (ids_bytes == 8) k_mark_ids<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->num_ids, h->id_bits, h->aux, c);
+  else k_mark_ids<int><<<gn, kNT, 0, st>>>((const int*)ids, n, h->num_ids, h->id_bits, h->aux, c);
+
+  IdEmit ie{h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, uids, ucnt, uranks, uslots, 0};
+  compact(ArrWords{h->id_bits}, IdFin{h->capacity}, ie, h->nw_ids, h->block_cnt, nullptr, c, G_ALWAYS, st);
+
+  if (ids_bytes == 8) k_inverse<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->aux, inverse, c);
+  else k_inverse<int><<<gn, kNT, 0, st>>>((const int*)ids, n, h->aux, inverse, c);
+
+  k_plan<<<1, 1, 0, st>>>(c, h->capacity, h->evict_mode, (int64_t)h->dim * 4 <= h->buffer_bytes);
+
+  EvictEmit ee{h->evicted_ranks, h->victim_slots, h->rank_to_slot, 0};
+  compact(CandWords{h->res_bits, h->prot_bits}, EvictFin{}, ee, h->nw_ids, h->block_cnt, win_evict(c), c,
+          G_EVICT, st);
+  int rc = launch_evict_rows(h, st);
+  if (rc) return rc;
+
+  compact(ArrWords{h->miss_bits}, AdmitFin{}, RankEmit{h->admitted_ranks}, h->nw_ids, h->block_cnt,
+          win_admit(c), c, G_ADMIT, st);
+  compact(ArrWords{h->free_bits}, FreeFin{}, RankEmit{h->target_slots}, h->nw_slots, h->block_cnt2,
+          win_admit(c), c, G_ADMIT, st);
+  rc = launch_transfer_rows(h, st);
+  if (rc) return rc;
+
+  const int gu = grid_for(std::min<int64_t>(n, h->capacity), kNT, kSMs * 4);
+  k_finish<<<gu, kNT, 0, st>>>(uids, uranks, uslots, h->aux, h->rank_to_slot, h->prot_bits, h->miss_bits, c);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------------ select_evictions (:205-216)
+__global__ void k_set_prot(const int64_t* __restrict__ ranks, int64_t n, int64_t num_ids, uint32_t* prot,
+                           bool set) {
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+    const long long r = ranks[i];
+    if (r < 0 || r >= num_ids) continue;  // a rank that is not resident cannot matter
+    if (set) atomicOr(&prot[r >> 5], 1u << (r & 31));
+    else prot[r >> 5] = 0u;
+  }
+}
+
+__global__ void k_set_needed(Counters* c, int needed) { c->needed = needed; }
+
+int launch_select_evictions(fc_cache* h, int64_t needed, const int64_t* prot, int64_t nprot, cudaStream_t st) {
+  Counters* c = h->ctr;
+  k_begin<<<1, 1, 0, st>>>(c);
+  const int g = grid_for(nprot, kNT, kSMs * 4);
+  if (nprot) k_set_prot<<<g, kNT, 0, st>>>(prot, nprot, h->num_ids, h->prot_bits, true);
+  k_set_needed<<<1, 1, 0, st>>>(c, (int)needed);
+  EvictEmit ee{h->evicted_ranks, h->victim_slots, h->rank_to_slot, 0};
+  compact(CandWords{h->res_bits, h->prot_bits}, EvictFin{}, ee, h->nw_ids, h->block_cnt, win_evict(c), c,
+          G_EVICT, st);
+  if (nprot) k_set_prot<<<g, kNT, 0, st>>>(prot, nprot, h->num_ids, h->prot_bits, false);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------------ warmup (:351-390)
+__global__ void k_warm_state(int32_t k, int32_t* slot_to_rank, int32_t* rank_to_slot, uint8_t* dirty,
+                             uint32_t* res, uint32_t* freeb, Counters* c) {
+  for (int s = blockIdx.x * kNT + threadIdx.x; s < k; s += gridDim.x * kNT) {
+    slot_to_rank[s] = s;
+    rank_to_slot[s] = s;
+    dirty[s] = 0;
+    atomicOr(&res[s >> 5], 1u << (s & 31));
+    atomicAnd(&freeb[s >> 5], ~(1u << (s & 31)));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) c->free_count -= k;
+}
+
+int launch_warmup_state(fc_cache* h, int64_t k, cudaStream_t st) {
+  k_warm_state<<<grid_for(k, kNT, kSMs * 4), kNT, 0, st>>>((int32_t)k, h->slot_to_rank, h->rank_to_slot, h->dirty,
+                                                           h->res_bits, h->free_bits, h->ctr);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------------ mark_dirty (:393-400)
+__global__ void k_check_slots(const int64_t* __restrict__ s, int64_t n, int cap, Counters* c) {
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT)
+    if (s[i] < 0 || s[i] >= cap) c->err = FC_ERR_SLOT_OUT_OF_RANGE;
+}
+__global__ void k_set_dirty(const int64_t* __restrict__ s, int64_t n, uint8_t* dirty, const Counters* c) {
+  if (c->err) return;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) dirty[s[i]] = 1;
+}
+
+int launch_mark_dirty(fc_cache* h, const int64_t* slots, int64_t n, cudaStream_t st) {
+  k_begin<<<1, 1, 0, st>>>(h->ctr);
+  const int g = grid_for(n, kNT, kSMs * 4);
+  k_check_slots<<<g, kNT, 0, st>>>(slots, n, h->capacity, h->ctr);
+  k_set_dirty<<<g, kNT, 0, st>>>(slots, n, h->dirty, h->ctr);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+}  // namespace fc

@@ -1,0 +1,228 @@
+// Internal declarations shared by the freqcache_b200 translation units.
+//
+// Device-resident layout of one cache (one reference CacheStack,
+// /root/reference/pkg/src/freqcache/cache_manager.py:441-562):
+//
+//   rank_of       int32[num_ids]   IdxMap.rank_of (freq_stats.py:52-73)
+//   rank_to_slot  int32[num_ids]   CacheState.rank_to_slot (-1 = ABSENT)
+//   slot_to_rank  int32[C]         CacheState.slot_to_rank (-1 = EMPTY)
+//   dirty         uint8[C]
+//   fast          fp32[C, D]       FastTierStore.slots (row stride D)
+//   fast_state    fp32[C, S]       optimizer state cached with the row (S may be 0)
+//   res_bits      u32[ceil(num_ids/32)]  resident-rank bitmap (rank space)
+//   free_bits     u32[ceil(C/32)]        empty-slot bitmap (slot space)
+//   id_bits / miss_bits / prot_bits      per-batch bitmaps, all-zero between calls
+//   aux           int32[num_ids]   per-batch id counts, then unique positions; zero between calls
+//
+// Ordered outputs (ascending unique ids, ascending admitted ranks, ascending free
+// slots, descending victim ranks) all come from one primitive: an ordered
+// compaction of set bits of a bitmap (count -> scan -> emit). Bitmaps over the id
+// or rank space are a 1-pass radix (counting) sort: O(N + num_ids/32) with no
+// key comparisons, instead of np.unique / np.sort / np.partition.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/freqcache_b200.h"
+
+#define FC_FULL 0xffffffffu
+
+namespace fc {
+
+constexpr int kNT = 256;                 // threads per block for streaming kernels
+constexpr int kSMs = 148;                // B200 SM count
+constexpr int kMaxScanBlocks = kSMs * 8; // blocks of one bitmap pass (<= 1184)
+
+enum Gate : int { G_ALWAYS = 0, G_OK = 1, G_EVICT = 2, G_ADMIT = 3, G_EMITTED = 4 };
+
+// Per-call device counters. `free_count` is persistent across calls.
+struct Counters {
+  int32_t err;
+  int32_t emitted;      // id compaction produced outputs (cleanup needed)
+  long long lo;         // smallest negative id seen
+  long long hi;         // largest id >= num_ids seen
+  int32_t unique;
+  int32_t misses;
+  int32_t needed;
+  int32_t free_count;
+  int32_t wb_rows;
+  int32_t candidates;
+  int32_t win_evict[2]; // order-index window of the victim emission
+  int32_t win_admit[2];
+  int32_t flush_rows;
+  int32_t bad_slot;
+};
+
+}  // namespace fc
+
+struct fc_cache {
+  int64_t num_ids;
+  int32_t capacity;
+  int32_t dim;
+  int32_t sw;             // optimizer-state width
+  int32_t write_back;
+  int32_t evict_mode;
+  int64_t buffer_bytes;
+  int device;
+  int64_t nw_ids;         // words of a rank/id bitmap (padded)
+  int64_t nw_slots;       // words of the slot bitmap (padded)
+
+  int32_t* rank_of;
+  int32_t* rank_to_slot;
+  int32_t* slot_to_rank;
+  uint8_t* dirty;
+  float* fast;
+  float* fast_state;
+  uint32_t* res_bits;
+  uint32_t* free_bits;
+  uint32_t* id_bits;
+  uint32_t* miss_bits;
+  uint32_t* prot_bits;
+  int32_t* aux;
+
+  int32_t* evicted_ranks;   // [C] descending
+  int32_t* victim_slots;    // [C]
+  int32_t* wb_ranks;        // [C] rank per staged write-back row or -1
+  float* wb_stage;          // [C, D]
+  float* wb_stage_state;    // [C, S]
+  int32_t* admitted_ranks;  // [C] ascending
+  int32_t* target_slots;    // [C] ascending
+  int32_t* block_cnt;       // [kMaxScanBlocks + 1]
+  int32_t* block_cnt2;      // second scan lane (concurrent compactions)
+  fc::Counters* ctr;        // device
+  fc::Counters* ctr_host;   // pinned mirror
+  cudaEvent_t done;
+
+  // scratch for sort-based kernels (backward / scatter_update), grown on demand
+  void* scratch;
+  size_t scratch_bytes;
+
+  float* slow;              // host rows (device-mapped)
+  int64_t slow_ld;
+  float* slow_state;
+  int64_t state_ld;
+
+  int32_t last_needed;
+  int32_t last_misses;
+  int32_t host_free;        // host mirror of free_count
+};
+
+namespace fc {
+
+void set_error(const char* fmt, ...);
+int cuda_fail(cudaError_t e, const char* what);
+
+#define FC_CUDA(call)                                 \
+  do {                                                \
+    cudaError_t e__ = (call);                         \
+    if (e__ != cudaSuccess) return fc::cuda_fail(e__, #call); \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int grid_for(int64_t items, int per_block, int max_blocks = kSMs * 8) {
+  int64_t b = (items + per_block - 1) / per_block;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return static_cast<int>(b);
+}
+
+// lanes per row group: enough lanes to cover a row with 16-byte (vec) or 4-byte accesses
+inline int row_group(int width, bool vec) {
+  int units = vec ? (width + 3) / 4 : width;
+  int g = 1;
+  while (g < units && g < 32) g <<= 1;
+  return g;
+}
+
+// index-space kernels (fc_index.cu)
+int launch_prepare(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt,
+                   int32_t* uranks, int32_t* uslots, int32_t* inverse, cudaStream_t st);
+int launch_select_evictions(fc_cache* h, int64_t needed, const int64_t* prot, int64_t nprot, cudaStream_t st);
+int launch_warmup_state(fc_cache* h, int64_t k, cudaStream_t st);
+int launch_mark_dirty(fc_cache* h, const int64_t* slots, int64_t n, cudaStream_t st);
+int launch_reset_counters(fc_cache* h, cudaStream_t st);
+
+// row kernels (fc_rows.cu)
+int launch_evict_rows(fc_cache* h, cudaStream_t st);
+int launch_transfer_rows(fc_cache* h, cudaStream_t st);
+int launch_flush(fc_cache* h, cudaStream_t st);
+int launch_pool(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const void* offsets,
+                int off_bytes, int64_t nbags, int include_last, const float* psw, int mode, float* out,
+                cudaStream_t st);
+int launch_gather_rows(fc_cache* h, const int32_t* slots, int64_t n, float* out, cudaStream_t st);
+int launch_unique_add(fc_cache* h, const int32_t* uslots, int64_t u, const float* add, cudaStream_t st);
+int launch_synthetic(fc_cache* h, const int32_t* uids, const int32_t* ucnt, const int32_t* uslots, int64_t u,
+                     uint64_t salt, const float* colw, cudaStream_t st);
+int launch_scatter_update(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt,
+                          int64_t u, int64_t n, const float* deltas, cudaStream_t st);
+int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u,
+                    int64_t n, const void* offsets, int off_bytes, int64_t nbags, int include_last,
+                    const float* psw, int mode, const float* grad, int optim, float lr, float eps,
+                    cudaStream_t st);
+
+// sort / scan helpers (fc_sort.cu)
+size_t sort_scratch_bytes(int64_t n);
+int radix_sort_pairs(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* keys_out, int32_t* vals_out,
+                     int64_t n, int key_bits, void* scratch, cudaStream_t st);
+int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch, cudaStream_t st);
+size_t scan_scratch_bytes(int64_t n);
+int ensure_scratch(fc_cache* h, size_t bytes);
+
+// ---------------------------------------------------------------- device utils
+__device__ __forceinline__ int warp_sum(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FC_FULL, v, o);
+  return v;
+}
+
+// Block-wide exclusive scan of one int per thread. `sm` needs NT/32 + 1 ints.
+template <int NT>
+__device__ __forceinline__ int block_excl_scan(int v, int* sm, int& total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  int x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(FC_FULL, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sm[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int w = (lane < NT / 32) ? sm[lane] : 0;
+    int s = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(FC_FULL, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < NT / 32) sm[lane] = s - w;
+    if (lane == NT / 32 - 1) sm[NT / 32] = s;
+  }
+  __syncthreads();
+  int r = x - v + sm[wid];
+  total = sm[NT / 32];
+  __syncthreads();
+  return r;
+}
+
+template <int NT>
+__device__ __forceinline__ int block_sum(int v, int* sm) {
+  int t;
+  block_excl_scan<NT>(v, sm, t);
+  return t;
+}
+
+__device__ __forceinline__ bool gate_open(const Counters* c, int gate) {
+  switch (gate) {
+    case G_ALWAYS: return true;
+    case G_OK: return c->err == 0;
+    case G_EVICT: return c->err == 0 && c->needed > 0;
+    case G_ADMIT: return c->err == 0 && c->misses > 0;
+    case G_EMITTED: return c->emitted != 0;
+  }
+  return true;
+}
+
+}  // namespace fc

@@ -1,0 +1,690 @@
+// Row-moving kernels: eviction staging, host<->HBM transfers, flush, pooled
+// EmbeddingBag forward, updates and the fused backward + sparse optimizer.
+//
+// Rows are moved by "row groups": G lanes (G = pow2 >= row_width/4, <= 32) own one
+// row and move it with 16-byte accesses. Groups never straddle warps, so a warp
+// walks ceil(items / (groups per grid)) rounds in lock-step and can __syncwarp.
+//
+// The slow tier lives in pinned, device-mapped host memory (fc_host_alloc). The
+// GPU reads admitted rows from it and writes evicted dirty rows into it directly
+// over PCIe/C2C, both directions in the same kernel so the duplex link is used
+// both ways at once (transmitter.py:144-207 moves rows through a bounded host
+// buffer; here the "buffer" is the HBM staging area of the victims).
+#include <algorithm>
+
+#include "fc_internal.cuh"
+
+namespace fc {
+
+struct RowCtx {
+  float* fast;
+  float* fstate;
+  float* slow;
+  float* sstate;
+  int64_t ld;   // slow row stride (floats)
+  int64_t sld;  // slow state stride
+  int D, S;
+  int32_t* slot_to_rank;
+  int32_t* rank_to_slot;
+  uint8_t* dirty;
+  uint32_t* res;
+  uint32_t* freeb;
+  int32_t* evicted;
+  int32_t* vslots;
+  int32_t* wb_ranks;
+  float* stage;
+  float* stage_state;
+  int32_t* admitted;
+  int32_t* target;
+  int always;
+  Counters* c;
+};
+
+static RowCtx row_ctx(fc_cache* h) {
+  RowCtx x;
+  x.fast = h->fast;
+  x.fstate = h->fast_state;
+  x.slow = h->slow;
+  x.sstate = h->slow_state;
+  x.ld = h->slow_ld;
+  x.sld = h->state_ld;
+  x.D = h->dim;
+  x.S = h->sw;
+  x.slot_to_rank = h->slot_to_rank;
+  x.rank_to_slot = h->rank_to_slot;
+  x.dirty = h->dirty;
+  x.res = h->res_bits;
+  x.freeb = h->free_bits;
+  x.evicted = h->evicted_ranks;
+  x.vslots = h->victim_slots;
+  x.wb_ranks = h->wb_ranks;
+  x.stage = h->wb_stage;
+  x.stage_state = h->wb_stage_state;
+  x.admitted = h->admitted_ranks;
+  x.target = h->target_slots;
+  x.always = h->write_back == FC_WB_ALWAYS;
+  x.c = h->ctr;
+  return x;
+}
+
+static bool vec_ok(fc_cache* h) {
+  auto al = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  bool v = (h->dim % 4 == 0) && (h->slow_ld % 4 == 0) && al(h->slow) && al(h->fast);
+  if (h->sw) v = v && (h->sw % 4 == 0) && (h->state_ld % 4 == 0) && al(h->slow_state) && al(h->fast_state);
+  return v;
+}
+
+template <bool VEC>
+__device__ __forceinline__ void copy_row(float* __restrict__ dst, const float* __restrict__ src, int w, int gl, int G) {
+  if (VEC) {
+    for (int c = gl * 4; c < w; c += G * 4)
+      *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<const float4*>(src + c);
+  } else {
+    for (int c = gl; c < w; c += G) dst[c] = src[c];
+  }
+}
+
+// two independent row copies with both loads issued before both stores
+template <bool VEC>
+__device__ __forceinline__ void copy_two_rows(float* d1, const float* s1, bool a1, float* d2, const float* s2, bool a2,
+                                              int w, int gl, int G) {
+  if (VEC) {
+    for (int c = gl * 4; c < w; c += G * 4) {
+      float4 x, y;
+      if (a1) x = *reinterpret_cast<const float4*>(s1 + c);
+      if (a2) y = *reinterpret_cast<const float4*>(s2 + c);
+      if (a1) *reinterpret_cast<float4*>(d1 + c) = x;
+      if (a2) *reinterpret_cast<float4*>(d2 + c) = y;
+    }
+  } else {
+    for (int c = gl; c < w; c += G) {
+      float x = 0.f, y = 0.f;
+      if (a1) x = s1[c];
+      if (a2) y = s2[c];
+      if (a1) d1[c] = x;
+      if (a2) d2[c] = y;
+    }
+  }
+}
+
+struct GroupIdx {
+  int lane, gw, gl, gpw;
+  int64_t warp, nwarps;
+  __device__ GroupIdx(int G) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    lane = threadIdx.x & 31;
+    gpw = 32 / G;
+    gw = lane / G;
+    gl = lane % G;
+    warp = t >> 5;
+    nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  }
+};
+
+// ------------------------------------------------------------- eviction (:298-308, _write_back :219-231)
+template <bool VEC>
+__global__ void __launch_bounds__(kNT) k_evict_rows(RowCtx x, int G) {
+  __shared__ int sm[kNT / 32 + 1];
+  if (!gate_open(x.c, G_EVICT)) return;
+  const int needed = x.c->needed;
+  GroupIdx g(G);
+  int wb_count = 0;
+  for (int64_t base = g.warp * g.gpw; base < needed; base += g.nwarps * g.gpw) {
+    const int64_t v = base + g.gw;
+    const bool act = v < needed;
+    int s = 0, r = 0;
+    bool wb = false;
+    if (act) {
+      s = x.vslots[v];
+      r = x.evicted[v];
+      wb = x.always || x.dirty[s];
+    }
+    __syncwarp();
+    if (wb) {
+      copy_row<VEC>(x.stage + v * x.D, x.fast + (int64_t)s * x.D, x.D, g.gl, G);
+      if (x.S) copy_row<VEC>(x.stage_state + v * x.S, x.fstate + (int64_t)s * x.S, x.S, g.gl, G);
+    }
+    if (act && g.gl == 0) {
+      x.wb_ranks[v] = wb ? r : -1;
+      x.slot_to_rank[s] = -1;
+      x.rank_to_slot[r] = -1;
+      x.dirty[s] = 0;
+      atomicAnd(&x.res[r >> 5], ~(1u << (r & 31)));
+      atomicOr(&x.freeb[s >> 5], 1u << (s & 31));
+      wb_count += wb;
+    }
+  }
+  wb_count = block_sum<kNT>(wb_count, sm);
+  if (threadIdx.x == 0 && wb_count) atomicAdd(&x.c->wb_rows, wb_count);
+  if (blockIdx.x == 0 && threadIdx.x == 0) x.c->free_count += needed;
+}
+
+// ------------------------------------------------------------- write-back + admission rows (:304,319-323)
+template <bool VEC>
+__global__ void __launch_bounds__(kNT) k_transfer_rows(RowCtx x, int G) {
+  if (!gate_open(x.c, G_OK)) return;
+  const int needed = x.c->needed, m = x.c->misses;
+  const int items = max(needed, m);
+  GroupIdx g(G);
+  for (int64_t base = g.warp * g.gpw; base < items; base += g.nwarps * g.gpw) {
+    const int64_t j = base + g.gw;
+    int r1 = -1, r2 = 0, s2 = 0;
+    if (j < needed) r1 = x.wb_ranks[j];
+    const bool a1 = r1 >= 0;
+    const bool a2 = j < m;
+    if (a2) {
+      r2 = x.admitted[j];
+      s2 = x.target[j];
+    }
+    copy_two_rows<VEC>(x.slow + (int64_t)r1 * x.ld, x.stage + j * x.D, a1, x.fast + (int64_t)s2 * x.D,
+                       x.slow + (int64_t)r2 * x.ld, a2, x.D, g.gl, G);
+    if (x.S)
+      copy_two_rows<VEC>(x.sstate + (int64_t)r1 * x.sld, x.stage_state + j * x.S, a1, x.fstate + (int64_t)s2 * x.S,
+                         x.sstate + (int64_t)r2 * x.sld, a2, x.S, g.gl, G);
+    if (a2 && g.gl == 0) {
+      x.slot_to_rank[s2] = r2;
+      x.rank_to_slot[r2] = s2;
+      x.dirty[s2] = 0;
+      atomicOr(&x.res[r2 >> 5], 1u << (r2 & 31));
+      atomicAnd(&x.freeb[s2 >> 5], ~(1u << (s2 & 31)));
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) x.c->free_count -= m;
+}
+
+static int rows_grid() { return kSMs * 8; }
+
+int launch_evict_rows(fc_cache* h, cudaStream_t st) {
+  RowCtx x = row_ctx(h);
+  const bool v = vec_ok(h);
+  const int G = row_group(std::max(h->dim, h->sw), v);
+  if (v) k_evict_rows<true><<<rows_grid(), kNT, 0, st>>>(x, G);
+  else k_evict_rows<false><<<rows_grid(), kNT, 0, st>>>(x, G);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+int launch_transfer_rows(fc_cache* h, cudaStream_t st) {
+  RowCtx x = row_ctx(h);
+  const bool v = vec_ok(h);
+  const int G = row_group(std::max(h->dim, h->sw), v);
+  if (v) k_transfer_rows<true><<<rows_grid(), kNT, 0, st>>>(x, G);
+  else k_transfer_rows<false><<<rows_grid(), kNT, 0, st>>>(x, G);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------- flush (:403-415)
+template <bool VEC>
+__global__ void __launch_bounds__(kNT) k_flush(RowCtx x, int cap, int G) {
+  __shared__ int sm[kNT / 32 + 1];
+  GroupIdx g(G);
+  int cnt = 0;
+  for (int64_t base = g.warp * g.gpw; base < cap; base += g.nwarps * g.gpw) {
+    const int64_t s = base + g.gw;
+    const bool d = s < cap && x.dirty[s];
+    int r = 0;
+    if (d) r = x.slot_to_rank[s];
+    __syncwarp();
+    if (d) {
+      copy_row<VEC>(x.slow + (int64_t)r * x.ld, x.fast + s * x.D, x.D, g.gl, G);
+      if (x.S) copy_row<VEC>(x.sstate + (int64_t)r * x.sld, x.fstate + s * x.S, x.S, g.gl, G);
+    }
+    if (d && g.gl == 0) {
+      x.dirty[s] = 0;
+      ++cnt;
+    }
+  }
+  cnt = block_sum<kNT>(cnt, sm);
+  if (threadIdx.x == 0 && cnt) atomicAdd(&x.c->flush_rows, cnt);
+}
+
+int launch_flush(fc_cache* h, cudaStream_t st) {
+  RowCtx x = row_ctx(h);
+  const bool v = vec_ok(h);
+  const int G = row_group(std::max(h->dim, h->sw), v);
+  const int grid = grid_for((int64_t)h->capacity * G, kNT, kSMs * 8);
+  if (v) k_flush<true><<<grid, kNT, 0, st>>>(x, h->capacity, G);
+  else k_flush<false><<<grid, kNT, 0, st>>>(x, h->capacity, G);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------- pooled EmbeddingBag forward
+template <typename OffT>
+__device__ __forceinline__ void bag_bounds(const OffT* off, int64_t b, int64_t nbags, int64_t n, int incl, int64_t& s,
+                                           int64_t& e) {
+  if (off == nullptr) {
+    s = b;
+    e = b + 1;
+    return;
+  }
+  s = (int64_t)off[b];
+  e = (incl || b + 1 < nbags) ? (int64_t)off[b + 1] : n;
+}
+
+template <bool VEC, typename OffT>
+__global__ void __launch_bounds__(kNT) k_pool(const float* __restrict__ fast, int D, const int32_t* __restrict__ uslots,
+                                              const int32_t* __restrict__ inv, int64_t n, const OffT* __restrict__ off,
+                                              int64_t nbags, int incl, const float* __restrict__ psw, int mode,
+                                              float* __restrict__ out, int G) {
+  GroupIdx g(G);
+  for (int64_t base = g.warp * g.gpw; base < nbags; base += g.nwarps * g.gpw) {
+    const int64_t b = base + g.gw;
+    if (b >= nbags) continue;
+    int64_t s, e;
+    bag_bounds(off, b, nbags, n, incl, s, e);
+    const float scale = (mode == FC_POOL_MEAN) ? (e > s ? 1.0f / (float)(e - s) : 0.0f) : 1.0f;
+    if (VEC) {
+      for (int c = g.gl * 4; c < D; c += G * 4) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        int64_t j = s;
+        for (; j + 1 < e; j += 2) {  // two rows in flight per lane
+          const int r0 = uslots[inv[j]], r1 = uslots[inv[j + 1]];
+          const float4 v0 = __ldg(reinterpret_cast<const float4*>(fast + (int64_t)r0 * D + c));
+          const float4 v1 = __ldg(reinterpret_cast<const float4*>(fast + (int64_t)r1 * D + c));
+          const float w0 = psw ? psw[j] : 1.0f, w1 = psw ? psw[j + 1] : 1.0f;
+          acc.x += w0 * v0.x; acc.y += w0 * v0.y; acc.z += w0 * v0.z; acc.w += w0 * v0.w;
+          acc.x += w1 * v1.x; acc.y += w1 * v1.y; acc.z += w1 * v1.z; acc.w += w1 * v1.w;
+        }
+        if (j < e) {
+          const int r0 = uslots[inv[j]];
+          const float4 v0 = __ldg(reinterpret_cast<const float4*>(fast + (int64_t)r0 * D + c));
+          const float w0 = psw ? psw[j] : 1.0f;
+          acc.x += w0 * v0.x; acc.y += w0 * v0.y; acc.z += w0 * v0.z; acc.w += w0 * v0.w;
+        }
+        acc.x *= scale; acc.y *= scale; acc.z *= scale; acc.w *= scale;
+        __stcs(reinterpret_cast<float4*>(out + b * D + c), acc);
+      }
+    } else {
+      for (int c = g.gl; c < D; c += G) {
+        float acc = 0.f;
+        for (int64_t j = s; j < e; ++j) {
+          const float w = psw ? psw[j] : 1.0f;
+          acc += w * fast[(int64_t)uslots[inv[j]] * D + c];
+        }
+        out[b * D + c] = acc * scale;
+      }
+    }
+  }
+}
+
+int launch_pool(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const void* offsets, int off_bytes,
+                int64_t nbags, int include_last, const float* psw, int mode, float* out, cudaStream_t st) {
+  if (nbags <= 0) return FC_OK;
+  const int D = h->dim;
+  const bool v = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  const int G = row_group(D, v);
+  const int grid = grid_for(nbags * G, kNT, kSMs * 16);
+#define FC_POOL(VV, T) \
+  k_pool<VV, T><<<grid, kNT, 0, st>>>(h->fast, D, uslots, inv, n, (const T*)offsets, nbags, include_last, psw, mode, out, G)
+  if (off_bytes == 4) {
+    if (v) FC_POOL(true, int32_t); else FC_POOL(false, int32_t);
+  } else {
+    if (v) FC_POOL(true, long long); else FC_POOL(false, long long);
+  }
+#undef FC_POOL
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------- gather_unique (:509-510)
+template <bool VEC>
+__global__ void __launch_bounds__(kNT) k_gather_rows(const float* __restrict__ fast, int D, const int32_t* __restrict__ slots,
+                                                     int64_t n, float* __restrict__ out, int G) {
+  GroupIdx g(G);
+  for (int64_t base = g.warp * g.gpw; base < n; base += g.nwarps * g.gpw) {
+    const int64_t p = base + g.gw;
+    if (p < n) copy_row<VEC>(out + p * D, fast + (int64_t)slots[p] * D, D, g.gl, G);
+  }
+}
+
+int launch_gather_rows(fc_cache* h, const int32_t* slots, int64_t n, float* out, cudaStream_t st) {
+  if (n <= 0) return FC_OK;
+  const bool v = (h->dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  const int G = row_group(h->dim, v);
+  const int grid = grid_for(n * G, kNT, kSMs * 16);
+  if (v) k_gather_rows<true><<<grid, kNT, 0, st>>>(h->fast, h->dim, slots, n, out, G);
+  else k_gather_rows<false><<<grid, kNT, 0, st>>>(h->fast, h->dim, slots, n, out, G);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------- apply_unique_update (:517-523)
+__global__ void __launch_bounds__(kNT) k_unique_add(float* fast, int D, const int32_t* __restrict__ uslots, int64_t u,
+                                                    const float* __restrict__ add, uint8_t* dirty, int G) {
+  GroupIdx g(G);
+  for (int64_t base = g.warp * g.gpw; base < u; base += g.nwarps * g.gpw) {
+    const int64_t p = base + g.gw;
+    if (p >= u) continue;
+    const int64_t s = uslots[p];
+    for (int c = g.gl; c < D; c += G) fast[s * D + c] = __fadd_rn(fast[s * D + c], add[p * D + c]);
+    if (g.gl == 0) dirty[s] = 1;
+  }
+}
+
+int launch_unique_add(fc_cache* h, const int32_t* uslots, int64_t u, const float* add, cudaStream_t st) {
+  if (u <= 0) return FC_OK;
+  const int G = row_group(h->dim, false);
+  k_unique_add<<<grid_for(u * G, kNT, kSMs * 16), kNT, 0, st>>>(h->fast, h->dim, uslots, u, add, h->dirty, G);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------- the simulator's update (simulator.py:229-260,433)
+__device__ __forceinline__ float hash_unit(uint64_t v, uint64_t salt) {
+  uint64_t z = v * 0x9E3779B97F4A7C15ull + salt;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  z ^= z >> 31;
+  return __fmul_rn(__uint2float_rn((unsigned)(z >> 40)), 5.9604644775390625e-08f);  // * 2^-24, exact
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kNT) k_synthetic(float* fast, int D, const int32_t* __restrict__ uids,
+                                                   const int32_t* __restrict__ ucnt, const int32_t* __restrict__ uslots,
+                                                   int64_t u, uint64_t salt, const float* __restrict__ colw,
+                                                   uint8_t* dirty, int G) {
+  GroupIdx g(G);
+  for (int64_t base = g.warp * g.gpw; base < u; base += g.nwarps * g.gpw) {
+    const int64_t p = base + g.gw;
+    if (p >= u) continue;
+    // g = (hash - 0.5) * count, all fp32 with round-to-nearest like numpy
+    const float gs = __fmul_rn(__fsub_rn(hash_unit((uint64_t)uids[p], salt), 0.5f), __int2float_rn(ucnt[p]));
+    const int64_t s = uslots[p];
+    float* row = fast + s * D;
+    if (VEC) {
+      for (int c = g.gl * 4; c < D; c += G * 4) {
+        float4 w = *reinterpret_cast<float4*>(row + c);
+        const float4 cw = *reinterpret_cast<const float4*>(colw + c);
+        w.x = __fadd_rn(w.x, __fmul_rn(gs, cw.x));
+        w.y = __fadd_rn(w.y, __fmul_rn(gs, cw.y));
+        w.z = __fadd_rn(w.z, __fmul_rn(gs, cw.z));
+        w.w = __fadd_rn(w.w, __fmul_rn(gs, cw.w));
+        *reinterpret_cast<float4*>(row + c) = w;
+      }
+    } else {
+      for (int c = g.gl; c < D; c += G) row[c] = __fadd_rn(row[c], __fmul_rn(gs, colw[c]));
+    }
+    if (g.gl == 0) dirty[s] = 1;
+  }
+}
+
+int launch_synthetic(fc_cache* h, const int32_t* uids, const int32_t* ucnt, const int32_t* uslots, int64_t u,
+                     uint64_t salt, const float* colw, cudaStream_t st) {
+  if (u <= 0) return FC_OK;
+  const bool v = (h->dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(colw) & 15) == 0);
+  const int G = row_group(h->dim, v);
+  const int grid = grid_for(u * G, kNT, kSMs * 16);
+  if (v) k_synthetic<true><<<grid, kNT, 0, st>>>(h->fast, h->dim, uids, ucnt, uslots, u, salt, colw, h->dirty, G);
+  else k_synthetic<false><<<grid, kNT, 0, st>>>(h->fast, h->dim, uids, ucnt, uslots, u, salt, colw, h->dirty, G);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------- grouping occurrences by unique row
+// keys = inverse (unique position), values = occurrence index; stable sort keeps batch order
+struct Grouping {
+  int32_t* order;      // [n] occurrence indices grouped by unique row, batch order inside a group
+  int32_t* seg_start;  // [u+1]
+  char* rest;          // remaining scratch
+};
+
+static int key_bits_for(int64_t u) {
+  int b = 1;
+  while ((int64_t(1) << b) < u) ++b;
+  return b;
+}
+
+__global__ void k_iota(int32_t* v, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) v[i] = (int32_t)i;
+}
+
+static size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
+
+static size_t grouping_bytes(int64_t n, int64_t u) {
+  return align16(n * 4) * 3 + align16((u + 1) * 4) + align16(scan_scratch_bytes(u)) + align16(sort_scratch_bytes(n));
+}
+
+static int build_grouping(fc_cache* h, const int32_t* inv, const int32_t* ucnt, int64_t u, int64_t n, size_t extra,
+                          Grouping& out, cudaStream_t st) {
+  const size_t need = grouping_bytes(n, u) + extra;
+  int rc = ensure_scratch(h, need);
+  if (rc) return rc;
+  char* p = static_cast<char*>(h->scratch);
+  int32_t* iota = reinterpret_cast<int32_t*>(p);
+  p += align16(n * 4);
+  uint32_t* ksorted = reinterpret_cast<uint32_t*>(p);
+  p += align16(n * 4);
+  out.order = reinterpret_cast<int32_t*>(p);
+  p += align16(n * 4);
+  out.seg_start = reinterpret_cast<int32_t*>(p);
+  p += align16((u + 1) * 4);
+  void* scan_scr = p;
+  p += align16(scan_scratch_bytes(u));
+  void* sort_scr = p;
+  p += align16(sort_scratch_bytes(n));
+  out.rest = p;
+  k_iota<<<grid_for(n, kNT, kSMs * 8), kNT, 0, st>>>(iota, n);
+  rc = radix_sort_pairs(reinterpret_cast<const uint32_t*>(inv), iota, ksorted, out.order, n, key_bits_for(u), sort_scr,
+                        st);
+  if (rc) return rc;
+  return exclusive_scan_i32(ucnt, out.seg_start, u, scan_scr, st);
+}
+
+// ------------------------------------------------------------- scatter_update (:423-438), bit-exact with np.add.at
+template <bool VEC>
+__global__ void __launch_bounds__(kNT) k_seg_add_seq(float* fast, int D, const int32_t* __restrict__ uslots, int64_t u,
+                                                     const int32_t* __restrict__ seg, const int32_t* __restrict__ order,
+                                                     const float* __restrict__ deltas, uint8_t* dirty, int G) {
+  GroupIdx g(G);
+  for (int64_t base = g.warp * g.gpw; base < u; base += g.nwarps * g.gpw) {
+    const int64_t p = base + g.gw;
+    if (p >= u) continue;
+    const int64_t s = uslots[p];
+    float* row = fast + s * D;
+    const int j0 = seg[p], j1 = seg[p + 1];
+    for (int c = g.gl; c < D; c += G) {
+      float acc = row[c];
+      for (int j = j0; j < j1; ++j) acc = __fadd_rn(acc, deltas[(int64_t)order[j] * D + c]);  // batch order
+      row[c] = acc;
+    }
+    if (g.gl == 0) dirty[s] = 1;
+  }
+}
+
+int launch_scatter_update(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u,
+                          int64_t n, const float* deltas, cudaStream_t st) {
+  if (u <= 0 || n <= 0) return FC_OK;
+  Grouping gr;
+  int rc = build_grouping(h, inv, ucnt, u, n, 0, gr, st);
+  if (rc) return rc;
+  const int G = row_group(h->dim, false);
+  k_seg_add_seq<false><<<grid_for(u * G, kNT, kSMs * 16), kNT, 0, st>>>(h->fast, h->dim, uslots, u, gr.seg_start,
+                                                                      gr.order, deltas, h->dirty, G);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------- backward + sparse optimizer (north star item 6)
+// Occurrences grouped by unique row are cut into parts of <= kPart occurrences.
+// Phase 1 (one row group per part) sums coef_j * grad_out[bag(j)] in batch order;
+// single-part rows apply the optimizer directly, others write a partial row.
+// Phase 2 sums a multi-part row's partials in part order, then applies the
+// optimizer. Fixed summation order -> deterministic results.
+constexpr int kPart = 128;
+
+template <typename OffT>
+__global__ void __launch_bounds__(kNT) k_bag_coef(const OffT* __restrict__ off, int64_t nbags, int64_t n, int incl,
+                                                  const float* __restrict__ psw, int mode, int32_t* bag_of,
+                                                  float* coef) {
+  for (int64_t b = (int64_t)blockIdx.x * kNT + threadIdx.x; b < nbags; b += (int64_t)gridDim.x * kNT) {
+    int64_t s, e;
+    bag_bounds(off, b, nbags, n, incl, s, e);
+    const float scale = (mode == FC_POOL_MEAN) ? (e > s ? 1.0f / (float)(e - s) : 0.0f) : 1.0f;
+    for (int64_t j = s; j < e; ++j) {
+      bag_of[j] = (int32_t)b;
+      coef[j] = psw ? scale * psw[j] : scale;
+    }
+  }
+}
+
+__global__ void k_parts(const int32_t* __restrict__ ucnt, int64_t u, int32_t* nparts) {
+  for (int64_t p = (int64_t)blockIdx.x * kNT + threadIdx.x; p < u; p += (int64_t)gridDim.x * kNT)
+    nparts[p] = (ucnt[p] + kPart - 1) / kPart;
+}
+
+__global__ void k_part_map(const int32_t* __restrict__ nparts, const int32_t* __restrict__ pstart, int64_t u,
+                           int32_t* part_seg) {
+  for (int64_t p = (int64_t)blockIdx.x * kNT + threadIdx.x; p < u; p += (int64_t)gridDim.x * kNT)
+    for (int k = 0; k < nparts[p]; ++k) part_seg[pstart[p] + k] = (int32_t)p;
+}
+
+struct OptArgs {
+  int optim;
+  float lr, eps;
+};
+
+__device__ __forceinline__ void apply_opt(float* w, float* st, int c, float gsum, const OptArgs& o) {
+  if (o.optim == FC_OPT_ADAGRAD) {
+    const float s = st[c] + gsum * gsum;
+    st[c] = s;
+    w[c] -= o.lr * gsum / (sqrtf(s) + o.eps);
+  } else {
+    w[c] -= o.lr * gsum;
+  }
+}
+
+template <bool VEC>
+__global__ void __launch_bounds__(kNT) k_bwd_parts(float* fast, float* fstate, int D, const int32_t* __restrict__ uslots,
+                                                   const int32_t* __restrict__ ucnt, const int32_t* __restrict__ seg,
+                                                   const int32_t* __restrict__ order, const int32_t* __restrict__ nparts,
+                                                   const int32_t* __restrict__ pstart, const int32_t* __restrict__ part_seg,
+                                                   const int32_t* total_parts, const int32_t* __restrict__ bag_of,
+                                                   const float* __restrict__ coef, const float* __restrict__ grad,
+                                                   float* partial, uint8_t* dirty, OptArgs o, int G) {
+  const int64_t T = *total_parts;
+  GroupIdx g(G);
+  for (int64_t base = g.warp * g.gpw; base < T; base += g.nwarps * g.gpw) {
+    const int64_t t = base + g.gw;
+    if (t >= T) continue;
+    const int p = part_seg[t];
+    const int k = (int)(t - pstart[p]);
+    const int j0 = seg[p] + k * kPart;
+    const int j1 = min(seg[p] + ucnt[p], j0 + kPart);
+    const bool single = nparts[p] == 1;
+    const int64_t s = uslots[p];
+    for (int c = g.gl * (VEC ? 4 : 1); c < D; c += G * (VEC ? 4 : 1)) {
+      if (VEC) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = j0; j < j1; ++j) {
+          const int i = order[j];
+          const float cf = coef[i];
+          const float4 gv = __ldg(reinterpret_cast<const float4*>(grad + (int64_t)bag_of[i] * D + c));
+          acc.x += cf * gv.x; acc.y += cf * gv.y; acc.z += cf * gv.z; acc.w += cf * gv.w;
+        }
+        if (single) {
+          float* w = fast + s * D;
+          float* stt = fstate ? fstate + s * D : nullptr;
+          apply_opt(w, stt, c, acc.x, o);
+          apply_opt(w, stt, c + 1, acc.y, o);
+          apply_opt(w, stt, c + 2, acc.z, o);
+          apply_opt(w, stt, c + 3, acc.w, o);
+        } else {
+          *reinterpret_cast<float4*>(partial + t * D + c) = acc;
+        }
+      } else {
+        float acc = 0.f;
+        for (int j = j0; j < j1; ++j) {
+          const int i = order[j];
+          acc += coef[i] * grad[(int64_t)bag_of[i] * D + c];
+        }
+        if (single) apply_opt(fast + s * D, fstate ? fstate + s * D : nullptr, c, acc, o);
+        else partial[t * D + c] = acc;
+      }
+    }
+    if (single && g.gl == 0) dirty[s] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(kNT) k_bwd_combine(float* fast, float* fstate, int D, const int32_t* __restrict__ uslots,
+                                                     int64_t u, const int32_t* __restrict__ nparts,
+                                                     const int32_t* __restrict__ pstart, const float* __restrict__ partial,
+                                                     uint8_t* dirty, OptArgs o, int G) {
+  GroupIdx g(G);
+  for (int64_t base = g.warp * g.gpw; base < u; base += g.nwarps * g.gpw) {
+    const int64_t p = base + g.gw;
+    if (p >= u || nparts[p] <= 1) continue;
+    const int64_t s = uslots[p];
+    const int t0 = pstart[p], t1 = t0 + nparts[p];
+    for (int c = g.gl; c < D; c += G) {
+      float acc = 0.f;
+      for (int t = t0; t < t1; ++t) acc += partial[(int64_t)t * D + c];
+      apply_opt(fast + s * D, fstate ? fstate + s * D : nullptr, c, acc, o);
+    }
+    if (g.gl == 0) dirty[s] = 1;
+  }
+}
+
+int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u, int64_t n,
+                    const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw, int mode,
+                    const float* grad, int optim, float lr, float eps, cudaStream_t st) {
+  if (u <= 0 || n <= 0) return FC_OK;
+  if (optim == FC_OPT_ADAGRAD && (h->fast_state == nullptr || h->sw != h->dim)) {
+    set_error("Adagrad needs a cache created with state_width == dim");
+    return FC_ERR_BAD_ARG;
+  }
+  const int D = h->dim;
+  const int64_t max_parts = n / kPart + u + 1;
+  const size_t extra = align16(n * 4) * 2 + align16(u * 4) + align16((u + 1) * 4) + align16(max_parts * 4) +
+                       align16(max_parts * (size_t)D * 4) + align16(scan_scratch_bytes(u));
+  Grouping gr;
+  int rc = build_grouping(h, inv, ucnt, u, n, extra, gr, st);
+  if (rc) return rc;
+  char* p = gr.rest;
+  int32_t* bag_of = reinterpret_cast<int32_t*>(p);
+  p += align16(n * 4);
+  float* coef = reinterpret_cast<float*>(p);
+  p += align16(n * 4);
+  int32_t* nparts = reinterpret_cast<int32_t*>(p);
+  p += align16(u * 4);
+  int32_t* pstart = reinterpret_cast<int32_t*>(p);
+  p += align16((u + 1) * 4);
+  int32_t* part_seg = reinterpret_cast<int32_t*>(p);
+  p += align16(max_parts * 4);
+  float* partial = reinterpret_cast<float*>(p);
+  p += align16(max_parts * (size_t)D * 4);
+  void* scan_scr = p;
+
+  const int gb = grid_for(nbags, kNT, kSMs * 8);
+  // occurrences outside every bag (include_last_offset with a short last offset) contribute 0
+  FC_CUDA(cudaMemsetAsync(bag_of, 0, n * 4, st));
+  FC_CUDA(cudaMemsetAsync(coef, 0, n * 4, st));
+  if (off_bytes == 4)
+    k_bag_coef<int32_t><<<gb, kNT, 0, st>>>((const int32_t*)offsets, nbags, n, include_last, psw, mode, bag_of, coef);
+  else
+    k_bag_coef<long long><<<gb, kNT, 0, st>>>((const long long*)offsets, nbags, n, include_last, psw, mode, bag_of,
+                                             coef);
+  const int gu = grid_for(u, kNT, kSMs * 8);
+  k_parts<<<gu, kNT, 0, st>>>(ucnt, u, nparts);
+  rc = exclusive_scan_i32(nparts, pstart, u, scan_scr, st);
+  if (rc) return rc;
+  k_part_map<<<gu, kNT, 0, st>>>(nparts, pstart, u, part_seg);
+  const bool v = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 15) == 0);
+  const int G = row_group(D, v);
+  OptArgs o{optim, lr, eps};
+  const int grid = grid_for(max_parts * G, kNT, kSMs * 16);
+  if (v)
+    k_bwd_parts<true><<<grid, kNT, 0, st>>>(h->fast, h->fast_state, D, uslots, ucnt, gr.seg_start, gr.order, nparts,
+                                            pstart, part_seg, pstart + u, bag_of, coef, grad, partial, h->dirty, o, G);
+  else
+    k_bwd_parts<false><<<grid, kNT, 0, st>>>(h->fast, h->fast_state, D, uslots, ucnt, gr.seg_start, gr.order, nparts,
+                                             pstart, part_seg, pstart + u, bag_of, coef, grad, partial, h->dirty, o, G);
+  const int G1 = row_group(D, false);
+  k_bwd_combine<<<grid_for(u * G1, kNT, kSMs * 16), kNT, 0, st>>>(h->fast, h->fast_state, D, uslots, u, nparts, pstart,
+                                                                  partial, h->dirty, o, G1);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+}  // namespace fc

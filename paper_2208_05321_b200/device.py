@@ -1,0 +1,213 @@
+"""`DeviceCache`: the Python owner of one libfreqcache_b200 handle.
+
+Thin ctypes plumbing: torch supplies device memory for per-call outputs, the
+current CUDA stream and zero-copy tensor views of the handle's HBM state; all
+cache computation happens in the library's sm_100a kernels.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .errors import check
+
+
+class _CudaArray:
+    """`__cuda_array_interface__` wrapper so torch can view handle-owned memory."""
+
+    def __init__(self, ptr: int, shape, typestr: str, owner):
+        self._owner = owner  # keeps the handle (and its memory) alive
+        self.__cuda_array_interface__ = {"shape": tuple(int(s) for s in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 3, "strides": None}
+
+
+def _ptr(t) -> int:
+    return 0 if t is None else int(t.data_ptr())
+
+
+class DeviceCache:
+    """One device-resident cache (a CacheStack's state + fast tier) on one GPU."""
+
+    def __init__(self, num_ids: int, capacity: int, dim: int, *, state_width: int = 0,
+                 write_back: str = "dirty_only", evict_mode: str = "occupancy_aware",
+                 buffer_bytes: int = 64 * 2**20, device=None):
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("freqcache_b200 needs a CUDA device (no CPU fallback)")
+        self.torch = torch
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else
+                                   torch.device(device).index or 0)
+        self.lib = _lib.load()
+        self.num_ids, self.capacity, self.dim, self.state_width = int(num_ids), int(capacity), int(dim), int(state_width)
+        self.write_back, self.evict_mode = write_back, evict_mode
+        self.buffer_bytes = int(buffer_bytes)
+        h = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            check(self.lib.fc_create(self.num_ids, self.capacity, self.dim, self.state_width,
+                                     _lib.WB[write_back], _lib.EVICT[evict_mode], self.buffer_bytes,
+                                     self.device.index, ctypes.byref(h)))
+        self.h = h
+        v = _lib.Views()
+        check(self.lib.fc_get_views(self.h, ctypes.byref(v)))
+        dev = self.device
+
+        def view(ptr, shape, typestr):
+            return torch.as_tensor(_CudaArray(ptr, shape, typestr, self), device=dev)
+
+        self.fast_rows = view(v.fast_rows, (self.capacity, self.dim), "<f4")
+        self.fast_state = view(v.fast_state, (self.capacity, self.state_width), "<f4") if self.state_width else None
+        self.slot_to_rank = view(v.slot_to_rank, (self.capacity,), "<i4")
+        self.rank_to_slot = view(v.rank_to_slot, (self.num_ids,), "<i4")
+        self.dirty = view(v.dirty, (self.capacity,), "|u1")
+        self.rank_of = view(v.rank_of, (self.num_ids,), "<i4")
+        self._slow = None
+        self._slow_state = None
+
+    # ------------------------------------------------------------------ plumbing
+    def stream(self):
+        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.fc_destroy(self.h)
+            self.h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_modes(self, write_back: str, evict_mode: str) -> None:
+        if (write_back, evict_mode) != (self.write_back, self.evict_mode):
+            check(self.lib.fc_set_modes(self.h, _lib.WB[write_back], _lib.EVICT[evict_mode]))
+            self.write_back, self.evict_mode = write_back, evict_mode
+
+    @property
+    def free_count(self) -> int:
+        return int(self.lib.fc_free_count(self.h))
+
+    def to_device_ids(self, ids):
+        """Accept numpy / list / torch ids; return a contiguous CUDA int64/int32 tensor."""
+        torch = self.torch
+        if isinstance(ids, torch.Tensor):
+            t = ids.reshape(-1)
+            if t.dtype not in (torch.int64, torch.int32):
+                t = t.to(torch.int64)
+            return t.to(self.device, non_blocking=True).contiguous()
+        a = np.asarray(ids).reshape(-1)
+        if a.dtype not in (np.int64, np.int32):
+            a = a.astype(np.int64)
+        return torch.from_numpy(np.ascontiguousarray(a)).to(self.device)
+
+    # ------------------------------------------------------------------ setup
+    def set_idx_map(self, rank_of: np.ndarray) -> None:
+        r = np.ascontiguousarray(np.asarray(rank_of, dtype=np.int64))
+        if r.shape != (self.num_ids,):
+            raise ValueError(f"rank_of must have {self.num_ids} entries")
+        check(self.lib.fc_set_idx_map(self.h, r.ctypes.data_as(ctypes.c_void_p), self.stream()))
+
+    def attach_slow(self, rows: np.ndarray, state_rows: np.ndarray | None = None) -> None:
+        if rows.dtype != np.float32 or rows.shape[1] != self.dim or rows.shape[0] != self.num_ids:
+            raise ValueError("slow tier must be float32 [num_ids, dim]")
+        ld = rows.strides[0] // 4
+        sp, sld = None, 0
+        if state_rows is not None:
+            sp, sld = state_rows.ctypes.data_as(ctypes.c_void_p), state_rows.strides[0] // 4
+        check(self.lib.fc_attach_slow_tier(self.h, rows.ctypes.data_as(ctypes.c_void_p), ld, sp, sld))
+        self._slow, self._slow_state = rows, state_rows  # keep the host buffers alive
+
+    # ------------------------------------------------------------------ verbs
+    def warmup(self, k: int) -> None:
+        check(self.lib.fc_warmup(self.h, int(k), self.stream()))
+
+    def prepare(self, ids, batch_seq: int = 0):
+        """Run prepare_cache on device. Returns (info, uids, ucnt, uranks, uslots, inverse, d_ids)."""
+        torch = self.torch
+        d_ids = self.to_device_ids(ids)
+        n = int(d_ids.numel())
+        k = min(n, self.capacity)
+        buf = torch.empty(4 * k + n, dtype=torch.int32, device=self.device)
+        uids, ucnt, uranks, uslots = buf[:k], buf[k:2 * k], buf[2 * k:3 * k], buf[3 * k:4 * k]
+        inverse = buf[4 * k:]
+        info = _lib.PrepareInfo()
+        rc = self.lib.fc_prepare(self.h, ctypes.c_void_p(_ptr(d_ids)), d_ids.element_size(), n, int(batch_seq),
+                                 ctypes.c_void_p(_ptr(uids)), ctypes.c_void_p(_ptr(ucnt)),
+                                 ctypes.c_void_p(_ptr(uranks)), ctypes.c_void_p(_ptr(uslots)),
+                                 ctypes.c_void_p(_ptr(inverse)), self.stream(), ctypes.byref(info))
+        check(rc)
+        u = int(info.unique)
+        return info, uids[:u], ucnt[:u], uranks[:u], uslots[:u], inverse, d_ids
+
+    def last_events(self, evictions: int, misses: int):
+        ev = np.empty(evictions, dtype=np.int64)
+        ad = np.empty(misses, dtype=np.int64)
+        check(self.lib.fc_last_events(self.h, ev.ctypes.data_as(ctypes.c_void_p),
+                                      ad.ctypes.data_as(ctypes.c_void_p), self.stream()))
+        return ev, ad
+
+    def flush(self) -> int:
+        rows = ctypes.c_int64()
+        check(self.lib.fc_flush(self.h, self.stream(), ctypes.byref(rows)))
+        return int(rows.value)
+
+    def mark_dirty(self, slots: np.ndarray) -> None:
+        d = self.torch.from_numpy(np.ascontiguousarray(slots, dtype=np.int64)).to(self.device)
+        check(self.lib.fc_mark_dirty(self.h, ctypes.c_void_p(_ptr(d)), int(d.numel()), self.stream()))
+
+    def select_evictions(self, needed: int, protected: np.ndarray) -> np.ndarray:
+        p = self.torch.from_numpy(np.ascontiguousarray(protected, dtype=np.int64)).to(self.device)
+        out = np.empty(max(needed, 0), dtype=np.int64)
+        check(self.lib.fc_select_evictions(self.h, int(needed), ctypes.c_void_p(_ptr(p)), int(p.numel()),
+                                           out.ctypes.data_as(ctypes.c_void_p), self.stream()))
+        return out
+
+    def pooled(self, uslots, inverse, n: int, offsets=None, n_bags: int | None = None, include_last_offset=False,
+               per_sample_weights=None, mode: str = "sum", out=None):
+        torch = self.torch
+        if offsets is None:
+            n_bags = n
+        elif n_bags is None:
+            n_bags = int(offsets.numel()) - (1 if include_last_offset else 0)
+        if out is None:
+            out = torch.empty((n_bags, self.dim), dtype=torch.float32, device=self.device)
+        check(self.lib.fc_pooled_forward(self.h, ctypes.c_void_p(_ptr(uslots)), ctypes.c_void_p(_ptr(inverse)), n,
+                                         ctypes.c_void_p(_ptr(offsets)), 0 if offsets is None else offsets.element_size(),
+                                         n_bags, int(bool(include_last_offset)),
+                                         ctypes.c_void_p(_ptr(per_sample_weights)), _lib.POOL[mode],
+                                         ctypes.c_void_p(_ptr(out)), self.stream()))
+        return out
+
+    def gather_rows(self, slots):
+        out = self.torch.empty((int(slots.numel()), self.dim), dtype=self.torch.float32, device=self.device)
+        check(self.lib.fc_gather_rows(self.h, ctypes.c_void_p(_ptr(slots)), int(slots.numel()),
+                                      ctypes.c_void_p(_ptr(out)), self.stream()))
+        return out
+
+    def unique_add(self, uslots, add) -> None:
+        check(self.lib.fc_apply_unique_update(self.h, ctypes.c_void_p(_ptr(uslots)), int(uslots.numel()),
+                                              ctypes.c_void_p(_ptr(add)), self.stream()))
+
+    def synthetic(self, uids, ucnt, uslots, salt: int, colw) -> None:
+        check(self.lib.fc_apply_synthetic_update(self.h, ctypes.c_void_p(_ptr(uids)), ctypes.c_void_p(_ptr(ucnt)),
+                                                 ctypes.c_void_p(_ptr(uslots)), int(uslots.numel()),
+                                                 ctypes.c_uint64(int(salt) % (1 << 64)),
+                                                 ctypes.c_void_p(_ptr(colw)), self.stream()))
+
+    def scatter_update(self, uslots, inverse, ucnt, deltas) -> None:
+        check(self.lib.fc_scatter_update(self.h, ctypes.c_void_p(_ptr(uslots)), ctypes.c_void_p(_ptr(inverse)),
+                                         ctypes.c_void_p(_ptr(ucnt)), int(uslots.numel()), int(inverse.numel()),
+                                         ctypes.c_void_p(_ptr(deltas)), self.stream()))
+
+    def backward_update(self, uslots, inverse, ucnt, offsets, n_bags, include_last_offset, per_sample_weights,
+                        mode, grad_out, optim: str, lr: float, eps: float) -> None:
+        check(self.lib.fc_backward_update(
+            self.h, ctypes.c_void_p(_ptr(uslots)), ctypes.c_void_p(_ptr(inverse)), ctypes.c_void_p(_ptr(ucnt)),
+            int(uslots.numel()), int(inverse.numel()), ctypes.c_void_p(_ptr(offsets)),
+            0 if offsets is None else offsets.element_size(), int(n_bags), int(bool(include_last_offset)),
+            ctypes.c_void_p(_ptr(per_sample_weights)), _lib.POOL[mode], ctypes.c_void_p(_ptr(grad_out)),
+            _lib.OPTIM[optim], float(lr), float(eps), self.stream()))
