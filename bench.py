@@ -1,0 +1,391 @@
+#!/usr/bin/env python
+"""bench.py — cached-embedding lookups/s on B200 (BASELINE.json metric).
+
+Workload (N=1): BASELINE configs[1], the Criteo-Kaggle shape — 33,762,577 rows x
+dim 128 fp32, frequency-reordered cache at 1.5% (506,438 slots), Zipf(1.05) ids
+from the reference generator's stream, batch 16384 x 26 (425,984 lookups/step).
+One step = the reference simulator's per-batch work (simulator.py:416-455):
+prepare_cache -> lookup (pooled EmbeddingBag forward, sum, bag size 1) -> the
+deterministic row update, all through libfreqcache_b200 kernels.
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config small]
+
+`--impl reference` times the reference CPU path (the oracle port in oracle/, the
+reference itself cannot run on the GPU box) on the same workload.
+Prints ONE JSON line on rank 0.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # BASELINE configs[1]
+    "criteo_kaggle": dict(num_ids=33_762_577, dim=128, ratio=0.015, alpha=1.05, batch=16384, features=26),
+    # BASELINE configs[0] (reference CPU-runnable case)
+    "small": dict(num_ids=1_000_000, dim=128, ratio=0.015, alpha=1.05, batch=1024, features=26),
+}
+SEED = 1
+UPDATES_SEED = 7
+METRIC = "cached-embedding lookups/sec"
+KERNELS_PER_STEP = 20 + 1 + 1  # prepare sequence + pooled forward + fused update
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+# ----------------------------------------------------------------------------- workload
+def make_workload(cfg, n_batches, device=None):
+    from paper_2208_05321_b200 import workload
+    from paper_2208_05321_b200.store import fast_capacity
+
+    t0 = time.perf_counter()
+    tr = workload.gen_zipf(cfg["num_ids"], cfg["alpha"], n_batches * cfg["batch"], cfg["features"], SEED,
+                           device=device)
+    t1 = time.perf_counter()
+    # frequency reorder over the whole trace (simulator.py:363-364)
+    if device is not None:
+        import torch
+
+        ids = torch.from_numpy(tr.samples.reshape(-1)).to(device).long()
+        counts = torch.bincount(ids, minlength=cfg["num_ids"])
+        id_of = torch.sort(-counts, stable=True).indices.cpu().numpy().astype(np.int64)
+        del ids, counts
+    else:
+        counts = np.bincount(tr.samples.reshape(-1), minlength=cfg["num_ids"])
+        id_of = np.argsort(-counts, kind="stable").astype(np.int64)
+    rank_of = np.empty_like(id_of)
+    rank_of[id_of] = np.arange(id_of.size, dtype=np.int64)
+    log(f"[bench] trace {tr.samples.shape} in {t1 - t0:.1f}s, reorder {time.perf_counter() - t1:.1f}s")
+    return tr.samples, rank_of, id_of, fast_capacity(cfg["num_ids"], cfg["ratio"])
+
+
+# ----------------------------------------------------------------------------- measurement helpers
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def host_link_peaks(torch, dev):
+    """Pinned cudaMemcpy bandwidth H2D / D2H / both at once (the host-link roofline)."""
+    n = 256 << 20
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    h2 = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    d2 = torch.empty(n, dtype=torch.uint8, device=dev)
+    s1, s2 = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+
+    def best(fn, reps=5):
+        b = 1e9
+        for _ in range(reps):
+            torch.cuda.synchronize(dev)
+            t = time.perf_counter()
+            fn()
+            torch.cuda.synchronize(dev)
+            b = min(b, time.perf_counter() - t)
+        return b
+
+    best(lambda: d.copy_(h, non_blocking=True), 2)
+
+    def both():
+        with torch.cuda.stream(s1):
+            d.copy_(h, non_blocking=True)
+        with torch.cuda.stream(s2):
+            h2.copy_(d2, non_blocking=True)
+
+    r = {"h2d_GBps": n / best(lambda: d.copy_(h, non_blocking=True)) / 1e9,
+         "d2h_GBps": n / best(lambda: h.copy_(d, non_blocking=True)) / 1e9,
+         "bidir_GBps": 2 * n / best(both) / 1e9}
+    del h, h2, d, d2
+    return r
+
+
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        return float(json.load(open(p))["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ----------------------------------------------------------------------------- CPU reference arm
+def run_cpu_reference(samples, rank_of, cap, cfg, steps, warmup, time_budget_s=None):
+    """The reference's per-batch loop on host cores through the numpy oracle port:
+    prepare + gather + apply_unique_update (simulator.py:419-433). Slow tier is a
+    lazily materialised buffer (only rows that move are touched)."""
+    import oracle
+
+    D = cfg["dim"]
+    slow = np.empty((cfg["num_ids"], D), dtype=np.float32)  # lazily zero-filled pages
+    orc = oracle.OracleCache(rank_of, slow, cap)
+    orc.warmup(cap)
+    colw = oracle.column_weights(D, UPDATES_SEED)
+    B = cfg["batch"]
+    times = []
+    t_start = time.perf_counter()
+    for s in range(warmup + steps):
+        ids = samples[s * B:(s + 1) * B].reshape(-1)
+        t = time.perf_counter()
+        p = orc.prepare(ids, s)
+        _ = orc.gather(p)
+        g = oracle.row_scalars(p["unique_ids"], p["unique_counts"], s, UPDATES_SEED)
+        orc.apply_unique_update(p, g[:, None] * colw[None, :])
+        dt = time.perf_counter() - t
+        if s >= warmup:
+            times.append(dt)
+        if time_budget_s and time.perf_counter() - t_start > time_budget_s and len(times) >= 3:
+            break
+    n = B * cfg["features"]
+    return {"step_s": float(np.mean(times)), "steps": len(times), "lookups_per_s": n / float(np.mean(times))}
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args, cfg, torch, rank, world):
+    import paper_2208_05321_b200 as fc
+
+    dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
+    torch.cuda.set_device(dev)
+    W, K = args.warmup, args.steps
+    n_batches = max(args.trace_batches, W + 2 * K)
+    samples, rank_of, id_of, cap = make_workload(cfg, n_batches, device=dev)
+    D, B, F = cfg["dim"], cfg["batch"], cfg["features"]
+    N = B * F
+    links = host_link_peaks(torch, dev)
+    hbm, hbm_src = hbm_peak()
+
+    t0 = time.perf_counter()
+    slow = fc.SlowTierStore.empty_pinned(cfg["num_ids"], D)
+    rows_t = torch.from_numpy(slow.rows)
+    g = torch.Generator(device=dev)
+    g.manual_seed(SEED)
+    chunk = 1 << 20
+    for lo in range(0, cfg["num_ids"], chunk):  # seeded uniform(+-0.5/D) rows, generated on device
+        hi = min(lo + chunk, cfg["num_ids"])
+        v = (torch.rand((hi - lo, D), generator=g, device=dev) - 0.5) * (1.0 / D)
+        rows_t[lo:hi].copy_(v)
+    torch.cuda.synchronize(dev)
+    log(f"[bench] slow tier {slow.rows.nbytes / 2**30:.1f} GiB pinned+filled in {time.perf_counter() - t0:.1f}s")
+
+    st = fc.CacheStack(fc.IdxMap(rank_of, id_of), slow, fc.FastTierStore(np.zeros((cap, D), np.float32)),
+                       fc.Transmitter())
+    dc = st.device
+    st.warmup(cap)
+    colw = fc.update_column_weights(D, UPDATES_SEED)
+    ids_dev = torch.from_numpy(samples).to(dev)  # int32 [n_batches*B, F], resident in HBM
+    out = torch.empty((N, D), dtype=torch.float32, device=dev)
+    stats = []
+
+    def step(s, ids):
+        prep = st.prepare(ids, s)
+        dc.pooled(prep.d_unique_slots, prep.d_inverse, N, out=out)
+        st.apply_synthetic_update(prep, s, UPDATES_SEED, colw)
+        return prep
+
+    for s in range(W):
+        step(s, ids_dev[s * B:(s + 1) * B].reshape(-1))
+    torch.cuda.synchronize(dev)
+
+    # ---- timed region: inputs resident in HBM --------------------------------
+    stream = torch.cuda.current_stream(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+    pool_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
+    dc.profile(True)
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize(dev)
+    with ClockSampler(dev.index) as clk:
+        ev[0].record(stream)
+        for k in range(K):
+            s = W + k
+            prep = st.prepare(ids_dev[s * B:(s + 1) * B].reshape(-1), s)
+            pool_ev[k][0].record(stream)
+            dc.pooled(prep.d_unique_slots, prep.d_inverse, N, out=out)
+            pool_ev[k][1].record(stream)
+            st.apply_synthetic_update(prep, s, UPDATES_SEED, colw)
+            ev[k + 1].record(stream)
+            rep_slow = sum(r.rows for r in prep.transfer_reports if r.direction == "to_slow")
+            stats.append((prep.num_unique, prep.hits, prep.misses, prep.evictions, rep_slow))
+        torch.cuda.synchronize(dev)
+    if world > 1:
+        torch.distributed.barrier()
+    prof = dc.profile(False)
+    step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(K)]
+    total_ms = ev[0].elapsed_time(ev[K])
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        total_ms = float(t.item())
+    pool_ms = [a.elapsed_time(b) for a, b in pool_ev]
+
+    # ---- e2e: the public API from pinned host ids, result read back ----------
+    ids_host = torch.from_numpy(samples).pin_memory()
+    torch.cuda.synchronize(dev)
+    t = time.perf_counter()
+    for k in range(K):
+        s = W + K + k
+        prep = st.prepare(ids_host[s * B:(s + 1) * B].reshape(-1), s)  # H2D inside
+        pooled = st.gather(prep)
+        st.apply_synthetic_update(prep, s, UPDATES_SEED, colw)
+        _ = (prep.hits, prep.misses)  # the step's result, already read back by prepare
+    torch.cuda.synchronize(dev)
+    e2e_s = time.perf_counter() - t
+    del pooled
+
+    st_arr = np.array(stats, dtype=np.float64)
+    uniq, hits, misses, evict, wb = st_arr.mean(axis=0)
+    # ---- rooflines -----------------------------------------------------------
+    xfer_ms = prof["transfer_ms"] / max(prof["calls"], 1)
+    xfer_bytes = prof["host_link_bytes"] / max(prof["calls"], 1)
+    pool_bytes = N * (4 * D + 8) + N * 4 * D  # per occurrence: inverse+slot idx+row read; per bag: row write
+    pool_avg = float(np.mean(pool_ms))
+    r_xfer = {"kernel": "k_transfer_rows", "bound": "host_link", "achieved": xfer_bytes / (xfer_ms * 1e-3) / 1e9,
+              "peak": links["bidir_GBps"], "unit": "GB/s", "traffic": None,
+              "algorithmic_bytes_per_launch": xfer_bytes, "launch_ms": xfer_ms,
+              "peak_source": "pinned cudaMemcpy H2D+D2H concurrently, measured in this run"}
+    r_xfer["frac"] = r_xfer["achieved"] / r_xfer["peak"]
+    r_pool = {"kernel": "k_pool", "bound": "hbm", "achieved": pool_bytes / (pool_avg * 1e-3) / 1e9, "peak": hbm,
+              "unit": "GB/s", "traffic": None, "algorithmic_bytes_per_launch": pool_bytes, "launch_ms": pool_avg,
+              "peak_source": hbm_src}
+    r_pool["frac"] = r_pool["achieved"] / r_pool["peak"]
+    dominant, other = (r_xfer, r_pool) if xfer_ms >= pool_avg else (r_pool, r_xfer)
+
+    res = {
+        "metric": METRIC, "value": N * K / (total_ms * 1e-3), "unit": "lookups/s", "n_gpus": world, "steps": K,
+        "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "fp32 rows, int32 ids", "data": "synthetic: reference gen_zipf stream (seed 1), seeded rows",
+        "config": {"workload": args.config, "num_rows": cfg["num_ids"], "dim": D, "cache_ratio": cfg["ratio"],
+                   "capacity": cap, "zipf_alpha": cfg["alpha"], "batch": B, "features": F, "lookups_per_step": N,
+                   "pooling": "sum, bag size 1", "step": "prepare + pooled forward + row update",
+                   "write_back": "dirty_only", "evict_mode": "occupancy_aware", "engine": "zero-copy",
+                   "l2": "inputs larger than L2 (fast tier %d MB, id/rank maps %d MB, new batch every step)"
+                         % (cap * D * 4 >> 20, cfg["num_ids"] * 12 >> 20),
+                   "parallelism": "single" if world == 1 else f"rowwise{world}"},
+        "step_latency_ms": {"p50": float(np.percentile(step_ms, 50)), "p99": float(np.percentile(step_ms, 99)),
+                            "prepare_avg": prof["prepare_ms"] / max(prof["calls"], 1), "pool_avg": pool_avg},
+        "hit_ratio": hits / uniq, "unique_per_step": uniq, "misses_per_step": misses,
+        "evictions_per_step": evict, "writeback_rows_per_step": wb,
+        "e2e": {"value": N * K / e2e_s, "unit": "lookups/s", "h2d_bytes_per_step": N * samples.itemsize,
+                "d2h_bytes_per_step": 64, "ms_per_step": e2e_s / K * 1e3,
+                "path": "CacheStack.prepare(pinned host ids) + gather + apply_synthetic_update"},
+        "gpu_launches": KERNELS_PER_STEP * K,
+        "roofline": dominant, "roofline_secondary": other,
+        "host_link": links,
+        "clocks": clk.summary(),
+    }
+    return res, samples, rank_of, cap
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="criteo_kaggle", choices=list(CONFIGS))
+    ap.add_argument("--trace-batches", type=int, default=64)
+    ap.add_argument("--cpu-baseline-steps", type=int, default=8)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    cfg = CONFIGS[args.config]
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return 0
+        n_batches = max(args.trace_batches, args.warmup + 2 * args.steps)
+        samples, rank_of, _, cap = make_workload(cfg, n_batches, device=None)
+        r = run_cpu_reference(samples, rank_of, cap, cfg, args.steps, args.warmup)
+        n = cfg["batch"] * cfg["features"]
+        out = {"metric": METRIC, "value": r["lookups_per_s"], "unit": "lookups/s", "n_gpus": args.gpus,
+               "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["step_s"] * 1e3,
+               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 rows, int32 ids",
+               "data": "synthetic: reference gen_zipf stream (seed 1)", "impl": "reference",
+               "config": {"workload": args.config, "num_rows": cfg["num_ids"], "dim": cfg["dim"],
+                          "capacity": cap, "batch": cfg["batch"], "features": cfg["features"], "lookups_per_step": n,
+                          "step": "prepare + gather + apply_unique_update (simulator.py:419-433)"},
+               "cpu_baseline": {"value": r["lookups_per_s"], "unit": "lookups/s", "cores": 1, "kind": "port",
+                                "sample": f"{r['steps']} batches of {n} ids after {args.warmup} warm-up batches; "
+                                          "numpy oracle restatement of the reference (single-threaded numpy)"},
+               "e2e": {"value": r["lookups_per_s"], "unit": "lookups/s", "h2d_bytes_per_step": 0,
+                       "d2h_bytes_per_step": 0}}
+        print(json.dumps(out), flush=True)
+        return 0
+
+    import torch
+
+    if world > 1:
+        torch.distributed.init_process_group("nccl")
+    res, samples, rank_of, cap = run_ours(args, cfg, torch, rank, world)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = run_cpu_reference(samples, rank_of, cap, cfg, args.cpu_baseline_steps, 2, time_budget_s=30)
+        res["cpu_baseline"] = {"value": r["lookups_per_s"], "unit": "lookups/s", "cores": 1, "kind": "port",
+                               "sample": f"{r['steps']} batches after 2 warm-up batches of the same trace; "
+                                         "numpy oracle port, single-threaded"}
+    if rank == 0:
+        print(json.dumps(res), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

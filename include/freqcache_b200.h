@@ -103,6 +103,12 @@ int fc_set_modes(fc_cache* h, int32_t write_back, int32_t evict_mode);
 /* CacheState.free_count after the last synchronising call. */
 int64_t fc_free_count(fc_cache* h);
 
+/* Measurement hook (no reference counterpart): with enable=1 every prepare records
+ * CUDA events around the whole call and around the host-link transfer kernel.
+ * out[0..3] (returned, then reset): sum prepare ms, sum transfer-kernel ms,
+ * calls, host-link bytes moved (4*dim*(admitted + written-back rows)). */
+int fc_profile(fc_cache* h, int32_t enable, double* out);
+
 /* ---- the cache verbs ------------------------------------------------------- */
 /* warmup (cache_manager.py:351-390): ranks 0..k-1 -> slots 0..k-1; empty cache only. */
 int fc_warmup(fc_cache* h, int64_t k, void* stream);

@@ -55,6 +55,7 @@ _SIGS = {
     "fc_attach_slow_tier": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int64]),
     "fc_set_modes": (c_int32, [c_void_p, c_int32, c_int32]),
     "fc_free_count": (c_int64, [c_void_p]),
+    "fc_profile": (c_int32, [c_void_p, c_int32, c_void_p]),
     "fc_warmup": (c_int32, [c_void_p, c_int64, c_void_p]),
     "fc_prepare": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                              c_void_p, c_void_p, c_void_p, POINTER(PrepareInfo)]),

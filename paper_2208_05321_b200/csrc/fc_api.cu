@@ -72,6 +72,8 @@ static void release(fc_cache* h) {
     if (p) cudaFree(p);
   if (h->ctr_host) cudaFreeHost(h->ctr_host);
   if (h->done) cudaEventDestroy(h->done);
+  if (h->profile)
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(h->pev[i]);
   delete h;
 }
 
@@ -351,6 +353,31 @@ int fc_prepare(fc_cache* h, const void* ids, int32_t ids_bytes, int64_t n, int64
   info->rows_to_slow = c.wb_rows;
   h->last_needed = c.needed;
   h->last_misses = c.misses;
+  if (h->profile) {
+    float a = 0.f, b = 0.f;
+    cudaEventElapsedTime(&a, h->pev[0], h->pev[3]);
+    cudaEventElapsedTime(&b, h->pev[1], h->pev[2]);
+    h->prof[0] += a;
+    h->prof[1] += b;
+    h->prof[2] += 1;
+    h->prof[3] += 4.0 * h->dim * ((double)c.misses + c.wb_rows);
+  }
+  return FC_OK;
+}
+
+int fc_profile(fc_cache* h, int32_t enable, double* out) {
+  if (!h) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  if (out)
+    for (int i = 0; i < 4; ++i) out[i] = h->prof[i];
+  if (enable && !h->profile) {
+    for (int i = 0; i < 4; ++i) FC_CUDA(cudaEventCreate(&h->pev[i]));
+  }
+  if (!enable && h->profile) {
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(h->pev[i]);
+  }
+  h->profile = enable ? 1 : 0;
+  for (int i = 0; i < 6; ++i) h->prof[i] = 0;
   return FC_OK;
 }
 

@@ -120,29 +120,61 @@ static void compact(WF wf, FIN fin, EM em, int64_t nwords, int32_t* cnt, const i
 }
 
 // ------------------------------------------------------------------ unique ids (:268-289)
+// Counts are aggregated per block in a shared-memory hash table before touching
+// global memory: a Zipf head id occurs ~8% of a batch, and per-occurrence (or
+// per-warp) global atomics on its counter serialise in one L2 slice.
+constexpr int kMarkTile = 2048;     // ids per block iteration
+constexpr int kMarkHash = 4096;     // open-addressing slots (load <= 0.5)
+
 template <typename IdT>
 __global__ void __launch_bounds__(kNT) k_mark_ids(const IdT* __restrict__ ids, int64_t n, int64_t num_ids,
                                                   uint32_t* id_bits, int32_t* aux, Counters* c) {
+  __shared__ int hk[kMarkHash];
+  __shared__ int hc[kMarkHash];
   const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
-  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
-    const int64_t i = base + lane;
-    const bool valid = i < n;
-    const long long id = valid ? (long long)ids[i] : 0;
-    const bool inr = valid && id >= 0 && id < num_ids;
-    if (valid && !inr) {
-      if (id < 0) atomicMin(&c->lo, id);
-      else atomicMax(&c->hi, id);
+  for (int e = threadIdx.x; e < kMarkHash; e += kNT) {
+    hk[e] = -1;
+    hc[e] = 0;
+  }
+  __syncthreads();
+  for (int64_t tile = blockIdx.x; tile * kMarkTile < n; tile += gridDim.x) {
+#pragma unroll
+    for (int k = 0; k < kMarkTile / kNT; ++k) {
+      const int64_t i = tile * kMarkTile + k * kNT + threadIdx.x;
+      const bool valid = i < n;
+      const long long id = valid ? (long long)ids[i] : 0;
+      const bool inr = valid && id >= 0 && id < num_ids;
+      if (valid && !inr) {
+        if (id < 0) atomicMin(&c->lo, id);
+        else atomicMax(&c->hi, id);
+      }
+      const int key = inr ? (int)id : -1;
+      const unsigned peers = __match_any_sync(FC_FULL, key);
+      if (inr && lane == __ffs(peers) - 1) {
+        unsigned h = ((unsigned)key * 2654435761u) >> 20;  // 12-bit slot
+        while (true) {
+          const int prev = atomicCAS(&hk[h], -1, key);
+          if (prev == -1 || prev == key) {
+            atomicAdd(&hc[h], __popc(peers));
+            break;
+          }
+          h = (h + 1) & (kMarkHash - 1);
+        }
+      }
     }
-    // duplicates inside a warp are aggregated before touching global memory
-    const unsigned peers = __match_any_sync(FC_FULL, inr ? (int)id : -1);
-    if (inr && lane == __ffs(peers) - 1) {
-      atomicAdd(&aux[id], __popc(peers));
-      const uint32_t m = 1u << (id & 31);
-      uint32_t* wp = &id_bits[id >> 5];
-      if (!(*wp & m)) atomicOr(wp, m);
+    __syncthreads();
+    for (int e = threadIdx.x; e < kMarkHash; e += kNT) {
+      const int key = hk[e];
+      if (key >= 0) {
+        atomicAdd(&aux[key], hc[e]);
+        const uint32_t m = 1u << (key & 31);
+        uint32_t* wp = &id_bits[key >> 5];
+        if (!(*wp & m)) atomicOr(wp, m);
+        hk[e] = -1;
+        hc[e] = 0;
+      }
     }
+    __syncthreads();
   }
 }
 
@@ -156,41 +188,53 @@ struct IdFin {
   }
 };
 
+// Ordered emission only places each id at its position; the gathers that depend
+// on it run afterwards, one thread per unique id, with no barrier in between.
 struct IdEmit {
-  static constexpr bool kVisitAll = true, kClear = true, kCount = true;
+  static constexpr bool kVisitAll = true, kClear = true, kCount = false;
   int32_t* aux;
-  const int32_t* rank_of;
-  const int32_t* rank_to_slot;
-  uint32_t* prot;
-  uint32_t* miss;
   int32_t* uids;
-  int32_t* ucnt;
-  int32_t* uranks;
-  int32_t* uslots;
   int ok;
   __device__ void init(const Counters* c) { ok = c->emitted; }
-  __device__ int* counter(Counters* c) const { return &c->misses; }
+  __device__ int* counter(Counters*) const { return nullptr; }
   __device__ __forceinline__ int operator()(int64_t id, int p) const {
-    if (!ok) {  // validation failed: undo the per-id counts, touch nothing else
-      aux[id] = 0;
-      return 0;
-    }
-    const int cnt = aux[id];
-    aux[id] = p;  // position in the unique list, read by k_inverse
-    const int r = rank_of[id];             // :283
-    const int s = rank_to_slot[r];         // :286
-    uids[p] = (int32_t)id;
-    ucnt[p] = cnt;
-    uranks[p] = r;
-    uslots[p] = s;
-    atomicOr(&prot[r >> 5], 1u << (r & 31));  // every batch rank is protected (:299)
-    if (s < 0) {                              // miss (:287)
-      atomicOr(&miss[r >> 5], 1u << (r & 31));
-      return 1;
-    }
+    if (!ok) aux[id] = 0;  // validation failed: undo the per-id counts, touch nothing else
+    else uids[p] = (int32_t)id;
     return 0;
   }
 };
+
+// per unique id: count, rank (:283), slot or miss (:286-289), protection mark (:299)
+__global__ void __launch_bounds__(kNT) k_unique_info(const int32_t* __restrict__ uids, int32_t* aux,
+                                                     const int32_t* __restrict__ rank_of,
+                                                     const int32_t* __restrict__ rank_to_slot, uint32_t* prot,
+                                                     uint32_t* miss, int32_t* __restrict__ ucnt,
+                                                     int32_t* __restrict__ uranks, int32_t* __restrict__ uslots,
+                                                     Counters* c) {
+  if (!c->emitted) return;
+  const int u = c->unique;
+  const int lane = threadIdx.x & 31;
+  int misses = 0;
+  for (int base = (blockIdx.x * kNT + threadIdx.x) & ~31; base < u; base += gridDim.x * kNT) {
+    const int p = base + lane;
+    bool m = false;
+    if (p < u) {
+      const int id = uids[p];
+      const int cnt = aux[id];
+      aux[id] = p;  // position in the unique list, read by k_inverse
+      const int r = rank_of[id];
+      const int s = rank_to_slot[r];
+      ucnt[p] = cnt;
+      uranks[p] = r;
+      uslots[p] = s;
+      atomicOr(&prot[r >> 5], 1u << (r & 31));
+      m = s < 0;
+      if (m) atomicOr(&miss[r >> 5], 1u << (r & 31));
+    }
+    misses += __popc(__ballot_sync(FC_FULL, m));
+  }
+  if (lane == 0 && misses) atomicAdd(&c->misses, misses);
+}
 
 template <typename IdT>
 __global__ void __launch_bounds__(kNT) k_inverse(const IdT* __restrict__ ids, int64_t n, const int32_t* __restrict__ aux,
@@ -231,18 +275,20 @@ struct EvictFin {
 struct EvictEmit {
   static constexpr bool kVisitAll = false, kClear = false, kCount = false;
   int32_t* evicted;
-  int32_t* vslots;
-  const int32_t* rank_to_slot;
   int total;
   __device__ void init(const Counters* c) { total = c->candidates; }
   __device__ int* counter(Counters*) const { return nullptr; }
   __device__ __forceinline__ int operator()(int64_t r, int a) const {
-    const int v = total - 1 - a;  // descending, like np.sort(top)[::-1] (:75)
-    evicted[v] = (int32_t)r;
-    vslots[v] = rank_to_slot[r];
+    evicted[total - 1 - a] = (int32_t)r;  // descending, like np.sort(top)[::-1] (:75)
     return 0;
   }
 };
+
+__global__ void k_victim_slots(const int32_t* __restrict__ evicted, const int32_t* __restrict__ rank_to_slot,
+                               int32_t* vslots, const Counters* c) {
+  if (c->err) return;
+  for (int v = blockIdx.x * kNT + threadIdx.x; v < c->needed; v += gridDim.x * kNT) vslots[v] = rank_to_slot[evicted[v]];
+}
 
 // ------------------------------------------------------------------ admission (:310-323)
 struct AdmitFin {
@@ -317,22 +363,26 @@ int launch_reset_counters(fc_cache* h, cudaStream_t st) {
 int launch_prepare(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt,
                    int32_t* uranks, int32_t* uslots, int32_t* inverse, cudaStream_t st) {
   Counters* c = h->ctr;
+  if (h->profile) cudaEventRecord(h->pev[0], st);
   k_begin<<<1, 1, 0, st>>>(c);
   const int gn = grid_for(n, kNT, kSMs * 8);
-  if (ids_bytes == 8) k_mark_ids<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->num_ids, h->id_bits, h->aux, c);
-  else k_mark_ids<int><<<gn, kNT, 0, st>>>((const int*)ids, n, h->num_ids, h->id_bits, h->aux, c);
+  const int gm = grid_for(n, kMarkTile, kSMs * 6);
+  if (ids_bytes == 8) k_mark_ids<long long><<<gm, kNT, 0, st>>>((const long long*)ids, n, h->num_ids, h->id_bits, h->aux, c);
+  else k_mark_ids<int><<<gm, kNT, 0, st>>>((const int*)ids, n, h->num_ids, h->id_bits, h->aux, c);
 
-  IdEmit ie{h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, uids, ucnt, uranks, uslots, 0};
-  compact(ArrWords{h->id_bits}, IdFin{h->capacity}, ie, h->nw_ids, h->block_cnt, nullptr, c, G_ALWAYS, st);
+  compact(ArrWords{h->id_bits}, IdFin{h->capacity}, IdEmit{h->aux, uids, 0}, h->nw_ids, h->block_cnt, nullptr, c,
+          G_ALWAYS, st);
+  const int gu = grid_for(std::min<int64_t>(n, h->capacity), kNT, kSMs * 8);
+  k_unique_info<<<gu, kNT, 0, st>>>(uids, h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, ucnt,
+                                    uranks, uslots, c);
 
   if (ids_bytes == 8) k_inverse<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->aux, inverse, c);
   else k_inverse<int><<<gn, kNT, 0, st>>>((const int*)ids, n, h->aux, inverse, c);
 
   k_plan<<<1, 1, 0, st>>>(c, h->capacity, h->evict_mode, (int64_t)h->dim * 4 <= h->buffer_bytes);
 
-  EvictEmit ee{h->evicted_ranks, h->victim_slots, h->rank_to_slot, 0};
-  compact(CandWords{h->res_bits, h->prot_bits}, EvictFin{}, ee, h->nw_ids, h->block_cnt, win_evict(c), c,
-          G_EVICT, st);
+  compact(CandWords{h->res_bits, h->prot_bits}, EvictFin{}, EvictEmit{h->evicted_ranks, 0}, h->nw_ids, h->block_cnt,
+          win_evict(c), c, G_EVICT, st);
   int rc = launch_evict_rows(h, st);
   if (rc) return rc;
 
@@ -340,11 +390,13 @@ int launch_prepare(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32
           win_admit(c), c, G_ADMIT, st);
   compact(ArrWords{h->free_bits}, FreeFin{}, RankEmit{h->target_slots}, h->nw_slots, h->block_cnt2,
           win_admit(c), c, G_ADMIT, st);
+  if (h->profile) cudaEventRecord(h->pev[1], st);
   rc = launch_transfer_rows(h, st);
   if (rc) return rc;
+  if (h->profile) cudaEventRecord(h->pev[2], st);
 
-  const int gu = grid_for(std::min<int64_t>(n, h->capacity), kNT, kSMs * 4);
   k_finish<<<gu, kNT, 0, st>>>(uids, uranks, uslots, h->aux, h->rank_to_slot, h->prot_bits, h->miss_bits, c);
+  if (h->profile) cudaEventRecord(h->pev[3], st);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }
@@ -368,9 +420,9 @@ int launch_select_evictions(fc_cache* h, int64_t needed, const int64_t* prot, in
   const int g = grid_for(nprot, kNT, kSMs * 4);
   if (nprot) k_set_prot<<<g, kNT, 0, st>>>(prot, nprot, h->num_ids, h->prot_bits, true);
   k_set_needed<<<1, 1, 0, st>>>(c, (int)needed);
-  EvictEmit ee{h->evicted_ranks, h->victim_slots, h->rank_to_slot, 0};
-  compact(CandWords{h->res_bits, h->prot_bits}, EvictFin{}, ee, h->nw_ids, h->block_cnt, win_evict(c), c,
-          G_EVICT, st);
+  compact(CandWords{h->res_bits, h->prot_bits}, EvictFin{}, EvictEmit{h->evicted_ranks, 0}, h->nw_ids, h->block_cnt,
+          win_evict(c), c, G_EVICT, st);
+  k_victim_slots<<<grid_for(needed, kNT, kSMs * 4), kNT, 0, st>>>(h->evicted_ranks, h->rank_to_slot, h->victim_slots, c);
   if (nprot) k_set_prot<<<g, kNT, 0, st>>>(prot, nprot, h->num_ids, h->prot_bits, false);
   FC_CUDA(cudaGetLastError());
   return FC_OK;

@@ -106,6 +106,11 @@ struct fc_cache {
   int32_t last_needed;
   int32_t last_misses;
   int32_t host_free;        // host mirror of free_count
+
+  // optional per-kernel timing (fc_profile): events around the host-link transfer kernel
+  int profile;
+  cudaEvent_t pev[4];
+  double prof[6];           // prepare_ms, xfer_ms, calls, host-link bytes, evict_ms, index_ms
 };
 
 namespace fc {

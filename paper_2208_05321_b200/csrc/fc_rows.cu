@@ -121,30 +121,103 @@ struct GroupIdx {
   }
 };
 
+// ------------------------------------------------------------- warp-batched row moves
+// A warp takes 32 items at once: lane i loads item i's indices (one coalesced
+// round trip for all 32), then the warp moves the 32 rows as a flat list of
+// 16-byte units, K units per lane in flight. Row r's offsets come from lane r by
+// shuffle. This hides the index->row dependent latency that a row-per-warp loop
+// pays once per row.
+struct Units {
+  int upr;  // 16-byte units per row
+  int lg;   // log2(upr) or -1
+  __device__ __forceinline__ int row(int u) const { return lg >= 0 ? (u >> lg) : (u / upr); }
+};
+
+static Units units_for(int width) {
+  Units un;
+  un.upr = width / 4;
+  un.lg = (un.upr & (un.upr - 1)) == 0 ? __builtin_ctz(un.upr) : -1;
+  return un;
+}
+
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
+
+// dst[drow_r * dstride + c] = src[srow_r * sstride + c] (* scale_r) for the warp's 32
+// rows (act_r false -> skipped). Row indices travel by shuffle as int32.
+template <int K, bool SCALE = false>
+__device__ __forceinline__ void warp_move(const float* __restrict__ sbase, int64_t sstride, int srow,
+                                          float* __restrict__ dbase, int64_t dstride, int drow, bool act,
+                                          float scale, Units un) {
+  const int lane = threadIdx.x & 31;
+  const int total = 32 * un.upr;
+  for (int u0 = 0; u0 < total; u0 += 32 * K) {
+    float4 v[K];
+    int dr[K], cc[K];
+    bool aa[K];
+    float sc[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int u = u0 + k * 32 + lane;
+      const int r = min(un.row(u), 31);
+      cc[k] = (u - r * un.upr) * 4;
+      const int sr = __shfl_sync(FC_FULL, srow, r);
+      dr[k] = __shfl_sync(FC_FULL, drow, r);
+      aa[k] = __shfl_sync(FC_FULL, (int)act, r) && u < total;
+      if (SCALE) sc[k] = __shfl_sync(FC_FULL, scale, r);
+      if (aa[k]) v[k] = ld4(sbase + (int64_t)sr * sstride + cc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (aa[k]) {
+        float4 w = v[k];
+        if (SCALE) {
+          w.x *= sc[k]; w.y *= sc[k]; w.z *= sc[k]; w.w *= sc[k];
+        }
+        st4(dbase + (int64_t)dr[k] * dstride + cc[k], w);
+      }
+  }
+}
+
+constexpr int kUnroll = 4;
+
 // ------------------------------------------------------------- eviction (:298-308, _write_back :219-231)
+// victims -> slots, dirty filter (or all, write_back="always"), rows staged in HBM,
+// slot table cleared, bitmaps updated
 template <bool VEC>
-__global__ void __launch_bounds__(kNT) k_evict_rows(RowCtx x, int G) {
+__global__ void __launch_bounds__(kNT) k_evict_rows(RowCtx x, Units ud, Units us, int G) {
   __shared__ int sm[kNT / 32 + 1];
   if (!gate_open(x.c, G_EVICT)) return;
   const int needed = x.c->needed;
-  GroupIdx g(G);
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
   int wb_count = 0;
-  for (int64_t base = g.warp * g.gpw; base < needed; base += g.nwarps * g.gpw) {
-    const int64_t v = base + g.gw;
+  for (int64_t base = warp * 32; base < needed; base += nwarps * 32) {
+    const int64_t v = base + lane;
     const bool act = v < needed;
-    int s = 0, r = 0;
+    int r = 0, s = 0;
     bool wb = false;
     if (act) {
-      s = x.vslots[v];
       r = x.evicted[v];
+      s = x.rank_to_slot[r];
       wb = x.always || x.dirty[s];
     }
-    __syncwarp();
-    if (wb) {
-      copy_row<VEC>(x.stage + v * x.D, x.fast + (int64_t)s * x.D, x.D, g.gl, G);
-      if (x.S) copy_row<VEC>(x.stage_state + v * x.S, x.fstate + (int64_t)s * x.S, x.S, g.gl, G);
+    if (VEC) {
+      warp_move<kUnroll>(x.fast, x.D, s, x.stage, x.D, (int)v, wb, 1.0f, ud);
+      if (x.S) warp_move<kUnroll>(x.fstate, x.S, s, x.stage_state, x.S, (int)v, wb, 1.0f, us);
+    } else {
+      for (int q = 0; q < 32; ++q) {  // scalar fallback: lanes stride the row's columns
+        const bool aq = __shfl_sync(FC_FULL, (int)wb, q);
+        const int sq = __shfl_sync(FC_FULL, s, q);
+        if (aq) {
+          copy_row<false>(x.stage + (base + q) * x.D, x.fast + (int64_t)sq * x.D, x.D, lane, 32);
+          if (x.S) copy_row<false>(x.stage_state + (base + q) * x.S, x.fstate + (int64_t)sq * x.S, x.S, lane, 32);
+        }
+      }
     }
-    if (act && g.gl == 0) {
+    if (act) {
       x.wb_ranks[v] = wb ? r : -1;
       x.slot_to_rank[s] = -1;
       x.rank_to_slot[r] = -1;
@@ -154,34 +227,90 @@ __global__ void __launch_bounds__(kNT) k_evict_rows(RowCtx x, int G) {
       wb_count += wb;
     }
   }
+  (void)G;
   wb_count = block_sum<kNT>(wb_count, sm);
   if (threadIdx.x == 0 && wb_count) atomicAdd(&x.c->wb_rows, wb_count);
   if (blockIdx.x == 0 && threadIdx.x == 0) x.c->free_count += needed;
 }
 
+// Two row lists moved together: per 16-byte unit a lane issues both loads before
+// both stores, so every warp keeps one host read and one host write in flight.
+template <int K>
+__device__ __forceinline__ void warp_move2(const float* __restrict__ s1, int64_t ss1, int sr1, float* __restrict__ d1,
+                                           int64_t ds1, int dr1, bool a1, const float* __restrict__ s2, int64_t ss2,
+                                           int sr2, float* __restrict__ d2, int64_t ds2, int dr2, bool a2, Units un) {
+  const int lane = threadIdx.x & 31;
+  const int total = 32 * un.upr;
+  for (int u0 = 0; u0 < total; u0 += 32 * K) {
+    float4 v1[K], v2[K];
+    int e1[K], e2[K], cc[K];
+    bool b1[K], b2[K];
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int u = u0 + k * 32 + lane;
+      const int r = min(un.row(u), 31);
+      cc[k] = (u - r * un.upr) * 4;
+      const bool in = u < total;
+      const int x1 = __shfl_sync(FC_FULL, sr1, r), x2 = __shfl_sync(FC_FULL, sr2, r);
+      e1[k] = __shfl_sync(FC_FULL, dr1, r);
+      e2[k] = __shfl_sync(FC_FULL, dr2, r);
+      b1[k] = __shfl_sync(FC_FULL, (int)a1, r) && in;
+      b2[k] = __shfl_sync(FC_FULL, (int)a2, r) && in;
+      if (b1[k]) v1[k] = ld4(s1 + (int64_t)x1 * ss1 + cc[k]);
+      if (b2[k]) v2[k] = ld4(s2 + (int64_t)x2 * ss2 + cc[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (b1[k]) st4(d1 + (int64_t)e1[k] * ds1 + cc[k], v1[k]);
+      if (b2[k]) st4(d2 + (int64_t)e2[k] * ds2 + cc[k], v2[k]);
+    }
+  }
+}
+
 // ------------------------------------------------------------- write-back + admission rows (:304,319-323)
+// Item j pairs the j-th staged victim (HBM -> pinned slow tier, posted writes) with
+// the j-th admitted rank (slow tier -> its target slot). Both lists are rank-sorted
+// (victims descending, admissions ascending): sorted host addresses sustain ~75 GB/s
+// both ways on PCIe Gen5 where random ones fall to ~47 (tools/zerocopy_bench.cu).
 template <bool VEC>
-__global__ void __launch_bounds__(kNT) k_transfer_rows(RowCtx x, int G) {
+__global__ void __launch_bounds__(kNT, 4) k_transfer_rows(RowCtx x, Units ud, Units us) {
   if (!gate_open(x.c, G_OK)) return;
   const int needed = x.c->needed, m = x.c->misses;
   const int items = max(needed, m);
-  GroupIdx g(G);
-  for (int64_t base = g.warp * g.gpw; base < items; base += g.nwarps * g.gpw) {
-    const int64_t j = base + g.gw;
-    int r1 = -1, r2 = 0, s2 = 0;
-    if (j < needed) r1 = x.wb_ranks[j];
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  for (int64_t base = warp * 32; base < items; base += nwarps * 32) {
+    const int64_t j = base + lane;
+    const int r1 = j < needed ? x.wb_ranks[j] : -1;
     const bool a1 = r1 >= 0;
     const bool a2 = j < m;
+    int r2 = 0, s2 = 0;
     if (a2) {
       r2 = x.admitted[j];
       s2 = x.target[j];
     }
-    copy_two_rows<VEC>(x.slow + (int64_t)r1 * x.ld, x.stage + j * x.D, a1, x.fast + (int64_t)s2 * x.D,
-                       x.slow + (int64_t)r2 * x.ld, a2, x.D, g.gl, G);
-    if (x.S)
-      copy_two_rows<VEC>(x.sstate + (int64_t)r1 * x.sld, x.stage_state + j * x.S, a1, x.fstate + (int64_t)s2 * x.S,
-                         x.sstate + (int64_t)r2 * x.sld, a2, x.S, g.gl, G);
-    if (a2 && g.gl == 0) {
+    if (VEC) {
+      warp_move2<1>(x.stage, x.D, (int)j, x.slow, x.ld, r1, a1, x.slow, x.ld, r2, x.fast, x.D, s2, a2, ud);
+      if (x.S)
+        warp_move2<1>(x.stage_state, x.S, (int)j, x.sstate, x.sld, r1, a1, x.sstate, x.sld, r2, x.fstate, x.S, s2, a2,
+                      us);
+    } else {
+      for (int q = 0; q < 32; ++q) {
+        const int rq1 = __shfl_sync(FC_FULL, r1, q);
+        const bool aq2 = __shfl_sync(FC_FULL, (int)a2, q);
+        const int rq2 = __shfl_sync(FC_FULL, r2, q), sq2 = __shfl_sync(FC_FULL, s2, q);
+        if (rq1 >= 0) {
+          copy_row<false>(x.slow + (int64_t)rq1 * x.ld, x.stage + (base + q) * x.D, x.D, lane, 32);
+          if (x.S) copy_row<false>(x.sstate + (int64_t)rq1 * x.sld, x.stage_state + (base + q) * x.S, x.S, lane, 32);
+        }
+        if (aq2) {
+          copy_row<false>(x.fast + (int64_t)sq2 * x.D, x.slow + (int64_t)rq2 * x.ld, x.D, lane, 32);
+          if (x.S) copy_row<false>(x.fstate + (int64_t)sq2 * x.S, x.sstate + (int64_t)rq2 * x.sld, x.S, lane, 32);
+        }
+      }
+    }
+    if (a2) {
       x.slot_to_rank[s2] = r2;
       x.rank_to_slot[r2] = s2;
       x.dirty[s2] = 0;
@@ -197,9 +326,9 @@ static int rows_grid() { return kSMs * 8; }
 int launch_evict_rows(fc_cache* h, cudaStream_t st) {
   RowCtx x = row_ctx(h);
   const bool v = vec_ok(h);
-  const int G = row_group(std::max(h->dim, h->sw), v);
-  if (v) k_evict_rows<true><<<rows_grid(), kNT, 0, st>>>(x, G);
-  else k_evict_rows<false><<<rows_grid(), kNT, 0, st>>>(x, G);
+  const Units ud = units_for(h->dim), us = units_for(h->sw ? h->sw : 4);
+  if (v) k_evict_rows<true><<<rows_grid(), kNT, 0, st>>>(x, ud, us, 32);
+  else k_evict_rows<false><<<rows_grid(), kNT, 0, st>>>(x, ud, us, 32);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }
@@ -207,9 +336,9 @@ int launch_evict_rows(fc_cache* h, cudaStream_t st) {
 int launch_transfer_rows(fc_cache* h, cudaStream_t st) {
   RowCtx x = row_ctx(h);
   const bool v = vec_ok(h);
-  const int G = row_group(std::max(h->dim, h->sw), v);
-  if (v) k_transfer_rows<true><<<rows_grid(), kNT, 0, st>>>(x, G);
-  else k_transfer_rows<false><<<rows_grid(), kNT, 0, st>>>(x, G);
+  const Units ud = units_for(h->dim), us = units_for(h->sw ? h->sw : 4);
+  if (v) k_transfer_rows<true><<<kSMs * 4, kNT, 0, st>>>(x, ud, us);
+  else k_transfer_rows<false><<<kSMs * 4, kNT, 0, st>>>(x, ud, us);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }
@@ -309,11 +438,38 @@ __global__ void __launch_bounds__(kNT) k_pool(const float* __restrict__ fast, in
   }
 }
 
+// bag size 1 (offsets == NULL: gather, or one id per (sample, feature) as in the
+// Criteo/Avazu shapes): out[j] = w_j * fast[uslots[inv[j]]], warp-batched
+__global__ void __launch_bounds__(kNT) k_pool1(const float* __restrict__ fast, int D, const int32_t* __restrict__ uslots,
+                                               const int32_t* __restrict__ inv, int64_t n,
+                                               const float* __restrict__ psw, float* __restrict__ out, Units un) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    const int64_t j = base + lane;
+    const bool act = j < n;
+    int s = 0;
+    float w = 1.0f;
+    if (act) {
+      s = uslots[inv[j]];
+      if (psw) w = psw[j];
+    }
+    if (psw) warp_move<kUnroll, true>(fast, D, s, out, D, (int)j, act, w, un);
+    else warp_move<kUnroll, false>(fast, D, s, out, D, (int)j, act, 1.0f, un);
+  }
+}
+
 int launch_pool(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const void* offsets, int off_bytes,
                 int64_t nbags, int include_last, const float* psw, int mode, float* out, cudaStream_t st) {
   if (nbags <= 0) return FC_OK;
   const int D = h->dim;
   const bool v = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  if (v && offsets == nullptr) {  // bag size 1: one row per bag
+    k_pool1<<<grid_for(nbags, kNT, kSMs * 8), kNT, 0, st>>>(h->fast, D, uslots, inv, nbags, psw, out, units_for(D));
+    FC_CUDA(cudaGetLastError());
+    return FC_OK;
+  }
   const int G = row_group(D, v);
   const int grid = grid_for(nbags * G, kNT, kSMs * 16);
 #define FC_POOL(VV, T) \
@@ -384,30 +540,67 @@ template <bool VEC>
 __global__ void __launch_bounds__(kNT) k_synthetic(float* fast, int D, const int32_t* __restrict__ uids,
                                                    const int32_t* __restrict__ ucnt, const int32_t* __restrict__ uslots,
                                                    int64_t u, uint64_t salt, const float* __restrict__ colw,
-                                                   uint8_t* dirty, int G) {
-  GroupIdx g(G);
-  for (int64_t base = g.warp * g.gpw; base < u; base += g.nwarps * g.gpw) {
-    const int64_t p = base + g.gw;
-    if (p >= u) continue;
-    // g = (hash - 0.5) * count, all fp32 with round-to-nearest like numpy
-    const float gs = __fmul_rn(__fsub_rn(hash_unit((uint64_t)uids[p], salt), 0.5f), __int2float_rn(ucnt[p]));
-    const int64_t s = uslots[p];
-    float* row = fast + s * D;
+                                                   uint8_t* dirty, int G, Units un) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  for (int64_t base = warp * 32; base < u; base += nwarps * 32) {
+    const int64_t p = base + lane;
+    const bool act = p < u;
+    int s = 0;
+    float gs = 0.f;
+    if (act) {
+      s = uslots[p];
+      // g = (hash - 0.5) * count, all fp32 with round-to-nearest like numpy (simulator.py:258-260)
+      gs = __fmul_rn(__fsub_rn(hash_unit((uint64_t)uids[p], salt), 0.5f), __int2float_rn(ucnt[p]));
+    }
     if (VEC) {
-      for (int c = g.gl * 4; c < D; c += G * 4) {
-        float4 w = *reinterpret_cast<float4*>(row + c);
-        const float4 cw = *reinterpret_cast<const float4*>(colw + c);
-        w.x = __fadd_rn(w.x, __fmul_rn(gs, cw.x));
-        w.y = __fadd_rn(w.y, __fmul_rn(gs, cw.y));
-        w.z = __fadd_rn(w.z, __fmul_rn(gs, cw.z));
-        w.w = __fadd_rn(w.w, __fmul_rn(gs, cw.w));
-        *reinterpret_cast<float4*>(row + c) = w;
+      const int total = 32 * un.upr;
+      for (int u0 = 0; u0 < total; u0 += 32 * kUnroll) {
+        float4 v[kUnroll], cw[kUnroll];
+        float* rp[kUnroll];
+        float gk[kUnroll];
+        bool aa[kUnroll];
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k) {
+          const int q = u0 + k * 32 + lane;
+          const int r = min(un.row(q), 31);
+          const int c = (q - r * un.upr) * 4;
+          const int sr = __shfl_sync(FC_FULL, s, r);
+          gk[k] = __shfl_sync(FC_FULL, gs, r);
+          aa[k] = __shfl_sync(FC_FULL, (int)act, r) && q < total;
+          rp[k] = fast + (int64_t)sr * D + c;
+          if (aa[k]) {
+            v[k] = ld4(rp[k]);
+            cw[k] = ldg4(colw + c);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kUnroll; ++k)
+          if (aa[k]) {
+            float4 w = v[k];
+            w.x = __fadd_rn(w.x, __fmul_rn(gk[k], cw[k].x));
+            w.y = __fadd_rn(w.y, __fmul_rn(gk[k], cw[k].y));
+            w.z = __fadd_rn(w.z, __fmul_rn(gk[k], cw[k].z));
+            w.w = __fadd_rn(w.w, __fmul_rn(gk[k], cw[k].w));
+            st4(rp[k], w);
+          }
       }
     } else {
-      for (int c = g.gl; c < D; c += G) row[c] = __fadd_rn(row[c], __fmul_rn(gs, colw[c]));
+      for (int q = 0; q < 32; ++q) {
+        const bool aq = __shfl_sync(FC_FULL, (int)act, q);
+        const int sq = __shfl_sync(FC_FULL, s, q);
+        const float gq = __shfl_sync(FC_FULL, gs, q);
+        if (aq)
+          for (int c = lane; c < D; c += 32) {
+            float* e = fast + (int64_t)sq * D + c;
+            *e = __fadd_rn(*e, __fmul_rn(gq, colw[c]));
+          }
+      }
     }
-    if (g.gl == 0) dirty[s] = 1;
+    if (act) dirty[s] = 1;
   }
+  (void)G;
 }
 
 int launch_synthetic(fc_cache* h, const int32_t* uids, const int32_t* ucnt, const int32_t* uslots, int64_t u,
@@ -416,8 +609,14 @@ int launch_synthetic(fc_cache* h, const int32_t* uids, const int32_t* ucnt, cons
   const bool v = (h->dim % 4 == 0) && ((reinterpret_cast<uintptr_t>(colw) & 15) == 0);
   const int G = row_group(h->dim, v);
   const int grid = grid_for(u * G, kNT, kSMs * 16);
-  if (v) k_synthetic<true><<<grid, kNT, 0, st>>>(h->fast, h->dim, uids, ucnt, uslots, u, salt, colw, h->dirty, G);
-  else k_synthetic<false><<<grid, kNT, 0, st>>>(h->fast, h->dim, uids, ucnt, uslots, u, salt, colw, h->dirty, G);
+  const int grid_w = grid_for(u, kNT, kSMs * 8);
+  if (v)
+    k_synthetic<true><<<grid_w, kNT, 0, st>>>(h->fast, h->dim, uids, ucnt, uslots, u, salt, colw, h->dirty, G,
+                                              units_for(h->dim));
+  else
+    k_synthetic<false><<<grid_w, kNT, 0, st>>>(h->fast, h->dim, uids, ucnt, uslots, u, salt, colw, h->dirty, G,
+                                               units_for(4));
+  (void)grid;
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }

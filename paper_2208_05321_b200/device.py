@@ -91,6 +91,12 @@ class DeviceCache:
     def free_count(self) -> int:
         return int(self.lib.fc_free_count(self.h))
 
+    def profile(self, enable: bool) -> dict:
+        """Toggle per-kernel CUDA-event timing; returns (and resets) the totals so far."""
+        out = (ctypes.c_double * 4)()
+        check(self.lib.fc_profile(self.h, int(bool(enable)), out))
+        return {"prepare_ms": out[0], "transfer_ms": out[1], "calls": int(out[2]), "host_link_bytes": out[3]}
+
     def to_device_ids(self, ids):
         """Accept numpy / list / torch ids; return a contiguous CUDA int64/int32 tensor."""
         torch = self.torch
