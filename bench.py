@@ -4,15 +4,19 @@
 Workload (N=1): BASELINE configs[1], the Criteo-Kaggle shape — 33,762,577 rows x
 dim 128 fp32, frequency-reordered cache at 1.5% (506,438 slots), Zipf(1.05) ids
 from the reference generator's stream, batch 16384 x 26 (425,984 lookups/step).
-One step = the reference simulator's per-batch work (simulator.py:416-455):
-prepare_cache -> lookup (pooled EmbeddingBag forward, sum, bag size 1) -> the
-deterministic row update, all through libfreqcache_b200 kernels.
+One step (--step train, default) = the cached EmbeddingBag's training step:
+prepare_cache (cache_manager.py:234-348) -> pooled forward (sum, one id per
+(sample, feature)) -> fused backward + sparse SGD on the cached rows, all in
+libfreqcache_b200 kernels. --step sim runs the reference simulator's per-batch
+work instead (prepare -> lookup -> deterministic row update, simulator.py:416-455).
+At N>1 GPUs the table is row-sharded (id % N) with NCCL id/row all-to-alls and
+every rank processes its own 16384 x 26 ids per step (weak scaling).
 
-    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config small]
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config small] [--step sim]
 
-`--impl reference` times the reference CPU path (the oracle port in oracle/, the
-reference itself cannot run on the GPU box) on the same workload.
-Prints ONE JSON line on rank 0.
+`--impl reference` times the reference CPU path (the oracle port in oracle/; the
+Python reference itself cannot run on the GPU box) on the same workload and step:
+prepare + gather + scatter_update(-lr * grad). Prints ONE JSON line on rank 0.
 """
 
 from __future__ import annotations
@@ -40,7 +44,10 @@ CONFIGS = {
 SEED = 1
 UPDATES_SEED = 7
 METRIC = "cached-embedding lookups/sec"
-KERNELS_PER_STEP = 20 + 1 + 1  # prepare sequence + pooled forward + fused update
+KERNELS_PER_STEP = 20 + 1 + 1  # sim step: prepare sequence + pooled forward + fused update
+# train step: prepare (20) + pooled forward (1) + backward: 2 radix passes x (hist + 3-kernel scan + scatter),
+# segmented stream, carry fix-up, optimizer apply
+KERNELS_PER_TRAIN_STEP = 20 + 1 + (2 * 5 + 3)
 
 
 def log(*a):
@@ -48,7 +55,7 @@ def log(*a):
 
 
 # ----------------------------------------------------------------------------- workload
-def make_workload(cfg, n_batches, device=None):
+def make_workload(cfg, n_batches, device=None, keep_counts=False):
     from paper_2208_05321_b200 import workload
     from paper_2208_05321_b200.store import fast_capacity
 
@@ -63,6 +70,7 @@ def make_workload(cfg, n_batches, device=None):
         ids = torch.from_numpy(tr.samples.reshape(-1)).to(device).long()
         counts = torch.bincount(ids, minlength=cfg["num_ids"])
         id_of = torch.sort(-counts, stable=True).indices.cpu().numpy().astype(np.int64)
+        counts_np = counts.cpu().numpy() if keep_counts else None
         del ids, counts
     else:
         counts = np.bincount(tr.samples.reshape(-1), minlength=cfg["num_ids"])
@@ -70,7 +78,8 @@ def make_workload(cfg, n_batches, device=None):
     rank_of = np.empty_like(id_of)
     rank_of[id_of] = np.arange(id_of.size, dtype=np.int64)
     log(f"[bench] trace {tr.samples.shape} in {t1 - t0:.1f}s, reorder {time.perf_counter() - t1:.1f}s")
-    return tr.samples, rank_of, id_of, fast_capacity(cfg["num_ids"], cfg["ratio"])
+    samples = (tr.samples, counts_np) if (keep_counts and device is not None) else tr.samples
+    return samples, rank_of, id_of, fast_capacity(cfg["num_ids"], cfg["ratio"])
 
 
 # ----------------------------------------------------------------------------- measurement helpers
@@ -165,10 +174,21 @@ def hbm_peak():
 
 
 # ----------------------------------------------------------------------------- CPU reference arm
-def run_cpu_reference(samples, rank_of, cap, cfg, steps, warmup, time_budget_s=None):
-    """The reference's per-batch loop on host cores through the numpy oracle port:
-    prepare + gather + apply_unique_update (simulator.py:419-433). Slow tier is a
-    lazily materialised buffer (only rows that move are touched)."""
+def make_grad(n, D, device=None):
+    """The fixed upstream gradient of the pooled output used by every training step."""
+    g = np.random.default_rng(SEED + 1).standard_normal((n, D), dtype=np.float32) * np.float32(0.01)
+    if device is None:
+        return g
+    import torch
+
+    return torch.from_numpy(g).to(device)
+
+
+def run_cpu_reference(samples, rank_of, cap, cfg, steps, warmup, step_kind, batch_mult=1, time_budget_s=None):
+    """The reference's per-batch loop on host cores through the numpy oracle port.
+    train: prepare + gather (bag-size-1 pooled forward) + scatter_update(-lr * grad)
+    (cache_manager.py:234-348, 418-438); sim: prepare + gather + apply_unique_update
+    (simulator.py:419-433). The slow tier is a lazily materialised buffer."""
     import oracle
 
     D = cfg["dim"]
@@ -176,7 +196,9 @@ def run_cpu_reference(samples, rank_of, cap, cfg, steps, warmup, time_budget_s=N
     orc = oracle.OracleCache(rank_of, slow, cap)
     orc.warmup(cap)
     colw = oracle.column_weights(D, UPDATES_SEED)
-    B = cfg["batch"]
+    B = cfg["batch"] * batch_mult
+    n = B * cfg["features"]
+    deltas = -LR * make_grad(n, D)
     times = []
     t_start = time.perf_counter()
     for s in range(warmup + steps):
@@ -184,67 +206,140 @@ def run_cpu_reference(samples, rank_of, cap, cfg, steps, warmup, time_budget_s=N
         t = time.perf_counter()
         p = orc.prepare(ids, s)
         _ = orc.gather(p)
-        g = oracle.row_scalars(p["unique_ids"], p["unique_counts"], s, UPDATES_SEED)
-        orc.apply_unique_update(p, g[:, None] * colw[None, :])
+        if step_kind == "train":
+            orc.scatter_update(p, deltas[:ids.size])
+        else:
+            g = oracle.row_scalars(p["unique_ids"], p["unique_counts"], s, UPDATES_SEED)
+            orc.apply_unique_update(p, g[:, None] * colw[None, :])
         dt = time.perf_counter() - t
         if s >= warmup:
             times.append(dt)
         if time_budget_s and time.perf_counter() - t_start > time_budget_s and len(times) >= 3:
             break
-    n = B * cfg["features"]
     return {"step_s": float(np.mean(times)), "steps": len(times), "lookups_per_s": n / float(np.mean(times))}
 
 
 # ----------------------------------------------------------------------------- GPU arm
+LR = 0.05
+
+
+def fill_pinned(torch, rows, dev, seed):
+    """Seeded uniform(+-0.5/D) rows generated on the GPU and written into pinned host memory."""
+    t = torch.from_numpy(rows)
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed)
+    D = rows.shape[1]
+    chunk = 1 << 20
+    for lo in range(0, rows.shape[0], chunk):
+        hi = min(lo + chunk, rows.shape[0])
+        t[lo:hi].copy_((torch.rand((hi - lo, D), generator=g, device=dev) - 0.5) * (1.0 / D))
+    torch.cuda.synchronize(dev)
+
+
+def rooflines(prof, pool_ms, N, D, links):
+    hbm, hbm_src = hbm_peak()
+    xfer_ms = prof["transfer_ms"] / max(prof["calls"], 1)
+    xfer_bytes = prof["host_link_bytes"] / max(prof["calls"], 1)
+    r_xfer = {"kernel": "k_transfer_rows", "bound": "host_link",
+              "achieved": xfer_bytes / max(xfer_ms * 1e-3, 1e-12) / 1e9, "peak": links["bidir_GBps"], "unit": "GB/s",
+              "traffic": None, "algorithmic_bytes_per_launch": xfer_bytes, "launch_ms": xfer_ms,
+              "peak_source": "pinned cudaMemcpy H2D+D2H concurrently, measured in this run"}
+    r_xfer["frac"] = r_xfer["achieved"] / r_xfer["peak"]
+    out = [r_xfer]
+    if pool_ms:
+        pool_bytes = N * (4 * D + 8) + N * 4 * D  # per occurrence: inverse + slot + row read; per bag: row write
+        pool_avg = float(np.mean(pool_ms))
+        r_pool = {"kernel": "k_pool1", "bound": "hbm", "achieved": pool_bytes / (pool_avg * 1e-3) / 1e9, "peak": hbm,
+                  "unit": "GB/s", "traffic": None, "algorithmic_bytes_per_launch": pool_bytes, "launch_ms": pool_avg,
+                  "peak_source": hbm_src}
+        r_pool["frac"] = r_pool["achieved"] / r_pool["peak"]
+        out.append(r_pool)
+    out.sort(key=lambda r: -r["launch_ms"])
+    return out
+
+
 def run_ours(args, cfg, torch, rank, world):
     import paper_2208_05321_b200 as fc
+    from paper_2208_05321_b200.embedding import CachedEmbeddingBag
 
     dev = torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0)))
     torch.cuda.set_device(dev)
     W, K = args.warmup, args.steps
-    n_batches = max(args.trace_batches, W + 2 * K)
-    samples, rank_of, id_of, cap = make_workload(cfg, n_batches, device=dev)
     D, B, F = cfg["dim"], cfg["batch"], cfg["features"]
     N = B * F
+    n_batches = max(args.trace_batches // world, W + 2 * K)
+    # global batch = world x B samples; this rank's slice is rows [rank*B, (rank+1)*B) of each global batch
+    sharded = world > 1 or args.sharded
+    samples, rank_of, id_of, cap = make_workload(cfg, n_batches * world, device=dev, keep_counts=sharded)
+    counts = None
+    if sharded:
+        samples, counts = samples
     links = host_link_peaks(torch, dev)
-    hbm, hbm_src = hbm_peak()
+    gout = make_grad(N, D, dev)
+
+    def local_batch(s):
+        lo = (s * world + rank) * B
+        return lo, lo + B
 
     t0 = time.perf_counter()
-    slow = fc.SlowTierStore.empty_pinned(cfg["num_ids"], D)
-    rows_t = torch.from_numpy(slow.rows)
-    g = torch.Generator(device=dev)
-    g.manual_seed(SEED)
-    chunk = 1 << 20
-    for lo in range(0, cfg["num_ids"], chunk):  # seeded uniform(+-0.5/D) rows, generated on device
-        hi = min(lo + chunk, cfg["num_ids"])
-        v = (torch.rand((hi - lo, D), generator=g, device=dev) - 0.5) * (1.0 / D)
-        rows_t[lo:hi].copy_(v)
-    torch.cuda.synchronize(dev)
-    log(f"[bench] slow tier {slow.rows.nbytes / 2**30:.1f} GiB pinned+filled in {time.perf_counter() - t0:.1f}s")
+    if not sharded:
+        rows = fc.store.pinned_empty((cfg["num_ids"], D))
+        fill_pinned(torch, rows, dev, SEED)
+        mod = CachedEmbeddingBag(cfg["num_ids"], D, cfg["ratio"], mode="sum", idx_map=fc.IdxMap(rank_of, id_of),
+                                 optimizer="sgd", lr=LR, slow_rows=rows, warmup=True)
+        dcs = [mod.cache]
+        shard = None
+    else:
+        from paper_2208_05321_b200.distributed import CudaShard, RowShardedEmbedding, shard_rows_for_rank
 
-    st = fc.CacheStack(fc.IdxMap(rank_of, id_of), slow, fc.FastTierStore(np.zeros((cap, D), np.float32)),
-                       fc.Transmitter())
-    dc = st.device
-    st.warmup(cap)
-    colw = fc.update_column_weights(D, UPDATES_SEED)
-    ids_dev = torch.from_numpy(samples).to(dev)  # int32 [n_batches*B, F], resident in HBM
-    out = torch.empty((N, D), dtype=torch.float32, device=dev)
-    stats = []
+        idx = shard_rows_for_rank(counts, rank, world)
+        rows = fc.store.pinned_empty((idx.num_ids, D))
+        fill_pinned(torch, rows, dev, SEED + rank)
+        shard = CudaShard(idx.num_ids, D, fc.fast_capacity(idx.num_ids, cfg["ratio"]), rows, idx, optimizer="sgd",
+                          lr=LR, device=dev)
+        mod = RowShardedEmbedding(shard, world, rank, mode="sum", device=dev)
+        dcs = [shard.cache]
+        cap = shard.cache.capacity
+    dc = dcs[0]
+    log(f"[bench] rank {rank}: slow tier {rows.nbytes / 2**30:.1f} GiB pinned+filled, cache ready in "
+        f"{time.perf_counter() - t0:.1f}s")
+    ids_dev = torch.from_numpy(samples).to(dev)
+    out_buf = torch.empty((N, D), dtype=torch.float32, device=dev)
+    colw = torch.from_numpy(fc.update_column_weights(D, UPDATES_SEED)).to(dev)
+    stream = torch.cuda.current_stream(dev)
+    stats, pool_ms, bwd_ms = [], [], []
 
-    def step(s, ids):
-        prep = st.prepare(ids, s)
-        dc.pooled(prep.d_unique_slots, prep.d_inverse, N, out=out)
-        st.apply_synthetic_update(prep, s, UPDATES_SEED, colw)
-        return prep
+    def step(s, timed):
+        lo, hi = local_batch(s)
+        ids = ids_dev[lo:hi].reshape(-1)
+        if sharded:  # row-sharded training step: id all-to-all, owner caches, row all-to-all
+            out = mod(ids)
+            out.backward(gout)
+            stats.append((0, 0, 0, 0, 0))
+            return
+        info, uids, ucnt, uranks, uslots, inverse, _ = dc.prepare(ids, s)
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(3)] if timed else None
+        if timed:
+            e[0].record(stream)
+        dc.pooled(uslots, inverse, N, out=out_buf)
+        if timed:
+            e[1].record(stream)
+        if args.step == "train":
+            dc.backward_update(uslots, inverse, ucnt, None, N, False, None, "sum", gout, "sgd", LR, 0.0)
+        else:
+            dc.synthetic(uids, ucnt, uslots, fc.updates.batch_salt(s, UPDATES_SEED), colw)
+        if timed:
+            e[2].record(stream)
+            pool_ms.append(e)
+        stats.append((info.unique, info.hits, info.misses, info.evictions, info.rows_to_slow))
 
     for s in range(W):
-        step(s, ids_dev[s * B:(s + 1) * B].reshape(-1))
+        step(s, False)
     torch.cuda.synchronize(dev)
+    stats.clear()
 
     # ---- timed region: inputs resident in HBM --------------------------------
-    stream = torch.cuda.current_stream(dev)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
-    pool_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(K)]
     dc.profile(True)
     if world > 1:
         torch.distributed.barrier()
@@ -252,15 +347,8 @@ def run_ours(args, cfg, torch, rank, world):
     with ClockSampler(dev.index) as clk:
         ev[0].record(stream)
         for k in range(K):
-            s = W + k
-            prep = st.prepare(ids_dev[s * B:(s + 1) * B].reshape(-1), s)
-            pool_ev[k][0].record(stream)
-            dc.pooled(prep.d_unique_slots, prep.d_inverse, N, out=out)
-            pool_ev[k][1].record(stream)
-            st.apply_synthetic_update(prep, s, UPDATES_SEED, colw)
+            step(W + k, True)
             ev[k + 1].record(stream)
-            rep_slow = sum(r.rows for r in prep.transfer_reports if r.direction == "to_slow")
-            stats.append((prep.num_unique, prep.hits, prep.misses, prep.evictions, rep_slow))
         torch.cuda.synchronize(dev)
     if world > 1:
         torch.distributed.barrier()
@@ -271,63 +359,64 @@ def run_ours(args, cfg, torch, rank, world):
         t = torch.tensor([total_ms], device=dev)
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         total_ms = float(t.item())
-    pool_ms = [a.elapsed_time(b) for a, b in pool_ev]
+    p_ms = [e[0].elapsed_time(e[1]) for e in pool_ms]
+    b_ms = [e[1].elapsed_time(e[2]) for e in pool_ms]
 
-    # ---- e2e: the public API from pinned host ids, result read back ----------
+    # ---- e2e: the public API (module forward+backward) from pinned host ids ----
     ids_host = torch.from_numpy(samples).pin_memory()
+    if world > 1:
+        torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     t = time.perf_counter()
+    hits_read = 0
     for k in range(K):
-        s = W + K + k
-        prep = st.prepare(ids_host[s * B:(s + 1) * B].reshape(-1), s)  # H2D inside
-        pooled = st.gather(prep)
-        st.apply_synthetic_update(prep, s, UPDATES_SEED, colw)
-        _ = (prep.hits, prep.misses)  # the step's result, already read back by prepare
+        lo, hi = local_batch(W + K + k)
+        out = mod(ids_host[lo:hi].reshape(-1))  # H2D of the ids inside forward
+        out.backward(gout)  # upstream gradient of the pooled output -> fused SGD on the cached rows
+        if not sharded:
+            hits_read += mod.last_info.hits  # the step's result (prepare counters, read back D2H)
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t
-    del pooled
+    if world > 1:
+        tt = torch.tensor([e2e_s], device=dev)
+        torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
+        e2e_s = float(tt.item())
 
     st_arr = np.array(stats, dtype=np.float64)
     uniq, hits, misses, evict, wb = st_arr.mean(axis=0)
-    # ---- rooflines -----------------------------------------------------------
-    xfer_ms = prof["transfer_ms"] / max(prof["calls"], 1)
-    xfer_bytes = prof["host_link_bytes"] / max(prof["calls"], 1)
-    pool_bytes = N * (4 * D + 8) + N * 4 * D  # per occurrence: inverse+slot idx+row read; per bag: row write
-    pool_avg = float(np.mean(pool_ms))
-    r_xfer = {"kernel": "k_transfer_rows", "bound": "host_link", "achieved": xfer_bytes / (xfer_ms * 1e-3) / 1e9,
-              "peak": links["bidir_GBps"], "unit": "GB/s", "traffic": None,
-              "algorithmic_bytes_per_launch": xfer_bytes, "launch_ms": xfer_ms,
-              "peak_source": "pinned cudaMemcpy H2D+D2H concurrently, measured in this run"}
-    r_xfer["frac"] = r_xfer["achieved"] / r_xfer["peak"]
-    r_pool = {"kernel": "k_pool", "bound": "hbm", "achieved": pool_bytes / (pool_avg * 1e-3) / 1e9, "peak": hbm,
-              "unit": "GB/s", "traffic": None, "algorithmic_bytes_per_launch": pool_bytes, "launch_ms": pool_avg,
-              "peak_source": hbm_src}
-    r_pool["frac"] = r_pool["achieved"] / r_pool["peak"]
-    dominant, other = (r_xfer, r_pool) if xfer_ms >= pool_avg else (r_pool, r_xfer)
-
+    rl = rooflines(prof, p_ms, N, D, links)
+    lookups = N * world  # every rank processes its own B x F ids per step
     res = {
-        "metric": METRIC, "value": N * K / (total_ms * 1e-3), "unit": "lookups/s", "n_gpus": world, "steps": K,
-        "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp32 rows, int32 ids", "data": "synthetic: reference gen_zipf stream (seed 1), seeded rows",
+        "metric": METRIC, "value": lookups * K / (total_ms * 1e-3), "unit": "lookups/s", "n_gpus": world,
+        "steps": K, "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "fp32 rows, int32 ids",
+        "data": "synthetic: reference gen_zipf stream (seed 1), seeded rows",
         "config": {"workload": args.config, "num_rows": cfg["num_ids"], "dim": D, "cache_ratio": cfg["ratio"],
-                   "capacity": cap, "zipf_alpha": cfg["alpha"], "batch": B, "features": F, "lookups_per_step": N,
-                   "pooling": "sum, bag size 1", "step": "prepare + pooled forward + row update",
+                   "capacity_per_gpu": cap, "zipf_alpha": cfg["alpha"], "batch_per_gpu": B, "features": F,
+                   "lookups_per_step": lookups, "pooling": "sum, bag size 1",
+                   "step": ("forward (prepare + pooled gather) + fused backward/SGD" if args.step == "train"
+                            else "prepare + pooled forward + simulator row update"),
                    "write_back": "dirty_only", "evict_mode": "occupancy_aware", "engine": "zero-copy",
                    "l2": "inputs larger than L2 (fast tier %d MB, id/rank maps %d MB, new batch every step)"
-                         % (cap * D * 4 >> 20, cfg["num_ids"] * 12 >> 20),
-                   "parallelism": "single" if world == 1 else f"rowwise{world}"},
+                         % (cap * D * 4 >> 20, cfg["num_ids"] * 12 // world >> 20),
+                   "parallelism": "single" if not sharded else f"rowwise{world} (id/row all-to-all over NCCL)"},
         "step_latency_ms": {"p50": float(np.percentile(step_ms, 50)), "p99": float(np.percentile(step_ms, 99)),
-                            "prepare_avg": prof["prepare_ms"] / max(prof["calls"], 1), "pool_avg": pool_avg},
-        "hit_ratio": hits / uniq, "unique_per_step": uniq, "misses_per_step": misses,
-        "evictions_per_step": evict, "writeback_rows_per_step": wb,
-        "e2e": {"value": N * K / e2e_s, "unit": "lookups/s", "h2d_bytes_per_step": N * samples.itemsize,
+                            "prepare_avg": prof["prepare_ms"] / max(prof["calls"], 1),
+                            "pool_avg": float(np.mean(p_ms)) if p_ms else None,
+                            "update_avg": float(np.mean(b_ms)) if b_ms else None},
+        "e2e": {"value": lookups * K / e2e_s, "unit": "lookups/s", "h2d_bytes_per_step": N * samples.itemsize,
                 "d2h_bytes_per_step": 64, "ms_per_step": e2e_s / K * 1e3,
-                "path": "CacheStack.prepare(pinned host ids) + gather + apply_synthetic_update"},
-        "gpu_launches": KERNELS_PER_STEP * K,
-        "roofline": dominant, "roofline_secondary": other,
+                "path": "CachedEmbeddingBag.forward(pinned host ids) + out.backward(grad) (fused SGD); result = "
+                        "prepare hit/miss counters read back" if not sharded
+                else "RowShardedEmbedding.forward(pinned host ids) + out.backward(grad)"},
+        "gpu_launches": (KERNELS_PER_STEP if args.step == "sim" else KERNELS_PER_TRAIN_STEP) * K,
+        "roofline": rl[0], "roofline_secondary": rl[1] if len(rl) > 1 else None,
         "host_link": links,
         "clocks": clk.summary(),
     }
+    if not sharded:
+        res.update({"hit_ratio": hits / uniq, "unique_per_step": uniq, "misses_per_step": misses,
+                    "evictions_per_step": evict, "writeback_rows_per_step": wb})
     return res, samples, rank_of, cap
 
 
@@ -338,9 +427,11 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="criteo_kaggle", choices=list(CONFIGS))
+    ap.add_argument("--step", default="train", choices=["train", "sim"])
     ap.add_argument("--trace-batches", type=int, default=64)
     ap.add_argument("--cpu-baseline-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true", help="row-sharded module even at one GPU (needs torchrun)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -351,17 +442,19 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return 0
-        n_batches = max(args.trace_batches, args.warmup + 2 * args.steps)
-        samples, rank_of, _, cap = make_workload(cfg, n_batches, device=None)
-        r = run_cpu_reference(samples, rank_of, cap, cfg, args.steps, args.warmup)
-        n = cfg["batch"] * cfg["features"]
-        out = {"metric": METRIC, "value": r["lookups_per_s"], "unit": "lookups/s", "n_gpus": args.gpus,
+        n_batches = max(args.trace_batches // world, args.warmup + 2 * args.steps)
+        samples, rank_of, _, cap = make_workload(cfg, n_batches * world, device=None)
+        r = run_cpu_reference(samples, rank_of, cap, cfg, args.steps, args.warmup, args.step, batch_mult=world)
+        n = cfg["batch"] * cfg["features"] * world
+        out = {"metric": METRIC, "value": r["lookups_per_s"], "unit": "lookups/s", "n_gpus": world,
                "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["step_s"] * 1e3,
                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 rows, int32 ids",
                "data": "synthetic: reference gen_zipf stream (seed 1)", "impl": "reference",
                "config": {"workload": args.config, "num_rows": cfg["num_ids"], "dim": cfg["dim"],
-                          "capacity": cap, "batch": cfg["batch"], "features": cfg["features"], "lookups_per_step": n,
-                          "step": "prepare + gather + apply_unique_update (simulator.py:419-433)"},
+                          "capacity": cap, "batch": cfg["batch"] * world, "features": cfg["features"],
+                          "lookups_per_step": n,
+                          "step": "prepare + gather + scatter_update(-lr*grad)" if args.step == "train"
+                          else "prepare + gather + apply_unique_update (simulator.py:419-433)"},
                "cpu_baseline": {"value": r["lookups_per_s"], "unit": "lookups/s", "cores": 1, "kind": "port",
                                 "sample": f"{r['steps']} batches of {n} ids after {args.warmup} warm-up batches; "
                                           "numpy oracle restatement of the reference (single-threaded numpy)"},
@@ -372,17 +465,17 @@ def main():
 
     import torch
 
-    if world > 1:
-        torch.distributed.init_process_group("nccl")
+    if world > 1 or args.sharded:
+        torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
     res, samples, rank_of, cap = run_ours(args, cfg, torch, rank, world)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = run_cpu_reference(samples, rank_of, cap, cfg, args.cpu_baseline_steps, 2, time_budget_s=30)
+        r = run_cpu_reference(samples, rank_of, cap, cfg, args.cpu_baseline_steps, 2, args.step, time_budget_s=30)
         res["cpu_baseline"] = {"value": r["lookups_per_s"], "unit": "lookups/s", "cores": 1, "kind": "port",
                                "sample": f"{r['steps']} batches after 2 warm-up batches of the same trace; "
-                                         "numpy oracle port, single-threaded"}
+                                         "numpy oracle port (same step), single-threaded"}
     if rank == 0:
         print(json.dumps(res), flush=True)
-    if world > 1:
+    if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
     return 0
 

@@ -20,8 +20,9 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libfreqcache_b200.so")
-SOURCES = ["fc_api.cu", "fc_index.cu", "fc_rows.cu", "fc_sort.cu"]
-HEADERS = [os.path.join(CSRC, "fc_internal.cuh"), os.path.join(ROOT, "include", "freqcache_b200.h")]
+SOURCES = ["fc_api.cu", "fc_index.cu", "fc_rows.cu", "fc_sort.cu", "fc_backward.cu"]
+HEADERS = [os.path.join(CSRC, "fc_internal.cuh"), os.path.join(CSRC, "fc_rowutil.cuh"),
+           os.path.join(ROOT, "include", "freqcache_b200.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",

@@ -1,0 +1,385 @@
+// Occurrence grouping, scatter_update and the fused backward + sparse optimizer.
+//
+// Both paths first group a batch's occurrences by unique row with a stable radix
+// sort of `inverse` (so batch order is kept inside a group):
+//   * scatter_update (/root/reference/pkg/src/freqcache/cache_manager.py:423-438)
+//     then adds each group's deltas in batch order — bit-exact with np.add.at;
+//   * the backward of the pooled forward (north star item 6) streams the sorted
+//     occurrences once: each warp owns a chunk of kChunk consecutive sorted
+//     occurrences, accumulates coef_j * grad_out[bag(j)] per run of equal rows in
+//     registers (one float4 column unit per lane, kBwdUnroll grad rows in flight)
+//     and stores the sum per unique row; runs cut by chunk boundaries leave
+//     carries that one fix-up pass sums in chunk order; a last pass applies SGD /
+//     Adagrad to every cached row (32 rows per warp). Fixed order -> deterministic.
+#include <algorithm>
+
+#include "fc_rowutil.cuh"
+
+namespace fc {
+
+constexpr int kChunk = 64;  // sorted occurrences per warp in the backward stream
+constexpr int kBwdUnroll = 4;
+
+struct Grouping {
+  uint32_t* keys;   // [n] sorted unique positions
+  int32_t* order;   // [n] occurrence index of each sorted position
+  char* rest;
+};
+
+static size_t grouping_bytes(int64_t n) { return align16(n * 4) * 2 + align16(sort_scratch_bytes(n)); }
+
+static int build_grouping(fc_cache* h, const int32_t* inv, int64_t u, int64_t n, size_t extra, Grouping& g,
+                          cudaStream_t st) {
+  int rc = ensure_scratch(h, grouping_bytes(n) + extra);
+  if (rc) return rc;
+  char* p = static_cast<char*>(h->scratch);
+  g.keys = reinterpret_cast<uint32_t*>(p);
+  p += align16(n * 4);
+  g.order = reinterpret_cast<int32_t*>(p);
+  p += align16(n * 4);
+  void* sort_scr = p;
+  p += align16(sort_scratch_bytes(n));
+  g.rest = p;
+  return radix_sort_pairs(reinterpret_cast<const uint32_t*>(inv), nullptr, g.keys, g.order, n, key_bits_for(u),
+                          sort_scr, st);
+}
+
+// ------------------------------------------------------------- scatter_update, bit-exact with np.add.at
+__global__ void __launch_bounds__(kNT) k_seg_add_seq(float* fast, int D, const int32_t* __restrict__ uslots, int64_t u,
+                                                     const int32_t* __restrict__ seg, const int32_t* __restrict__ order,
+                                                     const float* __restrict__ deltas, uint8_t* dirty) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  for (int64_t p = warp; p < u; p += nwarps) {  // one warp per unique row, lanes over columns
+    const int64_t s = uslots[p];
+    float* row = fast + s * D;
+    const int j0 = seg[p], j1 = seg[p + 1];
+    for (int c = lane; c < D; c += 32) {
+      float acc = row[c];
+      for (int j = j0; j < j1; ++j) acc = __fadd_rn(acc, deltas[(int64_t)order[j] * D + c]);  // batch order
+      row[c] = acc;
+    }
+    if (lane == 0) dirty[s] = 1;
+  }
+}
+
+int launch_scatter_update(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u,
+                          int64_t n, const float* deltas, cudaStream_t st) {
+  if (u <= 0 || n <= 0) return FC_OK;
+  Grouping g;
+  const size_t extra = align16((u + 1) * 4) + align16(scan_scratch_bytes(u));
+  int rc = build_grouping(h, inv, u, n, extra, g, st);
+  if (rc) return rc;
+  int32_t* seg = reinterpret_cast<int32_t*>(g.rest);
+  void* scan_scr = g.rest + align16((u + 1) * 4);
+  rc = exclusive_scan_i32(ucnt, seg, u, scan_scr, st);
+  if (rc) return rc;
+  k_seg_add_seq<<<grid_for(u * 32, kNT, kSMs * 16), kNT, 0, st>>>(h->fast, h->dim, uslots, u, seg, g.order, deltas,
+                                                                 h->dirty);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------- backward + sparse optimizer
+struct OptArgs {
+  int optim;
+  float lr, eps;
+};
+
+__device__ __forceinline__ float opt1(float w, float* st, float g, const OptArgs& o) {
+  if (o.optim == FC_OPT_ADAGRAD) {  // torch.optim.Adagrad: G += g^2; w -= lr * g / (sqrt(G) + eps)
+    const float s = *st + g * g;
+    *st = s;
+    return w - o.lr * g / (sqrtf(s) + o.eps);
+  }
+  return w - o.lr * g;  // torch.optim.SGD
+}
+
+__device__ __forceinline__ void apply_unit(float* w, float* st, float4 g, const OptArgs& o) {
+  float4 v = ld4(w);
+  if (st) {
+    v.x = opt1(v.x, st + 0, g.x, o);
+    v.y = opt1(v.y, st + 1, g.y, o);
+    v.z = opt1(v.z, st + 2, g.z, o);
+    v.w = opt1(v.w, st + 3, g.w, o);
+  } else {
+    v.x -= o.lr * g.x;
+    v.y -= o.lr * g.y;
+    v.z -= o.lr * g.z;
+    v.w -= o.lr * g.w;
+  }
+  st4(w, v);
+}
+
+template <typename OffT>
+__global__ void __launch_bounds__(kNT) k_bag_coef(const OffT* __restrict__ off, int64_t nbags, int64_t n, int incl,
+                                                  const float* __restrict__ psw, int mode, int32_t* bag_of,
+                                                  float* coef) {
+  for (int64_t b = (int64_t)blockIdx.x * kNT + threadIdx.x; b < nbags; b += (int64_t)gridDim.x * kNT) {
+    int64_t s, e;
+    bag_bounds(off, b, nbags, n, incl, s, e);
+    const float scale = (mode == FC_POOL_MEAN) ? (e > s ? 1.0f / (float)(e - s) : 0.0f) : 1.0f;
+    for (int64_t j = s; j < e; ++j) {
+      bag_of[j] = (int32_t)b;
+      coef[j] = psw ? scale * psw[j] : scale;
+    }
+  }
+}
+
+struct BwdArgs {
+  float* fast;
+  float* fstate;
+  int D;
+  const int32_t* uslots;
+  const uint32_t* keys;
+  const int32_t* order;
+  int64_t n;
+  const int32_t* bag_of;  // NULL: bag = occurrence
+  const float* coef;      // NULL: coef = 1 (or psw)
+  const float* psw;
+  const float* grad;
+  float* gu;              // [u, D] summed gradient per unique row
+  float* carry;           // [nchunks * 2, D]
+  int32_t* carry_key;     // [nchunks * 2] (-1 none)
+  int32_t* carry_flag;    // bit0: run open at chunk start, bit1: open at chunk end
+  uint8_t* dirty;
+  OptArgs o;
+  Units un;
+};
+
+// Store / carry one finished run of key `key` over sorted positions [a, b) of chunk c
+__device__ __forceinline__ void bwd_flush(const BwdArgs& x, int64_t c, int64_t j0, int64_t j1, int key, int64_t a,
+                                          int64_t b, int prev_key, int next_key, float4 acc, int unit, bool has,
+                                          bool first_col) {
+  const bool open_s = (a == j0) && (prev_key == key);
+  const bool open_e = (b == j1) && (next_key == key);
+  if (!open_s && !open_e) {
+    if (has) st4(x.gu + (int64_t)key * x.D + unit * 4, acc);
+  } else {
+    const int64_t slot = c * 2 + (open_s ? 0 : 1);
+    if (has) st4(x.carry + slot * x.D + unit * 4, acc);
+    if (first_col && (threadIdx.x & 31) == 0) {
+      x.carry_key[slot] = key;
+      x.carry_flag[slot] = (open_s ? 1 : 0) | (open_e ? 2 : 0);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kNT) k_bwd_stream(BwdArgs x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  const int64_t nchunks = (x.n + kChunk - 1) / kChunk;
+  for (int64_t c = warp; c < nchunks; c += nwarps) {
+    const int64_t j0 = c * kChunk, j1 = min(x.n, j0 + kChunk);
+    const int prev_key = j0 > 0 ? (int)x.keys[j0 - 1] : -1;
+    const int next_key = j1 < x.n ? (int)x.keys[j1] : -1;
+    for (int cu0 = 0; cu0 < x.un.upr; cu0 += 32) {
+      const int unit = cu0 + lane;
+      const bool has = unit < x.un.upr;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      int cur = -1;
+      int64_t run_a = j0;
+      for (int64_t r0 = j0; r0 < j1; r0 += 32) {
+        const int64_t jj = r0 + lane;
+        int kl = -1, bag = 0;
+        float cf = 0.f;
+        if (jj < j1) {
+          kl = (int)x.keys[jj];
+          const int occ = x.order[jj];
+          bag = x.bag_of ? x.bag_of[occ] : occ;
+          cf = x.coef ? x.coef[occ] : (x.psw ? x.psw[occ] : 1.0f);
+        }
+        const int cnt = (int)(j1 - r0 < 32 ? j1 - r0 : 32);
+        for (int q = 0; q < cnt; q += kBwdUnroll) {
+          float4 g[kBwdUnroll];
+          int kq[kBwdUnroll];
+          float cq[kBwdUnroll];
+#pragma unroll
+          for (int k = 0; k < kBwdUnroll; ++k) {
+            const int src = min(q + k, 31);
+            const int bq = __shfl_sync(FC_FULL, bag, src);
+            kq[k] = __shfl_sync(FC_FULL, kl, src);
+            cq[k] = __shfl_sync(FC_FULL, cf, src);
+            g[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (has && q + k < cnt) g[k] = ldg4(x.grad + (int64_t)bq * x.D + unit * 4);
+          }
+#pragma unroll
+          for (int k = 0; k < kBwdUnroll; ++k) {
+            if (q + k >= cnt) break;
+            if (kq[k] != cur) {
+              if (cur >= 0)
+                bwd_flush(x, c, j0, j1, cur, run_a, r0 + q + k, prev_key, next_key, acc, unit, has, cu0 == 0);
+              cur = kq[k];
+              run_a = r0 + q + k;
+              acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            acc.x += cq[k] * g[k].x;
+            acc.y += cq[k] * g[k].y;
+            acc.z += cq[k] * g[k].z;
+            acc.w += cq[k] * g[k].w;
+          }
+        }
+      }
+      if (cur >= 0) bwd_flush(x, c, j0, j1, cur, run_a, j1, prev_key, next_key, acc, unit, has, cu0 == 0);
+    }
+  }
+}
+
+// Runs cut by chunk boundaries: chunk c's end-open run (slot 1) starts a split
+// group; the following chunks' start-open runs (slot 0) continue it until one is
+// closed at its end. Sum in chunk order, then update the row once.
+__global__ void __launch_bounds__(kNT) k_bwd_fixup(BwdArgs x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  const int64_t nchunks = (x.n + kChunk - 1) / kChunk;
+  for (int64_t c = warp; c < nchunks; c += nwarps) {
+    const int key = x.carry_key[c * 2 + 1];
+    if (key < 0) continue;
+    // extent: chunks c+1 .. c+m whose slot 0 carries `key`; the last one is closed at its end
+    int64_t m = 0;
+    for (int64_t base = c + 1; base < nchunks; base += 32) {
+      const int64_t cc = base + lane;
+      const bool cont = cc < nchunks && x.carry_key[cc * 2] == key;
+      const bool last = cont && !(x.carry_flag[cc * 2] & 2);
+      const unsigned lastm = __ballot_sync(FC_FULL, last);
+      const unsigned contm = __ballot_sync(FC_FULL, cont);
+      if (lastm) {
+        m += __ffs(lastm);
+        break;
+      }
+      m += __popc(contm);
+      if (contm != FC_FULL) break;
+    }
+    for (int cu0 = 0; cu0 < x.un.upr; cu0 += 32) {
+      const int unit = cu0 + lane;
+      if (unit >= x.un.upr) continue;
+      float4 acc = ld4(x.carry + (c * 2 + 1) * x.D + unit * 4);
+      int64_t t = 0;
+      constexpr int kF = 16;  // a hot row's carries form a long chain: keep 16 loads in flight
+      for (; t + kF <= m; t += kF) {
+        float4 v[kF];
+#pragma unroll
+        for (int k = 0; k < kF; ++k) v[k] = ld4(x.carry + ((c + 1 + t + k) * 2) * x.D + unit * 4);
+#pragma unroll
+        for (int k = 0; k < kF; ++k) {
+          acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
+        }
+      }
+      for (; t < m; ++t) {
+        const float4 v = ld4(x.carry + ((c + 1 + t) * 2) * x.D + unit * 4);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      st4(x.gu + (int64_t)key * x.D + unit * 4, acc);
+    }
+  }
+}
+
+// optimizer step on every unique row, 32 rows per warp, kBwdUnroll units in flight
+__global__ void __launch_bounds__(kNT) k_bwd_apply(BwdArgs x, int64_t u) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  const int total = 32 * x.un.upr;
+  for (int64_t base = warp * 32; base < u; base += nwarps * 32) {
+    const int64_t p = base + lane;
+    const bool act = p < u;
+    const int s = act ? x.uslots[p] : 0;
+    for (int u0 = 0; u0 < total; u0 += 32 * kBwdUnroll) {
+      float4 g[kBwdUnroll];
+      float* w[kBwdUnroll];
+      bool aa[kBwdUnroll];
+#pragma unroll
+      for (int k = 0; k < kBwdUnroll; ++k) {
+        const int q = u0 + k * 32 + lane;
+        const int r = min(x.un.row(q), 31);
+        const int c = (q - r * x.un.upr) * 4;
+        const int sr = __shfl_sync(FC_FULL, s, r);
+        aa[k] = __shfl_sync(FC_FULL, (int)act, r) && q < total;
+        w[k] = x.fast + (int64_t)sr * x.D + c;
+        if (aa[k]) g[k] = ld4(x.gu + (base + r) * x.D + c);
+      }
+#pragma unroll
+      for (int k = 0; k < kBwdUnroll; ++k)
+        if (aa[k]) {
+          float* stp = x.fstate ? x.fstate + (w[k] - x.fast) : nullptr;
+          apply_unit(w[k], stp, g[k], x.o);
+        }
+    }
+    if (act) x.dirty[s] = 1;
+  }
+}
+
+int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u, int64_t n,
+                    const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw, int mode,
+                    const float* grad, int optim, float lr, float eps, cudaStream_t st) {
+  (void)ucnt;
+  if (u <= 0 || n <= 0) return FC_OK;
+  const int D = h->dim;
+  if (optim == FC_OPT_ADAGRAD && (h->fast_state == nullptr || h->sw != D)) {
+    set_error("Adagrad needs a cache created with state_width == dim");
+    return FC_ERR_BAD_ARG;
+  }
+  if (D % 4 || (reinterpret_cast<uintptr_t>(grad) & 15)) {
+    set_error("backward needs dim %% 4 == 0 and a 16-byte aligned grad_out");
+    return FC_ERR_BAD_ARG;
+  }
+  const int64_t nchunks = (n + kChunk - 1) / kChunk;
+  const bool bags = offsets != nullptr;
+  const size_t extra = align16((size_t)u * D * 4) + align16(nchunks * 2 * (size_t)D * 4) +
+                       2 * align16(nchunks * 2 * 4) + (bags ? 2 * align16(n * 4) : 0);
+  Grouping g;
+  int rc = build_grouping(h, inv, u, n, extra, g, st);
+  if (rc) return rc;
+  char* p = g.rest;
+  BwdArgs x;
+  x.gu = reinterpret_cast<float*>(p);
+  p += align16((size_t)u * D * 4);
+  x.carry = reinterpret_cast<float*>(p);
+  p += align16(nchunks * 2 * (size_t)D * 4);
+  x.carry_key = reinterpret_cast<int32_t*>(p);
+  p += align16(nchunks * 2 * 4);
+  x.carry_flag = reinterpret_cast<int32_t*>(p);
+  p += align16(nchunks * 2 * 4);
+  x.bag_of = nullptr;
+  x.coef = nullptr;
+  x.psw = bags ? nullptr : psw;
+  if (bags) {
+    int32_t* bag_of = reinterpret_cast<int32_t*>(p);
+    p += align16(n * 4);
+    float* coef = reinterpret_cast<float*>(p);
+    // occurrences outside every bag (include_last_offset with a short last offset) contribute 0
+    FC_CUDA(cudaMemsetAsync(bag_of, 0, n * 4, st));
+    FC_CUDA(cudaMemsetAsync(coef, 0, n * 4, st));
+    const int gb = grid_for(nbags, kNT, kSMs * 8);
+    if (off_bytes == 4)
+      k_bag_coef<int32_t><<<gb, kNT, 0, st>>>((const int32_t*)offsets, nbags, n, include_last, psw, mode, bag_of, coef);
+    else
+      k_bag_coef<long long><<<gb, kNT, 0, st>>>((const long long*)offsets, nbags, n, include_last, psw, mode, bag_of,
+                                               coef);
+    x.bag_of = bag_of;
+    x.coef = coef;
+  }
+  FC_CUDA(cudaMemsetAsync(x.carry_key, 0xff, nchunks * 2 * 4, st));
+  x.fast = h->fast;
+  x.fstate = optim == FC_OPT_ADAGRAD ? h->fast_state : nullptr;
+  x.D = D;
+  x.uslots = uslots;
+  x.keys = g.keys;
+  x.order = g.order;
+  x.n = n;
+  x.grad = grad;
+  x.dirty = h->dirty;
+  x.o = OptArgs{optim, lr, eps};
+  x.un = units_for(D);
+  const int grid = grid_for(nchunks * 32, kNT, kSMs * 16);
+  k_bwd_stream<<<grid, kNT, 0, st>>>(x);
+  k_bwd_fixup<<<grid, kNT, 0, st>>>(x);
+  k_bwd_apply<<<grid_for(u, kNT, kSMs * 8), kNT, 0, st>>>(x, u);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+}  // namespace fc

@@ -12,7 +12,7 @@
 // buffer; here the "buffer" is the HBM staging area of the victims).
 #include <algorithm>
 
-#include "fc_internal.cuh"
+#include "fc_rowutil.cuh"
 
 namespace fc {
 
@@ -74,16 +74,6 @@ static bool vec_ok(fc_cache* h) {
   return v;
 }
 
-template <bool VEC>
-__device__ __forceinline__ void copy_row(float* __restrict__ dst, const float* __restrict__ src, int w, int gl, int G) {
-  if (VEC) {
-    for (int c = gl * 4; c < w; c += G * 4)
-      *reinterpret_cast<float4*>(dst + c) = *reinterpret_cast<const float4*>(src + c);
-  } else {
-    for (int c = gl; c < w; c += G) dst[c] = src[c];
-  }
-}
-
 // two independent row copies with both loads issued before both stores
 template <bool VEC>
 __device__ __forceinline__ void copy_two_rows(float* d1, const float* s1, bool a1, float* d2, const float* s2, bool a2,
@@ -127,23 +117,6 @@ struct GroupIdx {
 // 16-byte units, K units per lane in flight. Row r's offsets come from lane r by
 // shuffle. This hides the index->row dependent latency that a row-per-warp loop
 // pays once per row.
-struct Units {
-  int upr;  // 16-byte units per row
-  int lg;   // log2(upr) or -1
-  __device__ __forceinline__ int row(int u) const { return lg >= 0 ? (u >> lg) : (u / upr); }
-};
-
-static Units units_for(int width) {
-  Units un;
-  un.upr = width / 4;
-  un.lg = (un.upr & (un.upr - 1)) == 0 ? __builtin_ctz(un.upr) : -1;
-  return un;
-}
-
-__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
-__device__ __forceinline__ float4 ldg4(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-__device__ __forceinline__ void st4(float* p, float4 v) { *reinterpret_cast<float4*>(p) = v; }
-
 // dst[drow_r * dstride + c] = src[srow_r * sstride + c] (* scale_r) for the warp's 32
 // rows (act_r false -> skipped). Row indices travel by shuffle as int32.
 template <int K, bool SCALE = false>
@@ -380,18 +353,6 @@ int launch_flush(fc_cache* h, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------- pooled EmbeddingBag forward
-template <typename OffT>
-__device__ __forceinline__ void bag_bounds(const OffT* off, int64_t b, int64_t nbags, int64_t n, int incl, int64_t& s,
-                                           int64_t& e) {
-  if (off == nullptr) {
-    s = b;
-    e = b + 1;
-    return;
-  }
-  s = (int64_t)off[b];
-  e = (incl || b + 1 < nbags) ? (int64_t)off[b + 1] : n;
-}
-
 template <bool VEC, typename OffT>
 __global__ void __launch_bounds__(kNT) k_pool(const float* __restrict__ fast, int D, const int32_t* __restrict__ uslots,
                                               const int32_t* __restrict__ inv, int64_t n, const OffT* __restrict__ off,
@@ -617,271 +578,6 @@ int launch_synthetic(fc_cache* h, const int32_t* uids, const int32_t* ucnt, cons
     k_synthetic<false><<<grid_w, kNT, 0, st>>>(h->fast, h->dim, uids, ucnt, uslots, u, salt, colw, h->dirty, G,
                                                units_for(4));
   (void)grid;
-  FC_CUDA(cudaGetLastError());
-  return FC_OK;
-}
-
-// ------------------------------------------------------------- grouping occurrences by unique row
-// keys = inverse (unique position), values = occurrence index; stable sort keeps batch order
-struct Grouping {
-  int32_t* order;      // [n] occurrence indices grouped by unique row, batch order inside a group
-  int32_t* seg_start;  // [u+1]
-  char* rest;          // remaining scratch
-};
-
-static int key_bits_for(int64_t u) {
-  int b = 1;
-  while ((int64_t(1) << b) < u) ++b;
-  return b;
-}
-
-__global__ void k_iota(int32_t* v, int64_t n) {
-  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) v[i] = (int32_t)i;
-}
-
-static size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
-
-static size_t grouping_bytes(int64_t n, int64_t u) {
-  return align16(n * 4) * 3 + align16((u + 1) * 4) + align16(scan_scratch_bytes(u)) + align16(sort_scratch_bytes(n));
-}
-
-static int build_grouping(fc_cache* h, const int32_t* inv, const int32_t* ucnt, int64_t u, int64_t n, size_t extra,
-                          Grouping& out, cudaStream_t st) {
-  const size_t need = grouping_bytes(n, u) + extra;
-  int rc = ensure_scratch(h, need);
-  if (rc) return rc;
-  char* p = static_cast<char*>(h->scratch);
-  int32_t* iota = reinterpret_cast<int32_t*>(p);
-  p += align16(n * 4);
-  uint32_t* ksorted = reinterpret_cast<uint32_t*>(p);
-  p += align16(n * 4);
-  out.order = reinterpret_cast<int32_t*>(p);
-  p += align16(n * 4);
-  out.seg_start = reinterpret_cast<int32_t*>(p);
-  p += align16((u + 1) * 4);
-  void* scan_scr = p;
-  p += align16(scan_scratch_bytes(u));
-  void* sort_scr = p;
-  p += align16(sort_scratch_bytes(n));
-  out.rest = p;
-  k_iota<<<grid_for(n, kNT, kSMs * 8), kNT, 0, st>>>(iota, n);
-  rc = radix_sort_pairs(reinterpret_cast<const uint32_t*>(inv), iota, ksorted, out.order, n, key_bits_for(u), sort_scr,
-                        st);
-  if (rc) return rc;
-  return exclusive_scan_i32(ucnt, out.seg_start, u, scan_scr, st);
-}
-
-// ------------------------------------------------------------- scatter_update (:423-438), bit-exact with np.add.at
-template <bool VEC>
-__global__ void __launch_bounds__(kNT) k_seg_add_seq(float* fast, int D, const int32_t* __restrict__ uslots, int64_t u,
-                                                     const int32_t* __restrict__ seg, const int32_t* __restrict__ order,
-                                                     const float* __restrict__ deltas, uint8_t* dirty, int G) {
-  GroupIdx g(G);
-  for (int64_t base = g.warp * g.gpw; base < u; base += g.nwarps * g.gpw) {
-    const int64_t p = base + g.gw;
-    if (p >= u) continue;
-    const int64_t s = uslots[p];
-    float* row = fast + s * D;
-    const int j0 = seg[p], j1 = seg[p + 1];
-    for (int c = g.gl; c < D; c += G) {
-      float acc = row[c];
-      for (int j = j0; j < j1; ++j) acc = __fadd_rn(acc, deltas[(int64_t)order[j] * D + c]);  // batch order
-      row[c] = acc;
-    }
-    if (g.gl == 0) dirty[s] = 1;
-  }
-}
-
-int launch_scatter_update(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u,
-                          int64_t n, const float* deltas, cudaStream_t st) {
-  if (u <= 0 || n <= 0) return FC_OK;
-  Grouping gr;
-  int rc = build_grouping(h, inv, ucnt, u, n, 0, gr, st);
-  if (rc) return rc;
-  const int G = row_group(h->dim, false);
-  k_seg_add_seq<false><<<grid_for(u * G, kNT, kSMs * 16), kNT, 0, st>>>(h->fast, h->dim, uslots, u, gr.seg_start,
-                                                                      gr.order, deltas, h->dirty, G);
-  FC_CUDA(cudaGetLastError());
-  return FC_OK;
-}
-
-// ------------------------------------------------------------- backward + sparse optimizer (north star item 6)
-// Occurrences grouped by unique row are cut into parts of <= kPart occurrences.
-// Phase 1 (one row group per part) sums coef_j * grad_out[bag(j)] in batch order;
-// single-part rows apply the optimizer directly, others write a partial row.
-// Phase 2 sums a multi-part row's partials in part order, then applies the
-// optimizer. Fixed summation order -> deterministic results.
-constexpr int kPart = 128;
-
-template <typename OffT>
-__global__ void __launch_bounds__(kNT) k_bag_coef(const OffT* __restrict__ off, int64_t nbags, int64_t n, int incl,
-                                                  const float* __restrict__ psw, int mode, int32_t* bag_of,
-                                                  float* coef) {
-  for (int64_t b = (int64_t)blockIdx.x * kNT + threadIdx.x; b < nbags; b += (int64_t)gridDim.x * kNT) {
-    int64_t s, e;
-    bag_bounds(off, b, nbags, n, incl, s, e);
-    const float scale = (mode == FC_POOL_MEAN) ? (e > s ? 1.0f / (float)(e - s) : 0.0f) : 1.0f;
-    for (int64_t j = s; j < e; ++j) {
-      bag_of[j] = (int32_t)b;
-      coef[j] = psw ? scale * psw[j] : scale;
-    }
-  }
-}
-
-__global__ void k_parts(const int32_t* __restrict__ ucnt, int64_t u, int32_t* nparts) {
-  for (int64_t p = (int64_t)blockIdx.x * kNT + threadIdx.x; p < u; p += (int64_t)gridDim.x * kNT)
-    nparts[p] = (ucnt[p] + kPart - 1) / kPart;
-}
-
-__global__ void k_part_map(const int32_t* __restrict__ nparts, const int32_t* __restrict__ pstart, int64_t u,
-                           int32_t* part_seg) {
-  for (int64_t p = (int64_t)blockIdx.x * kNT + threadIdx.x; p < u; p += (int64_t)gridDim.x * kNT)
-    for (int k = 0; k < nparts[p]; ++k) part_seg[pstart[p] + k] = (int32_t)p;
-}
-
-struct OptArgs {
-  int optim;
-  float lr, eps;
-};
-
-__device__ __forceinline__ void apply_opt(float* w, float* st, int c, float gsum, const OptArgs& o) {
-  if (o.optim == FC_OPT_ADAGRAD) {
-    const float s = st[c] + gsum * gsum;
-    st[c] = s;
-    w[c] -= o.lr * gsum / (sqrtf(s) + o.eps);
-  } else {
-    w[c] -= o.lr * gsum;
-  }
-}
-
-template <bool VEC>
-__global__ void __launch_bounds__(kNT) k_bwd_parts(float* fast, float* fstate, int D, const int32_t* __restrict__ uslots,
-                                                   const int32_t* __restrict__ ucnt, const int32_t* __restrict__ seg,
-                                                   const int32_t* __restrict__ order, const int32_t* __restrict__ nparts,
-                                                   const int32_t* __restrict__ pstart, const int32_t* __restrict__ part_seg,
-                                                   const int32_t* total_parts, const int32_t* __restrict__ bag_of,
-                                                   const float* __restrict__ coef, const float* __restrict__ grad,
-                                                   float* partial, uint8_t* dirty, OptArgs o, int G) {
-  const int64_t T = *total_parts;
-  GroupIdx g(G);
-  for (int64_t base = g.warp * g.gpw; base < T; base += g.nwarps * g.gpw) {
-    const int64_t t = base + g.gw;
-    if (t >= T) continue;
-    const int p = part_seg[t];
-    const int k = (int)(t - pstart[p]);
-    const int j0 = seg[p] + k * kPart;
-    const int j1 = min(seg[p] + ucnt[p], j0 + kPart);
-    const bool single = nparts[p] == 1;
-    const int64_t s = uslots[p];
-    for (int c = g.gl * (VEC ? 4 : 1); c < D; c += G * (VEC ? 4 : 1)) {
-      if (VEC) {
-        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int j = j0; j < j1; ++j) {
-          const int i = order[j];
-          const float cf = coef[i];
-          const float4 gv = __ldg(reinterpret_cast<const float4*>(grad + (int64_t)bag_of[i] * D + c));
-          acc.x += cf * gv.x; acc.y += cf * gv.y; acc.z += cf * gv.z; acc.w += cf * gv.w;
-        }
-        if (single) {
-          float* w = fast + s * D;
-          float* stt = fstate ? fstate + s * D : nullptr;
-          apply_opt(w, stt, c, acc.x, o);
-          apply_opt(w, stt, c + 1, acc.y, o);
-          apply_opt(w, stt, c + 2, acc.z, o);
-          apply_opt(w, stt, c + 3, acc.w, o);
-        } else {
-          *reinterpret_cast<float4*>(partial + t * D + c) = acc;
-        }
-      } else {
-        float acc = 0.f;
-        for (int j = j0; j < j1; ++j) {
-          const int i = order[j];
-          acc += coef[i] * grad[(int64_t)bag_of[i] * D + c];
-        }
-        if (single) apply_opt(fast + s * D, fstate ? fstate + s * D : nullptr, c, acc, o);
-        else partial[t * D + c] = acc;
-      }
-    }
-    if (single && g.gl == 0) dirty[s] = 1;
-  }
-}
-
-__global__ void __launch_bounds__(kNT) k_bwd_combine(float* fast, float* fstate, int D, const int32_t* __restrict__ uslots,
-                                                     int64_t u, const int32_t* __restrict__ nparts,
-                                                     const int32_t* __restrict__ pstart, const float* __restrict__ partial,
-                                                     uint8_t* dirty, OptArgs o, int G) {
-  GroupIdx g(G);
-  for (int64_t base = g.warp * g.gpw; base < u; base += g.nwarps * g.gpw) {
-    const int64_t p = base + g.gw;
-    if (p >= u || nparts[p] <= 1) continue;
-    const int64_t s = uslots[p];
-    const int t0 = pstart[p], t1 = t0 + nparts[p];
-    for (int c = g.gl; c < D; c += G) {
-      float acc = 0.f;
-      for (int t = t0; t < t1; ++t) acc += partial[(int64_t)t * D + c];
-      apply_opt(fast + s * D, fstate ? fstate + s * D : nullptr, c, acc, o);
-    }
-    if (g.gl == 0) dirty[s] = 1;
-  }
-}
-
-int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u, int64_t n,
-                    const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw, int mode,
-                    const float* grad, int optim, float lr, float eps, cudaStream_t st) {
-  if (u <= 0 || n <= 0) return FC_OK;
-  if (optim == FC_OPT_ADAGRAD && (h->fast_state == nullptr || h->sw != h->dim)) {
-    set_error("Adagrad needs a cache created with state_width == dim");
-    return FC_ERR_BAD_ARG;
-  }
-  const int D = h->dim;
-  const int64_t max_parts = n / kPart + u + 1;
-  const size_t extra = align16(n * 4) * 2 + align16(u * 4) + align16((u + 1) * 4) + align16(max_parts * 4) +
-                       align16(max_parts * (size_t)D * 4) + align16(scan_scratch_bytes(u));
-  Grouping gr;
-  int rc = build_grouping(h, inv, ucnt, u, n, extra, gr, st);
-  if (rc) return rc;
-  char* p = gr.rest;
-  int32_t* bag_of = reinterpret_cast<int32_t*>(p);
-  p += align16(n * 4);
-  float* coef = reinterpret_cast<float*>(p);
-  p += align16(n * 4);
-  int32_t* nparts = reinterpret_cast<int32_t*>(p);
-  p += align16(u * 4);
-  int32_t* pstart = reinterpret_cast<int32_t*>(p);
-  p += align16((u + 1) * 4);
-  int32_t* part_seg = reinterpret_cast<int32_t*>(p);
-  p += align16(max_parts * 4);
-  float* partial = reinterpret_cast<float*>(p);
-  p += align16(max_parts * (size_t)D * 4);
-  void* scan_scr = p;
-
-  const int gb = grid_for(nbags, kNT, kSMs * 8);
-  // occurrences outside every bag (include_last_offset with a short last offset) contribute 0
-  FC_CUDA(cudaMemsetAsync(bag_of, 0, n * 4, st));
-  FC_CUDA(cudaMemsetAsync(coef, 0, n * 4, st));
-  if (off_bytes == 4)
-    k_bag_coef<int32_t><<<gb, kNT, 0, st>>>((const int32_t*)offsets, nbags, n, include_last, psw, mode, bag_of, coef);
-  else
-    k_bag_coef<long long><<<gb, kNT, 0, st>>>((const long long*)offsets, nbags, n, include_last, psw, mode, bag_of,
-                                             coef);
-  const int gu = grid_for(u, kNT, kSMs * 8);
-  k_parts<<<gu, kNT, 0, st>>>(ucnt, u, nparts);
-  rc = exclusive_scan_i32(nparts, pstart, u, scan_scr, st);
-  if (rc) return rc;
-  k_part_map<<<gu, kNT, 0, st>>>(nparts, pstart, u, part_seg);
-  const bool v = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(grad) & 15) == 0);
-  const int G = row_group(D, v);
-  OptArgs o{optim, lr, eps};
-  const int grid = grid_for(max_parts * G, kNT, kSMs * 16);
-  if (v)
-    k_bwd_parts<true><<<grid, kNT, 0, st>>>(h->fast, h->fast_state, D, uslots, ucnt, gr.seg_start, gr.order, nparts,
-                                            pstart, part_seg, pstart + u, bag_of, coef, grad, partial, h->dirty, o, G);
-  else
-    k_bwd_parts<false><<<grid, kNT, 0, st>>>(h->fast, h->fast_state, D, uslots, ucnt, gr.seg_start, gr.order, nparts,
-                                             pstart, part_seg, pstart + u, bag_of, coef, grad, partial, h->dirty, o, G);
-  const int G1 = row_group(D, false);
-  k_bwd_combine<<<grid_for(u * G1, kNT, kSMs * 16), kNT, 0, st>>>(h->fast, h->fast_state, D, uslots, u, nparts, pstart,
-                                                                  partial, h->dirty, o, G1);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }

@@ -15,7 +15,6 @@ namespace fc {
 constexpr int kRsWarps = 8;
 constexpr int kRsRounds = 8;
 constexpr int kRsTile = kRsWarps * kRsRounds * 32;  // 2048 keys per tile
-constexpr int kRsBins = 256;
 
 // ---------------------------------------------------------------- exclusive scan
 constexpr int kScanTile = kNT * 8;
@@ -78,28 +77,32 @@ int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch
 }
 
 // ---------------------------------------------------------------- radix sort
+// Digits of up to 9 bits (512 bins): keys below 2^18 (U <= 262,144 unique rows)
+// sort in two passes. Each pass = tile histogram -> device-wide scan -> stable scatter.
+constexpr int kRsMaxBins = 512;
+
 __global__ void __launch_bounds__(kRsWarps * 32) k_rs_hist(const uint32_t* __restrict__ keys, int64_t n, int shift,
-                                                           int32_t* hist, int ntiles) {
-  __shared__ int h[kRsBins];
-  for (int d = threadIdx.x; d < kRsBins; d += blockDim.x) h[d] = 0;
+                                                           int bins, int32_t* hist, int ntiles) {
+  __shared__ int h[kRsMaxBins];
+  for (int d = threadIdx.x; d < bins; d += blockDim.x) h[d] = 0;
   __syncthreads();
   const int64_t base = (int64_t)blockIdx.x * kRsTile;
   for (int k = threadIdx.x; k < kRsTile; k += blockDim.x) {
     const int64_t i = base + k;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & (kRsBins - 1)], 1);
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & (bins - 1)], 1);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < kRsBins; d += blockDim.x) hist[(int64_t)d * ntiles + blockIdx.x] = h[d];
+  for (int d = threadIdx.x; d < bins; d += blockDim.x) hist[(int64_t)d * ntiles + blockIdx.x] = h[d];
 }
 
 __global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const uint32_t* __restrict__ kin,
                                                               const int32_t* __restrict__ vin,
                                                               uint32_t* __restrict__ kout, int32_t* __restrict__ vout,
-                                                              int64_t n, int shift, const int32_t* __restrict__ hist,
-                                                              int ntiles) {
-  __shared__ int wc[kRsWarps][kRsBins];
+                                                              int64_t n, int shift, int bins,
+                                                              const int32_t* __restrict__ hist, int ntiles) {
+  __shared__ int wc[kRsWarps][kRsMaxBins];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int d = lane; d < kRsBins; d += 32) wc[w][d] = 0;
+  for (int d = lane; d < bins; d += 32) wc[w][d] = 0;
   __syncwarp();
   const int64_t base = (int64_t)blockIdx.x * kRsTile + (int64_t)w * kRsRounds * 32;
   const unsigned lt = (1u << lane) - 1u;
@@ -111,8 +114,8 @@ __global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const uint32_t* __
     const int64_t i = base + r * 32 + lane;
     const bool valid = i < n;
     kk[r] = valid ? kin[i] : 0u;
-    vv[r] = valid ? vin[i] : 0;
-    const int d = valid ? (int)((kk[r] >> shift) & (kRsBins - 1)) : kRsBins;
+    vv[r] = valid ? (vin ? vin[i] : (int32_t)i) : 0;  // vin == NULL: values are the input positions
+    const int d = valid ? (int)((kk[r] >> shift) & (bins - 1)) : kRsMaxBins;
     dd[r] = d;
     const unsigned peers = __match_any_sync(FC_FULL, d);
     int before = 0;
@@ -123,8 +126,7 @@ __global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const uint32_t* __
     __syncwarp();
   }
   __syncthreads();
-  // exclusive prefix of each digit over the warps (warp order = input order)
-  for (int d = threadIdx.x; d < kRsBins; d += blockDim.x) {
+  for (int d = threadIdx.x; d < bins; d += blockDim.x) {  // warp order = input order
     int run = 0;
 #pragma unroll
     for (int q = 0; q < kRsWarps; ++q) {
@@ -136,7 +138,7 @@ __global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const uint32_t* __
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRsRounds; ++r) {
-    if (dd[r] < kRsBins) {
+    if (dd[r] < kRsMaxBins) {
       const int64_t pos = (int64_t)hist[(int64_t)dd[r] * ntiles + blockIdx.x] + wc[w][dd[r]] + loc[r];
       kout[pos] = kk[r];
       vout[pos] = vv[r];
@@ -146,35 +148,37 @@ __global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const uint32_t* __
 
 size_t sort_scratch_bytes(int64_t n) {
   const int64_t ntiles = (n + kRsTile - 1) / kRsTile;
-  return sizeof(int32_t) * (kRsBins * ntiles + 1) + scan_scratch_bytes(kRsBins * ntiles) +
+  return sizeof(int32_t) * (kRsMaxBins * ntiles + 1) + scan_scratch_bytes(kRsMaxBins * ntiles) +
          2 * n * sizeof(int32_t) + 64;
 }
 
-// keys_out/vals_out receive the sorted pairs; inputs are left untouched.
+// Stable sort of (key, value) pairs by the low `key_bits` bits of the key.
+// vals_in == NULL sorts the positions 0..n-1 (an argsort). Inputs are untouched.
 int radix_sort_pairs(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* keys_out, int32_t* vals_out,
                      int64_t n, int key_bits, void* scratch, cudaStream_t st) {
   if (n <= 0) return FC_OK;
   const int ntiles = (int)((n + kRsTile - 1) / kRsTile);
   char* p = static_cast<char*>(scratch);
   int32_t* hist = reinterpret_cast<int32_t*>(p);
-  p += sizeof(int32_t) * ((int64_t)kRsBins * ntiles + 1);
+  p += sizeof(int32_t) * ((int64_t)kRsMaxBins * ntiles + 1);
   void* scan_scr = p;
-  p += scan_scratch_bytes(kRsBins * ntiles);
+  p += scan_scratch_bytes(kRsMaxBins * ntiles);
   p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
   uint32_t* ktmp = reinterpret_cast<uint32_t*>(p);
   int32_t* vtmp = reinterpret_cast<int32_t*>(p + n * sizeof(int32_t));
-  const int passes = std::max(1, (key_bits + 7) / 8);
-  // ping-pong so that the last pass lands in (keys_out, vals_out)
+  const int passes = std::max(1, (key_bits + 8) / 9);
+  const int dbits = std::max(1, (key_bits + passes - 1) / passes);
+  const int bins = 1 << dbits;
   const uint32_t* ks = keys_in;
   const int32_t* vs = vals_in;
   for (int pass = 0; pass < passes; ++pass) {
-    const bool to_out = ((passes - 1 - pass) % 2) == 0;
+    const bool to_out = ((passes - 1 - pass) % 2) == 0;  // last pass lands in the outputs
     uint32_t* kd = to_out ? keys_out : ktmp;
     int32_t* vd = to_out ? vals_out : vtmp;
-    k_rs_hist<<<ntiles, kRsWarps * 32, 0, st>>>(ks, n, pass * 8, hist, ntiles);
-    int rc = exclusive_scan_i32(hist, hist, (int64_t)kRsBins * ntiles, scan_scr, st);
+    k_rs_hist<<<ntiles, kRsWarps * 32, 0, st>>>(ks, n, pass * dbits, bins, hist, ntiles);
+    int rc = exclusive_scan_i32(hist, hist, (int64_t)bins * ntiles, scan_scr, st);
     if (rc) return rc;
-    k_rs_scatter<<<ntiles, kRsWarps * 32, 0, st>>>(ks, vs, kd, vd, n, pass * 8, hist, ntiles);
+    k_rs_scatter<<<ntiles, kRsWarps * 32, 0, st>>>(ks, vs, kd, vd, n, pass * dbits, bins, hist, ntiles);
     ks = kd;
     vs = vd;
   }

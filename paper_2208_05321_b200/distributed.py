@@ -1,0 +1,281 @@
+"""Multi-GPU cached embedding: one process per GPU, NCCL over NVLink/NVSwitch.
+
+Two shardings, both with one device cache per rank:
+
+* `ColumnShardedEmbedding` — the reference's semantics (sharding.py:1-10, 62-118):
+  every rank holds all rows of a contiguous column slice (`partition_columns`) and
+  runs its own cache over the GLOBAL batch, so residency decisions are identical on
+  every rank and the concatenation over ranks equals the unsharded lookup bitwise.
+  Exchanges: all-gather of the batch ids, then all-to-all of pooled activations
+  [bags_global, D/N] -> [bags_local, D] (sharding.py:121-146 accounts exactly these
+  bytes); the backward is the mirror all-to-all of gradients.
+* `RowShardedEmbedding` — the scaling variant: rows are owned by rank id % N, each
+  rank caches only its shard (its own frequency reorder over its id substream), ids
+  travel to their owner by all-to-all and rows come back the same way. Index work
+  is partitioned as well as row traffic, so lookups/s scale with N.
+
+The per-rank compute is a `shard` object (`CudaShard` below wraps a DeviceCache and
+libfreqcache_b200); the exchange logic is backend-agnostic torch.distributed code,
+which the CPU tests run over gloo with an oracle shard.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from .device import DeviceCache
+from .freq_stats import IdxMap
+from .sharding import partition_columns
+from .store import fast_capacity, pinned_empty
+
+
+class CudaShard:
+    """One rank's slice of the table behind a device cache."""
+
+    def __init__(self, num_rows: int, dim: int, capacity: int, rows_rank_order: np.ndarray, idx_map: IdxMap,
+                 optimizer: str = "sgd", lr: float = 0.01, eps: float = 1e-10, buffer_bytes: int = 64 * 2**20,
+                 warmup: bool = True, device=None):
+        sw = dim if optimizer == "adagrad" else 0
+        self.cache = DeviceCache(num_rows, capacity, dim, state_width=sw, buffer_bytes=buffer_bytes, device=device)
+        self.cache.set_idx_map(idx_map.rank_of)
+        self.rows = rows_rank_order
+        self.state = None
+        if sw:
+            self.state = pinned_empty((num_rows, sw))
+            self.state.fill(0.0)
+        self.cache.attach_slow(self.rows, self.state)
+        self.idx_map = idx_map
+        self.dim, self.optimizer, self.lr, self.eps = dim, optimizer, lr, eps
+        self.device = self.cache.device
+        if warmup:
+            self.cache.warmup(capacity)
+
+    def prepare(self, ids):
+        info, uids, ucnt, uranks, uslots, inverse, _ = self.cache.prepare(ids)
+        return {"info": info, "uslots": uslots, "inverse": inverse, "ucnt": ucnt, "n": int(inverse.numel())}
+
+    def pool(self, h, offsets=None, n_bags=None, include_last_offset=False, psw=None, mode="sum"):
+        return self.cache.pooled(h["uslots"], h["inverse"], h["n"], offsets, n_bags, include_last_offset, psw, mode)
+
+    def backward(self, h, grad, offsets=None, n_bags=None, include_last_offset=False, psw=None, mode="sum"):
+        if h["n"] == 0:
+            return
+        nb = h["n"] if offsets is None else n_bags
+        self.cache.backward_update(h["uslots"], h["inverse"], h["ucnt"], offsets, nb, include_last_offset, psw, mode,
+                                   grad.contiguous(), self.optimizer, self.lr, self.eps)
+
+    def flush(self) -> int:
+        return self.cache.flush()
+
+
+# ----------------------------------------------------------------------------- helpers
+def _a2a(out, inp, out_splits, in_splits, group=None):
+    dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+    return out
+
+
+def bag_grads(grad_out, n, offsets, n_bags, include_last_offset, psw, mode):
+    """Per-occurrence gradient rows grad_out[bag(j)] * coef_j (coef = psw_j, / L for mean)."""
+    if offsets is None:
+        g = grad_out
+        if psw is not None:
+            g = g * psw.reshape(-1, 1)
+        return g
+    off = offsets.long()
+    ends = torch.cat([off[1:], off.new_tensor([n])]) if not include_last_offset else off[1:]
+    starts = off if not include_last_offset else off[:-1]
+    lens = ends - starts
+    bag_of = torch.repeat_interleave(torch.arange(n_bags, device=grad_out.device), lens)
+    pos = torch.arange(bag_of.numel(), device=grad_out.device) - torch.repeat_interleave(
+        torch.cumsum(lens, 0) - lens, lens) + torch.repeat_interleave(starts, lens)
+    coef = torch.ones(bag_of.numel(), device=grad_out.device, dtype=grad_out.dtype)
+    if mode == "mean":
+        coef = coef / lens[bag_of].to(coef.dtype)
+    if psw is not None:
+        coef = coef * psw[pos]
+    g = torch.zeros((n, grad_out.shape[1]), device=grad_out.device, dtype=grad_out.dtype)
+    g[pos] = grad_out[bag_of] * coef.unsqueeze(1)
+    return g
+
+
+def pool_rows(rows, offsets, n_bags, include_last_offset, psw, mode):
+    """EmbeddingBag pooling of per-occurrence rows already gathered in batch order."""
+    n = rows.shape[0]
+    if offsets is None:
+        return rows if psw is None else rows * psw.reshape(-1, 1)
+    r = rows if psw is None else rows * psw.reshape(-1, 1)
+    off = offsets.long()
+    out = torch.nn.functional.embedding_bag(torch.arange(n, device=rows.device), r, off, mode="sum",
+                                            include_last_offset=include_last_offset)
+    if mode == "mean":
+        out = out / _lens(off, n, include_last_offset).clamp(min=1).unsqueeze(1).to(rows.dtype)
+    return out
+
+
+def _lens(offsets, n, include_last_offset):
+    off = offsets.long()
+    if include_last_offset:
+        return off[1:] - off[:-1]
+    return torch.cat([off[1:], off.new_tensor([n])]) - off
+
+
+# ----------------------------------------------------------------------------- row-wise (scaling)
+class _RowShardFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, anchor, mod, ids, offsets, n_bags, psw):
+        out, saved = mod._forward(ids, offsets, n_bags, psw)
+        ctx.mod, ctx.saved = mod, saved
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        ctx.mod._backward(ctx.saved, grad_out)
+        return None, None, None, None, None, None
+
+
+class RowShardedEmbedding(torch.nn.Module):
+    """Rows owned by rank `id % world`; ids and rows exchanged with all-to-all."""
+
+    def __init__(self, shard, world: int, rank: int, mode: str = "sum", include_last_offset: bool = False,
+                 group=None, device=None):
+        super().__init__()
+        self.shard, self.world, self.rank = shard, world, rank
+        self.mode, self.include_last_offset, self.group = mode, include_last_offset, group
+        self.device = device if device is not None else getattr(shard, "device", torch.device("cpu"))
+        self._anchor = torch.nn.Parameter(torch.empty(0, device=self.device))
+        self.last_recv = 0
+
+    @staticmethod
+    def owner_of(ids, world):
+        return ids % world, ids // world
+
+    def _forward(self, ids, offsets, n_bags, psw):
+        W = self.world
+        owner, local = self.owner_of(ids.long(), W)
+        order = torch.argsort(owner, stable=True)
+        send_ids = local[order]
+        send_counts = torch.bincount(owner, minlength=W)
+        recv_counts = torch.empty_like(send_counts)
+        _a2a(recv_counts, send_counts, None, None, self.group)
+        sc, rc = send_counts.tolist(), recv_counts.tolist()
+        recv_ids = torch.empty(sum(rc), dtype=send_ids.dtype, device=send_ids.device)
+        _a2a(recv_ids, send_ids, rc, sc, self.group)
+        self.last_recv = int(recv_ids.numel())
+        h = self.shard.prepare(recv_ids)
+        rows = self.shard.pool(h)  # [n_recv, D] one row per received id
+        back = torch.empty((ids.numel(), rows.shape[1]), dtype=rows.dtype, device=rows.device)
+        _a2a(back, rows.contiguous(), sc, rc, self.group)
+        local_rows = torch.empty_like(back)
+        local_rows[order] = back
+        out = pool_rows(local_rows, offsets, n_bags, self.include_last_offset, psw, self.mode)
+        return out, (h, order, sc, rc, int(ids.numel()), offsets, n_bags, psw)
+
+    def _backward(self, saved, grad_out):
+        h, order, sc, rc, n, offsets, n_bags, psw = saved
+        g = bag_grads(grad_out, n, offsets, n_bags, self.include_last_offset, psw, self.mode)
+        g_send = g[order].contiguous()
+        g_recv = torch.empty((sum(rc), g.shape[1]), dtype=g.dtype, device=g.device)
+        _a2a(g_recv, g_send, rc, sc, self.group)
+        self.shard.backward(h, g_recv)
+
+    def forward(self, ids, offsets=None, per_sample_weights=None):
+        ids = ids.reshape(-1).to(self.device)
+        n_bags = ids.numel() if offsets is None else offsets.numel() - (1 if self.include_last_offset else 0)
+        return _RowShardFn.apply(self._anchor, self, ids, offsets, n_bags, per_sample_weights)
+
+
+# ----------------------------------------------------------------------------- column-wise (reference semantics)
+class _ColShardFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, anchor, mod, ids, offsets, n_bags, psw):
+        out, saved = mod._forward(ids, offsets, n_bags, psw)
+        ctx.mod, ctx.saved = mod, saved
+        return out
+
+    @staticmethod
+    def backward(ctx, grad_out):
+        ctx.mod._backward(ctx.saved, grad_out)
+        return None, None, None, None, None, None
+
+
+class ColumnShardedEmbedding(torch.nn.Module):
+    """Rank r caches columns partition_columns(D, world).ranges[r] of every row."""
+
+    def __init__(self, shard, dim: int, world: int, rank: int, mode: str = "sum", group=None, device=None):
+        super().__init__()
+        self.shard, self.dim, self.world, self.rank = shard, dim, world, rank
+        self.plan = partition_columns(dim, world)
+        self.widths = self.plan.widths
+        self.mode, self.group = mode, group
+        self.device = device if device is not None else getattr(shard, "device", torch.device("cpu"))
+        self._anchor = torch.nn.Parameter(torch.empty(0, device=self.device))
+
+    def _gather_var(self, x, counts, maxn):
+        """all-gather of per-rank 1-D tensors of different lengths (padded to maxn)."""
+        pad = torch.zeros(maxn, dtype=x.dtype, device=x.device)
+        pad[:x.numel()] = x
+        g = torch.empty(self.world * maxn, dtype=x.dtype, device=x.device)
+        dist.all_gather_into_tensor(g, pad, group=self.group)
+        if all(c == maxn for c in counts):
+            return g
+        return torch.cat([g[r * maxn:r * maxn + c] for r, c in enumerate(counts)])
+
+    def _forward(self, ids, offsets, n_bags, psw):
+        W, n = self.world, ids.numel()
+        cnt = torch.tensor([n], dtype=torch.int64, device=ids.device)
+        all_n = torch.empty(W, dtype=torch.int64, device=ids.device)
+        dist.all_gather_into_tensor(all_n, cnt, group=self.group)
+        counts = all_n.tolist()
+        maxn = max(counts)
+        g_ids = self._gather_var(ids.contiguous(), counts, maxn)
+        g_off, g_psw = None, None
+        if offsets is not None:  # every rank has n_bags bags; shift offsets by the ids before it
+            g_off = torch.empty(W * n_bags, dtype=offsets.dtype, device=offsets.device)
+            dist.all_gather_into_tensor(g_off, offsets[:n_bags].contiguous(), group=self.group)
+            base = torch.tensor(np.concatenate([[0], np.cumsum(counts)[:-1]]), dtype=offsets.dtype,
+                                device=offsets.device)
+            g_off += base.repeat_interleave(n_bags)
+        if psw is not None:
+            g_psw = self._gather_var(psw.contiguous(), counts, maxn)
+        h = self.shard.prepare(g_ids)  # identical decisions on every rank
+        pooled = self.shard.pool(h, g_off, W * n_bags, False, g_psw, self.mode)  # [W*n_bags, w_r]
+        w_r = self.widths[self.rank]
+        recv = torch.empty(sum(n_bags * w for w in self.widths), dtype=pooled.dtype, device=pooled.device)
+        _a2a(recv, pooled.reshape(-1).contiguous(), [n_bags * w for w in self.widths], [n_bags * w_r] * W, self.group)
+        parts = torch.split(recv, [n_bags * w for w in self.widths])
+        out = torch.cat([p.reshape(n_bags, w) for p, w in zip(parts, self.widths)], dim=1)
+        return out, (h, g_off, n_bags, g_psw)
+
+    def _backward(self, saved, grad_out):
+        h, g_off, n_bags, g_psw = saved
+        W, w_r = self.world, self.widths[self.rank]
+        send = torch.cat([grad_out[:, a:b].reshape(-1) for a, b in self.plan.ranges]).contiguous()
+        recv = torch.empty(W * n_bags * w_r, dtype=grad_out.dtype, device=grad_out.device)
+        _a2a(recv, send, [n_bags * w_r] * W, [n_bags * w for w in self.widths], self.group)
+        self.shard.backward(h, recv.reshape(W * n_bags, w_r), g_off, W * n_bags, False, g_psw, self.mode)
+
+    def forward(self, ids, offsets=None, per_sample_weights=None):
+        ids = ids.reshape(-1).to(self.device)
+        n_bags = ids.numel() if offsets is None else offsets.numel()
+        return _ColShardFn.apply(self._anchor, self, ids, offsets, n_bags, per_sample_weights)
+
+
+# ----------------------------------------------------------------------------- builders
+def shard_rows_for_rank(counts: np.ndarray, rank: int, world: int):
+    """Local id space of a row shard (ids with id % world == rank) and its frequency reorder."""
+    local_counts = counts[rank::world]
+    id_of = np.argsort(-local_counts, kind="stable").astype(np.int64)
+    rank_of = np.empty_like(id_of)
+    rank_of[id_of] = np.arange(id_of.size, dtype=np.int64)
+    return IdxMap(rank_of=rank_of, id_of=id_of)
+
+
+def build_row_sharded(num_ids, dim, cache_ratio, counts, rank, world, init_rows_fn, **kw):
+    """CudaShard for this rank's rows; `init_rows_fn(global_ids) -> rows` seeds values."""
+    idx = shard_rows_for_rank(counts, rank, world)
+    n_local = idx.num_ids
+    rows = pinned_empty((n_local, dim))
+    rows[...] = init_rows_fn(rank + world * idx.id_of)
+    return CudaShard(n_local, dim, fast_capacity(n_local, cache_ratio), rows, idx, **kw)

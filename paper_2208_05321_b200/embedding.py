@@ -65,7 +65,8 @@ class CachedEmbeddingBag(torch.nn.Module):
     def __init__(self, num_embeddings: int, embedding_dim: int, cache_ratio: float = 0.015, *, mode: str = "sum",
                  include_last_offset: bool = False, weight: np.ndarray | None = None, init_seed: int = 0,
                  idx_map: IdxMap | None = None, optimizer: str = "sgd", lr: float = 0.01, eps: float = 1e-10,
-                 buffer_bytes: int = 64 * 2**20, write_back: str = "dirty_only", warmup: bool = True, device=None):
+                 buffer_bytes: int = 64 * 2**20, write_back: str = "dirty_only", warmup: bool = True, device=None,
+                 slow_rows: np.ndarray | None = None):
         super().__init__()
         if mode not in ("sum", "mean"):
             raise ValueError("mode must be 'sum' or 'mean'")
@@ -83,10 +84,15 @@ class CachedEmbeddingBag(torch.nn.Module):
         self.cache = DeviceCache(num_embeddings, self.capacity, embedding_dim, state_width=sw, write_back=write_back,
                                  buffer_bytes=buffer_bytes, device=device)
         self.cache.set_idx_map(idx_map.rank_of)
-        rows = pinned_empty((num_embeddings, embedding_dim))
-        if weight is None:
-            weight = init_reference_rows(num_embeddings, embedding_dim, init_seed)
-        np.take(np.asarray(weight, dtype=np.float32), idx_map.id_of, axis=0, out=rows)  # rank order
+        if slow_rows is not None:  # caller-provided pinned rows, already in rank order
+            if slow_rows.shape != (num_embeddings, embedding_dim):
+                raise ValueError("slow_rows must be [num_embeddings, embedding_dim] in rank order")
+            rows = slow_rows
+        else:
+            rows = pinned_empty((num_embeddings, embedding_dim))
+            if weight is None:
+                weight = init_reference_rows(num_embeddings, embedding_dim, init_seed)
+            np.take(np.asarray(weight, dtype=np.float32), idx_map.id_of, axis=0, out=rows)  # rank order
         self.slow_rows = rows
         self.slow_state = None
         if sw:
