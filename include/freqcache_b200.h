@@ -103,10 +103,23 @@ int fc_set_modes(fc_cache* h, int32_t write_back, int32_t evict_mode);
 /* CacheState.free_count after the last synchronising call. */
 int64_t fc_free_count(fc_cache* h);
 
+/* Transfer engine. 0 (default): one kernel pairs each staged victim write-back
+ * (HBM -> pinned slow tier) with an admission (slow tier -> slot), all SM-issued
+ * over the host link; the slow tier is current when prepare returns.
+ * 1: victims are staged in HBM (double-buffered) and shipped D2H by the copy
+ * engine on a side stream, then scattered into the slow tier by host threads,
+ * overlapped with later work; admissions read the newest copy (HBM stage if the
+ * rank is still pending). The slow tier is current after fc_flush / fc_drain. */
+int fc_set_engine(fc_cache* h, int32_t engine);
+int fc_drain(fc_cache* h);
+
 /* Measurement hook (no reference counterpart): with enable=1 every prepare records
  * CUDA events around the whole call and around the host-link transfer kernel.
- * out[0..3] (returned, then reset): sum prepare ms, sum transfer-kernel ms,
- * calls, host-link bytes moved (4*dim*(admitted + written-back rows)). */
+ * out[0..4] (returned, then reset): sum prepare ms, sum transfer-kernel ms,
+ * calls, bytes the transfer kernel moved over the host link (4*dim*(admitted +
+ * written-back rows) for engine 0, admitted rows only for engine 1),
+ * written-back bytes, host ms spent waiting for async write-backs (engine 1),
+ * host scatter ms and scatter jobs completed (engine 1). `out` holds 8 doubles. */
 int fc_profile(fc_cache* h, int32_t enable, double* out);
 
 /* ---- the cache verbs ------------------------------------------------------- */

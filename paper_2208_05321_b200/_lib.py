@@ -56,6 +56,8 @@ _SIGS = {
     "fc_set_modes": (c_int32, [c_void_p, c_int32, c_int32]),
     "fc_free_count": (c_int64, [c_void_p]),
     "fc_profile": (c_int32, [c_void_p, c_int32, c_void_p]),
+    "fc_set_engine": (c_int32, [c_void_p, c_int32]),
+    "fc_drain": (c_int32, [c_void_p]),
     "fc_warmup": (c_int32, [c_void_p, c_int64, c_void_p]),
     "fc_prepare": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                              c_void_p, c_void_p, c_void_p, POINTER(PrepareInfo)]),

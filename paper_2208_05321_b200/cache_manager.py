@@ -101,7 +101,8 @@ class CacheState:
 
     # -- binding ------------------------------------------------------------
     def bind(self, idx_map: IdxMap, slow: SlowTierStore, fast: FastTierStore, transmitter: Transmitter,
-             write_back: str = "dirty_only", evict_mode: str = "occupancy_aware", device=None) -> DeviceCache:
+             write_back: str = "dirty_only", evict_mode: str = "occupancy_aware", device=None,
+             engine: str = "zerocopy") -> DeviceCache:
         """Create the device cache for this state and move the tiers into place:
         slow rows pinned + mapped, fast rows copied into HBM (FastTierStore.slots
         becomes a CUDA tensor view)."""
@@ -114,6 +115,8 @@ class CacheState:
         dev.set_idx_map(idx_map.rank_of)
         slow.pin()
         dev.attach_slow(slow.rows)
+        if engine != "zerocopy":
+            dev.set_engine(engine)
         init = fast.slots
         if isinstance(init, np.ndarray):
             if np.any(init):
@@ -388,7 +391,7 @@ class CacheStack:
     def __init__(self, idx_map: IdxMap, slow: SlowTierStore, fast: FastTierStore, transmitter: Transmitter,
                  reference: ReferenceStore | None = None, policy=None, write_back: str = "dirty_only",
                  evict_mode: str = "occupancy_aware", log_events: bool = False, col_range: tuple | None = None,
-                 device=None):
+                 device=None, engine: str = "zerocopy"):
         if slow.embedding_dim != fast.embedding_dim:
             raise ValueError("slow and fast tier column widths differ")
         if write_back not in WRITE_BACK_MODES:
@@ -406,7 +409,9 @@ class CacheStack:
         self.events: list[CacheEvent] | None = [] if log_events else None
         self.col_range = col_range if col_range is not None else (0, slow.embedding_dim)
         self.state = CacheState(fast.capacity, idx_map.num_ids)
-        self.device = self.state.bind(idx_map, slow, fast, transmitter, write_back, evict_mode, device)
+        # engine "zerocopy": the slow tier is current after every prepare (reference semantics);
+        # "async": write-backs land later, the slow tier is current after flush()
+        self.device = self.state.bind(idx_map, slow, fast, transmitter, write_back, evict_mode, device, engine)
         self._colw = {}
 
     @property

@@ -64,6 +64,7 @@ static int dalloc(T** p, size_t count) {
 }
 
 static void release(fc_cache* h) {
+  engine_release(h);
   void* dev[] = {h->rank_of, h->rank_to_slot, h->slot_to_rank, h->dirty, h->fast, h->fast_state,
                  h->res_bits, h->free_bits, h->id_bits, h->miss_bits, h->prot_bits, h->aux,
                  h->evicted_ranks, h->victim_slots, h->wb_ranks, h->wb_stage, h->wb_stage_state,
@@ -229,6 +230,18 @@ int fc_set_modes(fc_cache* h, int32_t write_back, int32_t evict_mode) {
 
 int64_t fc_free_count(fc_cache* h) { return h ? h->host_free : -1; }
 
+int fc_set_engine(fc_cache* h, int32_t engine) {
+  if (!h) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  return engine_set(h, engine);
+}
+
+int fc_drain(fc_cache* h) {
+  if (!h) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  return engine_drain(h);
+}
+
 int fc_set_idx_map(fc_cache* h, const int64_t* rank_of_host, void* stream) {
   if (!h || !rank_of_host) return FC_ERR_BAD_ARG;
   DeviceGuard dg(h->device);
@@ -258,6 +271,7 @@ int fc_attach_slow_tier(fc_cache* h, float* rows_host, int64_t row_stride, float
     return FC_ERR_BAD_ARG;
   }
   h->slow = static_cast<float*>(dptr);
+  h->slow_host = rows_host;
   h->slow_ld = row_stride;
   if (h->sw) {
     if (!state_host || state_stride < h->sw) {
@@ -271,6 +285,7 @@ int fc_attach_slow_tier(fc_cache* h, float* rows_host, int64_t row_stride, float
       return FC_ERR_BAD_ARG;
     }
     h->slow_state = static_cast<float*>(dptr);
+    h->slow_state_host = state_host;
     h->state_ld = state_stride;
   }
   return FC_OK;
@@ -314,8 +329,10 @@ int fc_prepare(fc_cache* h, const void* ids, int32_t ids_bytes, int64_t n, int64
   if (!h->slow) return FC_ERR_NO_SLOW_TIER;
   DeviceGuard dg(h->device);
   cudaStream_t st = as_stream(stream);
+  FC_TRY(engine_begin(h, st));
   FC_TRY(launch_prepare(h, ids, ids_bytes, n, uids, ucnt, uranks, uslots, inverse, st));
   FC_TRY(sync_counters(h, st));
+  FC_TRY(engine_after_prepare(h, st));
   const Counters& c = *h->ctr_host;
   info->unique = c.unique;
   info->free_count = c.free_count;
@@ -360,7 +377,10 @@ int fc_prepare(fc_cache* h, const void* ids, int32_t ids_bytes, int64_t n, int64
     h->prof[0] += a;
     h->prof[1] += b;
     h->prof[2] += 1;
-    h->prof[3] += 4.0 * h->dim * ((double)c.misses + c.wb_rows);
+    // bytes the bracketed kernel moves over the host link: both directions for the
+    // paired engine 0; admissions only for engine 1 (its write-back rides the copy engine)
+    h->prof[3] += 4.0 * h->dim * ((double)c.misses + (h->engine == 1 ? 0 : c.wb_rows));
+    h->prof[4] += 4.0 * h->dim * (double)c.wb_rows;
   }
   return FC_OK;
 }
@@ -368,8 +388,10 @@ int fc_prepare(fc_cache* h, const void* ids, int32_t ids_bytes, int64_t n, int64
 int fc_profile(fc_cache* h, int32_t enable, double* out) {
   if (!h) return FC_ERR_BAD_ARG;
   DeviceGuard dg(h->device);
-  if (out)
-    for (int i = 0; i < 4; ++i) out[i] = h->prof[i];
+  if (out) {
+    for (int i = 0; i < 6; ++i) out[i] = h->prof[i];
+    engine_stats(h, out + 6);
+  }
   if (enable && !h->profile) {
     for (int i = 0; i < 4; ++i) FC_CUDA(cudaEventCreate(&h->pev[i]));
   }
@@ -399,6 +421,7 @@ int fc_flush(fc_cache* h, void* stream, int64_t* rows_written) {
   if (!h->slow) return FC_ERR_NO_SLOW_TIER;
   DeviceGuard dg(h->device);
   cudaStream_t st = as_stream(stream);
+  FC_TRY(engine_drain(h));  // queued write-backs land before flush's own
   FC_TRY(launch_reset_counters(h, st));
   FC_TRY(launch_flush(h, st));
   FC_TRY(sync_counters(h, st));

@@ -383,7 +383,7 @@ int launch_prepare(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32
 
   compact(CandWords{h->res_bits, h->prot_bits}, EvictFin{}, EvictEmit{h->evicted_ranks, 0}, h->nw_ids, h->block_cnt,
           win_evict(c), c, G_EVICT, st);
-  int rc = launch_evict_rows(h, st);
+  int rc = h->engine == 1 ? engine_evict(h, st) : launch_evict_rows(h, st);
   if (rc) return rc;
 
   compact(ArrWords{h->miss_bits}, AdmitFin{}, RankEmit{h->admitted_ranks}, h->nw_ids, h->block_cnt,
@@ -391,7 +391,7 @@ int launch_prepare(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32
   compact(ArrWords{h->free_bits}, FreeFin{}, RankEmit{h->target_slots}, h->nw_slots, h->block_cnt2,
           win_admit(c), c, G_ADMIT, st);
   if (h->profile) cudaEventRecord(h->pev[1], st);
-  rc = launch_transfer_rows(h, st);
+  rc = h->engine == 1 ? engine_admit(h, st) : launch_transfer_rows(h, st);
   if (rc) return rc;
   if (h->profile) cudaEventRecord(h->pev[2], st);
 

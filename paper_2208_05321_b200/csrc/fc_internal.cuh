@@ -54,6 +54,8 @@ struct Counters {
   int32_t bad_slot;
 };
 
+struct AsyncWB;  // async write-back engine state (fc_engine.cu)
+
 }  // namespace fc
 
 struct fc_cache {
@@ -98,10 +100,12 @@ struct fc_cache {
   void* scratch;
   size_t scratch_bytes;
 
-  float* slow;              // host rows (device-mapped)
+  float* slow;              // slow tier rows, device-mapped pointer
   int64_t slow_ld;
   float* slow_state;
   int64_t state_ld;
+  float* slow_host;         // the same rows, host pointer (host-side scatter)
+  float* slow_state_host;
 
   int32_t last_needed;
   int32_t last_misses;
@@ -111,7 +115,23 @@ struct fc_cache {
   int profile;
   cudaEvent_t pev[4];
   double prof[6];           // prepare_ms, xfer_ms, calls, host-link bytes, evict_ms, index_ms
+
+  // async write-back engine (fc_engine.cu); engine 0 = paired zero-copy kernel
+  int engine;
+  fc::AsyncWB* awb;
 };
+
+namespace fc {
+// engine hooks (fc_engine.cu)
+int engine_set(fc_cache* h, int engine);
+int engine_begin(fc_cache* h, cudaStream_t st);              // before a prepare's kernels
+int engine_evict(fc_cache* h, cudaStream_t st);              // replaces k_evict_rows
+int engine_admit(fc_cache* h, cudaStream_t st);              // replaces k_transfer_rows
+int engine_after_prepare(fc_cache* h, cudaStream_t st);      // after the prepare's sync
+int engine_drain(fc_cache* h);                               // all write-backs landed in the slow tier
+void engine_release(fc_cache* h);
+void engine_stats(fc_cache* h, double* out);                 // host scatter ms, jobs (then reset)
+}  // namespace fc
 
 namespace fc {
 

@@ -91,11 +91,22 @@ class DeviceCache:
     def free_count(self) -> int:
         return int(self.lib.fc_free_count(self.h))
 
+    def set_engine(self, engine: str) -> None:
+        """'zerocopy' (paired SM-issued transfers, slow tier current after every prepare)
+        or 'async' (copy-engine write-back + host scatter; current after flush/drain)."""
+        check(self.lib.fc_set_engine(self.h, {"zerocopy": 0, "async": 1}[engine]))
+        self.engine = engine
+
+    def drain(self) -> None:
+        """Wait until every queued write-back has landed in the slow tier."""
+        check(self.lib.fc_drain(self.h))
+
     def profile(self, enable: bool) -> dict:
         """Toggle per-kernel CUDA-event timing; returns (and resets) the totals so far."""
-        out = (ctypes.c_double * 4)()
+        out = (ctypes.c_double * 8)()
         check(self.lib.fc_profile(self.h, int(bool(enable)), out))
-        return {"prepare_ms": out[0], "transfer_ms": out[1], "calls": int(out[2]), "host_link_bytes": out[3]}
+        return {"prepare_ms": out[0], "transfer_ms": out[1], "calls": int(out[2]), "host_link_bytes": out[3],
+                "writeback_bytes": out[4], "host_wait_ms": out[5], "scatter_ms": out[6], "scatter_jobs": int(out[7])}
 
     def to_device_ids(self, ids):
         """Accept numpy / list / torch ids; return a contiguous CUDA int64/int32 tensor."""

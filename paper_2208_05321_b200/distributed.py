@@ -36,7 +36,7 @@ class CudaShard:
 
     def __init__(self, num_rows: int, dim: int, capacity: int, rows_rank_order: np.ndarray, idx_map: IdxMap,
                  optimizer: str = "sgd", lr: float = 0.01, eps: float = 1e-10, buffer_bytes: int = 64 * 2**20,
-                 warmup: bool = True, device=None):
+                 warmup: bool = True, device=None, engine: str = "async"):
         sw = dim if optimizer == "adagrad" else 0
         self.cache = DeviceCache(num_rows, capacity, dim, state_width=sw, buffer_bytes=buffer_bytes, device=device)
         self.cache.set_idx_map(idx_map.rank_of)
@@ -46,6 +46,7 @@ class CudaShard:
             self.state = pinned_empty((num_rows, sw))
             self.state.fill(0.0)
         self.cache.attach_slow(self.rows, self.state)
+        self.cache.set_engine(engine)
         self.idx_map = idx_map
         self.dim, self.optimizer, self.lr, self.eps = dim, optimizer, lr, eps
         self.device = self.cache.device

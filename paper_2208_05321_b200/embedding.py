@@ -60,13 +60,16 @@ class CachedEmbeddingBag(torch.nn.Module):
         idx_map: frequency reorder (build_reorder(scan_frequencies(trace))); default identity.
         optimizer: "sgd" or "adagrad" (fused into backward), lr, eps.
         warmup: pre-fill the cache with the hottest rows (ranks 0..C-1).
+        slow_rows: optional pinned host rows already in rank order (fc_host_alloc / pinned_empty).
+        engine: "async" (write-backs ride the copy engine and host threads, off the
+            critical path; the table is current after flush()) or "zerocopy".
     """
 
     def __init__(self, num_embeddings: int, embedding_dim: int, cache_ratio: float = 0.015, *, mode: str = "sum",
                  include_last_offset: bool = False, weight: np.ndarray | None = None, init_seed: int = 0,
                  idx_map: IdxMap | None = None, optimizer: str = "sgd", lr: float = 0.01, eps: float = 1e-10,
                  buffer_bytes: int = 64 * 2**20, write_back: str = "dirty_only", warmup: bool = True, device=None,
-                 slow_rows: np.ndarray | None = None):
+                 slow_rows: np.ndarray | None = None, engine: str = "async"):
         super().__init__()
         if mode not in ("sum", "mean"):
             raise ValueError("mode must be 'sum' or 'mean'")
@@ -99,6 +102,7 @@ class CachedEmbeddingBag(torch.nn.Module):
             self.slow_state = pinned_empty((num_embeddings, sw))
             self.slow_state.fill(0.0)
         self.cache.attach_slow(self.slow_rows, self.slow_state)
+        self.cache.set_engine(engine)
         if warmup:
             self.cache.warmup(self.capacity)
         self._anchor = torch.nn.Parameter(torch.empty(0, device=self.cache.device), requires_grad=True)

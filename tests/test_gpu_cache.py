@@ -309,12 +309,15 @@ def test_golden_sharded_lookup():
 
 # ---------------- randomized parity at larger sizes against the oracle ------
 
-@pytest.mark.parametrize("num_ids,cap,dim,nb,bsz,always", [
-    (50_000, 3_000, 32, 40, 2_000, False),
-    (200_000, 12_000, 128, 12, 9_000, True),
-    (7_001, 700, 12, 30, 500, False),
+@pytest.mark.parametrize("num_ids,cap,dim,nb,bsz,always,engine", [
+    (50_000, 3_000, 32, 40, 2_000, False, "zerocopy"),
+    (200_000, 12_000, 128, 12, 9_000, True, "zerocopy"),
+    (7_001, 700, 12, 30, 500, False, "zerocopy"),
+    (50_000, 3_000, 32, 40, 2_000, False, "async"),
+    (200_000, 12_000, 128, 12, 9_000, True, "async"),
+    (3_000, 400, 16, 60, 350, False, "async"),  # tiny cache: ranks bounce out and back in while pending
 ])
-def test_random_parity_vs_oracle(num_ids, cap, dim, nb, bsz, always):
+def test_random_parity_vs_oracle(num_ids, cap, dim, nb, bsz, always, engine):
     rng = np.random.default_rng(num_ids)
     p = 1.0 / np.arange(1, num_ids + 1) ** 1.05
     perm = rng.permutation(num_ids)
@@ -326,7 +329,8 @@ def test_random_parity_vs_oracle(num_ids, cap, dim, nb, bsz, always):
     orc = oracle.OracleCache(rank_of, ref[id_of].copy(), cap, write_back=wb, buffer_bytes=1 << 16)
     st = fc.CacheStack(fc.IdxMap(rank_of, id_of), fc.SlowTierStore(ref[id_of].copy()),
                        fc.FastTierStore(np.zeros((cap, dim), np.float32)),
-                       fc.Transmitter(buffer=fc.TransferBuffer(1 << 16)), write_back=wb, log_events=True)
+                       fc.Transmitter(buffer=fc.TransferBuffer(1 << 16)), write_back=wb, log_events=True,
+                       engine=engine)
     orc.warmup(cap // 2)
     st.warmup(cap // 2)
     colw = oracle.column_weights(dim, 9)
