@@ -32,6 +32,10 @@ import time
 
 import numpy as np
 
+# more hardware work queues than torch's/the library's streams: no false dependencies
+# between the index, transfer, copy-engine and compute streams (set before CUDA init)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -48,6 +52,9 @@ KERNELS_PER_STEP = 20 + 1 + 1  # sim step: prepare sequence + pooled forward + f
 # train step: prepare (20) + pooled forward (1) + backward: 2 radix passes x (hist + 3-kernel scan + scatter),
 # segmented stream, carry fix-up, optimizer apply
 KERNELS_PER_TRAIN_STEP = 20 + 1 + (2 * 5 + 3)
+# prefetch pipeline: index phase adds k_evict_state + k_admit_state; rows move in
+# k_admit_stage (transfer stream) + k_evict_commit + k_admit_commit instead of two kernels
+PIPELINE_EXTRA_KERNELS = 3
 KSTEPS = 5  # extra steps timed kernel by kernel after the timed region
 
 
@@ -246,11 +253,13 @@ def ncu_traffic(kernel):
         return None
 
 
-def rooflines(prof, pool_ms, N, D, links, engine="async"):
+def rooflines(prof, pool_ms, N, D, links, engine="async", pipelined=False):
     hbm, hbm_src = hbm_peak()
-    xfer_ms = prof["transfer_ms"] / max(prof["calls"], 1)
+    xfer_ms = prof["transfer_ms"] / max(prof["transfer_launches"] if pipelined else prof["calls"], 1)
     xfer_bytes = prof["host_link_bytes"] / max(prof["calls"], 1)
-    if engine == "async":  # admissions only (H2D); write-backs ride the copy engine off the critical path
+    if pipelined:  # admissions staged host -> HBM on the transfer stream; write-backs on the copy engine
+        kname, peak, src = "k_admit_stage", links["h2d_GBps"], "pinned cudaMemcpy H2D, measured in this run"
+    elif engine == "async":  # admissions only (H2D); write-backs ride the copy engine off the critical path
         kname, peak, src = "k_admit_async", links["h2d_GBps"], "pinned cudaMemcpy H2D, measured in this run"
     else:
         kname, peak, src = "k_transfer_rows", links["bidir_GBps"], "pinned cudaMemcpy H2D+D2H concurrently, measured"
@@ -285,7 +294,7 @@ def run_ours(args, cfg, torch, rank, world):
     W, K = args.warmup, args.steps
     D, B, F = cfg["dim"], cfg["batch"], cfg["features"]
     N = B * F
-    n_batches = max(args.trace_batches // world, W + 2 * K + KSTEPS)
+    n_batches = max(args.trace_batches // world, W + 2 * K + KSTEPS + 2)
     # global batch = world x B samples; this rank's slice is rows [rank*B, (rank+1)*B) of each global batch
     sharded = world > 1 or args.sharded
     samples, rank_of, id_of, cap = make_workload(cfg, n_batches * world, device=dev, keep_counts=sharded)
@@ -336,13 +345,19 @@ def run_ours(args, cfg, torch, rank, world):
             out.backward(gout)
             stats.append((0, 0, 0, 0, 0))
             return
-        info, uids, ucnt, uranks, uslots, inverse, _ = dc.prepare(ids, s)
+        if pipelined:  # batch s was prefetched during step s-1: commit it
+            info, uids, ucnt, uranks, uslots, inverse, _ = dc.prepare_commit()
+        else:
+            info, uids, ucnt, uranks, uslots, inverse, _ = dc.prepare(ids, s)
         e = step_events[len(pool_ms)] if timed else None  # created before the timed region
         if timed:
             e[0].record(stream)
         dc.pooled(uslots, inverse, N, out=out_buf)
         if timed:
             e[1].record(stream)
+        if pipelined:  # batch s+1's index phase + miss staging overlap this batch's backward
+            nlo, nhi = local_batch(s + 1)
+            dc.prepare_begin(ids_dev[nlo:nhi].reshape(-1), s + 1)
         if args.step == "train":
             dc.backward_update(uslots, inverse, ucnt, None, N, False, None, "sum", gout, "sgd", LR, 0.0)
         else:
@@ -352,6 +367,10 @@ def run_ours(args, cfg, torch, rank, world):
             pool_ms.append(e)
         stats.append((info.unique, info.hits, info.misses, info.evictions, info.rows_to_slow))
 
+    pipelined = (not sharded) and args.engine == "async" and not args.no_prefetch
+    if pipelined:
+        lo0, hi0 = local_batch(0)
+        dc.prepare_begin(ids_dev[lo0:hi0].reshape(-1), 0)
     for s in range(W):
         step(s, False)
     torch.cuda.synchronize(dev)
@@ -388,23 +407,29 @@ def run_ours(args, cfg, torch, rank, world):
     b_ms = [e[1].elapsed_time(e[2]) for e in pool_ms]
 
     # ---- e2e: the public API (module forward+backward) from pinned host ids ----
+    if pipelined and dc.prefetch_outstanding:
+        dc.prepare_commit()
     ids_host = torch.from_numpy(samples).pin_memory()
+    hb = [ids_host[local_batch(k)[0]:local_batch(k)[1]].reshape(-1) for k in range(n_batches)]
     for k in range(W):  # the first autograd backward starts torch's device thread (~1.4 s, once)
-        lo, hi = local_batch(k)
-        mod(ids_host[lo:hi].reshape(-1)).backward(gout)
+        mod(hb[k]).backward(gout)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
     t = time.perf_counter()
     hits_read = 0
+    e0 = W + K + KSTEPS
     for k in range(K):
-        lo, hi = local_batch(W + K + KSTEPS + k)
-        out = mod(ids_host[lo:hi].reshape(-1))  # H2D of the ids inside forward
+        out = mod(hb[e0 + k])  # H2D of the ids inside forward (or inside the previous step's prefetch)
+        if pipelined:
+            mod.prefetch(hb[e0 + k + 1])  # next batch's cache work overlaps this backward
         out.backward(gout)  # upstream gradient of the pooled output -> fused SGD on the cached rows
         if not sharded:
             hits_read += mod.last_info.hits  # the step's result (prepare counters, read back D2H)
     torch.cuda.synchronize(dev)
     e2e_s = time.perf_counter() - t
+    if pipelined:
+        mod.flush()  # commits the last prefetch
     if world > 1:
         tt = torch.tensor([e2e_s], device=dev)
         torch.distributed.all_reduce(tt, op=torch.distributed.ReduceOp.MAX)
@@ -412,7 +437,7 @@ def run_ours(args, cfg, torch, rank, world):
 
     st_arr = np.array(stats_main, dtype=np.float64)
     uniq, hits, misses, evict, wb = st_arr.mean(axis=0)
-    rl = rooflines(prof, p_ms, N, D, links, args.engine)
+    rl = rooflines(prof, p_ms, N, D, links, args.engine, pipelined)
     lookups = N * world  # every rank processes its own B x F ids per step
     res = {
         "metric": METRIC, "value": lookups * K / (total_ms * 1e-3), "unit": "lookups/s", "n_gpus": world,
@@ -425,11 +450,13 @@ def run_ours(args, cfg, torch, rank, world):
                    "step": ("forward (prepare + pooled gather) + fused backward/SGD" if args.step == "train"
                             else "prepare + pooled forward + simulator row update"),
                    "write_back": "dirty_only", "evict_mode": "occupancy_aware", "engine": args.engine,
+                   "prefetch": pipelined,
                    "l2": "inputs larger than L2 (fast tier %d MB, id/rank maps %d MB, new batch every step)"
                          % (cap * D * 4 >> 20, cfg["num_ids"] * 12 // world >> 20),
                    "parallelism": "single" if not sharded else f"rowwise{world} (id/row all-to-all over NCCL)"},
         "step_latency_ms": {"p50": float(np.percentile(step_ms, 50)), "p99": float(np.percentile(step_ms, 99)),
-                            "prepare_avg": prof["prepare_ms"] / max(prof["calls"], 1),
+                            "prepare_avg": (None if pipelined else prof["prepare_ms"] / max(prof["calls"], 1)),
+                            "miss_transfer_avg": rl[0]["launch_ms"] if rl[0]["bound"] == "host_link" else None,
                             "pool_avg": float(np.mean(p_ms)) if p_ms else None,
                             "update_avg": float(np.mean(b_ms)) if b_ms else None,
                             "async_writeback_wait_avg": prof["host_wait_ms"] / max(prof["calls"], 1),
@@ -439,7 +466,8 @@ def run_ours(args, cfg, torch, rank, world):
                 "path": "CachedEmbeddingBag.forward(pinned host ids) + out.backward(grad) (fused SGD); result = "
                         "prepare hit/miss counters read back" if not sharded
                 else "RowShardedEmbedding.forward(pinned host ids) + out.backward(grad)"},
-        "gpu_launches": (KERNELS_PER_STEP if args.step == "sim" else KERNELS_PER_TRAIN_STEP) * K,
+        "gpu_launches": ((KERNELS_PER_STEP if args.step == "sim" else KERNELS_PER_TRAIN_STEP)
+                         + (PIPELINE_EXTRA_KERNELS if pipelined else 0)) * K,
         "roofline": rl[0], "roofline_secondary": rl[1] if len(rl) > 1 else None,
         "host_link": links,
         "clocks": clk.summary(),
@@ -462,6 +490,8 @@ def main():
     ap.add_argument("--cpu-baseline-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="row-sharded module even at one GPU (needs torchrun)")
+    ap.add_argument("--no-prefetch", action="store_true",
+                    help="synchronous prepare each step (no lookahead pipeline)")
     ap.add_argument("--engine", default="async", choices=["async", "zerocopy"],
                     help="transfer engine: async copy-engine write-back (default) or paired zero-copy kernel")
     args = ap.parse_args()

@@ -119,8 +119,17 @@ int fc_drain(fc_cache* h);
  * calls, bytes the transfer kernel moved over the host link (4*dim*(admitted +
  * written-back rows) for engine 0, admitted rows only for engine 1),
  * written-back bytes, host ms spent waiting for async write-backs (engine 1),
- * host scatter ms and scatter jobs completed (engine 1). `out` holds 8 doubles. */
+ * host scatter ms and scatter jobs completed (engine 1), transfer launches timed
+ * (prefetch pipeline: out[1] covers k_admit_stage). `out` holds 9 doubles. */
 int fc_profile(fc_cache* h, int32_t enable, double* out);
+
+/* Timeline tracing (diagnostics, no reference counterpart): while enabled the
+ * pipeline records tagged CUDA events (1/2 index phase begin/end, 3/4 miss staging
+ * begin/end, 5/6 commit begin/end) and fc_trace_mark adds caller tags on any
+ * stream. fc_trace_read returns up to `max` (tag, ms since the first event) pairs. */
+int fc_trace(fc_cache* h, int32_t enable);
+int fc_trace_mark(fc_cache* h, int32_t tag, void* stream);
+int64_t fc_trace_read(fc_cache* h, int32_t* tags, double* ms, int64_t max);
 
 /* ---- the cache verbs ------------------------------------------------------- */
 /* warmup (cache_manager.py:351-390): ranks 0..k-1 -> slots 0..k-1; empty cache only. */
@@ -135,6 +144,27 @@ int fc_warmup(fc_cache* h, int64_t k, void* stream);
 int fc_prepare(fc_cache* h, const void* ids_dev, int32_t ids_bytes, int64_t n, int64_t batch_seq,
                int32_t* unique_ids, int32_t* unique_counts, int32_t* unique_ranks,
                int32_t* unique_slots, int32_t* inverse, void* stream, fc_prepare_info* info);
+
+/* Prefetch pipeline (extension; the paper's future-work prefetch).
+ * fc_prepare_begin launches batch t+1's prepare without waiting for batch t's
+ * forward/backward: the index phase (dedup, lookups, victim and slot choice, every
+ * slot-table change; no row and no dirty bit touched) runs on `stream`, and the
+ * admitted rows are staged host -> HBM on a library-owned transfer stream. Outputs
+ * are as fc_prepare's and become valid once fc_prepare_commit returns.
+ * fc_prepare_commit, on the stream that runs the forward/backward, writes the
+ * victims (already carrying batch t's update) to the write-back stage and moves the
+ * staged rows into their slots; it fills `info` (rows_to_slow = -1: the dirty filter
+ * runs on device) and reports validation errors (nothing is mutated on error).
+ * The resulting cache state, slot assignment and write-backs are bit-identical to
+ * calling fc_prepare at commit time. Requires the async engine (fc_set_engine 1).
+ * At most one begin may be outstanding; the synchronous verbs refuse while one is. */
+int fc_prepare_begin(fc_cache* h, const void* ids_dev, int32_t ids_bytes, int64_t n, int64_t batch_seq,
+                     int32_t* unique_ids, int32_t* unique_counts, int32_t* unique_ranks, int32_t* unique_slots,
+                     int32_t* inverse, void* stream);
+int fc_prepare_commit(fc_cache* h, void* stream, fc_prepare_info* info);
+/* Rows the last fc_prepare_commit wrote back (its dirty filter ran on device);
+ * waits for that commit's kernels. 0 after a synchronous fc_prepare. */
+int fc_last_writebacks(fc_cache* h, int64_t* rows);
 
 /* Event-log payload of the last prepare (CacheEvent, cache_manager.py:78-99):
  * evicted ranks (descending) and admitted ranks (ascending), device -> host. */

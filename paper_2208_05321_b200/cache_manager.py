@@ -287,15 +287,40 @@ def prepare_cache(state: CacheState, idx_map: IdxMap, ids, transmitter: Transmit
         raise ValueError(f"evict_mode must be one of {EVICT_MODES}, got {evict_mode!r}")
     policy = _check_policy(policy)
     dev = _bound(state, idx_map, transmitter, slow, fast, write_back, evict_mode)
+    if dev.prefetch_outstanding:
+        # a prefetched batch is executed first (its commit); `ids` itself is that batch
+        # when it is the very object handed to prefetch, else it is prepared after it
+        res = dev.prepare_commit()
+        if dev.committed_matches(ids):
+            return _prepare_result(dev, ids, res, transmitter, fast, policy, batch_seq, event_log,
+                                   rows_to_slow=dev.last_writebacks())
     dev.set_modes(write_back, evict_mode)
-    info, uids, ucnt, uranks, uslots, inverse, d_ids = dev.prepare(ids, batch_seq)
+    return _prepare_result(dev, ids, dev.prepare(ids, batch_seq), transmitter, fast, policy, batch_seq, event_log)
+
+
+def prefetch_cache(state: CacheState, idx_map: IdxMap, ids, transmitter: Transmitter, slow: SlowTierStore,
+                   fast: FastTierStore, *, write_back: str = "dirty_only", evict_mode: str = "occupancy_aware",
+                   batch_seq: int = 0) -> None:
+    """Start `ids`' prepare ahead of time (extension; the paper's future-work prefetch,
+    PAPER.md:490): the index phase and the host -> HBM staging of its misses overlap
+    the previous batch's row work. The next prepare_cache call with the same `ids`
+    object commits it; the outcome is bit-identical to a plain prepare_cache then."""
+    dev = _bound(state, idx_map, transmitter, slow, fast, write_back, evict_mode)
+    dev.set_modes(write_back, evict_mode)
+    dev.prepare_begin(ids, batch_seq)
+
+
+def _prepare_result(dev, ids, res, transmitter, fast, policy, batch_seq, event_log, rows_to_slow=None):
+    info, uids, ucnt, uranks, uslots, inverse, d_ids = res
+    if rows_to_slow is None:
+        rows_to_slow = int(info.rows_to_slow)
     if int(d_ids.numel()) == 0:
         return PrepareResult(ids if not hasattr(ids, "shape") else ids, d_ids=d_ids)
     row_bytes = fast.embedding_dim * 4
     reports = []
     if info.evictions:
-        reports.append(transmitter.report(TO_SLOW, int(info.rows_to_slow), row_bytes)
-                       if info.rows_to_slow else TransferReport.empty(TO_SLOW))
+        reports.append(transmitter.report(TO_SLOW, rows_to_slow, row_bytes)
+                       if rows_to_slow else TransferReport.empty(TO_SLOW))
     if info.misses:
         reports.append(transmitter.report(TO_FAST, int(info.misses), row_bytes))
     prep = PrepareResult(ids, d_ids, uids, ucnt, uranks, uslots, inverse, info.hits, info.misses, info.evictions,
@@ -426,6 +451,12 @@ class CacheStack:
         return prepare_cache(self.state, self.idx_map, ids, self.transmitter, self.slow, self.fast,
                              policy=self.policy, write_back=self.write_back, evict_mode=self.evict_mode,
                              batch_seq=batch_seq, event_log=self.events)
+
+    def prefetch(self, ids, batch_seq: int) -> None:
+        """Start the prepare of the next batch early (see prefetch_cache); the following
+        prepare(ids, ...) with the same ids object commits it."""
+        prefetch_cache(self.state, self.idx_map, ids, self.transmitter, self.slow, self.fast,
+                       write_back=self.write_back, evict_mode=self.evict_mode, batch_seq=batch_seq)
 
     def gather(self, prep: PrepareResult):
         return gather(self.fast, prep)

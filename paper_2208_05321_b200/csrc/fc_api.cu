@@ -24,6 +24,28 @@ int cuda_fail(cudaError_t e, const char* what) {
   return FC_ERR_CUDA;
 }
 
+struct TraceEv {
+  int tag;
+  cudaEvent_t ev;
+};
+
+void trace_mark(fc_cache* h, int tag, cudaStream_t st) {
+  if (!h->trace) return;
+  auto* v = static_cast<std::vector<TraceEv>*>(h->trace);
+  cudaEvent_t e;
+  if (cudaEventCreate(&e) != cudaSuccess) return;
+  cudaEventRecord(e, st);
+  v->push_back(TraceEv{tag, e});
+}
+
+static void trace_clear(fc_cache* h) {
+  if (!h->trace) return;
+  auto* v = static_cast<std::vector<TraceEv>*>(h->trace);
+  for (auto& t : *v) cudaEventDestroy(t.ev);
+  delete v;
+  h->trace = nullptr;
+}
+
 int ensure_scratch(fc_cache* h, size_t bytes) {
   if (bytes <= h->scratch_bytes) return FC_OK;
   size_t nb = std::max(bytes, h->scratch_bytes + h->scratch_bytes / 2);
@@ -64,6 +86,8 @@ static int dalloc(T** p, size_t count) {
 }
 
 static void release(fc_cache* h) {
+  trace_clear(h);
+  pipe_release(h);
   engine_release(h);
   void* dev[] = {h->rank_of, h->rank_to_slot, h->slot_to_rank, h->dirty, h->fast, h->fast_state,
                  h->res_bits, h->free_bits, h->id_bits, h->miss_bits, h->prot_bits, h->aux,
@@ -81,6 +105,15 @@ static void release(fc_cache* h) {
 }  // namespace fc
 
 using namespace fc;
+
+// Synchronous verbs see the state only after a prefetched prepare is committed.
+#define FC_NO_OUTSTANDING(h)                                                          \
+  do {                                                                                \
+    if (pipe_outstanding(h)) {                                                        \
+      set_error("a prefetched prepare is outstanding: call fc_prepare_commit first"); \
+      return FC_ERR_BAD_ARG;                                                          \
+    }                                                                                 \
+  } while (0)
 
 #define FC_TRY(expr)          \
   do {                        \
@@ -192,6 +225,9 @@ int fc_create(int64_t num_ids, int64_t capacity, int32_t dim, int32_t state_widt
     return rc;
   }
   h->host_free = (int32_t)capacity;
+  h->live = h->ctr;
+  h->ev_src = h->evicted_ranks;
+  h->ad_src = h->admitted_ranks;
   *out = h;
   return FC_OK;
 }
@@ -223,6 +259,7 @@ int fc_set_modes(fc_cache* h, int32_t write_back, int32_t evict_mode) {
   if (!h || (write_back != FC_WB_DIRTY_ONLY && write_back != FC_WB_ALWAYS) ||
       (evict_mode != FC_EVICT_OCCUPANCY_AWARE && evict_mode != FC_EVICT_PAPER_LITERAL))
     return FC_ERR_BAD_ARG;
+  FC_NO_OUTSTANDING(h);
   h->write_back = write_back;
   h->evict_mode = evict_mode;
   return FC_OK;
@@ -232,6 +269,7 @@ int64_t fc_free_count(fc_cache* h) { return h ? h->host_free : -1; }
 
 int fc_set_engine(fc_cache* h, int32_t engine) {
   if (!h) return FC_ERR_BAD_ARG;
+  FC_NO_OUTSTANDING(h);
   DeviceGuard dg(h->device);
   return engine_set(h, engine);
 }
@@ -293,6 +331,7 @@ int fc_attach_slow_tier(fc_cache* h, float* rows_host, int64_t row_stride, float
 
 int fc_warmup(fc_cache* h, int64_t k, void* stream) {
   if (!h) return FC_ERR_BAD_ARG;
+  FC_NO_OUTSTANDING(h);
   if (k < 0 || k > h->capacity) {
     set_error("warmup k must be in [0, capacity=%d], got %lld", h->capacity, (long long)k);
     return FC_ERR_BAD_ARG;
@@ -309,6 +348,7 @@ int fc_warmup(fc_cache* h, int64_t k, void* stream) {
   }
   DeviceGuard dg(h->device);
   cudaStream_t st = as_stream(stream);
+  FC_TRY(pipe_order(h, st));
   // ranks 0..k-1 are contiguous in the slow tier: one DMA copy, no gather
   FC_CUDA(cudaMemcpy2DAsync(h->fast, (size_t)h->dim * 4, h->slow, (size_t)h->slow_ld * 4, (size_t)h->dim * 4, (size_t)k,
                             cudaMemcpyDefault, st));
@@ -323,14 +363,19 @@ int fc_prepare(fc_cache* h, const void* ids, int32_t ids_bytes, int64_t n, int64
                int32_t* ucnt, int32_t* uranks, int32_t* uslots, int32_t* inverse, void* stream, fc_prepare_info* info) {
   (void)batch_seq;
   if (!h || !info || (ids_bytes != 4 && ids_bytes != 8) || n < 0 || n > INT32_MAX) return FC_ERR_BAD_ARG;
+  FC_NO_OUTSTANDING(h);
   std::memset(info, 0, sizeof(*info));
   info->free_count = h->host_free;
   if (n == 0) return FC_OK;
   if (!h->slow) return FC_ERR_NO_SLOW_TIER;
   DeviceGuard dg(h->device);
   cudaStream_t st = as_stream(stream);
+  FC_TRY(pipe_order(h, st));
   FC_TRY(engine_begin(h, st));
   FC_TRY(launch_prepare(h, ids, ids_bytes, n, uids, ucnt, uranks, uslots, inverse, st));
+  h->ev_src = h->evicted_ranks;
+  h->ad_src = h->admitted_ranks;
+  h->last_wb_dev = nullptr;
   FC_TRY(sync_counters(h, st));
   FC_TRY(engine_after_prepare(h, st));
   const Counters& c = *h->ctr_host;
@@ -385,12 +430,91 @@ int fc_prepare(fc_cache* h, const void* ids, int32_t ids_bytes, int64_t n, int64
   return FC_OK;
 }
 
+int fc_prepare_begin(fc_cache* h, const void* ids, int32_t ids_bytes, int64_t n, int64_t batch_seq, int32_t* uids,
+                     int32_t* ucnt, int32_t* uranks, int32_t* uslots, int32_t* inverse, void* stream) {
+  (void)batch_seq;
+  if (!h || (ids_bytes != 4 && ids_bytes != 8) || n < 1 || n > INT32_MAX) return FC_ERR_BAD_ARG;
+  if (!h->slow) return FC_ERR_NO_SLOW_TIER;
+  DeviceGuard dg(h->device);
+  return pipe_begin(h, ids, ids_bytes, n, uids, ucnt, uranks, uslots, inverse, as_stream(stream));
+}
+
+int fc_prepare_commit(fc_cache* h, void* stream, fc_prepare_info* info) {
+  if (!h || !info) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  const int rc = pipe_commit(h, as_stream(stream), info);
+  switch (rc) {
+    case FC_OK:
+      break;
+    case FC_ERR_ID_OUT_OF_RANGE:
+      set_error("id out of range: %lld not in [0, %lld)", (long long)info->bad_id, (long long)h->num_ids);
+      break;
+    case FC_ERR_BATCH_EXCEEDS_CAPACITY:
+      set_error("batch has %lld unique ids but the fast tier holds %d; the cache ratio is too small for this batch",
+                (long long)info->unique, h->capacity);
+      break;
+    case FC_ERR_BUFFER_TOO_SMALL:
+      set_error("row of %d B cannot fit in a %lld B buffer", h->dim * 4, (long long)h->buffer_bytes);
+      break;
+    case FC_ERR_INSUFFICIENT_FREE_SLOTS:
+    case FC_ERR_INSUFFICIENT_EVICTABLE:
+      set_error("not enough free or evictable slots for this batch");
+      break;
+    default:
+      break;
+  }
+  return rc;
+}
+
+int fc_last_writebacks(fc_cache* h, int64_t* rows) {
+  if (!h || !rows) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  *rows = 0;
+  if (!h->last_wb_dev) return FC_OK;
+  int32_t v = 0;
+  FC_TRY(pipe_sync_commits(h));  // the commit's kernels have run
+  FC_CUDA(cudaMemcpy(&v, h->last_wb_dev, sizeof(v), cudaMemcpyDeviceToHost));
+  *rows = v;
+  return FC_OK;
+}
+
+int fc_trace(fc_cache* h, int32_t enable) {
+  if (!h) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  trace_clear(h);
+  if (enable) h->trace = new std::vector<TraceEv>();
+  return FC_OK;
+}
+
+int fc_trace_mark(fc_cache* h, int32_t tag, void* stream) {
+  if (!h) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  trace_mark(h, tag, as_stream(stream));
+  return FC_OK;
+}
+
+int64_t fc_trace_read(fc_cache* h, int32_t* tags, double* ms, int64_t max) {
+  if (!h || !h->trace) return 0;
+  DeviceGuard dg(h->device);
+  auto* v = static_cast<std::vector<TraceEv>*>(h->trace);
+  const int64_t n = std::min<int64_t>(max, (int64_t)v->size());
+  for (int64_t i = 0; i < n; ++i) {
+    cudaEventSynchronize((*v)[i].ev);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, (*v)[0].ev, (*v)[i].ev);
+    tags[i] = (*v)[i].tag;
+    ms[i] = t;
+  }
+  return n;
+}
+
 int fc_profile(fc_cache* h, int32_t enable, double* out) {
   if (!h) return FC_ERR_BAD_ARG;
   DeviceGuard dg(h->device);
   if (out) {
     for (int i = 0; i < 6; ++i) out[i] = h->prof[i];
     engine_stats(h, out + 6);
+    out[8] = h->prof[6];
   }
   if (enable && !h->profile) {
     for (int i = 0; i < 4; ++i) FC_CUDA(cudaEventCreate(&h->pev[i]));
@@ -399,7 +523,7 @@ int fc_profile(fc_cache* h, int32_t enable, double* out) {
     for (int i = 0; i < 4; ++i) cudaEventDestroy(h->pev[i]);
   }
   h->profile = enable ? 1 : 0;
-  for (int i = 0; i < 6; ++i) h->prof[i] = 0;
+  for (int i = 0; i < 8; ++i) h->prof[i] = 0;
   return FC_OK;
 }
 
@@ -408,8 +532,8 @@ int fc_last_events(fc_cache* h, int64_t* evicted_host, int64_t* admitted_host, v
   DeviceGuard dg(h->device);
   cudaStream_t st = as_stream(stream);
   std::vector<int32_t> a((size_t)h->last_needed), b((size_t)h->last_misses);
-  if (!a.empty()) FC_CUDA(cudaMemcpyAsync(a.data(), h->evicted_ranks, a.size() * 4, cudaMemcpyDeviceToHost, st));
-  if (!b.empty()) FC_CUDA(cudaMemcpyAsync(b.data(), h->admitted_ranks, b.size() * 4, cudaMemcpyDeviceToHost, st));
+  if (!a.empty()) FC_CUDA(cudaMemcpyAsync(a.data(), h->ev_src, a.size() * 4, cudaMemcpyDeviceToHost, st));
+  if (!b.empty()) FC_CUDA(cudaMemcpyAsync(b.data(), h->ad_src, b.size() * 4, cudaMemcpyDeviceToHost, st));
   FC_CUDA(cudaStreamSynchronize(st));
   for (size_t i = 0; i < a.size(); ++i) evicted_host[i] = a[i];
   for (size_t i = 0; i < b.size(); ++i) admitted_host[i] = b[i];
@@ -418,9 +542,11 @@ int fc_last_events(fc_cache* h, int64_t* evicted_host, int64_t* admitted_host, v
 
 int fc_flush(fc_cache* h, void* stream, int64_t* rows_written) {
   if (!h) return FC_ERR_BAD_ARG;
+  FC_NO_OUTSTANDING(h);
   if (!h->slow) return FC_ERR_NO_SLOW_TIER;
   DeviceGuard dg(h->device);
   cudaStream_t st = as_stream(stream);
+  FC_TRY(pipe_order(h, st));
   FC_TRY(engine_drain(h));  // queued write-backs land before flush's own
   FC_TRY(launch_reset_counters(h, st));
   FC_TRY(launch_flush(h, st));
@@ -431,9 +557,11 @@ int fc_flush(fc_cache* h, void* stream, int64_t* rows_written) {
 
 int fc_mark_dirty(fc_cache* h, const int64_t* slots, int64_t n, void* stream) {
   if (!h || n < 0) return FC_ERR_BAD_ARG;
+  FC_NO_OUTSTANDING(h);
   if (n == 0) return FC_OK;
   DeviceGuard dg(h->device);
   cudaStream_t st = as_stream(stream);
+  FC_TRY(pipe_order(h, st));
   FC_TRY(launch_mark_dirty(h, slots, n, st));
   FC_TRY(sync_counters(h, st));
   if (h->ctr_host->err) {
@@ -446,9 +574,11 @@ int fc_mark_dirty(fc_cache* h, const int64_t* slots, int64_t n, void* stream) {
 int fc_select_evictions(fc_cache* h, int64_t needed, const int64_t* prot, int64_t nprot, int64_t* slots_host,
                         void* stream) {
   if (!h || needed < 0 || nprot < 0) return FC_ERR_BAD_ARG;
+  FC_NO_OUTSTANDING(h);
   if (needed == 0) return FC_OK;
   DeviceGuard dg(h->device);
   cudaStream_t st = as_stream(stream);
+  FC_TRY(pipe_order(h, st));
   FC_TRY(launch_select_evictions(h, needed, prot, nprot, st));
   FC_TRY(sync_counters(h, st));
   if (h->ctr_host->err) {

@@ -32,6 +32,10 @@
 #include <thread>
 #include <vector>
 
+#include <climits>
+
+#include <cuda.h>
+
 #include "fc_rowutil.cuh"
 
 namespace fc {
@@ -50,18 +54,25 @@ struct AsyncWB {
   float* hstage[2] = {nullptr, nullptr};   // pinned
   float* hsstage[2] = {nullptr, nullptr};
   int32_t* hranks[2] = {nullptr, nullptr};
-  int64_t rows_in[2] = {0, 0};             // rows currently staged in each buffer
+  volatile uint32_t* done_host = nullptr;  // pinned mapped: last finished job's sequence number
+  CUdeviceptr done_dev = 0;                // its device address (stream wait-value target)
+  int32_t* dev_rows = nullptr;             // device int32[2]: rows staged by a pipeline commit
+  int32_t* hrows = nullptr;                // pinned int32[2]: their D2H copies
+  int64_t rows_in[2] = {0, 0};             // rows currently staged in each buffer (upper bound)
+  bool rows_on_dev[2] = {false, false};    // the exact count is dev_rows[b]
   uint64_t seq_of[2] = {0, 0};             // job sequence number using each buffer
   cudaStream_t side = nullptr;
   cudaEvent_t d2h[2] = {nullptr, nullptr};
   int cur = 0;
   int device = 0;
+  bool vec = true;                         // rows move as 16-byte units (dim % 4 == 0, aligned)
 
   // FIFO scatter jobs, one dispatcher + helpers
   std::mutex m;
   std::condition_variable cv_q, cv_done, cv_help, cv_helped;
   std::deque<Job> q;
-  uint64_t next_seq = 1, done_seq = 0;
+  uint64_t next_seq = 1, done_seq = 0, started_seq = 0;
+  std::condition_variable cv_started;
   bool stop = false;
   std::thread dispatcher;
   std::vector<std::thread> helpers;
@@ -146,7 +157,10 @@ static void dispatcher_main(AsyncWB* a) {
     a->q.pop_front();
     lk.unlock();
     cudaEventSynchronize(a->d2h[j.buf]);  // the staged rows are in pinned memory
+    if (j.rows < 0) j.rows = a->hrows[j.buf];  // pipeline commit: count known only on device
     lk.lock();
+    a->started_seq = j.seq;  // d2h[j.buf] / hrows[j.buf] may be re-recorded from here on
+    a->cv_started.notify_all();
     a->src = a->hstage[j.buf];
     a->ssrc = a->hsstage[j.buf];
     a->ranks = a->hranks[j.buf];
@@ -163,8 +177,23 @@ static void dispatcher_main(AsyncWB* a) {
     a->scatter_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     a->jobs_done += 1;
     a->done_seq = j.seq;
+    *a->done_host = (uint32_t)j.seq;  // releases streams waiting on this job (stream wait-value)
     a->cv_done.notify_all();
   }
+}
+
+// cuStreamWaitValue32 through the runtime's driver entry point (no -lcuda link)
+typedef CUresult (*WaitValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static WaitValueFn wait_value_fn() {
+  static WaitValueFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<WaitValueFn>(p);
+  }();
+  return fn;
 }
 
 static void wait_seq(AsyncWB* a, uint64_t seq) {
@@ -174,12 +203,56 @@ static void wait_seq(AsyncWB* a, uint64_t seq) {
 
 // ------------------------------------------------------------------ kernels
 __global__ void k_clear_pending(const int32_t* __restrict__ ranks, int64_t n, int32_t* pending, int32_t base,
-                                int32_t cap) {
+                                int32_t cap, const int32_t* n_dev) {
+  if (n_dev) n = *n_dev;
   for (int64_t k = (int64_t)blockIdx.x * kNT + threadIdx.x; k < n; k += (int64_t)gridDim.x * kNT) {
     const int r = ranks[k];
     if (pending[r] == base + (int32_t)k) pending[r] = -1;  // unless re-staged since
   }
   (void)cap;
+}
+
+// Copy 32 rows per warp: lane i owns row i (src/dst row pointers, active flag); the
+// lanes then sweep the rows' units (16-byte when VEC, else single floats) with 4
+// loads in flight per lane.
+template <bool VEC>
+__device__ __forceinline__ void warp_copy_rows(const float* sp, float* dp, bool act, Units un) {
+  const int lane = threadIdx.x & 31;
+  const int total = 32 * un.upr;
+  constexpr int W = VEC ? 4 : 1;
+  for (int u0 = 0; u0 < total; u0 += 32 * 4) {
+    float4 v[4];
+    float* d[4];
+    bool a[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int u = u0 + q * 32 + lane;
+      const int rr = min(un.row(u), 31);
+      const int c = (u - rr * un.upr) * W;
+      const float* s = reinterpret_cast<const float*>(__shfl_sync(FC_FULL, reinterpret_cast<long long>(sp), rr));
+      d[q] = reinterpret_cast<float*>(__shfl_sync(FC_FULL, reinterpret_cast<long long>(dp), rr)) + c;
+      a[q] = __shfl_sync(FC_FULL, (int)act, rr) && u < total;
+      if (a[q]) {
+        if (VEC) v[q] = ld4(s + c);
+        else v[q].x = s[c];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (a[q]) {
+        if (VEC) st4(d[q], v[q]);
+        else *d[q] = v[q].x;
+      }
+  }
+}
+
+// 16-byte units per row when VEC, else one unit per float
+inline Units row_units(int width, bool vec) {
+  if (vec) return units_for(width);
+  Units un;
+  un.upr = width > 0 ? width : 1;
+  un.lg = (un.upr & (un.upr - 1)) == 0 ? __builtin_ctz(un.upr) : -1;
+  return un;
 }
 
 struct EngArgs {
@@ -209,14 +282,13 @@ struct EngArgs {
 };
 
 // victims -> slot, dirty filter, compacted staging into stage[buf] + pending marks, state cleared
+template <bool VEC>
 __global__ void __launch_bounds__(kNT) k_evict_async(EngArgs x) {
-  __shared__ int sm[kNT / 32 + 1];
   if (!gate_open(x.c, G_EVICT)) return;
   const int needed = x.c->needed;
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
-  int wb_count = 0;
   for (int64_t base = warp * 32; base < needed; base += nwarps * 32) {
     const int64_t v = base + lane;
     const bool act = v < needed;
@@ -232,37 +304,8 @@ __global__ void __launch_bounds__(kNT) k_evict_async(EngArgs x) {
     if (lane == 0 && m) k0 = atomicAdd(&x.c->wb_rows, __popc(m));
     k0 = __shfl_sync(FC_FULL, k0, 0);
     const int k = k0 + __popc(m & ((1u << lane) - 1u));
-    // rows: lane i's victim row fast[s_i] -> stage[buf][k_i]
-    const int total = 32 * x.ud.upr;
-    for (int u0 = 0; u0 < total; u0 += 32 * 4) {
-      float4 val[4];
-      int dk[4], cc[4];
-      bool aa[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int u = u0 + q * 32 + lane;
-        const int rr = min(x.ud.row(u), 31);
-        cc[q] = (u - rr * x.ud.upr) * 4;
-        const int sr = __shfl_sync(FC_FULL, s, rr);
-        dk[q] = __shfl_sync(FC_FULL, k, rr);
-        aa[q] = __shfl_sync(FC_FULL, (int)wb, rr) && u < total;
-        if (aa[q]) val[q] = ld4(x.fast + (int64_t)sr * x.D + cc[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (aa[q]) st4(x.stage[x.buf] + (int64_t)dk[q] * x.D + cc[q], val[q]);
-    }
-    if (x.S) {
-      const int totals = 32 * x.us.upr;
-      for (int u = lane; u < totals; u += 32) {
-        const int rr = min(x.us.row(u), 31);
-        const int c = (u - rr * x.us.upr) * 4;
-        const int sr = __shfl_sync(FC_FULL, s, rr);
-        const int kr = __shfl_sync(FC_FULL, k, rr);
-        if (__shfl_sync(FC_FULL, (int)wb, rr))
-          st4(x.sstage[x.buf] + (int64_t)kr * x.S + c, ld4(x.fstate + (int64_t)sr * x.S + c));
-      }
-    }
+    warp_copy_rows<VEC>(x.fast + (int64_t)s * x.D, x.stage[x.buf] + (int64_t)k * x.D, wb, x.ud);
+    if (x.S) warp_copy_rows<VEC>(x.fstate + (int64_t)s * x.S, x.sstage[x.buf] + (int64_t)k * x.S, wb, x.us);
     if (act) {
       if (wb) {
         x.sranks[k] = r;
@@ -274,14 +317,12 @@ __global__ void __launch_bounds__(kNT) k_evict_async(EngArgs x) {
       atomicAnd(&x.res[r >> 5], ~(1u << (r & 31)));
       atomicOr(&x.freeb[s >> 5], 1u << (s & 31));
     }
-    wb_count += wb;
   }
-  (void)wb_count;
-  (void)sm;
   if (blockIdx.x == 0 && threadIdx.x == 0) x.c->free_count += needed;
 }
 
 // admissions: newest copy of each admitted rank -> its target slot
+template <bool VEC>
 __global__ void __launch_bounds__(kNT) k_admit_async(EngArgs x) {
   if (!gate_open(x.c, G_OK)) return;
   const int m = x.c->misses;
@@ -291,51 +332,18 @@ __global__ void __launch_bounds__(kNT) k_admit_async(EngArgs x) {
   for (int64_t base = warp * 32; base < m; base += nwarps * 32) {
     const int64_t j = base + lane;
     const bool act = j < m;
-    int r = 0, s = 0, pk = -1;
+    int r = 0, s = 0;
+    const float* src = nullptr;
+    const float* ssrc = nullptr;
     if (act) {
       r = x.admitted[j];
       s = x.target[j];
-      pk = x.pending[r];
+      const int pk = x.pending[r];
+      src = pk >= 0 ? x.stage[pk / x.cap] + (int64_t)(pk % x.cap) * x.D : x.slow + (int64_t)r * x.ld;
+      if (x.S) ssrc = pk >= 0 ? x.sstage[pk / x.cap] + (int64_t)(pk % x.cap) * x.S : x.sstate + (int64_t)r * x.sld;
     }
-    const int total = 32 * x.ud.upr;
-    for (int u0 = 0; u0 < total; u0 += 32 * 4) {
-      float4 val[4];
-      int ds[4], cc[4];
-      bool aa[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int u = u0 + q * 32 + lane;
-        const int rr = min(x.ud.row(u), 31);
-        cc[q] = (u - rr * x.ud.upr) * 4;
-        const int rq = __shfl_sync(FC_FULL, r, rr);
-        const int pq = __shfl_sync(FC_FULL, pk, rr);
-        ds[q] = __shfl_sync(FC_FULL, s, rr);
-        aa[q] = __shfl_sync(FC_FULL, (int)act, rr) && u < total;
-        if (aa[q]) {
-          const float* src = pq >= 0 ? x.stage[pq / x.cap] + (int64_t)(pq % x.cap) * x.D
-                                     : x.slow + (int64_t)rq * x.ld;
-          val[q] = ld4(src + cc[q]);
-        }
-      }
-#pragma unroll
-      for (int q = 0; q < 4; ++q)
-        if (aa[q]) st4(x.fast + (int64_t)ds[q] * x.D + cc[q], val[q]);
-    }
-    if (x.S) {
-      const int totals = 32 * x.us.upr;
-      for (int u = lane; u < totals; u += 32) {
-        const int rr = min(x.us.row(u), 31);
-        const int c = (u - rr * x.us.upr) * 4;
-        const int rq = __shfl_sync(FC_FULL, r, rr);
-        const int pq = __shfl_sync(FC_FULL, pk, rr);
-        const int sq = __shfl_sync(FC_FULL, s, rr);
-        if (__shfl_sync(FC_FULL, (int)act, rr)) {
-          const float* src = pq >= 0 ? x.sstage[pq / x.cap] + (int64_t)(pq % x.cap) * x.S
-                                     : x.sstate + (int64_t)rq * x.sld;
-          st4(x.fstate + (int64_t)sq * x.S + c, ld4(src + c));
-        }
-      }
-    }
+    warp_copy_rows<VEC>(src, x.fast + (int64_t)s * x.D, act, x.ud);
+    if (x.S) warp_copy_rows<VEC>(ssrc, x.fstate + (int64_t)s * x.S, act, x.us);
     if (act) {
       x.slot_to_rank[s] = r;
       x.rank_to_slot[r] = s;
@@ -369,12 +377,9 @@ int engine_set(fc_cache* h, int engine) {
     set_error("attach the slow tier before selecting the async engine");
     return FC_ERR_NO_SLOW_TIER;
   }
-  if (!vec_ok_engine(h)) {
-    set_error("async engine needs dim %% 4 == 0 and 16-byte aligned rows");
-    return FC_ERR_BAD_ARG;
-  }
   AsyncWB* a = new AsyncWB();
   a->h = h;
+  a->vec = vec_ok_engine(h);
   a->device = h->device;
   const size_t C = (size_t)h->capacity;
   cudaError_t e = cudaMalloc(&a->pending, (size_t)h->num_ids * 4);
@@ -391,6 +396,15 @@ int engine_set(fc_cache* h, int engine) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a->d2h[b], cudaEventDisableTiming | cudaEventBlockingSync);
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaMalloc(&a->dev_rows, 2 * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaHostAlloc((void**)&a->done_host, 64, cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    *a->done_host = 0;
+    void* dp = nullptr;
+    e = cudaHostGetDevicePointer(&dp, (void*)a->done_host, 0);
+    a->done_dev = reinterpret_cast<CUdeviceptr>(dp);
+  }
+  if (e == cudaSuccess) e = cudaHostAlloc(&a->hrows, 2 * sizeof(int32_t), cudaHostAllocDefault);
   h->awb = a;
   if (e != cudaSuccess) {
     engine_release(h);
@@ -413,9 +427,11 @@ int engine_begin(fc_cache* h, cudaStream_t st) {
     const auto t0 = std::chrono::steady_clock::now();
     wait_seq(a, a->seq_of[b]);
     h->prof[5] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-    k_clear_pending<<<grid_for(a->rows_in[b], kNT, kSMs * 4), kNT, 0, st>>>(a->sranks[b], a->rows_in[b], a->pending,
-                                                                            (int32_t)(b * h->capacity), h->capacity);
+    k_clear_pending<<<grid_for(a->rows_in[b], kNT, kSMs * 4), kNT, 0, st>>>(
+        a->sranks[b], a->rows_in[b], a->pending, (int32_t)(b * h->capacity), h->capacity,
+        a->rows_on_dev[b] ? a->dev_rows + b : nullptr);
     a->rows_in[b] = 0;
+    a->rows_on_dev[b] = false;
     FC_CUDA(cudaGetLastError());
   }
   return FC_OK;
@@ -450,21 +466,23 @@ static EngArgs eng_args(fc_cache* h) {
   x.cap = h->capacity;
   x.always = h->write_back == FC_WB_ALWAYS;
   x.c = h->ctr;
-  x.ud = units_for(h->dim);
-  x.us = units_for(h->sw ? h->sw : 4);
+  x.ud = row_units(h->dim, a->vec);
+  x.us = row_units(h->sw ? h->sw : 4, a->vec);
   return x;
 }
 
 int engine_evict(fc_cache* h, cudaStream_t st) {
   EngArgs x = eng_args(h);
-  k_evict_async<<<kSMs * 8, kNT, 0, st>>>(x);
+  if (h->awb->vec) k_evict_async<true><<<kSMs * 8, kNT, 0, st>>>(x);
+  else k_evict_async<false><<<kSMs * 8, kNT, 0, st>>>(x);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }
 
 int engine_admit(fc_cache* h, cudaStream_t st) {
   EngArgs x = eng_args(h);
-  k_admit_async<<<kSMs * 4, kNT, 0, st>>>(x);
+  if (h->awb->vec) k_admit_async<true><<<kSMs * 4, kNT, 0, st>>>(x);
+  else k_admit_async<false><<<kSMs * 4, kNT, 0, st>>>(x);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }
@@ -520,6 +538,9 @@ void engine_release(fc_cache* h) {
   for (auto& t : a->helpers)
     if (t.joinable()) t.join();
   cudaFree(a->pending);
+  cudaFree(a->dev_rows);
+  cudaFreeHost(a->hrows);
+  if (a->done_host) cudaFreeHost((void*)a->done_host);
   for (int b = 0; b < 2; ++b) {
     cudaFree(a->stage[b]);
     cudaFree(a->sranks[b]);
@@ -532,6 +553,434 @@ void engine_release(fc_cache* h) {
   if (a->side) cudaStreamDestroy(a->side);
   delete a;
   h->awb = nullptr;
+}
+
+// ------------------------------------------------------------------ prefetch pipeline
+// fc_prepare_begin / fc_prepare_commit split one prepare (cache_manager.py:234-348)
+// so that batch t+1's cache work overlaps batch t's forward/backward:
+//
+//   begin(t+1), caller's index stream:  launch_index_phase (every decision and every
+//       slot-table change; no row, no dirty bit) -> counters D2H;
+//   begin(t+1), transfer stream:        k_admit_stage — the admitted rows' newest
+//       copies (HBM write-back stage if pending, else the pinned slow tier over the
+//       host link) -> HBM admission stage[t+1 % 2];
+//   commit(t+1), caller's main stream (after backward(t) in stream order):
+//       k_evict_commit — dirty victims -> write-back stage, pending marks, dirty
+//       cleared (the victim rows already carry backward(t)'s update);
+//       k_admit_commit — admission stage -> target slots (HBM -> HBM), dirty cleared;
+//       then the async engine ships the write-back stage D2H as usual.
+//
+// The outcome is bit-identical to sequential prepares: the index phase reads only
+// slot tables, which forward/backward never touch; victims are staged after the
+// previous batch's update; admitted rows are read after the previous commit's
+// write-back marks exist. Ordering is enforced with events:
+//   index(t+1)  after index(t), and after commit(t-1) (its parity's buffers);
+//   stage(t+1)  after index(t+1) and commit(t) (pending marks, stage reuse);
+//   commit(t+1) after stage(t+1) (and the caller's stream order).
+
+struct Pipe {
+  IndexBufs ib[2];
+  Counters* hctr[2] = {nullptr, nullptr};  // pinned mapped copies of the index counters
+  Counters* hctr_dev[2] = {nullptr, nullptr};
+  float* astage[2] = {nullptr, nullptr};   // admission stage [C, D]
+  float* astage_s[2] = {nullptr, nullptr}; // [C, S]
+  cudaStream_t xfer = nullptr;             // transfer stream (k_admit_stage)
+  cudaEvent_t ev_index[2] = {nullptr, nullptr};
+  cudaEvent_t ev_xfer[2] = {nullptr, nullptr};
+  cudaEvent_t ev_commit[2] = {nullptr, nullptr};
+  cudaEvent_t px[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // profiling: around k_admit_stage
+  bool has_index[2] = {false, false};
+  bool has_commit[2] = {false, false};
+  bool timed[2] = {false, false};
+  int par = 0;
+  bool outstanding = false;
+  int xfer_blocks = kSMs;                  // k_admit_stage grid (one block per SM: enough loads in flight)
+};
+
+bool pipe_outstanding(const fc_cache* h) { return h->pipe && h->pipe->outstanding; }
+
+// Host wait for every recorded pipeline commit (their kernels have finished).
+int pipe_sync_commits(fc_cache* h) {
+  Pipe* q = h->pipe;
+  if (!q) return FC_OK;
+  for (int p = 0; p < 2; ++p)
+    if (q->has_commit[p]) FC_CUDA(cudaEventSynchronize(q->ev_commit[p]));
+  return FC_OK;
+}
+
+// A synchronous verb on stream `st` runs after every committed pipeline step.
+int pipe_order(fc_cache* h, cudaStream_t st) {
+  Pipe* q = h->pipe;
+  if (!q) return FC_OK;
+  for (int p = 0; p < 2; ++p) {
+    if (q->has_commit[p]) FC_CUDA(cudaStreamWaitEvent(st, q->ev_commit[p], 0));
+  }
+  return FC_OK;
+}
+
+void pipe_release(fc_cache* h) {
+  Pipe* q = h->pipe;
+  if (!q) return;
+  for (int p = 0; p < 2; ++p) {
+    cudaFree(q->ib[p].ctr);
+    cudaFree(q->ib[p].evicted);
+    cudaFree(q->ib[p].vslots);
+    cudaFree(q->ib[p].admitted);
+    cudaFree(q->ib[p].target);
+    cudaFree(q->astage[p]);
+    cudaFree(q->astage_s[p]);
+    cudaFreeHost(q->hctr[p]);
+    for (cudaEvent_t ev : {q->ev_index[p], q->ev_xfer[p], q->ev_commit[p], q->px[p][0], q->px[p][1]})
+      if (ev) cudaEventDestroy(ev);
+  }
+  if (q->xfer) cudaStreamDestroy(q->xfer);
+  delete q;
+  h->pipe = nullptr;
+}
+
+static int pipe_create(fc_cache* h) {
+  Pipe* q = new Pipe();
+  std::memset(q->ib, 0, sizeof(q->ib));
+  h->pipe = q;
+  const size_t C = (size_t)h->capacity;
+  cudaError_t e = cudaSuccess;
+  for (int p = 0; p < 2 && e == cudaSuccess; ++p) {
+    e = cudaMalloc(&q->ib[p].ctr, sizeof(Counters));
+    if (e == cudaSuccess) e = cudaMemset(q->ib[p].ctr, 0, sizeof(Counters));
+    if (e == cudaSuccess) e = cudaMalloc(&q->ib[p].evicted, C * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&q->ib[p].vslots, C * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&q->ib[p].admitted, C * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&q->ib[p].target, C * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&q->astage[p], C * h->dim * 4);
+    if (e == cudaSuccess && h->sw) e = cudaMalloc(&q->astage_s[p], C * h->sw * 4);
+    // mapped: the index phase publishes its counters with a kernel store instead of a
+    // cudaMemcpy that would queue behind the write-back D2H on the copy engine
+    if (e == cudaSuccess) e = cudaHostAlloc(&q->hctr[p], sizeof(Counters), cudaHostAllocMapped);
+    if (e == cudaSuccess) e = cudaHostGetDevicePointer(reinterpret_cast<void**>(&q->hctr_dev[p]), q->hctr[p], 0);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q->ev_index[p], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q->ev_xfer[p], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q->ev_commit[p], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreate(&q->px[p][0]);
+    if (e == cudaSuccess) e = cudaEventCreate(&q->px[p][1]);
+  }
+  // the transfer kernel is latency-bound on the host link and needs few SM resources,
+  // but it is on the critical path: give its stream the highest priority
+  int lo = 0, hi = 0;
+  if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&q->xfer, cudaStreamNonBlocking, hi);
+  q->xfer_blocks = kSMs;
+  if (const char* env = std::getenv("FC_XFER_BLOCKS")) q->xfer_blocks = std::max(1, std::atoi(env));
+  if (e != cudaSuccess) {
+    pipe_release(h);
+    return cuda_fail(e, "pipeline buffers");
+  }
+  return FC_OK;
+}
+
+struct PipeArgs {
+  float* fast;
+  float* fstate;
+  const float* slow;
+  const float* sstate;
+  int64_t ld, sld;
+  int D, S;
+  uint8_t* dirty;
+  const int32_t* evicted;
+  const int32_t* vslots;
+  const int32_t* admitted;
+  const int32_t* target;
+  int32_t* pending;
+  float* wstage[2];   // write-back stage (AsyncWB)
+  float* wstage_s[2];
+  int32_t* sranks;
+  int32_t* stage_rows;
+  float* astage;
+  float* astage_s;
+  int buf;
+  int32_t cap;
+  int always;
+  Counters* c;
+  Units ud, us;
+};
+
+// counters -> pinned mapped host copy (system-scope stores, visible once the stream event fires)
+__global__ void k_publish(const Counters* __restrict__ c, Counters* host) {
+  const int* src = reinterpret_cast<const int*>(c);
+  int* dst = reinterpret_cast<int*>(host);
+  constexpr int kWords = (int)(sizeof(Counters) / sizeof(int));
+  for (int i = threadIdx.x; i < kWords; i += blockDim.x) dst[i] = src[i];
+  __threadfence_system();
+}
+
+// transfer stream: newest copy of each admitted rank -> admission stage (host link)
+template <bool VEC>
+__global__ void __launch_bounds__(kNT) k_admit_stage(PipeArgs x) {
+  if (!gate_open(x.c, G_ADMIT)) return;
+  const int m = x.c->misses;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  for (int64_t base = warp * 32; base < m; base += nwarps * 32) {
+    const int64_t j = base + lane;
+    const bool act = j < m;
+    const float* src = nullptr;
+    const float* ssrc = nullptr;
+    if (act) {
+      const int r = x.admitted[j];
+      const int pk = x.pending[r];
+      src = pk >= 0 ? x.wstage[pk / x.cap] + (int64_t)(pk % x.cap) * x.D : x.slow + (int64_t)r * x.ld;
+      if (x.S) ssrc = pk >= 0 ? x.wstage_s[pk / x.cap] + (int64_t)(pk % x.cap) * x.S : x.sstate + (int64_t)r * x.sld;
+    }
+    warp_copy_rows<VEC>(src, x.astage + j * x.D, act, x.ud);
+    if (x.S) warp_copy_rows<VEC>(ssrc, x.astage_s + j * x.S, act, x.us);
+  }
+}
+
+// commit: dirty victims (rows already carry the previous batch's update) -> write-back stage
+template <bool VEC>
+__global__ void __launch_bounds__(kNT) k_evict_commit(PipeArgs x) {
+  if (!gate_open(x.c, G_EVICT)) return;
+  const int needed = x.c->needed;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  for (int64_t base = warp * 32; base < needed; base += nwarps * 32) {
+    const int64_t v = base + lane;
+    const bool act = v < needed;
+    int r = 0, s = 0;
+    bool wb = false;
+    if (act) {
+      r = x.evicted[v];
+      s = x.vslots[v];
+      wb = x.always || x.dirty[s];
+    }
+    const unsigned m = __ballot_sync(FC_FULL, wb);
+    int k0 = 0;
+    if (lane == 0 && m) {
+      k0 = atomicAdd(x.stage_rows, __popc(m));
+      atomicAdd(&x.c->wb_rows, __popc(m));
+    }
+    k0 = __shfl_sync(FC_FULL, k0, 0);
+    const int k = k0 + __popc(m & ((1u << lane) - 1u));
+    warp_copy_rows<VEC>(x.fast + (int64_t)s * x.D, x.wstage[x.buf] + (int64_t)k * x.D, wb, x.ud);
+    if (x.S) warp_copy_rows<VEC>(x.fstate + (int64_t)s * x.S, x.wstage_s[x.buf] + (int64_t)k * x.S, wb, x.us);
+    if (wb) {
+      x.sranks[k] = r;
+      x.pending[r] = x.buf * x.cap + k;
+    }
+    if (act) x.dirty[s] = 0;
+  }
+}
+
+// commit: admission stage -> target slots
+template <bool VEC>
+__global__ void __launch_bounds__(kNT) k_admit_commit(PipeArgs x) {
+  if (!gate_open(x.c, G_ADMIT)) return;
+  const int m = x.c->misses;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  for (int64_t base = warp * 32; base < m; base += nwarps * 32) {
+    const int64_t j = base + lane;
+    const bool act = j < m;
+    const int t = act ? x.target[j] : 0;
+    warp_copy_rows<VEC>(x.astage + j * x.D, x.fast + (int64_t)t * x.D, act, x.ud);
+    if (x.S) warp_copy_rows<VEC>(x.astage_s + j * x.S, x.fstate + (int64_t)t * x.S, act, x.us);
+    if (act) x.dirty[t] = 0;
+  }
+}
+
+static PipeArgs pipe_args(fc_cache* h, int p) {
+  AsyncWB* a = h->awb;
+  Pipe* q = h->pipe;
+  PipeArgs x;
+  x.fast = h->fast;
+  x.fstate = h->fast_state;
+  x.slow = h->slow;
+  x.sstate = h->slow_state;
+  x.ld = h->slow_ld;
+  x.sld = h->state_ld;
+  x.D = h->dim;
+  x.S = h->sw;
+  x.dirty = h->dirty;
+  x.evicted = q->ib[p].evicted;
+  x.vslots = q->ib[p].vslots;
+  x.admitted = q->ib[p].admitted;
+  x.target = q->ib[p].target;
+  x.pending = a->pending;
+  x.wstage[0] = a->stage[0];
+  x.wstage[1] = a->stage[1];
+  x.wstage_s[0] = a->sstage[0];
+  x.wstage_s[1] = a->sstage[1];
+  x.sranks = a->sranks[a->cur];
+  x.stage_rows = a->dev_rows + a->cur;
+  x.astage = q->astage[p];
+  x.astage_s = q->astage_s[p];
+  x.buf = a->cur;
+  x.cap = h->capacity;
+  x.always = h->write_back == FC_WB_ALWAYS;
+  x.c = q->ib[p].ctr;
+  x.ud = row_units(h->dim, a->vec);
+  x.us = row_units(h->sw ? h->sw : 4, a->vec);
+  return x;
+}
+
+int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt, int32_t* uranks,
+               int32_t* uslots, int32_t* inverse, cudaStream_t st) {
+  if (h->engine != 1) {
+    set_error("the prefetch pipeline needs the async engine (fc_set_engine(h, 1))");
+    return FC_ERR_BAD_ARG;
+  }
+  if (!h->pipe) {
+    int rc = pipe_create(h);
+    if (rc) return rc;
+  }
+  Pipe* q = h->pipe;
+  if (q->outstanding) {
+    set_error("a prefetched prepare is outstanding: commit it first");
+    return FC_ERR_BAD_ARG;
+  }
+  const int p = q->par;
+  const int o = p ^ 1;
+  // index(t+1) after index(t) (state order) and after commit(t-1) (this parity's buffers)
+  if (q->has_index[o]) FC_CUDA(cudaStreamWaitEvent(st, q->ev_index[o], 0));
+  if (q->has_commit[p]) FC_CUDA(cudaStreamWaitEvent(st, q->ev_commit[p], 0));
+  trace_mark(h, T_INDEX_BEGIN, st);
+  int rc = launch_index_phase(h, ids, ids_bytes, n, uids, ucnt, uranks, uslots, inverse, q->ib[p], st);
+  if (rc) return rc;
+  k_publish<<<1, 32, 0, st>>>(q->ib[p].ctr, q->hctr_dev[p]);
+  FC_CUDA(cudaGetLastError());
+  trace_mark(h, T_INDEX_END, st);
+  FC_CUDA(cudaEventRecord(q->ev_index[p], st));
+  q->has_index[p] = true;
+  // stage(t+1) after index(t+1) and commit(t): pending marks and the stage's last reader
+  FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_index[p], 0));
+  if (q->has_commit[o]) FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_commit[o], 0));
+  if (q->has_commit[p]) FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_commit[p], 0));
+  PipeArgs x = pipe_args(h, p);
+  q->timed[p] = h->profile != 0;
+  if (q->timed[p]) FC_CUDA(cudaEventRecord(q->px[p][0], q->xfer));
+  trace_mark(h, T_XFER_BEGIN, q->xfer);
+  if (h->awb->vec) k_admit_stage<true><<<q->xfer_blocks, kNT, 0, q->xfer>>>(x);
+  else k_admit_stage<false><<<q->xfer_blocks, kNT, 0, q->xfer>>>(x);
+  FC_CUDA(cudaGetLastError());
+  trace_mark(h, T_XFER_END, q->xfer);
+  if (q->timed[p]) FC_CUDA(cudaEventRecord(q->px[p][1], q->xfer));
+  FC_CUDA(cudaEventRecord(q->ev_xfer[p], q->xfer));
+  q->outstanding = true;
+  q->par = o;
+  return FC_OK;
+}
+
+int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
+  Pipe* q = h->pipe;
+  std::memset(info, 0, sizeof(*info));
+  if (!q || !q->outstanding) {
+    set_error("no prefetched prepare to commit");
+    return FC_ERR_BAD_ARG;
+  }
+  const int p = q->par ^ 1;
+  q->outstanding = false;
+  FC_CUDA(cudaEventSynchronize(q->ev_index[p]));
+  const Counters c = *q->hctr[p];
+  h->host_free = c.free_count;
+  info->unique = c.unique;
+  info->free_count = c.free_count;
+  info->candidates = c.candidates;
+  h->last_needed = 0;
+  h->last_misses = 0;
+  if (c.err) {
+    // nothing was mutated; the transfer kernel was gated off as well
+    FC_CUDA(cudaStreamWaitEvent(st, q->ev_xfer[p], 0));
+    FC_CUDA(cudaEventRecord(q->ev_commit[p], st));
+    q->has_commit[p] = true;
+    if (c.err == FC_ERR_ID_OUT_OF_RANGE) info->bad_id = (c.lo != LLONG_MAX) ? c.lo : c.hi;
+    return c.err;
+  }
+  AsyncWB* a = h->awb;
+  const int b = a->cur;
+  if (a->rows_in[b] > 0) {  // write-back stage b still holds a job from two commits ago
+    // the stream (not the host) waits until the host threads have scattered that job;
+    // fall back to a host wait when stream memory operations are unavailable
+    WaitValueFn wv = wait_value_fn();
+    if (!wv || wv(reinterpret_cast<CUstream>(st), a->done_dev, (cuuint32_t)a->seq_of[b], CU_STREAM_WAIT_VALUE_GEQ) !=
+                   CUDA_SUCCESS) {
+      const auto t0 = std::chrono::steady_clock::now();
+      wait_seq(a, a->seq_of[b]);
+      h->prof[5] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    k_clear_pending<<<grid_for(a->rows_in[b], kNT, kSMs * 4), kNT, 0, st>>>(
+        a->sranks[b], a->rows_in[b], a->pending, (int32_t)(b * h->capacity), h->capacity,
+        a->rows_on_dev[b] ? a->dev_rows + b : nullptr);
+    a->rows_in[b] = 0;
+    a->rows_on_dev[b] = false;
+  }
+  FC_CUDA(cudaStreamWaitEvent(st, q->ev_xfer[p], 0));
+  trace_mark(h, T_COMMIT_BEGIN, st);
+  PipeArgs x = pipe_args(h, p);
+  if (c.needed > 0) {
+    FC_CUDA(cudaMemsetAsync(a->dev_rows + b, 0, sizeof(int32_t), st));
+    if (a->vec) k_evict_commit<true><<<kSMs * 8, kNT, 0, st>>>(x);
+    else k_evict_commit<false><<<kSMs * 8, kNT, 0, st>>>(x);
+  }
+  if (c.misses > 0) {
+    if (a->vec) k_admit_commit<true><<<kSMs * 8, kNT, 0, st>>>(x);
+    else k_admit_commit<false><<<kSMs * 8, kNT, 0, st>>>(x);
+  }
+  FC_CUDA(cudaGetLastError());
+  trace_mark(h, T_COMMIT_END, st);
+  FC_CUDA(cudaEventRecord(q->ev_commit[p], st));
+  q->has_commit[p] = true;
+  h->last_wb_dev = c.needed > 0 ? a->dev_rows + b : nullptr;
+  if (c.needed > 0) {  // ship the write-back stage (upper bound: every victim) D2H on the side stream
+    {  // the dispatcher must have consumed d2h[b] of the previous job on stage b before it is re-recorded
+      std::unique_lock<std::mutex> lk(a->m);
+      a->cv_started.wait(lk, [&] { return a->started_seq >= a->seq_of[b]; });
+    }
+    FC_CUDA(cudaStreamWaitEvent(a->side, q->ev_commit[p], 0));
+    FC_CUDA(cudaMemcpyAsync(a->hrows + b, a->dev_rows + b, sizeof(int32_t), cudaMemcpyDeviceToHost, a->side));
+    FC_CUDA(cudaMemcpyAsync(a->hranks[b], a->sranks[b], (size_t)c.needed * 4, cudaMemcpyDeviceToHost, a->side));
+    FC_CUDA(cudaMemcpyAsync(a->hstage[b], a->stage[b], (size_t)c.needed * h->dim * 4, cudaMemcpyDeviceToHost,
+                            a->side));
+    if (h->sw)
+      FC_CUDA(cudaMemcpyAsync(a->hsstage[b], a->sstage[b], (size_t)c.needed * h->sw * 4, cudaMemcpyDeviceToHost,
+                              a->side));
+    FC_CUDA(cudaEventRecord(a->d2h[b], a->side));
+    {
+      std::lock_guard<std::mutex> lk(a->m);
+      const uint64_t seq = a->next_seq++;
+      a->q.push_back(Job{b, -1, seq});
+      a->seq_of[b] = seq;
+    }
+    a->cv_q.notify_one();
+    a->rows_in[b] = c.needed;
+    a->rows_on_dev[b] = true;
+    a->cur ^= 1;
+  }
+  info->misses = c.misses;
+  info->hits = c.unique - c.misses;
+  info->evictions = c.needed;
+  info->rows_to_slow = -1;  // decided on device by the commit (dirty filter); see fc_profile
+  h->last_needed = c.needed;
+  h->last_misses = c.misses;
+  h->ev_src = q->ib[p].evicted;
+  h->ad_src = q->ib[p].admitted;
+  if (h->profile) {
+    // the previous prefetch's transfer kernel is long finished: harvest its time
+    const int o = p ^ 1;
+    if (q->timed[o]) {
+      float ms = 0.f;
+      if (cudaEventSynchronize(q->px[o][1]) == cudaSuccess && cudaEventElapsedTime(&ms, q->px[o][0], q->px[o][1]) == cudaSuccess) {
+        h->prof[1] += ms;
+        h->prof[6] += 1;
+      }
+      q->timed[o] = false;
+    }
+    h->prof[2] += 1;
+    h->prof[3] += 4.0 * h->dim * (double)c.misses;
+    h->prof[4] += 4.0 * h->dim * (double)c.needed;
+  }
+  return FC_OK;
 }
 
 }  // namespace fc

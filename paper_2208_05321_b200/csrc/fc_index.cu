@@ -19,6 +19,12 @@
 
 namespace fc {
 
+#define FC_TRY_I(expr)     \
+  do {                     \
+    int rc__ = (expr);     \
+    if (rc__) return rc__; \
+  } while (0)
+
 // ------------------------------------------------------------------ word sources
 struct ArrWords {
   uint32_t* w;
@@ -314,7 +320,11 @@ struct FreeFin {
   }
 };
 
-__global__ void k_begin(Counters* c) {
+// Reset the per-call counters; the persistent free_count is carried over from the
+// counters of the last call (`src`), which may be another counters block (the
+// prefetch pipeline double-buffers its counters).
+__global__ void k_begin(Counters* c, const Counters* src) {
+  if (src != c) c->free_count = src->free_count;
   c->err = 0;
   c->emitted = 0;
   c->lo = LLONG_MAX;
@@ -356,7 +366,8 @@ static const int32_t* win_admit(Counters* c) {
 }
 
 int launch_reset_counters(fc_cache* h, cudaStream_t st) {
-  k_begin<<<1, 1, 0, st>>>(h->ctr);
+  k_begin<<<1, 1, 0, st>>>(h->ctr, h->live);
+  h->live = h->ctr;
   return FC_OK;
 }
 
@@ -364,7 +375,8 @@ int launch_prepare(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32
                    int32_t* uranks, int32_t* uslots, int32_t* inverse, cudaStream_t st) {
   Counters* c = h->ctr;
   if (h->profile) cudaEventRecord(h->pev[0], st);
-  k_begin<<<1, 1, 0, st>>>(c);
+  k_begin<<<1, 1, 0, st>>>(c, h->live);
+  h->live = c;
   const int gn = grid_for(n, kNT, kSMs * 8);
   const int gm = grid_for(n, kMarkTile, kSMs * 6);
   if (ids_bytes == 8) k_mark_ids<long long><<<gm, kNT, 0, st>>>((const long long*)ids, n, h->num_ids, h->id_bits, h->aux, c);
@@ -416,7 +428,8 @@ __global__ void k_set_needed(Counters* c, int needed) { c->needed = needed; }
 
 int launch_select_evictions(fc_cache* h, int64_t needed, const int64_t* prot, int64_t nprot, cudaStream_t st) {
   Counters* c = h->ctr;
-  k_begin<<<1, 1, 0, st>>>(c);
+  k_begin<<<1, 1, 0, st>>>(c, h->live);
+  h->live = c;
   const int g = grid_for(nprot, kNT, kSMs * 4);
   if (nprot) k_set_prot<<<g, kNT, 0, st>>>(prot, nprot, h->num_ids, h->prot_bits, true);
   k_set_needed<<<1, 1, 0, st>>>(c, (int)needed);
@@ -442,6 +455,7 @@ __global__ void k_warm_state(int32_t k, int32_t* slot_to_rank, int32_t* rank_to_
 }
 
 int launch_warmup_state(fc_cache* h, int64_t k, cudaStream_t st) {
+  FC_TRY_I(launch_reset_counters(h, st));
   k_warm_state<<<grid_for(k, kNT, kSMs * 4), kNT, 0, st>>>((int32_t)k, h->slot_to_rank, h->rank_to_slot, h->dirty,
                                                            h->res_bits, h->free_bits, h->ctr);
   FC_CUDA(cudaGetLastError());
@@ -459,10 +473,91 @@ __global__ void k_set_dirty(const int64_t* __restrict__ s, int64_t n, uint8_t* d
 }
 
 int launch_mark_dirty(fc_cache* h, const int64_t* slots, int64_t n, cudaStream_t st) {
-  k_begin<<<1, 1, 0, st>>>(h->ctr);
+  FC_TRY_I(launch_reset_counters(h, st));
   const int g = grid_for(n, kNT, kSMs * 4);
   k_check_slots<<<g, kNT, 0, st>>>(slots, n, h->capacity, h->ctr);
   k_set_dirty<<<g, kNT, 0, st>>>(slots, n, h->dirty, h->ctr);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+// ------------------------------------------------------------------ prefetch pipeline: index phase
+// Everything Alg. 1 decides and every state-table change it makes, without
+// touching a row or a dirty bit: victims leave the slot tables, admitted ranks
+// take their target slots, and unique_slots are final. The row side runs later:
+// the admitted rows are staged host -> HBM on the transfer stream
+// (k_admit_stage, fc_engine.cu) and the commit phase writes victims back and
+// moves the staged rows into their slots (k_evict_commit / k_admit_commit). So
+// this phase may run while the previous batch's forward/backward still reads
+// and updates rows: those kernels address rows through their own unique_slots.
+
+// victims (descending ranks) -> slots; leave the slot tables; free their slots (:305-308)
+__global__ void k_evict_state(const int32_t* __restrict__ evicted, int32_t* __restrict__ vslots, int32_t* slot_to_rank,
+                              int32_t* rank_to_slot, uint32_t* res, uint32_t* freeb, Counters* c) {
+  if (!gate_open(c, G_EVICT)) return;
+  const int needed = c->needed;
+  for (int v = blockIdx.x * kNT + threadIdx.x; v < needed; v += gridDim.x * kNT) {
+    const int r = evicted[v];
+    const int s = rank_to_slot[r];
+    vslots[v] = s;
+    slot_to_rank[s] = -1;
+    rank_to_slot[r] = -1;
+    atomicAnd(&res[r >> 5], ~(1u << (r & 31)));
+    atomicOr(&freeb[s >> 5], 1u << (s & 31));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) c->free_count += needed;
+}
+
+// admitted ranks (ascending) take the first free slots (ascending) (:310-323)
+__global__ void k_admit_state(const int32_t* __restrict__ admitted, const int32_t* __restrict__ target,
+                              int32_t* slot_to_rank, int32_t* rank_to_slot, uint32_t* res, uint32_t* freeb,
+                              Counters* c) {
+  if (!gate_open(c, G_ADMIT)) return;
+  const int m = c->misses;
+  for (int j = blockIdx.x * kNT + threadIdx.x; j < m; j += gridDim.x * kNT) {
+    const int r = admitted[j];
+    const int s = target[j];
+    slot_to_rank[s] = r;
+    rank_to_slot[r] = s;
+    atomicOr(&res[r >> 5], 1u << (r & 31));
+    atomicAnd(&freeb[s >> 5], ~(1u << (s & 31)));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) c->free_count -= m;
+}
+
+int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt,
+                       int32_t* uranks, int32_t* uslots, int32_t* inverse, const IndexBufs& b, cudaStream_t st) {
+  Counters* c = b.ctr;
+  k_begin<<<1, 1, 0, st>>>(c, h->live);
+  h->live = c;
+  const int gn = grid_for(n, kNT, kSMs * 8);
+  const int gm = grid_for(n, kMarkTile, kSMs * 6);
+  if (ids_bytes == 8) k_mark_ids<long long><<<gm, kNT, 0, st>>>((const long long*)ids, n, h->num_ids, h->id_bits, h->aux, c);
+  else k_mark_ids<int><<<gm, kNT, 0, st>>>((const int*)ids, n, h->num_ids, h->id_bits, h->aux, c);
+  trace_mark(h, 20, st);
+  compact(ArrWords{h->id_bits}, IdFin{h->capacity}, IdEmit{h->aux, uids, 0}, h->nw_ids, h->block_cnt, nullptr, c,
+          G_ALWAYS, st);
+  trace_mark(h, 21, st);
+  const int gu = grid_for(std::min<int64_t>(n, h->capacity), kNT, kSMs * 8);
+  k_unique_info<<<gu, kNT, 0, st>>>(uids, h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, ucnt,
+                                    uranks, uslots, c);
+  if (ids_bytes == 8) k_inverse<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->aux, inverse, c);
+  else k_inverse<int><<<gn, kNT, 0, st>>>((const int*)ids, n, h->aux, inverse, c);
+  trace_mark(h, 22, st);
+  k_plan<<<1, 1, 0, st>>>(c, h->capacity, h->evict_mode, (int64_t)h->dim * 4 <= h->buffer_bytes);
+  compact(CandWords{h->res_bits, h->prot_bits}, EvictFin{}, EvictEmit{b.evicted, 0}, h->nw_ids, h->block_cnt,
+          win_evict(c), c, G_EVICT, st);
+  k_evict_state<<<grid_for(h->capacity, kNT, kSMs * 4), kNT, 0, st>>>(b.evicted, b.vslots, h->slot_to_rank,
+                                                                      h->rank_to_slot, h->res_bits, h->free_bits, c);
+  trace_mark(h, 23, st);
+  compact(ArrWords{h->miss_bits}, AdmitFin{}, RankEmit{b.admitted}, h->nw_ids, h->block_cnt, win_admit(c), c, G_ADMIT,
+          st);
+  compact(ArrWords{h->free_bits}, FreeFin{}, RankEmit{b.target}, h->nw_slots, h->block_cnt2, win_admit(c), c, G_ADMIT,
+          st);
+  k_admit_state<<<grid_for(h->capacity, kNT, kSMs * 4), kNT, 0, st>>>(b.admitted, b.target, h->slot_to_rank,
+                                                                      h->rank_to_slot, h->res_bits, h->free_bits, c);
+  trace_mark(h, 24, st);
+  k_finish<<<gu, kNT, 0, st>>>(uids, uranks, uslots, h->aux, h->rank_to_slot, h->prot_bits, h->miss_bits, c);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }

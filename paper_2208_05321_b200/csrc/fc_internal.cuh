@@ -55,6 +55,16 @@ struct Counters {
 };
 
 struct AsyncWB;  // async write-back engine state (fc_engine.cu)
+struct Pipe;     // prefetch pipeline state (fc_engine.cu)
+
+// Per-prepare index buffers of the prefetch pipeline (double-buffered by batch parity).
+struct IndexBufs {
+  Counters* ctr;
+  int32_t* evicted;   // [C] victim ranks, descending
+  int32_t* vslots;    // [C] their slots
+  int32_t* admitted;  // [C] admitted ranks, ascending
+  int32_t* target;    // [C] their slots, ascending
+};
 
 }  // namespace fc
 
@@ -92,8 +102,9 @@ struct fc_cache {
   int32_t* target_slots;    // [C] ascending
   int32_t* block_cnt;       // [kMaxScanBlocks + 1]
   int32_t* block_cnt2;      // second scan lane (concurrent compactions)
-  fc::Counters* ctr;        // device
+  fc::Counters* ctr;        // device (synchronous verbs)
   fc::Counters* ctr_host;   // pinned mirror
+  fc::Counters* live;       // counters of the last call: holds the current free_count
   cudaEvent_t done;
 
   // scratch for sort-based kernels (backward / scatter_update), grown on demand
@@ -114,11 +125,17 @@ struct fc_cache {
   // optional per-kernel timing (fc_profile): events around the host-link transfer kernel
   int profile;
   cudaEvent_t pev[4];
-  double prof[6];           // prepare_ms, xfer_ms, calls, host-link bytes, evict_ms, index_ms
+  double prof[8];           // prepare_ms, xfer_ms, calls, host-link bytes, write-back bytes, host wait ms,
+                            // timed transfer launches (pipeline)
 
   // async write-back engine (fc_engine.cu); engine 0 = paired zero-copy kernel
   int engine;
   fc::AsyncWB* awb;
+  fc::Pipe* pipe;           // prefetch pipeline (fc_prepare_begin / fc_prepare_commit), lazily created
+  void* trace;              // std::vector of tagged events (fc_trace), NULL when off
+  const int32_t* last_wb_dev; // device count of the last pipeline commit's write-backs (or NULL)
+  const int32_t* ev_src;    // device lists read by fc_last_events (last prepare's buffers)
+  const int32_t* ad_src;
 };
 
 namespace fc {
@@ -131,11 +148,23 @@ int engine_after_prepare(fc_cache* h, cudaStream_t st);      // after the prepar
 int engine_drain(fc_cache* h);                               // all write-backs landed in the slow tier
 void engine_release(fc_cache* h);
 void engine_stats(fc_cache* h, double* out);                 // host scatter ms, jobs (then reset)
+// prefetch pipeline (fc_engine.cu)
+int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt, int32_t* uranks,
+               int32_t* uslots, int32_t* inverse, cudaStream_t st);
+int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info);
+bool pipe_outstanding(const fc_cache* h);
+int pipe_order(fc_cache* h, cudaStream_t st);
+int pipe_sync_commits(fc_cache* h);
+void pipe_release(fc_cache* h);
 }  // namespace fc
 
 namespace fc {
 
 void set_error(const char* fmt, ...);
+// timeline tracing (fc_trace): record a tagged event on `st` when tracing is on
+void trace_mark(fc_cache* h, int tag, cudaStream_t st);
+enum TraceTag : int { T_INDEX_BEGIN = 1, T_INDEX_END = 2, T_XFER_BEGIN = 3, T_XFER_END = 4, T_COMMIT_BEGIN = 5,
+                      T_COMMIT_END = 6, T_HOST_WAIT_END = 7 };
 int cuda_fail(cudaError_t e, const char* what);
 
 #define FC_CUDA(call)                                 \
@@ -168,6 +197,8 @@ int launch_select_evictions(fc_cache* h, int64_t needed, const int64_t* prot, in
 int launch_warmup_state(fc_cache* h, int64_t k, cudaStream_t st);
 int launch_mark_dirty(fc_cache* h, const int64_t* slots, int64_t n, cudaStream_t st);
 int launch_reset_counters(fc_cache* h, cudaStream_t st);
+int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt,
+                       int32_t* uranks, int32_t* uslots, int32_t* inverse, const IndexBufs& b, cudaStream_t st);
 
 // row kernels (fc_rows.cu)
 int launch_evict_rows(fc_cache* h, cudaStream_t st);

@@ -66,6 +66,9 @@ class DeviceCache:
         self.rank_of = view(v.rank_of, (self.num_ids,), "<i4")
         self._slow = None
         self._slow_state = None
+        # prefetch pipeline: run the index phase on the caller's stream (serialised with
+        # the forward/backward; only the miss staging overlaps) or on a side stream
+        self.index_on_main = False
 
     # ------------------------------------------------------------------ plumbing
     def stream(self):
@@ -103,10 +106,26 @@ class DeviceCache:
 
     def profile(self, enable: bool) -> dict:
         """Toggle per-kernel CUDA-event timing; returns (and resets) the totals so far."""
-        out = (ctypes.c_double * 8)()
+        out = (ctypes.c_double * 9)()
         check(self.lib.fc_profile(self.h, int(bool(enable)), out))
         return {"prepare_ms": out[0], "transfer_ms": out[1], "calls": int(out[2]), "host_link_bytes": out[3],
-                "writeback_bytes": out[4], "host_wait_ms": out[5], "scatter_ms": out[6], "scatter_jobs": int(out[7])}
+                "writeback_bytes": out[4], "host_wait_ms": out[5], "scatter_ms": out[6], "scatter_jobs": int(out[7]),
+                "transfer_launches": int(out[8])}
+
+    def trace(self, enable: bool) -> None:
+        """Timeline tracing of the pipeline (fc_trace)."""
+        check(self.lib.fc_trace(self.h, int(bool(enable))))
+
+    def trace_mark(self, tag: int, stream=None) -> None:
+        s = self.stream() if stream is None else ctypes.c_void_p(stream.cuda_stream)
+        check(self.lib.fc_trace_mark(self.h, int(tag), s))
+
+    def trace_read(self, max_events: int = 100000):
+        tags = np.zeros(max_events, np.int32)
+        ms = np.zeros(max_events, np.float64)
+        n = int(self.lib.fc_trace_read(self.h, tags.ctypes.data_as(ctypes.c_void_p), ms.ctypes.data_as(ctypes.c_void_p),
+                                       max_events))
+        return tags[:n], ms[:n]
 
     def to_device_ids(self, ids):
         """Accept numpy / list / torch ids; return a contiguous CUDA int64/int32 tensor."""
@@ -159,6 +178,84 @@ class DeviceCache:
         check(rc)
         u = int(info.unique)
         return info, uids[:u], ucnt[:u], uranks[:u], uslots[:u], inverse, d_ids
+
+    # ------------------------------------------------------------------ prefetch pipeline
+    @property
+    def prefetch_outstanding(self) -> bool:
+        return getattr(self, "_pf", None) is not None
+
+    def prepare_begin(self, ids, batch_seq: int = 0, index_on_main: bool | None = None):
+        """Launch the next batch's prepare ahead of time (fc_prepare_begin): the index
+        phase runs on this cache's index stream and the admitted rows are staged
+        host -> HBM on the library's transfer stream, both overlapping whatever the
+        current stream is still running (the previous batch's forward/backward).
+        The result is claimed with prepare_commit()."""
+        torch = self.torch
+        if self.prefetch_outstanding:
+            raise RuntimeError("a prefetched prepare is outstanding: commit it first")
+        if getattr(self, "index_stream", None) is None:
+            # highest priority: the index phase is short but on the pipeline's critical
+            # path, and must not queue behind the previous batch's backward blocks
+            self.index_stream = torch.cuda.Stream(self.device, priority=-100)
+        main = torch.cuda.current_stream(self.device)
+        if index_on_main is None:
+            index_on_main = self.index_on_main
+        idx = main if index_on_main else self.index_stream
+        with torch.cuda.stream(idx):
+            # allocated on the index stream (no reuse hazard with blocks main still uses),
+            # then marked as used by main, which consumes them after the commit
+            d_ids = self.to_device_ids(ids)
+            n = int(d_ids.numel())
+            if n == 0:
+                raise ValueError("prefetch needs a non-empty batch")
+            k = min(n, self.capacity)
+            buf = torch.empty(4 * k + n, dtype=torch.int32, device=self.device)
+        d_ids.record_stream(main)
+        buf.record_stream(main)
+        check(self.lib.fc_prepare_begin(self.h, ctypes.c_void_p(_ptr(d_ids)), d_ids.element_size(), n, int(batch_seq),
+                                        ctypes.c_void_p(_ptr(buf[:k])), ctypes.c_void_p(_ptr(buf[k:2 * k])),
+                                        ctypes.c_void_p(_ptr(buf[2 * k:3 * k])),
+                                        ctypes.c_void_p(_ptr(buf[3 * k:4 * k])), ctypes.c_void_p(_ptr(buf[4 * k:])),
+                                        ctypes.c_void_p(idx.cuda_stream)))
+        self._pf = (buf, k, d_ids, ids)
+
+    def prepare_commit(self):
+        """Finish the outstanding prefetch on the current stream (fc_prepare_commit).
+        Returns what prepare() returns; info.rows_to_slow is -1 (decided on device)."""
+        if not self.prefetch_outstanding:
+            raise RuntimeError("no prefetched prepare to commit")
+        buf, k, d_ids, obj = self._pf
+        self._pf = None
+        self._last_pf = (obj, d_ids)
+        info = _lib.PrepareInfo()
+        check(self.lib.fc_prepare_commit(self.h, self.stream(), ctypes.byref(info)))
+        u = int(info.unique)
+        return info, buf[:u], buf[k:k + u], buf[2 * k:2 * k + u], buf[3 * k:3 * k + u], buf[4 * k:], d_ids
+
+    def last_writebacks(self) -> int:
+        """Rows written back by the last commit (waits for its kernels)."""
+        v = ctypes.c_int64()
+        check(self.lib.fc_last_writebacks(self.h, ctypes.byref(v)))
+        return int(v.value)
+
+    def prefetched_ids(self):
+        """The ids object passed to the outstanding prepare_begin (or None)."""
+        return self._pf[3] if self.prefetch_outstanding else None
+
+    def committed_matches(self, ids) -> bool:
+        """After prepare_commit: was the committed batch `ids`? Same object, or equal
+        contents (compared after the commit, so the index stream's copy is complete)."""
+        pf = getattr(self, "_last_pf", None)
+        if pf is None:
+            return False
+        obj, d_ids = pf
+        if obj is ids:
+            return True
+        torch = self.torch
+        b = ids if isinstance(ids, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(ids))
+        if b.numel() != d_ids.numel():
+            return False
+        return bool(torch.equal(d_ids.reshape(-1).long(), b.reshape(-1).to(d_ids.device).long()))
 
     def last_events(self, evictions: int, misses: int):
         ev = np.empty(evictions, dtype=np.int64)

@@ -109,26 +109,45 @@ class CachedEmbeddingBag(torch.nn.Module):
         self._generation = 0
         self.last_info = None
 
+    def prefetch(self, indices) -> None:
+        """Start the cache work of the NEXT batch now (the paper's future-work prefetch,
+        PAPER.md:490): its index phase runs on a side stream and its misses are staged
+        host -> HBM on the transfer stream while this batch's backward still runs.
+        Call it after forward(batch t) and before backward(t); the next forward with
+        the same `indices` object commits it. Cache decisions, slot assignment and
+        write-backs are bit-identical to not prefetching."""
+        self.cache.prepare_begin(indices)
+
     def forward(self, indices, offsets=None, per_sample_weights=None):
         dev = self.cache.device
-        indices = indices.to(dev, non_blocking=True).reshape(-1)
+        n = int(indices.numel())
         if offsets is not None:
             offsets = offsets.to(dev, non_blocking=True).contiguous()
             n_bags = int(offsets.numel()) - (1 if self.include_last_offset else 0)
         else:
-            n_bags = int(indices.numel())
+            n_bags = n
         if per_sample_weights is not None:
             if per_sample_weights.requires_grad:
                 raise NotImplementedError("gradients w.r.t. per_sample_weights are not supported")
             per_sample_weights = per_sample_weights.to(dev, dtype=torch.float32).reshape(-1).contiguous()
-        info, uids, ucnt, uranks, uslots, inverse, _ = self.cache.prepare(indices)
+        res = None
+        if self.cache.prefetch_outstanding:  # the prefetched batch is executed first (its commit)
+            res = self.cache.prepare_commit()
+            if not self.cache.committed_matches(indices):
+                res = None
+        if res is None:
+            res = self.cache.prepare(indices.to(dev, non_blocking=True).reshape(-1))
+        info, uids, ucnt, uranks, uslots, inverse, _ = res
         self._generation += 1
         self.last_info = info
-        prep = {"uslots": uslots, "inverse": inverse, "ucnt": ucnt, "u": int(info.unique), "n": int(indices.numel())}
+        prep = {"uslots": uslots, "inverse": inverse, "ucnt": ucnt, "u": int(info.unique), "n": n}
         return _CachedBagFn.apply(self._anchor, self, prep, offsets, n_bags, per_sample_weights)
 
     def flush(self) -> int:
-        """Write every dirty cached row (and optimizer state) back to host memory."""
+        """Write every dirty cached row (and optimizer state) back to host memory.
+        An outstanding prefetch is committed first (its batch becomes resident)."""
+        if self.cache.prefetch_outstanding:
+            self.cache.prepare_commit()
         return self.cache.flush()
 
     def weight(self) -> np.ndarray:

@@ -1,0 +1,238 @@
+"""GPU parity of the prefetch pipeline (fc_prepare_begin / fc_prepare_commit).
+
+Batch t+1's prepare is launched BEFORE batch t's row update runs (the update is
+queued on the main stream after the prefetch), exactly the overlap the pipeline
+exists for. Everything must stay bit-identical to the sequential reference order
+prepare(t) -> update(t) -> prepare(t+1): unique ids / ranks / counts / slots,
+hits / misses / evictions, evicted and admitted lists, transfer reports, slot
+tables, dirty bits and the post-flush slow tier (reference:
+/root/reference/pkg/src/freqcache/cache_manager.py:234-348, simulator.py:416-461)."""
+
+import hashlib
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+from conftest import load_golden, split  # noqa: E402
+from _replay import batches, expect_batch_rows, sim_inputs  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+import paper_2208_05321_b200 as fc  # noqa: E402
+from paper_2208_05321_b200 import cache_manager as cm  # noqa: E402
+from paper_2208_05321_b200.embedding import CachedEmbeddingBag  # noqa: E402
+
+
+def golden_stack(g, write_back):
+    num_ids, cap, dim, buf, _ = (int(v) for v in g["meta"])
+    idx = fc.IdxMap(rank_of=g["rank_of"], id_of=g["id_of"])
+    ref = np.empty((num_ids, dim), np.float32)
+    ref[g["id_of"]] = g["slow0"]
+    return fc.CacheStack(idx, fc.SlowTierStore(g["slow0"].copy()), fc.FastTierStore(np.zeros((cap, dim), np.float32)),
+                         fc.Transmitter(buffer=fc.TransferBuffer(buf)), reference=fc.ReferenceStore(ref),
+                         write_back=write_back, log_events=True, engine="async")
+
+
+@pytest.mark.parametrize("name", ["stream_dirty_zipf", "stream_always_zipf", "stream_dirty_ident"])
+def test_prefetched_golden_stream(name):
+    g = load_golden(name)
+    st = golden_stack(g, "always" if int(g["meta"][4]) else "dirty_only")
+    ids = split(g["ids"], g["ids_off"])
+    deltas = split(g["deltas"], g["ids_off"])
+    want = {k: split(g[k], g[k + "_off"]) for k in
+            ("unique_ids", "unique_ranks", "unique_counts", "unique_slots", "evicted", "admitted")}
+    p = st.prepare(ids[0], 0)
+    for b in range(len(ids)):
+        got = {"unique_ids": p.unique_ids, "unique_ranks": p.unique_ranks, "unique_counts": p.unique_counts,
+               "unique_slots": p.unique_slots, "evicted": st.events[-1].evicted_ranks,
+               "admitted": st.events[-1].admitted_ranks}
+        for k in want:
+            assert np.array_equal(got[k], want[k][b]), (b, k)
+        rep = np.zeros(6, np.int64)
+        for r in p.transfer_reports:
+            o = 0 if r.direction == "to_slow" else 3
+            rep[o:o + 3] += (r.rows, r.bytes, r.messages)
+        assert np.array_equal(np.concatenate([[p.hits, p.misses, p.evictions], rep]), g["scalars"][b]), b
+        if b + 1 < len(ids):
+            st.prefetch(ids[b + 1], b + 1)  # batch b+1's prepare is in flight ...
+        st.scatter_update(p, deltas[b])     # ... while batch b's update is queued behind it
+        if b + 1 < len(ids):
+            p = st.prepare(ids[b + 1], b + 1)  # commit
+    f = st.flush()
+    assert [f.rows, f.bytes, f.messages] == g["flush"].tolist()
+    assert np.array_equal(st.state.slot_to_rank, g["slot_to_rank"])
+    assert np.array_equal(st.state.rank_to_slot, g["rank_to_slot"])
+    assert np.array_equal(st.state.dirty, g["dirty"]) and st.state.free_count == int(g["free_count"])
+    assert np.array_equal(st.slow.rows, g["slow_final"])  # bitwise
+    assert st.first_divergence() is None
+
+
+@pytest.mark.parametrize("name", ["sim_small", "sim_small_always", "sim_medium"])
+def test_prefetched_simulator_run(name):
+    g = load_golden(name)
+    s = sim_inputs(g)
+    idx = fc.build_reorder(fc.scan_frequencies(s["trace"], s["num_ids"]))
+    slow, _, ref = fc.init_stores(s["num_ids"], s["dim"], s["capacity"] / s["num_ids"], s["init_seed"], idx)
+    fast = fc.FastTierStore(np.zeros((s["capacity"], s["dim"]), np.float32))
+    st = fc.CacheStack(idx, slow, fast, fc.Transmitter(buffer=fc.TransferBuffer(s["buffer_bytes"])), reference=ref,
+                       write_back=s["write_back"], log_events=True, engine="async")
+    st.warmup(s["capacity"])
+    colw = fc.update_column_weights(s["dim"], s["updates_seed"])
+    bl = list(batches(s["trace"], s["batch_size"]))
+    rows = []
+    p = st.prepare(bl[0][1], 0)
+    for i, (seq, _) in enumerate(bl):
+        tf = sum(r.rows for r in p.transfer_reports if r.direction == "to_fast")
+        ts = sum(r.rows for r in p.transfer_reports if r.direction == "to_slow")
+        rows.append([p.num_unique, p.hits, p.misses, p.evictions, tf, ts, tf * s["dim"] * 4, ts * s["dim"] * 4,
+                     sum(r.messages for r in p.transfer_reports)])
+        if i + 1 < len(bl):
+            st.prefetch(bl[i + 1][1], bl[i + 1][0])
+        st.gather_unique(p)
+        st.apply_synthetic_update(p, seq, s["updates_seed"], colw)
+        if i + 1 < len(bl):
+            p = st.prepare(bl[i + 1][1], bl[i + 1][0])
+    st.flush()
+    torch.cuda.synchronize()
+    pb, evicted, admitted = expect_batch_rows(g)
+    assert np.array_equal(np.array(rows, np.int64), pb)
+    evs = [e for e in st.events if e.batch_seq >= 0]
+    for b, e in enumerate(evs):
+        assert np.array_equal(e.evicted_ranks, evicted[b]), b
+        assert np.array_equal(e.admitted_ranks, admitted[b]), b
+    assert np.array_equal(st.state.slot_to_rank, g["slot_to_rank"])
+    assert np.array_equal(st.state.dirty, g["dirty"])
+    assert hashlib.sha256(st.slow.rows.tobytes()).hexdigest() == str(g["slow_final_sha"])
+
+
+@pytest.mark.parametrize("num_ids,cap,dim,nb,bsz,always", [
+    (50_000, 3_000, 32, 40, 2_000, False),
+    (200_000, 12_000, 128, 12, 9_000, True),
+    (3_000, 400, 16, 60, 350, False),   # tiny cache: ranks bounce out and back while their write-back is pending
+    (5_000, 900, 8, 50, 600, False),
+])
+def test_prefetched_random_parity_vs_oracle(num_ids, cap, dim, nb, bsz, always):
+    rng = np.random.default_rng(num_ids + 1)
+    p = 1.0 / np.arange(1, num_ids + 1) ** 1.05
+    trace = rng.permutation(num_ids)[rng.choice(num_ids, size=(nb, bsz), p=p / p.sum())]
+    rank_of, id_of = oracle.rank_permutation(oracle.frequency_counts(trace, num_ids))
+    ref = oracle.init_rows(num_ids, dim, 3)
+    wb = "always" if always else "dirty_only"
+    orc = oracle.OracleCache(rank_of, ref[id_of].copy(), cap, write_back=wb, buffer_bytes=1 << 16)
+    st = fc.CacheStack(fc.IdxMap(rank_of, id_of), fc.SlowTierStore(ref[id_of].copy()),
+                       fc.FastTierStore(np.zeros((cap, dim), np.float32)),
+                       fc.Transmitter(buffer=fc.TransferBuffer(1 << 16)), write_back=wb, log_events=True,
+                       engine="async")
+    orc.warmup(cap // 2)
+    st.warmup(cap // 2)
+    colw = oracle.column_weights(dim, 9)
+    ids = [trace[b] for b in range(nb)]
+    q = st.prepare(ids[0], 0)
+    for b in range(nb):
+        a = orc.prepare(ids[b], b)
+        for k in ("unique_ids", "unique_ranks", "unique_counts", "unique_slots"):
+            assert np.array_equal(getattr(q, k), a[k]), (b, k)
+        assert (q.hits, q.misses, q.evictions) == (a["hits"], a["misses"], a["evictions"])
+        assert np.array_equal(st.events[-1].evicted_ranks, a["evicted"])
+        assert np.array_equal(st.events[-1].admitted_ranks, a["admitted"])
+        assert np.array_equal(q.slots_for_ids(), orc.occurrence_slots(a))
+        if b + 1 < nb:
+            st.prefetch(ids[b + 1], b + 1)
+        gs = oracle.row_scalars(a["unique_ids"], a["unique_counts"], b, 9)
+        orc.apply_unique_update(a, gs[:, None] * colw[None, :])
+        st.apply_synthetic_update(q, b, 9, colw)
+        if b + 1 < nb:
+            q = st.prepare(ids[b + 1], b + 1)
+    assert st.flush().rows == orc.flush()["rows"]
+    torch.cuda.synchronize()
+    assert np.array_equal(st.state.slot_to_rank, orc.slot_rank)
+    assert np.array_equal(st.state.rank_to_slot, orc.rank_slot)
+    assert np.array_equal(st.slow.rows, orc.slow)
+    st.state.check_invariants()
+
+
+def test_prefetch_errors_and_mixing():
+    num_ids, cap, dim = 64, 4, 8
+    idx = fc.IdxMap(np.arange(num_ids), np.arange(num_ids))
+    slow, _, ref = fc.init_stores(num_ids, dim, cap / num_ids, init_seed=1, idx_map=idx)
+    st = fc.CacheStack(idx, slow, fc.FastTierStore(np.zeros((cap, dim), np.float32)), fc.Transmitter(),
+                       reference=ref, log_events=True, engine="async")
+    st.prepare(np.array([1, 2]), 0)
+    before = (st.state.slot_to_rank.copy(), st.state.rank_to_slot.copy(), st.state.free_count)
+    bad = np.array([1, 2, 3, 4, 5])
+    st.prefetch(bad, 1)
+    with pytest.raises(cm.BatchExceedsCapacity):  # reported at commit; nothing mutated
+        st.prepare(bad, 1)
+    assert np.array_equal(st.state.slot_to_rank, before[0]) and st.state.free_count == before[2]
+    oob = np.array([3, 99])
+    st.prefetch(oob, 2)
+    with pytest.raises(ValueError, match="99"):
+        st.prepare(oob, 2)
+    # a sync verb refuses while a prefetch is outstanding
+    nxt = np.array([7, 8])
+    st.prefetch(nxt, 3)
+    with pytest.raises(Exception):
+        st.state.device.flush()
+    p = st.prepare(nxt, 3)  # commits the prefetch
+    assert (p.hits, p.misses, p.evictions) == (0, 2, 0)
+    # a prefetch of X followed by prepare(Y): X is executed first, then Y
+    x, y = np.array([9, 10]), np.array([11, 12])
+    st.prefetch(x, 4)
+    p = st.prepare(y, 5)
+    assert (p.hits, p.misses, p.evictions) == (0, 2, 2)
+    # X evicted the largest unprotected ranks 8, 7; Y then evicted 10, 9 (identity reorder)
+    assert set(st.state.occupied_ranks().tolist()) == {1, 2, 11, 12}
+    # mix pipelined and synchronous prepares; then flush matches the reference mirror
+    q = st.prepare(np.array([9, 11]), 6)
+    st.scatter_update(q, np.ones((2, dim), np.float32))
+    st.prefetch(np.array([1, 2, 3]), 7)
+    q = st.prepare(np.array([1, 2, 3]), 7)
+    st.scatter_update(q, np.full((3, dim), 0.5, np.float32))
+    st.flush()
+    torch.cuda.synchronize()
+    assert st.first_divergence() is None
+    st.state.check_invariants()
+
+
+@pytest.mark.parametrize("optimizer,mode,bags", [("sgd", "sum", False), ("adagrad", "mean", True)])
+def test_module_prefetch_matches_sequential(optimizer, mode, bags):
+    """Training through CachedEmbeddingBag with prefetch() gives bit-identical tables
+    (and optimizer state) to training without it; both match the dense oracle."""
+    rng = np.random.default_rng(5)
+    num_ids, dim, steps, B = 20_000, 32, 12, 3_000
+    p = 1.0 / np.arange(1, num_ids + 1) ** 1.1
+    trace = rng.permutation(num_ids)[rng.choice(num_ids, size=(steps, B), p=p / p.sum())]
+    w0 = rng.uniform(-0.1, 0.1, (num_ids, dim)).astype(np.float32)
+    idx = fc.build_reorder(fc.scan_frequencies(trace, num_ids))
+    grads = [rng.standard_normal((B // 3 if bags else B, dim)).astype(np.float32) for _ in range(steps)]
+    offs = torch.arange(0, B, 3) if bags else None
+
+    def train(prefetch):
+        m = CachedEmbeddingBag(num_ids, dim, 0.1, mode=mode, weight=w0, idx_map=idx, optimizer=optimizer, lr=0.05)
+        ids = [torch.from_numpy(trace[s]) for s in range(steps)]
+        for s in range(steps):
+            out = m(ids[s], offs)
+            if prefetch and s + 1 < steps:
+                m.prefetch(ids[s + 1])
+            out.backward(torch.from_numpy(grads[s]).cuda())
+        m.flush()
+        return m.weight().copy(), (m.optimizer_state().copy() if optimizer == "adagrad" else None)
+
+    w_seq, s_seq = train(False)
+    w_pf, s_pf = train(True)
+    assert np.array_equal(w_seq, w_pf)
+    if s_seq is not None:
+        assert np.array_equal(s_seq, s_pf)
+    # dense oracle: torch EmbeddingBag + optimizer on the full table
+    emb = torch.nn.EmbeddingBag(num_ids, dim, mode=mode, sparse=True)
+    emb.weight.data = torch.from_numpy(w0.copy())
+    opt = (torch.optim.SGD if optimizer == "sgd" else torch.optim.Adagrad)(emb.parameters(), lr=0.05)
+    for s in range(steps):
+        o = emb(torch.from_numpy(trace[s]), offs if bags else torch.arange(0, B))
+        opt.zero_grad()
+        o.backward(torch.from_numpy(grads[s]))
+        opt.step()
+    np.testing.assert_allclose(w_pf, emb.weight.detach().numpy(), rtol=1e-5, atol=1e-6)

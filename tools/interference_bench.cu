@@ -1,0 +1,191 @@
+// Interference microbenchmark: how much host-link traffic slows a concurrent
+// HBM-bound kernel (and vice versa). Decides how the prefetch pipeline may overlap
+// the miss staging with the forward/backward.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o ib tools/interference_bench.cu
+// Cases (each timed alone and concurrently on two streams, CUDA events):
+//   H  HBM stream copy, 1 GiB, float4, grid = 148*8
+//   Z  zero-copy gather of random 512 B rows from pinned host memory (like k_admit_stage), 67k rows
+//   ZS Z with its blocks limited (grid 148 / 32)
+//   DH cudaMemcpyAsync H2D contiguous 34.5 MB;  DD cudaMemcpyAsync D2H 34.5 MB
+//   BA cudaMemcpyBatchAsync of 67k random 512 B host rows -> HBM (copy engine gather)
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <random>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#define CK(x)                                                             \
+  do {                                                                    \
+    cudaError_t e = (x);                                                  \
+    if (e != cudaSuccess) {                                               \
+      printf("%s: %s (line %d)\n", #x, cudaGetErrorString(e), __LINE__); \
+      exit(1);                                                            \
+    }                                                                     \
+  } while (0)
+
+__global__ void hbm_copy(const float4* __restrict__ a, float4* __restrict__ b, long n) {
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) b[i] = a[i];
+}
+
+// lane i of a warp owns row i; 4 units in flight per lane (mirrors warp_copy_rows)
+template <int U>
+__global__ void zc_gather(const float4* __restrict__ host, float4* __restrict__ dev, const int* __restrict__ idx,
+                          int nrows, int upr) {
+  const int lane = threadIdx.x & 31;
+  const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const long nw = (gridDim.x * (long)blockDim.x) >> 5;
+  for (long base = warp * 32; base < nrows; base += nw * 32) {
+    const long j = base + lane;
+    const long src = j < nrows ? (long)idx[j] : 0;
+    const int total = 32 * upr;
+    for (int u0 = 0; u0 < total; u0 += 32 * U) {
+      float4 v[U];
+      long d[U];
+      bool a[U];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        const int u = u0 + q * 32 + lane;
+        const int rr = u / upr;
+        const int c = u - rr * upr;
+        const long s = __shfl_sync(0xffffffffu, src, rr);
+        a[q] = base + rr < nrows;
+        d[q] = (base + rr) * upr + c;
+        if (a[q]) v[q] = host[s * upr + c];
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q)
+        if (a[q]) dev[d[q]] = v[q];
+    }
+  }
+}
+
+struct Timer {
+  cudaEvent_t a, b;
+  Timer() {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  float ms() {
+    float t;
+    cudaEventElapsedTime(&t, a, b);
+    return t;
+  }
+};
+
+int main() {
+  const long nH = (1L << 30) / 16;  // 1 GiB of float4
+  const int rows = 67438, upr = 32;  // 512 B rows
+  const long table_rows = 33762577;
+  float4 *ha, *hb;
+  CK(cudaMalloc(&ha, nH * 16));
+  CK(cudaMalloc(&hb, nH * 16));
+  float4* host;
+  CK(cudaHostAlloc(&host, table_rows * 512, cudaHostAllocMapped));
+  float4* hostd;
+  CK(cudaHostGetDevicePointer((void**)&hostd, host, 0));
+  float4* zdst;
+  CK(cudaMalloc(&zdst, (long)rows * 512));
+  float4* hstage;
+  CK(cudaHostAlloc(&hstage, (long)rows * 512, cudaHostAllocDefault));
+  std::vector<int> idx(rows);
+  std::mt19937_64 g(1);
+  for (int i = 0; i < rows; ++i) idx[i] = (int)(g() % table_rows);
+  std::sort(idx.begin(), idx.end());
+  int* didx;
+  CK(cudaMalloc(&didx, rows * 4));
+  CK(cudaMemcpy(didx, idx.data(), rows * 4, cudaMemcpyHostToDevice));
+  cudaStream_t s1, s2;
+  CK(cudaStreamCreateWithFlags(&s1, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  // batch copy descriptors
+  std::vector<void*> bsrc(rows), bdst(rows);
+  std::vector<size_t> bsz(rows, 512);
+  for (int i = 0; i < rows; ++i) {
+    bsrc[i] = (char*)host + (long)idx[i] * 512;
+    bdst[i] = (char*)zdst + (long)i * 512;
+  }
+
+  auto H = [&](cudaStream_t s) { hbm_copy<<<148 * 8, 256, 0, s>>>(ha, hb, nH); };
+  auto Z = [&](cudaStream_t s, int grid) { zc_gather<4><<<grid, 256, 0, s>>>(hostd, zdst, didx, rows, upr); };
+  auto ZC = [&](int grid, int threads, int unroll) {
+    return [=](cudaStream_t s) {
+      if (unroll == 8) zc_gather<8><<<grid, threads, 0, s>>>(hostd, zdst, didx, rows, upr);
+      else if (unroll == 16) zc_gather<16><<<grid, threads, 0, s>>>(hostd, zdst, didx, rows, upr);
+      else zc_gather<4><<<grid, threads, 0, s>>>(hostd, zdst, didx, rows, upr);
+    };
+  };
+  auto DH = [&](cudaStream_t s) { cudaMemcpyAsync(zdst, hstage, (long)rows * 512, cudaMemcpyHostToDevice, s); };
+  auto DD = [&](cudaStream_t s) { cudaMemcpyAsync(hstage, zdst, (long)rows * 512, cudaMemcpyDeviceToHost, s); };
+  auto BA = [&](cudaStream_t s) {
+    cudaMemcpyAttributes attr = {};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+    size_t attr_idx = 0, fail = 0;
+    cudaError_t e = cudaMemcpyBatchAsync(bdst.data(), bsrc.data(), bsz.data(), rows, &attr, &attr_idx, 1, &fail, s);
+    if (e != cudaSuccess) printf("batch: %s\n", cudaGetErrorString(e));
+  };
+
+  auto alone = [&](const char* name, auto fn) {
+    Timer t;
+    for (int w = 0; w < 2; ++w) fn(s1);
+    CK(cudaDeviceSynchronize());
+    float best = 1e9;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(t.a, s1);
+      fn(s1);
+      cudaEventRecord(t.b, s1);
+      CK(cudaEventSynchronize(t.b));
+      best = std::min(best, t.ms());
+    }
+    printf("%-28s alone %8.3f ms\n", name, best);
+    return best;
+  };
+  auto both = [&](const char* name, auto f1, auto f2) {
+    Timer t1, t2, t0;
+    float b1 = 1e9, b2 = 1e9;
+    for (int r = 0; r < 5; ++r) {
+      CK(cudaDeviceSynchronize());
+      cudaEventRecord(t0.a, s1);
+      cudaStreamWaitEvent(s2, t0.a, 0);
+      cudaEventRecord(t1.a, s1);
+      cudaEventRecord(t2.a, s2);
+      f1(s1);
+      f2(s2);
+      cudaEventRecord(t1.b, s1);
+      cudaEventRecord(t2.b, s2);
+      CK(cudaDeviceSynchronize());
+      b1 = std::min(b1, t1.ms());
+      b2 = std::min(b2, t2.ms());
+    }
+    printf("%-28s together %8.3f | %8.3f ms\n", name, b1, b2);
+  };
+  const float tH = alone("H  hbm copy 2x1GiB", H);
+  printf("   -> %.0f GB/s\n", 2.0 * nH * 16 / tH / 1e6);
+  const float tZ = alone("Z  zc gather grid 148", [&](cudaStream_t s) { Z(s, 148); });
+  printf("   -> %.1f GB/s\n", rows * 512.0 / tZ / 1e6);
+  alone("Z  zc gather grid 592", [&](cudaStream_t s) { Z(s, 592); });
+  alone("ZS zc gather grid 32", [&](cudaStream_t s) { Z(s, 32); });
+  alone("DH memcpy H2D 34.5MB", DH);
+  alone("DD memcpy D2H 34.5MB", DD);
+
+  const int cfgs[][3] = {{16, 1024, 4}, {32, 1024, 4}, {32, 1024, 8}, {48, 1024, 8}, {64, 512, 8}, {64, 1024, 8},
+                         {32, 512, 16}, {148, 128, 4}, {148, 256, 8}};
+  for (auto& c : cfgs) {
+    char nm[64];
+    snprintf(nm, sizeof nm, "Z grid %d x %d unroll %d", c[0], c[1], c[2]);
+    const float t = alone(nm, ZC(c[0], c[1], c[2]));
+    printf("   -> %.1f GB/s\n", rows * 512.0 / t / 1e6);
+    snprintf(nm, sizeof nm, "H + Z(%d x %d u%d)", c[0], c[1], c[2]);
+    both(nm, H, ZC(c[0], c[1], c[2]));
+  }
+  both("H + Z(148)", H, [&](cudaStream_t s) { Z(s, 148); });
+  both("H + Z(32)", H, [&](cudaStream_t s) { Z(s, 32); });
+  both("H + DH", H, DH);
+  both("H + DD", H, DD);
+
+  both("Z(148) + DD", [&](cudaStream_t s) { Z(s, 148); }, DD);
+
+  return 0;
+}
