@@ -44,6 +44,15 @@ CONFIGS = {
     "criteo_kaggle": dict(num_ids=33_762_577, dim=128, ratio=0.015, alpha=1.05, batch=16384, features=26),
     # BASELINE configs[0] (reference CPU-runnable case)
     "small": dict(num_ids=1_000_000, dim=128, ratio=0.015, alpha=1.05, batch=1024, features=26),
+    # BASELINE configs[2]: Avazu shape, mean pooling with per-sample weights (sum(w*row)/L), 5% cache,
+    # batch 65,536 (the paper's Avazu batch); Zipf(1.05) like the other configs
+    "avazu": dict(num_ids=9_445_823, dim=64, ratio=0.05, alpha=1.05, batch=65536, features=22, mode="mean",
+                  psw=True),
+    # BASELINE configs[4], one GPU's share of the 8-GPU job: 204,184,588 rows / 8 (row-sharded),
+    # uniform ids, 0.5% cache, 65,536 lookups per step (SURVEY 8d instantiation (i)), Adagrad with the
+    # optimizer state cached and written back with its rows
+    "stress": dict(num_ids=25_523_073, dim=128, ratio=0.005, alpha=None, batch=65536, features=1,
+                   optimizer="adagrad"),
 }
 SEED = 1
 UPDATES_SEED = 7
@@ -68,8 +77,11 @@ def make_workload(cfg, n_batches, device=None, keep_counts=False):
     from paper_2208_05321_b200.store import fast_capacity
 
     t0 = time.perf_counter()
-    tr = workload.gen_zipf(cfg["num_ids"], cfg["alpha"], n_batches * cfg["batch"], cfg["features"], SEED,
-                           device=device)
+    if cfg["alpha"] is None:
+        tr = workload.gen_uniform(cfg["num_ids"], n_batches * cfg["batch"], cfg["features"], SEED)
+    else:
+        tr = workload.gen_zipf(cfg["num_ids"], cfg["alpha"], n_batches * cfg["batch"], cfg["features"], SEED,
+                               device=device)
     t1 = time.perf_counter()
     # frequency reorder over the whole trace (simulator.py:363-364)
     if device is not None:
@@ -253,7 +265,7 @@ def ncu_traffic(kernel):
         return None
 
 
-def rooflines(prof, pool_ms, N, D, links, engine="async", pipelined=False):
+def rooflines(prof, pool_ms, N, D, links, engine="async", pipelined=False, psw=False):
     hbm, hbm_src = hbm_peak()
     xfer_ms = prof["transfer_ms"] / max(prof["transfer_launches"] if pipelined else prof["calls"], 1)
     xfer_bytes = prof["host_link_bytes"] / max(prof["calls"], 1)
@@ -272,7 +284,8 @@ def rooflines(prof, pool_ms, N, D, links, engine="async", pipelined=False):
     r_xfer["frac"] = r_xfer["achieved"] / r_xfer["peak"]
     out = [r_xfer]
     if pool_ms:
-        pool_bytes = N * (4 * D + 8) + N * 4 * D  # per occurrence: inverse + slot + row read; per bag: row write
+        # per occurrence: inverse + slot + row read (+ weight); per bag (= occurrence here): row write
+        pool_bytes = N * (4 * D + 8 + (4 if psw else 0)) + N * 4 * D
         pool_avg = float(np.mean(pool_ms))
         r_pool = {"kernel": "k_pool1", "bound": "hbm", "achieved": pool_bytes / (pool_avg * 1e-3) / 1e9, "peak": hbm,
                   "unit": "GB/s", "traffic": ncu_traffic("k_pool1"),
@@ -303,6 +316,12 @@ def run_ours(args, cfg, torch, rank, world):
         samples, counts = samples
     links = host_link_peaks(torch, dev)
     gout = make_grad(N, D, dev)
+    MODE, OPT = cfg.get("mode", "sum"), cfg.get("optimizer", "sgd")
+    psw = None
+    if cfg.get("psw"):  # per-sample weights ~ U(0, 1), seeded, one per lookup
+        g = torch.Generator(device=dev)
+        g.manual_seed(SEED + 2)
+        psw = torch.rand(N, generator=g, device=dev)
 
     def local_batch(s):
         lo = (s * world + rank) * B
@@ -312,8 +331,8 @@ def run_ours(args, cfg, torch, rank, world):
     if not sharded:
         rows = fc.store.pinned_empty((cfg["num_ids"], D))
         fill_pinned(torch, rows, dev, SEED)
-        mod = CachedEmbeddingBag(cfg["num_ids"], D, cfg["ratio"], mode="sum", idx_map=fc.IdxMap(rank_of, id_of),
-                                 optimizer="sgd", lr=LR, slow_rows=rows, warmup=True, engine=args.engine)
+        mod = CachedEmbeddingBag(cfg["num_ids"], D, cfg["ratio"], mode=MODE, idx_map=fc.IdxMap(rank_of, id_of),
+                                 optimizer=OPT, lr=LR, slow_rows=rows, warmup=True, engine=args.engine)
         dcs = [mod.cache]
         shard = None
     else:
@@ -322,9 +341,9 @@ def run_ours(args, cfg, torch, rank, world):
         idx = shard_rows_for_rank(counts, rank, world)
         rows = fc.store.pinned_empty((idx.num_ids, D))
         fill_pinned(torch, rows, dev, SEED + rank)
-        shard = CudaShard(idx.num_ids, D, fc.fast_capacity(idx.num_ids, cfg["ratio"]), rows, idx, optimizer="sgd",
+        shard = CudaShard(idx.num_ids, D, fc.fast_capacity(idx.num_ids, cfg["ratio"]), rows, idx, optimizer=OPT,
                           lr=LR, device=dev, engine=args.engine)
-        mod = RowShardedEmbedding(shard, world, rank, mode="sum", device=dev)
+        mod = RowShardedEmbedding(shard, world, rank, mode=MODE, device=dev)
         dcs = [shard.cache]
         cap = shard.cache.capacity
     dc = dcs[0]
@@ -341,7 +360,7 @@ def run_ours(args, cfg, torch, rank, world):
         lo, hi = local_batch(s)
         ids = ids_dev[lo:hi].reshape(-1)
         if sharded:  # row-sharded training step: id all-to-all, owner caches, row all-to-all
-            out = mod(ids)
+            out = mod(ids, None, psw)
             out.backward(gout)
             stats.append((0, 0, 0, 0, 0))
             return
@@ -352,14 +371,14 @@ def run_ours(args, cfg, torch, rank, world):
         e = step_events[len(pool_ms)] if timed else None  # created before the timed region
         if timed:
             e[0].record(stream)
-        dc.pooled(uslots, inverse, N, out=out_buf)
+        dc.pooled(uslots, inverse, N, per_sample_weights=psw, mode=MODE, out=out_buf)
         if timed:
             e[1].record(stream)
         if pipelined:  # batch s+1's index phase + miss staging overlap this batch's backward
             nlo, nhi = local_batch(s + 1)
             dc.prepare_begin(ids_dev[nlo:nhi].reshape(-1), s + 1)
         if args.step == "train":
-            dc.backward_update(uslots, inverse, ucnt, None, N, False, None, "sum", gout, "sgd", LR, 0.0)
+            dc.backward_update(uslots, inverse, ucnt, None, N, False, psw, MODE, gout, OPT, LR, 1e-10)
         else:
             dc.synthetic(uids, ucnt, uslots, fc.updates.batch_salt(s, UPDATES_SEED), colw)
         if timed:
@@ -412,7 +431,7 @@ def run_ours(args, cfg, torch, rank, world):
     ids_host = torch.from_numpy(samples).pin_memory()
     hb = [ids_host[local_batch(k)[0]:local_batch(k)[1]].reshape(-1) for k in range(n_batches)]
     for k in range(W):  # the first autograd backward starts torch's device thread (~1.4 s, once)
-        mod(hb[k]).backward(gout)
+        mod(hb[k], None, psw).backward(gout)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
@@ -420,7 +439,7 @@ def run_ours(args, cfg, torch, rank, world):
     hits_read = 0
     e0 = W + K + KSTEPS
     for k in range(K):
-        out = mod(hb[e0 + k])  # H2D of the ids inside forward (or inside the previous step's prefetch)
+        out = mod(hb[e0 + k], None, psw)  # H2D of the ids inside forward (or inside the previous step's prefetch)
         if pipelined:
             mod.prefetch(hb[e0 + k + 1])  # next batch's cache work overlaps this backward
         out.backward(gout)  # upstream gradient of the pooled output -> fused SGD on the cached rows
@@ -437,7 +456,7 @@ def run_ours(args, cfg, torch, rank, world):
 
     st_arr = np.array(stats_main, dtype=np.float64)
     uniq, hits, misses, evict, wb = st_arr.mean(axis=0)
-    rl = rooflines(prof, p_ms, N, D, links, args.engine, pipelined)
+    rl = rooflines(prof, p_ms, N, D, links, args.engine, pipelined, psw is not None)
     lookups = N * world  # every rank processes its own B x F ids per step
     res = {
         "metric": METRIC, "value": lookups * K / (total_ms * 1e-3), "unit": "lookups/s", "n_gpus": world,
@@ -446,8 +465,10 @@ def run_ours(args, cfg, torch, rank, world):
         "data": "synthetic: reference gen_zipf stream (seed 1), seeded rows",
         "config": {"workload": args.config, "num_rows": cfg["num_ids"], "dim": D, "cache_ratio": cfg["ratio"],
                    "capacity_per_gpu": cap, "zipf_alpha": cfg["alpha"], "batch_per_gpu": B, "features": F,
-                   "lookups_per_step": lookups, "pooling": "sum, bag size 1",
-                   "step": ("forward (prepare + pooled gather) + fused backward/SGD" if args.step == "train"
+                   "lookups_per_step": lookups,
+                   "pooling": MODE + (" with per-sample weights" if psw is not None else "") + ", bag size 1",
+                   "optimizer": OPT, "ids": "uniform" if cfg["alpha"] is None else f"zipf({cfg['alpha']})",
+                   "step": (f"forward (prepare + pooled gather) + fused backward/{OPT}" if args.step == "train"
                             else "prepare + pooled forward + simulator row update"),
                    "write_back": "dirty_only", "evict_mode": "occupancy_aware", "engine": args.engine,
                    "prefetch": pipelined,

@@ -424,8 +424,8 @@ int fc_prepare(fc_cache* h, const void* ids, int32_t ids_bytes, int64_t n, int64
     h->prof[2] += 1;
     // bytes the bracketed kernel moves over the host link: both directions for the
     // paired engine 0; admissions only for engine 1 (its write-back rides the copy engine)
-    h->prof[3] += 4.0 * h->dim * ((double)c.misses + (h->engine == 1 ? 0 : c.wb_rows));
-    h->prof[4] += 4.0 * h->dim * (double)c.wb_rows;
+    h->prof[3] += 4.0 * (h->dim + h->sw) * ((double)c.misses + (h->engine == 1 ? 0 : c.wb_rows));
+    h->prof[4] += 4.0 * (h->dim + h->sw) * (double)c.wb_rows;
   }
   return FC_OK;
 }

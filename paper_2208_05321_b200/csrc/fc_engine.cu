@@ -977,8 +977,8 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
       q->timed[o] = false;
     }
     h->prof[2] += 1;
-    h->prof[3] += 4.0 * h->dim * (double)c.misses;
-    h->prof[4] += 4.0 * h->dim * (double)c.needed;
+    h->prof[3] += 4.0 * (h->dim + h->sw) * (double)c.misses;
+    h->prof[4] += 4.0 * (h->dim + h->sw) * (double)c.needed;
   }
   return FC_OK;
 }

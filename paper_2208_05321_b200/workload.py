@@ -81,6 +81,19 @@ def gen_zipf(num_ids: int, exponent: float, num_samples: int, features: int, see
                   "num_samples": num_samples, "seed": int(seed)})
 
 
+def gen_uniform(num_ids: int, num_samples: int, features: int, seed: int) -> Trace:
+    """num_samples x features ids drawn uniformly (the eviction/transfer stress stream of
+    BASELINE configs[4]; the reference has no uniform generator, so this one is simply a
+    seeded numpy PCG64 draw, identical for the GPU build and the CPU reference arm)."""
+    if num_samples < 0 or features < 1 or num_ids < 1:
+        raise ValueError("num_samples must be >= 0, features >= 1, num_ids >= 1")
+    dtype = np.int32 if num_ids <= np.iinfo(np.int32).max else np.int64
+    rng = np.random.default_rng(np.random.SeedSequence(seed))
+    out = rng.integers(0, num_ids, size=num_samples * features, dtype=np.int64).astype(dtype)
+    return Trace(num_ids, features, out.reshape(num_samples, features),
+                 {"generator": "uniform", "num_samples": num_samples, "seed": int(seed)})
+
+
 def batches(trace: Trace, batch_size: int):
     """Consecutive windows of batch_size samples, flattened (workload.py:259-270)."""
     if batch_size < 1:
