@@ -9,8 +9,10 @@
 //     occurrences, accumulates coef_j * grad_out[bag(j)] per run of equal rows in
 //     registers (one float4 column unit per lane, kBwdUnroll grad rows in flight)
 //     and stores the sum per unique row; runs cut by chunk boundaries leave
-//     carries that one fix-up pass sums in chunk order; a last pass applies SGD /
-//     Adagrad to every cached row (32 rows per warp). Fixed order -> deterministic.
+//     carries that one fix-up pass sums (a block per split row, its warps summing
+//     contiguous slices of the carry chain, combined in warp order); a last pass
+//     applies SGD / Adagrad to every cached row (32 rows per warp). Fixed order ->
+//     deterministic.
 #include <algorithm>
 
 #include "fc_rowutil.cuh"
@@ -148,7 +150,9 @@ struct BwdArgs {
   Units un;
 };
 
-// Store / carry one finished run of key `key` over sorted positions [a, b) of chunk c
+// One finished run of key `key` over sorted positions [a, b) of chunk c: its sum
+// goes to gu[key] (coalesced) when the run lies inside the chunk, else it is parked
+// as a carry for the fix-up pass.
 __device__ __forceinline__ void bwd_flush(const BwdArgs& x, int64_t c, int64_t j0, int64_t j1, int key, int64_t a,
                                           int64_t b, int prev_key, int next_key, float4 acc, int unit, bool has,
                                           bool first_col) {
@@ -228,52 +232,83 @@ __global__ void __launch_bounds__(kNT) k_bwd_stream(BwdArgs x) {
 }
 
 // Runs cut by chunk boundaries: chunk c's end-open run (slot 1) starts a split
-// group; the following chunks' start-open runs (slot 0) continue it until one is
-// closed at its end. Sum in chunk order, then update the row once.
+// row; the following chunks' start-open runs (slot 0) continue it until one is
+// closed at its end. One block per chunk index; blocks whose chunk starts no
+// chain exit at once. A chain's carries are split into kFixWarps contiguous
+// slices, each summed by one warp (16 loads in flight), and the slices are added
+// in warp order: a hot row spanning hundreds of chunks costs a few latencies,
+// not hundreds. The row's sum lands in gu like every other row's.
+constexpr int kFixWarps = kNT / 32;
+
 __global__ void __launch_bounds__(kNT) k_bwd_fixup(BwdArgs x) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  extern __shared__ float4 part[];  // [kFixWarps][units per row]
+  __shared__ int64_t s_m;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int64_t nchunks = (x.n + kChunk - 1) / kChunk;
-  for (int64_t c = warp; c < nchunks; c += nwarps) {
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
     const int key = x.carry_key[c * 2 + 1];
-    if (key < 0) continue;
-    // extent: chunks c+1 .. c+m whose slot 0 carries `key`; the last one is closed at its end
-    int64_t m = 0;
-    for (int64_t base = c + 1; base < nchunks; base += 32) {
-      const int64_t cc = base + lane;
-      const bool cont = cc < nchunks && x.carry_key[cc * 2] == key;
-      const bool last = cont && !(x.carry_flag[cc * 2] & 2);
-      const unsigned lastm = __ballot_sync(FC_FULL, last);
-      const unsigned contm = __ballot_sync(FC_FULL, cont);
-      if (lastm) {
-        m += __ffs(lastm);
-        break;
+    if (key < 0) continue;  // uniform across the block
+    if (wid == 0) {  // extent: chunks c+1 .. c+m whose slot 0 carries `key`; the last is closed at its end
+      int64_t m = 0;
+      for (int64_t base = c + 1; base < nchunks; base += 32) {
+        const int64_t cc = base + lane;
+        const bool cont = cc < nchunks && x.carry_key[cc * 2] == key;
+        const bool last = cont && !(x.carry_flag[cc * 2] & 2);
+        const unsigned lastm = __ballot_sync(FC_FULL, last);
+        const unsigned contm = __ballot_sync(FC_FULL, cont);
+        if (lastm) {
+          m += __ffs(lastm);
+          break;
+        }
+        m += __popc(contm);
+        if (contm != FC_FULL) break;
       }
-      m += __popc(contm);
-      if (contm != FC_FULL) break;
+      if (lane == 0) s_m = m;
     }
+    __syncthreads();
+    const int64_t m = s_m;
+    // carries in chain order: k = 0 is chunk c's slot 1, k = 1..m are chunks c+k's slot 0
+    const int64_t per = (m + 1 + kFixWarps - 1) / kFixWarps;
+    const int64_t k0 = wid * per, k1 = min(m + 1, k0 + per);
     for (int cu0 = 0; cu0 < x.un.upr; cu0 += 32) {
       const int unit = cu0 + lane;
-      if (unit >= x.un.upr) continue;
-      float4 acc = ld4(x.carry + (c * 2 + 1) * x.D + unit * 4);
-      int64_t t = 0;
-      constexpr int kF = 16;  // a hot row's carries form a long chain: keep 16 loads in flight
-      for (; t + kF <= m; t += kF) {
-        float4 v[kF];
+      const bool has = unit < x.un.upr;
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (has) {
+        int64_t k = k0;
+        constexpr int kF = 16;
+        for (; k + kF <= k1; k += kF) {
+          float4 v[kF];
 #pragma unroll
-        for (int k = 0; k < kF; ++k) v[k] = ld4(x.carry + ((c + 1 + t + k) * 2) * x.D + unit * 4);
+          for (int q = 0; q < kF; ++q) {
+            const int64_t slot = (k + q == 0) ? c * 2 + 1 : (c + k + q) * 2;
+            v[q] = ld4(x.carry + slot * x.D + unit * 4);
+          }
 #pragma unroll
-        for (int k = 0; k < kF; ++k) {
-          acc.x += v[k].x; acc.y += v[k].y; acc.z += v[k].z; acc.w += v[k].w;
+          for (int q = 0; q < kF; ++q) {
+            acc.x += v[q].x; acc.y += v[q].y; acc.z += v[q].z; acc.w += v[q].w;
+          }
         }
+        for (; k < k1; ++k) {
+          const int64_t slot = (k == 0) ? c * 2 + 1 : (c + k) * 2;
+          const float4 v = ld4(x.carry + slot * x.D + unit * 4);
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        part[wid * x.un.upr + unit] = acc;
       }
-      for (; t < m; ++t) {
-        const float4 v = ld4(x.carry + ((c + 1 + t) * 2) * x.D + unit * 4);
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-      }
-      st4(x.gu + (int64_t)key * x.D + unit * 4, acc);
     }
+    __syncthreads();
+    if (wid == 0) {
+      for (int unit = lane; unit < x.un.upr; unit += 32) {
+        float4 acc = part[unit];
+        for (int w = 1; w < kFixWarps; ++w) {
+          const float4 v = part[w * x.un.upr + unit];
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        st4(x.gu + (int64_t)key * x.D + unit * 4, acc);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -376,7 +411,10 @@ int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, cons
   x.un = units_for(D);
   const int grid = grid_for(nchunks * 32, kNT, kSMs * 16);
   k_bwd_stream<<<grid, kNT, 0, st>>>(x);
-  k_bwd_fixup<<<grid, kNT, 0, st>>>(x);
+  const size_t fix_smem = (size_t)kFixWarps * x.un.upr * sizeof(float4);
+  if (fix_smem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_bwd_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                         (int)fix_smem));
+  k_bwd_fixup<<<(int)std::min<int64_t>(nchunks, kSMs * 16), kNT, fix_smem, st>>>(x);
   k_bwd_apply<<<grid_for(u, kNT, kSMs * 8), kNT, 0, st>>>(x, u);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
