@@ -632,8 +632,10 @@ int fc_backward_update(fc_cache* h, const int32_t* uslots, const int32_t* inv, c
   if (!h || (optim != FC_OPT_SGD && optim != FC_OPT_ADAGRAD) || (offsets && off_bytes != 4 && off_bytes != 8))
     return FC_ERR_BAD_ARG;
   DeviceGuard dg(h->device);
-  return launch_backward(h, uslots, inv, ucnt, u, n, offsets, off_bytes, nbags, include_last, psw, mode, grad, optim, lr,
-                         eps, as_stream(stream));
+  cudaStream_t st = as_stream(stream);
+  FC_TRY(launch_backward(h, uslots, inv, ucnt, u, n, offsets, off_bytes, nbags, include_last, psw, mode, grad, optim,
+                         lr, eps, st));
+  return pipe_launch_xfer(h, st);  // deferred miss staging of a prefetched batch runs after this update
 }
 
 }  // extern "C"

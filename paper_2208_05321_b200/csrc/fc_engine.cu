@@ -595,7 +595,17 @@ struct Pipe {
   int par = 0;
   bool outstanding = false;
   int xfer_blocks = kSMs;                  // k_admit_stage grid (one block per SM: enough loads in flight)
+  bool defer_xfer = false;                 // launch the staging after the next row update (fc_backward_update)
+  bool xfer_pending = false;
+  int xfer_par = 0;
+  cudaEvent_t ev_after = nullptr;
 };
+
+#define FC_TRY_E(expr)     \
+  do {                     \
+    int rc__ = (expr);     \
+    if (rc__) return rc__; \
+  } while (0)
 
 bool pipe_outstanding(const fc_cache* h) { return h->pipe && h->pipe->outstanding; }
 
@@ -634,6 +644,7 @@ void pipe_release(fc_cache* h) {
       if (ev) cudaEventDestroy(ev);
   }
   if (q->xfer) cudaStreamDestroy(q->xfer);
+  if (q->ev_after) cudaEventDestroy(q->ev_after);
   delete q;
   h->pipe = nullptr;
 }
@@ -668,6 +679,8 @@ static int pipe_create(fc_cache* h) {
   int lo = 0, hi = 0;
   if (e == cudaSuccess) e = cudaDeviceGetStreamPriorityRange(&lo, &hi);
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&q->xfer, cudaStreamNonBlocking, hi);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q->ev_after, cudaEventDisableTiming);
+  if (const char* env = std::getenv("FC_XFER_AFTER_UPDATE")) q->defer_xfer = std::atoi(env) != 0;
   q->xfer_blocks = kSMs;
   if (const char* env = std::getenv("FC_XFER_BLOCKS")) q->xfer_blocks = std::max(1, std::atoi(env));
   if (e != cudaSuccess) {
@@ -853,10 +866,31 @@ int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* 
   trace_mark(h, T_INDEX_END, st);
   FC_CUDA(cudaEventRecord(q->ev_index[p], st));
   q->has_index[p] = true;
+  q->outstanding = true;
+  q->par = o;
+  q->xfer_pending = true;
+  q->xfer_par = p;
+  if (!q->defer_xfer) return pipe_launch_xfer(h, nullptr);
+  return FC_OK;
+}
+
+// Launch the outstanding prefetch's miss staging on the transfer stream. With
+// `after` set, the staging also waits for everything queued so far on that stream
+// (deferred mode: launched at the end of the row update so that the host-link
+// kernel does not run beside the HBM-bound backward).
+int pipe_launch_xfer(fc_cache* h, cudaStream_t after) {
+  Pipe* q = h->pipe;
+  if (!q || !q->xfer_pending) return FC_OK;
+  q->xfer_pending = false;
+  const int p = q->xfer_par, o = p ^ 1;
   // stage(t+1) after index(t+1) and commit(t): pending marks and the stage's last reader
   FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_index[p], 0));
   if (q->has_commit[o]) FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_commit[o], 0));
   if (q->has_commit[p]) FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_commit[p], 0));
+  if (after) {
+    FC_CUDA(cudaEventRecord(q->ev_after, after));
+    FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_after, 0));
+  }
   PipeArgs x = pipe_args(h, p);
   q->timed[p] = h->profile != 0;
   if (q->timed[p]) FC_CUDA(cudaEventRecord(q->px[p][0], q->xfer));
@@ -867,10 +901,10 @@ int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* 
   trace_mark(h, T_XFER_END, q->xfer);
   if (q->timed[p]) FC_CUDA(cudaEventRecord(q->px[p][1], q->xfer));
   FC_CUDA(cudaEventRecord(q->ev_xfer[p], q->xfer));
-  q->outstanding = true;
-  q->par = o;
   return FC_OK;
 }
+
+
 
 int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
   Pipe* q = h->pipe;
@@ -880,6 +914,7 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
     return FC_ERR_BAD_ARG;
   }
   const int p = q->par ^ 1;
+  FC_TRY_E(pipe_launch_xfer(h, nullptr));  // deferred staging not triggered by an update: launch it now
   q->outstanding = false;
   FC_CUDA(cudaEventSynchronize(q->ev_index[p]));
   const Counters c = *q->hctr[p];
