@@ -84,14 +84,12 @@ def make_workload(cfg, n_batches, device=None, keep_counts=False):
                                device=device)
     t1 = time.perf_counter()
     # frequency reorder over the whole trace (simulator.py:363-364)
-    if device is not None:
-        import torch
+    if device is not None:  # libfreqcache_b200's fc_build_reorder (bincount + stable radix argsort on device)
+        from paper_2208_05321_b200.freq_stats import build_reorder_device
 
-        ids = torch.from_numpy(tr.samples.reshape(-1)).to(device).long()
-        counts = torch.bincount(ids, minlength=cfg["num_ids"])
-        id_of = torch.sort(-counts, stable=True).indices.cpu().numpy().astype(np.int64)
-        counts_np = counts.cpu().numpy() if keep_counts else None
-        del ids, counts
+        freq, idx = build_reorder_device(tr.samples, cfg["num_ids"], device, keep_counts=keep_counts)
+        id_of = idx.id_of
+        counts_np = freq.counts if keep_counts else None
     else:
         counts = np.bincount(tr.samples.reshape(-1), minlength=cfg["num_ids"])
         id_of = np.argsort(-counts, kind="stable").astype(np.int64)

@@ -181,6 +181,16 @@ int fc_mark_dirty(fc_cache* h, const int64_t* slots_dev, int64_t n, void* stream
 int fc_select_evictions(fc_cache* h, int64_t needed, const int64_t* protected_dev, int64_t n_protected,
                         int64_t* slots_host, void* stream);
 
+/* ---- frequency reorder ------------------------------------------------------ */
+/* scan_frequencies + build_reorder (freq_stats.py:97-111, 136-148) on device:
+ * counts = bincount(trace, minlength=num_ids) (int64), id_of = argsort(-counts,
+ * stable) i.e. descending count, ties and unseen ids by ascending id, and
+ * rank_of = its inverse (both int32). ids_dev: n ids, int64 if ids_bytes==8 else
+ * int32. FC_ERR_ID_OUT_OF_RANGE names the smallest negative id, else the largest
+ * id >= num_ids (freq_stats.py:82-90), in *bad_id. Synchronises `stream`. */
+int fc_build_reorder(const void* ids_dev, int32_t ids_bytes, int64_t n, int64_t num_ids, int64_t* counts_dev,
+                     int32_t* id_of_dev, int32_t* rank_of_dev, int64_t* bad_id, void* stream);
+
 /* ---- lookups and updates ---------------------------------------------------- */
 /* Pooled EmbeddingBag forward over cached rows (north star; semantics of
  * torch.nn.functional.embedding_bag; mean+psw = sum(w*row)/L, empty bag -> 0).

@@ -65,6 +65,8 @@ _SIGS = {
                                    c_void_p, c_void_p, c_void_p]),
     "fc_prepare_commit": (c_int32, [c_void_p, c_void_p, POINTER(PrepareInfo)]),
     "fc_last_writebacks": (c_int32, [c_void_p, POINTER(c_int64)]),
+    "fc_build_reorder": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
+                                   POINTER(c_int64), c_void_p]),
     "fc_trace": (c_int32, [c_void_p, c_int32]),
     "fc_trace_mark": (c_int32, [c_void_p, c_int32, c_void_p]),
     "fc_trace_read": (c_int64, [c_void_p, c_void_p, c_void_p, c_int64]),
