@@ -1,0 +1,73 @@
+"""Parity at BASELINE.json's full index sizes (GPU): the real num_ids, capacities and
+batch shapes of configs[1], [2] and [4], with a narrow row width so the numpy oracle
+finishes in seconds (the index work — dedup, lookups, victim choice, slot assignment,
+write-back selection — does not depend on the width; the row kernels are covered at
+width 128 elsewhere). Runs through the prefetch pipeline with the simulator's update
+queued behind each prefetch. Bit-exact per batch (unique ids/ranks/counts/slots,
+hits/misses/evictions, evicted and admitted lists) and at the end (slot tables, dirty
+bits, post-flush slow tier). Reference: cache_manager.py:234-415, simulator.py:416-461."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+import paper_2208_05321_b200 as fc  # noqa: E402
+from paper_2208_05321_b200 import workload  # noqa: E402
+
+CASES = {
+    # configs[1]: Criteo-Kaggle shape
+    "criteo_kaggle": dict(num_ids=33_762_577, ratio=0.015, alpha=1.05, batch=16384, features=26, batches=6),
+    # configs[2]: Avazu shape, 5% cache, batch 65,536 x 22, cold start (eviction-heavy warm-up)
+    "avazu": dict(num_ids=9_445_823, ratio=0.05, alpha=1.05, batch=65536, features=22, batches=4, cold=True),
+    # configs[4] per-GPU share: uniform ids, 0.5% cache, 65,536 lookups per step
+    "stress": dict(num_ids=25_523_073, ratio=0.005, alpha=None, batch=65536, features=1, batches=6),
+}
+DIM = 4
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_fullsize_parity(name):
+    c = CASES[name]
+    n_ids, nb = c["num_ids"], c["batches"]
+    if c["alpha"] is None:
+        tr = workload.gen_uniform(n_ids, nb * c["batch"], c["features"], 11)
+    else:
+        tr = workload.gen_zipf(n_ids, c["alpha"], nb * c["batch"], c["features"], 11, device="cuda")
+    ids = [tr.samples[b * c["batch"]:(b + 1) * c["batch"]].reshape(-1) for b in range(nb)]
+    freq, idx = fc.build_reorder_device(tr.samples, n_ids)
+    assert np.array_equal(freq.counts, oracle.frequency_counts(tr.samples, n_ids))
+    cap = fc.fast_capacity(n_ids, c["ratio"])
+    rng = np.random.default_rng(3)
+    slow0 = rng.standard_normal((n_ids, DIM), dtype=np.float32)
+    orc = oracle.OracleCache(idx.rank_of, slow0.copy(), cap)
+    st = fc.CacheStack(idx, fc.SlowTierStore(slow0.copy()), fc.FastTierStore(np.zeros((cap, DIM), np.float32)),
+                       fc.Transmitter(), log_events=True, engine="async")
+    if not c.get("cold"):
+        orc.warmup(cap)
+        st.warmup(cap)
+    colw = oracle.column_weights(DIM, 5)
+    q = st.prepare(ids[0], 0)
+    for b in range(nb):
+        a = orc.prepare(ids[b], b)
+        for k in ("unique_ids", "unique_ranks", "unique_counts", "unique_slots"):
+            assert np.array_equal(getattr(q, k), a[k]), (name, b, k)
+        assert (q.hits, q.misses, q.evictions) == (a["hits"], a["misses"], a["evictions"]), (name, b)
+        assert np.array_equal(st.events[-1].evicted_ranks, a["evicted"]), (name, b)
+        assert np.array_equal(st.events[-1].admitted_ranks, a["admitted"]), (name, b)
+        if b + 1 < nb:
+            st.prefetch(ids[b + 1], b + 1)
+        g = oracle.row_scalars(a["unique_ids"], a["unique_counts"], b, 5)
+        orc.apply_unique_update(a, g[:, None] * colw[None, :])
+        st.apply_synthetic_update(q, b, 5, colw)
+        if b + 1 < nb:
+            q = st.prepare(ids[b + 1], b + 1)
+    assert st.flush().rows == orc.flush()["rows"]
+    torch.cuda.synchronize()
+    assert np.array_equal(st.state.slot_to_rank, orc.slot_rank)
+    assert np.array_equal(st.state.dirty, orc.dirty)
+    assert np.array_equal(st.slow.rows, orc.slow)  # bitwise, the whole 33.8M-row slow tier
