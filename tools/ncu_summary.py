@@ -24,7 +24,8 @@ def read(rep):
     h, units = rows[0], rows[1]
     res = []
     for r in rows[2:]:
-        d = {"kernel": r[h.index("Kernel Name")].split("(")[0]}
+        name = r[h.index("Kernel Name")].split("(")[0].replace("void ", "").strip()
+        d = {"kernel": name.split("<")[0]}
         for w in WANT:
             if w in h:
                 i = h.index(w)
