@@ -307,7 +307,7 @@ def run_ours(args, cfg, torch, rank, world):
     W, K = args.warmup, args.steps
     D, B, F = cfg["dim"], cfg["batch"], cfg["features"]
     N = B * F
-    n_batches = max(args.trace_batches // world, W + 2 * K + KSTEPS + 2)
+    n_batches = max(args.trace_batches // world, W + 2 * K + 2 * KSTEPS + 2)
     # global batch = world x B samples; this rank's slice is rows [rank*B, (rank+1)*B) of each global batch
     sharded = world > 1 or args.sharded
     samples, rank_of, id_of, cap = make_workload(cfg, n_batches * world, device=dev, keep_counts=sharded)
@@ -354,7 +354,7 @@ def run_ours(args, cfg, torch, rank, world):
     colw = torch.from_numpy(fc.update_column_weights(D, UPDATES_SEED)).to(dev)
     stream = torch.cuda.current_stream(dev)
     stats, pool_ms, bwd_ms = [], [], []
-    step_events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(KSTEPS)]
+    step_events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(2 * KSTEPS)]
 
     def step(s, timed):
         lo, hi = local_batch(s)
@@ -416,6 +416,24 @@ def run_ours(args, cfg, torch, rank, world):
         step(W + K + k, True)
     torch.cuda.synchronize(dev)
     prof = dc.profile(False)
+    # ---- the same kernels isolated: KSTEPS synchronous steps (no prefetch overlap), so the
+    # roofline of each kernel is also reported without the host-link interference
+    prof_iso, p_ms_iso = None, []
+    if pipelined and not sharded:
+        dc.prepare_commit()  # the batch prefetched by the last profiled step is executed first
+        pipelined = False
+        n_contended = len(pool_ms)
+        dc.profile(True)
+        for k in range(KSTEPS):
+            step(W + K + KSTEPS + k, True)
+        torch.cuda.synchronize(dev)
+        prof_iso = dc.profile(False)
+        pipelined = True
+        p_ms_iso = [e[0].elapsed_time(e[1]) for e in pool_ms[n_contended:]]
+        del pool_ms[n_contended:]
+        del stats[-KSTEPS:]
+        lo_n, hi_n = local_batch(W + K + 2 * KSTEPS)
+        dc.prepare_begin(ids_dev[lo_n:hi_n].reshape(-1), W + K + 2 * KSTEPS)
     step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(K)]
     total_ms = ev[0].elapsed_time(ev[K])
     if world > 1:
@@ -437,7 +455,7 @@ def run_ours(args, cfg, torch, rank, world):
     torch.cuda.synchronize(dev)
     t = time.perf_counter()
     hits_read = 0
-    e0 = W + K + KSTEPS
+    e0 = W + K + 2 * KSTEPS
     for k in range(K):
         out = mod(hb[e0 + k], None, psw)  # H2D of the ids inside forward (or inside the previous step's prefetch)
         if pipelined:
@@ -457,6 +475,7 @@ def run_ours(args, cfg, torch, rank, world):
     st_arr = np.array(stats_main, dtype=np.float64)
     uniq, hits, misses, evict, wb = st_arr.mean(axis=0)
     rl = rooflines(prof, p_ms, N, D, links, args.engine, pipelined, psw is not None)
+    rl_iso = rooflines(prof_iso, p_ms_iso, N, D, links, args.engine, False, psw is not None) if prof_iso else None
     lookups = N * world  # every rank processes its own B x F ids per step
     res = {
         "metric": METRIC, "value": lookups * K / (total_ms * 1e-3), "unit": "lookups/s", "n_gpus": world,
@@ -490,6 +509,8 @@ def run_ours(args, cfg, torch, rank, world):
         "gpu_launches": ((KERNELS_PER_STEP if args.step == "sim" else KERNELS_PER_TRAIN_STEP)
                          + (PIPELINE_EXTRA_KERNELS if pipelined else 0)) * K,
         "roofline": rl[0], "roofline_secondary": rl[1] if len(rl) > 1 else None,
+        "roofline_isolated": ({"note": "same kernels in synchronous steps (no prefetch overlap), after the "
+                                       "timed region", **{r["kernel"]: r for r in rl_iso}} if rl_iso else None),
         "host_link": links,
         "clocks": clk.summary(),
     }

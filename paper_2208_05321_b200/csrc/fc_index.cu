@@ -118,7 +118,8 @@ __global__ void __launch_bounds__(kNT) k_bits_emit(WF wf, EM em, int64_t nwords,
 template <class WF, class FIN, class EM>
 static void compact(WF wf, FIN fin, EM em, int64_t nwords, int32_t* cnt, const int32_t* win, Counters* ctr,
                     int gate, cudaStream_t st) {
-  const int nb = grid_for(nwords, 1024, kMaxScanBlocks);
+  // small bitmaps (the slot space) still get enough blocks to emit in parallel
+  const int nb = grid_for(nwords, 128, kMaxScanBlocks);
   const int64_t chunk = (nwords + nb - 1) / nb;
   k_bits_count<WF><<<nb, kNT, 0, st>>>(wf, nwords, chunk, cnt, ctr, gate);
   k_bits_scan<FIN><<<1, 1024, 0, st>>>(cnt, nb, fin, ctr, gate);
@@ -129,7 +130,7 @@ static void compact(WF wf, FIN fin, EM em, int64_t nwords, int32_t* cnt, const i
 // Counts are aggregated per block in a shared-memory hash table before touching
 // global memory: a Zipf head id occurs ~8% of a batch, and per-occurrence (or
 // per-warp) global atomics on its counter serialise in one L2 slice.
-constexpr int kMarkTile = 2048;     // ids per block iteration
+constexpr int kMarkTile = 512;      // ids per block iteration (a batch spans ~800 blocks)
 constexpr int kMarkHash = 4096;     // open-addressing slots (load <= 0.5)
 
 template <typename IdT>
@@ -210,7 +211,11 @@ struct IdEmit {
   }
 };
 
-// per unique id: count, rank (:283), slot or miss (:286-289), protection mark (:299)
+// per unique id: count, rank (:283), slot or miss (:286-289), protection mark (:299).
+// Three dependent random gathers per id (aux, rank_of, rank_to_slot): each thread
+// works on kUiIlp ids at once so their loads overlap.
+constexpr int kUiIlp = 4;
+
 __global__ void __launch_bounds__(kNT) k_unique_info(const int32_t* __restrict__ uids, int32_t* aux,
                                                      const int32_t* __restrict__ rank_of,
                                                      const int32_t* __restrict__ rank_to_slot, uint32_t* prot,
@@ -220,24 +225,39 @@ __global__ void __launch_bounds__(kNT) k_unique_info(const int32_t* __restrict__
   if (!c->emitted) return;
   const int u = c->unique;
   const int lane = threadIdx.x & 31;
+  const int stride = gridDim.x * kNT;
   int misses = 0;
-  for (int base = (blockIdx.x * kNT + threadIdx.x) & ~31; base < u; base += gridDim.x * kNT) {
-    const int p = base + lane;
-    bool m = false;
-    if (p < u) {
-      const int id = uids[p];
-      const int cnt = aux[id];
-      aux[id] = p;  // position in the unique list, read by k_inverse
-      const int r = rank_of[id];
-      const int s = rank_to_slot[r];
-      ucnt[p] = cnt;
-      uranks[p] = r;
-      uslots[p] = s;
-      atomicOr(&prot[r >> 5], 1u << (r & 31));
-      m = s < 0;
-      if (m) atomicOr(&miss[r >> 5], 1u << (r & 31));
+  for (int base = (blockIdx.x * kNT + threadIdx.x) & ~31; base < u; base += stride * kUiIlp) {
+    int id[kUiIlp], cnt[kUiIlp], r[kUiIlp], sl[kUiIlp];
+    bool in[kUiIlp];
+#pragma unroll
+    for (int k = 0; k < kUiIlp; ++k) {
+      const int p = base + k * stride + lane;
+      in[k] = p < u;
+      id[k] = in[k] ? uids[p] : 0;
     }
-    misses += __popc(__ballot_sync(FC_FULL, m));
+#pragma unroll
+    for (int k = 0; k < kUiIlp; ++k) {
+      cnt[k] = in[k] ? aux[id[k]] : 0;
+      r[k] = in[k] ? rank_of[id[k]] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < kUiIlp; ++k) sl[k] = in[k] ? rank_to_slot[r[k]] : 0;
+#pragma unroll
+    for (int k = 0; k < kUiIlp; ++k) {
+      const int p = base + k * stride + lane;
+      bool m = false;
+      if (in[k]) {
+        aux[id[k]] = p;  // position in the unique list, read by k_inverse
+        ucnt[p] = cnt[k];
+        uranks[p] = r[k];
+        uslots[p] = sl[k];
+        atomicOr(&prot[r[k] >> 5], 1u << (r[k] & 31));
+        m = sl[k] < 0;
+        if (m) atomicOr(&miss[r[k] >> 5], 1u << (r[k] & 31));
+      }
+      misses += __popc(__ballot_sync(FC_FULL, m));
+    }
   }
   if (lane == 0 && misses) atomicAdd(&c->misses, misses);
 }
@@ -385,7 +405,8 @@ int launch_prepare(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32
   compact(ArrWords{h->id_bits}, IdFin{h->capacity}, IdEmit{h->aux, uids, 0}, h->nw_ids, h->block_cnt, nullptr, c,
           G_ALWAYS, st);
   const int gu = grid_for(std::min<int64_t>(n, h->capacity), kNT, kSMs * 8);
-  k_unique_info<<<gu, kNT, 0, st>>>(uids, h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, ucnt,
+  k_unique_info<<<grid_for(std::min<int64_t>(n, h->capacity), kNT * kUiIlp, kSMs * 8), kNT, 0, st>>>(
+      uids, h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, ucnt,
                                     uranks, uslots, c);
 
   if (ids_bytes == 8) k_inverse<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->aux, inverse, c);
@@ -539,7 +560,8 @@ int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, i
           G_ALWAYS, st);
   trace_mark(h, 21, st);
   const int gu = grid_for(std::min<int64_t>(n, h->capacity), kNT, kSMs * 8);
-  k_unique_info<<<gu, kNT, 0, st>>>(uids, h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, ucnt,
+  k_unique_info<<<grid_for(std::min<int64_t>(n, h->capacity), kNT * kUiIlp, kSMs * 8), kNT, 0, st>>>(
+      uids, h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, ucnt,
                                     uranks, uslots, c);
   if (ids_bytes == 8) k_inverse<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->aux, inverse, c);
   else k_inverse<int><<<gn, kNT, 0, st>>>((const int*)ids, n, h->aux, inverse, c);
