@@ -10,7 +10,9 @@ the same exact float64 comparisons, so the ranks are identical.
 
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
+from functools import lru_cache
 
 import numpy as np
 
@@ -92,6 +94,68 @@ def gen_uniform(num_ids: int, num_samples: int, features: int, seed: int) -> Tra
     out = rng.integers(0, num_ids, size=num_samples * features, dtype=np.int64).astype(dtype)
     return Trace(num_ids, features, out.reshape(num_samples, features),
                  {"generator": "uniform", "num_samples": num_samples, "seed": int(seed)})
+
+
+# ----------------------------------------------------------------------------- skew presets
+# (workload.py:93-133, 195-248) — the calibrated laws the reference simulator's
+# `preset=` configs use: a named head share covering a named share of accesses.
+
+def expected_head_coverage(num_ids: int, exponent: float, top_fraction: float, shift: float = 0.0) -> float:
+    """Share of accesses on the top ceil(top_fraction * num_ids) ranks under the law."""
+    k = math.ceil(top_fraction * num_ids)
+    return 0.0 if k <= 0 else float(zipf_pmf(num_ids, exponent, shift)[:k].sum())
+
+
+def calibrate_exponent(num_ids: int, top_fraction: float, target_coverage: float, shift: float = 0.0,
+                       lo: float = 1e-3, hi: float = 64.0, iterations: int = 60) -> float:
+    """Bisection on the exponent (head coverage increases with it) until the head share is met."""
+    if not (0.0 < target_coverage < 1.0):
+        raise ValueError("target_coverage must be in (0, 1)")
+    c_lo = expected_head_coverage(num_ids, lo, top_fraction, shift)
+    c_hi = expected_head_coverage(num_ids, hi, top_fraction, shift)
+    if not (c_lo <= target_coverage <= c_hi):
+        raise ValueError(f"target {target_coverage} unreachable in exponent bracket [{lo}, {hi}] "
+                         f"(coverage range [{c_lo:.4f}, {c_hi:.4f}])")
+    for _ in range(iterations):
+        mid = 0.5 * (lo + hi)
+        if expected_head_coverage(num_ids, mid, top_fraction, shift) < target_coverage:
+            lo = mid
+        else:
+            hi = mid
+    return 0.5 * (lo + hi)
+
+
+@dataclass(frozen=True)
+class SkewPreset:
+    features: int
+    top_fraction: float
+    target_coverage: float
+    shift_frac: float
+
+
+PRESETS = {
+    "criteo_like": SkewPreset(features=26, top_fraction=0.0014, target_coverage=0.90, shift_frac=1e-3),
+    "avazu_like": SkewPreset(features=13, top_fraction=0.00012, target_coverage=0.90, shift_frac=5.5e-5),
+}
+
+
+@lru_cache(maxsize=64)
+def preset_params(name: str, num_ids: int) -> tuple[float, float]:
+    """(exponent, shift) of a preset at this id-space size."""
+    if name not in PRESETS:
+        raise ValueError(f"unknown preset {name!r}, have {sorted(PRESETS)}")
+    p = PRESETS[name]
+    shift = p.shift_frac * num_ids
+    return calibrate_exponent(num_ids, p.top_fraction, p.target_coverage, shift), shift
+
+
+def gen_preset(name: str, num_ids: int, num_samples: int, seed: int, features: int | None = None,
+               device=None) -> Trace:
+    exponent, shift = preset_params(name, num_ids)
+    tr = gen_zipf(num_ids, exponent, num_samples, PRESETS[name].features if features is None else features, seed,
+                  shift=shift, device=device)
+    tr.provenance["preset"] = name
+    return tr
 
 
 def batches(trace: Trace, batch_size: int):

@@ -257,6 +257,28 @@ def gen_embedding_bag():
     np.savez_compressed(os.path.join(OUT, "embedding_bag.npz"), **cases)
 
 
+def gen_sim_metrics():
+    """RunMetrics documents of the reference simulator (simulator.py:525-528), without the
+    wall-clock fields, for simulator.run on the GPU path to reproduce exactly."""
+    import json
+
+    docs = {}
+    cfgs = {
+        "preset_2shards_oracle": simulator.SimConfig(preset="criteo_like", num_ids=40_000, num_batches=10,
+                                                     batch_size=200, embedding_dim=12, cache_ratio=0.05,
+                                                     num_shards=2, seed=5, track_oracle=True, log_events=True),
+        "exponent_always_rowwise": simulator.SimConfig(preset=None, exponent=1.05, num_ids=30_000, features=4,
+                                                       num_batches=8, batch_size=300, embedding_dim=8,
+                                                       cache_ratio=0.03, write_back="always",
+                                                       policy="rowwise_transfer", buffer_bytes=4096, seed=9),
+    }
+    for name, cfg in cfgs.items():
+        m = simulator.run(cfg)
+        docs[name] = {"config": {k: v for k, v in vars(cfg).items()}, "metrics": json.loads(m.determinism_json())}
+    with open(os.path.join(OUT, "sim_metrics.json"), "w") as fh:
+        json.dump(docs, fh, sort_keys=True)
+
+
 def main():
     gen_random_stream("stream_dirty_zipf", "dirty_only")
     gen_random_stream("stream_always_zipf", "always", seed=21, init_seed=3)
@@ -273,6 +295,7 @@ def main():
     gen_sharded()
     gen_functions()
     gen_embedding_bag()
+    gen_sim_metrics()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

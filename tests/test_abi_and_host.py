@@ -105,3 +105,20 @@ def test_cache_state_validation_without_gpu():
         fc.CacheState(11, 10)
     st = fc.CacheState(4, 10)
     assert st.free_count == 4 and (st.slot_to_rank == -1).all()
+
+
+def test_simulator_config_and_presets_match_reference_goldens():
+    """The GPU simulator's host side (SimConfig.resolved, preset calibration) against the
+    reference's recorded RunMetrics config (tests/golden/sim_metrics.json)."""
+    import json
+
+    from conftest import GOLDEN
+    from paper_2208_05321_b200 import simulator
+
+    docs = json.load(open(os.path.join(GOLDEN, "sim_metrics.json")))
+    for doc in docs.values():
+        cfg = simulator.SimConfig(**doc["config"])
+        cfg.validate()
+        assert cfg.resolved() == doc["metrics"]["config"]
+    with pytest.raises(NotImplementedError):
+        simulator.SimConfig(policy="lru").validate()
