@@ -578,6 +578,11 @@ void engine_release(fc_cache* h) {
 //   stage(t+1)  after index(t+1) and commit(t) (pending marks, stage reuse);
 //   commit(t+1) after stage(t+1) (and the caller's stream order).
 
+constexpr int kTmaStages = 4;  // k_admit_stage_tma: row groups in flight per block
+constexpr int kTmaBlocks = 64;
+// rows per TMA group so that one stage holds <= 32 KB
+static inline int tma_group_rows(int row_bytes) { return std::max(1, std::min(32, 32768 / row_bytes)); }
+
 struct Pipe {
   IndexBufs ib[2];
   Counters* hctr[2] = {nullptr, nullptr};  // pinned mapped copies of the index counters
@@ -596,6 +601,8 @@ struct Pipe {
   bool outstanding = false;
   int xfer_blocks = kSMs;                  // k_admit_stage grid (one block per SM: enough loads in flight)
   bool defer_xfer = false;                 // launch the staging after the next row update (fc_backward_update)
+  bool tma = false;                        // stage through the bulk-copy engine (k_admit_stage_tma)
+  int tma_blocks = kTmaBlocks;
   bool xfer_pending = false;
   int xfer_par = 0;
   cudaEvent_t ev_after = nullptr;
@@ -681,6 +688,12 @@ static int pipe_create(fc_cache* h) {
   if (e == cudaSuccess) e = cudaStreamCreateWithPriority(&q->xfer, cudaStreamNonBlocking, hi);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&q->ev_after, cudaEventDisableTiming);
   if (const char* env = std::getenv("FC_XFER_AFTER_UPDATE")) q->defer_xfer = std::atoi(env) != 0;
+  // TMA staging needs 16-byte rows at 16-byte aligned addresses (the async engine's vec
+  // condition); FC_XFER_TMA=0 selects the SM-load kernel
+  q->tma = h->awb && h->awb->vec;
+  if (const char* env = std::getenv("FC_XFER_TMA")) q->tma = q->tma && std::atoi(env) != 0;
+  if (const char* env = std::getenv("FC_TMA_BLOCKS")) q->tma_blocks = std::max(1, std::atoi(env));
+
   q->xfer_blocks = kSMs;
   if (const char* env = std::getenv("FC_XFER_BLOCKS")) q->xfer_blocks = std::max(1, std::atoi(env));
   if (e != cudaSuccess) {
@@ -747,6 +760,105 @@ __global__ void __launch_bounds__(kNT) k_admit_stage(PipeArgs x) {
     warp_copy_rows<VEC>(src, x.astage + j * x.D, act, x.ud);
     if (x.S) warp_copy_rows<VEC>(ssrc, x.astage_s + j * x.S, act, x.us);
   }
+}
+
+// ---- TMA bulk-copy staging (sm_100a) -------------------------------------------
+// The same job as k_admit_stage, issued through the bulk-copy (TMA) engine: one
+// thread per block queues cp.async.bulk loads of whole rows (host-mapped slow tier
+// or the HBM write-back stage) into a shared-memory ring tracked by mbarriers, and
+// writes each group of G staged rows back with ONE bulk store (the admission stage is
+// contiguous). Measured (tools/interference_bench.cu, profiles/r01_interference_bench_tma.txt):
+// 50 GB/s alone vs 43 for SM loads, and a concurrent HBM-bound kernel slows by ~5%
+// instead of ~4x — the miss staging can overlap the backward.
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned phase) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
+          smem_u32(b)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(smem)),
+               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)),
+               "r"(bytes)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(32) k_admit_stage_tma(PipeArgs x, int G) {
+  extern __shared__ __align__(128) unsigned char ring[];  // kTmaStages x G x (D + S) floats
+  __shared__ uint64_t bar[kTmaStages];
+  const int lane = threadIdx.x;
+  if (!gate_open(x.c, G_ADMIT)) return;
+  const int m = x.c->misses;
+  const unsigned rb = (unsigned)x.D * 4, sb = (unsigned)x.S * 4;
+  const size_t stage_bytes = (size_t)G * (rb + sb);
+  if (lane == 0) {
+    for (int i = 0; i < kTmaStages; ++i) mbar_init(&bar[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  unsigned phase_bits = 0;
+  const int ngroups = (m + G - 1) / G;
+  // group k of this block = blockIdx.x + k * gridDim.x; up to kTmaStages groups in flight.
+  // The warp resolves a group's sources in parallel (admitted rank, pending mark: one
+  // row per lane), lane 0 arms the stage's mbarrier, every lane queues its own row.
+  int issued = 0, retired = 0;
+  const int mine = ngroups > (int)blockIdx.x ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  while (retired < mine) {
+    if (issued < mine && issued - retired < kTmaStages) {
+      const int st = issued % kTmaStages;
+      if (issued >= kTmaStages) {  // the stage's previous bulk store has finished reading it
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+      }
+      const int g = blockIdx.x + issued * gridDim.x;
+      const int j0 = g * G, cnt = min(G, m - j0);
+      unsigned char* rows = ring + st * stage_bytes;
+      unsigned char* srows = rows + (size_t)G * rb;
+      if (lane == 0) mbar_expect_tx(&bar[st], cnt * (rb + sb));
+      __syncwarp();
+      for (int i = lane; i < cnt; i += 32) {
+        const int r = x.admitted[j0 + i];
+        const int pk = x.pending[r];
+        const float* src = pk >= 0 ? x.wstage[pk / x.cap] + (int64_t)(pk % x.cap) * x.D : x.slow + (int64_t)r * x.ld;
+        bulk_g2s(rows + (size_t)i * rb, src, rb, &bar[st]);
+        if (x.S) {
+          const float* ss =
+              pk >= 0 ? x.wstage_s[pk / x.cap] + (int64_t)(pk % x.cap) * x.S : x.sstate + (int64_t)r * x.sld;
+          bulk_g2s(srows + (size_t)i * sb, ss, sb, &bar[st]);
+        }
+      }
+      ++issued;
+      continue;
+    }
+    // retire the oldest group: wait for its rows, one bulk store per array
+    const int st = retired % kTmaStages;
+    mbar_wait(&bar[st], (phase_bits >> st) & 1u);
+    phase_bits ^= 1u << st;
+    if (lane == 0) {
+      const int g = blockIdx.x + retired * gridDim.x;
+      const int j0 = g * G, cnt = min(G, m - j0);
+      unsigned char* rows = ring + st * stage_bytes;
+      bulk_s2g(x.astage + (int64_t)j0 * x.D, rows, cnt * rb);
+      if (x.S) bulk_s2g(x.astage_s + (int64_t)j0 * x.S, rows + (size_t)G * rb, cnt * sb);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    __syncwarp();
+    ++retired;
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
 // commit: dirty victims (rows already carry the previous batch's update) -> write-back stage
@@ -895,8 +1007,17 @@ int pipe_launch_xfer(fc_cache* h, cudaStream_t after) {
   q->timed[p] = h->profile != 0;
   if (q->timed[p]) FC_CUDA(cudaEventRecord(q->px[p][0], q->xfer));
   trace_mark(h, T_XFER_BEGIN, q->xfer);
-  if (h->awb->vec) k_admit_stage<true><<<q->xfer_blocks, kNT, 0, q->xfer>>>(x);
-  else k_admit_stage<false><<<q->xfer_blocks, kNT, 0, q->xfer>>>(x);
+  if (q->tma) {  // bulk-copy engine: rows are 16-byte multiples at 16-byte aligned addresses
+    const int G = tma_group_rows((h->dim + h->sw) * 4);
+    const size_t smem = (size_t)kTmaStages * G * (h->dim + h->sw) * 4;
+    if (smem > 48 * 1024)
+      FC_CUDA(cudaFuncSetAttribute(k_admit_stage_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_admit_stage_tma<<<q->tma_blocks, 32, smem, q->xfer>>>(x, G);
+  } else if (h->awb->vec) {
+    k_admit_stage<true><<<q->xfer_blocks, kNT, 0, q->xfer>>>(x);
+  } else {
+    k_admit_stage<false><<<q->xfer_blocks, kNT, 0, q->xfer>>>(x);
+  }
   FC_CUDA(cudaGetLastError());
   trace_mark(h, T_XFER_END, q->xfer);
   if (q->timed[p]) FC_CUDA(cudaEventRecord(q->px[p][1], q->xfer));
@@ -937,7 +1058,7 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
   if (a->rows_in[b] > 0) {  // write-back stage b still holds a job from two commits ago
     // the stream (not the host) waits until the host threads have scattered that job;
     // fall back to a host wait when stream memory operations are unavailable
-    WaitValueFn wv = wait_value_fn();
+    WaitValueFn wv = std::getenv("FC_HOST_WAIT") ? nullptr : wait_value_fn();
     if (!wv || wv(reinterpret_cast<CUstream>(st), a->done_dev, (cuuint32_t)a->seq_of[b], CU_STREAM_WAIT_VALUE_GEQ) !=
                    CUDA_SUCCESS) {
       const auto t0 = std::chrono::steady_clock::now();

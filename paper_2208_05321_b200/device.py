@@ -8,6 +8,7 @@ cache computation happens in the library's sm_100a kernels.
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 
@@ -68,7 +69,7 @@ class DeviceCache:
         self._slow_state = None
         # prefetch pipeline: run the index phase on the caller's stream (serialised with
         # the forward/backward; only the miss staging overlaps) or on a side stream
-        self.index_on_main = False
+        self.index_on_main = os.environ.get("FC_INDEX_ON_MAIN", "0") == "1"
 
     # ------------------------------------------------------------------ plumbing
     def stream(self):
