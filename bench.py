@@ -35,6 +35,8 @@ import numpy as np
 # more hardware work queues than torch's/the library's streams: no false dependencies
 # between the index, transfer, copy-engine and compute streams (set before CUDA init)
 os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+# rank 0 prints exactly one JSON line on stdout: keep NCCL's banner / logs on stderr
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
@@ -356,11 +358,14 @@ def run_ours(args, cfg, torch, rank, world):
     stats, pool_ms, bwd_ms = [], [], []
     step_events = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(2 * KSTEPS)]
 
+    bview = [ids_dev[local_batch(k)[0]:local_batch(k)[1]].reshape(-1) for k in range(n_batches)]
+
     def step(s, timed):
-        lo, hi = local_batch(s)
-        ids = ids_dev[lo:hi].reshape(-1)
-        if sharded:  # row-sharded training step: id all-to-all, owner caches, row all-to-all
+        ids = bview[s]
+        if sharded:  # row-sharded training step: unique-id all-to-all, owner caches, row all-to-all
             out = mod(ids, None, psw)
+            if pipelined:  # next batch's id exchange + owner prepare overlap this backward
+                mod.prefetch(bview[s + 1])
             out.backward(gout)
             stats.append((0, 0, 0, 0, 0))
             return
@@ -375,8 +380,7 @@ def run_ours(args, cfg, torch, rank, world):
         if timed:
             e[1].record(stream)
         if pipelined:  # batch s+1's index phase + miss staging overlap this batch's backward
-            nlo, nhi = local_batch(s + 1)
-            dc.prepare_begin(ids_dev[nlo:nhi].reshape(-1), s + 1)
+            dc.prepare_begin(bview[s + 1], s + 1)
         if args.step == "train":
             dc.backward_update(uslots, inverse, ucnt, None, N, False, psw, MODE, gout, OPT, LR, 1e-10)
         else:
@@ -386,10 +390,9 @@ def run_ours(args, cfg, torch, rank, world):
             pool_ms.append(e)
         stats.append((info.unique, info.hits, info.misses, info.evictions, info.rows_to_slow))
 
-    pipelined = (not sharded) and args.engine == "async" and not args.no_prefetch
-    if pipelined:
-        lo0, hi0 = local_batch(0)
-        dc.prepare_begin(ids_dev[lo0:hi0].reshape(-1), 0)
+    pipelined = args.engine == "async" and not args.no_prefetch
+    if pipelined and not sharded:
+        dc.prepare_begin(bview[0], 0)
     for s in range(W):
         step(s, False)
     torch.cuda.synchronize(dev)
@@ -432,8 +435,7 @@ def run_ours(args, cfg, torch, rank, world):
         p_ms_iso = [e[0].elapsed_time(e[1]) for e in pool_ms[n_contended:]]
         del pool_ms[n_contended:]
         del stats[-KSTEPS:]
-        lo_n, hi_n = local_batch(W + K + 2 * KSTEPS)
-        dc.prepare_begin(ids_dev[lo_n:hi_n].reshape(-1), W + K + 2 * KSTEPS)
+        dc.prepare_begin(bview[W + K + 2 * KSTEPS], W + K + 2 * KSTEPS)
     step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(K)]
     total_ms = ev[0].elapsed_time(ev[K])
     if world > 1:
@@ -444,7 +446,7 @@ def run_ours(args, cfg, torch, rank, world):
     b_ms = [e[1].elapsed_time(e[2]) for e in pool_ms]
 
     # ---- e2e: the public API (module forward+backward) from pinned host ids ----
-    if pipelined and dc.prefetch_outstanding:
+    if pipelined and not sharded and dc.prefetch_outstanding:
         dc.prepare_commit()
     ids_host = torch.from_numpy(samples).pin_memory()
     hb = [ids_host[local_batch(k)[0]:local_batch(k)[1]].reshape(-1) for k in range(n_batches)]

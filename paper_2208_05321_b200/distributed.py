@@ -57,6 +57,14 @@ class CudaShard:
         info, uids, ucnt, uranks, uslots, inverse, _ = self.cache.prepare(ids)
         return {"info": info, "uslots": uslots, "inverse": inverse, "ucnt": ucnt, "n": int(inverse.numel())}
 
+    # prefetch pipeline (DeviceCache.prepare_begin / prepare_commit)
+    def prepare_begin(self, ids):
+        self.cache.prepare_begin(ids)
+
+    def prepare_commit(self):
+        info, uids, ucnt, uranks, uslots, inverse, _ = self.cache.prepare_commit()
+        return {"info": info, "uslots": uslots, "inverse": inverse, "ucnt": ucnt, "n": int(inverse.numel())}
+
     def pool(self, h, offsets=None, n_bags=None, include_last_offset=False, psw=None, mode="sum"):
         return self.cache.pooled(h["uslots"], h["inverse"], h["n"], offsets, n_bags, include_last_offset, psw, mode)
 
@@ -126,7 +134,7 @@ def _lens(offsets, n, include_last_offset):
 class _RowShardFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, anchor, mod, ids, offsets, n_bags, psw):
-        out, saved = mod._forward(ids, offsets, n_bags, psw)
+        out, saved = mod._forward(ids, offsets, n_bags, psw, getattr(mod, "_src", None))
         ctx.mod, ctx.saved = mod, saved
         return out
 
@@ -137,7 +145,15 @@ class _RowShardFn(torch.autograd.Function):
 
 
 class RowShardedEmbedding(torch.nn.Module):
-    """Rows owned by rank `id % world`; ids and rows exchanged with all-to-all."""
+    """Rows owned by rank `id % world`; each rank sends its batch's UNIQUE ids to their
+    owners (all-to-all), owners prepare + gather, rows come back (all-to-all) and are
+    expanded through the inverse. The backward reduces the per-occurrence gradients to
+    one row per unique id before the mirror all-to-all, so both exchanges carry
+    unique rows only (a Zipf batch repeats each id ~3x at the Criteo shape).
+
+    `prefetch(next_ids)` (call after forward(t), before backward(t), on every rank)
+    runs the next batch's id exchange and starts the owner's prepare through the
+    cache's prefetch pipeline; the next forward with the same ids commits it."""
 
     def __init__(self, shard, world: int, rank: int, mode: str = "sum", include_last_offset: bool = False,
                  group=None, device=None):
@@ -147,14 +163,17 @@ class RowShardedEmbedding(torch.nn.Module):
         self.device = device if device is not None else getattr(shard, "device", torch.device("cpu"))
         self._anchor = torch.nn.Parameter(torch.empty(0, device=self.device))
         self.last_recv = 0
+        self._pf = None  # (ids, exchange) of a prefetched batch
 
     @staticmethod
     def owner_of(ids, world):
         return ids % world, ids // world
 
-    def _forward(self, ids, offsets, n_bags, psw):
+    def _exchange_ids(self, ids):
+        """Unique ids of this rank's batch to their owners; returns the routing."""
         W = self.world
-        owner, local = self.owner_of(ids.long(), W)
+        uniq, inv = torch.unique(ids.long(), sorted=True, return_inverse=True)
+        owner, local = self.owner_of(uniq, W)
         order = torch.argsort(owner, stable=True)
         send_ids = local[order]
         send_counts = torch.bincount(owner, minlength=W)
@@ -163,28 +182,62 @@ class RowShardedEmbedding(torch.nn.Module):
         sc, rc = send_counts.tolist(), recv_counts.tolist()
         recv_ids = torch.empty(sum(rc), dtype=send_ids.dtype, device=send_ids.device)
         _a2a(recv_ids, send_ids, rc, sc, self.group)
-        self.last_recv = int(recv_ids.numel())
-        h = self.shard.prepare(recv_ids)
-        rows = self.shard.pool(h)  # [n_recv, D] one row per received id
-        back = torch.empty((ids.numel(), rows.shape[1]), dtype=rows.dtype, device=rows.device)
-        _a2a(back, rows.contiguous(), sc, rc, self.group)
-        local_rows = torch.empty_like(back)
-        local_rows[order] = back
+        return {"inv": inv, "order": order, "sc": sc, "rc": rc, "recv_ids": recv_ids, "u": int(uniq.numel())}
+
+    def prefetch(self, ids):
+        dev_ids = ids.reshape(-1).to(self.device)
+        x = self._exchange_ids(dev_ids)
+        if hasattr(self.shard, "prepare_begin") and x["recv_ids"].numel() > 0:
+            self.shard.prepare_begin(x["recv_ids"])
+            x["begun"] = True
+        x["src"] = ids
+        self._pf = (dev_ids, x)
+
+    def _forward(self, ids, offsets, n_bags, psw, src=None):
+        x, h = None, None
+        if self._pf is not None:
+            pids, px = self._pf
+            self._pf = None
+            if px.get("begun"):
+                hp = self.shard.prepare_commit()  # the prefetched batch is executed first
+            if px["src"] is src or pids is ids or (pids.numel() == ids.numel() and bool(torch.equal(pids, ids))):
+                x = px
+                h = hp if px.get("begun") else None
+        if x is None:
+            x = self._exchange_ids(ids)
+        if h is None:
+            h = self.shard.prepare(x["recv_ids"])
+        self.last_recv = int(x["recv_ids"].numel())
+        rows = self.shard.pool(h)  # [n_recv, D] one row per received (unique per requester) id
+        back = torch.empty((x["u"], rows.shape[1]), dtype=rows.dtype, device=rows.device)
+        _a2a(back, rows.contiguous(), x["sc"], x["rc"], self.group)
+        uniq_rows = torch.empty_like(back)
+        uniq_rows[x["order"]] = back
+        local_rows = uniq_rows[x["inv"]]
         out = pool_rows(local_rows, offsets, n_bags, self.include_last_offset, psw, self.mode)
-        return out, (h, order, sc, rc, int(ids.numel()), offsets, n_bags, psw)
+        return out, (h, x, int(ids.numel()), offsets, n_bags, psw)
 
     def _backward(self, saved, grad_out):
-        h, order, sc, rc, n, offsets, n_bags, psw = saved
+        h, x, n, offsets, n_bags, psw = saved
         g = bag_grads(grad_out, n, offsets, n_bags, self.include_last_offset, psw, self.mode)
-        g_send = g[order].contiguous()
-        g_recv = torch.empty((sum(rc), g.shape[1]), dtype=g.dtype, device=g.device)
-        _a2a(g_recv, g_send, rc, sc, self.group)
+        gu = torch.zeros((x["u"], g.shape[1]), dtype=g.dtype, device=g.device)
+        gu.index_add_(0, x["inv"], g)  # one gradient row per unique id of this rank
+        g_send = gu[x["order"]].contiguous()
+        g_recv = torch.empty((sum(x["rc"]), g.shape[1]), dtype=g.dtype, device=g.device)
+        _a2a(g_recv, g_send, x["rc"], x["sc"], self.group)
         self.shard.backward(h, g_recv)
 
     def forward(self, ids, offsets=None, per_sample_weights=None):
+        self._src = ids
         ids = ids.reshape(-1).to(self.device)
         n_bags = ids.numel() if offsets is None else offsets.numel() - (1 if self.include_last_offset else 0)
         return _RowShardFn.apply(self._anchor, self, ids, offsets, n_bags, per_sample_weights)
+
+    def flush(self) -> int:
+        if self._pf is not None and self._pf[1].get("begun"):
+            self.shard.prepare_commit()
+        self._pf = None
+        return self.shard.flush()
 
 
 # ----------------------------------------------------------------------------- column-wise (reference semantics)

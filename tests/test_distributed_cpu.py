@@ -32,6 +32,14 @@ class OracleShard:
         p = self.c.prepare(ids.numpy())
         return {"p": p, "n": int(ids.numel()), "slots": self.c.occurrence_slots(p)}
 
+    # prefetch: the oracle executes the prepare at commit time (sequential semantics)
+    def prepare_begin(self, ids):
+        self._pending = ids
+
+    def prepare_commit(self):
+        ids, self._pending = self._pending, None
+        return self.prepare(ids)
+
     def pool(self, h, offsets=None, n_bags=None, include_last_offset=False, psw=None, mode="sum"):
         off = np.arange(h["n"]) if offsets is None else offsets.numpy()
         w = None if psw is None else psw.numpy()
@@ -76,7 +84,7 @@ def _free_port():
     return port
 
 
-def _worker(rank, world, port, kind, mode, q):
+def _worker(rank, world, port, kind, mode, q, prefetch=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -95,14 +103,19 @@ def _worker(rank, world, port, kind, mode, q):
             shard = OracleShard(rank_of, np.ascontiguousarray(table[:, a:b])[id_of], NUM // 2, LR)
             mod = ColumnShardedEmbedding(shard, DIM, world, rank, mode=mode)
         dense = table.copy()
-        for step in data:
+        out = None
+        tids = [torch.from_numpy(d[rank][0]) for d in data]
+        for si, step in enumerate(data):
             for r in range(world):  # dense reference of every rank's batch
                 ids, off, gout = step[r]
                 if r == rank:
                     want = oracle.pooled_bag(dense, ids, off, None, mode)
             ids, off, gout = step[rank]
-            out = mod(torch.from_numpy(ids), torch.from_numpy(off) if mode == "mean" else None)
+            t_ids = tids[si] if prefetch else torch.from_numpy(ids)
+            out = mod(t_ids, torch.from_numpy(off) if mode == "mean" else None)
             np.testing.assert_allclose(out.detach().numpy(), want, rtol=1e-5, atol=1e-6)
+            if prefetch and si + 1 < len(data):
+                mod.prefetch(tids[si + 1])  # next batch's exchange + prepare start, before this backward
             out.backward(torch.from_numpy(gout))
             # dense SGD with every rank's batch (each rank owns its own bags' gradients)
             grad = np.zeros((NUM, DIM))
@@ -126,13 +139,13 @@ def _worker(rank, world, port, kind, mode, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind", ["row", "column"])
+@pytest.mark.parametrize("kind,prefetch", [("row", False), ("row", True), ("column", False)])
 @pytest.mark.parametrize("mode", ["sum", "mean"])
-def test_two_rank_gloo_matches_dense(kind, mode):
+def test_two_rank_gloo_matches_dense(kind, mode, prefetch):
     ctx = mp.get_context("fork")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, mode, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, kind, mode, q, prefetch)) for r in range(2)]
     for p in procs:
         p.start()
     res = dict(q.get(timeout=120) for _ in procs)
