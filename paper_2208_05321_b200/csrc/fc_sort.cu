@@ -12,9 +12,9 @@
 
 namespace fc {
 
-constexpr int kRsWarps = 8;
+constexpr int kRsWarps = 16;
 constexpr int kRsRounds = 8;
-constexpr int kRsTile = kRsWarps * kRsRounds * 32;  // 2048 keys per tile
+constexpr int kRsTile = kRsWarps * kRsRounds * 32;  // 4096 keys per tile
 
 // ---------------------------------------------------------------- exclusive scan
 constexpr int kScanTile = kNT * 8;
@@ -76,42 +76,66 @@ int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch
   return FC_OK;
 }
 
-// ---------------------------------------------------------------- radix sort
-// Digits of up to 9 bits (512 bins): keys below 2^18 (U <= 262,144 unique rows)
-// sort in two passes. Each pass = tile histogram -> device-wide scan -> stable scatter.
+// ---------------------------------------------------------------- radix sort (one sweep per pass)
+// Digits of up to 9 bits (512 bins): keys below 2^18 (U <= 262,144 unique rows) sort
+// in two passes. Launches: one global histogram for every pass, then one kernel per
+// pass that ranks a tile of keys, finds the tile's per-digit offset by decoupled
+// look-back over the preceding tiles (tiles are claimed in order from an atomic
+// counter, so a predecessor always makes progress), and scatters. Stable: within a
+// tile the rank follows (warp, round, lane) = input order, across tiles tile order.
 constexpr int kRsMaxBins = 512;
+constexpr uint32_t kOsAgg = 1u << 30;     // status: tile's own count published
+constexpr uint32_t kOsPrefix = 2u << 30;  // status: inclusive prefix published
+constexpr uint32_t kOsMask = (1u << 30) - 1u;
+constexpr int kOsMaxPasses = 4;
 
-__global__ void __launch_bounds__(kRsWarps * 32) k_rs_hist(const uint32_t* __restrict__ keys, int64_t n, int shift,
-                                                           int bins, int32_t* hist, int ntiles) {
-  __shared__ int h[kRsMaxBins];
-  for (int d = threadIdx.x; d < bins; d += blockDim.x) h[d] = 0;
+__global__ void __launch_bounds__(kNT) k_os_hist(const uint32_t* __restrict__ keys, int64_t n, int passes, int dbits,
+                                                 int32_t* ghist) {
+  __shared__ int h[kOsMaxPasses * kRsMaxBins];
+  const int bins = 1 << dbits;
+  for (int d = threadIdx.x; d < passes * bins; d += kNT) h[d] = 0;
   __syncthreads();
-  const int64_t base = (int64_t)blockIdx.x * kRsTile;
-  for (int k = threadIdx.x; k < kRsTile; k += blockDim.x) {
-    const int64_t i = base + k;
-    if (i < n) atomicAdd(&h[(keys[i] >> shift) & (bins - 1)], 1);
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+    const uint32_t k = keys[i];
+    for (int p = 0; p < passes; ++p) atomicAdd(&h[p * bins + ((k >> (p * dbits)) & (bins - 1))], 1);
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < bins; d += blockDim.x) hist[(int64_t)d * ntiles + blockIdx.x] = h[d];
+  for (int d = threadIdx.x; d < passes * bins; d += kNT)
+    if (h[d]) atomicAdd(&ghist[d], h[d]);
 }
 
-__global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const uint32_t* __restrict__ kin,
+__device__ __forceinline__ uint32_t ld_status(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kRsWarps * 32) k_os_scatter(const uint32_t* __restrict__ kin,
                                                               const int32_t* __restrict__ vin,
                                                               uint32_t* __restrict__ kout, int32_t* __restrict__ vout,
                                                               int64_t n, int shift, int bins,
-                                                              const int32_t* __restrict__ hist, int ntiles) {
+                                                              const int32_t* __restrict__ ghist_pass,
+                                                              uint32_t* status, int32_t* tile_ctr) {
   __shared__ int wc[kRsWarps][kRsMaxBins];
+  __shared__ int base[kRsMaxBins];  // global digit start + exclusive tile prefix
+  __shared__ int s_tile;
+  __shared__ int sm[kRsWarps + 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_tile = atomicAdd(tile_ctr, 1);
   for (int d = lane; d < bins; d += 32) wc[w][d] = 0;
-  __syncwarp();
-  const int64_t base = (int64_t)blockIdx.x * kRsTile + (int64_t)w * kRsRounds * 32;
+  __syncthreads();
+  const int tile = s_tile;
+  const int64_t t0 = (int64_t)tile * kRsTile + (int64_t)w * kRsRounds * 32;
   const unsigned lt = (1u << lane) - 1u;
   uint32_t kk[kRsRounds];
   int32_t vv[kRsRounds];
   int dd[kRsRounds], loc[kRsRounds];
 #pragma unroll
   for (int r = 0; r < kRsRounds; ++r) {
-    const int64_t i = base + r * 32 + lane;
+    const int64_t i = t0 + r * 32 + lane;
     const bool valid = i < n;
     kk[r] = valid ? kin[i] : 0u;
     vv[r] = valid ? (vin ? vin[i] : (int32_t)i) : 0;  // vin == NULL: values are the input positions
@@ -126,20 +150,64 @@ __global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const uint32_t* __
     __syncwarp();
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < bins; d += blockDim.x) {  // warp order = input order
-    int run = 0;
+  // global digit starts (exclusive scan of the pass histogram, bins <= 512 = 2 per thread)
+  {
+    const int d0 = 2 * threadIdx.x;
+    const int a = d0 < bins ? ghist_pass[d0] : 0, b = d0 + 1 < bins ? ghist_pass[d0 + 1] : 0;
+    int tot;
+    const int e = block_excl_scan<kRsWarps * 32>(a + b, sm, tot);
+    if (d0 < bins) base[d0] = e;
+    if (d0 + 1 < bins) base[d0 + 1] = e + a;
+  }
+  __syncthreads();
+  // publish every digit's tile count first, then look back: a successor never waits on
+  // this tile's look-back of another digit
+  constexpr int kPer = kRsMaxBins / (kRsWarps * 32);
+  int cnts[kPer];
 #pragma unroll
-    for (int q = 0; q < kRsWarps; ++q) {
-      const int t = wc[q][d];
-      wc[q][d] = run;
-      run += t;
+  for (int q = 0; q < kPer; ++q) {
+    const int d = threadIdx.x + q * kRsWarps * 32;
+    cnts[q] = 0;
+    if (d >= bins) continue;
+    int cnt = 0;  // tile count of digit d; warp order = input order
+#pragma unroll
+    for (int wq = 0; wq < kRsWarps; ++wq) {
+      const int t = wc[wq][d];
+      wc[wq][d] = cnt;
+      cnt += t;
     }
+    cnts[q] = cnt;
+    st_status(status + (int64_t)tile * bins + d, (tile == 0 ? kOsPrefix : kOsAgg) | (uint32_t)cnt);
+  }
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int d = threadIdx.x + q * kRsWarps * 32;
+    if (d >= bins || tile == 0) continue;
+    // decoupled look-back, kLb predecessors' statuses loaded at once (independent loads)
+    constexpr int kLb = 8;
+    int excl = 0;
+    bool done = false;
+    for (int t0 = tile - 1; t0 >= 0 && !done; t0 -= kLb) {
+      uint32_t v[kLb];
+#pragma unroll
+      for (int j = 0; j < kLb; ++j) v[j] = t0 - j >= 0 ? ld_status(status + (int64_t)(t0 - j) * bins + d) : 0u;
+#pragma unroll
+      for (int j = 0; j < kLb; ++j) {
+        if (done || t0 - j < 0) continue;
+        uint32_t x = v[j];
+        while ((x & ~kOsMask) == 0u) x = ld_status(status + (int64_t)(t0 - j) * bins + d);  // not yet published
+        excl += (int)(x & kOsMask);
+        if (x & kOsPrefix) done = true;
+      }
+    }
+    st_status(status + (int64_t)tile * bins + d, kOsPrefix | (uint32_t)(excl + cnts[q]));
+    base[d] += excl;
   }
   __syncthreads();
 #pragma unroll
   for (int r = 0; r < kRsRounds; ++r) {
     if (dd[r] < kRsMaxBins) {
-      const int64_t pos = (int64_t)hist[(int64_t)dd[r] * ntiles + blockIdx.x] + wc[w][dd[r]] + loc[r];
+      const int64_t pos = (int64_t)base[dd[r]] + wc[w][dd[r]] + loc[r];
       kout[pos] = kk[r];
       vout[pos] = vv[r];
     }
@@ -148,8 +216,8 @@ __global__ void __launch_bounds__(kRsWarps * 32) k_rs_scatter(const uint32_t* __
 
 size_t sort_scratch_bytes(int64_t n) {
   const int64_t ntiles = (n + kRsTile - 1) / kRsTile;
-  return sizeof(int32_t) * (kRsMaxBins * ntiles + 1) + scan_scratch_bytes(kRsMaxBins * ntiles) +
-         2 * n * sizeof(int32_t) + 64;
+  return sizeof(int32_t) * (kOsMaxPasses * kRsMaxBins + kOsMaxPasses + 4) +
+         sizeof(uint32_t) * (size_t)kOsMaxPasses * kRsMaxBins * ntiles + 2 * n * sizeof(int32_t) + 64;
 }
 
 // Stable sort of (key, value) pairs by the low `key_bits` bits of the key.
@@ -157,28 +225,36 @@ size_t sort_scratch_bytes(int64_t n) {
 int radix_sort_pairs(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* keys_out, int32_t* vals_out,
                      int64_t n, int key_bits, void* scratch, cudaStream_t st) {
   if (n <= 0) return FC_OK;
+  if (n > (int64_t)kOsMask) {
+    set_error("radix sort of %lld keys exceeds the 30-bit tile counters", (long long)n);
+    return FC_ERR_BAD_ARG;
+  }
   const int ntiles = (int)((n + kRsTile - 1) / kRsTile);
+  const int passes = std::max(1, (key_bits + 8) / 9);
+  if (passes > kOsMaxPasses) return FC_ERR_BAD_ARG;
+  const int dbits = std::max(1, (key_bits + passes - 1) / passes);
+  const int bins = 1 << dbits;
+  // scratch: [ghist passes*bins][tile counters passes] | status passes*ntiles*bins | ktmp | vtmp
   char* p = static_cast<char*>(scratch);
-  int32_t* hist = reinterpret_cast<int32_t*>(p);
-  p += sizeof(int32_t) * ((int64_t)kRsMaxBins * ntiles + 1);
-  void* scan_scr = p;
-  p += scan_scratch_bytes(kRsMaxBins * ntiles);
+  int32_t* ghist = reinterpret_cast<int32_t*>(p);
+  int32_t* tctr = ghist + kOsMaxPasses * kRsMaxBins;
+  const size_t head = sizeof(int32_t) * (kOsMaxPasses * kRsMaxBins + kOsMaxPasses + 4);
+  uint32_t* status = reinterpret_cast<uint32_t*>(p + head);
+  const size_t status_bytes = sizeof(uint32_t) * (size_t)passes * bins * ntiles;
+  p += head + status_bytes;
   p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
   uint32_t* ktmp = reinterpret_cast<uint32_t*>(p);
   int32_t* vtmp = reinterpret_cast<int32_t*>(p + n * sizeof(int32_t));
-  const int passes = std::max(1, (key_bits + 8) / 9);
-  const int dbits = std::max(1, (key_bits + passes - 1) / passes);
-  const int bins = 1 << dbits;
+  FC_CUDA(cudaMemsetAsync(scratch, 0, head + status_bytes, st));  // histograms, counters, status flags
+  k_os_hist<<<grid_for(n, kNT * 8, kSMs * 4), kNT, 0, st>>>(keys_in, n, passes, dbits, ghist);
   const uint32_t* ks = keys_in;
   const int32_t* vs = vals_in;
   for (int pass = 0; pass < passes; ++pass) {
     const bool to_out = ((passes - 1 - pass) % 2) == 0;  // last pass lands in the outputs
     uint32_t* kd = to_out ? keys_out : ktmp;
     int32_t* vd = to_out ? vals_out : vtmp;
-    k_rs_hist<<<ntiles, kRsWarps * 32, 0, st>>>(ks, n, pass * dbits, bins, hist, ntiles);
-    int rc = exclusive_scan_i32(hist, hist, (int64_t)bins * ntiles, scan_scr, st);
-    if (rc) return rc;
-    k_rs_scatter<<<ntiles, kRsWarps * 32, 0, st>>>(ks, vs, kd, vd, n, pass * dbits, bins, hist, ntiles);
+    k_os_scatter<<<ntiles, kRsWarps * 32, 0, st>>>(ks, vs, kd, vd, n, pass * dbits, bins, ghist + pass * bins,
+                                                   status + (size_t)pass * bins * ntiles, tctr + pass);
     ks = kd;
     vs = vd;
   }
