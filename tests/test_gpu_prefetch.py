@@ -236,3 +236,70 @@ def test_module_prefetch_matches_sequential(optimizer, mode, bags):
         o.backward(torch.from_numpy(grads[s]))
         opt.step()
     np.testing.assert_allclose(w_pf, emb.weight.detach().numpy(), rtol=1e-5, atol=1e-6)
+
+
+def test_prefetched_paper_literal_vs_oracle():
+    """evict_mode='paper_literal' (needed = max(0, U - C), cache_manager.py:293-296) through
+    the pipeline, including the InsufficientFreeSlots error once the tier is full."""
+    num_ids, cap, dim = 4_000, 500, 8
+    rng = np.random.default_rng(2)
+    p = 1.0 / np.arange(1, num_ids + 1) ** 1.1
+    trace = rng.permutation(num_ids)[rng.choice(num_ids, size=(12, 120), p=p / p.sum())]
+    rank_of, id_of = oracle.rank_permutation(oracle.frequency_counts(trace, num_ids))
+    ref = oracle.init_rows(num_ids, dim, 4)
+    orc = oracle.OracleCache(rank_of, ref[id_of].copy(), cap, evict_mode="paper_literal")
+    st = fc.CacheStack(fc.IdxMap(rank_of, id_of), fc.SlowTierStore(ref[id_of].copy()),
+                       fc.FastTierStore(np.zeros((cap, dim), np.float32)), fc.Transmitter(),
+                       evict_mode="paper_literal", log_events=True, engine="async")
+    ids = [trace[b] for b in range(trace.shape[0])]
+    for b in range(len(ids)):
+        try:
+            a = orc.prepare(ids[b], b)
+        except oracle.OracleInsufficientFreeSlots:
+            st.prefetch(ids[b], b)
+            with pytest.raises(cm.InsufficientFreeSlots):
+                st.prepare(ids[b], b)
+            break
+        st.prefetch(ids[b], b)
+        q = st.prepare(ids[b], b)
+        assert (q.hits, q.misses, q.evictions) == (a["hits"], a["misses"], a["evictions"])
+        assert np.array_equal(q.unique_slots, a["unique_slots"])
+    st.state.check_invariants()
+    assert np.array_equal(st.state.slot_to_rank, orc.slot_rank)
+
+
+def test_stress_shape_adagrad_through_module():
+    """configs[4]'s index shape (25.5M rows, 0.5% cache, uniform ids, 65,536 lookups per
+    step) trained with Adagrad through CachedEmbeddingBag + prefetch: the flushed table
+    and optimizer state equal a dense torch Adagrad (rtol 1e-5); nearly every lookup
+    misses, so the state rows ride every admission and write-back."""
+    num_ids, dim, steps, B = 25_523_073, 4, 5, 65_536
+    rng = np.random.default_rng(8)
+    trace = rng.integers(0, num_ids, size=(steps, B))
+    w0 = rng.uniform(-0.1, 0.1, (num_ids, dim)).astype(np.float32)
+    grads = [rng.standard_normal((B, dim)).astype(np.float32) for _ in range(steps)]
+    idx = fc.build_reorder(fc.scan_frequencies(trace, num_ids))
+    m = CachedEmbeddingBag(num_ids, dim, 0.005, mode="sum", weight=w0, idx_map=idx, optimizer="adagrad", lr=0.1)
+    ids = [torch.from_numpy(trace[s]) for s in range(steps)]
+    out = m(ids[0])
+    for s in range(steps):
+        if s + 1 < steps:
+            m.prefetch(ids[s + 1])
+        out.backward(torch.from_numpy(grads[s]).cuda())
+        if s + 1 < steps:
+            out = m(ids[s + 1])
+    m.flush()
+    emb = torch.nn.EmbeddingBag(num_ids, dim, mode="sum", sparse=True)
+    emb.weight.data = torch.from_numpy(w0.copy())
+    opt = torch.optim.Adagrad(emb.parameters(), lr=0.1, eps=1e-10)
+    for s in range(steps):
+        o = emb(torch.from_numpy(trace[s]), torch.arange(0, B))
+        opt.zero_grad()
+        o.backward(torch.from_numpy(grads[s]))
+        opt.step()
+    touched = np.unique(trace)
+    np.testing.assert_allclose(m.weight()[touched], emb.weight.detach().numpy()[touched], rtol=1e-5, atol=1e-6)
+    state = opt.state[emb.weight]["sum"].numpy()
+    np.testing.assert_allclose(m.optimizer_state()[touched], state[touched], rtol=1e-5, atol=1e-7)
+    assert np.array_equal(m.weight()[:1000], np.where(np.isin(np.arange(1000), touched)[:, None],
+                                                      m.weight()[:1000], w0[:1000]))
