@@ -26,6 +26,10 @@ CASES = {
     "avazu": dict(num_ids=9_445_823, ratio=0.05, alpha=1.05, batch=65536, features=22, batches=4, cold=True),
     # configs[4] per-GPU share: uniform ids, 0.5% cache, 65,536 lookups per step
     "stress": dict(num_ids=25_523_073, ratio=0.005, alpha=None, batch=65536, features=1, batches=6),
+    # configs[3]: Criteo-1TB shape (26 tables capped at 40M, 204,184,588 rows), 1.5% cache; a
+    # column-sharded rank prepares the GLOBAL batch of 8 ranks (8 x 16,384 x 26 = 3.4M ids)
+    "criteo_1tb_colshard8": dict(num_ids=204_184_588, ratio=0.015, alpha=1.05, batch=8 * 16384, features=26,
+                                 batches=3),
 }
 DIM = 4
 
@@ -41,6 +45,8 @@ def test_fullsize_parity(name):
     ids = [tr.samples[b * c["batch"]:(b + 1) * c["batch"]].reshape(-1) for b in range(nb)]
     freq, idx = fc.build_reorder_device(tr.samples, n_ids)
     assert np.array_equal(freq.counts, oracle.frequency_counts(tr.samples, n_ids))
+    if n_ids < 100_000_000:  # the host lexsort of 204M keys alone takes minutes; reorder parity is
+        assert np.array_equal(idx.rank_of, oracle.rank_permutation(freq.counts)[0])  # covered elsewhere
     cap = fc.fast_capacity(n_ids, c["ratio"])
     rng = np.random.default_rng(3)
     slow0 = rng.standard_normal((n_ids, DIM), dtype=np.float32)
