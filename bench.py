@@ -344,7 +344,7 @@ def run_ours(args, cfg, torch, rank, world):
         rows = fc.store.pinned_empty((idx.num_ids, D))
         fill_pinned(torch, rows, dev, SEED + rank)
         shard = CudaShard(idx.num_ids, D, fc.fast_capacity(idx.num_ids, cfg["ratio"]), rows, idx, optimizer=OPT,
-                          lr=LR, device=dev, engine=args.engine)
+                          lr=LR, device=dev, engine=args.engine, global_num_ids=cfg["num_ids"])
         mod = RowShardedEmbedding(shard, world, rank, mode=MODE, device=dev)
         dcs = [shard.cache]
         cap = shard.cache.capacity
@@ -522,7 +522,28 @@ def run_ours(args, cfg, torch, rank, world):
     return res, samples, rank_of, cap
 
 
+_STDOUT = None
+
+
+def quiet_stdout():
+    """Send everything written to fd 1 (native libraries' banners, e.g. NCCL's version
+    line) to stderr, so that the one JSON result line is all that reaches stdout."""
+    global _STDOUT
+    sys.stdout.flush()
+    _STDOUT = os.dup(1)
+    os.dup2(2, 1)
+
+
+def emit(doc):
+    sys.stdout.flush()
+    if _STDOUT is not None:
+        os.write(_STDOUT, (json.dumps(doc) + "\n").encode())
+    else:
+        print(json.dumps(doc), flush=True)
+
+
 def main():
+    quiet_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -566,7 +587,7 @@ def main():
                                           "numpy oracle restatement of the reference (single-threaded numpy)"},
                "e2e": {"value": r["lookups_per_s"], "unit": "lookups/s", "h2d_bytes_per_step": 0,
                        "d2h_bytes_per_step": 0}}
-        print(json.dumps(out), flush=True)
+        emit(out)
         return 0
 
     import torch
@@ -583,7 +604,7 @@ def main():
                                "sample": f"{r['steps']} batches after 2 warm-up batches of the same trace; "
                                          "numpy oracle port (same step), single-threaded"}
     if rank == 0:
-        print(json.dumps(res), flush=True)
+        emit(res)
     if torch.distributed.is_initialized():
         torch.distributed.destroy_process_group()
     return 0

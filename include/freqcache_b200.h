@@ -231,6 +231,36 @@ int fc_backward_update(fc_cache* h, const int32_t* unique_slots, const int32_t* 
                        int32_t include_last_offset, const float* per_sample_weights, int32_t mode,
                        const float* grad_out, int32_t optim, float lr, float eps, void* stream);
 
+/* ---- row-sharded exchange (multi-GPU, no reference counterpart: the reference's
+ * sharding is column-wise only, sharding.py:62-118; this is the partitioned
+ * scaling variant of SURVEY 8e/8f rank 2) ------------------------------------- */
+typedef struct fc_router fc_router;  /* bitmap + scratch over a [world x S] routing key space */
+
+int fc_router_create(int64_t num_ids, int32_t world, int32_t device, fc_router** out);
+int fc_router_destroy(fc_router* r);
+
+/* A requester's batch routed to row owners (owner = id % world, owner-local row =
+ * id / world): unique ids grouped by owner, ascending within each owner, written as
+ * owner-local ids to local_ids_dev (capacity n); inverse_dev[j] = position of ids[j]
+ * in that list; owner_counts_host[o] = how many go to owner o; *unique = list length.
+ * Synchronises `stream` (the counts size the all-to-all). */
+int fc_route(fc_router* r, const void* ids_dev, int32_t ids_bytes, int64_t n, int32_t* local_ids_dev,
+             int32_t* inverse_dev, int64_t* owner_counts_host, int64_t* unique, void* stream);
+
+/* Pooled EmbeddingBag forward over a dense row buffer: occurrence j uses
+ * rows[inverse[j]] (the rows the owners sent back, in routing order). */
+int fc_pool_rows(const float* rows_dev, int32_t dim, const int32_t* inverse_dev, int64_t n, const void* offsets,
+                 int32_t offsets_bytes, int64_t n_bags, int32_t include_last_offset,
+                 const float* per_sample_weights, int32_t mode, float* out, void* stream);
+
+/* The backward of fc_pool_rows: one gradient row per routed unique id,
+ * grad_unique[p] = sum over occurrences j with inverse[j] == p of coef_j * grad_out[bag(j)]
+ * (deterministic order), ready to be sent to the owners. */
+int fc_route_grads(fc_router* r, const int32_t* inverse_dev, int64_t u, int64_t n, const void* offsets,
+                   int32_t offsets_bytes, int64_t n_bags, int32_t include_last_offset,
+                   const float* per_sample_weights, int32_t mode, const float* grad_out, int32_t dim,
+                   float* grad_unique, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -67,6 +67,14 @@ _SIGS = {
     "fc_last_writebacks": (c_int32, [c_void_p, POINTER(c_int64)]),
     "fc_build_reorder": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                    POINTER(c_int64), c_void_p]),
+    "fc_router_create": (c_int32, [c_int64, c_int32, c_int32, POINTER(c_void_p)]),
+    "fc_router_destroy": (c_int32, [c_void_p]),
+    "fc_route": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_void_p, POINTER(c_int64),
+                           c_void_p]),
+    "fc_pool_rows": (c_int32, [c_void_p, c_int32, c_void_p, c_int64, c_void_p, c_int32, c_int64, c_int32, c_void_p,
+                               c_int32, c_void_p, c_void_p]),
+    "fc_route_grads": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_int32, c_void_p,
+                                 c_int32, c_void_p, c_int32, c_void_p, c_void_p]),
     "fc_trace": (c_int32, [c_void_p, c_int32]),
     "fc_trace_mark": (c_int32, [c_void_p, c_int32, c_void_p]),
     "fc_trace_read": (c_int64, [c_void_p, c_void_p, c_void_p, c_int64]),

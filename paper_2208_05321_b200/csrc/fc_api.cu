@@ -46,16 +46,18 @@ static void trace_clear(fc_cache* h) {
   h->trace = nullptr;
 }
 
-int ensure_scratch(fc_cache* h, size_t bytes) {
-  if (bytes <= h->scratch_bytes) return FC_OK;
-  size_t nb = std::max(bytes, h->scratch_bytes + h->scratch_bytes / 2);
-  if (h->scratch) FC_CUDA(cudaFree(h->scratch));
-  h->scratch = nullptr;
-  h->scratch_bytes = 0;
-  FC_CUDA(cudaMalloc(&h->scratch, nb));
-  h->scratch_bytes = nb;
+int ensure_scratch_buf(void** p, size_t* have, size_t bytes) {
+  if (bytes <= *have) return FC_OK;
+  size_t nb = std::max(bytes, *have + *have / 2);
+  if (*p) FC_CUDA(cudaFree(*p));  // synchronising: no kernel still uses the old buffer
+  *p = nullptr;
+  *have = 0;
+  FC_CUDA(cudaMalloc(p, nb));
+  *have = nb;
   return FC_OK;
 }
+
+int ensure_scratch(fc_cache* h, size_t bytes) { return ensure_scratch_buf(&h->scratch, &h->scratch_bytes, bytes); }
 
 // sync the stream through the handle's event and pull the counters
 static int sync_counters(fc_cache* h, cudaStream_t st) {

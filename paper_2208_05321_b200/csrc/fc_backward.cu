@@ -30,11 +30,11 @@ struct Grouping {
 
 static size_t grouping_bytes(int64_t n) { return align16(n * 4) * 2 + align16(sort_scratch_bytes(n)); }
 
-static int build_grouping(fc_cache* h, const int32_t* inv, int64_t u, int64_t n, size_t extra, Grouping& g,
-                          cudaStream_t st) {
-  int rc = ensure_scratch(h, grouping_bytes(n) + extra);
+static int build_grouping(void** scratch, size_t* scratch_bytes, const int32_t* inv, int64_t u, int64_t n,
+                          size_t extra, Grouping& g, cudaStream_t st) {
+  int rc = ensure_scratch_buf(scratch, scratch_bytes, grouping_bytes(n) + extra);
   if (rc) return rc;
-  char* p = static_cast<char*>(h->scratch);
+  char* p = static_cast<char*>(*scratch);
   g.keys = reinterpret_cast<uint32_t*>(p);
   p += align16(n * 4);
   g.order = reinterpret_cast<int32_t*>(p);
@@ -71,7 +71,7 @@ int launch_scatter_update(fc_cache* h, const int32_t* uslots, const int32_t* inv
   if (u <= 0 || n <= 0) return FC_OK;
   Grouping g;
   const size_t extra = align16((u + 1) * 4) + align16(scan_scratch_bytes(u));
-  int rc = build_grouping(h, inv, u, n, extra, g, st);
+  int rc = build_grouping(&h->scratch, &h->scratch_bytes, inv, u, n, extra, g, st);
   if (rc) return rc;
   int32_t* seg = reinterpret_cast<int32_t*>(g.rest);
   void* scan_scr = g.rest + align16((u + 1) * 4);
@@ -347,31 +347,30 @@ __global__ void __launch_bounds__(kNT) k_bwd_apply(BwdArgs x, int64_t u) {
   }
 }
 
-int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u, int64_t n,
-                    const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw, int mode,
-                    const float* grad, int optim, float lr, float eps, cudaStream_t st) {
-  (void)ucnt;
-  if (u <= 0 || n <= 0) return FC_OK;
-  const int D = h->dim;
-  if (optim == FC_OPT_ADAGRAD && (h->fast_state == nullptr || h->sw != D)) {
-    set_error("Adagrad needs a cache created with state_width == dim");
-    return FC_ERR_BAD_ARG;
-  }
-  if (D % 4 || (reinterpret_cast<uintptr_t>(grad) & 15)) {
-    set_error("backward needs dim %% 4 == 0 and a 16-byte aligned grad_out");
+// Per-unique gradient of the pooled forward: group the occurrences by unique row
+// (stable radix sort of `inverse`), stream the sorted occurrences accumulating
+// coef_j * grad_out[bag(j)], fix up the runs cut by chunk edges. Leaves x ready for
+// k_bwd_apply (x.gu = per-unique sums, in `gu_out` when given, else in scratch).
+static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* inv, int64_t u, int64_t n,
+                         const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw,
+                         int mode, const float* grad, int D, float* gu_out, BwdArgs& x, cudaStream_t st) {
+  if (D % 4 || (reinterpret_cast<uintptr_t>(grad) & 15) || (reinterpret_cast<uintptr_t>(gu_out) & 15)) {
+    set_error("backward needs dim %% 4 == 0 and 16-byte aligned gradient rows");
     return FC_ERR_BAD_ARG;
   }
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const bool bags = offsets != nullptr;
-  const size_t extra = align16((size_t)u * D * 4) + align16(nchunks * 2 * (size_t)D * 4) +
+  const size_t extra = (gu_out ? 0 : align16((size_t)u * D * 4)) + align16(nchunks * 2 * (size_t)D * 4) +
                        2 * align16(nchunks * 2 * 4) + (bags ? 2 * align16(n * 4) : 0);
   Grouping g;
-  int rc = build_grouping(h, inv, u, n, extra, g, st);
+  int rc = build_grouping(scratch, scratch_bytes, inv, u, n, extra, g, st);
   if (rc) return rc;
   char* p = g.rest;
-  BwdArgs x;
-  x.gu = reinterpret_cast<float*>(p);
-  p += align16((size_t)u * D * 4);
+  x.gu = gu_out;
+  if (!gu_out) {
+    x.gu = reinterpret_cast<float*>(p);
+    p += align16((size_t)u * D * 4);
+  }
   x.carry = reinterpret_cast<float*>(p);
   p += align16(nchunks * 2 * (size_t)D * 4);
   x.carry_key = reinterpret_cast<int32_t*>(p);
@@ -398,16 +397,11 @@ int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, cons
     x.coef = coef;
   }
   FC_CUDA(cudaMemsetAsync(x.carry_key, 0xff, nchunks * 2 * 4, st));
-  x.fast = h->fast;
-  x.fstate = optim == FC_OPT_ADAGRAD ? h->fast_state : nullptr;
   x.D = D;
-  x.uslots = uslots;
   x.keys = g.keys;
   x.order = g.order;
   x.n = n;
   x.grad = grad;
-  x.dirty = h->dirty;
-  x.o = OptArgs{optim, lr, eps};
   x.un = units_for(D);
   const int grid = grid_for(nchunks * 32, kNT, kSMs * 16);
   k_bwd_stream<<<grid, kNT, 0, st>>>(x);
@@ -415,9 +409,44 @@ int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, cons
   if (fix_smem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_bwd_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                          (int)fix_smem));
   k_bwd_fixup<<<(int)std::min<int64_t>(nchunks, kSMs * 16), kNT, fix_smem, st>>>(x);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u, int64_t n,
+                    const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw, int mode,
+                    const float* grad, int optim, float lr, float eps, cudaStream_t st) {
+  (void)ucnt;
+  if (u <= 0 || n <= 0) return FC_OK;
+  const int D = h->dim;
+  if (optim == FC_OPT_ADAGRAD && (h->fast_state == nullptr || h->sw != D)) {
+    set_error("Adagrad needs a cache created with state_width == dim");
+    return FC_ERR_BAD_ARG;
+  }
+  BwdArgs x;
+  x.uslots = uslots;
+  int rc = segment_grads(&h->scratch, &h->scratch_bytes, inv, u, n, offsets, off_bytes, nbags, include_last, psw, mode,
+                         grad, D, nullptr, x, st);
+  if (rc) return rc;
+  x.fast = h->fast;
+  x.fstate = optim == FC_OPT_ADAGRAD ? h->fast_state : nullptr;
+  x.dirty = h->dirty;
+  x.o = OptArgs{optim, lr, eps};
   k_bwd_apply<<<grid_for(u, kNT, kSMs * 8), kNT, 0, st>>>(x, u);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
+}
+
+// Per-unique gradient rows without an optimizer step (the row-sharded exchange: a
+// requester reduces its occurrences' gradients before sending them to the owners).
+int launch_unique_grads(void** scratch, size_t* scratch_bytes, const int32_t* inv, int64_t u, int64_t n,
+                        const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw,
+                        int mode, const float* grad, int D, float* gu, cudaStream_t st) {
+  if (u <= 0 || n <= 0) return FC_OK;
+  BwdArgs x;
+  x.uslots = nullptr;
+  return segment_grads(scratch, scratch_bytes, inv, u, n, offsets, off_bytes, nbags, include_last, psw, mode, grad, D,
+                       gu, x, st);
 }
 
 }  // namespace fc

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstddef>
+#include <cstring>
 
 #include "fc_internal.cuh"
 
@@ -584,4 +585,239 @@ int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, i
   return FC_OK;
 }
 
+// ------------------------------------------------------------------ row-sharded exchange planner
+// A requester's batch, routed to row owners (owner = id % world, the owner's local
+// row = id / world): unique ids grouped by owner and ascending within each owner —
+// one ordered compaction of a bitmap over the key space key = owner * S + id / world —
+// plus every occurrence's position in that list (its inverse) and per-owner counts
+// for the all-to-all splits. Same machinery as prepare's dedup (k_mark_ids / IdEmit).
+template <typename IdT>
+__global__ void __launch_bounds__(kNT) k_route_mark(const IdT* __restrict__ ids, int64_t n, int64_t num_ids, int W,
+                                                    int64_t S, uint32_t* bits, Counters* c) {
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+    const long long id = (long long)ids[i];
+    if (id < 0 || id >= num_ids) {
+      if (id < 0) atomicMin(&c->lo, id);
+      else atomicMax(&c->hi, id);
+      continue;
+    }
+    const int64_t key = (id % W) * S + id / W;
+    const uint32_t m = 1u << (key & 31);
+    uint32_t* wp = &bits[key >> 5];
+    if (!(*wp & m)) atomicOr(wp, m);
+  }
+}
+
+struct RouteFin {
+  __device__ void operator()(int total, Counters* c) const {
+    c->unique = total;
+    if (c->lo != LLONG_MAX || c->hi != LLONG_MIN) c->err = FC_ERR_ID_OUT_OF_RANGE;
+    c->emitted = (c->err == 0);
+  }
+};
+
+struct RouteEmit {
+  static constexpr bool kVisitAll = true, kClear = true, kCount = false;
+  int32_t* ukeys;
+  int32_t* ulocal;
+  int32_t* aux;
+  int64_t S;
+  int ok;
+  __device__ void init(const Counters* c) { ok = c->emitted; }
+  __device__ int* counter(Counters*) const { return nullptr; }
+  __device__ __forceinline__ int operator()(int64_t key, int p) const {
+    if (ok) {
+      ukeys[p] = (int32_t)key;
+      ulocal[p] = (int32_t)(key % S);
+      aux[key] = p;
+    }
+    return 0;
+  }
+};
+
+template <typename IdT>
+__global__ void __launch_bounds__(kNT) k_route_inverse(const IdT* __restrict__ ids, int64_t n, int W, int64_t S,
+                                                       const int32_t* __restrict__ aux, int32_t* __restrict__ inv,
+                                                       const Counters* c) {
+  if (!c->emitted) return;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
+    const long long id = (long long)ids[i];
+    inv[i] = aux[(id % W) * S + id / W];
+  }
+}
+
+// per-owner counts: owner o's ids are the keys in [o*S, (o+1)*S) of the sorted unique list
+__global__ void k_route_counts(const int32_t* __restrict__ ukeys, int64_t S, int W, const Counters* c,
+                               long long* owner_cnt) {
+  const int o = threadIdx.x;
+  if (o > W) return;
+  const int u = c->emitted ? c->unique : 0;
+  const long long target = (long long)o * S;
+  int lo = 0, hi = u;  // first position with key >= o*S
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if ((long long)ukeys[mid] < target) lo = mid + 1;
+    else hi = mid;
+  }
+  __shared__ int start[65];
+  start[o] = (o == W) ? u : lo;
+  __syncthreads();
+  if (o < W) owner_cnt[o] = start[o + 1] - start[o];
+}
+
+__global__ void __launch_bounds__(kNT) k_route_finish(const int32_t* __restrict__ ukeys, int32_t* aux, const Counters* c) {
+  if (!c->emitted) return;
+  for (int p = blockIdx.x * kNT + threadIdx.x; p < c->unique; p += gridDim.x * kNT) aux[ukeys[p]] = 0;
+}
+
 }  // namespace fc
+
+struct fc_router {
+  int64_t num_ids;
+  int32_t world;
+  int64_t S;       // keys per owner (multiple of 32)
+  int64_t nw;      // bitmap words
+  int device;
+  uint32_t* bits;
+  int32_t* aux;
+  int32_t* ukeys;
+  int64_t ukeys_cap;
+  int32_t* block_cnt;
+  fc::Counters* ctr;
+  fc::Counters* ctr_host;
+  long long* owner_cnt;
+  long long* owner_cnt_host;
+  void* scratch;
+  size_t scratch_bytes;
+};
+
+namespace fc {
+
+static void router_release(fc_router* r) {
+  void* dev[] = {r->bits, r->aux, r->ukeys, r->block_cnt, r->ctr, r->owner_cnt, r->scratch};
+  for (void* p : dev)
+    if (p) cudaFree(p);
+  if (r->ctr_host) cudaFreeHost(r->ctr_host);
+  if (r->owner_cnt_host) cudaFreeHost(r->owner_cnt_host);
+  delete r;
+}
+
+}  // namespace fc
+
+using namespace fc;
+
+extern "C" int fc_router_create(int64_t num_ids, int32_t world, int32_t device, fc_router** out) {
+  if (!out || num_ids < 1 || world < 1 || world > 64) return FC_ERR_BAD_ARG;
+  *out = nullptr;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  fc_router* r = new fc_router();
+  std::memset(r, 0, sizeof(*r));
+  r->num_ids = num_ids;
+  r->world = world;
+  r->S = ((num_ids + world - 1) / world + 31) / 32 * 32;
+  if (r->S * world > INT32_MAX - 64) {
+    delete r;
+    cudaSetDevice(prev);
+    set_error("routing key space exceeds int32");
+    return FC_ERR_BAD_ARG;
+  }
+  r->nw = (r->S * world / 32 + 3) / 4 * 4;
+  r->device = device;
+  cudaError_t e = cudaMalloc(&r->bits, r->nw * 4);
+  if (e == cudaSuccess) e = cudaMemset(r->bits, 0, r->nw * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&r->aux, (size_t)r->S * world * 4);
+  if (e == cudaSuccess) e = cudaMemset(r->aux, 0, (size_t)r->S * world * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&r->block_cnt, (kMaxScanBlocks + 1) * 4);
+  if (e == cudaSuccess) e = cudaMalloc(&r->ctr, sizeof(Counters));
+  if (e == cudaSuccess) e = cudaHostAlloc(&r->ctr_host, sizeof(Counters), cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaMalloc(&r->owner_cnt, 64 * sizeof(long long));
+  if (e == cudaSuccess) e = cudaHostAlloc(&r->owner_cnt_host, 64 * sizeof(long long), cudaHostAllocDefault);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    router_release(r);
+    return cuda_fail(e, "fc_router_create");
+  }
+  *out = r;
+  return FC_OK;
+}
+
+extern "C" int fc_router_destroy(fc_router* r) {
+  if (!r) return FC_OK;
+  cudaDeviceSynchronize();
+  router_release(r);
+  return FC_OK;
+}
+
+extern "C" int fc_route(fc_router* r, const void* ids, int32_t ids_bytes, int64_t n, int32_t* local_ids,
+                        int32_t* inverse, int64_t* owner_counts, int64_t* unique, void* stream) {
+  if (!r || !owner_counts || !unique || (ids_bytes != 4 && ids_bytes != 8) || n < 0 || n > INT32_MAX)
+    return FC_ERR_BAD_ARG;
+  *unique = 0;
+  for (int o = 0; o < r->world; ++o) owner_counts[o] = 0;
+  if (n == 0) return FC_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != r->device) cudaSetDevice(r->device);
+  cudaStream_t st = as_stream(stream);
+  int rc = FC_OK;
+  if (r->ukeys_cap < n) {
+    if (r->ukeys) cudaFree(r->ukeys);
+    r->ukeys = nullptr;
+    r->ukeys_cap = 0;
+    if (cudaMalloc(&r->ukeys, (size_t)n * 4) != cudaSuccess) {
+      if (prev != r->device) cudaSetDevice(prev);
+      return cuda_fail(cudaGetLastError(), "fc_route");
+    }
+    r->ukeys_cap = n;
+  }
+  Counters* c = r->ctr;
+  k_begin<<<1, 1, 0, st>>>(c, c);
+  const int g = grid_for(n, kNT, kSMs * 8);
+  if (ids_bytes == 8) k_route_mark<long long><<<g, kNT, 0, st>>>((const long long*)ids, n, r->num_ids, r->world, r->S, r->bits, c);
+  else k_route_mark<int><<<g, kNT, 0, st>>>((const int*)ids, n, r->num_ids, r->world, r->S, r->bits, c);
+  compact(ArrWords{r->bits}, RouteFin{}, RouteEmit{r->ukeys, local_ids, r->aux, r->S, 0}, r->nw, r->block_cnt, nullptr,
+          c, G_ALWAYS, st);
+  if (ids_bytes == 8) k_route_inverse<long long><<<g, kNT, 0, st>>>((const long long*)ids, n, r->world, r->S, r->aux, inverse, c);
+  else k_route_inverse<int><<<g, kNT, 0, st>>>((const int*)ids, n, r->world, r->S, r->aux, inverse, c);
+  k_route_counts<<<1, 65, 0, st>>>(r->ukeys, r->S, r->world, c, r->owner_cnt);
+  k_route_finish<<<grid_for(n, kNT, kSMs * 4), kNT, 0, st>>>(r->ukeys, r->aux, c);
+  cudaError_t e = cudaGetLastError();
+  if (e == cudaSuccess) e = cudaMemcpyAsync(r->ctr_host, c, sizeof(Counters), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(r->owner_cnt_host, r->owner_cnt, r->world * sizeof(long long), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) rc = cuda_fail(e, "fc_route");
+  if (rc == FC_OK && r->ctr_host->err) {
+    const long long b = r->ctr_host->lo != LLONG_MAX ? r->ctr_host->lo : r->ctr_host->hi;
+    set_error("id out of range: %lld not in [0, %lld)", b, (long long)r->num_ids);
+    rc = FC_ERR_ID_OUT_OF_RANGE;
+  }
+  if (rc == FC_OK) {
+    *unique = r->ctr_host->unique;
+    for (int o = 0; o < r->world; ++o) owner_counts[o] = r->owner_cnt_host[o];
+  }
+  if (prev != r->device) cudaSetDevice(prev);
+  return rc;
+}
+
+extern "C" int fc_route_grads(fc_router* r, const int32_t* inverse, int64_t u, int64_t n, const void* offsets,
+                              int32_t off_bytes, int64_t nbags, int32_t include_last, const float* psw, int32_t mode,
+                              const float* grad, int32_t dim, float* grad_unique, void* stream) {
+  if (!r || (mode != FC_POOL_SUM && mode != FC_POOL_MEAN) || (offsets && off_bytes != 4 && off_bytes != 8))
+    return FC_ERR_BAD_ARG;
+  cudaStream_t st = as_stream(stream);  // every unique id has an occurrence: all u rows are written
+  return launch_unique_grads(&r->scratch, &r->scratch_bytes, inverse, u, n, offsets, off_bytes, nbags, include_last, psw,
+                             mode, grad, dim, grad_unique, st);
+}
+
+extern "C" int fc_pool_rows(const float* rows, int32_t dim, const int32_t* inverse, int64_t n, const void* offsets,
+                            int32_t off_bytes, int64_t nbags, int32_t include_last, const float* psw, int32_t mode,
+                            float* out, void* stream) {
+  if (!rows || dim < 1 || (mode != FC_POOL_SUM && mode != FC_POOL_MEAN) || (offsets && off_bytes != 4 && off_bytes != 8))
+    return FC_ERR_BAD_ARG;
+  return launch_pool_rows(rows, dim, nullptr, inverse, n, offsets, off_bytes, nbags, include_last, psw, mode, out,
+                          as_stream(stream));
+}
+

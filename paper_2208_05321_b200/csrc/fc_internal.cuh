@@ -226,6 +226,13 @@ int radix_sort_pairs(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* 
 int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch, cudaStream_t st);
 size_t scan_scratch_bytes(int64_t n);
 int ensure_scratch(fc_cache* h, size_t bytes);
+int ensure_scratch_buf(void** p, size_t* have, size_t bytes);
+int launch_unique_grads(void** scratch, size_t* scratch_bytes, const int32_t* inv, int64_t u, int64_t n,
+                        const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw,
+                        int mode, const float* grad, int D, float* gu, cudaStream_t st);
+int launch_pool_rows(const float* rows, int D, const int32_t* uslots, const int32_t* inv, int64_t n,
+                     const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw, int mode,
+                     float* out, cudaStream_t st);
 
 // ---------------------------------------------------------------- device utils
 __device__ __forceinline__ int warp_sum(int v) {

@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(kNT) k_pool(const float* __restrict__ fast, in
         float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
         int64_t j = s;
         for (; j + 1 < e; j += 2) {  // two rows in flight per lane
-          const int r0 = uslots[inv[j]], r1 = uslots[inv[j + 1]];
+          const int r0 = uslots ? uslots[inv[j]] : inv[j], r1 = uslots ? uslots[inv[j + 1]] : inv[j + 1];
           const float4 v0 = __ldg(reinterpret_cast<const float4*>(fast + (int64_t)r0 * D + c));
           const float4 v1 = __ldg(reinterpret_cast<const float4*>(fast + (int64_t)r1 * D + c));
           const float w0 = psw ? psw[j] : 1.0f, w1 = psw ? psw[j + 1] : 1.0f;
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kNT) k_pool(const float* __restrict__ fast, in
           acc.x += w1 * v1.x; acc.y += w1 * v1.y; acc.z += w1 * v1.z; acc.w += w1 * v1.w;
         }
         if (j < e) {
-          const int r0 = uslots[inv[j]];
+          const int r0 = uslots ? uslots[inv[j]] : inv[j];
           const float4 v0 = __ldg(reinterpret_cast<const float4*>(fast + (int64_t)r0 * D + c));
           const float w0 = psw ? psw[j] : 1.0f;
           acc.x += w0 * v0.x; acc.y += w0 * v0.y; acc.z += w0 * v0.z; acc.w += w0 * v0.w;
@@ -391,7 +391,7 @@ __global__ void __launch_bounds__(kNT) k_pool(const float* __restrict__ fast, in
         float acc = 0.f;
         for (int64_t j = s; j < e; ++j) {
           const float w = psw ? psw[j] : 1.0f;
-          acc += w * fast[(int64_t)uslots[inv[j]] * D + c];
+          acc += w * fast[(int64_t)(uslots ? uslots[inv[j]] : inv[j]) * D + c];
         }
         out[b * D + c] = acc * scale;
       }
@@ -413,7 +413,7 @@ __global__ void __launch_bounds__(kNT) k_pool1(const float* __restrict__ fast, i
     int s = 0;
     float w = 1.0f;
     if (act) {
-      s = uslots[inv[j]];
+      s = uslots ? uslots[inv[j]] : inv[j];  // uslots == NULL: inv indexes the rows directly
       if (psw) w = psw[j];
     }
     if (psw) warp_move<kUnroll, true>(fast, D, s, out, D, (int)j, act, w, un);
@@ -423,18 +423,24 @@ __global__ void __launch_bounds__(kNT) k_pool1(const float* __restrict__ fast, i
 
 int launch_pool(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const void* offsets, int off_bytes,
                 int64_t nbags, int include_last, const float* psw, int mode, float* out, cudaStream_t st) {
+  return launch_pool_rows(h->fast, h->dim, uslots, inv, n, offsets, off_bytes, nbags, include_last, psw, mode, out, st);
+}
+
+// pooled forward over any row buffer; uslots == NULL means row = inv[j]
+int launch_pool_rows(const float* rows, int D, const int32_t* uslots, const int32_t* inv, int64_t n,
+                     const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw, int mode,
+                     float* out, cudaStream_t st) {
   if (nbags <= 0) return FC_OK;
-  const int D = h->dim;
-  const bool v = (D % 4 == 0) && ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+  const bool v = (D % 4 == 0) && (((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(rows)) & 15) == 0);
   if (v && offsets == nullptr) {  // bag size 1: one row per bag
-    k_pool1<<<grid_for(nbags, kNT, kSMs * 8), kNT, 0, st>>>(h->fast, D, uslots, inv, nbags, psw, out, units_for(D));
+    k_pool1<<<grid_for(nbags, kNT, kSMs * 8), kNT, 0, st>>>(rows, D, uslots, inv, nbags, psw, out, units_for(D));
     FC_CUDA(cudaGetLastError());
     return FC_OK;
   }
   const int G = row_group(D, v);
   const int grid = grid_for(nbags * G, kNT, kSMs * 16);
 #define FC_POOL(VV, T) \
-  k_pool<VV, T><<<grid, kNT, 0, st>>>(h->fast, D, uslots, inv, n, (const T*)offsets, nbags, include_last, psw, mode, out, G)
+  k_pool<VV, T><<<grid, kNT, 0, st>>>(rows, D, uslots, inv, n, (const T*)offsets, nbags, include_last, psw, mode, out, G)
   if (off_bytes == 4) {
     if (v) FC_POOL(true, int32_t); else FC_POOL(false, int32_t);
   } else {

@@ -36,7 +36,8 @@ class CudaShard:
 
     def __init__(self, num_rows: int, dim: int, capacity: int, rows_rank_order: np.ndarray, idx_map: IdxMap,
                  optimizer: str = "sgd", lr: float = 0.01, eps: float = 1e-10, buffer_bytes: int = 64 * 2**20,
-                 warmup: bool = True, device=None, engine: str = "async"):
+                 warmup: bool = True, device=None, engine: str = "async", global_num_ids: int | None = None):
+        self.global_num_ids = global_num_ids  # whole-table id space (row-sharded exchange)
         sw = dim if optimizer == "adagrad" else 0
         self.cache = DeviceCache(num_rows, capacity, dim, state_width=sw, buffer_bytes=buffer_bytes, device=device)
         self.cache.set_idx_map(idx_map.rank_of)
@@ -77,6 +78,76 @@ class CudaShard:
 
     def flush(self) -> int:
         return self.cache.flush()
+
+
+class Router:
+    """libfreqcache_b200's row-sharded exchange planner (fc_route / fc_pool_rows /
+    fc_route_grads): dedup + group-by-owner of a requester's ids with the same bitmap
+    machinery as prepare, the pooled forward over the rows the owners send back, and
+    its backward reduced to one deterministic gradient row per routed id."""
+
+    def __init__(self, num_ids: int, world: int, device):
+        import ctypes
+
+        from . import _lib
+        from .errors import check
+
+        self._ct, self._check = ctypes, check
+        self.lib = _lib.load()
+        self.device = torch.device(device)
+        self.world = int(world)
+        h = ctypes.c_void_p()
+        check(self.lib.fc_router_create(int(num_ids), self.world, self.device.index or 0, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None) is not None and self.h.value:
+            self.lib.fc_router_destroy(self.h)
+            self.h = self._ct.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _stream(self):
+        return self._ct.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+
+    def route(self, ids):
+        """-> (owner-local unique ids grouped by owner, inverse, per-owner counts)"""
+        ct = self._ct
+        n = int(ids.numel())
+        local = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        inv = torch.empty(max(n, 1), dtype=torch.int32, device=self.device)
+        counts = (ct.c_int64 * self.world)()
+        u = ct.c_int64()
+        self._check(self.lib.fc_route(self.h, ct.c_void_p(ids.data_ptr()), ids.element_size(), n,
+                                      ct.c_void_p(local.data_ptr()), ct.c_void_p(inv.data_ptr()), counts,
+                                      ct.byref(u), self._stream()))
+        return local[:u.value], inv[:n], list(counts)
+
+    def pool(self, rows, inv, offsets, n_bags, include_last_offset, psw, mode):
+        ct = self._ct
+        out = torch.empty((n_bags, rows.shape[1]), dtype=torch.float32, device=self.device)
+        self._check(self.lib.fc_pool_rows(
+            ct.c_void_p(rows.data_ptr()), int(rows.shape[1]), ct.c_void_p(inv.data_ptr()), int(inv.numel()),
+            ct.c_void_p(0 if offsets is None else offsets.data_ptr()), 0 if offsets is None else offsets.element_size(),
+            int(n_bags), int(bool(include_last_offset)), ct.c_void_p(0 if psw is None else psw.data_ptr()),
+            {"sum": 0, "mean": 1}[mode], ct.c_void_p(out.data_ptr()), self._stream()))
+        return out
+
+    def grads(self, inv, u, grad_out, offsets, n_bags, include_last_offset, psw, mode):
+        ct = self._ct
+        gu = torch.empty((u, grad_out.shape[1]), dtype=torch.float32, device=self.device)
+        g = grad_out.contiguous()
+        self._check(self.lib.fc_route_grads(
+            self.h, ct.c_void_p(inv.data_ptr()), int(u), int(inv.numel()),
+            ct.c_void_p(0 if offsets is None else offsets.data_ptr()), 0 if offsets is None else offsets.element_size(),
+            int(n_bags), int(bool(include_last_offset)), ct.c_void_p(0 if psw is None else psw.data_ptr()),
+            {"sum": 0, "mean": 1}[mode], ct.c_void_p(g.data_ptr()), int(g.shape[1]), ct.c_void_p(gu.data_ptr()),
+            self._stream()))
+        return gu
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -164,6 +235,13 @@ class RowShardedEmbedding(torch.nn.Module):
         self._anchor = torch.nn.Parameter(torch.empty(0, device=self.device))
         self.last_recv = 0
         self._pf = None  # (ids, exchange) of a prefetched batch
+        # on a GPU the exchange planning, expansion and gradient reduction run in
+        # libfreqcache_b200 (Router); on CPU (gloo tests) the same steps in torch
+        self.router = None
+        if self.device.type == "cuda":
+            num_ids = getattr(shard, "global_num_ids", None)
+            if num_ids is not None:
+                self.router = Router(num_ids, world, self.device)
 
     @staticmethod
     def owner_of(ids, world):
@@ -172,17 +250,23 @@ class RowShardedEmbedding(torch.nn.Module):
     def _exchange_ids(self, ids):
         """Unique ids of this rank's batch to their owners; returns the routing."""
         W = self.world
-        uniq, inv = torch.unique(ids.long(), sorted=True, return_inverse=True)
-        owner, local = self.owner_of(uniq, W)
-        order = torch.argsort(owner, stable=True)
-        send_ids = local[order]
-        send_counts = torch.bincount(owner, minlength=W)
+        if self.router is not None:  # grouped by owner already: no permutation to undo
+            send_ids, inv, sc = self.router.route(ids)
+            order = None
+            send_counts = torch.tensor(sc, dtype=torch.int64, device=ids.device)
+        else:
+            uniq, inv = torch.unique(ids.long(), sorted=True, return_inverse=True)
+            owner, local = self.owner_of(uniq, W)
+            order = torch.argsort(owner, stable=True)
+            send_ids = local[order]
+            send_counts = torch.bincount(owner, minlength=W)
+            sc = send_counts.tolist()
         recv_counts = torch.empty_like(send_counts)
         _a2a(recv_counts, send_counts, None, None, self.group)
-        sc, rc = send_counts.tolist(), recv_counts.tolist()
+        rc = recv_counts.tolist()
         recv_ids = torch.empty(sum(rc), dtype=send_ids.dtype, device=send_ids.device)
-        _a2a(recv_ids, send_ids, rc, sc, self.group)
-        return {"inv": inv, "order": order, "sc": sc, "rc": rc, "recv_ids": recv_ids, "u": int(uniq.numel())}
+        _a2a(recv_ids, send_ids.contiguous(), rc, sc, self.group)
+        return {"inv": inv, "order": order, "sc": sc, "rc": rc, "recv_ids": recv_ids, "u": int(send_ids.numel())}
 
     def prefetch(self, ids):
         dev_ids = ids.reshape(-1).to(self.device)
@@ -211,18 +295,25 @@ class RowShardedEmbedding(torch.nn.Module):
         rows = self.shard.pool(h)  # [n_recv, D] one row per received (unique per requester) id
         back = torch.empty((x["u"], rows.shape[1]), dtype=rows.dtype, device=rows.device)
         _a2a(back, rows.contiguous(), x["sc"], x["rc"], self.group)
-        uniq_rows = torch.empty_like(back)
-        uniq_rows[x["order"]] = back
-        local_rows = uniq_rows[x["inv"]]
-        out = pool_rows(local_rows, offsets, n_bags, self.include_last_offset, psw, self.mode)
+        if self.router is not None:  # back is in routing order: pool straight through the inverse
+            out = self.router.pool(back, x["inv"], offsets, n_bags, self.include_last_offset, psw, self.mode)
+        else:
+            uniq_rows = torch.empty_like(back)
+            uniq_rows[x["order"]] = back
+            out = pool_rows(uniq_rows[x["inv"]], offsets, n_bags, self.include_last_offset, psw, self.mode)
         return out, (h, x, int(ids.numel()), offsets, n_bags, psw)
 
     def _backward(self, saved, grad_out):
         h, x, n, offsets, n_bags, psw = saved
-        g = bag_grads(grad_out, n, offsets, n_bags, self.include_last_offset, psw, self.mode)
-        gu = torch.zeros((x["u"], g.shape[1]), dtype=g.dtype, device=g.device)
-        gu.index_add_(0, x["inv"], g)  # one gradient row per unique id of this rank
-        g_send = gu[x["order"]].contiguous()
+        if self.router is not None:  # one deterministic gradient row per routed id, in routing order
+            g_send = self.router.grads(x["inv"], x["u"], grad_out, offsets, n_bags, self.include_last_offset, psw,
+                                       self.mode)
+        else:
+            g = bag_grads(grad_out, n, offsets, n_bags, self.include_last_offset, psw, self.mode)
+            gu = torch.zeros((x["u"], g.shape[1]), dtype=g.dtype, device=g.device)
+            gu.index_add_(0, x["inv"], g)  # one gradient row per unique id of this rank
+            g_send = gu[x["order"]].contiguous()
+        g = g_send
         g_recv = torch.empty((sum(x["rc"]), g.shape[1]), dtype=g.dtype, device=g.device)
         _a2a(g_recv, g_send, x["rc"], x["sc"], self.group)
         self.shard.backward(h, g_recv)
@@ -332,4 +423,5 @@ def build_row_sharded(num_ids, dim, cache_ratio, counts, rank, world, init_rows_
     n_local = idx.num_ids
     rows = pinned_empty((n_local, dim))
     rows[...] = init_rows_fn(rank + world * idx.id_of)
+    kw.setdefault("global_num_ids", num_ids)
     return CudaShard(n_local, dim, fast_capacity(n_local, cache_ratio), rows, idx, **kw)

@@ -1,0 +1,90 @@
+"""Row-sharded exchange planner (fc_route / fc_pool_rows / fc_route_grads) on one GPU,
+against numpy; and the RowShardedEmbedding training step through NCCL at world 1
+(every exchange kernel on the real path) against a dense torch EmbeddingBag + SGD."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+from paper_2208_05321_b200.distributed import CudaShard, Router, RowShardedEmbedding, shard_rows_for_rank  # noqa: E402
+from paper_2208_05321_b200.store import fast_capacity, pinned_empty  # noqa: E402
+
+
+@pytest.mark.parametrize("world,num_ids,n", [(1, 1000, 3000), (3, 50_001, 40_000), (8, 1_000_003, 200_000)])
+def test_route_matches_numpy(world, num_ids, n):
+    rng = np.random.default_rng(world)
+    p = 1.0 / np.arange(1, num_ids + 1) ** 1.05
+    ids = rng.permutation(num_ids)[rng.choice(num_ids, size=n, p=p / p.sum())]
+    r = Router(num_ids, world, "cuda")
+    local, inv, counts = r.route(torch.from_numpy(ids).cuda())
+    uniq = np.unique(ids)
+    order = np.lexsort((uniq // world, uniq % world))  # by owner, then owner-local id
+    want = uniq[order]
+    assert counts == np.bincount(uniq % world, minlength=world).tolist()
+    assert np.array_equal(local.cpu().numpy(), want // world)
+    pos = np.empty(uniq.max() + 1, np.int64)
+    pos[want] = np.arange(want.size)
+    assert np.array_equal(inv.cpu().numpy(), pos[ids])
+    # pooled forward through the inverse (bags of 3, mean with weights) and its backward
+    D = 8
+    rows = torch.randn(want.size, D, device="cuda")
+    off = torch.arange(0, n, 3, device="cuda")
+    w = torch.rand(n, device="cuda")
+    out = r.pool(rows, inv, off, off.numel(), False, w, "mean").cpu().numpy()
+    ref = oracle.pooled_bag(rows.cpu().numpy(), inv.cpu().numpy(), off.cpu().numpy(), w.cpu().numpy(), "mean")
+    np.testing.assert_allclose(out, ref, rtol=1e-5, atol=1e-6)
+    g = torch.randn(off.numel(), D, device="cuda")
+    gu = r.grads(inv, want.size, g, off, off.numel(), False, w, "mean").cpu().numpy()
+    ref_g = oracle.pooled_bag_backward_rows(g.cpu().numpy(), inv.cpu().numpy(), off.cpu().numpy(), want.size,
+                                            w.cpu().numpy(), "mean")
+    np.testing.assert_allclose(gu, ref_g, rtol=1e-4, atol=1e-5)
+    with pytest.raises(ValueError, match="out of range"):
+        r.route(torch.tensor([1, num_ids], device="cuda"))
+    r.route(torch.from_numpy(ids[:10]).cuda())  # state is clean after an error
+
+
+def test_row_sharded_module_nccl_world1_matches_dense():
+    import torch.distributed as dist
+
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1)
+    num_ids, dim, steps, B = 30_000, 16, 6, 4_000
+    rng = np.random.default_rng(4)
+    p = 1.0 / np.arange(1, num_ids + 1) ** 1.1
+    trace = rng.permutation(num_ids)[rng.choice(num_ids, size=(steps, B), p=p / p.sum())]
+    table = rng.uniform(-0.1, 0.1, (num_ids, dim)).astype(np.float32)
+    idx = shard_rows_for_rank(np.bincount(trace.reshape(-1), minlength=num_ids), 0, 1)
+    rows = pinned_empty((num_ids, dim))
+    rows[...] = table[idx.id_of]
+    shard = CudaShard(num_ids, dim, fast_capacity(num_ids, 0.05), rows, idx, lr=0.1, device="cuda",
+                      global_num_ids=num_ids)
+    mod = RowShardedEmbedding(shard, 1, 0, mode="sum", device=torch.device("cuda"))
+    assert mod.router is not None
+    grads = [rng.standard_normal((B, dim)).astype(np.float32) for _ in range(steps)]
+    ids = [torch.from_numpy(trace[s]).cuda() for s in range(steps)]
+    dense = torch.nn.EmbeddingBag(num_ids, dim, mode="sum", sparse=True)
+    dense.weight.data = torch.from_numpy(table.copy())
+    opt = torch.optim.SGD(dense.parameters(), lr=0.1)
+    for s in range(steps):
+        out = mod(ids[s])
+        want = dense(torch.from_numpy(trace[s]), torch.arange(B))
+        # fp32 sums of hot rows' gradients in a different order than torch's: 1e-5 of the
+        # values' scale (|w| <~ 0.5) as the absolute floor
+        np.testing.assert_allclose(out.detach().cpu().numpy(), want.detach().numpy(), rtol=1e-5, atol=5e-6)
+        if s + 1 < steps:
+            mod.prefetch(ids[s + 1])
+        out.backward(torch.from_numpy(grads[s]).cuda())
+        opt.zero_grad()
+        want.backward(torch.from_numpy(grads[s]))
+        opt.step()
+    mod.flush()
+    torch.cuda.synchronize()
+    got = np.empty_like(table)
+    got[idx.id_of] = rows
+    np.testing.assert_allclose(got, dense.weight.detach().numpy(), rtol=1e-5, atol=5e-6)
+    dist.destroy_process_group()
