@@ -479,8 +479,11 @@ int engine_evict(fc_cache* h, cudaStream_t st) {
   return FC_OK;
 }
 
+static int launch_admit_async_tma(fc_cache* h, const EngArgs& x, cudaStream_t st);  // below, with the TMA helpers
+
 int engine_admit(fc_cache* h, cudaStream_t st) {
   EngArgs x = eng_args(h);
+  if (h->awb->vec && !std::getenv("FC_NO_TMA")) return launch_admit_async_tma(h, x, st);
   if (h->awb->vec) k_admit_async<true><<<kSMs * 4, kNT, 0, st>>>(x);
   else k_admit_async<false><<<kSMs * 4, kNT, 0, st>>>(x);
   FC_CUDA(cudaGetLastError());
@@ -859,6 +862,88 @@ __global__ void __launch_bounds__(32) k_admit_stage_tma(PipeArgs x, int G) {
     ++retired;
   }
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// Synchronous-prepare admission through the bulk-copy engine: like k_admit_stage_tma,
+// but each staged row is stored straight to its target slot (one 16-byte-multiple bulk
+// store per row) and the lanes apply the admissions to the slot tables as they queue
+// them (nothing reads the rows before the next kernel).
+__global__ void __launch_bounds__(32) k_admit_async_tma(EngArgs x, int G) {
+  extern __shared__ __align__(128) unsigned char ring[];
+  __shared__ uint64_t bar[kTmaStages];
+  const int lane = threadIdx.x;
+  if (!gate_open(x.c, G_OK)) return;
+  const int m = x.c->misses;
+  const unsigned rb = (unsigned)x.D * 4, sb = (unsigned)x.S * 4;
+  const size_t stage_bytes = (size_t)G * (rb + sb);
+  if (lane == 0) {
+    for (int i = 0; i < kTmaStages; ++i) mbar_init(&bar[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (blockIdx.x == 0) x.c->free_count -= m;
+  }
+  __syncwarp();
+  unsigned phase_bits = 0;
+  const int ngroups = (m + G - 1) / G;
+  int issued = 0, retired = 0;
+  const int mine = ngroups > (int)blockIdx.x ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  while (retired < mine) {
+    if (issued < mine && issued - retired < kTmaStages) {
+      const int st = issued % kTmaStages;
+      if (issued >= kTmaStages) {
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // every lane stored rows of this stage
+        __syncwarp();
+      }
+      const int g = blockIdx.x + issued * gridDim.x;
+      const int j0 = g * G, cnt = min(G, m - j0);
+      unsigned char* rows = ring + st * stage_bytes;
+      unsigned char* srows = rows + (size_t)G * rb;
+      if (lane == 0) mbar_expect_tx(&bar[st], cnt * (rb + sb));
+      __syncwarp();
+      for (int i = lane; i < cnt; i += 32) {
+        const int r = x.admitted[j0 + i];
+        const int s = x.target[j0 + i];
+        const int pk = x.pending[r];
+        const float* src = pk >= 0 ? x.stage[pk / x.cap] + (int64_t)(pk % x.cap) * x.D : x.slow + (int64_t)r * x.ld;
+        bulk_g2s(rows + (size_t)i * rb, src, rb, &bar[st]);
+        if (x.S) {
+          const float* ss = pk >= 0 ? x.sstage[pk / x.cap] + (int64_t)(pk % x.cap) * x.S : x.sstate + (int64_t)r * x.sld;
+          bulk_g2s(srows + (size_t)i * sb, ss, sb, &bar[st]);
+        }
+        x.slot_to_rank[s] = r;
+        x.rank_to_slot[r] = s;
+        x.dirty[s] = 0;
+        atomicOr(&x.res[r >> 5], 1u << (r & 31));
+        atomicAnd(&x.freeb[s >> 5], ~(1u << (s & 31)));
+      }
+      ++issued;
+      continue;
+    }
+    const int st = retired % kTmaStages;
+    mbar_wait(&bar[st], (phase_bits >> st) & 1u);
+    phase_bits ^= 1u << st;
+    const int g = blockIdx.x + retired * gridDim.x;
+    const int j0 = g * G, cnt = min(G, m - j0);
+    unsigned char* rows = ring + st * stage_bytes;
+    for (int i = lane; i < cnt; i += 32) {  // rows go to scattered slots: one bulk store each
+      const int s = x.target[j0 + i];
+      bulk_s2g(x.fast + (int64_t)s * x.D, rows + (size_t)i * rb, rb);
+      if (x.S) bulk_s2g(x.fstate + (int64_t)s * x.S, rows + (size_t)G * rb + (size_t)i * sb, sb);
+    }
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    __syncwarp();
+    ++retired;
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+static int launch_admit_async_tma(fc_cache* h, const EngArgs& x, cudaStream_t st) {
+  const int G = tma_group_rows((h->dim + h->sw) * 4);
+  const size_t smem = (size_t)kTmaStages * G * (h->dim + h->sw) * 4;
+  if (smem > 48 * 1024)
+    FC_CUDA(cudaFuncSetAttribute(k_admit_async_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_admit_async_tma<<<kTmaBlocks, 32, smem, st>>>(x, G);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
 }
 
 // commit: dirty victims (rows already carry the previous batch's update) -> write-back stage
