@@ -68,6 +68,9 @@ KERNELS_PER_TRAIN_STEP = 21 + 1 + 6
 # prefetch pipeline: + k_evict_state, k_admit_state, k_publish (index phase) and
 # k_admit_stage / k_evict_commit / k_admit_commit instead of k_evict_async / k_admit_async
 PIPELINE_EXTRA_KERNELS = 3 + 1
+# miss staging / admission through the TMA bulk-copy engine (row width a multiple of 16 B;
+# FC_XFER_TMA=0 / FC_NO_TMA=1 select the SM-load kernels)
+TMA = os.environ.get("FC_XFER_TMA", "1") != "0" and not os.environ.get("FC_NO_TMA")
 KSTEPS = 5  # extra steps timed kernel by kernel after the timed region
 
 
@@ -272,9 +275,11 @@ def rooflines(prof, pool_ms, N, D, links, engine="async", pipelined=False, psw=F
     xfer_ms = prof["transfer_ms"] / max(prof["transfer_launches"] if pipelined else prof["calls"], 1)
     xfer_bytes = prof["host_link_bytes"] / max(prof["calls"], 1)
     if pipelined:  # admissions staged host -> HBM on the transfer stream; write-backs on the copy engine
-        kname, peak, src = "k_admit_stage", links["h2d_GBps"], "pinned cudaMemcpy H2D, measured in this run"
+        kname, peak, src = ("k_admit_stage_tma" if TMA else "k_admit_stage"), links["h2d_GBps"], \
+            "pinned cudaMemcpy H2D, measured in this run"
     elif engine == "async":  # admissions only (H2D); write-backs ride the copy engine off the critical path
-        kname, peak, src = "k_admit_async", links["h2d_GBps"], "pinned cudaMemcpy H2D, measured in this run"
+        kname, peak, src = ("k_admit_async_tma" if TMA else "k_admit_async"), links["h2d_GBps"], \
+            "pinned cudaMemcpy H2D, measured in this run"
     else:
         kname, peak, src = "k_transfer_rows", links["bidir_GBps"], "pinned cudaMemcpy H2D+D2H concurrently, measured"
     r_xfer = {"kernel": kname, "bound": "host_link",
