@@ -6,14 +6,17 @@
 //     then adds each group's deltas in batch order — bit-exact with np.add.at;
 //   * the backward of the pooled forward (north star item 6) streams the sorted
 //     occurrences once: each warp owns a chunk of kChunk consecutive sorted
-//     occurrences, accumulates coef_j * grad_out[bag(j)] per run of equal rows in
-//     registers (one float4 column unit per lane, kBwdUnroll grad rows in flight)
-//     and stores the sum per unique row; runs cut by chunk boundaries leave
-//     carries that one fix-up pass sums (a block per split row, its warps summing
-//     contiguous slices of the carry chain, combined in warp order); a last pass
-//     applies SGD / Adagrad to every cached row (32 rows per warp). Fixed order ->
-//     deterministic.
+//     occurrences and accumulates coef_j * grad_out[bag(j)] per run of equal rows in
+//     registers (one float4 column unit per lane, kBwdUnroll grad rows in flight).
+//     The optimizer step is fused into that pass: a run that starts and ends inside
+//     its chunk (almost every row) updates its cached row (SGD, or Adagrad with the
+//     state row) the moment it closes, with the row fetched when the run opened;
+//     runs cut by chunk edges leave carries that one fix-up pass sums (a block per
+//     split row, its warps summing contiguous slices of the chain, combined in warp
+//     order) and then updates. No per-row gradient buffer; fixed order ->
+//     deterministic. (FC_BWD_UNFUSED=1 selects sums-then-apply, k_bwd_apply.)
 #include <algorithm>
+#include <cstdlib>
 
 #include "fc_rowutil.cuh"
 
@@ -98,6 +101,23 @@ __device__ __forceinline__ float opt1(float w, float* st, float g, const OptArgs
   return w - o.lr * g;  // torch.optim.SGD
 }
 
+// optimizer step on one 16-byte unit already in registers (row v, state sv), stored back
+__device__ __forceinline__ void apply_unit_regs(float* w, float* st, float4 v, float4 sv, float4 g, const OptArgs& o) {
+  if (st) {
+    v.x = opt1(v.x, &sv.x, g.x, o);
+    v.y = opt1(v.y, &sv.y, g.y, o);
+    v.z = opt1(v.z, &sv.z, g.z, o);
+    v.w = opt1(v.w, &sv.w, g.w, o);
+    st4(st, sv);
+  } else {
+    v.x -= o.lr * g.x;
+    v.y -= o.lr * g.y;
+    v.z -= o.lr * g.z;
+    v.w -= o.lr * g.w;
+  }
+  st4(w, v);
+}
+
 __device__ __forceinline__ void apply_unit(float* w, float* st, float4 g, const OptArgs& o) {
   float4 v = ld4(w);
   if (st) {
@@ -150,27 +170,38 @@ struct BwdArgs {
   Units un;
 };
 
-// One finished run of key `key` over sorted positions [a, b) of chunk c: its sum
-// goes to gu[key] (coalesced) when the run lies inside the chunk, else it is parked
-// as a carry for the fix-up pass.
+// One finished run of key `key` over sorted positions [a, b) of chunk c. A run that
+// lies inside the chunk is final: APPLY updates the cached row right here with the
+// row (and optimizer state) prefetched when the run started; otherwise its sum goes to
+// gu[key] (coalesced). A run cut by a chunk edge is parked as a carry for the fix-up.
+template <bool APPLY>
 __device__ __forceinline__ void bwd_flush(const BwdArgs& x, int64_t c, int64_t j0, int64_t j1, int key, int64_t a,
                                           int64_t b, int prev_key, int next_key, float4 acc, int unit, bool has,
-                                          bool first_col) {
+                                          bool first_col, int slot, float4 wrow, float4 srow) {
   const bool open_s = (a == j0) && (prev_key == key);
   const bool open_e = (b == j1) && (next_key == key);
   if (!open_s && !open_e) {
-    if (has) st4(x.gu + (int64_t)key * x.D + unit * 4, acc);
+    if (APPLY) {
+      if (has) {
+        float* w = x.fast + (int64_t)slot * x.D + unit * 4;
+        apply_unit_regs(w, x.fstate ? x.fstate + (w - x.fast) : nullptr, wrow, srow, acc, x.o);
+      }
+      if (first_col && (threadIdx.x & 31) == 0) x.dirty[slot] = 1;
+    } else if (has) {
+      st4(x.gu + (int64_t)key * x.D + unit * 4, acc);
+    }
   } else {
-    const int64_t slot = c * 2 + (open_s ? 0 : 1);
-    if (has) st4(x.carry + slot * x.D + unit * 4, acc);
+    const int64_t cs = c * 2 + (open_s ? 0 : 1);
+    if (has) st4(x.carry + cs * x.D + unit * 4, acc);
     if (first_col && (threadIdx.x & 31) == 0) {
-      x.carry_key[slot] = key;
-      x.carry_flag[slot] = (open_s ? 1 : 0) | (open_e ? 2 : 0);
+      x.carry_key[cs] = key;
+      x.carry_flag[cs] = (open_s ? 1 : 0) | (open_e ? 2 : 0);
     }
   }
 }
 
-__global__ void __launch_bounds__(kNT) k_bwd_stream(BwdArgs x) {
+template <bool APPLY>
+__global__ void __launch_bounds__(kNT, APPLY ? 3 : 4) k_bwd_stream(BwdArgs x) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
@@ -183,22 +214,24 @@ __global__ void __launch_bounds__(kNT) k_bwd_stream(BwdArgs x) {
       const int unit = cu0 + lane;
       const bool has = unit < x.un.upr;
       float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-      int cur = -1;
+      float4 wrow = acc, srow = acc;
+      int cur = -1, cur_slot = 0;
       int64_t run_a = j0;
       for (int64_t r0 = j0; r0 < j1; r0 += 32) {
         const int64_t jj = r0 + lane;
-        int kl = -1, bag = 0;
+        int kl = -1, bag = 0, sl = 0;
         float cf = 0.f;
         if (jj < j1) {
           kl = (int)x.keys[jj];
           const int occ = x.order[jj];
           bag = x.bag_of ? x.bag_of[occ] : occ;
           cf = x.coef ? x.coef[occ] : (x.psw ? x.psw[occ] : 1.0f);
+          if (APPLY) sl = x.uslots[kl];
         }
         const int cnt = (int)(j1 - r0 < 32 ? j1 - r0 : 32);
         for (int q = 0; q < cnt; q += kBwdUnroll) {
           float4 g[kBwdUnroll];
-          int kq[kBwdUnroll];
+          int kq[kBwdUnroll], sq[kBwdUnroll];
           float cq[kBwdUnroll];
 #pragma unroll
           for (int k = 0; k < kBwdUnroll; ++k) {
@@ -206,6 +239,7 @@ __global__ void __launch_bounds__(kNT) k_bwd_stream(BwdArgs x) {
             const int bq = __shfl_sync(FC_FULL, bag, src);
             kq[k] = __shfl_sync(FC_FULL, kl, src);
             cq[k] = __shfl_sync(FC_FULL, cf, src);
+            sq[k] = APPLY ? __shfl_sync(FC_FULL, sl, src) : 0;
             g[k] = make_float4(0.f, 0.f, 0.f, 0.f);
             if (has && q + k < cnt) g[k] = ldg4(x.grad + (int64_t)bq * x.D + unit * 4);
           }
@@ -214,10 +248,17 @@ __global__ void __launch_bounds__(kNT) k_bwd_stream(BwdArgs x) {
             if (q + k >= cnt) break;
             if (kq[k] != cur) {
               if (cur >= 0)
-                bwd_flush(x, c, j0, j1, cur, run_a, r0 + q + k, prev_key, next_key, acc, unit, has, cu0 == 0);
+                bwd_flush<APPLY>(x, c, j0, j1, cur, run_a, r0 + q + k, prev_key, next_key, acc, unit, has, cu0 == 0,
+                                 cur_slot, wrow, srow);
               cur = kq[k];
+              cur_slot = sq[k];
               run_a = r0 + q + k;
               acc = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (APPLY && has) {  // the run's row, fetched while its gradients stream in
+                const float* w = x.fast + (int64_t)cur_slot * x.D + unit * 4;
+                wrow = ld4(w);
+                if (x.fstate) srow = ld4(x.fstate + (w - x.fast));
+              }
             }
             acc.x += cq[k] * g[k].x;
             acc.y += cq[k] * g[k].y;
@@ -226,7 +267,9 @@ __global__ void __launch_bounds__(kNT) k_bwd_stream(BwdArgs x) {
           }
         }
       }
-      if (cur >= 0) bwd_flush(x, c, j0, j1, cur, run_a, j1, prev_key, next_key, acc, unit, has, cu0 == 0);
+      if (cur >= 0)
+        bwd_flush<APPLY>(x, c, j0, j1, cur, run_a, j1, prev_key, next_key, acc, unit, has, cu0 == 0, cur_slot, wrow,
+                         srow);
     }
   }
 }
@@ -240,6 +283,7 @@ __global__ void __launch_bounds__(kNT) k_bwd_stream(BwdArgs x) {
 // not hundreds. The row's sum lands in gu like every other row's.
 constexpr int kFixWarps = kNT / 32;
 
+template <bool APPLY>
 __global__ void __launch_bounds__(kNT) k_bwd_fixup(BwdArgs x) {
   extern __shared__ float4 part[];  // [kFixWarps][units per row]
   __shared__ int64_t s_m;
@@ -299,14 +343,21 @@ __global__ void __launch_bounds__(kNT) k_bwd_fixup(BwdArgs x) {
     }
     __syncthreads();
     if (wid == 0) {
+      const int64_t slot = APPLY ? x.uslots[key] : 0;
       for (int unit = lane; unit < x.un.upr; unit += 32) {
         float4 acc = part[unit];
         for (int w = 1; w < kFixWarps; ++w) {
           const float4 v = part[w * x.un.upr + unit];
           acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
         }
-        st4(x.gu + (int64_t)key * x.D + unit * 4, acc);
+        if (APPLY) {
+          float* wr = x.fast + slot * x.D + unit * 4;
+          apply_unit(wr, x.fstate ? x.fstate + (wr - x.fast) : nullptr, acc, x.o);
+        } else {
+          st4(x.gu + (int64_t)key * x.D + unit * 4, acc);
+        }
       }
+      if (APPLY && lane == 0) x.dirty[slot] = 1;
     }
     __syncthreads();
   }
@@ -353,21 +404,21 @@ __global__ void __launch_bounds__(kNT) k_bwd_apply(BwdArgs x, int64_t u) {
 // k_bwd_apply (x.gu = per-unique sums, in `gu_out` when given, else in scratch).
 static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* inv, int64_t u, int64_t n,
                          const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw,
-                         int mode, const float* grad, int D, float* gu_out, BwdArgs& x, cudaStream_t st) {
+                         int mode, const float* grad, int D, float* gu_out, BwdArgs& x, bool apply, cudaStream_t st) {
   if (D % 4 || (reinterpret_cast<uintptr_t>(grad) & 15) || (reinterpret_cast<uintptr_t>(gu_out) & 15)) {
     set_error("backward needs dim %% 4 == 0 and 16-byte aligned gradient rows");
     return FC_ERR_BAD_ARG;
   }
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const bool bags = offsets != nullptr;
-  const size_t extra = (gu_out ? 0 : align16((size_t)u * D * 4)) + align16(nchunks * 2 * (size_t)D * 4) +
+  const size_t extra = (gu_out || apply ? 0 : align16((size_t)u * D * 4)) + align16(nchunks * 2 * (size_t)D * 4) +
                        2 * align16(nchunks * 2 * 4) + (bags ? 2 * align16(n * 4) : 0);
   Grouping g;
   int rc = build_grouping(scratch, scratch_bytes, inv, u, n, extra, g, st);
   if (rc) return rc;
   char* p = g.rest;
   x.gu = gu_out;
-  if (!gu_out) {
+  if (!gu_out && !apply) {
     x.gu = reinterpret_cast<float*>(p);
     p += align16((size_t)u * D * 4);
   }
@@ -404,11 +455,19 @@ static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* i
   x.grad = grad;
   x.un = units_for(D);
   const int grid = grid_for(nchunks * 32, kNT, kSMs * 16);
-  k_bwd_stream<<<grid, kNT, 0, st>>>(x);
   const size_t fix_smem = (size_t)kFixWarps * x.un.upr * sizeof(float4);
-  if (fix_smem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_bwd_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                         (int)fix_smem));
-  k_bwd_fixup<<<(int)std::min<int64_t>(nchunks, kSMs * 16), kNT, fix_smem, st>>>(x);
+  const int fgrid = (int)std::min<int64_t>(nchunks, kSMs * 16);
+  if (apply) {  // the optimizer step happens inside the reduction (no per-row gradient buffer)
+    k_bwd_stream<true><<<grid, kNT, 0, st>>>(x);
+    if (fix_smem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_bwd_fixup<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           (int)fix_smem));
+    k_bwd_fixup<true><<<fgrid, kNT, fix_smem, st>>>(x);
+  } else {
+    k_bwd_stream<false><<<grid, kNT, 0, st>>>(x);
+    if (fix_smem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_bwd_fixup<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                           (int)fix_smem));
+    k_bwd_fixup<false><<<fgrid, kNT, fix_smem, st>>>(x);
+  }
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }
@@ -425,14 +484,15 @@ int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, cons
   }
   BwdArgs x;
   x.uslots = uslots;
-  int rc = segment_grads(&h->scratch, &h->scratch_bytes, inv, u, n, offsets, off_bytes, nbags, include_last, psw, mode,
-                         grad, D, nullptr, x, st);
-  if (rc) return rc;
   x.fast = h->fast;
   x.fstate = optim == FC_OPT_ADAGRAD ? h->fast_state : nullptr;
   x.dirty = h->dirty;
   x.o = OptArgs{optim, lr, eps};
-  k_bwd_apply<<<grid_for(u, kNT, kSMs * 8), kNT, 0, st>>>(x, u);
+  static const bool fused = !std::getenv("FC_BWD_UNFUSED");
+  int rc = segment_grads(&h->scratch, &h->scratch_bytes, inv, u, n, offsets, off_bytes, nbags, include_last, psw, mode,
+                         grad, D, nullptr, x, fused, st);
+  if (rc || fused) return rc;
+  k_bwd_apply<<<grid_for(u, kNT, kSMs * 8), kNT, 0, st>>>(x, u);  // the unfused variant: per-row sums, then apply
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }
@@ -445,8 +505,11 @@ int launch_unique_grads(void** scratch, size_t* scratch_bytes, const int32_t* in
   if (u <= 0 || n <= 0) return FC_OK;
   BwdArgs x;
   x.uslots = nullptr;
+  x.fast = nullptr;
+  x.fstate = nullptr;
+  x.dirty = nullptr;
   return segment_grads(scratch, scratch_bytes, inv, u, n, offsets, off_bytes, nbags, include_last, psw, mode, grad, D,
-                       gu, x, st);
+                       gu, x, false, st);
 }
 
 }  // namespace fc
