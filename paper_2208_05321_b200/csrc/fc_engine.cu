@@ -5,16 +5,17 @@
 // 75 GB/s on this box (tools/zerocopy_bench.cu) where the DMA engines reach ~100.
 // Engine 1 takes the write-back direction off the SMs and off the critical path:
 //
-//   prepare t:  victims' dirty rows are compacted into HBM stage[t%2] and marked
-//               pending[rank] = (t%2, k); admissions read their row from the newest
+//   prepare t:  victims' dirty rows are compacted into HBM stage[b] (b rotates over
+//               kWbBufs buffers, one per prepare that wrote rows back) and marked
+//               pending[rank] = (b, k); admissions read their row from the newest
 //               copy: the HBM stage when the rank is pending, else the pinned slow
-//               tier (zero-copy, the H2D direction alone);
-//   after sync: stage[t%2] (+ ranks) goes D2H by cudaMemcpyAsync on a side stream
+//               tier (TMA bulk copies or SM loads over the host link);
+//   after sync: stage[b] (+ ranks) goes D2H by cudaMemcpyAsync on a side stream
 //               into pinned staging, and a host thread pool scatters the rows into
 //               the slow tier at their ranks — overlapped with the pooled forward /
 //               backward of step t and the index work of step t+1;
-//   prepare t+2: waits for that job, then clears the pending marks that still point
-//               into stage[t%2] before reusing it.
+//   the next prepare that reuses stage[b] (kWbBufs write-backs later) waits for that
+//               job, then clears the pending marks that still point into stage[b].
 //
 // Jobs run strictly FIFO so a rank written back twice lands its newest value last.
 // `flush` drains every job before its own write-back, so after flush the slow tier
@@ -40,6 +41,10 @@
 
 namespace fc {
 
+// Write-back stage buffers in rotation: a host scatter job may lag this many commits
+// behind before a stage reuse has to wait for it (absorbs host-thread jitter).
+constexpr int kWbBufs = 3;
+
 struct Job {
   int buf;
   int64_t rows;
@@ -48,21 +53,21 @@ struct Job {
 
 struct AsyncWB {
   int32_t* pending = nullptr;   // device int32[num_ids], -1 or buf*C + k
-  float* stage[2] = {nullptr, nullptr};
-  float* sstage[2] = {nullptr, nullptr};
-  int32_t* sranks[2] = {nullptr, nullptr};
-  float* hstage[2] = {nullptr, nullptr};   // pinned
-  float* hsstage[2] = {nullptr, nullptr};
-  int32_t* hranks[2] = {nullptr, nullptr};
+  float* stage[kWbBufs] = {};
+  float* sstage[kWbBufs] = {};
+  int32_t* sranks[kWbBufs] = {};
+  float* hstage[kWbBufs] = {};   // pinned
+  float* hsstage[kWbBufs] = {};
+  int32_t* hranks[kWbBufs] = {};
   volatile uint32_t* done_host = nullptr;  // pinned mapped: last finished job's sequence number
   CUdeviceptr done_dev = 0;                // its device address (stream wait-value target)
-  int32_t* dev_rows = nullptr;             // device int32[2]: rows staged by a pipeline commit
-  int32_t* hrows = nullptr;                // pinned int32[2]: their D2H copies
-  int64_t rows_in[2] = {0, 0};             // rows currently staged in each buffer (upper bound)
-  bool rows_on_dev[2] = {false, false};    // the exact count is dev_rows[b]
-  uint64_t seq_of[2] = {0, 0};             // job sequence number using each buffer
+  int32_t* dev_rows = nullptr;             // device int32[kWbBufs]: rows staged by a pipeline commit
+  int32_t* hrows = nullptr;                // pinned int32[kWbBufs]: their D2H copies
+  int64_t rows_in[kWbBufs] = {};           // rows currently staged in each buffer (upper bound)
+  bool rows_on_dev[kWbBufs] = {};          // the exact count is dev_rows[b]
+  uint64_t seq_of[kWbBufs] = {};           // job sequence number using each buffer
   cudaStream_t side = nullptr;
-  cudaEvent_t d2h[2] = {nullptr, nullptr};
+  cudaEvent_t d2h[kWbBufs] = {};
   int cur = 0;
   int device = 0;
   bool vec = true;                         // rows move as 16-byte units (dim % 4 == 0, aligned)
@@ -271,8 +276,8 @@ struct EngArgs {
   const int32_t* admitted;
   const int32_t* target;
   int32_t* pending;
-  float* stage[2];
-  float* sstage[2];
+  float* stage[kWbBufs];
+  float* sstage[kWbBufs];
   int32_t* sranks;
   int buf;
   int32_t cap;
@@ -377,6 +382,10 @@ int engine_set(fc_cache* h, int engine) {
     set_error("attach the slow tier before selecting the async engine");
     return FC_ERR_NO_SLOW_TIER;
   }
+  if ((int64_t)h->capacity * kWbBufs > INT32_MAX) {
+    set_error("capacity too large for the async engine's pending-row encoding");
+    return FC_ERR_BAD_ARG;
+  }
   AsyncWB* a = new AsyncWB();
   a->h = h;
   a->vec = vec_ok_engine(h);
@@ -384,7 +393,7 @@ int engine_set(fc_cache* h, int engine) {
   const size_t C = (size_t)h->capacity;
   cudaError_t e = cudaMalloc(&a->pending, (size_t)h->num_ids * 4);
   if (e == cudaSuccess) e = cudaMemset(a->pending, 0xff, (size_t)h->num_ids * 4);
-  for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+  for (int b = 0; b < kWbBufs && e == cudaSuccess; ++b) {
     e = cudaMalloc(&a->stage[b], C * h->dim * 4);
     if (e == cudaSuccess) e = cudaMalloc(&a->sranks[b], C * 4);
     if (e == cudaSuccess) e = cudaHostAlloc(&a->hstage[b], C * h->dim * 4, cudaHostAllocDefault);
@@ -396,7 +405,7 @@ int engine_set(fc_cache* h, int engine) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a->d2h[b], cudaEventDisableTiming | cudaEventBlockingSync);
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->side, cudaStreamNonBlocking);
-  if (e == cudaSuccess) e = cudaMalloc(&a->dev_rows, 2 * sizeof(int32_t));
+  if (e == cudaSuccess) e = cudaMalloc(&a->dev_rows, kWbBufs * sizeof(int32_t));
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&a->done_host, 64, cudaHostAllocMapped);
   if (e == cudaSuccess) {
     *a->done_host = 0;
@@ -404,7 +413,7 @@ int engine_set(fc_cache* h, int engine) {
     e = cudaHostGetDevicePointer(&dp, (void*)a->done_host, 0);
     a->done_dev = reinterpret_cast<CUdeviceptr>(dp);
   }
-  if (e == cudaSuccess) e = cudaHostAlloc(&a->hrows, 2 * sizeof(int32_t), cudaHostAllocDefault);
+  if (e == cudaSuccess) e = cudaHostAlloc(&a->hrows, kWbBufs * sizeof(int32_t), cudaHostAllocDefault);
   h->awb = a;
   if (e != cudaSuccess) {
     engine_release(h);
@@ -423,7 +432,7 @@ int engine_begin(fc_cache* h, cudaStream_t st) {
   if (h->engine != 1) return FC_OK;
   AsyncWB* a = h->awb;
   const int b = a->cur;
-  if (a->rows_in[b] > 0) {  // stage[b] still holds rows from two prepares ago
+  if (a->rows_in[b] > 0) {  // stage[b] still holds rows from kWbBufs prepares ago
     const auto t0 = std::chrono::steady_clock::now();
     wait_seq(a, a->seq_of[b]);
     h->prof[5] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
@@ -457,10 +466,10 @@ static EngArgs eng_args(fc_cache* h) {
   x.admitted = h->admitted_ranks;
   x.target = h->target_slots;
   x.pending = a->pending;
-  x.stage[0] = a->stage[0];
-  x.stage[1] = a->stage[1];
-  x.sstage[0] = a->sstage[0];
-  x.sstage[1] = a->sstage[1];
+  for (int b = 0; b < kWbBufs; ++b) {
+    x.stage[b] = a->stage[b];
+    x.sstage[b] = a->sstage[b];
+  }
   x.sranks = a->sranks[a->cur];
   x.buf = a->cur;
   x.cap = h->capacity;
@@ -511,7 +520,7 @@ int engine_after_prepare(fc_cache* h, cudaStream_t st) {
     }
     a->cv_q.notify_one();
     a->rows_in[b] = rows;
-    a->cur ^= 1;
+    a->cur = (a->cur + 1) % kWbBufs;
   }
   return FC_OK;
 }
@@ -544,7 +553,7 @@ void engine_release(fc_cache* h) {
   cudaFree(a->dev_rows);
   cudaFreeHost(a->hrows);
   if (a->done_host) cudaFreeHost((void*)a->done_host);
-  for (int b = 0; b < 2; ++b) {
+  for (int b = 0; b < kWbBufs; ++b) {
     cudaFree(a->stage[b]);
     cudaFree(a->sranks[b]);
     cudaFree(a->sstage[b]);
@@ -719,8 +728,8 @@ struct PipeArgs {
   const int32_t* admitted;
   const int32_t* target;
   int32_t* pending;
-  float* wstage[2];   // write-back stage (AsyncWB)
-  float* wstage_s[2];
+  float* wstage[kWbBufs];   // write-back stage (AsyncWB)
+  float* wstage_s[kWbBufs];
   int32_t* sranks;
   int32_t* stage_rows;
   float* astage;
@@ -1018,10 +1027,10 @@ static PipeArgs pipe_args(fc_cache* h, int p) {
   x.admitted = q->ib[p].admitted;
   x.target = q->ib[p].target;
   x.pending = a->pending;
-  x.wstage[0] = a->stage[0];
-  x.wstage[1] = a->stage[1];
-  x.wstage_s[0] = a->sstage[0];
-  x.wstage_s[1] = a->sstage[1];
+  for (int b = 0; b < kWbBufs; ++b) {
+    x.wstage[b] = a->stage[b];
+    x.wstage_s[b] = a->sstage[b];
+  }
   x.sranks = a->sranks[a->cur];
   x.stage_rows = a->dev_rows + a->cur;
   x.astage = q->astage[p];
@@ -1140,7 +1149,7 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
   }
   AsyncWB* a = h->awb;
   const int b = a->cur;
-  if (a->rows_in[b] > 0) {  // write-back stage b still holds a job from two commits ago
+  if (a->rows_in[b] > 0) {  // write-back stage b still holds a job from kWbBufs commits ago
     // the stream (not the host) waits until the host threads have scattered that job;
     // fall back to a host wait when stream memory operations are unavailable
     WaitValueFn wv = std::getenv("FC_HOST_WAIT") ? nullptr : wait_value_fn();
@@ -1196,7 +1205,7 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
     a->cv_q.notify_one();
     a->rows_in[b] = c.needed;
     a->rows_on_dev[b] = true;
-    a->cur ^= 1;
+    a->cur = (a->cur + 1) % kWbBufs;
   }
   info->misses = c.misses;
   info->hits = c.unique - c.misses;
