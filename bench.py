@@ -60,11 +60,11 @@ SEED = 1
 UPDATES_SEED = 7
 METRIC = "cached-embedding lookups/sec"
 # kernels launched per step (checked against the ncu launch list, profiles/r01_launches_*):
-# synchronous prepare = k_clear_pending + 20 (k_begin, k_mark_ids, 4 compactions x 3, k_unique_info,
-# k_inverse, k_plan, k_evict_async, k_admit_async, k_finish); pooled forward 1; sim update 1;
-# backward = radix sort (histogram + 2 one-sweep passes) + stream + fix-up + apply = 6
-KERNELS_PER_STEP = 21 + 1 + 1
-KERNELS_PER_TRAIN_STEP = 21 + 1 + 6
+# synchronous prepare = k_clear_pending + 16 (k_begin, k_mark_ids, 4 compactions x (count + emit),
+# k_unique_info, k_inverse, k_plan, k_evict_async, k_admit_async_tma, k_finish); pooled forward 1;
+# sim update 1; backward = radix sort (histogram + 2 one-sweep passes) + fused stream + fix-up = 5
+KERNELS_PER_STEP = 17 + 1 + 1
+KERNELS_PER_TRAIN_STEP = 17 + 1 + 5
 # prefetch pipeline: + k_evict_state, k_admit_state, k_publish (index phase) and
 # k_admit_stage / k_evict_commit / k_admit_commit instead of k_evict_async / k_admit_async
 PIPELINE_EXTRA_KERNELS = 3 + 1

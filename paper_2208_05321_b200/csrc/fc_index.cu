@@ -54,44 +54,50 @@ __global__ void __launch_bounds__(kNT) k_bits_count(WF wf, int64_t nwords, int64
   if (threadIdx.x == 0) cnt[blockIdx.x] = c;
 }
 
-template <class FIN>
-__global__ void __launch_bounds__(1024) k_bits_scan(int32_t* cnt, int nb, FIN fin, Counters* ctr, int gate) {
-  __shared__ int sm[1024 / 32 + 1];
-  if (!gate_open(ctr, gate)) return;
-  const int per = (nb + 1023) / 1024;
-  const int beg = threadIdx.x * per;
-  int s = 0;
-  for (int k = 0; k < per; ++k)
-    if (beg + k < nb) s += cnt[beg + k];
-  int tot;
-  int off = block_excl_scan<1024>(s, sm, tot);
-  for (int k = 0; k < per; ++k)
-    if (beg + k < nb) {
-      int v = cnt[beg + k];
-      cnt[beg + k] = off;
-      off += v;
-    }
-  if (threadIdx.x == 0) {
-    cnt[nb] = tot;
-    fin(tot, ctr);
-  }
-}
-
-template <class WF, class EM>
-__global__ void __launch_bounds__(kNT) k_bits_emit(WF wf, EM em, int64_t nwords, int64_t chunk, const int32_t* off,
-                                                   const int32_t* win, Counters* ctr, int gate) {
+// Emit, with the block-offset scan folded in: every block sums the per-block counts
+// before it (its base) and all of them (the total, <= kMaxScanBlocks loads per block),
+// runs the finisher on the total itself (the finishers only set counters, so the
+// blocks' identical writes are benign) and then emits its set bits in order.
+template <class WF, class EM, class FIN>
+__global__ void __launch_bounds__(kNT) k_bits_emit(WF wf, EM em, FIN fin, int64_t nwords, int64_t chunk,
+                                                   const int32_t* cnt, int nb, const int32_t* win, Counters* ctr,
+                                                   int gate) {
   __shared__ int sm[kNT / 32 + 1];
+  __shared__ int s_base;
+  __shared__ Counters lc;  // this block's view of the counters after the finisher
   if (!gate_open(ctr, gate)) return;
-  int lo = 0, hi = INT_MAX;
-  if (win != nullptr) {
-    lo = win[0];
-    hi = win[1];
+  int pre = 0, all = 0;
+  for (int b = threadIdx.x; b < nb; b += kNT) {
+    const int v = cnt[b];
+    all += v;
+    if (b < (int)blockIdx.x) pre += v;
   }
-  const int base = off[blockIdx.x];
-  const int bend = off[blockIdx.x + 1];
+  pre = block_sum<kNT>(pre, sm);
+  all = block_sum<kNT>(all, sm);
+  if (threadIdx.x == 0) {
+    s_base = pre;
+    // every block applies the finisher to a private copy (it only derives fields from
+    // the total and from fields earlier kernels set); block 0 alone publishes it, so
+    // 1000+ blocks do not all write the same counters line
+    lc = *ctr;
+    fin(all, &lc);
+    if (blockIdx.x == 0) fin(all, ctr);
+  }
+  __syncthreads();
+  if (!gate_open(&lc, gate)) return;  // the finisher may have raised an error
+  int lo = 0, hi = INT_MAX;
+  if (win != nullptr) {  // window fields read from the block's copy
+    const int32_t* lw = reinterpret_cast<const int32_t*>(reinterpret_cast<const char*>(&lc) +
+                                                         (reinterpret_cast<const char*>(win) -
+                                                          reinterpret_cast<const char*>(ctr)));
+    lo = lw[0];
+    hi = lw[1];
+  }
+  const int base = s_base;
+  const int bend = base + cnt[blockIdx.x];
   if (!EM::kVisitAll && (bend <= lo || base >= hi)) return;
   EM e = em;
-  e.init(ctr);
+  e.init(&lc);
   const int64_t b0 = (int64_t)blockIdx.x * chunk;
   const int64_t b1 = min(nwords, b0 + chunk);
   int run = base;
@@ -123,8 +129,7 @@ static void compact(WF wf, FIN fin, EM em, int64_t nwords, int32_t* cnt, const i
   const int nb = grid_for(nwords, 128, kMaxScanBlocks);
   const int64_t chunk = (nwords + nb - 1) / nb;
   k_bits_count<WF><<<nb, kNT, 0, st>>>(wf, nwords, chunk, cnt, ctr, gate);
-  k_bits_scan<FIN><<<1, 1024, 0, st>>>(cnt, nb, fin, ctr, gate);
-  k_bits_emit<WF, EM><<<nb, kNT, 0, st>>>(wf, em, nwords, chunk, cnt, win, ctr, gate);
+  k_bits_emit<WF, EM, FIN><<<nb, kNT, 0, st>>>(wf, em, fin, nwords, chunk, cnt, nb, win, ctr, gate);
 }
 
 // ------------------------------------------------------------------ unique ids (:268-289)
