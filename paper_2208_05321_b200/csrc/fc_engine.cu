@@ -27,6 +27,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstdlib>
+#include <cstdio>
 #include <cstring>
 #include <deque>
 #include <mutex>
@@ -40,6 +41,14 @@
 #include "fc_rowutil.cuh"
 
 namespace fc {
+
+// FC_DEBUG_WAITS=1: report host waits longer than 5 ms on stderr (diagnostics)
+static void slow_wait_note(const char* what, std::chrono::steady_clock::time_point t0) {
+  static const bool on = std::getenv("FC_DEBUG_WAITS") != nullptr;
+  if (!on) return;
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  if (ms > 5.0) fprintf(stderr, "[freqcache] slow host wait %.1f ms: %s\n", ms, what);
+}
 
 // Write-back stage buffers in rotation: a host scatter job may lag this many commits
 // behind before a stage reuse has to wait for it (absorbs host-thread jitter).
@@ -161,7 +170,9 @@ static void dispatcher_main(AsyncWB* a) {
     Job j = a->q.front();
     a->q.pop_front();
     lk.unlock();
+    const auto tw = std::chrono::steady_clock::now();
     cudaEventSynchronize(a->d2h[j.buf]);  // the staged rows are in pinned memory
+    slow_wait_note("dispatcher: write-back D2H event", tw);
     if (j.rows < 0) j.rows = a->hrows[j.buf];  // pipeline commit: count known only on device
     lk.lock();
     a->started_seq = j.seq;  // d2h[j.buf] / hrows[j.buf] may be re-recorded from here on
@@ -180,6 +191,7 @@ static void dispatcher_main(AsyncWB* a) {
     lk.lock();
     a->cv_helped.wait(lk, [&] { return a->helpers_left == 0; });
     a->scatter_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    slow_wait_note("dispatcher: host scatter of one job", t0);
     a->jobs_done += 1;
     a->done_seq = j.seq;
     *a->done_host = (uint32_t)j.seq;  // releases streams waiting on this job (stream wait-value)
@@ -1131,7 +1143,9 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
   const int p = q->par ^ 1;
   FC_TRY_E(pipe_launch_xfer(h, nullptr));  // deferred staging not triggered by an update: launch it now
   q->outstanding = false;
+  const auto tw0 = std::chrono::steady_clock::now();
   FC_CUDA(cudaEventSynchronize(q->ev_index[p]));
+  slow_wait_note("commit: index phase event", tw0);
   const Counters c = *q->hctr[p];
   h->host_free = c.free_count;
   info->unique = c.unique;
@@ -1185,7 +1199,9 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
   if (c.needed > 0) {  // ship the write-back stage (upper bound: every victim) D2H on the side stream
     {  // the dispatcher must have consumed d2h[b] of the previous job on stage b before it is re-recorded
       std::unique_lock<std::mutex> lk(a->m);
+      const auto tw1 = std::chrono::steady_clock::now();
       a->cv_started.wait(lk, [&] { return a->started_seq >= a->seq_of[b]; });
+      slow_wait_note("commit: previous write-back job on this stage to start", tw1);
     }
     FC_CUDA(cudaStreamWaitEvent(a->side, q->ev_commit[p], 0));
     FC_CUDA(cudaMemcpyAsync(a->hrows + b, a->dev_rows + b, sizeof(int32_t), cudaMemcpyDeviceToHost, a->side));

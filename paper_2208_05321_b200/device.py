@@ -67,6 +67,11 @@ class DeviceCache:
         self.rank_of = view(v.rank_of, (self.num_ids,), "<i4")
         self._slow = None
         self._slow_state = None
+        # prefetch pipeline: outputs in a ring of buffer sets owned by the cache (valid until
+        # PF_RING further prefetches; set by CachedEmbeddingBag, whose per-batch results die
+        # with the batch's backward) or freshly allocated per call (CacheStack results may
+        # be kept by the caller)
+        self.prefetch_ring = False
         # prefetch pipeline: run the index phase on the caller's stream (serialised with
         # the forward/backward; only the miss staging overlaps) or on a side stream
         self.index_on_main = os.environ.get("FC_INDEX_ON_MAIN", "0") == "1"
@@ -202,23 +207,58 @@ class DeviceCache:
         if index_on_main is None:
             index_on_main = self.index_on_main
         idx = main if index_on_main else self.index_stream
-        with torch.cuda.stream(idx):
-            # allocated on the index stream (no reuse hazard with blocks main still uses),
-            # then marked as used by main, which consumes them after the commit
-            d_ids = self.to_device_ids(ids)
-            n = int(d_ids.numel())
-            if n == 0:
-                raise ValueError("prefetch needs a non-empty batch")
+        slot = self._ring_slot(ids) if self.prefetch_ring else None
+        if slot is not None:
+            # a ring of PF_RING buffer sets owned by this cache: no per-step allocation (a
+            # cudaMalloc inside a training loop stalls the host for tens of ms). A set is
+            # rewritten PF_RING prefetches later, when the pipeline's event order has put
+            # its previous batch's backward behind us (see prefetch_ring)
+            buf, d_ids = slot
+            n = int(ids.numel())
+            with torch.cuda.stream(idx):
+                d_ids = d_ids[:n]
+                d_ids.copy_(ids.reshape(-1), non_blocking=True)
             k = min(n, self.capacity)
-            buf = torch.empty(4 * k + n, dtype=torch.int32, device=self.device)
-        d_ids.record_stream(main)
-        buf.record_stream(main)
+            buf = buf[:4 * k + n]
+        else:
+            with torch.cuda.stream(idx):
+                # allocated on the index stream (no reuse hazard with blocks main still uses),
+                # then marked as used by main, which consumes them after the commit
+                d_ids = self.to_device_ids(ids)
+                n = int(d_ids.numel())
+                if n == 0:
+                    raise ValueError("prefetch needs a non-empty batch")
+                k = min(n, self.capacity)
+                buf = torch.empty(4 * k + n, dtype=torch.int32, device=self.device)
+            d_ids.record_stream(main)
+            buf.record_stream(main)
         check(self.lib.fc_prepare_begin(self.h, ctypes.c_void_p(_ptr(d_ids)), d_ids.element_size(), n, int(batch_seq),
                                         ctypes.c_void_p(_ptr(buf[:k])), ctypes.c_void_p(_ptr(buf[k:2 * k])),
                                         ctypes.c_void_p(_ptr(buf[2 * k:3 * k])),
                                         ctypes.c_void_p(_ptr(buf[3 * k:4 * k])), ctypes.c_void_p(_ptr(buf[4 * k:])),
                                         ctypes.c_void_p(idx.cuda_stream)))
         self._pf = (buf, k, d_ids, ids)
+
+    PF_RING = 3
+
+    def _ring_slot(self, ids):
+        """Next buffer set of the prefetch ring, (re)allocated when the batch outgrows it;
+        None for inputs the ring does not take (non-tensor or empty ids)."""
+        torch = self.torch
+        if not isinstance(ids, torch.Tensor) or ids.numel() == 0 or ids.dtype not in (torch.int32, torch.int64):
+            return None
+        n = int(ids.numel())
+        ring = getattr(self, "_ring", None)
+        if ring is None or ring["n"] < n or ring["dtype"] != ids.dtype:
+            torch.cuda.synchronize(self.device)  # nothing in flight still uses the old ring
+            k = min(n, self.capacity)
+            ring = {"n": n, "dtype": ids.dtype, "i": 0,
+                    "sets": [(torch.empty(4 * k + n, dtype=torch.int32, device=self.device),
+                              torch.empty(n, dtype=ids.dtype, device=self.device)) for _ in range(self.PF_RING)]}
+            self._ring = ring
+        s = ring["sets"][ring["i"] % self.PF_RING]
+        ring["i"] += 1
+        return s
 
     def prepare_commit(self):
         """Finish the outstanding prefetch on the current stream (fc_prepare_commit).

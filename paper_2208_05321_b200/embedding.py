@@ -103,6 +103,7 @@ class CachedEmbeddingBag(torch.nn.Module):
             self.slow_state.fill(0.0)
         self.cache.attach_slow(self.slow_rows, self.slow_state)
         self.cache.set_engine(engine)
+        self.cache.prefetch_ring = True  # a batch's prepare outputs die with its backward
         if warmup:
             self.cache.warmup(self.capacity)
         self._anchor = torch.nn.Parameter(torch.empty(0, device=self.cache.device), requires_grad=True)

@@ -1,3 +1,7 @@
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_embedding.py tests/test_gpu_prefetch.py -x -q > gpurun_out/pytest_fused.log 2>&1; echo rc=$? >> gpurun_out/pytest_fused.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_sort.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-prefetch > gpurun_out/ncu_bench.log 2>&1
+rm -f gpurun_out/fused.txt
+for i in 1 2 3; do for v in X=1 FC_BWD_UNFUSED=1; do
+  env $v timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench_v.json 2> /dev/null
+  python -c "
+import json; d=json.load(open('gpurun_out/bench_v.json')); print('$v', round(d['value']/1e6,1), round(d['ms_per_step'],3), round(d['e2e']['value']/1e6,1))" >> gpurun_out/fused.txt
+done; done
