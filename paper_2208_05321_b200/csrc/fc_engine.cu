@@ -814,6 +814,26 @@ __device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned 
                "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
                : "memory");
 }
+// the same with an L2 evict-first hint: miss-staging traffic should not displace the
+// index tables and rows the concurrent kernels work on
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ void bulk_g2s_ef(void* smem, const void* gmem, unsigned bytes, uint64_t* bar, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(smem)),
+      "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_s2g_ef(void* gmem, const void* smem, unsigned bytes, uint64_t pol) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem),
+               "r"(smem_u32(smem)), "r"(bytes), "l"(pol)
+               : "memory");
+}
+
 __device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, unsigned bytes) {
   asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)),
                "r"(bytes)
@@ -833,6 +853,7 @@ __global__ void __launch_bounds__(32) k_admit_stage_tma(PipeArgs x, int G) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
+  const uint64_t pol = l2_evict_first();
   unsigned phase_bits = 0;
   const int ngroups = (m + G - 1) / G;
   // group k of this block = blockIdx.x + k * gridDim.x; up to kTmaStages groups in flight.
@@ -857,11 +878,11 @@ __global__ void __launch_bounds__(32) k_admit_stage_tma(PipeArgs x, int G) {
         const int r = x.admitted[j0 + i];
         const int pk = x.pending[r];
         const float* src = pk >= 0 ? x.wstage[pk / x.cap] + (int64_t)(pk % x.cap) * x.D : x.slow + (int64_t)r * x.ld;
-        bulk_g2s(rows + (size_t)i * rb, src, rb, &bar[st]);
+        bulk_g2s_ef(rows + (size_t)i * rb, src, rb, &bar[st], pol);
         if (x.S) {
           const float* ss =
               pk >= 0 ? x.wstage_s[pk / x.cap] + (int64_t)(pk % x.cap) * x.S : x.sstate + (int64_t)r * x.sld;
-          bulk_g2s(srows + (size_t)i * sb, ss, sb, &bar[st]);
+          bulk_g2s_ef(srows + (size_t)i * sb, ss, sb, &bar[st], pol);
         }
       }
       ++issued;
@@ -875,8 +896,8 @@ __global__ void __launch_bounds__(32) k_admit_stage_tma(PipeArgs x, int G) {
       const int g = blockIdx.x + retired * gridDim.x;
       const int j0 = g * G, cnt = min(G, m - j0);
       unsigned char* rows = ring + st * stage_bytes;
-      bulk_s2g(x.astage + (int64_t)j0 * x.D, rows, cnt * rb);
-      if (x.S) bulk_s2g(x.astage_s + (int64_t)j0 * x.S, rows + (size_t)G * rb, cnt * sb);
+      bulk_s2g_ef(x.astage + (int64_t)j0 * x.D, rows, cnt * rb, pol);
+      if (x.S) bulk_s2g_ef(x.astage_s + (int64_t)j0 * x.S, rows + (size_t)G * rb, cnt * sb, pol);
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
     }
     __syncwarp();

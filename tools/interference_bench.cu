@@ -14,6 +14,7 @@
 #include <random>
 #include <vector>
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #define CK(x)                                                             \
@@ -129,6 +130,18 @@ __global__ void tma_gather(const char* __restrict__ host, char* __restrict__ dev
     if (g >= ngroups && issued == 0) break;
   }
   asm volatile("cp.async.bulk.wait_group 0;");
+}
+
+// latency-bound: two dependent random index loads, then a random 512 B row per warp
+__global__ void dep_gather(const int* __restrict__ a, const int* __restrict__ b, const float4* __restrict__ rows,
+                           float4* __restrict__ out, int n, int nrows) {
+  const int lane = threadIdx.x & 31;
+  const long warp = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const long nw = (gridDim.x * (long)blockDim.x) >> 5;
+  for (long j = warp; j < n; j += nw) {
+    const int r = b[a[j] % nrows] % nrows;
+    out[j * 32 + lane] = rows[(long)r * 32 + lane];
+  }
 }
 
 struct Timer {
@@ -251,6 +264,74 @@ int main() {
     both(nm, H, ZC(c[0], c[1], c[2]));
   }
   CK(cudaFuncSetAttribute(tma_gather<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 512));
+  {  // latency-bound gather (the cache's index/backward kernels) next to the host-link staging
+    const int nL = 1 << 20, nrows = 1 << 21;  // 1M row gathers from a 1 GiB table
+    int *la, *lb;
+    CK(cudaMalloc(&la, nL * 4));
+    CK(cudaMalloc(&lb, nrows * 4));
+    std::vector<int> h1(nL), h2(nrows);
+    for (int i = 0; i < nL; ++i) h1[i] = (int)(g() % nrows);
+    for (int i = 0; i < nrows; ++i) h2[i] = (int)(g() % nrows);
+    CK(cudaMemcpy(la, h1.data(), nL * 4, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(lb, h2.data(), nrows * 4, cudaMemcpyHostToDevice));
+    float4* lout;
+    CK(cudaMalloc(&lout, (long)nL * 512));
+    auto L = [=](cudaStream_t s) { dep_gather<<<148 * 8, 256, 0, s>>>(la, lb, ha, lout, nL, nrows); };
+    const float tl = alone("L  dependent gather 1M rows", L);
+    printf("   -> %.0f GB/s\n", nL * 512.0 * 2 / tl / 1e6);
+    both("L + T(64)", L, [=](cudaStream_t s) {
+      tma_gather<4><<<64, 32, 4 * 32 * 512, s>>>((const char*)hostd, (char*)zdst, didx, rows);
+    });
+    both("L + Z(148)", L, [&](cudaStream_t s) { Z(s, 148); });
+    both("L + DH", L, DH);
+    {  // green contexts: the staging on its own SMs, the compute on the rest
+      CUdevice cdev;
+      cuDeviceGet(&cdev, 0);
+      CUdevResource all, part[1], rest;
+      unsigned nb = 1;
+      CUresult r = cuDeviceGetDevResource(cdev, &all, CU_DEV_RESOURCE_TYPE_SM);
+      if (r == CUDA_SUCCESS) r = cuDevSmResourceSplitByCount(part, &nb, &all, &rest, 0, 16);
+      CUdevResourceDesc d1, d2;
+      CUgreenCtx g1, g2;
+      CUstream gs1 = nullptr, gs2 = nullptr;
+      if (r == CUDA_SUCCESS) r = cuDevResourceGenerateDesc(&d1, part, 1);
+      if (r == CUDA_SUCCESS) r = cuDevResourceGenerateDesc(&d2, &rest, 1);
+      if (r == CUDA_SUCCESS) r = cuGreenCtxCreate(&g1, d1, cdev, CU_GREEN_CTX_DEFAULT_STREAM);
+      if (r == CUDA_SUCCESS) r = cuGreenCtxCreate(&g2, d2, cdev, CU_GREEN_CTX_DEFAULT_STREAM);
+      if (r == CUDA_SUCCESS) r = cuGreenCtxStreamCreate(&gs1, g1, CU_STREAM_NON_BLOCKING, 0);
+      if (r == CUDA_SUCCESS) r = cuGreenCtxStreamCreate(&gs2, g2, CU_STREAM_NON_BLOCKING, 0);
+      printf("green ctx setup: %d (staging SMs %u, compute SMs %u)\n", (int)r, part[0].sm.smCount, rest.sm.smCount);
+      if (r == CUDA_SUCCESS) {
+        cudaStream_t ts = (cudaStream_t)gs1, cs = (cudaStream_t)gs2;
+        auto run = [&](bool withT, bool withL) {
+          cudaEvent_t a, b, c, d;
+          cudaEventCreate(&a); cudaEventCreate(&b); cudaEventCreate(&c); cudaEventCreate(&d);
+          float bl = 1e9, bt = 1e9;
+          for (int rep = 0; rep < 5; ++rep) {
+            cudaDeviceSynchronize();
+            cudaEventRecord(a, cs);
+            cudaEventRecord(c, ts);
+            if (withL) dep_gather<<<148 * 8, 256, 0, cs>>>(la, lb, ha, lout, nL, nrows);
+            if (withT) tma_gather<4><<<64, 32, 4 * 32 * 512, ts>>>((const char*)hostd, (char*)zdst, didx, rows);
+            cudaEventRecord(b, cs);
+            cudaEventRecord(d, ts);
+            cudaDeviceSynchronize();
+            float x, y;
+            cudaEventElapsedTime(&x, a, b);
+            cudaEventElapsedTime(&y, c, d);
+            bl = std::min(bl, x);
+            bt = std::min(bt, y);
+          }
+          printf("green: L %s T %s -> L %.3f ms | T %.3f ms (err %s)\n", withL ? "on" : "off", withT ? "on" : "off", bl, bt,
+                 cudaGetErrorString(cudaGetLastError()));
+        };
+        run(false, true);
+        run(true, false);
+        run(true, true);
+      }
+    }
+    both("L + DD", L, DD);
+  }
   for (int grid : {16, 32, 64, 148}) {
     auto T = [=](cudaStream_t s) {
       tma_gather<4><<<grid, 32, 4 * 32 * 512, s>>>((const char*)hostd, (char*)zdst, didx, rows);
