@@ -201,7 +201,7 @@ __device__ __forceinline__ void bwd_flush(const BwdArgs& x, int64_t c, int64_t j
 }
 
 template <bool APPLY>
-__global__ void __launch_bounds__(kNT, APPLY ? 3 : 4) k_bwd_stream(BwdArgs x) {
+__global__ void __launch_bounds__(kNT, 4) k_bwd_stream(BwdArgs x) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
