@@ -350,7 +350,9 @@ def run_ours(args, cfg, torch, rank, world):
         fill_pinned(torch, rows, dev, SEED + rank)
         shard = CudaShard(idx.num_ids, D, fc.fast_capacity(idx.num_ids, cfg["ratio"]), rows, idx, optimizer=OPT,
                           lr=LR, device=dev, engine=args.engine, global_num_ids=cfg["num_ids"])
-        mod = RowShardedEmbedding(shard, world, rank, mode=MODE, device=dev)
+        # owners write the looked-up rows straight into the requesters' buffers over NVLink
+        # peer memory (fc_pool_to_peers); --no-peer keeps the NCCL all-to-all of the rows
+        mod = RowShardedEmbedding(shard, world, rank, mode=MODE, device=dev, peer_rows=0 if args.no_peer else N)
         dcs = [shard.cache]
         cap = shard.cache.capacity
     dc = dcs[0]
@@ -529,7 +531,9 @@ def run_ours(args, cfg, torch, rank, world):
                    "prefetch": pipelined,
                    "l2": "inputs larger than L2 (fast tier %d MB, id/rank maps %d MB, new batch every step)"
                          % (cap * D * 4 >> 20, cfg["num_ids"] * 12 // world >> 20),
-                   "parallelism": "single" if not sharded else f"rowwise{world} (id/row all-to-all over NCCL)"},
+                   "parallelism": "single" if not sharded else
+                   (f"rowwise{world} (unique ids by NCCL all-to-all; rows back "
+                    + ("by NCCL all-to-all)" if args.no_peer else "by owner-side peer-memory writes)"))},
         "step_latency_ms": {"p50": float(np.percentile(step_ms, 50)), "p99": float(np.percentile(step_ms, 99)),
                             "prepare_avg": (None if pipelined else prof["prepare_ms"] / max(prof["calls"], 1)),
                             "miss_transfer_avg": rl[0]["launch_ms"] if rl[0]["bound"] == "host_link" else None,
@@ -592,6 +596,8 @@ def main():
     ap.add_argument("--cpu-baseline-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--sharded", action="store_true", help="row-sharded module even at one GPU (needs torchrun)")
+    ap.add_argument("--no-peer", action="store_true",
+                    help="row-sharded runs: return rows with NCCL all-to-all instead of peer-memory writes")
     ap.add_argument("--no-prefetch", action="store_true",
                     help="synchronous prepare each step (no lookahead pipeline)")
     ap.add_argument("--engine", default="async", choices=["async", "zerocopy"],

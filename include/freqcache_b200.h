@@ -261,6 +261,19 @@ int fc_route_grads(fc_router* r, const int32_t* inverse_dev, int64_t u, int64_t 
                    const float* per_sample_weights, int32_t mode, const float* grad_out, int32_t dim,
                    float* grad_unique, void* stream);
 
+/* Owner side of the row-sharded forward fused with the return exchange: the cached row
+ * of received id i (requester r = the segment of i in seg_dev[0..world]) is written
+ * straight into requester r's receive buffer dst_ptrs_dev[r] (a peer pointer over NVLink,
+ * from fc_ipc_open, or local memory for r == self) at row dst_off_dev[r] + (i - seg[r]).
+ * Order it before a stream-ordered barrier (a tiny all-reduce) before requesters read. */
+int fc_pool_to_peers(fc_cache* h, const int32_t* unique_slots, const int32_t* inverse, int64_t n,
+                     const int64_t* seg_dev, int32_t world, float* const* dst_ptrs_dev, const int64_t* dst_off_dev,
+                     void* stream);
+/* CUDA IPC plumbing for the peer pointers (64-byte opaque handles). */
+int fc_ipc_handle(void* dev_ptr, void* handle_out);
+int fc_ipc_open(const void* handle, int32_t device, void** dev_ptr_out);
+int fc_ipc_close(void* dev_ptr);
+
 #ifdef __cplusplus
 }
 #endif

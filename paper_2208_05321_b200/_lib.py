@@ -75,6 +75,11 @@ _SIGS = {
                                c_int32, c_void_p, c_void_p]),
     "fc_route_grads": (c_int32, [c_void_p, c_void_p, c_int64, c_int64, c_void_p, c_int32, c_int64, c_int32, c_void_p,
                                  c_int32, c_void_p, c_int32, c_void_p, c_void_p]),
+    "fc_pool_to_peers": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                   c_void_p]),
+    "fc_ipc_handle": (c_int32, [c_void_p, c_void_p]),
+    "fc_ipc_open": (c_int32, [c_void_p, c_int32, POINTER(c_void_p)]),
+    "fc_ipc_close": (c_int32, [c_void_p]),
     "fc_trace": (c_int32, [c_void_p, c_int32]),
     "fc_trace_mark": (c_int32, [c_void_p, c_int32, c_void_p]),
     "fc_trace_read": (c_int64, [c_void_p, c_void_p, c_void_p, c_int64]),

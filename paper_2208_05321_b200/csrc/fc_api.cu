@@ -608,6 +608,35 @@ int fc_gather_rows(fc_cache* h, const int32_t* slots, int64_t n, float* out, voi
   return launch_gather_rows(h, slots, n, out, as_stream(stream));
 }
 
+int fc_pool_to_peers(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const int64_t* seg_dev,
+                     int32_t world, float* const* dst_ptrs_dev, const int64_t* dst_off_dev, void* stream) {
+  if (!h || world < 1 || world > 64 || n < 0) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  return launch_pool_to_peers(h, uslots, inv, n, seg_dev, world, dst_ptrs_dev, dst_off_dev, as_stream(stream));
+}
+
+int fc_ipc_handle(void* dev_ptr, void* handle_out) {
+  if (!dev_ptr || !handle_out) return FC_ERR_BAD_ARG;
+  cudaIpcMemHandle_t hd;
+  FC_CUDA(cudaIpcGetMemHandle(&hd, dev_ptr));
+  std::memcpy(handle_out, &hd, sizeof(hd));
+  return FC_OK;
+}
+
+int fc_ipc_open(const void* handle, int32_t device, void** dev_ptr_out) {
+  if (!handle || !dev_ptr_out) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(device);
+  cudaIpcMemHandle_t hd;
+  std::memcpy(&hd, handle, sizeof(hd));
+  FC_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, hd, cudaIpcMemLazyEnablePeerAccess));
+  return FC_OK;
+}
+
+int fc_ipc_close(void* dev_ptr) {
+  if (dev_ptr) FC_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  return FC_OK;
+}
+
 int fc_apply_unique_update(fc_cache* h, const int32_t* uslots, int64_t u, const float* add, void* stream) {
   if (!h) return FC_ERR_BAD_ARG;
   DeviceGuard dg(h->device);

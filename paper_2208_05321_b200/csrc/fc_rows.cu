@@ -451,6 +451,69 @@ int launch_pool_rows(const float* rows, int D, const int32_t* uslots, const int3
   return FC_OK;
 }
 
+// ------------------------------------------------------------- pooled rows straight to the requesters
+// Row-sharded forward, owner side, fused with the return exchange: received id i (from
+// requester r = the segment of i in seg[0..W]) is looked up in the cache and its row is
+// written directly into requester r's receive buffer over NVLink peer memory (CUDA IPC /
+// symmetric pointers), at row dst_off[r] + (i - seg[r]). Replaces "pool into a local
+// buffer, then all-to-all". The caller orders it before a stream-ordered barrier.
+__global__ void __launch_bounds__(kNT) k_pool_to_peers(const float* __restrict__ fast, int D,
+                                                       const int32_t* __restrict__ uslots,
+                                                       const int32_t* __restrict__ inv, int64_t n,
+                                                       const int64_t* __restrict__ seg, int W,
+                                                       float* const* __restrict__ dst, const int64_t* __restrict__ dst_off,
+                                                       Units un) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    const bool act = i < n;
+    const float* src = nullptr;
+    float* out = nullptr;
+    if (act) {
+      int r = 0;
+      while (r + 1 < W && seg[r + 1] <= i) ++r;  // W <= 64: a short scan
+      src = fast + (int64_t)uslots[inv[i]] * D;
+      out = dst[r] + (dst_off[r] + (i - seg[r])) * (int64_t)D;
+    }
+    // lanes sweep the 32 rows' 16-byte units (4 in flight), writing to each row's owner
+    const int total = 32 * un.upr;
+    for (int u0 = 0; u0 < total; u0 += 32 * 4) {
+      float4 v[4];
+      float* d[4];
+      bool a[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int u = u0 + q * 32 + lane;
+        const int rr = min(un.row(u), 31);
+        const int c = (u - rr * un.upr) * 4;
+        const float* sp = reinterpret_cast<const float*>(__shfl_sync(FC_FULL, reinterpret_cast<long long>(src), rr));
+        d[q] = reinterpret_cast<float*>(__shfl_sync(FC_FULL, reinterpret_cast<long long>(out), rr)) + c;
+        a[q] = __shfl_sync(FC_FULL, (int)act, rr) && u < total;
+        if (a[q]) v[q] = ld4(sp + c);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (a[q]) st4(d[q], v[q]);
+    }
+  }
+  __threadfence_system();  // peer-memory stores visible before the caller's barrier
+}
+
+int launch_pool_to_peers(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const int64_t* seg, int W,
+                         float* const* dst, const int64_t* dst_off, cudaStream_t st) {
+  if (n <= 0) return FC_OK;
+  if (h->dim % 4) {
+    set_error("pool_to_peers needs dim %% 4 == 0");
+    return FC_ERR_BAD_ARG;
+  }
+  k_pool_to_peers<<<grid_for(n, kNT, kSMs * 8), kNT, 0, st>>>(h->fast, h->dim, uslots, inv, n, seg, W, dst, dst_off,
+                                                              units_for(h->dim));
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
 // ------------------------------------------------------------- gather_unique (:509-510)
 template <bool VEC>
 __global__ void __launch_bounds__(kNT) k_gather_rows(const float* __restrict__ fast, int D, const int32_t* __restrict__ slots,

@@ -201,6 +201,71 @@ def _lens(offsets, n, include_last_offset):
     return torch.cat([off[1:], off.new_tensor([n])]) - off
 
 
+class PeerRows:
+    """The row-sharded forward's return exchange fused into the owner's gather: every rank
+    exposes one receive buffer [max_rows, D] to all peers (CUDA IPC handles exchanged once
+    with all_gather_object), and an owner's `fc_pool_to_peers` kernel writes each
+    requested row straight into its requester's buffer over NVLink, at the position the
+    requester's routing expects. A one-element all-reduce on the stream then orders the
+    writes before any requester reads. Replaces "gather into a local buffer + NCCL
+    all-to-all of the rows"."""
+
+    def __init__(self, shard, world: int, rank: int, max_rows: int, group, device):
+        import ctypes
+
+        from . import _lib
+        from .errors import check
+
+        self._ct, self._check, self.lib = ctypes, check, _lib.load()
+        self.world, self.rank, self.group, self.device = world, rank, group, torch.device(device)
+        self.max_rows, self.dim = int(max_rows), int(shard.dim)
+        self.rbuf = torch.empty((self.max_rows, self.dim), dtype=torch.float32, device=self.device)
+        hd = (ctypes.c_ubyte * 64)()
+        check(self.lib.fc_ipc_handle(ctypes.c_void_p(self.rbuf.data_ptr()), hd))
+        handles = [None] * world
+        dist.all_gather_object(handles, bytes(hd), group=group)
+        self._opened = []
+        ptrs = []
+        for r in range(world):
+            if r == rank:
+                ptrs.append(self.rbuf.data_ptr())
+                continue
+            p = ctypes.c_void_p()
+            buf = (ctypes.c_ubyte * 64).from_buffer_copy(handles[r])
+            check(self.lib.fc_ipc_open(buf, self.device.index or 0, ctypes.byref(p)))
+            self._opened.append(p)
+            ptrs.append(p.value)
+        self.dst = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    def close(self):
+        for p in getattr(self, "_opened", []):
+            self.lib.fc_ipc_close(p)
+        self._opened = []
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def pool_to_peers(self, shard, h, x):
+        ct = self._ct
+        m, me, W = x["mat"], self.rank, self.world
+        if x["u"] > self.max_rows:
+            raise RuntimeError(f"PeerRows buffer holds {self.max_rows} rows, batch routes {x['u']}")
+        seg = torch.tensor(np.concatenate([[0], np.cumsum(x["rc"])]), dtype=torch.int64, device=self.device)
+        # my segment in requester r's routing order starts after the ids r sends to owners < me
+        off = torch.tensor([sum(m[r][:me]) for r in range(W)], dtype=torch.int64, device=self.device)
+        stream = ct.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        self._check(self.lib.fc_pool_to_peers(shard.cache.h, ct.c_void_p(h["uslots"].data_ptr()),
+                                              ct.c_void_p(h["inverse"].data_ptr()), int(h["n"]),
+                                              ct.c_void_p(seg.data_ptr()), W, ct.c_void_p(self.dst.data_ptr()),
+                                              ct.c_void_p(off.data_ptr()), stream))
+        dist.all_reduce(self.flag, group=self.group)  # every owner's writes land before anyone reads
+        return self.rbuf[:x["u"]]
+
+
 # ----------------------------------------------------------------------------- row-wise (scaling)
 class _RowShardFn(torch.autograd.Function):
     @staticmethod
@@ -227,7 +292,7 @@ class RowShardedEmbedding(torch.nn.Module):
     cache's prefetch pipeline; the next forward with the same ids commits it."""
 
     def __init__(self, shard, world: int, rank: int, mode: str = "sum", include_last_offset: bool = False,
-                 group=None, device=None):
+                 group=None, device=None, peer_rows: int = 0):
         super().__init__()
         self.shard, self.world, self.rank = shard, world, rank
         self.mode, self.include_last_offset, self.group = mode, include_last_offset, group
@@ -238,10 +303,13 @@ class RowShardedEmbedding(torch.nn.Module):
         # on a GPU the exchange planning, expansion and gradient reduction run in
         # libfreqcache_b200 (Router); on CPU (gloo tests) the same steps in torch
         self.router = None
+        self.peer = None
         if self.device.type == "cuda":
             num_ids = getattr(shard, "global_num_ids", None)
             if num_ids is not None:
                 self.router = Router(num_ids, world, self.device)
+                if peer_rows:  # fused return exchange over NVLink peer memory (PeerRows)
+                    self.peer = PeerRows(shard, world, rank, int(peer_rows), group, self.device)
 
     @staticmethod
     def owner_of(ids, world):
@@ -253,6 +321,16 @@ class RowShardedEmbedding(torch.nn.Module):
         if self.router is not None:  # grouped by owner already: no permutation to undo
             send_ids, inv, sc = self.router.route(ids)
             order = None
+            if self.peer is not None:  # the full W x W count matrix: splits + peer-write offsets
+                mine = torch.tensor(sc, dtype=torch.int64, device=ids.device)
+                mat = torch.empty(W * W, dtype=torch.int64, device=ids.device)
+                dist.all_gather_into_tensor(mat, mine, group=self.group)
+                m = mat.view(W, W).tolist()  # m[r][o] = ids rank r sends to owner o
+                rc = [m[r][self.rank] for r in range(W)]
+                recv_ids = torch.empty(sum(rc), dtype=send_ids.dtype, device=send_ids.device)
+                _a2a(recv_ids, send_ids.contiguous(), rc, sc, self.group)
+                return {"inv": inv, "order": None, "sc": sc, "rc": rc, "recv_ids": recv_ids,
+                        "u": int(send_ids.numel()), "mat": m}
             send_counts = torch.tensor(sc, dtype=torch.int64, device=ids.device)
         else:
             uniq, inv = torch.unique(ids.long(), sorted=True, return_inverse=True)
@@ -292,9 +370,12 @@ class RowShardedEmbedding(torch.nn.Module):
         if h is None:
             h = self.shard.prepare(x["recv_ids"])
         self.last_recv = int(x["recv_ids"].numel())
-        rows = self.shard.pool(h)  # [n_recv, D] one row per received (unique per requester) id
-        back = torch.empty((x["u"], rows.shape[1]), dtype=rows.dtype, device=rows.device)
-        _a2a(back, rows.contiguous(), x["sc"], x["rc"], self.group)
+        if self.peer is not None:  # owners write the rows straight into the requesters' buffers
+            back = self.peer.pool_to_peers(self.shard, h, x)
+        else:
+            rows = self.shard.pool(h)  # [n_recv, D] one row per received (unique per requester) id
+            back = torch.empty((x["u"], rows.shape[1]), dtype=rows.dtype, device=rows.device)
+            _a2a(back, rows.contiguous(), x["sc"], x["rc"], self.group)
         if self.router is not None:  # back is in routing order: pool straight through the inverse
             out = self.router.pool(back, x["inv"], offsets, n_bags, self.include_last_offset, psw, self.mode)
         else:
