@@ -269,6 +269,12 @@ int fc_route_grads(fc_router* r, const int32_t* inverse_dev, int64_t u, int64_t 
 int fc_pool_to_peers(fc_cache* h, const int32_t* unique_slots, const int32_t* inverse, int64_t n,
                      const int64_t* seg_dev, int32_t world, float* const* dst_ptrs_dev, const int64_t* dst_off_dev,
                      void* stream);
+/* The backward's mirror: an owner pulls the gradient row of each received id i
+ * (requester r = the segment of i) from src_ptrs_dev[r] at row src_off_dev[r] + (i - seg[r])
+ * over peer memory into out [n, dim]; order it after a barrier that follows the
+ * requesters' writes. */
+int fc_gather_from_peers(const float* const* src_ptrs_dev, const int64_t* src_off_dev, const int64_t* seg_dev,
+                         int32_t world, int64_t n, int32_t dim, float* out, void* stream);
 /* CUDA IPC plumbing for the peer pointers (64-byte opaque handles). */
 int fc_ipc_handle(void* dev_ptr, void* handle_out);
 int fc_ipc_open(const void* handle, int32_t device, void** dev_ptr_out);

@@ -615,6 +615,12 @@ int fc_pool_to_peers(fc_cache* h, const int32_t* uslots, const int32_t* inv, int
   return launch_pool_to_peers(h, uslots, inv, n, seg_dev, world, dst_ptrs_dev, dst_off_dev, as_stream(stream));
 }
 
+int fc_gather_from_peers(const float* const* src_ptrs_dev, const int64_t* src_off_dev, const int64_t* seg_dev,
+                         int32_t world, int64_t n, int32_t dim, float* out, void* stream) {
+  if (world < 1 || world > 64 || n < 0 || dim < 1 || dim % 4) return FC_ERR_BAD_ARG;
+  return launch_gather_from_peers(src_ptrs_dev, src_off_dev, seg_dev, world, n, dim, out, as_stream(stream));
+}
+
 int fc_ipc_handle(void* dev_ptr, void* handle_out) {
   if (!dev_ptr || !handle_out) return FC_ERR_BAD_ARG;
   cudaIpcMemHandle_t hd;

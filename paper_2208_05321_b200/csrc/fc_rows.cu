@@ -514,6 +514,55 @@ int launch_pool_to_peers(fc_cache* h, const int32_t* uslots, const int32_t* inv,
   return FC_OK;
 }
 
+// The mirror for the backward: the owner pulls the gradient rows of its received ids
+// from the requesters' buffers over peer memory — received id i (requester r = segment
+// of i) reads src[r] row src_off[r] + (i - seg[r]) — into a local contiguous [n, D].
+__global__ void __launch_bounds__(kNT) k_gather_from_peers(const float* const* __restrict__ src,
+                                                           const int64_t* __restrict__ src_off,
+                                                           const int64_t* __restrict__ seg, int W, int64_t n, int D,
+                                                           float* __restrict__ out, Units un) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  for (int64_t base = warp * 32; base < n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    const bool act = i < n;
+    const float* sp = nullptr;
+    if (act) {
+      int r = 0;
+      while (r + 1 < W && seg[r + 1] <= i) ++r;
+      sp = src[r] + (src_off[r] + (i - seg[r])) * (int64_t)D;
+    }
+    const int total = 32 * un.upr;
+    for (int u0 = 0; u0 < total; u0 += 32 * 4) {
+      float4 v[4];
+      int64_t d[4];
+      bool a[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int u = u0 + q * 32 + lane;
+        const int rr = min(un.row(u), 31);
+        const int c = (u - rr * un.upr) * 4;
+        const float* s = reinterpret_cast<const float*>(__shfl_sync(FC_FULL, reinterpret_cast<long long>(sp), rr));
+        d[q] = (base + rr) * D + c;
+        a[q] = __shfl_sync(FC_FULL, (int)act, rr) && u < total;
+        if (a[q]) v[q] = ld4(s + c);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (a[q]) st4(out + d[q], v[q]);
+    }
+  }
+}
+
+int launch_gather_from_peers(const float* const* src, const int64_t* src_off, const int64_t* seg, int W, int64_t n,
+                             int D, float* out, cudaStream_t st) {
+  if (n <= 0) return FC_OK;
+  k_gather_from_peers<<<grid_for(n, kNT, kSMs * 8), kNT, 0, st>>>(src, src_off, seg, W, n, D, out, units_for(D));
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
 // ------------------------------------------------------------- gather_unique (:509-510)
 template <bool VEC>
 __global__ void __launch_bounds__(kNT) k_gather_rows(const float* __restrict__ fast, int D, const int32_t* __restrict__ slots,

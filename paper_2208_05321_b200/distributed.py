@@ -137,9 +137,9 @@ class Router:
             {"sum": 0, "mean": 1}[mode], ct.c_void_p(out.data_ptr()), self._stream()))
         return out
 
-    def grads(self, inv, u, grad_out, offsets, n_bags, include_last_offset, psw, mode):
+    def grads(self, inv, u, grad_out, offsets, n_bags, include_last_offset, psw, mode, out=None):
         ct = self._ct
-        gu = torch.empty((u, grad_out.shape[1]), dtype=torch.float32, device=self.device)
+        gu = torch.empty((u, grad_out.shape[1]), dtype=torch.float32, device=self.device) if out is None else out
         g = grad_out.contiguous()
         self._check(self.lib.fc_route_grads(
             self.h, ct.c_void_p(inv.data_ptr()), int(u), int(inv.numel()),
@@ -219,24 +219,32 @@ class PeerRows:
         self._ct, self._check, self.lib = ctypes, check, _lib.load()
         self.world, self.rank, self.group, self.device = world, rank, group, torch.device(device)
         self.max_rows, self.dim = int(max_rows), int(shard.dim)
-        self.rbuf = torch.empty((self.max_rows, self.dim), dtype=torch.float32, device=self.device)
-        hd = (ctypes.c_ubyte * 64)()
-        check(self.lib.fc_ipc_handle(ctypes.c_void_p(self.rbuf.data_ptr()), hd))
-        handles = [None] * world
-        dist.all_gather_object(handles, bytes(hd), group=group)
         self._opened = []
+        # rbuf: rows owners write to me (forward); gbuf: my per-id gradients owners read (backward)
+        self.rbuf = torch.empty((self.max_rows, self.dim), dtype=torch.float32, device=self.device)
+        self.gbuf = torch.empty((self.max_rows, self.dim), dtype=torch.float32, device=self.device)
+        self.dst = self._share(self.rbuf)
+        self.gsrc = self._share(self.gbuf)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+
+    def _share(self, buf):
+        """Every rank's pointer to its peers' copy of `buf` (CUDA IPC), as a device array."""
+        ct = self._ct
+        hd = (ct.c_ubyte * 64)()
+        self._check(self.lib.fc_ipc_handle(ct.c_void_p(buf.data_ptr()), hd))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, bytes(hd), group=self.group)
         ptrs = []
-        for r in range(world):
-            if r == rank:
-                ptrs.append(self.rbuf.data_ptr())
+        for r in range(self.world):
+            if r == self.rank:
+                ptrs.append(buf.data_ptr())
                 continue
-            p = ctypes.c_void_p()
-            buf = (ctypes.c_ubyte * 64).from_buffer_copy(handles[r])
-            check(self.lib.fc_ipc_open(buf, self.device.index or 0, ctypes.byref(p)))
+            p = ct.c_void_p()
+            hb = (ct.c_ubyte * 64).from_buffer_copy(handles[r])
+            self._check(self.lib.fc_ipc_open(hb, self.device.index or 0, ct.byref(p)))
             self._opened.append(p)
             ptrs.append(p.value)
-        self.dst = torch.tensor(ptrs, dtype=torch.int64, device=self.device)
-        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        return torch.tensor(ptrs, dtype=torch.int64, device=self.device)
 
     def close(self):
         for p in getattr(self, "_opened", []):
@@ -264,6 +272,30 @@ class PeerRows:
                                               ct.c_void_p(off.data_ptr()), stream))
         dist.all_reduce(self.flag, group=self.group)  # every owner's writes land before anyone reads
         return self.rbuf[:x["u"]]
+
+    def _segments(self, x):
+        m, me, W = x["mat"], self.rank, self.world
+        seg = torch.tensor(np.concatenate([[0], np.cumsum(x["rc"])]), dtype=torch.int64, device=self.device)
+        off = torch.tensor([sum(m[r][:me]) for r in range(W)], dtype=torch.int64, device=self.device)
+        return seg, off
+
+    def grads_from_peers(self, router, x, grad_out, offsets, n_bags, include_last_offset, psw, mode):
+        """Requester: per-routed-id gradients into the shared gbuf; barrier; owner: pull the
+        rows of its received ids from every requester's gbuf over peer memory."""
+        ct = self._ct
+        if x["u"] > self.max_rows:
+            raise RuntimeError(f"PeerRows buffer holds {self.max_rows} rows, batch routes {x['u']}")
+        router.grads(x["inv"], x["u"], grad_out, offsets, n_bags, include_last_offset, psw, mode,
+                     out=self.gbuf[:x["u"]])
+        dist.all_reduce(self.flag, group=self.group)  # every requester's gradients are in place
+        seg, off = self._segments(x)
+        n = int(sum(x["rc"]))
+        g_recv = torch.empty((n, self.dim), dtype=torch.float32, device=self.device)
+        stream = ct.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        self._check(self.lib.fc_gather_from_peers(ct.c_void_p(self.gsrc.data_ptr()), ct.c_void_p(off.data_ptr()),
+                                                  ct.c_void_p(seg.data_ptr()), self.world, n, self.dim,
+                                                  ct.c_void_p(g_recv.data_ptr()), stream))
+        return g_recv
 
 
 # ----------------------------------------------------------------------------- row-wise (scaling)
@@ -386,6 +418,11 @@ class RowShardedEmbedding(torch.nn.Module):
 
     def _backward(self, saved, grad_out):
         h, x, n, offsets, n_bags, psw = saved
+        if self.peer is not None:  # gradients travel back over peer memory as well
+            g_recv = self.peer.grads_from_peers(self.router, x, grad_out, offsets, n_bags, self.include_last_offset,
+                                                psw, self.mode)
+            self.shard.backward(h, g_recv)
+            return
         if self.router is not None:  # one deterministic gradient row per routed id, in routing order
             g_send = self.router.grads(x["inv"], x["u"], grad_out, offsets, n_bags, self.include_last_offset, psw,
                                        self.mode)

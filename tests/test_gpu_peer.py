@@ -136,3 +136,20 @@ def test_row_sharded_peer_rows_nccl_world1_matches_dense():
     got[idx.id_of] = rows
     np.testing.assert_allclose(got, dense.weight.detach().numpy(), rtol=1e-5, atol=5e-6)
     dist.destroy_process_group()
+
+
+def test_gather_from_peers_addressing():
+    D, W = 16, 3
+    seg = np.array([0, 40, 40, 100], dtype=np.int64)   # requester 1 sends nothing
+    off = np.array([5, 0, 12], dtype=np.int64)
+    srcs = [torch.randn((off[r] + seg[r + 1] - seg[r] + 3, D), device="cuda") for r in range(W)]
+    ptrs = torch.tensor([t.data_ptr() for t in srcs], dtype=torch.int64, device="cuda")
+    out = torch.empty((100, D), device="cuda")
+    st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    off_d, seg_d = torch.from_numpy(off).cuda(), torch.from_numpy(seg).cuda()  # kept alive across the launch
+    rc = lib.fc_gather_from_peers(ctypes.c_void_p(ptrs.data_ptr()), ctypes.c_void_p(off_d.data_ptr()),
+                                  ctypes.c_void_p(seg_d.data_ptr()), W, 100, D, ctypes.c_void_p(out.data_ptr()), st)
+    assert rc == _lib.OK
+    torch.cuda.synchronize()
+    want = torch.cat([srcs[r][off[r]:off[r] + seg[r + 1] - seg[r]] for r in range(W)])
+    assert torch.equal(out, want)
