@@ -409,6 +409,11 @@ static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* i
     set_error("backward needs dim %% 4 == 0 and 16-byte aligned gradient rows");
     return FC_ERR_BAD_ARG;
   }
+  if ((size_t)kFixWarps * (D / 4) * sizeof(float4) > 220 * 1024) {
+    set_error("backward supports rows up to %d floats (the carry fix-up's shared memory)",
+              (int)(220 * 1024 / (kFixWarps * sizeof(float4)) * 4));
+    return FC_ERR_BAD_ARG;
+  }
   const int64_t nchunks = (n + kChunk - 1) / kChunk;
   const bool bags = offsets != nullptr;
   const size_t extra = (gu_out || apply ? 0 : align16((size_t)u * D * 4)) + align16(nchunks * 2 * (size_t)D * 4) +

@@ -501,10 +501,11 @@ int engine_evict(fc_cache* h, cudaStream_t st) {
 }
 
 static int launch_admit_async_tma(fc_cache* h, const EngArgs& x, cudaStream_t st);  // below, with the TMA helpers
+static bool tma_fits(const fc_cache* h);
 
 int engine_admit(fc_cache* h, cudaStream_t st) {
   EngArgs x = eng_args(h);
-  if (h->awb->vec && !std::getenv("FC_NO_TMA")) return launch_admit_async_tma(h, x, st);
+  if (h->awb->vec && tma_fits(h) && !std::getenv("FC_NO_TMA")) return launch_admit_async_tma(h, x, st);
   if (h->awb->vec) k_admit_async<true><<<kSMs * 4, kNT, 0, st>>>(x);
   else k_admit_async<false><<<kSMs * 4, kNT, 0, st>>>(x);
   FC_CUDA(cudaGetLastError());
@@ -606,6 +607,11 @@ constexpr int kTmaStages = 4;  // k_admit_stage_tma: row groups in flight per bl
 constexpr int kTmaBlocks = 64;
 // rows per TMA group so that one stage holds <= 32 KB
 static inline int tma_group_rows(int row_bytes) { return std::max(1, std::min(32, 32768 / row_bytes)); }
+// the TMA ring must fit in shared memory (rows wider than ~12K floats use the SM kernels)
+static bool tma_fits(const fc_cache* h) {
+  const size_t rb = (size_t)(h->dim + h->sw) * 4;
+  return (size_t)kTmaStages * tma_group_rows((int)rb) * rb <= 200 * 1024;
+}
 
 struct Pipe {
   IndexBufs ib[2];
@@ -714,7 +720,7 @@ static int pipe_create(fc_cache* h) {
   if (const char* env = std::getenv("FC_XFER_AFTER_UPDATE")) q->defer_xfer = std::atoi(env) != 0;
   // TMA staging needs 16-byte rows at 16-byte aligned addresses (the async engine's vec
   // condition); FC_XFER_TMA=0 selects the SM-load kernel
-  q->tma = h->awb && h->awb->vec;
+  q->tma = h->awb && h->awb->vec && tma_fits(h);
   if (const char* env = std::getenv("FC_XFER_TMA")) q->tma = q->tma && std::atoi(env) != 0;
   if (const char* env = std::getenv("FC_TMA_BLOCKS")) q->tma_blocks = std::max(1, std::atoi(env));
 
