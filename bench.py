@@ -68,6 +68,12 @@ KERNELS_PER_TRAIN_STEP = 17 + 1 + 5
 # prefetch pipeline: + k_evict_state, k_admit_state, k_publish (index phase) and
 # k_admit_stage / k_evict_commit / k_admit_commit instead of k_evict_async / k_admit_async
 PIPELINE_EXTRA_KERNELS = 3 + 1
+# row-sharded training step (profiles/r01_launches_sharded*): fc_route 6 (k_begin, k_route_mark,
+# count + emit, k_route_inverse, k_route_finish) + the owner's pipelined prepare 17 + 4 + the
+# requester's gradient reduction 5 + the owner's apply (k_bwd_direct when every received id is
+# distinct, always at world 1; else the 5-kernel grouped backward) + row return (peer memory:
+# k_pool_to_peers + k_gather_from_peers; NCCL: the owner's k_pool1) + the requester's k_pool1
+SHARDED_BASE_KERNELS = 6 + 17 + 5 + 1  # + PIPELINE_EXTRA_KERNELS when prefetching
 # miss staging / admission through the TMA bulk-copy engine (row width a multiple of 16 B;
 # FC_XFER_TMA=0 / FC_NO_TMA=1 select the SM-load kernels)
 TMA = os.environ.get("FC_XFER_TMA", "1") != "0" and not os.environ.get("FC_NO_TMA")
@@ -359,6 +365,8 @@ def run_ours(args, cfg, torch, rank, world):
     log(f"[bench] rank {rank}: slow tier {rows.nbytes / 2**30:.1f} GiB pinned+filled, cache ready in "
         f"{time.perf_counter() - t0:.1f}s")
     ids_dev = torch.from_numpy(samples).to(dev)
+    ids_ready = torch.cuda.Event()  # the whole trace is resident before the first step
+    ids_ready.record(torch.cuda.current_stream(dev))
     out_buf = torch.empty((N, D), dtype=torch.float32, device=dev)
     colw = torch.from_numpy(fc.update_column_weights(D, UPDATES_SEED)).to(dev)
     stream = torch.cuda.current_stream(dev)
@@ -372,7 +380,7 @@ def run_ours(args, cfg, torch, rank, world):
         if sharded:  # row-sharded training step: unique-id all-to-all, owner caches, row all-to-all
             out = mod(ids, None, psw)
             if pipelined:  # next batch's id exchange + owner prepare overlap this backward
-                mod.prefetch(bview[s + 1])
+                mod.prefetch(bview[s + 1], ready=ids_ready)
             out.backward(gout)
             stats.append((0, 0, 0, 0, 0))
             return
@@ -387,7 +395,7 @@ def run_ours(args, cfg, torch, rank, world):
         if timed:
             e[1].record(stream)
         if pipelined:  # batch s+1's index phase + miss staging overlap this batch's backward
-            dc.prepare_begin(bview[s + 1], s + 1)
+            dc.prepare_begin(bview[s + 1], s + 1, ready=ids_ready)
         if args.step == "train":
             dc.backward_update(uslots, inverse, ucnt, None, N, False, psw, MODE, gout, OPT, LR, 1e-10)
         else:
@@ -399,7 +407,7 @@ def run_ours(args, cfg, torch, rank, world):
 
     pipelined = args.engine == "async" and not args.no_prefetch
     if pipelined and not sharded:
-        dc.prepare_begin(bview[0], 0)
+        dc.prepare_begin(bview[0], 0, ready=ids_ready)
     for s in range(W):
         step(s, False)
     torch.cuda.synchronize(dev)
@@ -426,6 +434,13 @@ def run_ours(args, cfg, torch, rank, world):
         step(W + K + k, True)
     torch.cuda.synchronize(dev)
     prof = dc.profile(False)
+    if os.environ.get("FC_TORCH_TRACE"):  # diagnostic: a CUPTI timeline of a few steps (tools/trace_gaps.py)
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as tp:
+            for k in range(4):
+                step(W + K + KSTEPS + k, False)
+            torch.cuda.synchronize(dev)
+        tp.export_chrome_trace(os.environ["FC_TORCH_TRACE"])
     # ---- the same kernels isolated: KSTEPS synchronous steps (no prefetch overlap), so the
     # roofline of each kernel is also reported without the host-link interference
     prof_iso, p_ms_iso = None, []
@@ -442,7 +457,7 @@ def run_ours(args, cfg, torch, rank, world):
         p_ms_iso = [e[0].elapsed_time(e[1]) for e in pool_ms[n_contended:]]
         del pool_ms[n_contended:]
         del stats[-KSTEPS:]
-        dc.prepare_begin(bview[W + K + 2 * KSTEPS], W + K + 2 * KSTEPS)
+        dc.prepare_begin(bview[W + K + 2 * KSTEPS], W + K + 2 * KSTEPS, ready=ids_ready)
     step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(K)]
     total_ms = ev[0].elapsed_time(ev[K])
     if world > 1:
@@ -549,8 +564,9 @@ def run_ours(args, cfg, torch, rank, world):
                 "path": "CachedEmbeddingBag.forward(pinned host ids) + out.backward(grad) (fused SGD); result = "
                         "prepare hit/miss counters read back" if not sharded
                 else "RowShardedEmbedding.forward(pinned host ids) + out.backward(grad)"},
-        "gpu_launches": ((KERNELS_PER_STEP if args.step == "sim" else KERNELS_PER_TRAIN_STEP)
-                         + (PIPELINE_EXTRA_KERNELS if pipelined else 0)) * K,
+        "gpu_launches": (((KERNELS_PER_STEP if args.step == "sim" else KERNELS_PER_TRAIN_STEP)
+                          + (PIPELINE_EXTRA_KERNELS if pipelined else 0)) if not sharded else
+                         (SHARDED_BASE_KERNELS + (PIPELINE_EXTRA_KERNELS if pipelined else 0) + (1 if world == 1 else 5) + (1 if args.no_peer else 2))) * K,
         "roofline": rl[0], "roofline_secondary": rl[1] if len(rl) > 1 else None,
         "roofline_isolated": ({"note": "same kernels in synchronous steps (no prefetch overlap), after the "
                                        "timed region", **{r["kernel"]: r for r in rl_iso}} if rl_iso else None),

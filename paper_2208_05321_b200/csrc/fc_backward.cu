@@ -398,6 +398,47 @@ __global__ void __launch_bounds__(kNT) k_bwd_apply(BwdArgs x, int64_t u) {
   }
 }
 
+// Every unique row has exactly one gradient row (u == n, no bags, no weights: the
+// row-sharded owner receiving one row per distinct id): `inverse` is a permutation,
+// so no grouping is needed -- occurrence i updates slot uslots[inv[i]] directly with
+// the same arithmetic as a one-element run of k_bwd_stream.
+__global__ void __launch_bounds__(kNT) k_bwd_direct(BwdArgs x, const int32_t* __restrict__ inv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
+  const int total = 32 * x.un.upr;
+  for (int64_t base = warp * 32; base < x.n; base += nwarps * 32) {
+    const int64_t i = base + lane;
+    const bool act = i < x.n;
+    const int s = act ? x.uslots[inv[i]] : 0;
+    for (int u0 = 0; u0 < total; u0 += 32 * kBwdUnroll) {
+      float4 g[kBwdUnroll];
+      float* w[kBwdUnroll];
+      bool aa[kBwdUnroll];
+#pragma unroll
+      for (int k = 0; k < kBwdUnroll; ++k) {
+        const int q = u0 + k * 32 + lane;
+        const int r = min(x.un.row(q), 31);
+        const int c = (q - r * x.un.upr) * 4;
+        const int sr = __shfl_sync(FC_FULL, s, r);
+        aa[k] = __shfl_sync(FC_FULL, (int)act, r) && q < total;
+        w[k] = x.fast + (int64_t)sr * x.D + c;
+        if (aa[k]) {
+          const float4 v = ld4(x.grad + (base + r) * x.D + c);
+          g[k] = make_float4(0.f + v.x, 0.f + v.y, 0.f + v.z, 0.f + v.w);  // a run's sum starts at 0
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kBwdUnroll; ++k)
+        if (aa[k]) {
+          float* stp = x.fstate ? x.fstate + (w[k] - x.fast) : nullptr;
+          apply_unit(w[k], stp, g[k], x.o);
+        }
+    }
+    if (act) x.dirty[s] = 1;
+  }
+}
+
 // Per-unique gradient of the pooled forward: group the occurrences by unique row
 // (stable radix sort of `inverse`), stream the sorted occurrences accumulating
 // coef_j * grad_out[bag(j)], fix up the runs cut by chunk edges. Leaves x ready for
@@ -494,6 +535,20 @@ int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, cons
   x.dirty = h->dirty;
   x.o = OptArgs{optim, lr, eps};
   static const bool fused = !std::getenv("FC_BWD_UNFUSED");
+  static const bool direct_ok = !std::getenv("FC_BWD_NO_DIRECT");
+  if (direct_ok && u == n && !offsets && !psw) {  // one gradient row per unique row: no grouping
+    if (D % 4 || (reinterpret_cast<uintptr_t>(grad) & 15)) {
+      set_error("backward needs dim %% 4 == 0 and 16-byte aligned gradient rows");
+      return FC_ERR_BAD_ARG;
+    }
+    x.D = D;
+    x.n = n;
+    x.grad = grad;
+    x.un = units_for(D);
+    k_bwd_direct<<<grid_for(n, kNT, kSMs * 8), kNT, 0, st>>>(x, inv);
+    FC_CUDA(cudaGetLastError());
+    return FC_OK;
+  }
   int rc = segment_grads(&h->scratch, &h->scratch_bytes, inv, u, n, offsets, off_bytes, nbags, include_last, psw, mode,
                          grad, D, nullptr, x, fused, st);
   if (rc || fused) return rc;

@@ -599,17 +599,27 @@ int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, i
 template <typename IdT>
 __global__ void __launch_bounds__(kNT) k_route_mark(const IdT* __restrict__ ids, int64_t n, int64_t num_ids, int W,
                                                     int64_t S, uint32_t* bits, Counters* c) {
-  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
-    const long long id = (long long)ids[i];
-    if (id < 0 || id >= num_ids) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t w = (uint32_t)W, s32 = (uint32_t)S;  // key space < 2^31 (checked at create)
+  for (int64_t base = (int64_t)blockIdx.x * kNT; base < n; base += (int64_t)gridDim.x * kNT) {
+    const int64_t i = base + threadIdx.x;
+    const bool valid = i < n;
+    const long long id = valid ? (long long)ids[i] : 0;
+    const bool inr = valid && id >= 0 && id < num_ids;
+    if (valid && !inr) {
       if (id < 0) atomicMin(&c->lo, id);
       else atomicMax(&c->hi, id);
-      continue;
     }
-    const int64_t key = (id % W) * S + id / W;
-    const uint32_t m = 1u << (key & 31);
-    uint32_t* wp = &bits[key >> 5];
-    if (!(*wp & m)) atomicOr(wp, m);
+    const uint32_t u = (uint32_t)id;
+    const int key = inr ? (int)((u % w) * s32 + u / w) : -1;
+    // one leader per distinct key of the warp; a read before the atomic skips the
+    // bits already set (Zipf batches repeat head ids a lot)
+    const unsigned peers = __match_any_sync(FC_FULL, key);
+    if (inr && lane == __ffs(peers) - 1) {
+      const uint32_t m = 1u << (key & 31);
+      uint32_t* wp = &bits[key >> 5];
+      if (!(*wp & m)) atomicOr(wp, m);
+    }
   }
 }
 
@@ -645,34 +655,35 @@ __global__ void __launch_bounds__(kNT) k_route_inverse(const IdT* __restrict__ i
                                                        const int32_t* __restrict__ aux, int32_t* __restrict__ inv,
                                                        const Counters* c) {
   if (!c->emitted) return;
+  const uint32_t w = (uint32_t)W, s32 = (uint32_t)S;
   for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
-    const long long id = (long long)ids[i];
-    inv[i] = aux[(id % W) * S + id / W];
+    const uint32_t u = (uint32_t)ids[i];
+    inv[i] = aux[(u % w) * s32 + u / w];
   }
 }
 
-// per-owner counts: owner o's ids are the keys in [o*S, (o+1)*S) of the sorted unique list
-__global__ void k_route_counts(const int32_t* __restrict__ ukeys, int64_t S, int W, const Counters* c,
-                               long long* owner_cnt) {
-  const int o = threadIdx.x;
-  if (o > W) return;
+// clears the key->position map for the next call; block 0 also writes the per-owner
+// counts: owner o's ids are the keys in [o*S, (o+1)*S) of the sorted unique list
+__global__ void __launch_bounds__(kNT) k_route_finish(const int32_t* __restrict__ ukeys, int32_t* aux, int64_t S, int W,
+                                                      const Counters* c, long long* owner_cnt) {
   const int u = c->emitted ? c->unique : 0;
-  const long long target = (long long)o * S;
-  int lo = 0, hi = u;  // first position with key >= o*S
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if ((long long)ukeys[mid] < target) lo = mid + 1;
-    else hi = mid;
+  if (blockIdx.x == 0) {
+    __shared__ int start[65];
+    const int o = threadIdx.x;
+    if (o <= W) {
+      const long long target = (long long)o * S;
+      int lo = 0, hi = u;  // first position with key >= o*S
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if ((long long)ukeys[mid] < target) lo = mid + 1;
+        else hi = mid;
+      }
+      start[o] = (o == W) ? u : lo;
+    }
+    __syncthreads();
+    if (o < W) owner_cnt[o] = start[o + 1] - start[o];
   }
-  __shared__ int start[65];
-  start[o] = (o == W) ? u : lo;
-  __syncthreads();
-  if (o < W) owner_cnt[o] = start[o + 1] - start[o];
-}
-
-__global__ void __launch_bounds__(kNT) k_route_finish(const int32_t* __restrict__ ukeys, int32_t* aux, const Counters* c) {
-  if (!c->emitted) return;
-  for (int p = blockIdx.x * kNT + threadIdx.x; p < c->unique; p += gridDim.x * kNT) aux[ukeys[p]] = 0;
+  for (int p = blockIdx.x * kNT + threadIdx.x; p < u; p += gridDim.x * kNT) aux[ukeys[p]] = 0;
 }
 
 }  // namespace fc
@@ -786,8 +797,7 @@ extern "C" int fc_route(fc_router* r, const void* ids, int32_t ids_bytes, int64_
           c, G_ALWAYS, st);
   if (ids_bytes == 8) k_route_inverse<long long><<<g, kNT, 0, st>>>((const long long*)ids, n, r->world, r->S, r->aux, inverse, c);
   else k_route_inverse<int><<<g, kNT, 0, st>>>((const int*)ids, n, r->world, r->S, r->aux, inverse, c);
-  k_route_counts<<<1, 65, 0, st>>>(r->ukeys, r->S, r->world, c, r->owner_cnt);
-  k_route_finish<<<grid_for(n, kNT, kSMs * 4), kNT, 0, st>>>(r->ukeys, r->aux, c);
+  k_route_finish<<<grid_for(n, kNT, kSMs * 4), kNT, 0, st>>>(r->ukeys, r->aux, r->S, r->world, c, r->owner_cnt);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpyAsync(r->ctr_host, c, sizeof(Counters), cudaMemcpyDeviceToHost, st);
   if (e == cudaSuccess)

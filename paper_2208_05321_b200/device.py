@@ -190,12 +190,18 @@ class DeviceCache:
     def prefetch_outstanding(self) -> bool:
         return getattr(self, "_pf", None) is not None
 
-    def prepare_begin(self, ids, batch_seq: int = 0, index_on_main: bool | None = None):
+    def prepare_begin(self, ids, batch_seq: int = 0, index_on_main: bool | None = None, ready=None):
         """Launch the next batch's prepare ahead of time (fc_prepare_begin): the index
         phase runs on this cache's index stream and the admitted rows are staged
         host -> HBM on the library's transfer stream, both overlapping whatever the
         current stream is still running (the previous batch's forward/backward).
-        The result is claimed with prepare_commit()."""
+        The result is claimed with prepare_commit().
+
+        Host ids are copied on the index stream. Device ids are read there once the
+        work queued so far on the current stream is done (they may be its output),
+        or, when `ready` (a torch.cuda.Event) is given, once that event has fired --
+        pass it for ids that were complete earlier, so the index phase does not wait
+        for this batch's queued forward."""
         torch = self.torch
         if self.prefetch_outstanding:
             raise RuntimeError("a prefetched prepare is outstanding: commit it first")
@@ -207,6 +213,11 @@ class DeviceCache:
         if index_on_main is None:
             index_on_main = self.index_on_main
         idx = main if index_on_main else self.index_stream
+        if idx is not main and isinstance(ids, torch.Tensor) and ids.is_cuda:
+            if ready is None:
+                idx.wait_stream(main)
+            else:
+                idx.wait_event(ready)
         slot = self._ring_slot(ids) if self.prefetch_ring else None
         if slot is not None:
             # a ring of PF_RING buffer sets owned by this cache: no per-step allocation (a

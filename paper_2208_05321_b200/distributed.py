@@ -151,6 +151,15 @@ class Router:
 
 
 # ----------------------------------------------------------------------------- helpers
+def _upload(vals, device):
+    """A small host list as an int64 device tensor without a host sync (a pageable
+    torch.tensor(..., device=cuda) blocks until the stream drains)."""
+    t = torch.tensor(vals, dtype=torch.int64)
+    if device.type != "cuda":
+        return t
+    return t.pin_memory().to(device, non_blocking=True)
+
+
 def _a2a(out, inp, out_splits, in_splits, group=None):
     dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
     return out
@@ -262,22 +271,29 @@ class PeerRows:
         m, me, W = x["mat"], self.rank, self.world
         if x["u"] > self.max_rows:
             raise RuntimeError(f"PeerRows buffer holds {self.max_rows} rows, batch routes {x['u']}")
-        seg = torch.tensor(np.concatenate([[0], np.cumsum(x["rc"])]), dtype=torch.int64, device=self.device)
-        # my segment in requester r's routing order starts after the ids r sends to owners < me
-        off = torch.tensor([sum(m[r][:me]) for r in range(W)], dtype=torch.int64, device=self.device)
+        seg, off = self._segments(x)
         stream = ct.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         self._check(self.lib.fc_pool_to_peers(shard.cache.h, ct.c_void_p(h["uslots"].data_ptr()),
                                               ct.c_void_p(h["inverse"].data_ptr()), int(h["n"]),
                                               ct.c_void_p(seg.data_ptr()), W, ct.c_void_p(self.dst.data_ptr()),
                                               ct.c_void_p(off.data_ptr()), stream))
-        dist.all_reduce(self.flag, group=self.group)  # every owner's writes land before anyone reads
+        if W > 1:  # every owner's writes land before anyone reads (one rank: stream order suffices)
+            dist.all_reduce(self.flag, group=self.group)
         return self.rbuf[:x["u"]]
 
-    def _segments(self, x):
+    def segments(self, x):
+        """Device arrays for the peer kernels, built once per exchange (uploaded without
+        a host sync): seg = prefix sums of what I receive from each requester; off[r] =
+        where my segment starts in requester r's routing order (after the ids r sends to
+        owners < me)."""
         m, me, W = x["mat"], self.rank, self.world
-        seg = torch.tensor(np.concatenate([[0], np.cumsum(x["rc"])]), dtype=torch.int64, device=self.device)
-        off = torch.tensor([sum(m[r][:me]) for r in range(W)], dtype=torch.int64, device=self.device)
-        return seg, off
+        x["seg"] = _upload([0] + np.cumsum(x["rc"]).tolist(), self.device)
+        x["off"] = _upload([sum(m[r][:me]) for r in range(W)], self.device)
+
+    def _segments(self, x):
+        if "seg" not in x:
+            self.segments(x)
+        return x["seg"], x["off"]
 
     def grads_from_peers(self, router, x, grad_out, offsets, n_bags, include_last_offset, psw, mode):
         """Requester: per-routed-id gradients into the shared gbuf; barrier; owner: pull the
@@ -287,7 +303,8 @@ class PeerRows:
             raise RuntimeError(f"PeerRows buffer holds {self.max_rows} rows, batch routes {x['u']}")
         router.grads(x["inv"], x["u"], grad_out, offsets, n_bags, include_last_offset, psw, mode,
                      out=self.gbuf[:x["u"]])
-        dist.all_reduce(self.flag, group=self.group)  # every requester's gradients are in place
+        if self.world > 1:  # every requester's gradients are in place
+            dist.all_reduce(self.flag, group=self.group)
         seg, off = self._segments(x)
         n = int(sum(x["rc"]))
         g_recv = torch.empty((n, self.dim), dtype=torch.float32, device=self.device)
@@ -351,19 +368,28 @@ class RowShardedEmbedding(torch.nn.Module):
         """Unique ids of this rank's batch to their owners; returns the routing."""
         W = self.world
         if self.router is not None:  # grouped by owner already: no permutation to undo
-            send_ids, inv, sc = self.router.route(ids)
+            send_ids, inv, sc = self.router.route(ids)  # (waits for the routing kernels only)
             order = None
+            if W == 1:  # one rank owns everything: the exchanges are identities
+                m = [list(sc)]
+                x = {"inv": inv, "order": None, "sc": sc, "rc": list(sc), "recv_ids": send_ids,
+                     "u": int(send_ids.numel()), "mat": m}
+                if self.peer is not None:
+                    self.peer.segments(x)
+                return x
             if self.peer is not None:  # the full W x W count matrix: splits + peer-write offsets
-                mine = torch.tensor(sc, dtype=torch.int64, device=ids.device)
+                mine = _upload(sc, ids.device)
                 mat = torch.empty(W * W, dtype=torch.int64, device=ids.device)
                 dist.all_gather_into_tensor(mat, mine, group=self.group)
                 m = mat.view(W, W).tolist()  # m[r][o] = ids rank r sends to owner o
                 rc = [m[r][self.rank] for r in range(W)]
                 recv_ids = torch.empty(sum(rc), dtype=send_ids.dtype, device=send_ids.device)
                 _a2a(recv_ids, send_ids.contiguous(), rc, sc, self.group)
-                return {"inv": inv, "order": None, "sc": sc, "rc": rc, "recv_ids": recv_ids,
-                        "u": int(send_ids.numel()), "mat": m}
-            send_counts = torch.tensor(sc, dtype=torch.int64, device=ids.device)
+                x = {"inv": inv, "order": None, "sc": sc, "rc": rc, "recv_ids": recv_ids,
+                     "u": int(send_ids.numel()), "mat": m}
+                self.peer.segments(x)
+                return x
+            send_counts = _upload(sc, ids.device)
         else:
             uniq, inv = torch.unique(ids.long(), sorted=True, return_inverse=True)
             owner, local = self.owner_of(uniq, W)
@@ -378,13 +404,43 @@ class RowShardedEmbedding(torch.nn.Module):
         _a2a(recv_ids, send_ids.contiguous(), rc, sc, self.group)
         return {"inv": inv, "order": order, "sc": sc, "rc": rc, "recv_ids": recv_ids, "u": int(send_ids.numel())}
 
-    def prefetch(self, ids):
-        dev_ids = ids.reshape(-1).to(self.device)
-        x = self._exchange_ids(dev_ids)
-        if hasattr(self.shard, "prepare_begin") and x["recv_ids"].numel() > 0:
-            self.shard.prepare_begin(x["recv_ids"])
-            x["begun"] = True
-        x["src"] = ids
+    def prefetch(self, ids, ready=None):
+        """Next batch's id exchange + the owner's prepare_begin. On a GPU they run on a
+        high-priority side stream, so the routing's host sync waits for the routing
+        kernels only, not for this batch's queued forward/backward. Host `ids` are
+        copied there; device `ids` are read after the work queued on the current stream,
+        or after `ready` (a torch.cuda.Event) when given."""
+        if self.device.type != "cuda":
+            dev_ids = ids.reshape(-1).to(self.device)
+            x = self._exchange_ids(dev_ids)
+            if hasattr(self.shard, "prepare_begin") and x["recv_ids"].numel() > 0:
+                self.shard.prepare_begin(x["recv_ids"])
+                x["begun"] = True
+            x["src"] = ids
+            self._pf = (dev_ids, x)
+            return
+        main = torch.cuda.current_stream(self.device)
+        if getattr(self, "_xstream", None) is None:
+            self._xstream = torch.cuda.Stream(self.device, priority=-100)
+        xs = self._xstream
+        with torch.cuda.stream(xs):
+            if ids.is_cuda:
+                if ready is None:
+                    xs.wait_stream(main)
+                else:
+                    xs.wait_event(ready)
+            dev_ids = ids.reshape(-1).to(self.device, non_blocking=True)
+            x = self._exchange_ids(dev_ids)
+            if hasattr(self.shard, "prepare_begin") and x["recv_ids"].numel() > 0:
+                self.shard.prepare_begin(x["recv_ids"])  # its index stream waits for xs
+                x["begun"] = True
+            ev = torch.cuda.Event()
+            ev.record(xs)
+        for k in ("inv", "recv_ids", "seg", "off"):  # allocated on xs, consumed on main
+            if isinstance(x.get(k), torch.Tensor):
+                x[k].record_stream(main)
+        dev_ids.record_stream(main)
+        x["ev"], x["src"] = ev, ids
         self._pf = (dev_ids, x)
 
     def _forward(self, ids, offsets, n_bags, psw, src=None):
@@ -392,6 +448,8 @@ class RowShardedEmbedding(torch.nn.Module):
         if self._pf is not None:
             pids, px = self._pf
             self._pf = None
+            if px.get("ev") is not None:  # the side stream's exchange is ordered before anything below
+                torch.cuda.current_stream(self.device).wait_event(px["ev"])
             if px.get("begun"):
                 hp = self.shard.prepare_commit()  # the prefetched batch is executed first
             if px["src"] is src or pids is ids or (pids.numel() == ids.numel() and bool(torch.equal(pids, ids))):
@@ -406,8 +464,11 @@ class RowShardedEmbedding(torch.nn.Module):
             back = self.peer.pool_to_peers(self.shard, h, x)
         else:
             rows = self.shard.pool(h)  # [n_recv, D] one row per received (unique per requester) id
-            back = torch.empty((x["u"], rows.shape[1]), dtype=rows.dtype, device=rows.device)
-            _a2a(back, rows.contiguous(), x["sc"], x["rc"], self.group)
+            if self.world == 1:
+                back = rows
+            else:
+                back = torch.empty((x["u"], rows.shape[1]), dtype=rows.dtype, device=rows.device)
+                _a2a(back, rows.contiguous(), x["sc"], x["rc"], self.group)
         if self.router is not None:  # back is in routing order: pool straight through the inverse
             out = self.router.pool(back, x["inv"], offsets, n_bags, self.include_last_offset, psw, self.mode)
         else:
@@ -432,17 +493,25 @@ class RowShardedEmbedding(torch.nn.Module):
             gu.index_add_(0, x["inv"], g)  # one gradient row per unique id of this rank
             g_send = gu[x["order"]].contiguous()
         g = g_send
-        g_recv = torch.empty((sum(x["rc"]), g.shape[1]), dtype=g.dtype, device=g.device)
-        _a2a(g_recv, g_send, x["rc"], x["sc"], self.group)
+        if self.world == 1:
+            g_recv = g_send
+        else:
+            g_recv = torch.empty((sum(x["rc"]), g.shape[1]), dtype=g.dtype, device=g.device)
+            _a2a(g_recv, g_send, x["rc"], x["sc"], self.group)
         self.shard.backward(h, g_recv)
 
     def forward(self, ids, offsets=None, per_sample_weights=None):
         self._src = ids
-        ids = ids.reshape(-1).to(self.device)
+        if self._pf is not None and self._pf[1].get("src") is ids:
+            ids = self._pf[0]  # already on the device (prefetch copied it)
+        else:
+            ids = ids.reshape(-1).to(self.device, non_blocking=True)
         n_bags = ids.numel() if offsets is None else offsets.numel() - (1 if self.include_last_offset else 0)
         return _RowShardFn.apply(self._anchor, self, ids, offsets, n_bags, per_sample_weights)
 
     def flush(self) -> int:
+        if self._pf is not None and self._pf[1].get("ev") is not None:
+            torch.cuda.current_stream(self.device).wait_event(self._pf[1]["ev"])
         if self._pf is not None and self._pf[1].get("begun"):
             self.shard.prepare_commit()
         self._pf = None

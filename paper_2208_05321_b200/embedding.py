@@ -110,14 +110,16 @@ class CachedEmbeddingBag(torch.nn.Module):
         self._generation = 0
         self.last_info = None
 
-    def prefetch(self, indices) -> None:
+    def prefetch(self, indices, ready=None) -> None:
         """Start the cache work of the NEXT batch now (the paper's future-work prefetch,
         PAPER.md:490): its index phase runs on a side stream and its misses are staged
         host -> HBM on the transfer stream while this batch's backward still runs.
         Call it after forward(batch t) and before backward(t); the next forward with
         the same `indices` object commits it. Cache decisions, slot assignment and
-        write-backs are bit-identical to not prefetching."""
-        self.cache.prepare_begin(indices)
+        write-backs are bit-identical to not prefetching. Device `indices` are read
+        after the work queued on the current stream, or after `ready` (a
+        torch.cuda.Event) when given (DeviceCache.prepare_begin)."""
+        self.cache.prepare_begin(indices, ready=ready)
 
     def forward(self, indices, offsets=None, per_sample_weights=None):
         dev = self.cache.device

@@ -88,3 +88,35 @@ def test_row_sharded_module_nccl_world1_matches_dense():
     got[idx.id_of] = rows
     np.testing.assert_allclose(got, dense.weight.detach().numpy(), rtol=1e-5, atol=5e-6)
     dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("opt", ["sgd", "adagrad"])
+def test_owner_direct_apply_equals_grouped(opt):
+    """An owner's backward gets one gradient row per distinct id (u == n, no bags):
+    k_bwd_direct applies it without the radix grouping. Bitwise equal to the grouped
+    path (the same ids as one-element bags), for SGD and Adagrad, after flush."""
+    num_ids, dim, n = 20_000, 32, 5_000
+    rng = np.random.default_rng(9)
+    table = rng.uniform(-0.1, 0.1, (num_ids, dim)).astype(np.float32)
+    idx = shard_rows_for_rank(np.ones(num_ids, np.int64), 0, 1)
+    out = []
+    for bags in (False, True):
+        rows = pinned_empty((num_ids, dim))
+        rows[...] = table[idx.id_of]
+        shard = CudaShard(num_ids, dim, fast_capacity(num_ids, 0.5), rows, idx, optimizer=opt, lr=0.05, device="cuda")
+        r2 = np.random.default_rng(10)
+        for _ in range(3):
+            ids = torch.from_numpy(r2.choice(num_ids, n, replace=False)).cuda()
+            g = torch.from_numpy(r2.standard_normal((n, dim)).astype(np.float32)).cuda()
+            h = shard.prepare(ids)
+            assert int(h["ucnt"].numel()) == n
+            if bags:
+                shard.backward(h, g, torch.arange(n, device="cuda"), n)
+            else:
+                shard.backward(h, g)
+        shard.flush()
+        torch.cuda.synchronize()
+        out.append((rows.copy(), None if shard.state is None else shard.state.copy()))
+    assert np.array_equal(out[0][0], out[1][0])
+    if opt == "adagrad":
+        assert np.array_equal(out[0][1], out[1][1])
