@@ -307,3 +307,44 @@ def test_stress_shape_adagrad_through_module():
     np.testing.assert_allclose(m.optimizer_state()[touched], state[touched], rtol=1e-5, atol=1e-7)
     assert np.array_equal(m.weight()[:1000], np.where(np.isin(np.arange(1000), touched)[:, None],
                                                       m.weight()[:1000], w0[:1000]))
+
+
+def test_prefetch_device_ids_written_on_main_stream():
+    """prefetch() of device ids that the current stream is still producing: the index
+    phase (on its own stream) must read them only after they are written. The ids are
+    written behind a ~2 ms spin on the main stream; the outcome must equal prefetching
+    ids that were complete long before (ready event) and training without prefetch."""
+    rng = np.random.default_rng(8)
+    num_ids, dim, steps, B = 20_000, 32, 6, 3_000
+    p = 1.0 / np.arange(1, num_ids + 1) ** 1.1
+    trace = rng.permutation(num_ids)[rng.choice(num_ids, size=(steps, B), p=p / p.sum())]
+    w0 = rng.uniform(-0.1, 0.1, (num_ids, dim)).astype(np.float32)
+    idx = fc.build_reorder(fc.scan_frequencies(trace, num_ids))
+    grads = [torch.from_numpy(rng.standard_normal((B, dim)).astype(np.float32)).cuda() for _ in range(steps)]
+    src = torch.from_numpy(trace).cuda()
+
+    def train(kind):
+        m = CachedEmbeddingBag(num_ids, dim, 0.1, mode="sum", weight=w0, idx_map=idx, lr=0.05)
+        ready = torch.cuda.Event()
+        ready.record()
+        nxt = None
+        for s in range(steps):
+            cur = nxt if nxt is not None else src[s].clone()
+            out = m(cur)
+            nxt = None
+            if kind != "none" and s + 1 < steps:
+                if kind == "late":  # the next ids are still being written when prefetch is called
+                    nxt = torch.full_like(src[s + 1], -7)
+                    torch.cuda._sleep(4_000_000)
+                    nxt.copy_(src[s + 1])
+                    m.prefetch(nxt)
+                else:
+                    nxt = src[s + 1]
+                    m.prefetch(nxt, ready=ready)
+            out.backward(grads[s])
+        m.flush()
+        return m.weight().copy()
+
+    w_none = train("none")
+    assert np.array_equal(train("late"), w_none)
+    assert np.array_equal(train("ready"), w_none)
