@@ -226,9 +226,17 @@ class DeviceCache:
             # its previous batch's backward behind us (see prefetch_ring)
             buf, d_ids = slot
             n = int(ids.numel())
-            with torch.cuda.stream(idx):
-                d_ids = d_ids[:n]
-                d_ids.copy_(ids.reshape(-1), non_blocking=True)
+            if ids.is_cuda and ids.device == self.device and ids.is_contiguous():
+                # device ids are read in place (the ordering above makes them complete; the
+                # caller must not rewrite them before the commit): no copy on the critical
+                # path, where it would queue behind the write-back on the copy engines
+                d_ids = ids.reshape(-1)
+                if idx is not main:
+                    d_ids.record_stream(idx)
+            else:
+                with torch.cuda.stream(idx):
+                    d_ids = d_ids[:n]
+                    d_ids.copy_(ids.reshape(-1), non_blocking=True)
             k = min(n, self.capacity)
             buf = buf[:4 * k + n]
         else:
