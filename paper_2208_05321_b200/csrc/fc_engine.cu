@@ -23,6 +23,7 @@
 #include <emmintrin.h>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -607,6 +608,15 @@ constexpr int kTmaStages = 4;  // k_admit_stage_tma: row groups in flight per bl
 constexpr int kTmaBlocks = 64;
 // rows per TMA group so that one stage holds <= 32 KB
 static inline int tma_group_rows(int row_bytes) { return std::max(1, std::min(32, 32768 / row_bytes)); }
+// Staging blocks of the prefetch pipeline: enough bulk copies in flight to keep the host
+// link busy (~2.5 MB), and no more -- extra requests queued on the link raise the memory
+// latency of every kernel running beside the staging. Measured optima on
+// the B200/PCIe box: 40 blocks for 512 B rows (64 KB in flight per block), 64 for 256 B,
+// 32 for 1 KB rows (profiles/r01_tma_blocks_sweep.txt).
+static inline int tma_pipe_blocks(int row_bytes) {
+  const double per_block = (double)kTmaStages * tma_group_rows(row_bytes) * row_bytes;
+  return std::max(32, std::min(64, (int)std::lround(2.5 * 1024 * 1024 / per_block)));
+}
 // the TMA ring must fit in shared memory (rows wider than ~12K floats use the SM kernels)
 static bool tma_fits(const fc_cache* h) {
   const size_t rb = (size_t)(h->dim + h->sw) * 4;
@@ -722,6 +732,7 @@ static int pipe_create(fc_cache* h) {
   // condition); FC_XFER_TMA=0 selects the SM-load kernel
   q->tma = h->awb && h->awb->vec && tma_fits(h);
   if (const char* env = std::getenv("FC_XFER_TMA")) q->tma = q->tma && std::atoi(env) != 0;
+  q->tma_blocks = tma_pipe_blocks((h->dim + h->sw) * 4);
   if (const char* env = std::getenv("FC_TMA_BLOCKS")) q->tma_blocks = std::max(1, std::atoi(env));
 
   q->xfer_blocks = kSMs;
