@@ -8,7 +8,11 @@
 //   ZS Z with its blocks limited (grid 148 / 32)
 //   DH cudaMemcpyAsync H2D contiguous 34.5 MB;  DD cudaMemcpyAsync D2H 34.5 MB
 //   BA cudaMemcpyBatchAsync of 67k random 512 B host rows -> HBM (copy engine gather)
+// `ib chain`: a dependent chain of 17 small kernels (the shape of the prepare's index
+// phase) alone and beside the TMA staging T(40) / zero-copy Z / copy-engine DH -- is the
+// cost per kernel or per byte?
 #include <algorithm>
+#include <string>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
@@ -132,6 +136,20 @@ __global__ void tma_gather(const char* __restrict__ host, char* __restrict__ dev
   asm volatile("cp.async.bulk.wait_group 0;");
 }
 
+// one tiny step of a kernel chain: a few dependent loads + a store (like k_begin / k_plan)
+__global__ void tiny_step(int* c, int k) {
+  int v = c[k];
+  v = c[(v & 7) + 8];
+  c[k + 1] = v + 1;
+}
+// one wide step: every thread loads one id and sets a bit (like k_mark_ids / k_bits_count)
+__global__ void wide_step(const int* __restrict__ ids, unsigned* bits, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int v = ids[i];
+    if (!(bits[v >> 5] & (1u << (v & 31)))) atomicOr(&bits[v >> 5], 1u << (v & 31));
+  }
+}
+
 // latency-bound: two dependent random index loads, then a random 512 B row per warp
 __global__ void dep_gather(const int* __restrict__ a, const int* __restrict__ b, const float4* __restrict__ rows,
                            float4* __restrict__ out, int n, int nrows) {
@@ -157,7 +175,8 @@ struct Timer {
   }
 };
 
-int main() {
+int main(int argc, char** argv) {
+  const bool chain = argc > 1 && std::string(argv[1]) == "chain";
   const long nH = (1L << 30) / 16;  // 1 GiB of float4
   const int rows = 67438, upr = 32;  // 512 B rows
   const long table_rows = 33762577;
@@ -245,6 +264,45 @@ int main() {
     }
     printf("%-28s together %8.3f | %8.3f ms\n", name, b1, b2);
   };
+  if (chain) {
+    CK(cudaFuncSetAttribute(tma_gather<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 512));
+    int* cc;
+    CK(cudaMalloc(&cc, 4096));
+    CK(cudaMemset(cc, 0, 4096));
+    const int nid = 425984;
+    int* ids;
+    unsigned* bits;
+    CK(cudaMalloc(&ids, nid * 4));
+    CK(cudaMalloc(&bits, (33762577 / 32 + 1) * 4));
+    {
+      std::vector<int> h(nid);
+      for (int i = 0; i < nid; ++i) h[i] = (int)(g() % 33762577);
+      CK(cudaMemcpy(ids, h.data(), nid * 4, cudaMemcpyHostToDevice));
+    }
+    auto E = [=](cudaStream_t s) {
+      for (int k = 0; k < 17; ++k) tiny_step<<<1, 32, 0, s>>>(cc, k);
+    };
+    auto W = [=](cudaStream_t s) {
+      for (int k = 0; k < 17; ++k) wide_step<<<148 * 8, 256, 0, s>>>(ids, bits, nid);
+    };
+    auto T40 = [=](cudaStream_t s) {
+      tma_gather<4><<<40, 32, 4 * 32 * 512, s>>>((const char*)hostd, (char*)zdst, didx, rows);
+    };
+    auto T148 = [=](cudaStream_t s) {
+      tma_gather<4><<<148, 32, 4 * 32 * 512, s>>>((const char*)hostd, (char*)zdst, didx, rows);
+    };
+    alone("E 17 tiny kernels", E);
+    alone("W 17 wide kernels", W);
+    alone("T(40)", T40);
+    both("E + T(40)", E, T40);
+    both("W + T(40)", W, T40);
+    both("E + T(148)", E, T148);
+    both("E + Z(148)", E, [&](cudaStream_t s) { Z(s, 148); });
+    both("E + DH", E, DH);
+    both("E + DD", E, DD);
+    both("W + DH", W, DH);
+    return 0;
+  }
   const float tH = alone("H  hbm copy 2x1GiB", H);
   printf("   -> %.0f GB/s\n", 2.0 * nH * 16 / tH / 1e6);
   const float tZ = alone("Z  zc gather grid 148", [&](cudaStream_t s) { Z(s, 148); });
