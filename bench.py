@@ -518,6 +518,16 @@ def run_ours(args, cfg, torch, rank, world):
     ms1 = torch.cuda.memory_stats(dev)
     alloc_diag = {k: ms1.get(k, 0) - ms0.get(k, 0) for k in ("num_alloc_retries", "num_device_alloc", "num_device_free",
                                                              "num_sync_all_streams")}
+    if os.environ.get("FC_TORCH_TRACE_E2E"):  # diagnostic: CUPTI timeline of a few module-API steps
+        from torch.profiler import ProfilerActivity, profile
+        with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as tp:
+            for k in range(K, K + 4):
+                out = mod(hb[(e0 + k) % n_batches], None, psw)
+                if pipelined:
+                    mod.prefetch(hb[(e0 + k + 1) % n_batches])
+                out.backward(gout)
+            torch.cuda.synchronize(dev)
+        tp.export_chrome_trace(os.environ["FC_TORCH_TRACE_E2E"])
     if pipelined:
         mod.flush()  # commits the last prefetch
     if world > 1:
