@@ -384,6 +384,8 @@ def run_ours(args, cfg, torch, rank, world):
             out.backward(gout)
             stats.append((0, 0, 0, 0, 0))
             return
+        if pipelined and depth2:  # batch s+1 begun before batch s is committed: its index phase
+            dc.prepare_begin(bview[s + 1], s + 1, ready=ids_ready)  # starts when batch s's ends
         if pipelined:  # batch s was prefetched during step s-1: commit it
             info, uids, ucnt, uranks, uslots, inverse, _ = dc.prepare_commit()
         else:
@@ -394,7 +396,7 @@ def run_ours(args, cfg, torch, rank, world):
         dc.pooled(uslots, inverse, N, per_sample_weights=psw, mode=MODE, out=out_buf)
         if timed:
             e[1].record(stream)
-        if pipelined:  # batch s+1's index phase + miss staging overlap this batch's backward
+        if pipelined and not depth2:  # batch s+1's index phase + miss staging overlap this backward
             dc.prepare_begin(bview[s + 1], s + 1, ready=ids_ready)
         if args.step == "train":
             dc.backward_update(uslots, inverse, ucnt, None, N, False, psw, MODE, gout, OPT, LR, 1e-10)
@@ -406,6 +408,7 @@ def run_ours(args, cfg, torch, rank, world):
         stats.append((info.unique, info.hits, info.misses, info.evictions, info.rows_to_slow))
 
     pipelined = args.engine == "async" and not args.no_prefetch
+    depth2 = args.prefetch_depth == 2 and not sharded and not os.environ.get("FC_XFER_AFTER_UPDATE")
     if pipelined and not sharded:
         dc.prepare_begin(bview[0], 0, ready=ids_ready)
     for s in range(W):
@@ -477,13 +480,17 @@ def run_ours(args, cfg, torch, rank, world):
     # cudaMalloc lands inside the timed region)
     e0 = W + K + 2 * KSTEPS
     ew = e0 - W
-    out = mod(hb[ew], None, psw)
-    for k in range(1, W):  # batches e0-W .. e0-1
-        if pipelined:
-            mod.prefetch(hb[ew + k])
-        out.backward(gout)
+    d2 = pipelined and depth2
+    if d2:
+        mod.prefetch(hb[ew])
+    out = None
+    for k in range(W):  # batches e0-W .. e0-1
+        if d2:
+            mod.prefetch(hb[ew + k + 1])  # batch k+1 begun before batch k's forward commits k
         out = mod(hb[ew + k], None, psw)
-    out.backward(gout)
+        if pipelined and not d2:
+            mod.prefetch(hb[ew + k + 1])
+        out.backward(gout)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize(dev)
@@ -505,8 +512,10 @@ def run_ours(args, cfg, torch, rank, world):
     ms0 = torch.cuda.memory_stats(dev)
     for k in range(K):
         th = time.perf_counter()
+        if d2:
+            mod.prefetch(hb[e0 + k + 1])  # next batch's cache work, begun ahead of this forward's commit
         out = mod(hb[e0 + k], None, psw)  # H2D of the ids inside forward (or inside the previous step's prefetch)
-        if pipelined:
+        if pipelined and not d2:
             mod.prefetch(hb[e0 + k + 1])  # next batch's cache work overlaps this backward
         out.backward(gout)  # upstream gradient of the pooled output -> fused SGD on the cached rows
         if not sharded:
@@ -522,8 +531,10 @@ def run_ours(args, cfg, torch, rank, world):
         from torch.profiler import ProfilerActivity, profile
         with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as tp:
             for k in range(K, K + 4):
+                if d2:
+                    mod.prefetch(hb[(e0 + k + 1) % n_batches])
                 out = mod(hb[(e0 + k) % n_batches], None, psw)
-                if pipelined:
+                if pipelined and not d2:
                     mod.prefetch(hb[(e0 + k + 1) % n_batches])
                 out.backward(gout)
             torch.cuda.synchronize(dev)
@@ -621,6 +632,8 @@ def main():
     ap.add_argument("--trace-batches", type=int, default=64)
     ap.add_argument("--cpu-baseline-steps", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--prefetch-depth", type=int, default=2, choices=[1, 2],
+                    help="2: batch t+1's prefetch is begun before batch t is committed (default)")
     ap.add_argument("--sharded", action="store_true", help="row-sharded module even at one GPU (needs torchrun)")
     ap.add_argument("--no-peer", action="store_true",
                     help="row-sharded runs: return rows with NCCL all-to-all instead of peer-memory writes")

@@ -98,7 +98,8 @@ int fc_set_idx_map(fc_cache* h, const int64_t* rank_of_host, void* stream);
 int fc_attach_slow_tier(fc_cache* h, float* rows_host, int64_t row_stride,
                         float* state_host, int64_t state_stride);
 
-/* Per-call modes of prepare_cache (write_back, evict_mode kwargs, cache_manager.py:241-245). */
+/* Per-call modes of prepare_cache (write_back, evict_mode kwargs, cache_manager.py:241-245).
+ * Changing them while a prefetch is outstanding is refused; re-setting the same modes is not. */
 int fc_set_modes(fc_cache* h, int32_t write_back, int32_t evict_mode);
 /* CacheState.free_count after the last synchronising call. */
 int64_t fc_free_count(fc_cache* h);
@@ -157,7 +158,10 @@ int fc_prepare(fc_cache* h, const void* ids_dev, int32_t ids_bytes, int64_t n, i
  * runs on device) and reports validation errors (nothing is mutated on error).
  * The resulting cache state, slot assignment and write-backs are bit-identical to
  * calling fc_prepare at commit time. Requires the async engine (fc_set_engine 1).
- * At most one begin may be outstanding; the synchronous verbs refuse while one is. */
+ * Up to two begins may be outstanding (commits are FIFO): fc_prepare_begin(t+1)
+ * before fc_prepare_commit(t) lets batch t+1's index phase start on the device as
+ * soon as batch t's ends (its staging is then launched by commit(t); not with
+ * FC_XFER_AFTER_UPDATE). The synchronous verbs refuse while any is outstanding. */
 int fc_prepare_begin(fc_cache* h, const void* ids_dev, int32_t ids_bytes, int64_t n, int64_t batch_seq,
                      int32_t* unique_ids, int32_t* unique_counts, int32_t* unique_ranks, int32_t* unique_slots,
                      int32_t* inverse, void* stream);

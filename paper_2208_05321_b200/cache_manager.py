@@ -294,6 +294,8 @@ def prepare_cache(state: CacheState, idx_map: IdxMap, ids, transmitter: Transmit
         if dev.committed_matches(ids):
             return _prepare_result(dev, ids, res, transmitter, fast, policy, batch_seq, event_log,
                                    rows_to_slow=dev.last_writebacks())
+        while dev.prefetch_outstanding:  # every prefetched batch runs before `ids`
+            dev.prepare_commit()
     dev.set_modes(write_back, evict_mode)
     return _prepare_result(dev, ids, dev.prepare(ids, batch_seq), transmitter, fast, policy, batch_seq, event_log)
 

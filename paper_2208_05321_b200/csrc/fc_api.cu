@@ -261,6 +261,7 @@ int fc_set_modes(fc_cache* h, int32_t write_back, int32_t evict_mode) {
   if (!h || (write_back != FC_WB_DIRTY_ONLY && write_back != FC_WB_ALWAYS) ||
       (evict_mode != FC_EVICT_OCCUPANCY_AWARE && evict_mode != FC_EVICT_PAPER_LITERAL))
     return FC_ERR_BAD_ARG;
+  if (write_back == h->write_back && evict_mode == h->evict_mode) return FC_OK;  // no change: allowed any time
   FC_NO_OUTSTANDING(h);
   h->write_back = write_back;
   h->evict_mode = evict_mode;

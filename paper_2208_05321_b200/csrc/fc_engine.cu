@@ -637,8 +637,8 @@ struct Pipe {
   bool has_index[2] = {false, false};
   bool has_commit[2] = {false, false};
   bool timed[2] = {false, false};
-  int par = 0;
-  bool outstanding = false;
+  int par = 0;   // parity of the next prepare_begin
+  int nout = 0;  // begun and not yet committed (0..2); the oldest has parity par ^ (nout & 1)
   int xfer_blocks = kSMs;                  // k_admit_stage grid (one block per SM: enough loads in flight)
   bool defer_xfer = false;                 // launch the staging after the next row update (fc_backward_update)
   bool tma = false;                        // stage through the bulk-copy engine (k_admit_stage_tma)
@@ -654,7 +654,7 @@ struct Pipe {
     if (rc__) return rc__; \
   } while (0)
 
-bool pipe_outstanding(const fc_cache* h) { return h->pipe && h->pipe->outstanding; }
+bool pipe_outstanding(const fc_cache* h) { return h->pipe && h->pipe->nout > 0; }
 
 // Host wait for every recorded pipeline commit (their kernels have finished).
 int pipe_sync_commits(fc_cache* h) {
@@ -1105,8 +1105,14 @@ int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* 
     if (rc) return rc;
   }
   Pipe* q = h->pipe;
-  if (q->outstanding) {
-    set_error("a prefetched prepare is outstanding: commit it first");
+  // Depth 2: batch t+1 may be begun while batch t is still uncommitted -- its index phase
+  // only needs index(t) (state order) and commit(t-1) (this parity's buffers), so it can
+  // start on the device the moment index(t) ends instead of after the host has committed
+  // t. Its staging must still follow commit(t) (pending write-back marks) and is launched
+  // by that commit.
+  if (q->nout >= 2 || (q->nout == 1 && q->defer_xfer)) {
+    set_error(q->nout >= 2 ? "two prefetched prepares are outstanding: commit one first"
+                           : "a prefetched prepare is outstanding: commit it first");
     return FC_ERR_BAD_ARG;
   }
   const int p = q->par;
@@ -1122,11 +1128,12 @@ int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* 
   trace_mark(h, T_INDEX_END, st);
   FC_CUDA(cudaEventRecord(q->ev_index[p], st));
   q->has_index[p] = true;
-  q->outstanding = true;
+  const bool behind_commit = q->nout == 1;  // commit(t) not launched yet: it launches this staging
+  q->nout += 1;
   q->par = o;
   q->xfer_pending = true;
   q->xfer_par = p;
-  if (!q->defer_xfer) return pipe_launch_xfer(h, nullptr);
+  if (!q->defer_xfer && !behind_commit) return pipe_launch_xfer(h, nullptr);
   return FC_OK;
 }
 
@@ -1134,6 +1141,21 @@ int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* 
 // `after` set, the staging also waits for everything queued so far on that stream
 // (deferred mode: launched at the end of the row update so that the host-link
 // kernel does not run beside the HBM-bound backward).
+// fc_profile: add a finished staging kernel's event time (block: wait for it; else only
+// when its end event has already fired)
+static void harvest_xfer_time(fc_cache* h, int par, bool block) {
+  Pipe* q = h->pipe;
+  if (!q->timed[par]) return;
+  if (!block && cudaEventQuery(q->px[par][1]) != cudaSuccess) return;
+  float ms = 0.f;
+  if (cudaEventSynchronize(q->px[par][1]) == cudaSuccess &&
+      cudaEventElapsedTime(&ms, q->px[par][0], q->px[par][1]) == cudaSuccess) {
+    h->prof[1] += ms;
+    h->prof[6] += 1;
+  }
+  q->timed[par] = false;
+}
+
 int pipe_launch_xfer(fc_cache* h, cudaStream_t after) {
   Pipe* q = h->pipe;
   if (!q || !q->xfer_pending) return FC_OK;
@@ -1148,6 +1170,7 @@ int pipe_launch_xfer(fc_cache* h, cudaStream_t after) {
     FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_after, 0));
   }
   PipeArgs x = pipe_args(h, p);
+  harvest_xfer_time(h, p, true);  // this parity's previous staging (long finished) before its events are reused
   q->timed[p] = h->profile != 0;
   if (q->timed[p]) FC_CUDA(cudaEventRecord(q->px[p][0], q->xfer));
   trace_mark(h, T_XFER_BEGIN, q->xfer);
@@ -1174,13 +1197,19 @@ int pipe_launch_xfer(fc_cache* h, cudaStream_t after) {
 int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
   Pipe* q = h->pipe;
   std::memset(info, 0, sizeof(*info));
-  if (!q || !q->outstanding) {
+  if (!q || q->nout == 0) {
     set_error("no prefetched prepare to commit");
     return FC_ERR_BAD_ARG;
   }
-  const int p = q->par ^ 1;
-  FC_TRY_E(pipe_launch_xfer(h, nullptr));  // deferred staging not triggered by an update: launch it now
-  q->outstanding = false;
+  const int p = q->par ^ (q->nout & 1);  // the oldest outstanding prepare
+  // deferred staging of this batch not triggered by an update: launch it now
+  if (q->xfer_pending && q->xfer_par == p) FC_TRY_E(pipe_launch_xfer(h, nullptr));
+  q->nout -= 1;
+  // a newer prepare begun behind this commit gets its staging once this commit is queued
+  auto launch_next_xfer = [&]() -> int {
+    if (q->xfer_pending && q->xfer_par == (p ^ 1)) return pipe_launch_xfer(h, nullptr);
+    return FC_OK;
+  };
   const auto tw0 = std::chrono::steady_clock::now();
   FC_CUDA(cudaEventSynchronize(q->ev_index[p]));
   slow_wait_note("commit: index phase event", tw0);
@@ -1196,6 +1225,7 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
     FC_CUDA(cudaStreamWaitEvent(st, q->ev_xfer[p], 0));
     FC_CUDA(cudaEventRecord(q->ev_commit[p], st));
     q->has_commit[p] = true;
+    FC_TRY_E(launch_next_xfer());
     if (c.err == FC_ERR_ID_OUT_OF_RANGE) info->bad_id = (c.lo != LLONG_MAX) ? c.lo : c.hi;
     return c.err;
   }
@@ -1233,6 +1263,7 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
   trace_mark(h, T_COMMIT_END, st);
   FC_CUDA(cudaEventRecord(q->ev_commit[p], st));
   q->has_commit[p] = true;
+  FC_TRY_E(launch_next_xfer());
   h->last_wb_dev = c.needed > 0 ? a->dev_rows + b : nullptr;
   if (c.needed > 0) {  // ship the write-back stage (upper bound: every victim) D2H on the side stream
     {  // the dispatcher must have consumed d2h[b] of the previous job on stage b before it is re-recorded
@@ -1270,16 +1301,7 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
   h->ev_src = q->ib[p].evicted;
   h->ad_src = q->ib[p].admitted;
   if (h->profile) {
-    // the previous prefetch's transfer kernel is long finished: harvest its time
-    const int o = p ^ 1;
-    if (q->timed[o]) {
-      float ms = 0.f;
-      if (cudaEventSynchronize(q->px[o][1]) == cudaSuccess && cudaEventElapsedTime(&ms, q->px[o][0], q->px[o][1]) == cudaSuccess) {
-        h->prof[1] += ms;
-        h->prof[6] += 1;
-      }
-      q->timed[o] = false;
-    }
+    for (int par = 0; par < 2; ++par) harvest_xfer_time(h, par, false);  // stagings that have finished
     h->prof[2] += 1;
     h->prof[3] += 4.0 * (h->dim + h->sw) * (double)c.misses;
     h->prof[4] += 4.0 * (h->dim + h->sw) * (double)c.needed;

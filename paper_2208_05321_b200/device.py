@@ -7,6 +7,7 @@ cache computation happens in the library's sm_100a kernels.
 
 from __future__ import annotations
 
+import collections
 import ctypes
 import os
 
@@ -188,7 +189,12 @@ class DeviceCache:
     # ------------------------------------------------------------------ prefetch pipeline
     @property
     def prefetch_outstanding(self) -> bool:
-        return getattr(self, "_pf", None) is not None
+        return bool(getattr(self, "_pfq", None))
+
+    @property
+    def prefetch_depth(self) -> int:
+        """Prefetched prepares begun and not yet committed (0, 1 or 2)."""
+        return len(getattr(self, "_pfq", ()))
 
     def prepare_begin(self, ids, batch_seq: int = 0, index_on_main: bool | None = None, ready=None):
         """Launch the next batch's prepare ahead of time (fc_prepare_begin): the index
@@ -201,10 +207,15 @@ class DeviceCache:
         work queued so far on the current stream is done (they may be its output),
         or, when `ready` (a torch.cuda.Event) is given, once that event has fired --
         pass it for ids that were complete earlier, so the index phase does not wait
-        for this batch's queued forward."""
+        for this batch's queued forward.
+
+        Up to two prepares may be outstanding (commits are FIFO): calling
+        prepare_begin(t+1) before prepare_commit(t) lets batch t+1's index phase start
+        on the device as soon as batch t's has ended, instead of after the host has
+        committed t; its staging is launched by that commit."""
         torch = self.torch
-        if self.prefetch_outstanding:
-            raise RuntimeError("a prefetched prepare is outstanding: commit it first")
+        if self.prefetch_depth >= 2:
+            raise RuntimeError("two prefetched prepares are outstanding: commit one first")
         if getattr(self, "index_stream", None) is None:
             # highest priority: the index phase is short but on the pipeline's critical
             # path, and must not queue behind the previous batch's backward blocks
@@ -256,7 +267,9 @@ class DeviceCache:
                                         ctypes.c_void_p(_ptr(buf[2 * k:3 * k])),
                                         ctypes.c_void_p(_ptr(buf[3 * k:4 * k])), ctypes.c_void_p(_ptr(buf[4 * k:])),
                                         ctypes.c_void_p(idx.cuda_stream)))
-        self._pf = (buf, k, d_ids, ids)
+        if not hasattr(self, "_pfq"):
+            self._pfq = collections.deque()
+        self._pfq.append((buf, k, d_ids, ids))
 
     PF_RING = 3
 
@@ -284,8 +297,7 @@ class DeviceCache:
         Returns what prepare() returns; info.rows_to_slow is -1 (decided on device)."""
         if not self.prefetch_outstanding:
             raise RuntimeError("no prefetched prepare to commit")
-        buf, k, d_ids, obj = self._pf
-        self._pf = None
+        buf, k, d_ids, obj = self._pfq.popleft()  # the oldest (fc_prepare_commit's order)
         self._last_pf = (obj, d_ids)
         info = _lib.PrepareInfo()
         check(self.lib.fc_prepare_commit(self.h, self.stream(), ctypes.byref(info)))
@@ -300,7 +312,7 @@ class DeviceCache:
 
     def prefetched_ids(self):
         """The ids object passed to the outstanding prepare_begin (or None)."""
-        return self._pf[3] if self.prefetch_outstanding else None
+        return self._pfq[0][3] if self.prefetch_outstanding else None
 
     def committed_matches(self, ids) -> bool:
         """After prepare_commit: was the committed batch `ids`? Same object, or equal

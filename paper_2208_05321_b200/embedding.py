@@ -115,7 +115,9 @@ class CachedEmbeddingBag(torch.nn.Module):
         PAPER.md:490): its index phase runs on a side stream and its misses are staged
         host -> HBM on the transfer stream while this batch's backward still runs.
         Call it after forward(batch t) and before backward(t); the next forward with
-        the same `indices` object commits it. Cache decisions, slot assignment and
+        the same `indices` object commits it. It may also be called before forward(t)
+        (two prefetches outstanding): batch t+1's index phase then starts on the device
+        as soon as batch t's has ended. Cache decisions, slot assignment and
         write-backs are bit-identical to not prefetching. Device `indices` are read
         after the work queued on the current stream, or after `ready` (a
         torch.cuda.Event) when given (DeviceCache.prepare_begin)."""
@@ -138,6 +140,8 @@ class CachedEmbeddingBag(torch.nn.Module):
             res = self.cache.prepare_commit()
             if not self.cache.committed_matches(indices):
                 res = None
+                while self.cache.prefetch_outstanding:  # every prefetched batch runs before `indices`
+                    self.cache.prepare_commit()
         if res is None:
             res = self.cache.prepare(indices.to(dev, non_blocking=True).reshape(-1))
         info, uids, ucnt, uranks, uslots, inverse, _ = res
@@ -149,7 +153,7 @@ class CachedEmbeddingBag(torch.nn.Module):
     def flush(self) -> int:
         """Write every dirty cached row (and optimizer state) back to host memory.
         An outstanding prefetch is committed first (its batch becomes resident)."""
-        if self.cache.prefetch_outstanding:
+        while self.cache.prefetch_outstanding:
             self.cache.prepare_commit()
         return self.cache.flush()
 

@@ -108,13 +108,16 @@ def test_prefetched_simulator_run(name):
     assert hashlib.sha256(st.slow.rows.tobytes()).hexdigest() == str(g["slow_final_sha"])
 
 
+@pytest.mark.parametrize("depth", [1, 2])
 @pytest.mark.parametrize("num_ids,cap,dim,nb,bsz,always", [
     (50_000, 3_000, 32, 40, 2_000, False),
     (200_000, 12_000, 128, 12, 9_000, True),
     (3_000, 400, 16, 60, 350, False),   # tiny cache: ranks bounce out and back while their write-back is pending
     (5_000, 900, 8, 50, 600, False),
 ])
-def test_prefetched_random_parity_vs_oracle(num_ids, cap, dim, nb, bsz, always):
+def test_prefetched_random_parity_vs_oracle(num_ids, cap, dim, nb, bsz, always, depth):
+    """depth 1: prefetch(b+1) after prepare(b); depth 2: prefetch(b+1) BEFORE prepare(b),
+    so two prefetches are outstanding and batch b+1's index phase runs ahead of commit(b)."""
     rng = np.random.default_rng(num_ids + 1)
     p = 1.0 / np.arange(1, num_ids + 1) ** 1.05
     trace = rng.permutation(num_ids)[rng.choice(num_ids, size=(nb, bsz), p=p / p.sum())]
@@ -130,8 +133,15 @@ def test_prefetched_random_parity_vs_oracle(num_ids, cap, dim, nb, bsz, always):
     st.warmup(cap // 2)
     colw = oracle.column_weights(dim, 9)
     ids = [trace[b] for b in range(nb)]
-    q = st.prepare(ids[0], 0)
+    if depth == 1:
+        q = st.prepare(ids[0], 0)
+    else:
+        st.prefetch(ids[0], 0)
     for b in range(nb):
+        if depth == 2:
+            if b + 1 < nb:
+                st.prefetch(ids[b + 1], b + 1)
+            q = st.prepare(ids[b], b)  # commits the older of the two outstanding prefetches
         a = orc.prepare(ids[b], b)
         for k in ("unique_ids", "unique_ranks", "unique_counts", "unique_slots"):
             assert np.array_equal(getattr(q, k), a[k]), (b, k)
@@ -139,12 +149,12 @@ def test_prefetched_random_parity_vs_oracle(num_ids, cap, dim, nb, bsz, always):
         assert np.array_equal(st.events[-1].evicted_ranks, a["evicted"])
         assert np.array_equal(st.events[-1].admitted_ranks, a["admitted"])
         assert np.array_equal(q.slots_for_ids(), orc.occurrence_slots(a))
-        if b + 1 < nb:
+        if b + 1 < nb and depth == 1:
             st.prefetch(ids[b + 1], b + 1)
         gs = oracle.row_scalars(a["unique_ids"], a["unique_counts"], b, 9)
         orc.apply_unique_update(a, gs[:, None] * colw[None, :])
         st.apply_synthetic_update(q, b, 9, colw)
-        if b + 1 < nb:
+        if b + 1 < nb and depth == 1:
             q = st.prepare(ids[b + 1], b + 1)
     assert st.flush().rows == orc.flush()["rows"]
     torch.cuda.synchronize()
@@ -191,6 +201,65 @@ def test_prefetch_errors_and_mixing():
     st.prefetch(np.array([1, 2, 3]), 7)
     q = st.prepare(np.array([1, 2, 3]), 7)
     st.scatter_update(q, np.full((3, dim), 0.5, np.float32))
+    st.flush()
+    torch.cuda.synchronize()
+    assert st.first_divergence() is None
+    st.state.check_invariants()
+
+
+@pytest.mark.parametrize("optimizer,mode,bags", [("sgd", "sum", False), ("adagrad", "mean", True)])
+def test_module_prefetch_depth2_matches_sequential(optimizer, mode, bags):
+    """prefetch(t+1) called BEFORE forward(t) (two outstanding): bit-identical tables and
+    optimizer state to training without prefetch."""
+    rng = np.random.default_rng(15)
+    num_ids, dim, steps, B = 20_000, 32, 10, 3_000
+    p = 1.0 / np.arange(1, num_ids + 1) ** 1.1
+    trace = rng.permutation(num_ids)[rng.choice(num_ids, size=(steps, B), p=p / p.sum())]
+    w0 = rng.uniform(-0.1, 0.1, (num_ids, dim)).astype(np.float32)
+    idx = fc.build_reorder(fc.scan_frequencies(trace, num_ids))
+    grads = [rng.standard_normal((B // 3 if bags else B, dim)).astype(np.float32) for _ in range(steps)]
+    offs = torch.arange(0, B, 3) if bags else None
+
+    def train(depth2):
+        m = CachedEmbeddingBag(num_ids, dim, 0.1, mode=mode, weight=w0, idx_map=idx, optimizer=optimizer, lr=0.05)
+        ids = [torch.from_numpy(trace[s]) for s in range(steps)]
+        if depth2:
+            m.prefetch(ids[0])
+        for s in range(steps):
+            if depth2 and s + 1 < steps:
+                m.prefetch(ids[s + 1])
+                assert m.cache.prefetch_depth == 2
+            out = m(ids[s], offs)
+            out.backward(torch.from_numpy(grads[s]).cuda())
+        m.flush()
+        return m.weight().copy(), (m.optimizer_state().copy() if optimizer == "adagrad" else None)
+
+    w_seq, s_seq = train(False)
+    w_pf, s_pf = train(True)
+    assert np.array_equal(w_seq, w_pf)
+    if s_seq is not None:
+        assert np.array_equal(s_seq, s_pf)
+
+
+def test_prefetch_depth2_limits_and_mismatch():
+    """A third outstanding begin is refused; a prepare of ids that match neither
+    prefetch runs both prefetched batches first (FIFO), then the ids."""
+    num_ids, cap, dim = 64, 4, 8
+    idx = fc.IdxMap(np.arange(num_ids), np.arange(num_ids))
+    slow, _, ref = fc.init_stores(num_ids, dim, cap / num_ids, init_seed=1, idx_map=idx)
+    st = fc.CacheStack(idx, slow, fc.FastTierStore(np.zeros((cap, dim), np.float32)), fc.Transmitter(),
+                       reference=ref, log_events=True, engine="async")
+    st.prepare(np.array([1, 2]), 0)
+    a, b = np.array([3, 4]), np.array([5, 6])
+    st.prefetch(a, 1)
+    st.prefetch(b, 2)
+    with pytest.raises(RuntimeError, match="two prefetched"):
+        st.prefetch(np.array([7]), 3)
+    p = st.prepare(np.array([1, 7]), 3)  # a, then b, then [1, 7]
+    # a filled the two free slots; b evicted the largest unprotected ranks 4, 3; [1, 7]
+    # hits 1 and evicts 6 for 7 (identity reorder)
+    assert (p.hits, p.misses, p.evictions) == (1, 1, 1)
+    assert set(st.state.occupied_ranks().tolist()) == {1, 2, 5, 7}
     st.flush()
     torch.cuda.synchronize()
     assert st.first_divergence() is None
