@@ -68,19 +68,26 @@ def test_pipeline_sequencing_rules():
     assert lib.fc_set_engine(h, 1) == _lib.OK
     n = 4
     ids = torch.tensor([1, 2, 3, 4], dtype=torch.int64, device="cuda")
-    out = torch.empty(5 * n, dtype=torch.int32, device="cuda")
+    out = torch.empty(10 * n, dtype=torch.int32, device="cuda")
     p = [ctypes.c_void_p(out[i * n:(i + 1) * n].data_ptr()) for i in range(5)]
+    p2 = [ctypes.c_void_p(out[i * n:(i + 1) * n].data_ptr()) for i in range(5, 10)]
     info = _lib.PrepareInfo()
     assert lib.fc_prepare_commit(h, None, ctypes.byref(info)) == _lib.ERR_BAD_ARG  # nothing to commit
     assert lib.fc_prepare_begin(h, ctypes.c_void_p(ids.data_ptr()), 8, n, 0, *p, None) == _lib.OK
-    assert lib.fc_prepare_begin(h, ctypes.c_void_p(ids.data_ptr()), 8, n, 1, *p, None) == _lib.ERR_BAD_ARG
+    assert lib.fc_prepare_begin(h, ctypes.c_void_p(ids.data_ptr()), 8, n, 1, *p2, None) == _lib.OK  # depth 2
+    assert lib.fc_prepare_begin(h, ctypes.c_void_p(ids.data_ptr()), 8, n, 2, *p, None) == _lib.ERR_BAD_ARG
     assert b"outstanding" in lib.fc_last_error()
     rows = ctypes.c_int64()
-    assert lib.fc_flush(h, None, ctypes.byref(rows)) == _lib.ERR_BAD_ARG       # sync verbs wait for the commit
+    assert lib.fc_flush(h, None, ctypes.byref(rows)) == _lib.ERR_BAD_ARG       # sync verbs wait for the commits
     assert lib.fc_set_engine(h, 0) == _lib.ERR_BAD_ARG
+    assert lib.fc_set_modes(h, 1, 0) == _lib.ERR_BAD_ARG                        # a mode change too
+    assert lib.fc_set_modes(h, 0, 0) == _lib.OK                                 # the same modes are fine
     assert lib.fc_prepare(h, ctypes.c_void_p(ids.data_ptr()), 8, n, 0, *p, None, ctypes.byref(info)) == _lib.ERR_BAD_ARG
-    assert lib.fc_prepare_commit(h, None, ctypes.byref(info)) == _lib.OK
+    assert lib.fc_prepare_commit(h, None, ctypes.byref(info)) == _lib.OK       # FIFO: batch 0 first
     assert (info.unique, info.misses, info.rows_to_slow) == (4, 4, -1)
+    assert lib.fc_flush(h, None, ctypes.byref(rows)) == _lib.ERR_BAD_ARG       # batch 1 still outstanding
+    assert lib.fc_prepare_commit(h, None, ctypes.byref(info)) == _lib.OK
+    assert (info.unique, info.misses, info.hits) == (4, 0, 4)
     wb = ctypes.c_int64()
     assert lib.fc_last_writebacks(h, ctypes.byref(wb)) == _lib.OK and wb.value == 0
     assert lib.fc_flush(h, None, ctypes.byref(rows)) == _lib.OK and rows.value == 0

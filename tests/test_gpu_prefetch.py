@@ -266,6 +266,36 @@ def test_prefetch_depth2_limits_and_mismatch():
     st.state.check_invariants()
 
 
+def test_prefetch_depth2_error_in_first():
+    """Two outstanding, the older one invalid: its commit raises and mutates nothing; the
+    newer one (whose index phase ran behind the failed one) then commits exactly as a
+    plain prepare would after the error."""
+    num_ids, cap, dim = 64, 4, 8
+    idx = fc.IdxMap(np.arange(num_ids), np.arange(num_ids))
+    slow, _, ref = fc.init_stores(num_ids, dim, cap / num_ids, init_seed=1, idx_map=idx)
+    st = fc.CacheStack(idx, slow, fc.FastTierStore(np.zeros((cap, dim), np.float32)), fc.Transmitter(),
+                       reference=ref, log_events=True, engine="async")
+    orc = oracle.OracleCache(np.arange(num_ids), np.zeros((num_ids, dim), np.float32), cap)
+    for ids in ([1, 2], [3, 4, 5]):
+        st.prepare(np.array(ids), 0)
+        orc.prepare(np.array(ids), 0)
+    for bad, err in ((np.array([1, 2, 3, 9, 10]), cm.BatchExceedsCapacity), (np.array([7, 99]), ValueError)):
+        good = np.array([6, 3, 7])
+        st.prefetch(bad, 1)
+        st.prefetch(good, 2)
+        with pytest.raises(err):
+            st.prepare(bad, 1)
+        p = st.prepare(good, 2)
+        a = orc.prepare(good, 2)
+        assert (p.hits, p.misses, p.evictions) == (a["hits"], a["misses"], a["evictions"])
+        assert np.array_equal(p.unique_slots, a["unique_slots"])
+        assert np.array_equal(st.state.slot_to_rank, orc.slot_rank)
+    st.flush()
+    torch.cuda.synchronize()
+    assert st.first_divergence() is None
+    st.state.check_invariants()
+
+
 @pytest.mark.parametrize("optimizer,mode,bags", [("sgd", "sum", False), ("adagrad", "mean", True)])
 def test_module_prefetch_matches_sequential(optimizer, mode, bags):
     """Training through CachedEmbeddingBag with prefetch() gives bit-identical tables
