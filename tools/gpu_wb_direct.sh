@@ -1,4 +1,5 @@
 #!/bin/bash
+# (historical record: FC_WB_DIRECT / k_wb_direct were removed after this sweep; see profiles/r01_wb_direct_sweep.txt)
 # direct write-back (FC_WB_DIRECT=1): parity tests, then A/B vs host scatter and a grid sweep
 FC_WB_DIRECT=1 timeout 900 python -m pytest tests/test_gpu_prefetch.py tests/test_gpu_fullsize.py tests/test_gpu_embedding.py tests/test_gpu_simulator.py -x -q 2>&1 | tail -2
 for i in 1 2; do
