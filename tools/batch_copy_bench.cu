@@ -3,9 +3,15 @@
 // would replace: time alone, host submit cost, and next to an HBM-bound (H) and a
 // latency-bound (L) kernel -- the interference that limits the prefetch pipeline
 // (DESIGN.md 4a).
+// argv[2] = "thp": the slow tier is 2 MB-aligned, madvise(MADV_HUGEPAGE) and
+// cudaHostRegister'ed instead of cudaHostAlloc'ed (does a coarser host mapping cut the
+// interference?). argv[3] = "quick": skip the batched-copy rows.
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/bcb tools/batch_copy_bench.cu -lcuda
+#include <sys/mman.h>
+
 #include <algorithm>
 #include <chrono>
+#include <cstring>
 #include <cstdio>
 #include <cstdlib>
 #include <random>
@@ -66,8 +72,20 @@ int main(int argc, char** argv) {
   float4 *ha, *hb;
   CK(cudaMalloc(&ha, nH * 16));
   CK(cudaMalloc(&hb, nH * 16));
+  const bool thp = argc > 2 && !strcmp(argv[2], "thp");
+  const bool quick = argc > 3 && !strcmp(argv[3], "quick");
   float4* host;
-  CK(cudaHostAlloc(&host, table_rows * 512, cudaHostAllocMapped));
+  auto ta = std::chrono::steady_clock::now();
+  if (thp) {
+    if (posix_memalign((void**)&host, 1 << 21, table_rows * 512)) return 1;
+    madvise(host, table_rows * 512, MADV_HUGEPAGE);
+    memset(host, 0, table_rows * 512);
+    CK(cudaHostRegister(host, table_rows * 512, cudaHostRegisterMapped | cudaHostRegisterPortable));
+  } else {
+    CK(cudaHostAlloc(&host, table_rows * 512, cudaHostAllocMapped));
+  }
+  printf("slow tier: %s, alloc %.0f ms\n", thp ? "THP + cudaHostRegister" : "cudaHostAlloc",
+         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta).count());
   for (long i = 0; i < table_rows * 32; i += 997) host[i] = make_float4((float)i, 1.f, 2.f, 3.f);
   float4* hostd;
   CK(cudaHostGetDevicePointer((void**)&hostd, host, 0));
@@ -173,6 +191,11 @@ int main(int argc, char** argv) {
   alone("H hbm copy 2x1GiB", H);
   alone("L dependent gather 1M rows", L);
   alone("Z zero-copy SM gather", Z);
+  if (quick) {
+    both("H + Z", H, Z);
+    both("L + Z", L, Z);
+    return 0;
+  }
   for (int chunk : {rows, 8192, 1024}) {
     char nm[80];
     snprintf(nm, sizeof nm, "BA h2d batch chunk %d", chunk);

@@ -39,6 +39,8 @@ def read(rep):
 
 
 def main():
+    if len(sys.argv) < 3 or sys.argv[1].startswith("-"):
+        sys.exit(__doc__)
     prefix, reps = sys.argv[1], sys.argv[2:]
     table, js = [], {}
     for rep in reps:
