@@ -311,7 +311,8 @@ class DeviceCache:
         return int(v.value)
 
     def prefetched_ids(self):
-        """The ids object passed to the outstanding prepare_begin (or None)."""
+        """The ids object of the oldest outstanding prepare_begin, the next one to be
+        committed (or None)."""
         return self._pfq[0][3] if self.prefetch_outstanding else None
 
     def committed_matches(self, ids) -> bool:
