@@ -48,7 +48,10 @@ def test_route_matches_numpy(world, num_ids, n):
     r.route(torch.from_numpy(ids[:10]).cuda())  # state is clean after an error
 
 
-def test_row_sharded_module_nccl_world1_matches_dense():
+@pytest.mark.parametrize("ids_on", ["cuda", "host", "cuda_ready"])
+def test_row_sharded_module_nccl_world1_matches_dense(ids_on):
+    """ids_on: device ids (the side-stream exchange waits for the current stream), pinned
+    host ids (copied on the side stream), device ids with a `ready` event."""
     import torch.distributed as dist
 
     if not dist.is_initialized():
@@ -66,7 +69,14 @@ def test_row_sharded_module_nccl_world1_matches_dense():
     mod = RowShardedEmbedding(shard, 1, 0, mode="sum", device=torch.device("cuda"))
     assert mod.router is not None
     grads = [rng.standard_normal((B, dim)).astype(np.float32) for _ in range(steps)]
-    ids = [torch.from_numpy(trace[s]).cuda() for s in range(steps)]
+    if ids_on == "host":
+        ids = [torch.from_numpy(trace[s]).pin_memory() for s in range(steps)]
+    else:
+        ids = [torch.from_numpy(trace[s]).cuda() for s in range(steps)]
+    ready = None
+    if ids_on == "cuda_ready":
+        ready = torch.cuda.Event()
+        ready.record()
     dense = torch.nn.EmbeddingBag(num_ids, dim, mode="sum", sparse=True)
     dense.weight.data = torch.from_numpy(table.copy())
     opt = torch.optim.SGD(dense.parameters(), lr=0.1)
@@ -77,7 +87,7 @@ def test_row_sharded_module_nccl_world1_matches_dense():
         # values' scale (|w| <~ 0.5) as the absolute floor
         np.testing.assert_allclose(out.detach().cpu().numpy(), want.detach().numpy(), rtol=1e-5, atol=5e-6)
         if s + 1 < steps:
-            mod.prefetch(ids[s + 1])
+            mod.prefetch(ids[s + 1], ready=ready)
         out.backward(torch.from_numpy(grads[s]).cuda())
         opt.zero_grad()
         want.backward(torch.from_numpy(grads[s]))
