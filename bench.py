@@ -114,52 +114,116 @@ def make_workload(cfg, n_batches, device=None, keep_counts=False):
 
 
 # ----------------------------------------------------------------------------- measurement helpers
+_NVML_POLLER = r"""
+import sys, time
+import pynvml as nv
+nv.nvmlInit()
+try:
+    h = nv.nvmlDeviceGetHandleByPciBusId(sys.argv[1])
+except Exception:
+    h = nv.nvmlDeviceGetHandleByIndex(int(sys.argv[2]))
+reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+print("ready", flush=True)
+while True:
+    t = time.monotonic()
+    print("%.6f,%d,%d,%d" % (t, nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx, reasons(h)), flush=True)
+    time.sleep(float(sys.argv[3]))
+"""
+
+
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region: an NVML poller in
+    its own process (no GIL shared with the timed loop) prints CLOCK_MONOTONIC-stamped
+    samples every 2 ms; only those between entering and leaving the region are kept.
+    Falls back to `nvidia-smi -lms 100` when nvidia-ml-py is missing."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+    BITS = [0x8, 0x40, 0x20, 0x4]  # nvmlClocksThrottleReason{HwSlowdown,HwThermal,SwThermal,SwPowerCap}
 
     def __init__(self, gpu: int):
         self.gpu = gpu
-        self.rows = []
+        self.period = float(os.environ.get("FC_CLOCK_POLL_MS", "2")) / 1e3
+        self.rows = []  # (sm_mhz, max_mhz, [4 bools])
         self.proc = None
+        self.source = None
+        self.lines = []
+
+    def _start_nvml(self):
+        bus = ""
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.gpu)
+            bus = "%08x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+        except Exception:
+            pass
+        proc = subprocess.Popen([sys.executable, "-c", _NVML_POLLER, bus, str(self.gpu), str(self.period)],
+                                stdout=subprocess.PIPE,
+                                stderr=subprocess.DEVNULL, text=True)
+        if proc.stdout.readline().strip() != "ready":
+            proc.kill()
+            raise RuntimeError("NVML poller did not start")
+        self.th = threading.Thread(target=lambda: self.lines.extend(proc.stdout), daemon=True)
+        self.th.start()
+        return proc
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.th = threading.Thread(target=self._read, daemon=True)
-            self.th.start()
+            self.proc = self._start_nvml()
+            self.source = "nvml poller, %g ms" % (self.period * 1e3)
         except Exception:
             self.proc = None
+        if self.proc is None:
+            try:
+                self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                                              "--format=csv,noheader,nounits", "-lms", "100"],
+                                             stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                self.source = "nvidia-smi, 100 ms"
+                self.th = threading.Thread(target=self._read_smi, daemon=True)
+                self.th.start()
+            except Exception:
+                self.proc = None
+        self.t0 = time.monotonic()
         return self
 
-    def _read(self):
+    def _read_smi(self):
         for line in self.proc.stdout:
             parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 6:
-                self.rows.append(parts)
+            if len(parts) == 6 and parts[0].replace(".", "").isdigit():
+                self.rows.append((float(parts[0]), float(parts[1]) if parts[1].replace(".", "").isdigit() else None,
+                                  [p == "Active" for p in parts[2:]]))
 
     def __exit__(self, *a):
-        if self.proc is not None:
-            time.sleep(0.25)
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=2)
-            except Exception:
-                self.proc.kill()
+        self.t1 = time.monotonic()
+        if self.proc is None:
+            return
+        time.sleep(0.01 if self.source.startswith("nvml") else 0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        self.th.join(timeout=2)
+        if self.source.startswith("nvml"):
+            for line in self.lines:
+                try:
+                    t, sm, mx, r = line.strip().split(",")
+                except ValueError:
+                    continue
+                if self.t0 <= float(t) <= self.t1:
+                    self.rows.append((float(sm), float(mx), [bool(int(r) & b) for b in self.BITS]))
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0,
+                    "source": self.source}
+        sm = [r[0] for r in self.rows]
+        mx = [r[1] for r in self.rows if r[1] is not None]
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4) if r[2][i]})
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows), "source": self.source}
 
 
 def host_link_peaks(torch, dev):
