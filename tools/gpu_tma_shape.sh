@@ -1,4 +1,5 @@
 #!/bin/bash
+# (historical record: the FC_TMA_STAGES knob was removed after this sweep; 4 stages are compiled in)
 # staging shape: stages per block x blocks (same bytes in flight along the diagonal)
 for i in 1 2; do
   for sb in 4:40 2:80 8:20 2:40 8:40; do
