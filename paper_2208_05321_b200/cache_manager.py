@@ -287,15 +287,17 @@ def prepare_cache(state: CacheState, idx_map: IdxMap, ids, transmitter: Transmit
         raise ValueError(f"evict_mode must be one of {EVICT_MODES}, got {evict_mode!r}")
     policy = _check_policy(policy)
     dev = _bound(state, idx_map, transmitter, slow, fast, write_back, evict_mode)
-    if dev.prefetch_outstanding:
-        # a prefetched batch is executed first (its commit); `ids` itself is that batch
-        # when it is the very object handed to prefetch, else it is prepared after it
+    while dev.prefetch_outstanding:
+        # prefetched batches are executed first (their commits, FIFO); when `ids` is one of
+        # them (the very object handed to prefetch, or equal contents) its commit is the
+        # result, else `ids` is prepared after all of them. Every commit is logged (event +
+        # transfer reports) like the prepare it is.
+        obj, seq = dev.prefetched_ids(), dev.prefetched_seq()
         res = dev.prepare_commit()
         if dev.committed_matches(ids):
             return _prepare_result(dev, ids, res, transmitter, fast, policy, batch_seq, event_log,
                                    rows_to_slow=dev.last_writebacks())
-        while dev.prefetch_outstanding:  # every prefetched batch runs before `ids`
-            dev.prepare_commit()
+        _prepare_result(dev, obj, res, transmitter, fast, policy, seq, event_log, rows_to_slow=dev.last_writebacks())
     dev.set_modes(write_back, evict_mode)
     return _prepare_result(dev, ids, dev.prepare(ids, batch_seq), transmitter, fast, policy, batch_seq, event_log)
 

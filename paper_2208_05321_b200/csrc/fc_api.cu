@@ -673,7 +673,7 @@ int fc_backward_update(fc_cache* h, const int32_t* uslots, const int32_t* inv, c
   cudaStream_t st = as_stream(stream);
   FC_TRY(launch_backward(h, uslots, inv, ucnt, u, n, offsets, off_bytes, nbags, include_last, psw, mode, grad, optim,
                          lr, eps, st));
-  return pipe_launch_xfer(h, st);  // deferred miss staging of a prefetched batch runs after this update
+  return pipe_launch_xfer(h, st, true);  // deferred miss staging of a prefetched batch runs after this update
 }
 
 }  // extern "C"

@@ -644,6 +644,8 @@ struct Pipe {
   bool tma = false;                        // stage through the bulk-copy engine (k_admit_stage_tma)
   int tma_blocks = kTmaBlocks;
   bool xfer_pending = false;
+  bool xfer_behind = false;                // the pending staging was begun behind an uncommitted prepare:
+                                           // only that prepare's commit may launch it
   int xfer_par = 0;
   cudaEvent_t ev_after = nullptr;
 };
@@ -1132,8 +1134,9 @@ int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* 
   q->nout += 1;
   q->par = o;
   q->xfer_pending = true;
+  q->xfer_behind = behind_commit;
   q->xfer_par = p;
-  if (!q->defer_xfer && !behind_commit) return pipe_launch_xfer(h, nullptr);
+  if (!q->defer_xfer && !behind_commit) return pipe_launch_xfer(h, nullptr, false);
   return FC_OK;
 }
 
@@ -1156,16 +1159,21 @@ static void harvest_xfer_time(fc_cache* h, int par, bool block) {
   q->timed[par] = false;
 }
 
-int pipe_launch_xfer(fc_cache* h, cudaStream_t after) {
+int pipe_launch_xfer(fc_cache* h, cudaStream_t after, bool from_update) {
   Pipe* q = h->pipe;
   if (!q || !q->xfer_pending) return FC_OK;
+  // A row update may not launch a staging that waits for an uncommitted prepare: its wait
+  // on that prepare's commit event would bind to a stale commit and the staging could
+  // read pending marks before that commit writes them. pipe_commit launches it.
+  if (from_update && q->xfer_behind) return FC_OK;
   q->xfer_pending = false;
+  q->xfer_behind = false;
   const int p = q->xfer_par, o = p ^ 1;
   // stage(t+1) after index(t+1) and commit(t): pending marks and the stage's last reader
   FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_index[p], 0));
   if (q->has_commit[o]) FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_commit[o], 0));
   if (q->has_commit[p]) FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_commit[p], 0));
-  if (after) {
+  if (from_update) {  // `after` may be the legacy default stream (NULL)
     FC_CUDA(cudaEventRecord(q->ev_after, after));
     FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_after, 0));
   }
@@ -1203,11 +1211,11 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
   }
   const int p = q->par ^ (q->nout & 1);  // the oldest outstanding prepare
   // deferred staging of this batch not triggered by an update: launch it now
-  if (q->xfer_pending && q->xfer_par == p) FC_TRY_E(pipe_launch_xfer(h, nullptr));
+  if (q->xfer_pending && q->xfer_par == p) FC_TRY_E(pipe_launch_xfer(h, nullptr, false));
   q->nout -= 1;
   // a newer prepare begun behind this commit gets its staging once this commit is queued
   auto launch_next_xfer = [&]() -> int {
-    if (q->xfer_pending && q->xfer_par == (p ^ 1)) return pipe_launch_xfer(h, nullptr);
+    if (q->xfer_pending && q->xfer_par == (p ^ 1)) return pipe_launch_xfer(h, nullptr, false);
     return FC_OK;
   };
   const auto tw0 = std::chrono::steady_clock::now();

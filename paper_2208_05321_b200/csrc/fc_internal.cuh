@@ -155,7 +155,7 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info);
 bool pipe_outstanding(const fc_cache* h);
 int pipe_order(fc_cache* h, cudaStream_t st);
 int pipe_sync_commits(fc_cache* h);
-int pipe_launch_xfer(fc_cache* h, cudaStream_t after);
+int pipe_launch_xfer(fc_cache* h, cudaStream_t after, bool from_update);  // after: extra dependency
 void pipe_release(fc_cache* h);
 }  // namespace fc
 

@@ -196,7 +196,7 @@ class DeviceCache:
         """Prefetched prepares begun and not yet committed (0, 1 or 2)."""
         return len(getattr(self, "_pfq", ()))
 
-    def prepare_begin(self, ids, batch_seq: int = 0, index_on_main: bool | None = None, ready=None):
+    def prepare_begin(self, ids, batch_seq: int = 0, index_on_main: bool | None = None, ready=None, consumer=None):
         """Launch the next batch's prepare ahead of time (fc_prepare_begin): the index
         phase runs on this cache's index stream and the admitted rows are staged
         host -> HBM on the library's transfer stream, both overlapping whatever the
@@ -207,7 +207,10 @@ class DeviceCache:
         work queued so far on the current stream is done (they may be its output),
         or, when `ready` (a torch.cuda.Event) is given, once that event has fired --
         pass it for ids that were complete earlier, so the index phase does not wait
-        for this batch's queued forward.
+        for this batch's queued forward. `consumer` is the stream that will use the
+        results after the commit (default: the current stream); the per-batch buffers
+        are recorded on it so the allocator cannot hand them out while it still reads
+        them (a caller that begins on a side stream passes its main stream here).
 
         Up to two prepares may be outstanding (commits are FIFO): calling
         prepare_begin(t+1) before prepare_commit(t) lets batch t+1's index phase start
@@ -220,7 +223,8 @@ class DeviceCache:
             # highest priority: the index phase is short but on the pipeline's critical
             # path, and must not queue behind the previous batch's backward blocks
             self.index_stream = torch.cuda.Stream(self.device, priority=-100)
-        main = torch.cuda.current_stream(self.device)
+        main = torch.cuda.current_stream(self.device)  # orders device ids
+        consumer = main if consumer is None else consumer
         if index_on_main is None:
             index_on_main = self.index_on_main
         idx = main if index_on_main else self.index_stream
@@ -260,8 +264,9 @@ class DeviceCache:
                     raise ValueError("prefetch needs a non-empty batch")
                 k = min(n, self.capacity)
                 buf = torch.empty(4 * k + n, dtype=torch.int32, device=self.device)
-            d_ids.record_stream(main)
-            buf.record_stream(main)
+            for st_ in {main, consumer}:
+                d_ids.record_stream(st_)
+                buf.record_stream(st_)
         check(self.lib.fc_prepare_begin(self.h, ctypes.c_void_p(_ptr(d_ids)), d_ids.element_size(), n, int(batch_seq),
                                         ctypes.c_void_p(_ptr(buf[:k])), ctypes.c_void_p(_ptr(buf[k:2 * k])),
                                         ctypes.c_void_p(_ptr(buf[2 * k:3 * k])),
@@ -269,7 +274,7 @@ class DeviceCache:
                                         ctypes.c_void_p(idx.cuda_stream)))
         if not hasattr(self, "_pfq"):
             self._pfq = collections.deque()
-        self._pfq.append((buf, k, d_ids, ids))
+        self._pfq.append((buf, k, d_ids, ids, int(batch_seq)))
 
     PF_RING = 3
 
@@ -297,7 +302,7 @@ class DeviceCache:
         Returns what prepare() returns; info.rows_to_slow is -1 (decided on device)."""
         if not self.prefetch_outstanding:
             raise RuntimeError("no prefetched prepare to commit")
-        buf, k, d_ids, obj = self._pfq.popleft()  # the oldest (fc_prepare_commit's order)
+        buf, k, d_ids, obj, _ = self._pfq.popleft()  # the oldest (fc_prepare_commit's order)
         self._last_pf = (obj, d_ids)
         info = _lib.PrepareInfo()
         check(self.lib.fc_prepare_commit(self.h, self.stream(), ctypes.byref(info)))
@@ -314,6 +319,10 @@ class DeviceCache:
         """The ids object of the oldest outstanding prepare_begin, the next one to be
         committed (or None)."""
         return self._pfq[0][3] if self.prefetch_outstanding else None
+
+    def prefetched_seq(self):
+        """The batch_seq of the oldest outstanding prepare_begin (or None)."""
+        return self._pfq[0][4] if self.prefetch_outstanding else None
 
     def committed_matches(self, ids) -> bool:
         """After prepare_commit: was the committed batch `ids`? Same object, or equal

@@ -59,8 +59,8 @@ class CudaShard:
         return {"info": info, "uslots": uslots, "inverse": inverse, "ucnt": ucnt, "n": int(inverse.numel())}
 
     # prefetch pipeline (DeviceCache.prepare_begin / prepare_commit)
-    def prepare_begin(self, ids):
-        self.cache.prepare_begin(ids)
+    def prepare_begin(self, ids, consumer=None):
+        self.cache.prepare_begin(ids, consumer=consumer)
 
     def prepare_commit(self):
         info, uids, ucnt, uranks, uslots, inverse, _ = self.cache.prepare_commit()
@@ -268,9 +268,6 @@ class PeerRows:
 
     def pool_to_peers(self, shard, h, x):
         ct = self._ct
-        m, me, W = x["mat"], self.rank, self.world
-        if x["u"] > self.max_rows:
-            raise RuntimeError(f"PeerRows buffer holds {self.max_rows} rows, batch routes {x['u']}")
         seg, off = self._segments(x)
         stream = ct.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         self._check(self.lib.fc_pool_to_peers(shard.cache.h, ct.c_void_p(h["uslots"].data_ptr()),
@@ -287,6 +284,12 @@ class PeerRows:
         where my segment starts in requester r's routing order (after the ids r sends to
         owners < me)."""
         m, me, W = x["mat"], self.rank, self.world
+        # every requester's buffer must hold what it routes: as an owner this rank writes into
+        # (forward) and reads from (backward) every peer's buffer, so the bound is checked on the
+        # full count matrix (identical on every rank: all raise together) before any peer kernel
+        need = max(int(sum(row)) for row in m)
+        if need > self.max_rows:
+            raise RuntimeError(f"PeerRows buffers hold {self.max_rows} rows, a rank routes {need}")
         x["seg"] = _upload([0] + np.cumsum(x["rc"]).tolist(), self.device)
         x["off"] = _upload([sum(m[r][:me]) for r in range(W)], self.device)
 
@@ -299,8 +302,6 @@ class PeerRows:
         """Requester: per-routed-id gradients into the shared gbuf; barrier; owner: pull the
         rows of its received ids from every requester's gbuf over peer memory."""
         ct = self._ct
-        if x["u"] > self.max_rows:
-            raise RuntimeError(f"PeerRows buffer holds {self.max_rows} rows, batch routes {x['u']}")
         router.grads(x["inv"], x["u"], grad_out, offsets, n_bags, include_last_offset, psw, mode,
                      out=self.gbuf[:x["u"]])
         if self.world > 1:  # every requester's gradients are in place
@@ -432,7 +433,8 @@ class RowShardedEmbedding(torch.nn.Module):
             dev_ids = ids.reshape(-1).to(self.device, non_blocking=True)
             x = self._exchange_ids(dev_ids)
             if hasattr(self.shard, "prepare_begin") and x["recv_ids"].numel() > 0:
-                self.shard.prepare_begin(x["recv_ids"])  # its index stream waits for xs
+                # its index stream waits for xs; the prepare's buffers are used on main
+                self.shard.prepare_begin(x["recv_ids"], consumer=main)
                 x["begun"] = True
             ev = torch.cuda.Event()
             ev.record(xs)

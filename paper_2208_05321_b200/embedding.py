@@ -136,12 +136,11 @@ class CachedEmbeddingBag(torch.nn.Module):
                 raise NotImplementedError("gradients w.r.t. per_sample_weights are not supported")
             per_sample_weights = per_sample_weights.to(dev, dtype=torch.float32).reshape(-1).contiguous()
         res = None
-        if self.cache.prefetch_outstanding:  # the prefetched batch is executed first (its commit)
+        while self.cache.prefetch_outstanding:  # prefetched batches are executed first (FIFO commits)
             res = self.cache.prepare_commit()
-            if not self.cache.committed_matches(indices):
-                res = None
-                while self.cache.prefetch_outstanding:  # every prefetched batch runs before `indices`
-                    self.cache.prepare_commit()
+            if self.cache.committed_matches(indices):
+                break
+            res = None  # not this batch: it runs after every prefetched one
         if res is None:
             res = self.cache.prepare(indices.to(dev, non_blocking=True).reshape(-1))
         info, uids, ucnt, uranks, uslots, inverse, _ = res

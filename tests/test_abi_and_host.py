@@ -122,3 +122,21 @@ def test_simulator_config_and_presets_match_reference_goldens():
         assert cfg.resolved() == doc["metrics"]["config"]
     with pytest.raises(NotImplementedError):
         simulator.SimConfig(policy="lru").validate()
+
+
+def test_peer_rows_bound_is_checked_on_the_full_count_matrix():
+    """An owner writes into (and reads from) EVERY requester's peer buffer, so the buffer
+    bound is checked against the largest row of the all-gathered count matrix before any
+    peer kernel runs -- not only against this rank's own routed count."""
+    import torch
+
+    from paper_2208_05321_b200.distributed import PeerRows
+
+    pr = object.__new__(PeerRows)
+    pr.rank, pr.world, pr.max_rows, pr.device = 0, 2, 10, torch.device("cpu")
+    x = {"mat": [[3, 4], [6, 6]], "rc": [3, 6], "u": 7}  # this rank routes 7 <= 10; rank 1 routes 12
+    with pytest.raises(RuntimeError, match="routes 12"):
+        pr.segments(x)
+    x = {"mat": [[3, 4], [4, 6]], "rc": [3, 4], "u": 7}
+    pr.segments(x)
+    assert x["seg"].tolist() == [0, 3, 7] and x["off"].tolist() == [0, 0]

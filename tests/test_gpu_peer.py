@@ -85,6 +85,7 @@ def test_pool_to_peers_over_cuda_ipc():
     proc = ctx.Process(target=_peer_child, args=(b,))
     proc.start()
     buf = torch.zeros((400, 16), device="cuda")
+    torch.cuda.synchronize()  # the zero fill lands before the peer process writes into buf
     hd = (ctypes.c_ubyte * 64)()
     assert lib.fc_ipc_handle(ctypes.c_void_p(buf.data_ptr()), hd) == _lib.OK
     a.send(bytes(hd))

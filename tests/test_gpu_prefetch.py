@@ -241,6 +241,38 @@ def test_module_prefetch_depth2_matches_sequential(optimizer, mode, bags):
         assert np.array_equal(s_seq, s_pf)
 
 
+def test_module_prefetch_two_ahead_before_backward():
+    """prefetch(t+2) after forward(t) and BEFORE backward(t), with t+1 still outstanding:
+    t+2's miss staging must wait for commit(t+1)'s write-back marks (a dirty row evicted
+    by t+1 and re-admitted by t+2 comes from the write-back stage, not the stale slow
+    tier). Small cache + skewed ids make that round trip frequent. Bit-identical to
+    training without prefetch."""
+    rng = np.random.default_rng(21)
+    num_ids, dim, steps, B = 6_000, 32, 14, 2_000
+    p = 1.0 / np.arange(1, num_ids + 1) ** 0.9
+    trace = rng.permutation(num_ids)[rng.choice(num_ids, size=(steps, B), p=p / p.sum())]
+    w0 = rng.uniform(-0.1, 0.1, (num_ids, dim)).astype(np.float32)
+    idx = fc.build_reorder(fc.scan_frequencies(trace, num_ids))
+    grads = [rng.standard_normal((B, dim)).astype(np.float32) for _ in range(steps)]
+
+    def train(ahead):
+        m = CachedEmbeddingBag(num_ids, dim, 0.25, mode="sum", weight=w0, idx_map=idx, lr=0.05)
+        ids = [torch.from_numpy(trace[s]) for s in range(steps)]
+        if ahead:
+            m.prefetch(ids[0])
+            m.prefetch(ids[1])
+        for s in range(steps):
+            out = m(ids[s])  # commits s; s+1 stays outstanding
+            if ahead and s + 2 < steps:
+                m.prefetch(ids[s + 2])  # begun behind the uncommitted s+1, before backward(s)
+                assert m.cache.prefetch_depth == 2
+            out.backward(torch.from_numpy(grads[s]).cuda())
+        m.flush()
+        return m.weight().copy()
+
+    assert np.array_equal(train(False), train(True))
+
+
 def test_prefetch_depth2_limits_and_mismatch():
     """A third outstanding begin is refused; a prepare of ids that match neither
     prefetch runs both prefetched batches first (FIFO), then the ids."""
@@ -260,6 +292,15 @@ def test_prefetch_depth2_limits_and_mismatch():
     # hits 1 and evicts 6 for 7 (identity reorder)
     assert (p.hits, p.misses, p.evictions) == (1, 1, 1)
     assert set(st.state.occupied_ranks().tolist()) == {1, 2, 5, 7}
+    # the bypassed prefetches are logged like the prepares they are (events in batch order)
+    assert [e.batch_seq for e in st.events] == [0, 1, 2, 3]
+    assert set(st.events[2].evicted_ranks.tolist()) == {3, 4}
+    # ids equal to the SECOND outstanding prefetch: the first is committed, then the second is the result
+    st.prefetch(np.array([8]), 4)
+    st.prefetch(np.array([9, 1]), 5)
+    p = st.prepare(np.array([9, 1]), 5)
+    assert (p.hits, p.misses) == (1, 1)
+    assert [e.batch_seq for e in st.events] == [0, 1, 2, 3, 4, 5]
     st.flush()
     torch.cuda.synchronize()
     assert st.first_divergence() is None
