@@ -101,6 +101,10 @@ int fc_attach_slow_tier(fc_cache* h, float* rows_host, int64_t row_stride,
 /* Per-call modes of prepare_cache (write_back, evict_mode kwargs, cache_manager.py:241-245).
  * Changing them while a prefetch is outstanding is refused; re-setting the same modes is not. */
 int fc_set_modes(fc_cache* h, int32_t write_back, int32_t evict_mode);
+/* The staging buffer of the transmitter passed to prepare_cache (transmitter.py:75-94; the
+ * reference takes the transmitter per call). Only BufferTooSmall and the message accounting
+ * depend on it. Refused while a prefetch is outstanding (unless unchanged). */
+int fc_set_buffer_bytes(fc_cache* h, int64_t buffer_bytes);
 /* CacheState.free_count after the last synchronising call. */
 int64_t fc_free_count(fc_cache* h);
 
@@ -279,7 +283,11 @@ int fc_pool_to_peers(fc_cache* h, const int32_t* unique_slots, const int32_t* in
  * requesters' writes. */
 int fc_gather_from_peers(const float* const* src_ptrs_dev, const int64_t* src_off_dev, const int64_t* seg_dev,
                          int32_t world, int64_t n, int32_t dim, float* out, void* stream);
-/* CUDA IPC plumbing for the peer pointers (64-byte opaque handles). */
+/* CUDA IPC plumbing for the peer pointers. handle_out: FC_IPC_HANDLE_BYTES opaque bytes
+ * (the allocation's cudaIpcMemHandle_t + the pointer's offset inside it, so pointers into a
+ * caching allocator's segment export correctly); fc_ipc_open returns the same address in
+ * the importing process; fc_ipc_close takes the pointer fc_ipc_open returned. */
+#define FC_IPC_HANDLE_BYTES 128
 int fc_ipc_handle(void* dev_ptr, void* handle_out);
 int fc_ipc_open(const void* handle, int32_t device, void** dev_ptr_out);
 int fc_ipc_close(void* dev_ptr);

@@ -210,9 +210,21 @@ class OracleCache:
         self.events: list[dict] = []
 
     # -- helpers ---------------------------------------------------------
+    def _move_messages(self, rows: int) -> int:
+        """Messages of one Transmitter._move (transmitter.py:144-195), raising where it
+        raises -- BEFORE any row is copied: a row larger than the buffer is an error for a
+        no-op move and for every block-mode move (:162-164, :179 rows_per_message);
+        row-wise moves send one message per row and never stage (:167-177)."""
+        row_bytes = self.dim * 4
+        if (rows == 0 or self.mode == "block") and row_bytes > self.buffer_bytes:
+            raise OracleBufferTooSmall(f"row of {row_bytes} B cannot fit in a {self.buffer_bytes} B buffer")
+        if rows == 0:
+            return 0
+        return rows if self.mode == "rowwise" else -(-rows // (self.buffer_bytes // row_bytes))
+
     def _report(self, direction: str, rows: int) -> dict:
         row_bytes = self.dim * 4
-        msgs = chunk_messages(rows, row_bytes, self.buffer_bytes, self.mode)
+        msgs = self._move_messages(rows)
         return {"direction": direction, "rows": int(rows), "bytes": int(rows * row_bytes), "messages": int(msgs)}
 
     def _occupied_ranks(self) -> np.ndarray:
@@ -263,9 +275,10 @@ class OracleCache:
             evicted = self._largest_unprotected(needed, ranks)
             vslots = self.rank_slot[evicted].astype(np.int64)
             wb = vslots if self.write_back == "always" else vslots[self.dirty[vslots]]
-            if wb.size:
+            if wb.size:  # _write_back skips the move (and its buffer check) when no victim is dirty (:227-230)
+                rep = self._report("to_slow", wb.size)  # raises before any mutation
                 self.slow[self.slot_rank[wb]] = self.fast[wb]
-                reports.append(self._report("to_slow", wb.size))
+                reports.append(rep)
             else:
                 reports.append({"direction": "to_slow", "rows": 0, "bytes": 0, "messages": 0})
             self.slot_rank[vslots] = EMPTY
@@ -278,8 +291,9 @@ class OracleCache:
             if empties.size < n_miss:
                 raise OracleInsufficientFreeSlots(f"{n_miss} to admit, {empties.size} free")
             tgt = empties[:n_miss]
+            rep = self._report("to_fast", n_miss)  # raises after the evictions above were applied
             self.fast[tgt] = self.slow[admitted]
-            reports.append(self._report("to_fast", n_miss))
+            reports.append(rep)
             self.slot_rank[tgt] = admitted
             self.rank_slot[admitted] = tgt.astype(np.int32)
             self.dirty[tgt] = False
@@ -300,6 +314,7 @@ class OracleCache:
         if k == 0:
             return {"direction": "to_fast", "rows": 0, "bytes": 0, "messages": 0}
         r = np.arange(k, dtype=np.int64)
+        rep = self._report("to_fast", k)
         self.fast[:k] = self.slow[:k]
         self.slot_rank[:k] = r
         self.rank_slot[:k] = r.astype(np.int32)
@@ -307,7 +322,7 @@ class OracleCache:
         self.free -= k
         self.events.append({"batch_seq": -1, "protected": np.empty(0, np.int64),
                             "evicted": np.empty(0, np.int64), "admitted": r, "hits": 0, "misses": k})
-        return self._report("to_fast", k)
+        return rep
 
     def mark_dirty(self, slots) -> None:
         s = np.asarray(slots, dtype=np.int64).reshape(-1)
@@ -319,9 +334,10 @@ class OracleCache:
         ds = np.nonzero(self.dirty)[0]
         if ds.size == 0:
             return {"direction": "to_slow", "rows": 0, "bytes": 0, "messages": 0}
+        rep = self._report("to_slow", ds.size)
         self.slow[self.slot_rank[ds]] = self.fast[ds]
         self.dirty[ds] = False
-        return self._report("to_slow", ds.size)
+        return rep
 
     def select_evictions(self, needed: int, protected) -> np.ndarray:
         if needed < 0:

@@ -26,6 +26,8 @@ ERR_SLOT_OUT_OF_RANGE = 8
 ERR_NOT_EMPTY = 9
 ERR_NO_SLOW_TIER = 10
 
+IPC_HANDLE_BYTES = 128  # FC_IPC_HANDLE_BYTES
+
 WB = {"dirty_only": 0, "always": 1}
 EVICT = {"occupancy_aware": 0, "paper_literal": 1}
 POOL = {"sum": 0, "mean": 1}
@@ -55,6 +57,7 @@ _SIGS = {
     "fc_attach_slow_tier": (c_int32, [c_void_p, c_void_p, c_int64, c_void_p, c_int64]),
     "fc_set_modes": (c_int32, [c_void_p, c_int32, c_int32]),
     "fc_free_count": (c_int64, [c_void_p]),
+    "fc_set_buffer_bytes": (c_int32, [c_void_p, c_int64]),
     "fc_profile": (c_int32, [c_void_p, c_int32, c_void_p]),
     "fc_set_engine": (c_int32, [c_void_p, c_int32]),
     "fc_drain": (c_int32, [c_void_p]),

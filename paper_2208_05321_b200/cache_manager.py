@@ -111,7 +111,7 @@ class CacheState:
         if idx_map.num_ids != self.num_ids:
             raise ValueError("idx_map does not match the state's id space")
         dev = DeviceCache(self.num_ids, self.capacity, fast.embedding_dim, write_back=write_back,
-                          evict_mode=evict_mode, buffer_bytes=transmitter.buffer.capacity_bytes, device=device)
+                          evict_mode=evict_mode, buffer_bytes=_device_buffer(transmitter, fast), device=device)
         dev.set_idx_map(idx_map.rank_of)
         slow.pin()
         dev.attach_slow(slow.rows)
@@ -257,6 +257,15 @@ class PrepareResult:
         return {int(i): int(s) for i, s in zip(self.unique_ids, self.unique_slots)}
 
 
+def _device_buffer(transmitter: Transmitter, fast: FastTierStore) -> int:
+    """The staging-buffer bound the device applies. Row-wise moves never stage a row
+    (transmitter.py:167-177), so only the block transmitter can refuse a row; and no
+    prepare issues a no-op move (the reference skips empty moves), so the row-wise bound
+    never binds."""
+    b = int(transmitter.buffer.capacity_bytes)
+    return b if transmitter.mode == "block" else max(b, fast.embedding_dim * 4)
+
+
 def _bound(state: CacheState, idx_map, transmitter, slow, fast, write_back="dirty_only",
            evict_mode="occupancy_aware") -> DeviceCache:
     if state.device is None:
@@ -299,6 +308,7 @@ def prepare_cache(state: CacheState, idx_map: IdxMap, ids, transmitter: Transmit
                                    rows_to_slow=dev.last_writebacks())
         _prepare_result(dev, obj, res, transmitter, fast, policy, seq, event_log, rows_to_slow=dev.last_writebacks())
     dev.set_modes(write_back, evict_mode)
+    dev.set_buffer_bytes(_device_buffer(transmitter, fast))  # the reference takes the transmitter per call
     return _prepare_result(dev, ids, dev.prepare(ids, batch_seq), transmitter, fast, policy, batch_seq, event_log)
 
 
@@ -311,6 +321,7 @@ def prefetch_cache(state: CacheState, idx_map: IdxMap, ids, transmitter: Transmi
     object commits it; the outcome is bit-identical to a plain prepare_cache then."""
     dev = _bound(state, idx_map, transmitter, slow, fast, write_back, evict_mode)
     dev.set_modes(write_back, evict_mode)
+    dev.set_buffer_bytes(_device_buffer(transmitter, fast))
     dev.prepare_begin(ids, batch_seq)
 
 
@@ -347,6 +358,7 @@ def warmup(state: CacheState, idx_map: IdxMap, k: int, transmitter: Transmitter,
         return TransferReport.empty(TO_FAST)
     report = transmitter.report(TO_FAST, int(k), fast.embedding_dim * 4)
     dev = _bound(state, idx_map, transmitter, slow, fast)
+    dev.set_buffer_bytes(_device_buffer(transmitter, fast))
     dev.warmup(int(k))
     if event_log is not None:
         name = policy.name if policy is not None else "warmup"
@@ -371,8 +383,8 @@ def flush(state: CacheState, transmitter: Transmitter, slow: SlowTierStore, fast
         return TransferReport.empty(TO_SLOW)
     dev = state.device
     row_bytes = fast.embedding_dim * 4
-    if row_bytes > transmitter.buffer.capacity_bytes and int(dev.dirty.sum().item()):
-        transmitter.buffer.rows_per_message(row_bytes)  # raises BufferTooSmall
+    if transmitter.mode == "block" and row_bytes > transmitter.buffer.capacity_bytes and int(dev.dirty.sum().item()):
+        transmitter.buffer.rows_per_message(row_bytes)  # raises BufferTooSmall before any mutation (:410-413)
     rows = dev.flush()
     if rows == 0:
         return TransferReport.empty(TO_SLOW)

@@ -4,7 +4,11 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
+
+#include <cuda.h>
 
 #include "fc_internal.cuh"
 
@@ -269,6 +273,14 @@ int fc_set_modes(fc_cache* h, int32_t write_back, int32_t evict_mode) {
 }
 
 int64_t fc_free_count(fc_cache* h) { return h ? h->host_free : -1; }
+
+int fc_set_buffer_bytes(fc_cache* h, int64_t buffer_bytes) {
+  if (!h || buffer_bytes < 1) return FC_ERR_BAD_ARG;
+  if (buffer_bytes == h->buffer_bytes) return FC_OK;
+  FC_NO_OUTSTANDING(h);
+  h->buffer_bytes = buffer_bytes;
+  return FC_OK;
+}
 
 int fc_set_engine(fc_cache* h, int32_t engine) {
   if (!h) return FC_ERR_BAD_ARG;
@@ -622,25 +634,74 @@ int fc_gather_from_peers(const float* const* src_ptrs_dev, const int64_t* src_of
   return launch_gather_from_peers(src_ptrs_dev, src_off_dev, seg_dev, world, n, dim, out, as_stream(stream));
 }
 
+// A CUDA IPC handle names a whole cudaMalloc allocation and cudaIpcOpenMemHandle maps its
+// BASE; a pointer inside a caching allocator's segment (torch) sits at an offset from it.
+// The exported handle therefore carries that offset, and the importer adds it back.
+struct IpcHandle {
+  cudaIpcMemHandle_t h;
+  int64_t offset;
+};
+static_assert(sizeof(IpcHandle) <= FC_IPC_HANDLE_BYTES, "IPC handle size");
+
+typedef CUresult (*AddrRangeFn)(CUdeviceptr*, size_t*, CUdeviceptr);
+static AddrRangeFn addr_range_fn() {
+  static AddrRangeFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<AddrRangeFn>(p);
+  }();
+  return fn;
+}
+
+static std::mutex g_ipc_m;
+static std::unordered_map<void*, void*> g_ipc_base;  // opened pointer -> mapped base (for close)
+
 int fc_ipc_handle(void* dev_ptr, void* handle_out) {
   if (!dev_ptr || !handle_out) return FC_ERR_BAD_ARG;
-  cudaIpcMemHandle_t hd;
-  FC_CUDA(cudaIpcGetMemHandle(&hd, dev_ptr));
-  std::memcpy(handle_out, &hd, sizeof(hd));
+  IpcHandle x;
+  std::memset(&x, 0, sizeof(x));
+  FC_CUDA(cudaIpcGetMemHandle(&x.h, dev_ptr));
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  AddrRangeFn fn = addr_range_fn();
+  if (!fn || fn(&base, &size, reinterpret_cast<CUdeviceptr>(dev_ptr)) != CUDA_SUCCESS) {
+    set_error("cuMemGetAddressRange failed for the IPC export");
+    return FC_ERR_CUDA;
+  }
+  x.offset = (int64_t)(reinterpret_cast<CUdeviceptr>(dev_ptr) - base);
+  std::memset(handle_out, 0, FC_IPC_HANDLE_BYTES);
+  std::memcpy(handle_out, &x, sizeof(x));
   return FC_OK;
 }
 
 int fc_ipc_open(const void* handle, int32_t device, void** dev_ptr_out) {
   if (!handle || !dev_ptr_out) return FC_ERR_BAD_ARG;
   DeviceGuard dg(device);
-  cudaIpcMemHandle_t hd;
-  std::memcpy(&hd, handle, sizeof(hd));
-  FC_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, hd, cudaIpcMemLazyEnablePeerAccess));
+  IpcHandle x;
+  std::memcpy(&x, handle, sizeof(x));
+  void* base = nullptr;
+  FC_CUDA(cudaIpcOpenMemHandle(&base, x.h, cudaIpcMemLazyEnablePeerAccess));
+  *dev_ptr_out = static_cast<char*>(base) + x.offset;
+  std::lock_guard<std::mutex> lk(g_ipc_m);
+  g_ipc_base[*dev_ptr_out] = base;
   return FC_OK;
 }
 
 int fc_ipc_close(void* dev_ptr) {
-  if (dev_ptr) FC_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+  if (!dev_ptr) return FC_OK;
+  void* base = dev_ptr;
+  {
+    std::lock_guard<std::mutex> lk(g_ipc_m);
+    auto it = g_ipc_base.find(dev_ptr);
+    if (it != g_ipc_base.end()) {
+      base = it->second;
+      g_ipc_base.erase(it);
+    }
+  }
+  FC_CUDA(cudaIpcCloseMemHandle(base));
   return FC_OK;
 }
 

@@ -1107,6 +1107,14 @@ int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* 
     if (rc) return rc;
   }
   Pipe* q = h->pipe;
+  if ((int64_t)h->dim * 4 > h->buffer_bytes) {
+    // the reference's order for a row larger than the buffer (write-back raises before
+    // mutation only when a victim is dirty) needs the dirty bits at decision time, which
+    // the concurrent row update of the previous batch may still change
+    set_error("the prefetch pipeline needs a staging buffer of at least one row (%d B > %lld B)", h->dim * 4,
+              (long long)h->buffer_bytes);
+    return FC_ERR_BUFFER_TOO_SMALL;
+  }
   // Depth 2: batch t+1 may be begun while batch t is still uncommitted -- its index phase
   // only needs index(t) (state order) and commit(t-1) (this parity's buffers), so it can
   // start on the device the moment index(t) ends instead of after the host has committed

@@ -277,17 +277,35 @@ __global__ void __launch_bounds__(kNT) k_inverse(const IdT* __restrict__ ids, in
 }
 
 // ------------------------------------------------------------------ eviction count (:293-296)
-__global__ void k_plan(Counters* c, int cap, int evict_mode, int row_fits) {
+__global__ void k_plan(Counters* c, int cap, int evict_mode) {
   if (c->err) return;
   const int m = c->misses, u = c->unique, fr = c->free_count;
   const int needed = evict_mode == FC_EVICT_OCCUPANCY_AWARE ? max(0, m - fr) : max(0, u - cap);
   c->needed = needed;
   if (fr + needed < m) c->err = FC_ERR_INSUFFICIENT_FREE_SLOTS;  // paper_literal (:313-317)
-  // a row larger than the staging buffer cannot move (transmitter.py:85-88); refuse
-  // before any mutation whenever this batch has rows to move
-  if (!row_fits && (m > 0 || needed > 0)) c->err = FC_ERR_BUFFER_TOO_SMALL;
   c->win_admit[0] = 0;
   c->win_admit[1] = m;
+}
+
+// A row larger than the staging buffer (transmitter.py:85-88) -- launched only in that
+// degenerate configuration, in the reference's order (cache_manager.py:298-323): the
+// write-back of victims raises BEFORE any mutation when there is a row to write back
+// (_write_back skips the move when every victim is clean); otherwise the evictions are
+// applied and the admission raises (k_bts_after_evict). A batch of hits raises nothing.
+__global__ void k_bts_before_evict(const int32_t* __restrict__ evicted, const int32_t* __restrict__ rank_to_slot,
+                                   const uint8_t* __restrict__ dirty, int always, Counters* c) {
+  if (c->err) return;
+  const int needed = c->needed;
+  if (needed == 0) {
+    if (c->misses > 0 && blockIdx.x == 0 && threadIdx.x == 0) c->err = FC_ERR_BUFFER_TOO_SMALL;
+    return;
+  }
+  for (int v = blockIdx.x * kNT + threadIdx.x; v < needed; v += gridDim.x * kNT)
+    if (always || dirty[rank_to_slot[evicted[v]]]) c->err = FC_ERR_BUFFER_TOO_SMALL;
+}
+
+__global__ void k_bts_after_evict(Counters* c) {
+  if (c->err == 0 && c->misses > 0) c->err = FC_ERR_BUFFER_TOO_SMALL;
 }
 
 // ------------------------------------------------------------------ victims (:298-303)
@@ -418,12 +436,17 @@ int launch_prepare(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32
   if (ids_bytes == 8) k_inverse<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->aux, inverse, c);
   else k_inverse<int><<<gn, kNT, 0, st>>>((const int*)ids, n, h->aux, inverse, c);
 
-  k_plan<<<1, 1, 0, st>>>(c, h->capacity, h->evict_mode, (int64_t)h->dim * 4 <= h->buffer_bytes);
+  k_plan<<<1, 1, 0, st>>>(c, h->capacity, h->evict_mode);
 
   compact(CandWords{h->res_bits, h->prot_bits}, EvictFin{}, EvictEmit{h->evicted_ranks, 0}, h->nw_ids, h->block_cnt,
           win_evict(c), c, G_EVICT, st);
+  const bool row_fits = (int64_t)h->dim * 4 <= h->buffer_bytes;
+  if (!row_fits)
+    k_bts_before_evict<<<grid_for(h->capacity, kNT, kSMs * 4), kNT, 0, st>>>(
+        h->evicted_ranks, h->rank_to_slot, h->dirty, h->write_back == FC_WB_ALWAYS, c);
   int rc = h->engine == 1 ? engine_evict(h, st) : launch_evict_rows(h, st);
   if (rc) return rc;
+  if (!row_fits) k_bts_after_evict<<<1, 1, 0, st>>>(c);
 
   compact(ArrWords{h->miss_bits}, AdmitFin{}, RankEmit{h->admitted_ranks}, h->nw_ids, h->block_cnt,
           win_admit(c), c, G_ADMIT, st);
@@ -572,7 +595,7 @@ int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, i
   if (ids_bytes == 8) k_inverse<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->aux, inverse, c);
   else k_inverse<int><<<gn, kNT, 0, st>>>((const int*)ids, n, h->aux, inverse, c);
   trace_mark(h, 22, st);
-  k_plan<<<1, 1, 0, st>>>(c, h->capacity, h->evict_mode, (int64_t)h->dim * 4 <= h->buffer_bytes);
+  k_plan<<<1, 1, 0, st>>>(c, h->capacity, h->evict_mode);  // (the pipeline requires a row to fit the buffer)
   compact(CandWords{h->res_bits, h->prot_bits}, EvictFin{}, EvictEmit{b.evicted, 0}, h->nw_ids, h->block_cnt,
           win_evict(c), c, G_EVICT, st);
   k_evict_state<<<grid_for(h->capacity, kNT, kSMs * 4), kNT, 0, st>>>(b.evicted, b.vslots, h->slot_to_rank,

@@ -97,6 +97,12 @@ class DeviceCache:
             check(self.lib.fc_set_modes(self.h, _lib.WB[write_back], _lib.EVICT[evict_mode]))
             self.write_back, self.evict_mode = write_back, evict_mode
 
+    def set_buffer_bytes(self, buffer_bytes: int) -> None:
+        """Staging-buffer size of the transmitter this call uses (BufferTooSmall + accounting)."""
+        if int(buffer_bytes) != self.buffer_bytes:
+            check(self.lib.fc_set_buffer_bytes(self.h, int(buffer_bytes)))
+            self.buffer_bytes = int(buffer_bytes)
+
     @property
     def free_count(self) -> int:
         return int(self.lib.fc_free_count(self.h))

@@ -238,8 +238,10 @@ class PeerRows:
 
     def _share(self, buf):
         """Every rank's pointer to its peers' copy of `buf` (CUDA IPC), as a device array."""
+        from . import _lib
+
         ct = self._ct
-        hd = (ct.c_ubyte * 64)()
+        hd = (ct.c_ubyte * _lib.IPC_HANDLE_BYTES)()
         self._check(self.lib.fc_ipc_handle(ct.c_void_p(buf.data_ptr()), hd))
         handles = [None] * self.world
         dist.all_gather_object(handles, bytes(hd), group=self.group)
@@ -249,7 +251,7 @@ class PeerRows:
                 ptrs.append(buf.data_ptr())
                 continue
             p = ct.c_void_p()
-            hb = (ct.c_ubyte * 64).from_buffer_copy(handles[r])
+            hb = (ct.c_ubyte * _lib.IPC_HANDLE_BYTES).from_buffer_copy(handles[r])
             self._check(self.lib.fc_ipc_open(hb, self.device.index or 0, ct.byref(p)))
             self._opened.append(p)
             ptrs.append(p.value)
@@ -272,9 +274,9 @@ class PeerRows:
         stream = ct.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
         self._check(self.lib.fc_pool_to_peers(shard.cache.h, ct.c_void_p(h["uslots"].data_ptr()),
                                               ct.c_void_p(h["inverse"].data_ptr()), int(h["n"]),
-                                              ct.c_void_p(seg.data_ptr()), W, ct.c_void_p(self.dst.data_ptr()),
+                                              ct.c_void_p(seg.data_ptr()), self.world, ct.c_void_p(self.dst.data_ptr()),
                                               ct.c_void_p(off.data_ptr()), stream))
-        if W > 1:  # every owner's writes land before anyone reads (one rank: stream order suffices)
+        if self.world > 1:  # every owner's writes land before anyone reads (one rank: stream order suffices)
             dist.all_reduce(self.flag, group=self.group)
         return self.rbuf[:x["u"]]
 

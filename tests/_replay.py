@@ -31,3 +31,12 @@ def batches(trace, batch_size):
 
 def expect_batch_rows(g):
     return g["per_batch"], split(g["evicted"], g["evicted_off"]), split(g["admitted"], g["admitted_off"])
+
+
+def bts_calls(g):
+    """The scripted calls of the buffer_too_small fixture (make_golden.gen_buffer_too_small):
+    (verb, buffer_bytes, write_back, ids) with verb in prepare / update / flush."""
+    ids = split(g["call_ids"], g["call_ids_off"])
+    for k in range(len(g["call_verb"])):
+        yield (("prepare", "update", "flush")[int(g["call_verb"][k])], int(g["call_buf"][k]),
+               "always" if int(g["call_always"][k]) else "dirty_only", np.asarray(ids[k], dtype=np.int64))

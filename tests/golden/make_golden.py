@@ -279,6 +279,68 @@ def gen_sim_metrics():
         json.dump(docs, fh, sort_keys=True)
 
 
+# ---------------------------------------------------------------------------
+# 7. BufferTooSmall ordering (cache_manager.py:219-231,298-323; transmitter.py:85-88,160-164)
+# ---------------------------------------------------------------------------
+
+BTS_CALLS = [  # (verb, buffer bytes, write_back, ids); rows are 32 B (dim 8)
+    ("prepare", 4096, "dirty_only", [1, 2, 3, 4]),  # fill the 4 slots
+    ("prepare", 16, "dirty_only", [1, 2]),          # all hits: nothing moves, no error
+    ("prepare", 16, "dirty_only", [5]),             # clean victim 4 evicted, then the admission raises
+    ("update", 4096, "dirty_only", [1, 2]),         # rows 1, 2 dirty
+    ("prepare", 16, "dirty_only", [6, 7]),          # needed 1: clean victim 3 evicted, admission raises
+    ("prepare", 16, "dirty_only", [8]),             # free slots cover the miss: raises before any mutation
+    ("prepare", 4096, "dirty_only", [8, 9]),        # admitted
+    ("prepare", 16, "dirty_only", [10]),            # clean victim 9 evicted, admission raises
+    ("prepare", 4096, "dirty_only", [10, 11]),      # clean victim 8 evicted + written nowhere, admitted
+    ("update", 4096, "dirty_only", [1, 2, 10, 11]), # everything dirty
+    ("prepare", 16, "dirty_only", [12]),            # dirty victim 11: the write-back raises before mutation
+    ("prepare", 16, "always", [12]),                # same under write_back='always'
+    ("flush", 16, "dirty_only", []),                # dirty rows: raises before mutation
+    ("flush", 4096, "dirty_only", []),              # writes them back
+    ("flush", 16, "dirty_only", []),                # nothing dirty: no error
+    ("prepare", 16, "always", [1, 2, 10, 11]),      # all hits: no error
+    ("prepare", 16, "always", [13]),                # 'always' writes even clean victims: raises before mutation
+]
+
+
+def gen_buffer_too_small():
+    num_ids, cap, dim = 16, 4, 8
+    idx = identity_map(num_ids)
+    slow, _, ref = init_stores(num_ids, dim, cap / num_ids, init_seed=0, idx_map=idx)
+    slow0 = slow.rows.copy()
+    fast = FastTierStore(slots=np.zeros((cap, dim), dtype=np.float32))
+    state = cm.CacheState(cap, num_ids)
+    raised, s2r, dirty, free, slows = [], [], [], [], []
+    prep = None
+    for verb, buf, wb, ids in BTS_CALLS:
+        tx = Transmitter(buffer=TransferBuffer(buf))
+        err = 0
+        try:
+            if verb == "prepare":
+                prep = cm.prepare_cache(state, idx, np.array(ids), tx, slow, fast, write_back=wb)
+            elif verb == "update":
+                prep = cm.prepare_cache(state, idx, np.array(ids), tx, slow, fast, write_back=wb)
+                cm.scatter_update(state, fast, prep, np.full((len(ids), dim), 0.25, np.float32))
+            else:
+                cm.flush(state, tx, slow, fast)
+        except freqcache.BufferTooSmall:
+            err = 1
+        raised.append(err)
+        s2r.append(state.slot_to_rank.copy())
+        dirty.append(state.dirty.copy())
+        free.append(state.free_count)
+        slows.append(slow.rows.copy())
+    ids_flat, ids_off = ragged([c[3] for c in BTS_CALLS])
+    np.savez_compressed(os.path.join(OUT, "buffer_too_small.npz"), slow0=slow0, raised=np.array(raised),
+                        call_verb=np.array([("prepare", "update", "flush").index(c[0]) for c in BTS_CALLS]),
+                        call_buf=np.array([c[1] for c in BTS_CALLS]),
+                        call_always=np.array([int(c[2] == "always") for c in BTS_CALLS]),
+                        call_ids=ids_flat, call_ids_off=ids_off,
+                        slot_to_rank=np.array(s2r), dirty=np.array(dirty), free_count=np.array(free),
+                        slow=np.array(slows), meta=np.array([num_ids, cap, dim], dtype=np.int64))
+
+
 def main():
     gen_random_stream("stream_dirty_zipf", "dirty_only")
     gen_random_stream("stream_always_zipf", "always", seed=21, init_seed=3)
@@ -296,6 +358,7 @@ def main():
     gen_functions()
     gen_embedding_bag()
     gen_sim_metrics()
+    gen_buffer_too_small()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -192,6 +192,50 @@ def test_buffer_too_small():
     assert st.state.free_count == 4
 
 
+@pytest.mark.parametrize("engine", ["zerocopy", "async"])
+def test_golden_buffer_too_small_ordering(engine):
+    """A row larger than the transmitter's staging buffer, call by call against the REAL
+    reference's recorded outcome (tests/golden/buffer_too_small.npz): which calls raise
+    BufferTooSmall and the slot table, dirty bits, free count and slow tier after each.
+    A dirty write-back raises before any mutation; clean victims are evicted before the
+    admission raises; hits raise nothing. The transmitter is passed per call, as in the
+    reference's functional API."""
+    from _replay import bts_calls
+
+    g = load_golden("buffer_too_small")
+    num_ids, cap, dim = (int(v) for v in g["meta"])
+    idx = identity_idx_map(num_ids)
+    state = cm.CacheState(cap, num_ids)
+    slow = fc.SlowTierStore(g["slow0"].copy())
+    fast = fc.FastTierStore(np.zeros((cap, dim), np.float32))
+    state.bind(idx, slow, fast, fc.Transmitter(), engine=engine)
+    for k, (verb, buf, wb, ids) in enumerate(bts_calls(g)):
+        tx = fc.Transmitter(buffer=fc.TransferBuffer(buf))
+        raised = 0
+        try:
+            if verb == "flush":
+                cm.flush(state, tx, slow, fast)
+            else:
+                p = cm.prepare_cache(state, idx, ids, tx, slow, fast, write_back=wb, batch_seq=k)
+                if verb == "update":
+                    cm.scatter_update(state, fast, p, np.full((ids.size, dim), 0.25, np.float32))
+        except fc.BufferTooSmall:
+            raised = 1
+        state.device.drain()
+        torch.cuda.synchronize()
+        assert raised == g["raised"][k], k
+        assert np.array_equal(state.slot_to_rank, g["slot_to_rank"][k]), k
+        assert np.array_equal(state.dirty, g["dirty"][k]) and state.free_count == g["free_count"][k], k
+        assert np.array_equal(slow.rows, g["slow"][k]), k
+        state.check_invariants()
+    # the prefetch pipeline needs one row to fit (it decides before the dirty bits are final)
+    dev = state.device
+    if engine == "async":
+        dev.set_buffer_bytes(16)
+        with pytest.raises(fc.BufferTooSmall):
+            dev.prepare_begin(np.array([1]))
+
+
 def test_event_log_jsonl_roundtrip(tmp_path):
     st = build_stack(capacity=2)
     st.prepare([0, 7], batch_seq=0)
@@ -254,7 +298,11 @@ def test_golden_random_stream(name):
     assert st.first_divergence() is None
 
 
-def run_gpu_sim(g):
+def run_gpu_sim(g, update="synthetic"):
+    """update="synthetic": the fused on-device update (k_synthetic); "unique": the
+    reference simulator's own path (simulator.py:429-433), host row_scalars x column
+    weights through CacheStack.apply_unique_update (k_unique_add), with every batch's
+    gather_unique rows checked bitwise against the dense mirror first."""
     s = sim_inputs(g)
     freq = fc.scan_frequencies(s["trace"], s["num_ids"])
     idx = fc.build_reorder(freq)
@@ -268,8 +316,13 @@ def run_gpu_sim(g):
     rows = []
     for seq, ids in batches(s["trace"], s["batch_size"]):
         p = st.prepare(ids, seq)
-        st.gather_unique(p)
-        st.apply_synthetic_update(p, seq, s["updates_seed"], colw)
+        rows_u = st.gather_unique(p)
+        if update == "synthetic":
+            st.apply_synthetic_update(p, seq, s["updates_seed"], colw)
+        else:
+            assert np.array_equal(rows_u.cpu().numpy(), st.reference.rows[p.unique_ids]), seq  # bitwise
+            gs = fc.update_row_scalars(p.unique_ids, p.unique_counts, seq, s["updates_seed"])
+            st.apply_unique_update(p, gs[:, None] * colw[None, :])
         tf = sum(r.rows for r in p.transfer_reports if r.direction == "to_fast")
         ts = sum(r.rows for r in p.transfer_reports if r.direction == "to_slow")
         rows.append([p.num_unique, p.hits, p.misses, p.evictions, tf, ts, tf * s["dim"] * 4, ts * s["dim"] * 4,
@@ -280,9 +333,10 @@ def run_gpu_sim(g):
 
 
 @pytest.mark.parametrize("name", ["sim_small", "sim_small_always", "sim_medium"])
-def test_golden_simulator_run(name):
+@pytest.mark.parametrize("update", ["synthetic", "unique"])
+def test_golden_simulator_run(name, update):
     g = load_golden(name)
-    st, per_batch = run_gpu_sim(g)
+    st, per_batch = run_gpu_sim(g, update)
     pb, evicted, admitted = expect_batch_rows(g)
     assert np.array_equal(per_batch, pb)
     evs = [e for e in st.events if e.batch_seq >= 0]

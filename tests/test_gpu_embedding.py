@@ -82,10 +82,12 @@ def test_training_through_small_cache_equals_dense(opt):
     dense = w0.copy()
     state = np.zeros_like(w0)
     off = np.arange(0, nbags * 3, 3)
+    moved = np.zeros(2, np.int64)  # misses, evictions over the run
     for s in range(steps):
         ids = trace[s]
         gout = rng.normal(0, 1, (nbags, dim)).astype(np.float32)
         out = m(torch.from_numpy(ids), torch.from_numpy(off))
+        moved += (m.last_info.misses, m.last_info.evictions)
         np.testing.assert_allclose(out.detach().cpu().numpy(), oracle.pooled_bag(dense, ids, off, None, "mean"),
                                    rtol=RTOL, atol=ATOL)
         out.backward(torch.from_numpy(gout).cuda())
@@ -95,7 +97,7 @@ def test_training_through_small_cache_equals_dense(opt):
             oracle.sparse_sgd(dense, touched, grad, 0.1)
         else:
             oracle.sparse_adagrad(dense, state, touched, grad, 0.1, 1e-10)
-    assert m.last_info.misses > 0 or True
+    assert moved[0] > 0 and moved[1] > 0, moved  # rows really crossed the host link both ways
     m.flush()
     np.testing.assert_allclose(m.weight(), dense, rtol=RTOL, atol=ATOL)
     if opt == "adagrad":

@@ -64,7 +64,7 @@ def _peer_child(conn):
     p = st.prepare(ids, 0)
     handle = conn.recv()
     ptr = ctypes.c_void_p()
-    buf = (ctypes.c_ubyte * 64).from_buffer_copy(handle)
+    buf = (ctypes.c_ubyte * 128).from_buffer_copy(handle)
     assert lb.fc_ipc_open(buf, 0, ctypes.byref(ptr)) == L.OK
     dst = t.tensor([ptr.value], dtype=t.int64, device="cuda")
     seg = t.tensor([0, ids.size], dtype=t.int64, device="cuda")
@@ -84,9 +84,12 @@ def test_pool_to_peers_over_cuda_ipc():
     a, b = ctx.Pipe()
     proc = ctx.Process(target=_peer_child, args=(b,))
     proc.start()
-    buf = torch.zeros((400, 16), device="cuda")
+    # buf sits at an offset inside its allocation (the caching allocator's case): the
+    # exported handle must carry the offset for the peer to write at buf, not at the base
+    big = torch.zeros((1000, 16), device="cuda")
+    buf = big[300:700]
     torch.cuda.synchronize()  # the zero fill lands before the peer process writes into buf
-    hd = (ctypes.c_ubyte * 64)()
+    hd = (ctypes.c_ubyte * 128)()
     assert lib.fc_ipc_handle(ctypes.c_void_p(buf.data_ptr()), hd) == _lib.OK
     a.send(bytes(hd))
     assert a.recv() == _lib.OK
@@ -94,6 +97,7 @@ def test_pool_to_peers_over_cuda_ipc():
     rows = np.random.default_rng(1).standard_normal((5000, 16)).astype(np.float32)
     got = buf.cpu().numpy()
     assert np.array_equal(got[10:310], rows[100:400]) and not got[:10].any()
+    assert not big[:300].cpu().numpy().any()  # nothing written at the allocation's base
 
 
 def test_row_sharded_peer_rows_nccl_world1_matches_dense():

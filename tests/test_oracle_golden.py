@@ -311,3 +311,31 @@ def test_mean_with_weights_rule():
     np.testing.assert_allclose(out[0], (0.5 * rows[0] + 2.0 * rows[1]) / 2)
     np.testing.assert_allclose(out[1], rows[3])
     np.testing.assert_allclose(out[2], 0.0)  # empty bag
+
+
+def test_golden_buffer_too_small_ordering():
+    """A row larger than the staging buffer, replayed against the REAL reference's
+    recorded outcome of every call: which calls raise BufferTooSmall, and the slot
+    table, dirty bits, free count and slow tier after each (a dirty write-back raises
+    before any mutation; clean victims are evicted before the admission raises)."""
+    from _replay import bts_calls
+
+    g = load_golden("buffer_too_small")
+    num_ids, cap, dim = (int(v) for v in g["meta"])
+    c = oracle.OracleCache(np.arange(num_ids), g["slow0"].copy(), cap)
+    for k, (verb, buf, wb, ids) in enumerate(bts_calls(g)):
+        c.buffer_bytes, c.write_back = buf, wb
+        raised = 0
+        try:
+            if verb == "flush":
+                c.flush()
+            else:
+                p = c.prepare(ids, k)
+                if verb == "update":
+                    c.scatter_update(p, np.full((ids.size, dim), 0.25, np.float32))
+        except oracle.OracleBufferTooSmall:
+            raised = 1
+        assert raised == g["raised"][k], k
+        assert np.array_equal(c.slot_rank, g["slot_to_rank"][k]), k
+        assert np.array_equal(c.dirty, g["dirty"][k]) and c.free == g["free_count"][k], k
+        assert np.array_equal(c.slow, g["slow"][k]), k
