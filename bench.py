@@ -55,6 +55,10 @@ CONFIGS = {
     # optimizer state cached and written back with its rows
     "stress": dict(num_ids=25_523_073, dim=128, ratio=0.005, alpha=None, batch=65536, features=1,
                    optimizer="adagrad"),
+    # BASELINE configs[3]: MLPerf DLRM Criteo-1TB shape, 26 tables capped at 40M rows (204,184,588 rows,
+    # TorchRec's MLPerf sizes), dim 128, 1.5% cache (3,062,768 slots), one global Zipf(1.05)
+    # law (the reference's model); the reference shards it column-wise (--shard column) at 2/4/8 GPUs
+    "criteo_1tb": dict(num_ids=204_184_588, dim=128, ratio=0.015, alpha=1.05, batch=16384, features=26),
 }
 SEED = 1
 UPDATES_SEED = 7
@@ -356,7 +360,7 @@ def rooflines(prof, pool_ms, N, D, links, engine="async", pipelined=False, psw=F
               "achieved": xfer_bytes / max(xfer_ms * 1e-3, 1e-12) / 1e9, "peak": peak, "unit": "GB/s",
               "traffic": ncu_traffic(kname), "traffic_note": "DRAM bytes only; the host-link bytes do not touch HBM",
               "algorithmic_bytes_per_launch": xfer_bytes, "launch_ms": xfer_ms,
-              "writeback_bytes_per_step": prof.get("writeback_bytes", 0) / max(prof["calls"], 1),
+              "writeback_d2h_bytes_per_step": prof.get("writeback_d2h_bytes", 0) / max(prof["calls"], 1),
               "peak_source": src}
     r_xfer["frac"] = r_xfer["achieved"] / r_xfer["peak"]
     out = [r_xfer]
@@ -375,6 +379,43 @@ def rooflines(prof, pool_ms, N, D, links, engine="async", pipelined=False, psw=F
     return out
 
 
+def workload_config(args, cfg, world):
+    """The workload both arms measure (identical dicts: the driver compares them)."""
+    D, B, F = cfg["dim"], cfg["batch"], cfg["features"]
+    shard = args.shard
+    return {"workload": args.config, "num_rows": cfg["num_ids"], "dim": D, "cache_ratio": cfg["ratio"],
+            "zipf_alpha": cfg["alpha"], "batch_per_gpu": B, "features": F, "lookups_per_step": B * F * world,
+            "pooling": cfg.get("mode", "sum") + (" with per-sample weights" if cfg.get("psw") else "") + ", bag size 1",
+            "optimizer": cfg.get("optimizer", "sgd"), "ids": "uniform" if cfg["alpha"] is None else f"zipf({cfg['alpha']})",
+            "step": ("forward (prepare + pooled gather) + backward/update" if args.step == "train"
+                     else "prepare + pooled forward + simulator row update"),
+            "write_back": "dirty_only", "evict_mode": "occupancy_aware",
+            "parallelism": "single" if shard is None else f"{shard}wise{world}",
+            "l2": "inputs larger than L2 (fast tier %d MB, id/rank maps %d MB, new batch every step)"
+                  % (fc_capacity(cfg) * D * 4 >> 20, cfg["num_ids"] * 12 >> 20)}
+
+
+def fc_capacity(cfg):
+    return max(1, int(cfg["ratio"] * cfg["num_ids"]))
+
+
+def trace_batches(args, world):
+    """Batches of B samples per rank in the generated trace (the frequency reorder scans all
+    of them; both arms generate the same trace for the same --steps/--warmup/--gpus)."""
+    return max(args.trace_batches // world, args.warmup + 2 * args.steps + 2 * KSTEPS + 2)
+
+
+def launches_per_step(args, shard_mode, pipelined, world):
+    """Our kernels launched per timed step (checked against the ncu launch lists in profiles/)."""
+    if shard_mode is None:
+        return ((KERNELS_PER_STEP if args.step == "sim" else KERNELS_PER_TRAIN_STEP)
+                + (PIPELINE_EXTRA_KERNELS if pipelined else 0))
+    if shard_mode == "column":  # synchronous prepare of the global batch + pool + fused backward (NCCL kernels not counted)
+        return KERNELS_PER_TRAIN_STEP
+    return (SHARDED_BASE_KERNELS + (PIPELINE_EXTRA_KERNELS if pipelined else 0) + (1 if world == 1 else 5)
+            + (1 if args.no_peer else 2))
+
+
 def run_ours(args, cfg, torch, rank, world):
     import paper_2208_05321_b200 as fc
     from paper_2208_05321_b200.embedding import CachedEmbeddingBag
@@ -384,12 +425,14 @@ def run_ours(args, cfg, torch, rank, world):
     W, K = args.warmup, args.steps
     D, B, F = cfg["dim"], cfg["batch"], cfg["features"]
     N = B * F
-    n_batches = max(args.trace_batches // world, W + 2 * K + 2 * KSTEPS + 2)
+    n_batches = trace_batches(args, world)
     # global batch = world x B samples; this rank's slice is rows [rank*B, (rank+1)*B) of each global batch
-    sharded = world > 1 or args.sharded
-    samples, rank_of, id_of, cap = make_workload(cfg, n_batches * world, device=dev, keep_counts=sharded)
+    shard_mode = args.shard
+    sharded = shard_mode is not None
+    rowwise = shard_mode == "row"
+    samples, rank_of, id_of, cap = make_workload(cfg, n_batches * world, device=dev, keep_counts=rowwise)
     counts = None
-    if sharded:
+    if rowwise:
         samples, counts = samples
     links = host_link_peaks(torch, dev)
     gout = make_grad(N, D, dev)
@@ -412,6 +455,18 @@ def run_ours(args, cfg, torch, rank, world):
                                  optimizer=OPT, lr=LR, slow_rows=rows, warmup=True, engine=args.engine)
         dcs = [mod.cache]
         shard = None
+    elif shard_mode == "column":
+        from paper_2208_05321_b200.distributed import ColumnShardedEmbedding, CudaShard
+
+        # the reference's column-wise split (sharding.py:46-118): every rank caches all rows of its
+        # column slice over the GLOBAL batch (identical decisions on every rank)
+        lo_c, hi_c = fc.partition_columns(D, world).ranges[rank]
+        rows = fc.store.pinned_empty((cfg["num_ids"], hi_c - lo_c))
+        fill_pinned(torch, rows, dev, SEED + rank)
+        shard = CudaShard(cfg["num_ids"], hi_c - lo_c, cap, rows, fc.IdxMap(rank_of, id_of), optimizer=OPT, lr=LR,
+                          device=dev, engine=args.engine)
+        mod = ColumnShardedEmbedding(shard, D, world, rank, mode=MODE, device=dev)
+        dcs = [shard.cache]
     else:
         from paper_2208_05321_b200.distributed import CudaShard, RowShardedEmbedding, shard_rows_for_rank
 
@@ -441,12 +496,14 @@ def run_ours(args, cfg, torch, rank, world):
 
     def step(s, timed):
         ids = bview[s]
-        if sharded:  # row-sharded training step: unique-id all-to-all, owner caches, row all-to-all
+        if sharded:  # sharded training step: id exchange, this rank's cache, row/activation exchange
             out = mod(ids, None, psw)
             if pipelined:  # next batch's id exchange + owner prepare overlap this backward
                 mod.prefetch(bview[s + 1], ready=ids_ready)
             out.backward(gout)
-            stats.append((0, 0, 0, 0, 0))
+            li = getattr(mod, "last_info", None)
+            stats.append((li.unique, li.hits, li.misses, li.evictions, li.rows_to_slow) if li is not None
+                         else (0, 0, 0, 0, 0))
             return
         if pipelined and depth2:  # batch s+1 begun before batch s is committed: its index phase
             dc.prepare_begin(bview[s + 1], s + 1, ready=ids_ready)  # starts when batch s's ends
@@ -471,7 +528,8 @@ def run_ours(args, cfg, torch, rank, world):
             pool_ms.append(e)
         stats.append((info.unique, info.hits, info.misses, info.evictions, info.rows_to_slow))
 
-    pipelined = args.engine == "async" and not args.no_prefetch
+    # the column-wise module has no lookahead (every rank prepares the all-gathered global batch)
+    pipelined = args.engine == "async" and not args.no_prefetch and shard_mode != "column"
     depth2 = args.prefetch_depth == 2 and not sharded and not os.environ.get("FC_XFER_AFTER_UPDATE")
     if pipelined and not sharded:
         dc.prepare_begin(bview[0], 0, ready=ids_ready)
@@ -489,6 +547,9 @@ def run_ours(args, cfg, torch, rank, world):
         ev[0].record(stream)
         for k in range(K):
             step(W + k, False)
+            if k == K - 1:  # the region ends when the async write-backs queued so far are in the slow tier
+                for c in dcs:
+                    c.drain_stream(stream)
             ev[k + 1].record(stream)
         torch.cuda.synchronize(dev)
     if world > 1:
@@ -620,20 +681,14 @@ def run_ours(args, cfg, torch, rank, world):
         "steps": K, "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "fp32 rows, int32 ids",
         "data": "synthetic: reference gen_zipf stream (seed 1), seeded rows",
-        "config": {"workload": args.config, "num_rows": cfg["num_ids"], "dim": D, "cache_ratio": cfg["ratio"],
-                   "capacity_per_gpu": cap, "zipf_alpha": cfg["alpha"], "batch_per_gpu": B, "features": F,
-                   "lookups_per_step": lookups,
-                   "pooling": MODE + (" with per-sample weights" if psw is not None else "") + ", bag size 1",
-                   "optimizer": OPT, "ids": "uniform" if cfg["alpha"] is None else f"zipf({cfg['alpha']})",
-                   "step": (f"forward (prepare + pooled gather) + fused backward/{OPT}" if args.step == "train"
-                            else "prepare + pooled forward + simulator row update"),
-                   "write_back": "dirty_only", "evict_mode": "occupancy_aware", "engine": args.engine,
-                   "prefetch": pipelined,
-                   "l2": "inputs larger than L2 (fast tier %d MB, id/rank maps %d MB, new batch every step)"
-                         % (cap * D * 4 >> 20, cfg["num_ids"] * 12 // world >> 20),
-                   "parallelism": "single" if not sharded else
-                   (f"rowwise{world} (unique ids by NCCL all-to-all; rows back "
-                    + ("by NCCL all-to-all)" if args.no_peer else "by owner-side peer-memory writes)"))},
+        "config": workload_config(args, cfg, world),
+        "implementation": {"engine": args.engine, "prefetch": pipelined,
+                           "prefetch_depth": (2 if depth2 else 1) if pipelined else 0,
+                           "exchange": (None if not rowwise else "unique ids by NCCL all-to-all; rows back "
+                                        + ("by NCCL all-to-all" if args.no_peer else "by owner-side peer-memory writes")
+                                        ) if shard_mode != "column" else
+                           "all-gather of ids; pooled columns by NCCL all-to-all (reference semantics)",
+                           "capacity_per_gpu": cap},
         "step_latency_ms": {"p50": float(np.percentile(step_ms, 50)), "p99": float(np.percentile(step_ms, 99)),
                             "prepare_avg": (None if pipelined else prof["prepare_ms"] / max(prof["calls"], 1)),
                             "miss_transfer_avg": rl[0]["launch_ms"] if rl[0]["bound"] == "host_link" else None,
@@ -649,16 +704,16 @@ def run_ours(args, cfg, torch, rank, world):
                 "path": "CachedEmbeddingBag.forward(pinned host ids) + out.backward(grad) (fused SGD); result = "
                         "prepare hit/miss counters read back" if not sharded
                 else "RowShardedEmbedding.forward(pinned host ids) + out.backward(grad)"},
-        "gpu_launches": (((KERNELS_PER_STEP if args.step == "sim" else KERNELS_PER_TRAIN_STEP)
-                          + (PIPELINE_EXTRA_KERNELS if pipelined else 0)) if not sharded else
-                         (SHARDED_BASE_KERNELS + (PIPELINE_EXTRA_KERNELS if pipelined else 0) + (1 if world == 1 else 5) + (1 if args.no_peer else 2))) * K,
+        "gpu_launches": launches_per_step(args, shard_mode, pipelined, world) * K,
         "roofline": rl[0], "roofline_secondary": rl[1] if len(rl) > 1 else None,
         "roofline_isolated": ({"note": "same kernels in synchronous steps (no prefetch overlap), after the "
                                        "timed region", **{r["kernel"]: r for r in rl_iso}} if rl_iso else None),
         "host_link": links,
         "clocks": clk.summary(),
     }
-    if not sharded:
+    if not rowwise:
+        if wb < 0:  # pipeline commits filter the dirty victims on device: the engine's exact count
+            wb = prof["writeback_rows"] / max(prof["scatter_jobs"], 1)
         res.update({"hit_ratio": hits / uniq, "unique_per_step": uniq, "misses_per_step": misses,
                     "evictions_per_step": evict, "writeback_rows_per_step": wb})
     return res, samples, rank_of, cap
@@ -684,6 +739,155 @@ def emit(doc):
         print(json.dumps(doc), flush=True)
 
 
+def reference_package():
+    """The UNMODIFIED reference package, installed into baseline/_ref by tools/install_reference.sh
+    (pip --target from /root/reference); None when it is absent (then the oracle port runs)."""
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "freqcache")) and ref not in sys.path:
+        sys.path.insert(0, ref)
+    try:
+        import freqcache  # noqa: F401
+        return freqcache
+    except ImportError:
+        return None
+
+
+def host_info():
+    """What the CPU numbers ran on (CPU model, cpu_count, thread counts)."""
+    model = None
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    threads = {"OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS"), "numpy": None}
+    try:
+        from threadpoolctl import threadpool_info
+        threads["numpy"] = {i.get("internal_api"): i.get("num_threads") for i in threadpool_info()}
+    except Exception:
+        pass
+    if "torch" in sys.modules:
+        threads["torch"] = sys.modules["torch"].get_num_threads()
+    return {"cpu_model": model, "cpu_count": os.cpu_count(), "threads": threads}
+
+
+def run_reference_arm(args, cfg, world, steps, warmup, time_budget_s=None):
+    """The reference's own CPU implementation of the path on this host: freqcache's CacheStack
+    (cache_manager.py:441-562) through its public API -- prepare -> gather (the bag-size-1 pooled
+    forward, x per-sample weight) -> scatter_update(-lr * grad) per step (or the simulator's
+    apply_unique_update for --step sim) -- on the same trace, reorder and sharding as the GPU arm:
+    one stack at N=1; at N>1 the reference's column-wise stacks (sharding.py:62-118, every shard
+    prepares the global batch, run one after another as shipped) or, for row-wise, one stack per
+    row shard (its id substream, its own reorder) run one after another. numpy is single-threaded
+    here, so it uses one core. Slow tiers are lazily zero-filled buffers (values do not change
+    the work). Returns (per-step seconds, steps timed, kind, sample note)."""
+    fq = reference_package()
+    if fq is None:  # not installed: the oracle port (oracle/) of the same loop
+        n_batches = trace_batches(args, world)
+        samples, rank_of, _, cap = make_workload(cfg, n_batches * world, device=None)
+        r = run_cpu_reference(samples, rank_of, cap, cfg, steps, warmup, args.step, batch_mult=world,
+                              time_budget_s=time_budget_s)
+        return r["step_s"], r["steps"], "port", "numpy oracle restatement of the reference (oracle/)"
+    from freqcache import cache_manager as rcm
+    from freqcache import freq_stats as rfs
+    from freqcache import sharding as rsh
+    from freqcache import simulator as rsim
+    from freqcache import store as rst
+    from freqcache import transmitter as rtx
+    from freqcache import workload as rwl
+
+    D, B, F = cfg["dim"], cfg["batch"], cfg["features"]
+    nb = trace_batches(args, world)
+    t0 = time.perf_counter()
+    if cfg["alpha"] is None:  # the reference has no uniform generator: the same seeded draw as the GPU arm
+        from paper_2208_05321_b200 import workload as wl
+        samples = wl.gen_uniform(cfg["num_ids"], nb * world * B, F, SEED).samples
+    else:
+        samples = rwl.gen_zipf(cfg["num_ids"], cfg["alpha"], nb * world * B, F, SEED).samples
+    counts = rfs.scan_frequencies(samples, cfg["num_ids"]).counts
+    log(f"[bench/ref] trace + reorder inputs in {time.perf_counter() - t0:.1f}s")
+
+    def stack(num_rows, width, idx_map):
+        cap = rst.fast_capacity(num_rows, cfg["ratio"])
+        st = rcm.CacheStack(idx_map=idx_map, slow=rst.SlowTierStore(rows=np.empty((num_rows, width), np.float32)),
+                            fast=rst.FastTierStore(slots=np.zeros((cap, width), np.float32)),
+                            transmitter=rtx.Transmitter())
+        st.warmup(cap)  # simulator.py:393-394
+        return st
+
+    shard = args.shard
+    if shard == "row":  # one stack per row shard: ids with id % world == r, rank-local reorder
+        stacks = []
+        for r in range(world):
+            stacks.append(stack(len(counts[r::world]), D,
+                                rfs.build_reorder(rfs.FrequencyTable(counts=counts[r::world],
+                                                                     num_ids=len(counts[r::world])))))
+        def parts(ids):
+            return [(st, ids[m] // world, m, (0, D)) for st, m in zip(stacks, [ids % world == r for r in range(world)])]
+    else:
+        idx = rfs.build_reorder(rfs.FrequencyTable(counts=counts, num_ids=cfg["num_ids"]))
+        plan = rsh.partition_columns(D, world if shard == "column" else 1)
+        stacks = [stack(cfg["num_ids"], e - s, idx) for s, e in plan.ranges]
+
+        def parts(ids):
+            return [(st, ids, None, cr) for st, cr in zip(stacks, plan.ranges)]
+    log(f"[bench/ref] {len(stacks)} reference stack(s) ready in {time.perf_counter() - t0:.1f}s")
+    n = B * F * world
+    gout = make_grad(n, D)
+    psw = None
+    if cfg.get("psw"):
+        psw = np.random.default_rng(SEED + 2).random(n, dtype=np.float32)
+        gout = gout * psw[:, None]
+    colw = rsim.update_column_weights(D, UPDATES_SEED)
+    times = []
+    t_start = time.perf_counter()
+    for s in range(warmup + steps):
+        ids = samples[s * world * B:(s + 1) * world * B].reshape(-1).astype(np.int64)
+        t = time.perf_counter()
+        for st, sub, m, (lo, hi) in parts(ids):
+            prep = st.prepare(sub, s)
+            rows = st.gather(prep)  # pooled forward, bag size 1
+            if psw is not None:
+                rows *= (psw if m is None else psw[m])[:, None]
+            if args.step == "train":
+                st.scatter_update(prep, -LR * (gout if m is None else gout[m])[:, lo:hi])
+            else:
+                g = rsim.update_row_scalars(prep.unique_ids, prep.unique_counts, s, UPDATES_SEED)
+                st.apply_unique_update(prep, g[:, None] * colw[None, lo:hi])
+        dt = time.perf_counter() - t
+        if s >= warmup:
+            times.append(dt)
+        if time_budget_s and time.perf_counter() - t_start > time_budget_s and len(times) >= 2:
+            break
+    note = (f"{len(times)} steps of {n} lookups after {warmup} warm-up steps, reference freqcache "
+            f"{getattr(fq, '__version__', '?')} from baseline/_ref ({len(stacks)} stack(s), run in sequence)")
+    return float(np.mean(times)), len(times), "reference", note
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` outside torchrun: re-launch under torch.distributed.run with one rank
+    per GPU (rendezvous on 127.0.0.1); fails loudly when the box has fewer GPUs."""
+    import socket
+
+    import torch
+
+    have = torch.cuda.device_count()
+    if have < args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus}: only {have} CUDA device(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    log("[bench] spawning: " + " ".join(cmd))
+    sys.stdout.flush()
+    if _STDOUT is not None:
+        os.dup2(_STDOUT, 1)  # the ranks print the JSON line to the real stdout
+    os.execv(sys.executable, cmd)
+
+
 def main():
     quiet_stdout()
     ap = argparse.ArgumentParser()
@@ -693,12 +897,15 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="criteo_kaggle", choices=list(CONFIGS))
     ap.add_argument("--step", default="train", choices=["train", "sim"])
+    ap.add_argument("--shard", default=None, choices=["row", "column"],
+                    help="table split over the ranks: row (id %% N owners, the scaling variant; default at N>1) "
+                         "or column (the reference's column-wise split, sharding.py:46-118)")
     ap.add_argument("--trace-batches", type=int, default=64)
-    ap.add_argument("--cpu-baseline-steps", type=int, default=8)
+    ap.add_argument("--cpu-baseline-s", type=float, default=20.0, help="time budget of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prefetch-depth", type=int, default=2, choices=[1, 2],
                     help="2: batch t+1's prefetch is begun before batch t is committed (default)")
-    ap.add_argument("--sharded", action="store_true", help="row-sharded module even at one GPU (needs torchrun)")
+    ap.add_argument("--sharded", action="store_true", help="alias of --shard row (also at one GPU)")
     ap.add_argument("--no-peer", action="store_true",
                     help="row-sharded runs: return rows with NCCL all-to-all instead of peer-memory writes")
     ap.add_argument("--no-prefetch", action="store_true",
@@ -708,47 +915,47 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.sharded and args.shard is None:
+        args.shard = "row"
+    if args.gpus > 1 and args.shard is None:
+        args.shard = "row"
     cfg = CONFIGS[args.config]
     rank = int(os.environ.get("RANK", 0))
-    world = int(os.environ.get("WORLD_SIZE", 1))
+    env_world = os.environ.get("WORLD_SIZE")
+    world = int(env_world) if env_world is not None else args.gpus
+    if env_world is not None and args.gpus != 1 and int(env_world) != args.gpus:
+        raise SystemExit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={env_world}")
 
-    if args.impl == "reference":
+    if args.impl == "reference":  # rank 0 alone runs the reference's CPU path; the others exit
         if rank != 0:
             return 0
-        n_batches = max(args.trace_batches // world, args.warmup + 2 * args.steps)
-        samples, rank_of, _, cap = make_workload(cfg, n_batches * world, device=None)
-        r = run_cpu_reference(samples, rank_of, cap, cfg, args.steps, args.warmup, args.step, batch_mult=world)
+        step_s, nsteps, kind, note = run_reference_arm(args, cfg, world, args.steps, args.warmup,
+                                                       time_budget_s=float(os.environ.get("FC_REF_BUDGET_S", "150")))
         n = cfg["batch"] * cfg["features"] * world
-        out = {"metric": METRIC, "value": r["lookups_per_s"], "unit": "lookups/s", "n_gpus": world,
-               "steps": r["steps"], "warmup": args.warmup, "ms_per_step": r["step_s"] * 1e3,
-               "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp32 rows, int32 ids",
-               "data": "synthetic: reference gen_zipf stream (seed 1)", "impl": "reference",
-               "config": {"workload": args.config, "num_rows": cfg["num_ids"], "dim": cfg["dim"],
-                          "capacity": cap, "batch": cfg["batch"] * world, "features": cfg["features"],
-                          "lookups_per_step": n,
-                          "step": "prepare + gather + scatter_update(-lr*grad)" if args.step == "train"
-                          else "prepare + gather + apply_unique_update (simulator.py:419-433)"},
-               "cpu_baseline": {"value": r["lookups_per_s"], "unit": "lookups/s", "cores": 1, "kind": "port",
-                                "sample": f"{r['steps']} batches of {n} ids after {args.warmup} warm-up batches; "
-                                          "numpy oracle restatement of the reference (single-threaded numpy)"},
-               "e2e": {"value": r["lookups_per_s"], "unit": "lookups/s", "h2d_bytes_per_step": 0,
-                       "d2h_bytes_per_step": 0}}
-        emit(out)
+        val = n / step_s
+        emit({"metric": METRIC, "value": val, "unit": "lookups/s", "n_gpus": world, "steps": nsteps,
+              "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+              "vs_baseline": None, "dtype": "fp32 rows, int64 ids", "data": "synthetic: reference gen_zipf stream (seed 1)",
+              "impl": "reference", "config": workload_config(args, cfg, world),
+              "cpu_baseline": {"value": val, "unit": "lookups/s", "cores": 1, "kind": kind, "sample": note,
+                               **host_info()},
+              "e2e": {"value": val, "unit": "lookups/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
         return 0
 
+    if env_world is None and args.shard is not None:
+        spawn_ranks(args)  # does not return
     import torch
 
-    if world > 1 or args.sharded:
+    if args.shard is not None:
         torch.distributed.init_process_group("nccl", device_id=torch.device("cuda", int(os.environ.get("LOCAL_RANK", 0))))
     torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", 0)))
     # a dedicated (non-legacy) stream: no implicit serialisation with the engine's side stream
     with torch.cuda.stream(torch.cuda.Stream()):
-        res, samples, rank_of, cap = run_ours(args, cfg, torch, rank, world)
+        res = run_ours(args, cfg, torch, rank, world)[0]
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = run_cpu_reference(samples, rank_of, cap, cfg, args.cpu_baseline_steps, 2, args.step, time_budget_s=30)
-        res["cpu_baseline"] = {"value": r["lookups_per_s"], "unit": "lookups/s", "cores": 1, "kind": "port",
-                               "sample": f"{r['steps']} batches after 2 warm-up batches of the same trace; "
-                                         "numpy oracle port (same step), single-threaded"}
+        step_s, nsteps, kind, note = run_reference_arm(args, cfg, 1, 8, 2, time_budget_s=args.cpu_baseline_s)
+        res["cpu_baseline"] = {"value": cfg["batch"] * cfg["features"] / step_s, "unit": "lookups/s", "cores": 1,
+                               "kind": kind, "sample": note, **host_info()}
     if rank == 0:
         emit(res)
     if torch.distributed.is_initialized():

@@ -117,15 +117,19 @@ int64_t fc_free_count(fc_cache* h);
  * rank is still pending). The slow tier is current after fc_flush / fc_drain. */
 int fc_set_engine(fc_cache* h, int32_t engine);
 int fc_drain(fc_cache* h);
+/* fc_drain as a stream-ordered wait: work queued on `stream` after this call runs once every
+ * write-back queued so far has landed in the slow tier; the host does not block. */
+int fc_drain_stream(fc_cache* h, void* stream);
 
 /* Measurement hook (no reference counterpart): with enable=1 every prepare records
  * CUDA events around the whole call and around the host-link transfer kernel.
- * out[0..4] (returned, then reset): sum prepare ms, sum transfer-kernel ms,
- * calls, bytes the transfer kernel moved over the host link (4*dim*(admitted +
- * written-back rows) for engine 0, admitted rows only for engine 1),
- * written-back bytes, host ms spent waiting for async write-backs (engine 1),
- * host scatter ms and scatter jobs completed (engine 1), transfer launches timed
- * (prefetch pipeline: out[1] covers k_admit_stage). `out` holds 9 doubles. */
+ * out (returned, then reset): [0] sum prepare ms, [1] sum transfer-kernel ms, [2] calls,
+ * [3] bytes the transfer kernel moved over the host link (4*(dim+state)*(admitted +
+ * written-back rows) for engine 0, admitted rows only for engine 1), [4] victim bytes
+ * (upper bound of the write-back), [5] host ms spent waiting for async write-backs,
+ * [6] host scatter ms and [7] scatter jobs completed (engine 1), [8] transfer launches
+ * timed (prefetch pipeline: [1] covers k_admit_stage), [9] rows written back to the slow
+ * tier and [10] bytes shipped device -> host for them (engine 1, exact). `out` holds 11 doubles. */
 int fc_profile(fc_cache* h, int32_t enable, double* out);
 
 /* Timeline tracing (diagnostics, no reference counterpart): while enabled the

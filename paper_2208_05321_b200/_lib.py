@@ -12,6 +12,8 @@ import os
 from ctypes import POINTER, c_char_p, c_float, c_int32, c_int64, c_uint64, c_void_p
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libfreqcache_b200.so")
+# A/B measurements only: another in-tree build of the same ABI (tools/build_ab.sh)
+LIB_PATH = os.environ.get("FC_LIB_PATH", LIB_PATH)
 
 # fc_status (include/freqcache_b200.h)
 OK = 0
@@ -61,6 +63,7 @@ _SIGS = {
     "fc_profile": (c_int32, [c_void_p, c_int32, c_void_p]),
     "fc_set_engine": (c_int32, [c_void_p, c_int32]),
     "fc_drain": (c_int32, [c_void_p]),
+    "fc_drain_stream": (c_int32, [c_void_p, c_void_p]),
     "fc_warmup": (c_int32, [c_void_p, c_int64, c_void_p]),
     "fc_prepare": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                              c_void_p, c_void_p, c_void_p, POINTER(PrepareInfo)]),
@@ -119,6 +122,8 @@ def load():
             "(the cache has no CPU fallback)")
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in _SIGS.items():
+        if "FC_LIB_PATH" in os.environ and not hasattr(lib, name):
+            continue  # an older A/B build may lack newer entry points
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

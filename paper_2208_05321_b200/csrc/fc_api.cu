@@ -295,6 +295,12 @@ int fc_drain(fc_cache* h) {
   return engine_drain(h);
 }
 
+int fc_drain_stream(fc_cache* h, void* stream) {
+  if (!h) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  return engine_drain_stream(h, as_stream(stream));
+}
+
 int fc_set_idx_map(fc_cache* h, const int64_t* rank_of_host, void* stream) {
   if (!h || !rank_of_host) return FC_ERR_BAD_ARG;
   DeviceGuard dg(h->device);
@@ -528,8 +534,13 @@ int fc_profile(fc_cache* h, int32_t enable, double* out) {
   DeviceGuard dg(h->device);
   if (out) {
     for (int i = 0; i < 6; ++i) out[i] = h->prof[i];
-    engine_stats(h, out + 6);
+    double es[4];
+    engine_stats(h, es);
+    out[6] = es[0];
+    out[7] = es[1];
     out[8] = h->prof[6];
+    out[9] = es[2];
+    out[10] = es[3];
   }
   if (enable && !h->profile) {
     for (int i = 0; i < 4; ++i) FC_CUDA(cudaEventCreate(&h->pev[i]));

@@ -57,8 +57,11 @@ constexpr int kWbBufs = 3;
 
 struct Job {
   int buf;
-  int64_t rows;
+  int64_t rows;      // -1: a pipeline commit's count is on device (d2h[buf] brings it back)
   uint64_t seq;
+  int64_t victims = 0;  // pipeline commit: rows the stage may hold (every victim)
+  bool shipped = false; // pipeline commit: all `victims` rows already queued D2H behind the commit
+  bool copied = false;  // the copier issued the rows' D2H itself (cev[buf] marks its end)
 };
 
 struct AsyncWB {
@@ -77,7 +80,9 @@ struct AsyncWB {
   bool rows_on_dev[kWbBufs] = {};          // the exact count is dev_rows[b]
   uint64_t seq_of[kWbBufs] = {};           // job sequence number using each buffer
   cudaStream_t side = nullptr;
+  cudaStream_t dside = nullptr;            // the dispatcher's own D2H stream (exact-size write-back copies)
   cudaEvent_t d2h[kWbBufs] = {};
+  cudaEvent_t cev[kWbBufs] = {};           // end of the copier's exact-size D2H of a buffer's job
   int cur = 0;
   int device = 0;
   bool vec = true;                         // rows move as 16-byte units (dim % 4 == 0, aligned)
@@ -85,11 +90,16 @@ struct AsyncWB {
   // FIFO scatter jobs, one dispatcher + helpers
   std::mutex m;
   std::condition_variable cv_q, cv_done, cv_help, cv_helped;
-  std::deque<Job> q;
+  std::deque<Job> q;       // jobs whose rows are (being) copied, in order: the dispatcher scatters them
+  std::deque<Job> qc;      // jobs in commit order: the copier ships their rows D2H
+  std::condition_variable cv_qc;
   uint64_t next_seq = 1, done_seq = 0, started_seq = 0;
   std::condition_variable cv_started;
   bool stop = false;
+  bool copier_done = false;  // the copier has exited (everything it queued is in q)
+  bool helpers_stop = false; // set after the dispatcher has exited
   std::thread dispatcher;
+  std::thread copier;
   std::vector<std::thread> helpers;
   // parallel-for state
   uint64_t gen = 0;
@@ -102,19 +112,26 @@ struct AsyncWB {
   fc_cache* h = nullptr;
   double scatter_ms = 0;  // host scatter time (stats, under m)
   int64_t jobs_done = 0;
+  double dirty_frac = 1.0;  // recent dirty share of the victims (pipeline commits; under m)
+  int64_t rows_done = 0;  // rows written back to the slow tier (stats, under m)
+  int64_t d2h_bytes = 0;  // bytes shipped device -> host for them (stats, under m)
 };
 
 void engine_stats(fc_cache* h, double* out) {
   AsyncWB* a = h->awb;
   if (!a) {
-    out[0] = out[1] = 0;
+    out[0] = out[1] = out[2] = out[3] = 0;
     return;
   }
   std::lock_guard<std::mutex> lk(a->m);
   out[0] = a->scatter_ms;
   out[1] = (double)a->jobs_done;
+  out[2] = (double)a->rows_done;
+  out[3] = (double)a->d2h_bytes;
   a->scatter_ms = 0;
   a->jobs_done = 0;
+  a->rows_done = 0;
+  a->d2h_bytes = 0;
 }
 
 
@@ -152,8 +169,8 @@ static void helper_main(AsyncWB* a) {
   uint64_t seen = 0;
   std::unique_lock<std::mutex> lk(a->m);
   while (true) {
-    a->cv_help.wait(lk, [&] { return a->stop || a->gen != seen; });
-    if (a->stop) return;
+    a->cv_help.wait(lk, [&] { return a->helpers_stop || a->gen != seen; });
+    if (a->gen == seen) return;  // helpers_stop and no new work
     seen = a->gen;
     lk.unlock();
     scatter_range(a);
@@ -162,22 +179,64 @@ static void helper_main(AsyncWB* a) {
   }
 }
 
+// Copier: jobs in commit order. A pipeline commit's dirty filter ran on device and only
+// its row count came back (d2h[buf]); the copier then ships exactly those rows -- not
+// every victim -- on its own stream, so job j+1's copy overlaps job j's host scatter.
+static void copier_main(AsyncWB* a) {
+  cudaSetDevice(a->device);
+  fc_cache* h = a->h;
+  std::unique_lock<std::mutex> lk(a->m);
+  while (true) {
+    a->cv_qc.wait(lk, [&] { return a->stop || !a->qc.empty(); });
+    if (a->stop && a->qc.empty()) {
+      a->copier_done = true;
+      a->cv_q.notify_all();
+      return;
+    }
+    Job j = a->qc.front();
+    a->qc.pop_front();
+    lk.unlock();
+    const auto tw = std::chrono::steady_clock::now();
+    cudaEventSynchronize(a->d2h[j.buf]);  // the staged rows (sync prepare) or their count (pipeline) are in pinned memory
+    slow_wait_note("copier: write-back count / D2H event", tw);
+    if (j.rows < 0) {
+      const int b = j.buf;
+      j.rows = a->hrows[b];
+      if (j.rows > 0 && !j.shipped) {
+        cudaMemcpyAsync(a->hranks[b], a->sranks[b], (size_t)j.rows * 4, cudaMemcpyDeviceToHost, a->dside);
+        cudaMemcpyAsync(a->hstage[b], a->stage[b], (size_t)j.rows * h->dim * 4, cudaMemcpyDeviceToHost, a->dside);
+        if (h->sw)
+          cudaMemcpyAsync(a->hsstage[b], a->sstage[b], (size_t)j.rows * h->sw * 4, cudaMemcpyDeviceToHost, a->dside);
+        cudaEventRecord(a->cev[b], a->dside);
+        j.copied = true;
+      }
+    }
+    lk.lock();
+    if (j.victims > 0) a->dirty_frac = 0.75 * a->dirty_frac + 0.25 * (double)j.rows / (double)j.victims;
+    a->started_seq = j.seq;  // d2h[j.buf] / hrows[j.buf] may be re-recorded from here on
+    a->cv_started.notify_all();
+    a->q.push_back(j);
+    a->cv_q.notify_one();
+  }
+}
+
 static void dispatcher_main(AsyncWB* a) {
   cudaSetDevice(a->device);
   std::unique_lock<std::mutex> lk(a->m);
   while (true) {
-    a->cv_q.wait(lk, [&] { return a->stop || !a->q.empty(); });
-    if (a->stop && a->q.empty()) return;
+    a->cv_q.wait(lk, [&] { return a->copier_done || !a->q.empty(); });
+    if (a->copier_done && a->q.empty()) return;
     Job j = a->q.front();
     a->q.pop_front();
     lk.unlock();
-    const auto tw = std::chrono::steady_clock::now();
-    cudaEventSynchronize(a->d2h[j.buf]);  // the staged rows are in pinned memory
-    slow_wait_note("dispatcher: write-back D2H event", tw);
-    if (j.rows < 0) j.rows = a->hrows[j.buf];  // pipeline commit: count known only on device
+    if (j.copied) {
+      const auto tw = std::chrono::steady_clock::now();
+      cudaEventSynchronize(a->cev[j.buf]);
+      slow_wait_note("dispatcher: write-back D2H", tw);
+    }
     lk.lock();
-    a->started_seq = j.seq;  // d2h[j.buf] / hrows[j.buf] may be re-recorded from here on
-    a->cv_started.notify_all();
+    a->rows_done += j.rows;
+    if (!j.shipped) a->d2h_bytes += j.rows * (4 + 4 * (int64_t)(a->h->dim + a->h->sw));
     a->src = a->hstage[j.buf];
     a->ssrc = a->hsstage[j.buf];
     a->ranks = a->hranks[j.buf];
@@ -418,6 +477,9 @@ int engine_set(fc_cache* h, int engine) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a->d2h[b], cudaEventDisableTiming | cudaEventBlockingSync);
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->side, cudaStreamNonBlocking);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->dside, cudaStreamNonBlocking);
+  for (int b = 0; b < kWbBufs && e == cudaSuccess; ++b)
+    e = cudaEventCreateWithFlags(&a->cev[b], cudaEventDisableTiming | cudaEventBlockingSync);
   if (e == cudaSuccess) e = cudaMalloc(&a->dev_rows, kWbBufs * sizeof(int32_t));
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&a->done_host, 64, cudaHostAllocMapped);
   if (e == cudaSuccess) {
@@ -437,6 +499,7 @@ int engine_set(fc_cache* h, int engine) {
   if (const char* env = std::getenv("FC_SCATTER_THREADS")) nh = std::max(0, std::atoi(env) - 1);
   for (int i = 0; i < nh; ++i) a->helpers.emplace_back(helper_main, a);
   a->dispatcher = std::thread(dispatcher_main, a);
+  a->copier = std::thread(copier_main, a);
   h->engine = 1;
   return FC_OK;
 }
@@ -529,10 +592,10 @@ int engine_after_prepare(fc_cache* h, cudaStream_t st) {
     {
       std::lock_guard<std::mutex> lk(a->m);
       const uint64_t seq = a->next_seq++;
-      a->q.push_back(Job{b, rows, seq});
+      a->qc.push_back(Job{b, rows, seq});
       a->seq_of[b] = seq;
     }
-    a->cv_q.notify_one();
+    a->cv_qc.notify_one();
     a->rows_in[b] = rows;
     a->cur = (a->cur + 1) % kWbBufs;
   }
@@ -551,6 +614,24 @@ int engine_drain(fc_cache* h) {
   return FC_OK;
 }
 
+// The same drain as a stream-ordered wait: work queued on `st` after this call starts only
+// once every write-back queued so far has landed in the slow tier (no host block).
+int engine_drain_stream(fc_cache* h, cudaStream_t st) {
+  if (h->engine != 1 || !h->awb) return FC_OK;
+  AsyncWB* a = h->awb;
+  uint64_t last;
+  {
+    std::lock_guard<std::mutex> lk(a->m);
+    last = a->next_seq - 1;
+    if (a->done_seq >= last) return FC_OK;
+  }
+  WaitValueFn wv = wait_value_fn();
+  if (!wv || wv(reinterpret_cast<CUstream>(st), a->done_dev, (cuuint32_t)last, CU_STREAM_WAIT_VALUE_GEQ) !=
+                 CUDA_SUCCESS)
+    wait_seq(a, last);
+  return FC_OK;
+}
+
 void engine_release(fc_cache* h) {
   AsyncWB* a = h->awb;
   if (!a) return;
@@ -558,9 +639,14 @@ void engine_release(fc_cache* h) {
     std::lock_guard<std::mutex> lk(a->m);
     a->stop = true;
   }
-  a->cv_q.notify_all();
+  a->cv_qc.notify_all();
+  if (a->copier.joinable()) a->copier.join();  // drains its queue into the dispatcher's, then sets copier_done
+  if (a->dispatcher.joinable()) a->dispatcher.join();  // scatters what is left
+  {
+    std::lock_guard<std::mutex> lk(a->m);
+    a->helpers_stop = true;
+  }
   a->cv_help.notify_all();
-  if (a->dispatcher.joinable()) a->dispatcher.join();
   for (auto& t : a->helpers)
     if (t.joinable()) t.join();
   cudaFree(a->pending);
@@ -577,6 +663,9 @@ void engine_release(fc_cache* h) {
     if (a->d2h[b]) cudaEventDestroy(a->d2h[b]);
   }
   if (a->side) cudaStreamDestroy(a->side);
+  if (a->dside) cudaStreamDestroy(a->dside);
+  for (int b = 0; b < kWbBufs; ++b)
+    if (a->cev[b]) cudaEventDestroy(a->cev[b]);
   delete a;
   h->awb = nullptr;
 }
@@ -1288,22 +1377,40 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
       a->cv_started.wait(lk, [&] { return a->started_seq >= a->seq_of[b]; });
       slow_wait_note("commit: previous write-back job on this stage to start", tw1);
     }
+    // The dirty filter ran on device: the host learns the write-back count W only when the
+    // commit has run. While most victims come back dirty (training: every victim was just
+    // updated) the whole victim stage is queued D2H right behind the commit, with no host
+    // round trip; once they are mostly clean (inference, read-mostly phases) only the count
+    // comes back here and the copier thread ships exactly W rows. Either way the host
+    // scatters exactly W rows. FC_WB_EXACT=1 always takes the exact path.
+    static const int exact_env = std::getenv("FC_WB_EXACT") ? std::atoi(std::getenv("FC_WB_EXACT")) : -1;
+    bool ship_all;
+    {
+      std::lock_guard<std::mutex> lk(a->m);
+      ship_all = exact_env == -1 ? a->dirty_frac >= 0.5 : exact_env == 0;
+    }
     FC_CUDA(cudaStreamWaitEvent(a->side, q->ev_commit[p], 0));
     FC_CUDA(cudaMemcpyAsync(a->hrows + b, a->dev_rows + b, sizeof(int32_t), cudaMemcpyDeviceToHost, a->side));
-    FC_CUDA(cudaMemcpyAsync(a->hranks[b], a->sranks[b], (size_t)c.needed * 4, cudaMemcpyDeviceToHost, a->side));
-    FC_CUDA(cudaMemcpyAsync(a->hstage[b], a->stage[b], (size_t)c.needed * h->dim * 4, cudaMemcpyDeviceToHost,
-                            a->side));
-    if (h->sw)
-      FC_CUDA(cudaMemcpyAsync(a->hsstage[b], a->sstage[b], (size_t)c.needed * h->sw * 4, cudaMemcpyDeviceToHost,
+    if (ship_all) {
+      FC_CUDA(cudaMemcpyAsync(a->hranks[b], a->sranks[b], (size_t)c.needed * 4, cudaMemcpyDeviceToHost, a->side));
+      FC_CUDA(cudaMemcpyAsync(a->hstage[b], a->stage[b], (size_t)c.needed * h->dim * 4, cudaMemcpyDeviceToHost,
                               a->side));
+      if (h->sw)
+        FC_CUDA(cudaMemcpyAsync(a->hsstage[b], a->sstage[b], (size_t)c.needed * h->sw * 4, cudaMemcpyDeviceToHost,
+                                a->side));
+    }
     FC_CUDA(cudaEventRecord(a->d2h[b], a->side));
     {
       std::lock_guard<std::mutex> lk(a->m);
       const uint64_t seq = a->next_seq++;
-      a->q.push_back(Job{b, -1, seq});
+      Job j{b, -1, seq};
+      j.victims = c.needed;
+      j.shipped = ship_all;
+      a->qc.push_back(j);
       a->seq_of[b] = seq;
+      a->d2h_bytes += ship_all ? c.needed * (4 + 4 * (int64_t)(h->dim + h->sw)) : 0;
     }
-    a->cv_q.notify_one();
+    a->cv_qc.notify_one();
     a->rows_in[b] = c.needed;
     a->rows_on_dev[b] = true;
     a->cur = (a->cur + 1) % kWbBufs;

@@ -146,8 +146,9 @@ int engine_evict(fc_cache* h, cudaStream_t st);              // replaces k_evict
 int engine_admit(fc_cache* h, cudaStream_t st);              // replaces k_transfer_rows
 int engine_after_prepare(fc_cache* h, cudaStream_t st);      // after the prepare's sync
 int engine_drain(fc_cache* h);                               // all write-backs landed in the slow tier
+int engine_drain_stream(fc_cache* h, cudaStream_t st);       // the same, as a wait on `st`
 void engine_release(fc_cache* h);
-void engine_stats(fc_cache* h, double* out);                 // host scatter ms, jobs (then reset)
+void engine_stats(fc_cache* h, double* out);                 // host scatter ms, jobs, rows, D2H bytes (then reset)
 // prefetch pipeline (fc_engine.cu)
 int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt, int32_t* uranks,
                int32_t* uslots, int32_t* inverse, cudaStream_t st);

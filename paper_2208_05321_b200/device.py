@@ -117,13 +117,21 @@ class DeviceCache:
         """Wait until every queued write-back has landed in the slow tier."""
         check(self.lib.fc_drain(self.h))
 
+    def drain_stream(self, stream=None) -> None:
+        """A stream-ordered drain: later work on `stream` (default: current) runs once every
+        queued write-back has landed in the slow tier."""
+        s = self.stream() if stream is None else ctypes.c_void_p(stream.cuda_stream)
+        if getattr(self.lib, "fc_drain_stream", None) is None:  # an older A/B build (FC_LIB_PATH)
+            return
+        check(self.lib.fc_drain_stream(self.h, s))
+
     def profile(self, enable: bool) -> dict:
         """Toggle per-kernel CUDA-event timing; returns (and resets) the totals so far."""
-        out = (ctypes.c_double * 9)()
+        out = (ctypes.c_double * 11)()
         check(self.lib.fc_profile(self.h, int(bool(enable)), out))
         return {"prepare_ms": out[0], "transfer_ms": out[1], "calls": int(out[2]), "host_link_bytes": out[3],
-                "writeback_bytes": out[4], "host_wait_ms": out[5], "scatter_ms": out[6], "scatter_jobs": int(out[7]),
-                "transfer_launches": int(out[8])}
+                "victim_bytes": out[4], "host_wait_ms": out[5], "scatter_ms": out[6], "scatter_jobs": int(out[7]),
+                "transfer_launches": int(out[8]), "writeback_rows": int(out[9]), "writeback_d2h_bytes": out[10]}
 
     def trace(self, enable: bool) -> None:
         """Timeline tracing of the pipeline (fc_trace)."""

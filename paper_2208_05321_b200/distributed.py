@@ -548,12 +548,20 @@ class ColumnShardedEmbedding(torch.nn.Module):
         self.device = device if device is not None else getattr(shard, "device", torch.device("cpu"))
         self._anchor = torch.nn.Parameter(torch.empty(0, device=self.device))
 
+    # the two collectives of the column-wise exchange (overridable: the tests drive the module
+    # over a CPU-only process group by staging these through host memory)
+    def _allgather(self, out, inp):
+        dist.all_gather_into_tensor(out, inp, group=self.group)
+
+    def _alltoall(self, out, inp, out_splits, in_splits):
+        _a2a(out, inp, out_splits, in_splits, self.group)
+
     def _gather_var(self, x, counts, maxn):
         """all-gather of per-rank 1-D tensors of different lengths (padded to maxn)."""
         pad = torch.zeros(maxn, dtype=x.dtype, device=x.device)
         pad[:x.numel()] = x
         g = torch.empty(self.world * maxn, dtype=x.dtype, device=x.device)
-        dist.all_gather_into_tensor(g, pad, group=self.group)
+        self._allgather(g, pad)
         if all(c == maxn for c in counts):
             return g
         return torch.cat([g[r * maxn:r * maxn + c] for r, c in enumerate(counts)])
@@ -562,24 +570,25 @@ class ColumnShardedEmbedding(torch.nn.Module):
         W, n = self.world, ids.numel()
         cnt = torch.tensor([n], dtype=torch.int64, device=ids.device)
         all_n = torch.empty(W, dtype=torch.int64, device=ids.device)
-        dist.all_gather_into_tensor(all_n, cnt, group=self.group)
+        self._allgather(all_n, cnt)
         counts = all_n.tolist()
         maxn = max(counts)
         g_ids = self._gather_var(ids.contiguous(), counts, maxn)
         g_off, g_psw = None, None
         if offsets is not None:  # every rank has n_bags bags; shift offsets by the ids before it
             g_off = torch.empty(W * n_bags, dtype=offsets.dtype, device=offsets.device)
-            dist.all_gather_into_tensor(g_off, offsets[:n_bags].contiguous(), group=self.group)
+            self._allgather(g_off, offsets[:n_bags].contiguous())
             base = torch.tensor(np.concatenate([[0], np.cumsum(counts)[:-1]]), dtype=offsets.dtype,
                                 device=offsets.device)
             g_off += base.repeat_interleave(n_bags)
         if psw is not None:
             g_psw = self._gather_var(psw.contiguous(), counts, maxn)
         h = self.shard.prepare(g_ids)  # identical decisions on every rank
+        self.last_info = h.get("info") if isinstance(h, dict) else None
         pooled = self.shard.pool(h, g_off, W * n_bags, False, g_psw, self.mode)  # [W*n_bags, w_r]
         w_r = self.widths[self.rank]
         recv = torch.empty(sum(n_bags * w for w in self.widths), dtype=pooled.dtype, device=pooled.device)
-        _a2a(recv, pooled.reshape(-1).contiguous(), [n_bags * w for w in self.widths], [n_bags * w_r] * W, self.group)
+        self._alltoall(recv, pooled.reshape(-1).contiguous(), [n_bags * w for w in self.widths], [n_bags * w_r] * W)
         parts = torch.split(recv, [n_bags * w for w in self.widths])
         out = torch.cat([p.reshape(n_bags, w) for p, w in zip(parts, self.widths)], dim=1)
         return out, (h, g_off, n_bags, g_psw)
@@ -589,7 +598,7 @@ class ColumnShardedEmbedding(torch.nn.Module):
         W, w_r = self.world, self.widths[self.rank]
         send = torch.cat([grad_out[:, a:b].reshape(-1) for a, b in self.plan.ranges]).contiguous()
         recv = torch.empty(W * n_bags * w_r, dtype=grad_out.dtype, device=grad_out.device)
-        _a2a(recv, send, [n_bags * w_r] * W, [n_bags * w for w in self.widths], self.group)
+        self._alltoall(recv, send, [n_bags * w_r] * W, [n_bags * w for w in self.widths])
         self.shard.backward(h, recv.reshape(W * n_bags, w_r), g_off, W * n_bags, False, g_psw, self.mode)
 
     def forward(self, ids, offsets=None, per_sample_weights=None):
