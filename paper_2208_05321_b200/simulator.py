@@ -33,6 +33,7 @@ from .transmitter import DEFAULT_BUFFER_BYTES, ChannelModel, TransferReport
 from .updates import update_column_weights, update_row_scalars
 
 TOOL_VERSION = "0.1.0"
+TRACE_FORMATS = ("global", "categorical")
 POLICIES = ("freq_lfu", "rowwise_transfer")
 NONDETERMINISTIC_FIELDS = ("created_unix", "elapsed_s", "gpu_timing")
 TO_FAST = "to_fast"
@@ -73,8 +74,8 @@ class SimConfig:
                                       f"have {POLICIES}")
         if self.shard_strategy != "column":
             raise NotImplementedError("table-wise placement statistics are not on the GPU path")
-        if self.trace_path is not None:
-            raise NotImplementedError("CSV traces are offline tooling; pass a Trace to run() instead")
+        if self.trace_format not in TRACE_FORMATS:
+            raise ValueError(f"trace_format must be one of {TRACE_FORMATS}")
         if self.write_back not in ("dirty_only", "always"):
             raise ValueError(f"write_back must be 'dirty_only' or 'always', got {self.write_back!r}")
         if self.evict_mode not in ("occupancy_aware", "paper_literal"):
@@ -87,9 +88,9 @@ class SimConfig:
             raise ValueError("batch_size must be >= 1 and num_batches >= 0")
         if self.num_shards < 1:
             raise ValueError("num_shards must be >= 1")
-        if self.preset is None and self.exponent is None:
-            raise ValueError("need a trace source: preset or exponent")
-        if self.preset is not None and self.preset not in workload.PRESETS:
+        if self.trace_path is None and self.preset is None and self.exponent is None:
+            raise ValueError("need a trace source: preset, exponent, or trace_path")
+        if self.trace_path is None and self.preset is not None and self.preset not in workload.PRESETS:
             raise ValueError(f"unknown preset {self.preset!r}, have {sorted(workload.PRESETS)}")
 
     def channel(self) -> ChannelModel:
@@ -98,6 +99,8 @@ class SimConfig:
     def resolved(self) -> dict:
         doc = asdict(self)
         doc["capacity"] = fast_capacity(self.num_ids, self.cache_ratio)
+        if self.trace_path is not None:  # a CSV trace: nothing generated, nothing resolved (simulator.py:185)
+            return doc
         if self.preset is not None:
             exp, shift = workload.preset_params(self.preset, self.num_ids)
             doc["exponent_resolved"] = exp
@@ -118,6 +121,12 @@ def derive_seeds(seed: int) -> dict:
 
 
 def build_trace(config: SimConfig) -> workload.Trace:
+    """The run's trace (simulator.py:208-225): a CSV file (global ids, or categorical columns
+    remapped with per-feature offsets) or a generated stream."""
+    if config.trace_path is not None:
+        if config.trace_format == "global":
+            return workload.load_csv(config.trace_path, id_remap="identity", num_ids=config.num_ids)
+        return workload.load_csv(config.trace_path)
     seeds = derive_seeds(config.seed)
     n = config.num_batches * config.batch_size
     if config.preset is not None:

@@ -164,3 +164,112 @@ def batches(trace: Trace, batch_size: int):
         raise ValueError("batch_size must be >= 1")
     for seq, lo in enumerate(range(0, trace.num_samples, batch_size)):
         yield Batch(seq, trace.samples[lo:lo + batch_size].reshape(-1))
+
+
+# ----------------------------------------------------------------------------- CSV ingestion
+# (workload.py:276-392) — the trace interchange format, feeding the device path: the loaded
+# Trace goes straight to build_reorder_device / CacheStack / simulator.run.
+
+@dataclass
+class ColumnRemap:
+    """Per-feature categorical remap into one offset global id space (workload.py:276-287)."""
+
+    maps: list
+    offsets: np.ndarray
+    num_ids: int
+
+    @property
+    def table_sizes(self) -> list:
+        return [len(m) for m in self.maps]
+
+
+def save_csv(trace: Trace, path) -> None:
+    """Header f0..fN, one sample per line, decimal global ids (workload.py:290-297)."""
+    with open(path, "w", newline="") as fh:
+        fh.write(",".join(f"f{i}" for i in range(trace.features)) + "\r\n")
+        if trace.samples.size:
+            np.savetxt(fh, np.asarray(trace.samples, dtype=np.int64), fmt="%d", delimiter=",", newline="\r\n")
+
+
+def _first_seen_ids(tokens, remap_dict: dict) -> np.ndarray:
+    """Column tokens -> local ids in first-seen order, extending `remap_dict` exactly as
+    the reference's per-row dict.setdefault does (workload.py:363-366), but vectorised:
+    unique tokens, each one's first position, new tokens ranked by it."""
+    tok = np.asarray(tokens, dtype=object)
+    if tok.size == 0:
+        return np.empty(0, dtype=np.int64)
+    uniq, first, inv = np.unique(tok.astype(str), return_index=True, return_inverse=True)
+    known = np.array([remap_dict.get(u, -1) for u in uniq], dtype=np.int64)
+    new = np.flatnonzero(known < 0)
+    base = len(remap_dict)
+    for k, u in enumerate(new[np.argsort(first[new], kind="stable")]):
+        known[u] = base + k
+        remap_dict[uniq[u]] = base + k
+    return known[inv.reshape(-1)]
+
+
+def load_csv(path, feature_columns: list | None = None, id_remap=None, num_ids: int | None = None,
+             on_error: str = "fail") -> Trace:
+    """A categorical CSV as a Trace (workload.py:300-392): every column remapped, per column
+    and in first-seen order, into a contiguous id space with per-feature offsets (the same raw
+    value in two columns gets two ids); a previous ColumnRemap keeps ids stable across files;
+    id_remap="identity" parses global ids directly (save_csv's format; id space = num_ids or
+    max + 1). Malformed rows raise with their line number, or are skipped (on_error="skip")."""
+    import csv
+
+    if on_error not in ("fail", "skip"):
+        raise ValueError("on_error must be 'fail' or 'skip'")
+    identity = id_remap == "identity"
+    with open(path, newline="") as fh:
+        reader = csv.reader(fh)
+        header = next(reader, None)
+        if header is None:
+            return Trace(num_ids=num_ids or 0, features=1, samples=np.empty((0, 1), dtype=np.int64))
+        header = [h.strip() for h in header]
+        if feature_columns is None:
+            cols = list(range(len(header)))
+        else:
+            missing = [c for c in feature_columns if c not in header]
+            if missing:
+                raise ValueError(f"{path}: feature columns not in header: {missing}")
+            cols = [header.index(c) for c in feature_columns]
+        features = len(cols)
+        if identity:
+            remap = None
+        elif id_remap is None:
+            remap = ColumnRemap(maps=[{} for _ in cols], offsets=np.zeros(features, dtype=np.int64), num_ids=0)
+        elif isinstance(id_remap, ColumnRemap):
+            remap = id_remap
+            if len(remap.maps) != features:
+                raise ValueError(f"id_remap covers {len(remap.maps)} columns, trace has {features}")
+        else:
+            raise ValueError(f"id_remap must be None, 'identity', or a ColumnRemap, got {id_remap!r}")
+        rows = []
+        for lineno, row in enumerate(reader, start=2):
+            if not row:
+                continue
+            if len(row) != len(header):
+                if on_error == "skip":
+                    continue
+                raise ValueError(f"{path}:{lineno}: expected {len(header)} fields, got {len(row)}")
+            if identity:
+                try:
+                    rows.append([int(row[c]) for c in cols])
+                except ValueError:
+                    if on_error == "skip":
+                        continue
+                    raise ValueError(f"{path}:{lineno}: malformed id field") from None
+            else:
+                rows.append([row[c] for c in cols])
+    if identity:
+        samples = np.asarray(rows, dtype=np.int64).reshape(-1, features)
+        space = num_ids if num_ids is not None else (int(samples.max()) + 1 if samples.size else 0)
+        return Trace(space, features, samples, {"source": str(path), "remap": "identity"})
+    tok = np.asarray(rows, dtype=object).reshape(-1, features)
+    local = np.stack([_first_seen_ids(tok[:, f], remap.maps[f]) for f in range(features)], axis=1) \
+        if tok.shape[0] else np.empty((0, features), dtype=np.int64)
+    sizes = remap.table_sizes
+    remap.offsets = np.concatenate([[0], np.cumsum(sizes[:-1])]).astype(np.int64)
+    remap.num_ids = int(sum(sizes))
+    samples = local.astype(np.int64).reshape(-1, features) + remap.offsets
+    return Trace(remap.num_ids, features, samples, {"source": str(path), "remap": "per_column"}, table_sizes=sizes)

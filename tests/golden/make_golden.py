@@ -341,6 +341,72 @@ def gen_buffer_too_small():
                         slow=np.array(slows), meta=np.array([num_ids, cap, dim], dtype=np.int64))
 
 
+# ---------------------------------------------------------------------------
+# 8. CSV trace ingestion (workload.py:276-392) and CSV-driven simulator runs (simulator.py:208-213)
+# ---------------------------------------------------------------------------
+
+CSV_CASES = {  # name -> (file text, load_csv kwargs); the reference's own test shapes (test_workload.py:112-166)
+    "remap": ("f0,f1\nx,y\nx,z\n", {}),
+    "remap_stable": ("f0,f1\na,b\nc,b\na,d\n", {}),
+    "empty": ("", {}),
+    "identity": ("a,b,c\n1,2,3\n4,5,6\n", {"id_remap": "identity", "num_ids": 10}),
+    "subset": ("a,b,c\n1,2,3\n4,5,6\n", {"feature_columns": ["a", "c"], "id_remap": "identity", "num_ids": 10}),
+    "malformed_skip": ("f0,f1\n1,2\n3\n", {"id_remap": "identity", "num_ids": 10, "on_error": "skip"}),
+    "malformed_fail": ("f0,f1\n1,2\n3\n", {"id_remap": "identity", "num_ids": 10}),
+    "badint_skip": ("f0,f1\n1,2\nx,3\n7,8\n", {"id_remap": "identity", "num_ids": 10, "on_error": "skip"}),
+    "remap_blank_and_quoted": ('f0,f1,f2\n"a,b",,x\n,q,x\n"a,b",q,y\n\nz,,x\n', {}),
+}
+
+
+def gen_csv():
+    import json
+    import tempfile
+
+    rng = np.random.default_rng(41)
+    # a categorical log: 3 string columns with per-column vocabularies of different sizes
+    lines = ["site,app,device"] + [f"s{a},app{b},d{c}" for a, b, c in zip(
+        rng.zipf(1.6, 600) % 50, rng.zipf(1.4, 600) % 300, rng.integers(0, 7, 600))]
+    CSV_CASES["categorical_log"] = ("\n".join(lines) + "\n", {})
+    out = {}
+    with tempfile.TemporaryDirectory() as d:
+        for name, (text, kw) in CSV_CASES.items():
+            path = os.path.join(d, name + ".csv")
+            with open(path, "w", newline="") as fh:
+                fh.write(text)
+            doc = {"text": text, "kwargs": kw}
+            try:
+                tr = workload.load_csv(path, **kw)
+                doc.update(samples=tr.samples.tolist(), num_ids=tr.num_ids, features=tr.features,
+                           table_sizes=tr.table_sizes)
+            except ValueError as e:
+                doc["error"] = str(e).replace(path, "<path>")
+            out[name] = doc
+    # save_csv bytes of a generated trace (the interchange format) and two simulator runs on CSV files
+    tr = workload.gen_zipf(3000, 1.2, 500, 3, seed=43)
+    path = os.path.join(OUT, "trace_global.csv")
+    workload.save_csv(tr, path)
+    with open(os.path.join(OUT, "trace_categorical.csv"), "w", newline="") as fh:
+        fh.write(CSV_CASES["categorical_log"][0])
+    runs = {}
+    for name, cfg in {
+        "global": simulator.SimConfig(preset=None, trace_path="tests/golden/trace_global.csv", trace_format="global",
+                                      num_ids=3000, batch_size=40, embedding_dim=8, cache_ratio=0.05, seed=6,
+                                      track_oracle=True),
+        "categorical": simulator.SimConfig(preset=None, trace_path="tests/golden/trace_categorical.csv",
+                                           trace_format="categorical", num_ids=1, batch_size=10, embedding_dim=4,
+                                           cache_ratio=0.3, seed=7, write_back="always"),
+    }.items():
+        cwd = os.getcwd()
+        os.chdir(os.path.dirname(os.path.dirname(OUT)))  # trace paths relative to the repo root
+        try:
+            m = simulator.run(cfg)
+        finally:
+            os.chdir(cwd)
+        runs[name] = {"config": {k: v for k, v in vars(cfg).items()}, "metrics": json.loads(m.determinism_json())}
+    with open(os.path.join(OUT, "csv.json"), "w") as fh:
+        json.dump({"load_csv": out, "runs": runs, "trace_global_samples": tr.samples.tolist()}, fh, sort_keys=True)
+
+
 def main():
     gen_random_stream("stream_dirty_zipf", "dirty_only")
     gen_random_stream("stream_always_zipf", "always", seed=21, init_seed=3)
@@ -359,6 +425,7 @@ def main():
     gen_embedding_bag()
     gen_sim_metrics()
     gen_buffer_too_small()
+    gen_csv()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -140,3 +140,30 @@ def test_peer_rows_bound_is_checked_on_the_full_count_matrix():
     x = {"mat": [[3, 4], [4, 6]], "rc": [3, 4], "u": 7}
     pr.segments(x)
     assert x["seg"].tolist() == [0, 3, 7] and x["off"].tolist() == [0, 0]
+
+
+def test_bench_reference_arm_and_gpu_count_check():
+    """bench.py's CPU arm prints one JSON line with the driver's keys (the reference package
+    from baseline/_ref when installed, else the oracle port), and `--gpus N` on a host with
+    fewer GPUs fails loudly instead of silently running one rank."""
+    import json
+    import subprocess
+    import sys
+
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "small",
+                        "--steps", "2", "--warmup", "1", "--trace-batches", "12"],
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1
+    doc = json.loads(lines[0])
+    assert doc["impl"] == "reference" and doc["unit"] == "lookups/s" and doc["value"] > 0
+    assert doc["cpu_baseline"]["kind"] in ("reference", "port") and doc["cpu_baseline"]["cores"] == 1
+    assert doc["config"]["workload"] == "small" and doc["config"]["parallelism"] == "single"
+    assert doc["e2e"]["h2d_bytes_per_step"] == 0
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "1"],
+                           capture_output=True, text=True, timeout=300)
+        assert r.returncode != 0 and "CUDA device" in r.stderr

@@ -53,3 +53,19 @@ def test_event_log_obeys_eviction_law():
     for st in stacks:
         assert st.events and simulator.replay_eviction_law(st.events, cfg.num_ids) == []
     assert metrics.summary["oracle"]["ok"] is True
+
+
+CSV = json.load(open(os.path.join(GOLDEN, "csv.json")))
+
+
+@pytest.mark.parametrize("name", sorted(CSV["runs"]))
+def test_csv_trace_run_matches_reference_metrics(name, monkeypatch):
+    """simulator.run on a CSV trace (simulator.py:208-213): save_csv's global-id format and a
+    categorical log remapped with per-feature offsets (load_csv), fed to the device caches;
+    the RunMetrics document equals the reference's."""
+    from conftest import ROOT
+
+    monkeypatch.chdir(ROOT)  # the recorded configs name the trace relative to the repo root
+    doc = CSV["runs"][name]
+    m = simulator.run(simulator.SimConfig(**doc["config"]), prefetch=True)
+    close(json.loads(m.determinism_json()), doc["metrics"])
