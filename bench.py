@@ -264,6 +264,17 @@ def host_link_peaks(torch, dev):
     return r
 
 
+def gpu_local_cpus(index):
+    """The GPU's NUMA-local CPU list (sysfs), where the library pins the slow tier and binds its threads."""
+    try:
+        import torch
+        pr = torch.cuda.get_device_properties(index)
+        bus = "%04x:%02x:%02x.0" % (pr.pci_domain_id, pr.pci_bus_id, pr.pci_device_id)
+        return open(f"/sys/bus/pci/devices/{bus}/local_cpulist").read().strip()
+    except Exception:
+        return None
+
+
 def hbm_peak():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
@@ -716,6 +727,17 @@ def run_ours(args, cfg, torch, rank, world):
             wb = prof["writeback_rows"] / max(prof["scatter_jobs"], 1)
         res.update({"hit_ratio": hits / uniq, "unique_per_step": uniq, "misses_per_step": misses,
                     "evictions_per_step": evict, "writeback_rows_per_step": wb})
+        # host-DRAM traffic of the step: the admitted rows are read by the GPU over the link; the
+        # write-back rows land in pinned staging (D2H), are read back and scattered into the slow
+        # tier by the host threads (non-temporal stores: no read-for-ownership)
+        row = 4 * (D + (D if OPT == "adagrad" else 0))
+        d2h = prof["writeback_d2h_bytes"] / max(prof["scatter_jobs"], 1)
+        hb = misses * row + d2h + wb * (row + 4) + wb * row
+        res["host_memory"] = {"bytes_per_step": hb, "GBps": hb / (total_ms / K * 1e-3) / 1e9,
+                              "parts": {"admission_reads": misses * row, "d2h_writes": d2h,
+                                        "scatter_reads": wb * (row + 4), "scatter_writes": wb * row},
+                              "scatter_threads": prof.get("scatter_threads"),
+                              "local_cpus": gpu_local_cpus(dev.index)}
     return res, samples, rank_of, cap
 
 

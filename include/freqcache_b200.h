@@ -129,7 +129,8 @@ int fc_drain_stream(fc_cache* h, void* stream);
  * (upper bound of the write-back), [5] host ms spent waiting for async write-backs,
  * [6] host scatter ms and [7] scatter jobs completed (engine 1), [8] transfer launches
  * timed (prefetch pipeline: [1] covers k_admit_stage), [9] rows written back to the slow
- * tier and [10] bytes shipped device -> host for them (engine 1, exact). `out` holds 11 doubles. */
+ * tier and [10] bytes shipped device -> host for them (engine 1, exact), [11] host scatter
+ * threads (engine 1; bound to the GPU's local CPUs). `out` holds 12 doubles. */
 int fc_profile(fc_cache* h, int32_t enable, double* out);
 
 /* Timeline tracing (diagnostics, no reference counterpart): while enabled the

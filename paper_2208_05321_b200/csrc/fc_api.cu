@@ -1,6 +1,10 @@
 // C ABI entry points (include/freqcache_b200.h). Each call validates on the host
 // what the reference validates before mutation, launches the device sequence on
 // the caller's stream and, where the reference returns scalars, synchronises.
+#include <pthread.h>
+#include <sched.h>
+
+#include <cctype>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -48,6 +52,50 @@ static void trace_clear(fc_cache* h) {
   for (auto& t : *v) cudaEventDestroy(t.ev);
   delete v;
   h->trace = nullptr;
+}
+
+// CPUs attached to the GPU's PCIe root (its NUMA node's cores), from sysfs; empty if unknown.
+std::vector<int> device_local_cpus(int device) {
+  std::vector<int> cpus;
+  char bus[64] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) {
+    cudaGetLastError();
+    return cpus;
+  }
+  for (char* c = bus; *c; ++c) *c = (char)std::tolower(*c);
+  char path[256];
+  std::snprintf(path, sizeof(path), "/sys/bus/pci/devices/%s/local_cpulist", bus);
+  FILE* f = std::fopen(path, "r");
+  if (!f) return cpus;
+  char line[4096] = {0};
+  if (std::fgets(line, sizeof(line), f)) {
+    for (char* tok = std::strtok(line, ",\n"); tok; tok = std::strtok(nullptr, ",\n")) {
+      int a = -1, b = -1;
+      if (std::sscanf(tok, "%d-%d", &a, &b) == 2) {
+        for (int x = a; x <= b; ++x) cpus.push_back(x);
+      } else if (std::sscanf(tok, "%d", &a) == 1) {
+        cpus.push_back(a);
+      }
+    }
+  }
+  std::fclose(f);
+  cpu_set_t allowed;  // keep only CPUs this process may run on (containers, taskset)
+  if (sched_getaffinity(0, sizeof(allowed), &allowed) == 0) {
+    std::vector<int> ok;
+    for (int c : cpus)
+      if (c >= 0 && c < CPU_SETSIZE && CPU_ISSET(c, &allowed)) ok.push_back(c);
+    cpus.swap(ok);
+  }
+  return cpus;
+}
+
+// Bind a thread (0 = the calling thread) to `cpus`; no-op when the list is empty.
+void bind_thread(pthread_t t, const std::vector<int>& cpus) {
+  if (cpus.empty()) return;
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  for (int c : cpus) CPU_SET(c, &set);
+  pthread_setaffinity_np(t, sizeof(set), &set);
 }
 
 int ensure_scratch_buf(void** p, size_t* have, size_t bytes) {
@@ -134,7 +182,18 @@ const char* fc_last_error(void) { return g_err; }
 int fc_host_alloc(int64_t bytes, void** out) {
   if (!out || bytes < 0) return FC_ERR_BAD_ARG;
   *out = nullptr;
-  FC_CUDA(cudaHostAlloc(out, std::max<int64_t>(bytes, 16), cudaHostAllocMapped | cudaHostAllocPortable));
+  // The pages are faulted in (pinned) by the calling thread, and land on its NUMA node: run
+  // the allocation on the current GPU's local CPUs so the slow tier sits next to its GPU
+  // (on multi-socket boxes the host scatter and the DMA then stay on one socket).
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const std::vector<int> cpus = device_local_cpus(dev);
+  cpu_set_t old;
+  const bool have_old = !cpus.empty() && sched_getaffinity(0, sizeof(old), &old) == 0;
+  if (have_old) bind_thread(pthread_self(), cpus);
+  const cudaError_t e = cudaHostAlloc(out, std::max<int64_t>(bytes, 16), cudaHostAllocMapped | cudaHostAllocPortable);
+  if (have_old) sched_setaffinity(0, sizeof(old), &old);
+  FC_CUDA(e);
   return FC_OK;
 }
 
@@ -541,6 +600,7 @@ int fc_profile(fc_cache* h, int32_t enable, double* out) {
     out[8] = h->prof[6];
     out[9] = es[2];
     out[10] = es[3];
+    out[11] = (double)engine_threads(h);
   }
   if (enable && !h->profile) {
     for (int i = 0; i < 4; ++i) FC_CUDA(cudaEventCreate(&h->pev[i]));

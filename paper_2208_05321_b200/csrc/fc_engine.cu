@@ -113,6 +113,7 @@ struct AsyncWB {
   double scatter_ms = 0;  // host scatter time (stats, under m)
   int64_t jobs_done = 0;
   double dirty_frac = 1.0;  // recent dirty share of the victims (pipeline commits; under m)
+  int threads = 0;          // host scatter threads (dispatcher + helpers)
   int64_t rows_done = 0;  // rows written back to the slow tier (stats, under m)
   int64_t d2h_bytes = 0;  // bytes shipped device -> host for them (stats, under m)
 };
@@ -494,12 +495,30 @@ int engine_set(fc_cache* h, int engine) {
     engine_release(h);
     return cuda_fail(e, "engine_set");
   }
-  unsigned hw = std::thread::hardware_concurrency();
-  int nh = (int)std::max(1u, std::min(7u, hw > 4 ? hw / 2 - 1 : 1u));  // half the cores: leave the rest to the caller
+  // Host threads of this cache: on the GPU's own socket (its local CPUs, where the slow tier
+  // was pinned by fc_host_alloc), and at most half of this rank's share of those cores --
+  // one process per GPU shares the socket with its peers (LOCAL_WORLD_SIZE from torchrun)
+  // and leaves the other half to the caller's threads.
+  const std::vector<int> cpus = device_local_cpus(h->device);
+  int cores = cpus.empty() ? (int)std::thread::hardware_concurrency() : (int)cpus.size();
+  int local_ranks = 1;
+  if (const char* env = std::getenv("LOCAL_WORLD_SIZE")) local_ranks = std::max(1, std::atoi(env));
+  if (!cpus.empty() && local_ranks > 1) {  // ranks sharing this socket: the GPUs whose local CPUs match
+    int same = 0, ndev = 0;
+    cudaGetDeviceCount(&ndev);
+    for (int d = 0; d < ndev; ++d) same += device_local_cpus(d) == cpus;
+    local_ranks = std::max(1, std::min(local_ranks, same));
+  }
+  const int share = std::max(1, cores / local_ranks);
+  int nh = std::max(1, std::min(7, share / 2 - 1));
   if (const char* env = std::getenv("FC_SCATTER_THREADS")) nh = std::max(0, std::atoi(env) - 1);
   for (int i = 0; i < nh; ++i) a->helpers.emplace_back(helper_main, a);
   a->dispatcher = std::thread(dispatcher_main, a);
   a->copier = std::thread(copier_main, a);
+  for (auto& t : a->helpers) bind_thread(t.native_handle(), cpus);
+  bind_thread(a->dispatcher.native_handle(), cpus);
+  bind_thread(a->copier.native_handle(), cpus);
+  a->threads = nh + 1;
   h->engine = 1;
   return FC_OK;
 }
@@ -631,6 +650,8 @@ int engine_drain_stream(fc_cache* h, cudaStream_t st) {
     wait_seq(a, last);
   return FC_OK;
 }
+
+int engine_threads(const fc_cache* h) { return h->awb ? h->awb->threads : 0; }
 
 void engine_release(fc_cache* h) {
   AsyncWB* a = h->awb;

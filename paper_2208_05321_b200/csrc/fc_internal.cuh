@@ -22,7 +22,10 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <pthread.h>
 #include <stdint.h>
+
+#include <vector>
 
 #include "../../include/freqcache_b200.h"
 
@@ -147,6 +150,7 @@ int engine_admit(fc_cache* h, cudaStream_t st);              // replaces k_trans
 int engine_after_prepare(fc_cache* h, cudaStream_t st);      // after the prepare's sync
 int engine_drain(fc_cache* h);                               // all write-backs landed in the slow tier
 int engine_drain_stream(fc_cache* h, cudaStream_t st);       // the same, as a wait on `st`
+int engine_threads(const fc_cache* h);                       // host scatter threads of the async engine
 void engine_release(fc_cache* h);
 void engine_stats(fc_cache* h, double* out);                 // host scatter ms, jobs, rows, D2H bytes (then reset)
 // prefetch pipeline (fc_engine.cu)
@@ -163,6 +167,9 @@ void pipe_release(fc_cache* h);
 namespace fc {
 
 void set_error(const char* fmt, ...);
+// host placement (fc_api.cu): the GPU's local CPUs (sysfs local_cpulist), thread binding
+std::vector<int> device_local_cpus(int device);
+void bind_thread(pthread_t t, const std::vector<int>& cpus);
 // timeline tracing (fc_trace): record a tagged event on `st` when tracing is on
 void trace_mark(fc_cache* h, int tag, cudaStream_t st);
 enum TraceTag : int { T_INDEX_BEGIN = 1, T_INDEX_END = 2, T_XFER_BEGIN = 3, T_XFER_END = 4, T_COMMIT_BEGIN = 5,

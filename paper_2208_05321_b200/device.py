@@ -127,11 +127,12 @@ class DeviceCache:
 
     def profile(self, enable: bool) -> dict:
         """Toggle per-kernel CUDA-event timing; returns (and resets) the totals so far."""
-        out = (ctypes.c_double * 11)()
+        out = (ctypes.c_double * 12)()
         check(self.lib.fc_profile(self.h, int(bool(enable)), out))
         return {"prepare_ms": out[0], "transfer_ms": out[1], "calls": int(out[2]), "host_link_bytes": out[3],
                 "victim_bytes": out[4], "host_wait_ms": out[5], "scatter_ms": out[6], "scatter_jobs": int(out[7]),
-                "transfer_launches": int(out[8]), "writeback_rows": int(out[9]), "writeback_d2h_bytes": out[10]}
+                "transfer_launches": int(out[8]), "writeback_rows": int(out[9]), "writeback_d2h_bytes": out[10],
+                "scatter_threads": int(out[11])}
 
     def trace(self, enable: bool) -> None:
         """Timeline tracing of the pipeline (fc_trace)."""

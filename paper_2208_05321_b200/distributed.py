@@ -353,15 +353,18 @@ class RowShardedEmbedding(torch.nn.Module):
         self.last_recv = 0
         self._pf = None  # (ids, exchange) of a prefetched batch
         # on a GPU the exchange planning, expansion and gradient reduction run in
-        # libfreqcache_b200 (Router); on CPU (gloo tests) the same steps in torch
+        # libfreqcache_b200 (Router) -- there is no torch fallback there; the torch restatement
+        # of the same steps below serves CPU process groups only (the gloo tests' oracle shards)
         self.router = None
         self.peer = None
         if self.device.type == "cuda":
             num_ids = getattr(shard, "global_num_ids", None)
-            if num_ids is not None:
-                self.router = Router(num_ids, world, self.device)
-                if peer_rows:  # fused return exchange over NVLink peer memory (PeerRows)
-                    self.peer = PeerRows(shard, world, rank, int(peer_rows), group, self.device)
+            if num_ids is None:
+                raise ValueError("RowShardedEmbedding on CUDA needs shard.global_num_ids (the whole table's id "
+                                 "space) for the libfreqcache_b200 router")
+            self.router = Router(num_ids, world, self.device)
+            if peer_rows:  # fused return exchange over NVLink peer memory (PeerRows)
+                self.peer = PeerRows(shard, world, rank, int(peer_rows), group, self.device)
 
     @staticmethod
     def owner_of(ids, world):

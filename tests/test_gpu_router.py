@@ -130,3 +130,15 @@ def test_owner_direct_apply_equals_grouped(opt):
     assert np.array_equal(out[0][0], out[1][0])
     if opt == "adagrad":
         assert np.array_equal(out[0][1], out[1][1])
+
+
+def test_row_sharded_on_cuda_requires_the_router():
+    """No torch fallback for the exchange on a GPU: a shard without the global id space is refused."""
+    from paper_2208_05321_b200.distributed import RowShardedEmbedding
+
+    class NoSpace:
+        device = torch.device("cuda")
+        dim = 4
+
+    with pytest.raises(ValueError, match="global_num_ids"):
+        RowShardedEmbedding(NoSpace(), 1, 0, device=torch.device("cuda"))
