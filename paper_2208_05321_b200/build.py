@@ -22,6 +22,7 @@ OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libfreqcache_b200.so")
 SOURCES = ["fc_api.cu", "fc_index.cu", "fc_rows.cu", "fc_sort.cu", "fc_backward.cu", "fc_engine.cu", "fc_reorder.cu"]
 HEADERS = [os.path.join(CSRC, "fc_internal.cuh"), os.path.join(CSRC, "fc_rowutil.cuh"),
+           os.path.join(CSRC, "fc_tma.cuh"),
            os.path.join(ROOT, "include", "freqcache_b200.h")]
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

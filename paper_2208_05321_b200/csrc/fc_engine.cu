@@ -40,6 +40,7 @@
 #include <cuda.h>
 
 #include "fc_rowutil.cuh"
+#include "fc_tma.cuh"
 
 namespace fc {
 
@@ -236,8 +237,6 @@ static void dispatcher_main(AsyncWB* a) {
       slow_wait_note("dispatcher: write-back D2H", tw);
     }
     lk.lock();
-    a->rows_done += j.rows;
-    if (!j.shipped) a->d2h_bytes += j.rows * (4 + 4 * (int64_t)(a->h->dim + a->h->sw));
     a->src = a->hstage[j.buf];
     a->ssrc = a->hsstage[j.buf];
     a->ranks = a->hranks[j.buf];
@@ -253,7 +252,9 @@ static void dispatcher_main(AsyncWB* a) {
     a->cv_helped.wait(lk, [&] { return a->helpers_left == 0; });
     a->scatter_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     slow_wait_note("dispatcher: host scatter of one job", t0);
-    a->jobs_done += 1;
+    a->jobs_done += 1;  // rows and bytes are counted with the job's completion, so the ratios hold mid-run
+    a->rows_done += j.rows;
+    if (!j.shipped) a->d2h_bytes += j.rows * (4 + 4 * (int64_t)(a->h->dim + a->h->sw));
     a->done_seq = j.seq;
     *a->done_host = (uint32_t)j.seq;  // releases streams waiting on this job (stream wait-value)
     a->cv_done.notify_all();
@@ -923,52 +924,6 @@ __global__ void __launch_bounds__(kNT) k_admit_stage(PipeArgs x) {
 // contiguous). Measured (tools/interference_bench.cu, profiles/r01_interference_bench_tma.txt):
 // 50 GB/s alone vs 43 for SM loads, and a concurrent HBM-bound kernel slows by ~5%
 // instead of ~4x — the miss staging can overlap the backward.
-__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ void mbar_init(uint64_t* b) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned phase) {
-  asm volatile(
-      "{\n .reg .pred p;\n WAIT_%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra WAIT_%=;\n}\n" ::"r"(
-          smem_u32(b)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* smem, const void* gmem, unsigned bytes, uint64_t* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_u32(smem)),
-               "l"(gmem), "r"(bytes), "r"(smem_u32(bar))
-               : "memory");
-}
-// the same with an L2 evict-first hint: miss-staging traffic should not displace the
-// index tables and rows the concurrent kernels work on
-__device__ __forceinline__ uint64_t l2_evict_first() {
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-__device__ __forceinline__ void bulk_g2s_ef(void* smem, const void* gmem, unsigned bytes, uint64_t* bar, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(smem)),
-      "l"(gmem), "r"(bytes), "r"(smem_u32(bar)), "l"(pol)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_s2g_ef(void* gmem, const void* smem, unsigned bytes, uint64_t pol) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem),
-               "r"(smem_u32(smem)), "r"(bytes), "l"(pol)
-               : "memory");
-}
-
-__device__ __forceinline__ void bulk_s2g(void* gmem, const void* smem, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem), "r"(smem_u32(smem)),
-               "r"(bytes)
-               : "memory");
-}
-
 __global__ void __launch_bounds__(32) k_admit_stage_tma(PipeArgs x, int G) {
   extern __shared__ __align__(128) unsigned char ring[];  // kTmaStages x G x (D + S) floats
   __shared__ uint64_t bar[kTmaStages];

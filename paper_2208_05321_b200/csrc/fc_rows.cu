@@ -11,8 +11,10 @@
 // both ways at once (transmitter.py:144-207 moves rows through a bounded host
 // buffer; here the "buffer" is the HBM staging area of the victims).
 #include <algorithm>
+#include <cstdlib>
 
 #include "fc_rowutil.cuh"
+#include "fc_tma.cuh"
 
 namespace fc {
 
@@ -421,6 +423,82 @@ __global__ void __launch_bounds__(kNT) k_pool1(const float* __restrict__ fast, i
   }
 }
 
+// Bag size 1 through the TMA bulk-copy engine: a one-warp block owns a ring of kPoolStages
+// stages of G rows; each lane queues one cp.async.bulk of its occurrence's cached row into
+// the stage (completion on the stage's mbarrier), the lanes scale the rows in shared
+// memory when there are per-sample weights, and lane 0 writes the G consecutive output
+// rows back with ONE bulk store. The SMs only resolve indices: the row bytes move
+// HBM -> SMEM -> HBM without passing through registers.
+constexpr int kPoolStages = 4;
+
+__global__ void __launch_bounds__(32) k_pool1_tma(const float* __restrict__ fast, int D,
+                                                  const int32_t* __restrict__ uslots, const int32_t* __restrict__ inv,
+                                                  int64_t n, const float* __restrict__ psw, float* __restrict__ out,
+                                                  int G) {
+  extern __shared__ __align__(128) unsigned char pring[];  // kPoolStages x G x D floats
+  __shared__ uint64_t bar[kPoolStages];
+  const int lane = threadIdx.x;
+  const unsigned rb = (unsigned)D * 4u;
+  if (lane == 0) {
+    for (int i = 0; i < kPoolStages; ++i) mbar_init(&bar[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t ngroups = (n + G - 1) / G;
+  const int64_t mine = ngroups > blockIdx.x ? (ngroups - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  unsigned phase_bits = 0;
+  int64_t issued = 0, retired = 0;
+  while (retired < mine) {
+    // at most kPoolStages - 1 stages loading: the stage refilled next was retired at least one
+    // retire ago, so its bulk store is at most the second newest and wait_group.read 1 covers it
+    if (issued < mine && issued - retired < kPoolStages - 1) {
+      const int st = (int)(issued % kPoolStages);
+      if (issued >= kPoolStages) {
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+        __syncwarp();
+      }
+      const int64_t j0 = (blockIdx.x + issued * gridDim.x) * G;
+      const int cnt = (int)min((int64_t)G, n - j0);
+      if (lane == 0) mbar_expect_tx(&bar[st], (unsigned)cnt * rb);
+      __syncwarp();
+      float* rows = reinterpret_cast<float*>(pring) + (size_t)st * G * D;
+      for (int i = lane; i < cnt; i += 32) {
+        const int sl = uslots ? uslots[inv[j0 + i]] : inv[j0 + i];
+        bulk_g2s(rows + (size_t)i * D, fast + (int64_t)sl * D, rb, &bar[st]);
+      }
+      ++issued;
+      continue;
+    }
+    const int st = (int)(retired % kPoolStages);
+    mbar_wait(&bar[st], (phase_bits >> st) & 1u);
+    phase_bits ^= 1u << st;
+    const int64_t j0 = (blockIdx.x + retired * gridDim.x) * G;
+    const int cnt = (int)min((int64_t)G, n - j0);
+    float* rows = reinterpret_cast<float*>(pring) + (size_t)st * G * D;
+    if (psw) {  // out[j] = w_j * row: scale in shared memory, then hand the stage back to the async proxy
+      float wl[(32 + 31) / 32 * 1];
+      wl[0] = lane < cnt ? psw[j0 + lane] : 0.f;  // G <= 32: one weight per lane
+      for (int i = 0; i < cnt; ++i) {
+        const float wj = __shfl_sync(FC_FULL, wl[0], i);
+        for (int c = lane * 4; c < D; c += 128) {
+          float4 v = *reinterpret_cast<float4*>(rows + (size_t)i * D + c);
+          v.x *= wj; v.y *= wj; v.z *= wj; v.w *= wj;
+          *reinterpret_cast<float4*>(rows + (size_t)i * D + c) = v;
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+    }
+    if (lane == 0) {
+      bulk_s2g(out + j0 * D, rows, (unsigned)cnt * rb);
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+    __syncwarp();
+    ++retired;
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int launch_pool(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const void* offsets, int off_bytes,
                 int64_t nbags, int include_last, const float* psw, int mode, float* out, cudaStream_t st) {
   return launch_pool_rows(h->fast, h->dim, uslots, inv, n, offsets, off_bytes, nbags, include_last, psw, mode, out, st);
@@ -432,6 +510,24 @@ int launch_pool_rows(const float* rows, int D, const int32_t* uslots, const int3
                      float* out, cudaStream_t st) {
   if (nbags <= 0) return FC_OK;
   const bool v = (D % 4 == 0) && (((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(rows)) & 15) == 0);
+  static const bool no_tma = std::getenv("FC_POOL_NO_TMA") != nullptr;
+  // bag size 1 without weights through the bulk-copy engine (with per-sample weights the
+  // register path is faster: scaling in shared memory serialises on the stage)
+  if (v && offsets == nullptr && !psw && !no_tma && D * 4 <= 8192) {
+    const int G = std::max(1, std::min(32, 16384 / (D * 4)));
+    const size_t smem = (size_t)kPoolStages * G * D * 4;
+    static bool attr = false;
+    if (!attr && smem > 48 * 1024) {
+      FC_CUDA(cudaFuncSetAttribute(k_pool1_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      attr = true;
+    }
+    const int per_sm = std::max(1, std::min(16, (int)((220 * 1024) / smem)));
+    const int64_t groups = (nbags + G - 1) / G;
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(groups, (int64_t)kSMs * per_sm));
+    k_pool1_tma<<<grid, 32, smem, st>>>(rows, D, uslots, inv, nbags, psw, out, G);
+    FC_CUDA(cudaGetLastError());
+    return FC_OK;
+  }
   if (v && offsets == nullptr) {  // bag size 1: one row per bag
     k_pool1<<<grid_for(nbags, kNT, kSMs * 8), kNT, 0, st>>>(rows, D, uslots, inv, nbags, psw, out, units_for(D));
     FC_CUDA(cudaGetLastError());
