@@ -421,8 +421,8 @@ def launches_per_step(args, shard_mode, pipelined, world):
     if shard_mode is None:
         return ((KERNELS_PER_STEP if args.step == "sim" else KERNELS_PER_TRAIN_STEP)
                 + (PIPELINE_EXTRA_KERNELS if pipelined else 0))
-    if shard_mode == "column":  # synchronous prepare of the global batch + pool + fused backward (NCCL kernels not counted)
-        return KERNELS_PER_TRAIN_STEP
+    if shard_mode == "column":  # prepare of the global batch + pool + fused backward (NCCL kernels not counted)
+        return KERNELS_PER_TRAIN_STEP + (PIPELINE_EXTRA_KERNELS if pipelined else 0)
     return (SHARDED_BASE_KERNELS + (PIPELINE_EXTRA_KERNELS if pipelined else 0) + (1 if world == 1 else 5)
             + (1 if args.no_peer else 2))
 
@@ -539,8 +539,9 @@ def run_ours(args, cfg, torch, rank, world):
             pool_ms.append(e)
         stats.append((info.unique, info.hits, info.misses, info.evictions, info.rows_to_slow))
 
-    # the column-wise module has no lookahead (every rank prepares the all-gathered global batch)
-    pipelined = args.engine == "async" and not args.no_prefetch and shard_mode != "column"
+    # sharded modules prefetch through their own prefetch() (column-wise: all-gather of the next
+    # batch's ids + prepare_begin of the global batch; row-wise: id exchange + the owner's prepare_begin)
+    pipelined = args.engine == "async" and not args.no_prefetch
     depth2 = args.prefetch_depth == 2 and not sharded and not os.environ.get("FC_XFER_AFTER_UPDATE")
     if pipelined and not sharded:
         dc.prepare_begin(bview[0], 0, ready=ids_ready)
@@ -714,7 +715,7 @@ def run_ours(args, cfg, torch, rank, world):
                                  "torch_allocator": alloc_diag},
                 "path": "CachedEmbeddingBag.forward(pinned host ids) + out.backward(grad) (fused SGD); result = "
                         "prepare hit/miss counters read back" if not sharded
-                else "RowShardedEmbedding.forward(pinned host ids) + out.backward(grad)"},
+                else f"{type(mod).__name__}.forward(pinned host ids) + prefetch(next ids) + out.backward(grad)"},
         "gpu_launches": launches_per_step(args, shard_mode, pipelined, world) * K,
         "roofline": rl[0], "roofline_secondary": rl[1] if len(rl) > 1 else None,
         "roofline_isolated": ({"note": "same kernels in synchronous steps (no prefetch overlap), after the "

@@ -1255,7 +1255,11 @@ int pipe_launch_xfer(fc_cache* h, cudaStream_t after, bool from_update) {
   q->timed[p] = h->profile != 0;
   if (q->timed[p]) FC_CUDA(cudaEventRecord(q->px[p][0], q->xfer));
   trace_mark(h, T_XFER_BEGIN, q->xfer);
-  if (q->tma) {  // bulk-copy engine: rows are 16-byte multiples at 16-byte aligned addresses
+  // FC_DEBUG_SKIP_STAGING=1: measurement only (admitted rows are NOT staged, results are
+  // wrong) -- how long the rest of the pipelined step takes without host-link traffic
+  static const bool skip_staging = std::getenv("FC_DEBUG_SKIP_STAGING") != nullptr;
+  if (skip_staging) {
+  } else if (q->tma) {  // bulk-copy engine: rows are 16-byte multiples at 16-byte aligned addresses
     const int G = tma_group_rows((h->dim + h->sw) * 4);
     const size_t smem = (size_t)kTmaStages * G * (h->dim + h->sw) * 4;
     if (smem > 48 * 1024)

@@ -510,10 +510,12 @@ int launch_pool_rows(const float* rows, int D, const int32_t* uslots, const int3
                      float* out, cudaStream_t st) {
   if (nbags <= 0) return FC_OK;
   const bool v = (D % 4 == 0) && (((reinterpret_cast<uintptr_t>(out) | reinterpret_cast<uintptr_t>(rows)) & 15) == 0);
-  static const bool no_tma = std::getenv("FC_POOL_NO_TMA") != nullptr;
-  // bag size 1 without weights through the bulk-copy engine (with per-sample weights the
-  // register path is faster: scaling in shared memory serialises on the stage)
-  if (v && offsets == nullptr && !psw && !no_tma && D * 4 <= 8192) {
+  // FC_POOL_TMA=1: bag size 1 without weights through the bulk-copy engine. Alone it
+  // matches the register path (72.8 vs ~73 us at cfg2, profiles/r02_pool_tma_bench.txt),
+  // but inside the prefetch pipeline it is slower (0.27-0.29 vs 0.18-0.24 ms in-step,
+  // 346 vs 371 M lookups/s, profiles/r02_ab_pool.txt), so the register path is the default.
+  static const bool use_tma = std::getenv("FC_POOL_TMA") != nullptr && std::atoi(std::getenv("FC_POOL_TMA")) != 0;
+  if (v && offsets == nullptr && !psw && use_tma && D * 4 <= 8192) {
     const int G = std::max(1, std::min(32, 16384 / (D * 4)));
     const size_t smem = (size_t)kPoolStages * G * D * 4;
     static bool attr = false;

@@ -528,19 +528,26 @@ class RowShardedEmbedding(torch.nn.Module):
 # ----------------------------------------------------------------------------- column-wise (reference semantics)
 class _ColShardFn(torch.autograd.Function):
     @staticmethod
-    def forward(ctx, anchor, mod, ids, offsets, n_bags, psw):
-        out, saved = mod._forward(ids, offsets, n_bags, psw)
+    def forward(ctx, anchor, mod, ids, offsets, n_bags, psw, src=None):
+        out, saved = mod._forward(ids, offsets, n_bags, psw, src)
         ctx.mod, ctx.saved = mod, saved
         return out
 
     @staticmethod
     def backward(ctx, grad_out):
         ctx.mod._backward(ctx.saved, grad_out)
-        return None, None, None, None, None, None
+        return None, None, None, None, None, None, None
 
 
 class ColumnShardedEmbedding(torch.nn.Module):
-    """Rank r caches columns partition_columns(D, world).ranges[r] of every row."""
+    """Rank r caches columns partition_columns(D, world).ranges[r] of every row.
+
+    `prefetch(next_ids)` (call after forward(t), before backward(t), on every rank; or
+    before forward(t) for two batches in flight) all-gathers the next batch's ids on a
+    high-priority side stream and starts this rank's prepare of the GLOBAL batch through
+    the cache's prefetch pipeline (DeviceCache.prepare_begin), so the index phase and the
+    miss staging overlap backward(t). The next forward with the same ids commits it.
+    Decisions are identical with and without prefetching (the commits are FIFO)."""
 
     def __init__(self, shard, dim: int, world: int, rank: int, mode: str = "sum", group=None, device=None):
         super().__init__()
@@ -550,6 +557,8 @@ class ColumnShardedEmbedding(torch.nn.Module):
         self.mode, self.group = mode, group
         self.device = device if device is not None else getattr(shard, "device", torch.device("cpu"))
         self._anchor = torch.nn.Parameter(torch.empty(0, device=self.device))
+        self._pfq = []  # prefetched batches, oldest first: dicts (src, ids, g_ids, counts, ev, begun)
+        self._xstream = None
 
     # the two collectives of the column-wise exchange (overridable: the tests drive the module
     # over a CPU-only process group by staging these through host memory)
@@ -561,34 +570,100 @@ class ColumnShardedEmbedding(torch.nn.Module):
 
     def _gather_var(self, x, counts, maxn):
         """all-gather of per-rank 1-D tensors of different lengths (padded to maxn)."""
+        if self.world == 1:
+            return x
+        if all(c == maxn for c in counts):  # the usual case: every rank has the same batch size
+            g = torch.empty(self.world * maxn, dtype=x.dtype, device=x.device)
+            self._allgather(g, x)
+            return g
         pad = torch.zeros(maxn, dtype=x.dtype, device=x.device)
         pad[:x.numel()] = x
         g = torch.empty(self.world * maxn, dtype=x.dtype, device=x.device)
         self._allgather(g, pad)
-        if all(c == maxn for c in counts):
-            return g
         return torch.cat([g[r * maxn:r * maxn + c] for r, c in enumerate(counts)])
 
-    def _forward(self, ids, offsets, n_bags, psw):
-        W, n = self.world, ids.numel()
+    def _gather_ids(self, ids):
+        """(global ids in rank order, per-rank counts). One host sync on the count
+        all-gather at world > 1, on whatever stream is current."""
+        n = ids.numel()
+        if self.world == 1:
+            return ids, [n]
         cnt = torch.tensor([n], dtype=torch.int64, device=ids.device)
-        all_n = torch.empty(W, dtype=torch.int64, device=ids.device)
+        all_n = torch.empty(self.world, dtype=torch.int64, device=ids.device)
         self._allgather(all_n, cnt)
         counts = all_n.tolist()
-        maxn = max(counts)
-        g_ids = self._gather_var(ids.contiguous(), counts, maxn)
+        return self._gather_var(ids.contiguous(), counts, max(counts)), counts
+
+    def prefetch(self, ids, ready=None):
+        """Next batch's id all-gather + this rank's prepare_begin of the global batch. On a
+        GPU both run on a side stream: host ids are copied there; device ids are read after
+        the work queued on the current stream, or after `ready` (a torch.cuda.Event)."""
+        if len(self._pfq) >= 2:
+            raise RuntimeError("two prefetched batches are outstanding: run a forward first")
+        can_begin = hasattr(self.shard, "prepare_begin")
+        if self.device.type != "cuda":
+            dev_ids = ids.reshape(-1).to(self.device)
+            g_ids, counts = self._gather_ids(dev_ids)
+            if can_begin:
+                self.shard.prepare_begin(g_ids)
+            self._pfq.append({"src": ids, "ids": dev_ids, "counts": counts, "ev": None, "begun": can_begin})
+            return
+        main = torch.cuda.current_stream(self.device)
+        if self._xstream is None:
+            self._xstream = torch.cuda.Stream(self.device, priority=-100)
+        xs = self._xstream
+        with torch.cuda.stream(xs):
+            if ids.is_cuda:
+                if ready is None:
+                    xs.wait_stream(main)
+                else:
+                    xs.wait_event(ready)
+            dev_ids = ids.reshape(-1).to(self.device, non_blocking=True)
+            g_ids, counts = self._gather_ids(dev_ids)
+            if can_begin:  # its index stream waits for xs; the prepare's buffers are used on main
+                self.shard.prepare_begin(g_ids, consumer=main)
+            ev = torch.cuda.Event()
+            ev.record(xs)
+        dev_ids.record_stream(main)
+        g_ids.record_stream(main)
+        self._pfq.append({"src": ids, "ids": dev_ids, "counts": counts, "ev": ev, "begun": can_begin})
+
+    def _take_prefetched(self, ids, src):
+        """Commit prefetched batches oldest first until `ids`' one (FIFO, like the cache's
+        own pipeline); returns (prepare handle, counts) or (None, None) when `ids` was not
+        prefetched (the bypassed batches are still executed, in order)."""
+        while self._pfq:
+            pf = self._pfq.pop(0)
+            if pf["ev"] is not None:
+                torch.cuda.current_stream(self.device).wait_event(pf["ev"])
+            h = self.shard.prepare_commit() if pf["begun"] else None
+            same = pf["src"] is src or pf["ids"] is ids or (
+                pf["ids"].numel() == ids.numel() and bool(torch.equal(pf["ids"], ids)))
+            if same and h is not None:
+                return h, pf["counts"]
+        return None, None
+
+    def _forward(self, ids, offsets, n_bags, psw, src=None):
+        W = self.world
+        h, counts = self._take_prefetched(ids, src) if self._pfq else (None, None)
+        if h is None:
+            g_ids, counts = self._gather_ids(ids)
+            h = self.shard.prepare(g_ids)  # identical decisions on every rank
         g_off, g_psw = None, None
         if offsets is not None:  # every rank has n_bags bags; shift offsets by the ids before it
-            g_off = torch.empty(W * n_bags, dtype=offsets.dtype, device=offsets.device)
-            self._allgather(g_off, offsets[:n_bags].contiguous())
-            base = torch.tensor(np.concatenate([[0], np.cumsum(counts)[:-1]]), dtype=offsets.dtype,
-                                device=offsets.device)
-            g_off += base.repeat_interleave(n_bags)
+            g_off = offsets[:n_bags].contiguous()
+            if W > 1:
+                g_off = torch.empty(W * n_bags, dtype=offsets.dtype, device=offsets.device)
+                self._allgather(g_off, offsets[:n_bags].contiguous())
+                base = torch.tensor(np.concatenate([[0], np.cumsum(counts)[:-1]]), dtype=offsets.dtype,
+                                    device=offsets.device)
+                g_off += base.repeat_interleave(n_bags)
         if psw is not None:
-            g_psw = self._gather_var(psw.contiguous(), counts, maxn)
-        h = self.shard.prepare(g_ids)  # identical decisions on every rank
+            g_psw = self._gather_var(psw.contiguous(), counts, max(counts))
         self.last_info = h.get("info") if isinstance(h, dict) else None
         pooled = self.shard.pool(h, g_off, W * n_bags, False, g_psw, self.mode)  # [W*n_bags, w_r]
+        if W == 1:
+            return pooled, (h, g_off, n_bags, g_psw)
         w_r = self.widths[self.rank]
         recv = torch.empty(sum(n_bags * w for w in self.widths), dtype=pooled.dtype, device=pooled.device)
         self._alltoall(recv, pooled.reshape(-1).contiguous(), [n_bags * w for w in self.widths], [n_bags * w_r] * W)
@@ -599,15 +674,31 @@ class ColumnShardedEmbedding(torch.nn.Module):
     def _backward(self, saved, grad_out):
         h, g_off, n_bags, g_psw = saved
         W, w_r = self.world, self.widths[self.rank]
-        send = torch.cat([grad_out[:, a:b].reshape(-1) for a, b in self.plan.ranges]).contiguous()
-        recv = torch.empty(W * n_bags * w_r, dtype=grad_out.dtype, device=grad_out.device)
-        self._alltoall(recv, send, [n_bags * w_r] * W, [n_bags * w for w in self.widths])
+        if W == 1:
+            recv = grad_out.contiguous()
+        else:
+            send = torch.cat([grad_out[:, a:b].reshape(-1) for a, b in self.plan.ranges]).contiguous()
+            recv = torch.empty(W * n_bags * w_r, dtype=grad_out.dtype, device=grad_out.device)
+            self._alltoall(recv, send, [n_bags * w_r] * W, [n_bags * w for w in self.widths])
         self.shard.backward(h, recv.reshape(W * n_bags, w_r), g_off, W * n_bags, False, g_psw, self.mode)
 
     def forward(self, ids, offsets=None, per_sample_weights=None):
-        ids = ids.reshape(-1).to(self.device)
+        src = ids
+        pf = next((p for p in self._pfq if p["src"] is ids), None)
+        ids = pf["ids"] if pf is not None else ids.reshape(-1).to(self.device, non_blocking=True)
         n_bags = ids.numel() if offsets is None else offsets.numel()
-        return _ColShardFn.apply(self._anchor, self, ids, offsets, n_bags, per_sample_weights)
+        return _ColShardFn.apply(self._anchor, self, ids, offsets, n_bags, per_sample_weights, src)
+
+    def flush(self) -> int:
+        """Commit outstanding prefetches (their batches become resident), then write every
+        dirty cached row of this rank's column slice back to its slow tier."""
+        while self._pfq:
+            pf = self._pfq.pop(0)
+            if pf["ev"] is not None:
+                torch.cuda.current_stream(self.device).wait_event(pf["ev"])
+            if pf["begun"]:
+                self.shard.prepare_commit()
+        return self.shard.flush()
 
 
 # ----------------------------------------------------------------------------- builders

@@ -139,7 +139,7 @@ def _worker(rank, world, port, kind, mode, q, prefetch=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,prefetch", [("row", False), ("row", True), ("column", False)])
+@pytest.mark.parametrize("kind,prefetch", [("row", False), ("row", True), ("column", False), ("column", True)])
 @pytest.mark.parametrize("mode", ["sum", "mean"])
 def test_two_rank_gloo_matches_dense(kind, mode, prefetch):
     ctx = mp.get_context("fork")

@@ -66,7 +66,8 @@ def oracle_slot_tables(trace):
     return out
 
 
-def test_column_sharded_nccl_world1_matches_dense_and_oracle():
+@pytest.mark.parametrize("prefetch", [False, True])
+def test_column_sharded_nccl_world1_matches_dense_and_oracle(prefetch):
     import torch.distributed as dist
 
     from paper_2208_05321_b200.distributed import ColumnShardedEmbedding
@@ -80,12 +81,15 @@ def test_column_sharded_nccl_world1_matches_dense_and_oracle():
         dense = table.copy()  # the oracle restatement of torch EmbeddingBag + SGD (float64 gradients)
         slots = oracle_slot_tables(trace)
         moved = 0
+        tids = [torch.from_numpy(trace[s]).cuda() for s in range(STEPS)]
         for s in range(STEPS):
-            out = mod(torch.from_numpy(trace[s]).cuda())
+            out = mod(tids[s])
             moved += mod.last_info.misses
             assert np.array_equal(shard.cache.slot_to_rank.cpu().numpy(), slots[s]), s
             want = oracle.pooled_bag(dense, trace[s], np.arange(B))
             np.testing.assert_allclose(out.detach().cpu().numpy(), want, rtol=1e-5, atol=1e-6)
+            if prefetch and s + 1 < STEPS:  # next batch's all-gather + prepare_begin overlap this backward
+                mod.prefetch(tids[s + 1])
             out.backward(torch.from_numpy(grads[s]).cuda())
             g = oracle.pooled_bag_backward_rows(grads[s], trace[s], np.arange(B), NUM)
             oracle.sparse_sgd(dense, np.unique(trace[s]), g, LR)
@@ -120,7 +124,7 @@ def _staged_module():
     return Staged
 
 
-def _rank_main(rank, world, port, q):
+def _rank_main(rank, world, port, q, prefetch=False):
     import torch.distributed as dist
 
     try:
@@ -133,11 +137,13 @@ def _rank_main(rank, world, port, q):
         per = B // world  # this rank's slice of every global batch
         slot_tables = []
         outs = []
+        tids = [torch.from_numpy(trace[s, rank * per:(rank + 1) * per]).cuda() for s in range(STEPS)]
         for s in range(STEPS):
-            ids = torch.from_numpy(trace[s, rank * per:(rank + 1) * per]).cuda()
-            out = mod(ids)
+            out = mod(tids[s])
             slot_tables.append(shard.cache.slot_to_rank.cpu().numpy())
             outs.append(out.detach().cpu().numpy())
+            if prefetch and s + 1 < STEPS:
+                mod.prefetch(tids[s + 1])
             out.backward(torch.from_numpy(grads[s, rank * per:(rank + 1) * per]).cuda())
         shard.flush()
         torch.cuda.synchronize()
@@ -153,7 +159,8 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_column_sharded_two_ranks_equal_world1_bitwise():
+@pytest.mark.parametrize("prefetch", [False, True])
+def test_column_sharded_two_ranks_equal_world1_bitwise(prefetch):
     import torch.multiprocessing as mp
 
     import paper_2208_05321_b200 as fc
@@ -163,7 +170,7 @@ def test_column_sharded_two_ranks_equal_world1_bitwise():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, prefetch)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict((r, (rows, st, outs)) for r, rows, st, outs in (q.get(timeout=300) for _ in range(world)))
