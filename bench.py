@@ -355,7 +355,8 @@ def ncu_traffic(kernel):
         return None
 
 
-def rooflines(prof, pool_ms, N, D, links, engine="async", pipelined=False, psw=False):
+def rooflines(prof, pool_ms, N, D, links, engine="async", pipelined=False, psw=False, bwd_ms=None, U=None,
+              adagrad=False):
     hbm, hbm_src = hbm_peak()
     xfer_ms = prof["transfer_ms"] / max(prof["transfer_launches"] if pipelined else prof["calls"], 1)
     xfer_bytes = prof["host_link_bytes"] / max(prof["calls"], 1)
@@ -386,6 +387,19 @@ def rooflines(prof, pool_ms, N, D, links, engine="async", pipelined=False, psw=F
                   "peak_source": hbm_src}
         r_pool["frac"] = r_pool["achieved"] / r_pool["peak"]
         out.append(r_pool)
+    if bwd_ms and U:
+        # fused backward + optimizer (radix grouping, k_bwd_stream, k_bwd_fixup): per occurrence
+        # its gradient row + sort key + order entry; per unique row a read-modify-write of the
+        # row (+ the Adagrad state row)
+        bwd_bytes = N * (4 * D + 8) + U * 8 * D * (2 if adagrad else 1)
+        bwd_avg = float(np.mean(bwd_ms))
+        r_bwd = {"kernel": "backward (k_os_hist + 2 x k_os_scatter + k_bwd_stream + k_bwd_fixup)", "bound": "hbm",
+                 "achieved": bwd_bytes / (bwd_avg * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                 "traffic": ncu_traffic("k_bwd_stream"),
+                 "traffic_note": "ncu DRAM bytes of k_bwd_stream alone", "algorithmic_bytes_per_launch": bwd_bytes,
+                 "launch_ms": bwd_avg, "peak_source": hbm_src}
+        r_bwd["frac"] = r_bwd["achieved"] / r_bwd["peak"]
+        out.append(r_bwd)
     out.sort(key=lambda r: -r["launch_ms"])
     return out
 
@@ -583,7 +597,7 @@ def run_ours(args, cfg, torch, rank, world):
         tp.export_chrome_trace(os.environ["FC_TORCH_TRACE"])
     # ---- the same kernels isolated: KSTEPS synchronous steps (no prefetch overlap), so the
     # roofline of each kernel is also reported without the host-link interference
-    prof_iso, p_ms_iso = None, []
+    prof_iso, p_ms_iso, b_ms_iso = None, [], []
     if pipelined and not sharded:
         dc.prepare_commit()  # the batch prefetched by the last profiled step is executed first
         pipelined = False
@@ -595,6 +609,7 @@ def run_ours(args, cfg, torch, rank, world):
         prof_iso = dc.profile(False)
         pipelined = True
         p_ms_iso = [e[0].elapsed_time(e[1]) for e in pool_ms[n_contended:]]
+        b_ms_iso = [e[1].elapsed_time(e[2]) for e in pool_ms[n_contended:]]
         del pool_ms[n_contended:]
         del stats[-KSTEPS:]
         dc.prepare_begin(bview[W + K + 2 * KSTEPS], W + K + 2 * KSTEPS, ready=ids_ready)
@@ -685,8 +700,11 @@ def run_ours(args, cfg, torch, rank, world):
 
     st_arr = np.array(stats_main, dtype=np.float64)
     uniq, hits, misses, evict, wb = st_arr.mean(axis=0)
-    rl = rooflines(prof, p_ms, N, D, links, args.engine, pipelined, psw is not None)
-    rl_iso = rooflines(prof_iso, p_ms_iso, N, D, links, args.engine, False, psw is not None) if prof_iso else None
+    train = args.step == "train" and not sharded
+    ada = OPT == "adagrad"
+    rl = rooflines(prof, p_ms, N, D, links, args.engine, pipelined, psw is not None, b_ms if train else None, uniq, ada)
+    rl_iso = rooflines(prof_iso, p_ms_iso, N, D, links, args.engine, False, psw is not None,
+                       b_ms_iso if train else None, uniq, ada) if prof_iso else None
     lookups = N * world  # every rank processes its own B x F ids per step
     res = {
         "metric": METRIC, "value": lookups * K / (total_ms * 1e-3), "unit": "lookups/s", "n_gpus": world,
@@ -718,6 +736,7 @@ def run_ours(args, cfg, torch, rank, world):
                 else f"{type(mod).__name__}.forward(pinned host ids) + prefetch(next ids) + out.backward(grad)"},
         "gpu_launches": launches_per_step(args, shard_mode, pipelined, world) * K,
         "roofline": rl[0], "roofline_secondary": rl[1] if len(rl) > 1 else None,
+        "roofline_all": {r["kernel"]: r for r in rl},
         "roofline_isolated": ({"note": "same kernels in synchronous steps (no prefetch overlap), after the "
                                        "timed region", **{r["kernel"]: r for r in rl_iso}} if rl_iso else None),
         "host_link": links,

@@ -179,6 +179,26 @@ int fc_prepare_commit(fc_cache* h, void* stream, fc_prepare_info* info);
  * waits for that commit's kernels. 0 after a synchronous fc_prepare. */
 int fc_last_writebacks(fc_cache* h, int64_t* rows);
 
+/* Memory report (replaces CacheStack.memory_report, cache_manager.py:553-562, which counts
+ * fast rows + the 64 MiB TransferBuffer + index arrays): every device allocation the
+ * cache holds, by category, so the total matches the device memory it takes. The staging
+ * buffers start at buffer_bytes worth of rows and grow only when a batch needs more.
+ * out[] needs FC_MEM_FIELDS entries (bytes unless noted). */
+enum {
+  FC_MEM_FAST_ROWS = 0,        /* cached rows (+ optimizer state) [C, D+S] */
+  FC_MEM_ID_SPACE = 1,         /* id/rank-space arrays: rank_of, rank_to_slot, aux, pending marks */
+  FC_MEM_BITMAPS = 2,          /* residency / per-batch / free-slot bitmaps */
+  FC_MEM_SLOT_SPACE = 3,       /* slot tables, per-slot lists, counters, pipeline index lists */
+  FC_MEM_STAGING = 4,          /* write-back and admission stages in HBM */
+  FC_MEM_SCRATCH = 5,          /* backward / scatter_update scratch (grown on demand) */
+  FC_MEM_TOTAL_DEVICE = 6,     /* sum of the above */
+  FC_MEM_PINNED_STAGING = 7,   /* pinned host staging of the write-back (not the slow tier) */
+  FC_MEM_WB_STAGE_ROWS = 8,    /* rows per write-back stage buffer (count) */
+  FC_MEM_ADMIT_STAGE_ROWS = 9, /* rows per admission stage buffer (count) */
+  FC_MEM_FIELDS = 10
+};
+int fc_memory_bytes(fc_cache* h, int64_t* out, int32_t n_out);
+
 /* Event-log payload of the last prepare (CacheEvent, cache_manager.py:78-99):
  * evicted ranks (descending) and admitted ranks (ascending), device -> host. */
 int fc_last_events(fc_cache* h, int64_t* evicted_host, int64_t* admitted_host, void* stream);

@@ -71,6 +71,7 @@ _SIGS = {
                                    c_void_p, c_void_p, c_void_p]),
     "fc_prepare_commit": (c_int32, [c_void_p, c_void_p, POINTER(PrepareInfo)]),
     "fc_last_writebacks": (c_int32, [c_void_p, POINTER(c_int64)]),
+    "fc_memory_bytes": (c_int32, [c_void_p, POINTER(c_int64), c_int32]),
     "fc_build_reorder": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                    POINTER(c_int64), c_void_p]),
     "fc_router_create": (c_int32, [c_int64, c_int32, c_int32, POINTER(c_void_p)]),

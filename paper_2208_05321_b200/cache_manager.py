@@ -538,8 +538,14 @@ class CacheStack:
         return None
 
     def memory_report(self) -> dict:
-        rows = self.fast.nbytes
-        buf = self.transmitter.buffer.capacity_bytes
-        index = self.state.index_bytes
-        return {"fast_rows_bytes": int(rows), "buffer_bytes": int(buf), "index_bytes": int(index),
-                "peak_fast_tier_bytes": int(rows + buf + index)}
+        """The reference's keys (cache_manager.py:553-562) filled with what the device cache
+        really holds: fast_rows_bytes = cached rows (+ optimizer state); buffer_bytes = the
+        HBM staging buffers (bounded like the reference's TransferBuffer, grown only when a
+        batch needs more) + scratch; index_bytes = every id-, slot- and bitmap-space array;
+        peak_fast_tier_bytes = their sum = all device memory the cache allocated. `device`
+        breaks it down (fc_memory_bytes)."""
+        m = self.device.memory()
+        buf = m["staging_bytes"] + m["scratch_bytes"]
+        index = m["id_space_bytes"] + m["bitmap_bytes"] + m["slot_space_bytes"]
+        return {"fast_rows_bytes": m["fast_rows_bytes"], "buffer_bytes": buf, "index_bytes": index,
+                "peak_fast_tier_bytes": m["device_total_bytes"], "device": m}

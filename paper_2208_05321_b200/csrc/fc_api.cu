@@ -255,8 +255,6 @@ int fc_create(int64_t num_ids, int64_t capacity, int32_t dim, int32_t state_widt
   A(h->evicted_ranks, C);
   A(h->victim_slots, C);
   A(h->wb_ranks, C);
-  A(h->wb_stage, C * dim);
-  if (state_width) A(h->wb_stage_state, C * state_width);
   A(h->admitted_ranks, C);
   A(h->target_slots, C);
   A(h->block_cnt, kMaxScanBlocks + 1);
@@ -544,6 +542,26 @@ int fc_prepare_commit(fc_cache* h, void* stream, fc_prepare_info* info) {
       break;
   }
   return rc;
+}
+
+int fc_memory_bytes(fc_cache* h, int64_t* out, int32_t n_out) {
+  if (!h || !out || n_out < FC_MEM_FIELDS) return FC_ERR_BAD_ARG;
+  int64_t e[6];
+  engine_memory(h, e);
+  const int64_t C = h->capacity, N = h->num_ids;
+  int64_t v[FC_MEM_FIELDS] = {};
+  v[FC_MEM_FAST_ROWS] = 4 * C * (int64_t)(h->dim + (h->fast_state ? h->sw : 0));
+  v[FC_MEM_ID_SPACE] = 3 * 4 * N + e[1];  // rank_of, rank_to_slot, aux (+ pending marks)
+  v[FC_MEM_BITMAPS] = 4 * 4 * h->nw_ids + 4 * h->nw_slots;
+  v[FC_MEM_SLOT_SPACE] = C * (4 + 1 + 4 * 5) + 2 * 4 * (kMaxScanBlocks + 1) + (int64_t)sizeof(Counters) + e[2];
+  v[FC_MEM_STAGING] = e[0] + (h->wb_stage ? 4 * C * (int64_t)(h->dim + (h->wb_stage_state ? h->sw : 0)) : 0);
+  v[FC_MEM_SCRATCH] = (int64_t)h->scratch_bytes;
+  for (int i = 0; i < FC_MEM_TOTAL_DEVICE; ++i) v[FC_MEM_TOTAL_DEVICE] += v[i];
+  v[FC_MEM_PINNED_STAGING] = e[3];
+  v[FC_MEM_WB_STAGE_ROWS] = e[4];
+  v[FC_MEM_ADMIT_STAGE_ROWS] = e[5];
+  for (int i = 0; i < FC_MEM_FIELDS; ++i) out[i] = v[i];
+  return FC_OK;
 }
 
 int fc_last_writebacks(fc_cache* h, int64_t* rows) {

@@ -66,7 +66,9 @@ struct Job {
 };
 
 struct AsyncWB {
-  int32_t* pending = nullptr;   // device int32[num_ids], -1 or buf*C + k
+  int32_t* pending = nullptr;   // device int32[num_ids], -1 or buf*rows + k
+  int32_t rows = 0;             // rows per write-back stage buffer (grown on demand, engine_grow)
+  int grows = 0;
   float* stage[kWbBufs] = {};
   float* sstage[kWbBufs] = {};
   int32_t* sranks[kWbBufs] = {};
@@ -442,6 +444,84 @@ static bool vec_ok_engine(fc_cache* h) {
   return v;
 }
 
+#define FC_TRY_A(expr)     \
+  do {                     \
+    int rc__ = (expr);     \
+    if (rc__) return rc__; \
+  } while (0)
+
+// Staging buffers are bounded like the reference's TransferBuffer (transmitter.py:19,75-94):
+// they start at buffer_bytes worth of rows (64 MiB by default) and grow only when a batch
+// needs more (engine_grow / pipe_grow_admission), instead of holding capacity-sized copies.
+// FC_STAGE_ROWS forces the initial row count (tests exercise the overflow paths with it).
+int32_t initial_stage_rows(const fc_cache* h) {
+  int64_t r = h->buffer_bytes / std::max<int64_t>(1, 4 * (int64_t)(h->dim + h->sw));
+  r = std::max<int64_t>(r, 1024);
+  if (const char* env = std::getenv("FC_STAGE_ROWS")) r = std::max<int64_t>(1, std::atoll(env));
+  return (int32_t)std::min<int64_t>(r, h->capacity);
+}
+
+static void free_wb_stages(AsyncWB* a) {
+  for (int b = 0; b < kWbBufs; ++b) {
+    cudaFree(a->stage[b]);
+    cudaFree(a->sranks[b]);
+    cudaFree(a->sstage[b]);
+    cudaFreeHost(a->hstage[b]);
+    cudaFreeHost(a->hranks[b]);
+    cudaFreeHost(a->hsstage[b]);
+    a->stage[b] = a->sstage[b] = a->hstage[b] = a->hsstage[b] = nullptr;
+    a->sranks[b] = a->hranks[b] = nullptr;
+  }
+  a->rows = 0;
+}
+
+static cudaError_t alloc_wb_stages(AsyncWB* a, const fc_cache* h, int32_t rows) {
+  const size_t R = (size_t)rows;
+  cudaError_t e = cudaSuccess;
+  for (int b = 0; b < kWbBufs && e == cudaSuccess; ++b) {
+    e = cudaMalloc(&a->stage[b], R * h->dim * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&a->sranks[b], R * 4);
+    if (e == cudaSuccess) e = cudaHostAlloc(&a->hstage[b], R * h->dim * 4, cudaHostAllocDefault);
+    if (e == cudaSuccess) e = cudaHostAlloc(&a->hranks[b], R * 4, cudaHostAllocDefault);
+    if (e == cudaSuccess && h->sw) e = cudaMalloc(&a->sstage[b], R * h->sw * 4);
+    if (e == cudaSuccess && h->sw) e = cudaHostAlloc(&a->hsstage[b], R * h->sw * 4, cudaHostAllocDefault);
+  }
+  if (e == cudaSuccess) a->rows = rows;
+  return e;
+}
+
+// Make every write-back stage hold `need` rows: wait for every queued job (the slow tier is
+// then authoritative, so all pending marks are dropped), then reallocate the buffers.
+// Rare: a batch evicting more rows than any before it.
+int engine_grow(fc_cache* h, int64_t need) {
+  AsyncWB* a = h->awb;
+  if (!a || need <= a->rows) return FC_OK;
+  FC_TRY_A(engine_drain(h));
+  FC_CUDA(cudaDeviceSynchronize());  // no kernel reads a stage or a pending mark any more
+  const int64_t grown = std::min<int64_t>(h->capacity, std::max<int64_t>(need + need / 4, 2 * (int64_t)a->rows));
+  free_wb_stages(a);
+  FC_CUDA(alloc_wb_stages(a, h, (int32_t)grown));
+  FC_CUDA(cudaMemset(a->pending, 0xff, (size_t)h->num_ids * 4));
+  for (int b = 0; b < kWbBufs; ++b) {
+    a->rows_in[b] = 0;
+    a->rows_on_dev[b] = false;
+  }
+  a->grows += 1;
+  return FC_OK;
+}
+
+// Synchronous prepare: the eviction count is known on the device only. When the batch could
+// evict more rows than a stage holds (min(n, C) > rows), read it back before the eviction
+// kernel and grow first; otherwise no host round trip.
+int engine_reserve(fc_cache* h, int64_t n, cudaStream_t st) {
+  AsyncWB* a = h->awb;
+  if (!a || std::min<int64_t>(n, h->capacity) <= a->rows) return FC_OK;
+  FC_CUDA(cudaMemcpyAsync(h->ctr_host, h->ctr, sizeof(Counters), cudaMemcpyDeviceToHost, st));
+  FC_CUDA(cudaStreamSynchronize(st));
+  if (h->ctr_host->err == 0 && h->ctr_host->needed > a->rows) return engine_grow(h, h->ctr_host->needed);
+  return FC_OK;
+}
+
 int engine_set(fc_cache* h, int engine) {
   if (engine == h->engine) return FC_OK;
   if (engine == 0) {
@@ -456,7 +536,7 @@ int engine_set(fc_cache* h, int engine) {
     set_error("attach the slow tier before selecting the async engine");
     return FC_ERR_NO_SLOW_TIER;
   }
-  if ((int64_t)h->capacity * kWbBufs > INT32_MAX) {
+  if ((int64_t)h->capacity * kWbBufs > INT32_MAX) {  // stage rows <= capacity
     set_error("capacity too large for the async engine's pending-row encoding");
     return FC_ERR_BAD_ARG;
   }
@@ -464,19 +544,13 @@ int engine_set(fc_cache* h, int engine) {
   a->h = h;
   a->vec = vec_ok_engine(h);
   a->device = h->device;
-  const size_t C = (size_t)h->capacity;
   cudaError_t e = cudaMalloc(&a->pending, (size_t)h->num_ids * 4);
   if (e == cudaSuccess) e = cudaMemset(a->pending, 0xff, (size_t)h->num_ids * 4);
+  if (e == cudaSuccess) e = alloc_wb_stages(a, h, initial_stage_rows(h));
   for (int b = 0; b < kWbBufs && e == cudaSuccess; ++b) {
-    e = cudaMalloc(&a->stage[b], C * h->dim * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&a->sranks[b], C * 4);
-    if (e == cudaSuccess) e = cudaHostAlloc(&a->hstage[b], C * h->dim * 4, cudaHostAllocDefault);
-    if (e == cudaSuccess) e = cudaHostAlloc(&a->hranks[b], C * 4, cudaHostAllocDefault);
-    if (e == cudaSuccess && h->sw) e = cudaMalloc(&a->sstage[b], C * h->sw * 4);
-    if (e == cudaSuccess && h->sw) e = cudaHostAlloc(&a->hsstage[b], C * h->sw * 4, cudaHostAllocDefault);
     // the dispatcher sleeps on these (a spinning cudaEventSynchronize would contend for
     // the driver with the caller's launches)
-    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&a->d2h[b], cudaEventDisableTiming | cudaEventBlockingSync);
+    e = cudaEventCreateWithFlags(&a->d2h[b], cudaEventDisableTiming | cudaEventBlockingSync);
   }
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->side, cudaStreamNonBlocking);
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->dside, cudaStreamNonBlocking);
@@ -533,7 +607,7 @@ int engine_begin(fc_cache* h, cudaStream_t st) {
     wait_seq(a, a->seq_of[b]);
     h->prof[5] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     k_clear_pending<<<grid_for(a->rows_in[b], kNT, kSMs * 4), kNT, 0, st>>>(
-        a->sranks[b], a->rows_in[b], a->pending, (int32_t)(b * h->capacity), h->capacity,
+        a->sranks[b], a->rows_in[b], a->pending, (int32_t)(b * a->rows), a->rows,
         a->rows_on_dev[b] ? a->dev_rows + b : nullptr);
     a->rows_in[b] = 0;
     a->rows_on_dev[b] = false;
@@ -568,7 +642,7 @@ static EngArgs eng_args(fc_cache* h) {
   }
   x.sranks = a->sranks[a->cur];
   x.buf = a->cur;
-  x.cap = h->capacity;
+  x.cap = a->rows;
   x.always = h->write_back == FC_WB_ALWAYS;
   x.c = h->ctr;
   x.ud = row_units(h->dim, a->vec);
@@ -675,15 +749,9 @@ void engine_release(fc_cache* h) {
   cudaFree(a->dev_rows);
   cudaFreeHost(a->hrows);
   if (a->done_host) cudaFreeHost((void*)a->done_host);
-  for (int b = 0; b < kWbBufs; ++b) {
-    cudaFree(a->stage[b]);
-    cudaFree(a->sranks[b]);
-    cudaFree(a->sstage[b]);
-    cudaFreeHost(a->hstage[b]);
-    cudaFreeHost(a->hranks[b]);
-    cudaFreeHost(a->hsstage[b]);
+  free_wb_stages(a);
+  for (int b = 0; b < kWbBufs; ++b)
     if (a->d2h[b]) cudaEventDestroy(a->d2h[b]);
-  }
   if (a->side) cudaStreamDestroy(a->side);
   if (a->dside) cudaStreamDestroy(a->dside);
   for (int b = 0; b < kWbBufs; ++b)
@@ -728,6 +796,14 @@ static inline int tma_pipe_blocks(int row_bytes) {
   const double per_block = (double)kTmaStages * tma_group_rows(row_bytes) * row_bytes;
   return std::max(32, std::min(64, (int)std::lround(2.5 * 1024 * 1024 / per_block)));
 }
+// Paced miss-staging rate (GB/s), FC_XFER_GBPS; 0 = unpaced (default). Alone, pacing the
+// staging below ~36 GB/s keeps every other kernel at its isolated speed
+// (profiles/r02_launch_latency.txt, runs 3-4), but in the pipeline the write-back's D2H copy
+// runs at the same time and its posted writes hold the staging's read requests in the same
+// upstream queue: with that copy beside it, even a 20 GB/s staging leaves kernel boundaries
+// at ~40 us (run 4). The in-pipeline sweep (profiles/r02_pace_sweep.txt) found no rate that
+// beats the unpaced ring, so pacing stays off.
+constexpr double kPacedGBps = 0.0;
 // the TMA ring must fit in shared memory (rows wider than ~12K floats use the SM kernels)
 static bool tma_fits(const fc_cache* h) {
   const size_t rb = (size_t)(h->dim + h->sw) * 4;
@@ -738,8 +814,11 @@ struct Pipe {
   IndexBufs ib[2];
   Counters* hctr[2] = {nullptr, nullptr};  // pinned mapped copies of the index counters
   Counters* hctr_dev[2] = {nullptr, nullptr};
-  float* astage[2] = {nullptr, nullptr};   // admission stage [C, D]
-  float* astage_s[2] = {nullptr, nullptr}; // [C, S]
+  float* astage[2] = {nullptr, nullptr};   // admission stage [arows, D]
+  float* astage_s[2] = {nullptr, nullptr}; // [arows, S]
+  int32_t arows = 0;                       // rows per admission stage (grown on demand)
+  int32_t scap[2] = {0, 0};                // rows the last staging of each parity staged at most
+  int grows = 0;
   cudaStream_t xfer = nullptr;             // transfer stream (k_admit_stage)
   cudaEvent_t ev_index[2] = {nullptr, nullptr};
   cudaEvent_t ev_xfer[2] = {nullptr, nullptr};
@@ -754,6 +833,7 @@ struct Pipe {
   bool defer_xfer = false;                 // launch the staging after the next row update (fc_backward_update)
   bool tma = false;                        // stage through the bulk-copy engine (k_admit_stage_tma)
   int tma_blocks = kTmaBlocks;
+  double xfer_gbps = 0.0;                  // paced staging rate (GB/s = B/ns); 0: unpaced
   bool xfer_pending = false;
   bool xfer_behind = false;                // the pending staging was begun behind an uncommitted prepare:
                                            // only that prepare's commit may launch it
@@ -814,6 +894,7 @@ static int pipe_create(fc_cache* h) {
   std::memset(q->ib, 0, sizeof(q->ib));
   h->pipe = q;
   const size_t C = (size_t)h->capacity;
+  q->arows = initial_stage_rows(h);
   cudaError_t e = cudaSuccess;
   for (int p = 0; p < 2 && e == cudaSuccess; ++p) {
     e = cudaMalloc(&q->ib[p].ctr, sizeof(Counters));
@@ -822,8 +903,8 @@ static int pipe_create(fc_cache* h) {
     if (e == cudaSuccess) e = cudaMalloc(&q->ib[p].vslots, C * 4);
     if (e == cudaSuccess) e = cudaMalloc(&q->ib[p].admitted, C * 4);
     if (e == cudaSuccess) e = cudaMalloc(&q->ib[p].target, C * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&q->astage[p], C * h->dim * 4);
-    if (e == cudaSuccess && h->sw) e = cudaMalloc(&q->astage_s[p], C * h->sw * 4);
+    if (e == cudaSuccess) e = cudaMalloc(&q->astage[p], (size_t)q->arows * h->dim * 4);
+    if (e == cudaSuccess && h->sw) e = cudaMalloc(&q->astage_s[p], (size_t)q->arows * h->sw * 4);
     // mapped: the index phase publishes its counters with a kernel store instead of a
     // cudaMemcpy that would queue behind the write-back D2H on the copy engine
     if (e == cudaSuccess) e = cudaHostAlloc(&q->hctr[p], sizeof(Counters), cudaHostAllocMapped);
@@ -847,6 +928,8 @@ static int pipe_create(fc_cache* h) {
   if (const char* env = std::getenv("FC_XFER_TMA")) q->tma = q->tma && std::atoi(env) != 0;
   q->tma_blocks = tma_pipe_blocks((h->dim + h->sw) * 4);
   if (const char* env = std::getenv("FC_TMA_BLOCKS")) q->tma_blocks = std::max(1, std::atoi(env));
+  q->xfer_gbps = kPacedGBps;
+  if (const char* env = std::getenv("FC_XFER_GBPS")) q->xfer_gbps = std::max(0.0, std::atof(env));
 
   q->xfer_blocks = kSMs;
   if (const char* env = std::getenv("FC_XFER_BLOCKS")) q->xfer_blocks = std::max(1, std::atoi(env));
@@ -877,7 +960,8 @@ struct PipeArgs {
   float* astage;
   float* astage_s;
   int buf;
-  int32_t cap;
+  int32_t cap;   // rows per write-back stage (pending-mark encoding)
+  int32_t acap;  // rows per admission stage: admitted rows past it are copied at commit
   int always;
   Counters* c;
   Units ud, us;
@@ -896,7 +980,7 @@ __global__ void k_publish(const Counters* __restrict__ c, Counters* host) {
 template <bool VEC>
 __global__ void __launch_bounds__(kNT) k_admit_stage(PipeArgs x) {
   if (!gate_open(x.c, G_ADMIT)) return;
-  const int m = x.c->misses;
+  const int m = min(x.c->misses, x.acap);  // the rest is copied by k_admit_commit
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
@@ -924,12 +1008,26 @@ __global__ void __launch_bounds__(kNT) k_admit_stage(PipeArgs x) {
 // contiguous). Measured (tools/interference_bench.cu, profiles/r01_interference_bench_tma.txt):
 // 50 GB/s alone vs 43 for SM loads, and a concurrent HBM-bound kernel slows by ~5%
 // instead of ~4x — the miss staging can overlap the backward.
-__global__ void __launch_bounds__(32) k_admit_stage_tma(PipeArgs x, int G) {
+// Pacing (gap_ns > 0): this block queues its k-th group no earlier than t0 + k * gap_ns
+// (%globaltimer), so the staging offers the host link a fixed request rate instead of as
+// many bulk copies as the ring allows. Unpaced, the requests queue up in front of the
+// link (it serves random 512 B reads at ~42 GB/s), and while that queue exists every
+// kernel boundary and memory fence anywhere on the GPU waits behind it: 60-100 us per
+// launch instead of ~4 (tools/launch_latency.cu, profiles/r02_launch_latency.txt). Paced
+// just below the link's rate the queue never forms and the index phase, pooled gather
+// and backward that run beside the staging keep their isolated speed.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(32) k_admit_stage_tma(PipeArgs x, int G, unsigned gap_ns) {
   extern __shared__ __align__(128) unsigned char ring[];  // kTmaStages x G x (D + S) floats
   __shared__ uint64_t bar[kTmaStages];
   const int lane = threadIdx.x;
   if (!gate_open(x.c, G_ADMIT)) return;
-  const int m = x.c->misses;
+  const int m = min(x.c->misses, x.acap);  // the rest is copied by k_admit_commit
   const unsigned rb = (unsigned)x.D * 4, sb = (unsigned)x.S * 4;
   const size_t stage_bytes = (size_t)G * (rb + sb);
   if (lane == 0) {
@@ -945,8 +1043,27 @@ __global__ void __launch_bounds__(32) k_admit_stage_tma(PipeArgs x, int G) {
   // row per lane), lane 0 arms the stage's mbarrier, every lane queues its own row.
   int issued = 0, retired = 0;
   const int mine = ngroups > (int)blockIdx.x ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  // blocks start staggered across one gap so the link sees an even request stream
+  const unsigned long long t0 =
+      gap_ns ? __shfl_sync(FC_FULL, global_ns(), 0) + (unsigned long long)blockIdx.x * gap_ns / gridDim.x : 0ull;
   while (retired < mine) {
-    if (issued < mine && issued - retired < kTmaStages) {
+    const bool slot_free = issued < mine && issued - retired < kTmaStages;
+    bool due = true;
+    if (gap_ns && slot_free) due = __shfl_sync(FC_FULL, global_ns(), 0) >= t0 + (unsigned long long)issued * gap_ns;
+    if (slot_free && !due && issued == retired) continue;  // nothing in flight: wait for the clock
+    if (slot_free && !due) {  // something in flight: retire it if it has landed, else keep polling
+      unsigned done = 0;
+      if (lane == 0) {
+        const int st0 = retired % kTmaStages;
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(&bar[st0])), "r"((phase_bits >> st0) & 1u)
+            : "memory");
+      }
+      if (!__shfl_sync(FC_FULL, done, 0)) continue;
+    }
+    if (slot_free && due) {
       const int st = issued % kTmaStages;
       if (issued >= kTmaStages) {  // the stage's previous bulk store has finished reading it
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -1120,8 +1237,18 @@ __global__ void __launch_bounds__(kNT) k_admit_commit(PipeArgs x) {
     const int64_t j = base + lane;
     const bool act = j < m;
     const int t = act ? x.target[j] : 0;
-    warp_copy_rows<VEC>(x.astage + j * x.D, x.fast + (int64_t)t * x.D, act, x.ud);
-    if (x.S) warp_copy_rows<VEC>(x.astage_s + j * x.S, x.fstate + (int64_t)t * x.S, act, x.us);
+    // rows past the admission stage (a batch with more misses than it holds; the stage grows
+    // after this commit) come straight from their newest copy, as the synchronous path does
+    const float* src = x.astage + j * x.D;
+    const float* ssrc = x.S ? x.astage_s + j * x.S : nullptr;
+    if (act && j >= x.acap) {
+      const int r = x.admitted[j];
+      const int pk = x.pending[r];
+      src = pk >= 0 ? x.wstage[pk / x.cap] + (int64_t)(pk % x.cap) * x.D : x.slow + (int64_t)r * x.ld;
+      if (x.S) ssrc = pk >= 0 ? x.wstage_s[pk / x.cap] + (int64_t)(pk % x.cap) * x.S : x.sstate + (int64_t)r * x.sld;
+    }
+    warp_copy_rows<VEC>(src, x.fast + (int64_t)t * x.D, act, x.ud);
+    if (x.S) warp_copy_rows<VEC>(ssrc, x.fstate + (int64_t)t * x.S, act, x.us);
     if (act) x.dirty[t] = 0;
   }
 }
@@ -1153,12 +1280,39 @@ static PipeArgs pipe_args(fc_cache* h, int p) {
   x.astage = q->astage[p];
   x.astage_s = q->astage_s[p];
   x.buf = a->cur;
-  x.cap = h->capacity;
+  x.cap = a->rows;
+  x.acap = q->scap[p];  // what this parity's staging was launched with (the stage may have grown since)
   x.always = h->write_back == FC_WB_ALWAYS;
   x.c = q->ib[p].ctr;
   x.ud = row_units(h->dim, a->vec);
   x.us = row_units(h->sw ? h->sw : 4, a->vec);
   return x;
+}
+
+// Admission stages for `need` rows from now on: after a device sync (no staging in flight),
+// new buffers take over the rows the old ones hold (a batch staged but not yet committed).
+static int pipe_grow_admission(fc_cache* h, int64_t need) {
+  Pipe* q = h->pipe;
+  if (need <= q->arows) return FC_OK;
+  FC_CUDA(cudaDeviceSynchronize());
+  const int64_t grown = std::min<int64_t>(h->capacity, std::max<int64_t>(need + need / 4, 2 * (int64_t)q->arows));
+  for (int p = 0; p < 2; ++p) {
+    float* nd = nullptr;
+    float* ns = nullptr;
+    FC_CUDA(cudaMalloc(&nd, (size_t)grown * h->dim * 4));
+    FC_CUDA(cudaMemcpy(nd, q->astage[p], (size_t)q->arows * h->dim * 4, cudaMemcpyDeviceToDevice));
+    cudaFree(q->astage[p]);
+    q->astage[p] = nd;
+    if (h->sw) {
+      FC_CUDA(cudaMalloc(&ns, (size_t)grown * h->sw * 4));
+      FC_CUDA(cudaMemcpy(ns, q->astage_s[p], (size_t)q->arows * h->sw * 4, cudaMemcpyDeviceToDevice));
+      cudaFree(q->astage_s[p]);
+      q->astage_s[p] = ns;
+    }
+  }
+  q->arows = (int32_t)grown;
+  q->grows += 1;
+  return FC_OK;
 }
 
 int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt, int32_t* uranks,
@@ -1250,6 +1404,7 @@ int pipe_launch_xfer(fc_cache* h, cudaStream_t after, bool from_update) {
     FC_CUDA(cudaEventRecord(q->ev_after, after));
     FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_after, 0));
   }
+  q->scap[p] = q->arows;
   PipeArgs x = pipe_args(h, p);
   harvest_xfer_time(h, p, true);  // this parity's previous staging (long finished) before its events are reused
   q->timed[p] = h->profile != 0;
@@ -1264,7 +1419,10 @@ int pipe_launch_xfer(fc_cache* h, cudaStream_t after, bool from_update) {
     const size_t smem = (size_t)kTmaStages * G * (h->dim + h->sw) * 4;
     if (smem > 48 * 1024)
       FC_CUDA(cudaFuncSetAttribute(k_admit_stage_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_admit_stage_tma<<<q->tma_blocks, 32, smem, q->xfer>>>(x, G);
+    // gap between one block's groups for the paced rate: blocks x group bytes / rate
+    const double group_bytes = (double)G * (h->dim + h->sw) * 4;
+    const unsigned gap = q->xfer_gbps > 0 ? (unsigned)(q->tma_blocks * group_bytes / q->xfer_gbps) : 0u;
+    k_admit_stage_tma<<<q->tma_blocks, 32, smem, q->xfer>>>(x, G, gap);
   } else if (h->awb->vec) {
     k_admit_stage<true><<<q->xfer_blocks, kNT, 0, q->xfer>>>(x);
   } else {
@@ -1315,6 +1473,7 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
     return c.err;
   }
   AsyncWB* a = h->awb;
+  if (c.needed > a->rows) FC_TRY_E(engine_grow(h, c.needed));  // more victims than a stage holds
   const int b = a->cur;
   if (a->rows_in[b] > 0) {  // write-back stage b still holds a job from kWbBufs commits ago
     // the stream (not the host) waits until the host threads have scattered that job;
@@ -1327,7 +1486,7 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
       h->prof[5] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
     k_clear_pending<<<grid_for(a->rows_in[b], kNT, kSMs * 4), kNT, 0, st>>>(
-        a->sranks[b], a->rows_in[b], a->pending, (int32_t)(b * h->capacity), h->capacity,
+        a->sranks[b], a->rows_in[b], a->pending, (int32_t)(b * a->rows), a->rows,
         a->rows_on_dev[b] ? a->dev_rows + b : nullptr);
     a->rows_in[b] = 0;
     a->rows_on_dev[b] = false;
@@ -1349,6 +1508,7 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
   FC_CUDA(cudaEventRecord(q->ev_commit[p], st));
   q->has_commit[p] = true;
   FC_TRY_E(launch_next_xfer());
+  if (c.misses > q->arows) FC_TRY_E(pipe_grow_admission(h, c.misses));  // this commit copied the overflow itself
   h->last_wb_dev = c.needed > 0 ? a->dev_rows + b : nullptr;
   if (c.needed > 0) {  // ship the write-back stage (upper bound: every victim) D2H on the side stream
     {  // the dispatcher must have consumed d2h[b] of the previous job on stage b before it is re-recorded
@@ -1410,6 +1570,26 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
     h->prof[4] += 4.0 * (h->dim + h->sw) * (double)c.needed;
   }
   return FC_OK;
+}
+
+// Device / pinned-host bytes the engine and the pipeline hold (fc_memory_bytes):
+// out = {stage bytes (device), id-space bytes (pending marks), other device bytes,
+//        pinned host staging bytes, write-back stage rows, admission stage rows}
+void engine_memory(const fc_cache* h, int64_t* out) {
+  for (int i = 0; i < 6; ++i) out[i] = 0;
+  const int64_t rb = 4 * (int64_t)(h->dim + h->sw);
+  if (const AsyncWB* a = h->awb) {
+    out[0] += kWbBufs * (int64_t)a->rows * (rb + 4);
+    out[1] += 4 * h->num_ids;
+    out[2] += kWbBufs * 4;
+    out[3] += kWbBufs * (int64_t)a->rows * (rb + 4);
+    out[4] = a->rows;
+  }
+  if (const Pipe* q = h->pipe) {
+    out[0] += 2 * (int64_t)q->arows * rb;
+    out[2] += 2 * (4 * 4 * (int64_t)h->capacity + (int64_t)sizeof(Counters));
+    out[5] = q->arows;
+  }
 }
 
 }  // namespace fc

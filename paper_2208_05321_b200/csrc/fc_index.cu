@@ -444,6 +444,7 @@ int launch_prepare(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32
   if (!row_fits)
     k_bts_before_evict<<<grid_for(h->capacity, kNT, kSMs * 4), kNT, 0, st>>>(
         h->evicted_ranks, h->rank_to_slot, h->dirty, h->write_back == FC_WB_ALWAYS, c);
+  if (h->engine == 1) FC_TRY_I(engine_reserve(h, n, st));  // grows the write-back stages if needed
   int rc = h->engine == 1 ? engine_evict(h, st) : launch_evict_rows(h, st);
   if (rc) return rc;
   if (!row_fits) k_bts_after_evict<<<1, 1, 0, st>>>(c);

@@ -99,7 +99,7 @@ struct fc_cache {
   int32_t* evicted_ranks;   // [C] descending
   int32_t* victim_slots;    // [C]
   int32_t* wb_ranks;        // [C] rank per staged write-back row or -1
-  float* wb_stage;          // [C, D]
+  float* wb_stage;          // [C, D] engine 0 only, allocated on its first eviction
   float* wb_stage_state;    // [C, S]
   int32_t* admitted_ranks;  // [C] ascending
   int32_t* target_slots;    // [C] ascending
@@ -151,6 +151,10 @@ int engine_after_prepare(fc_cache* h, cudaStream_t st);      // after the prepar
 int engine_drain(fc_cache* h);                               // all write-backs landed in the slow tier
 int engine_drain_stream(fc_cache* h, cudaStream_t st);       // the same, as a wait on `st`
 int engine_threads(const fc_cache* h);                       // host scatter threads of the async engine
+int engine_reserve(fc_cache* h, int64_t n, cudaStream_t st);  // sync prepare: stages hold this batch's victims
+int engine_grow(fc_cache* h, int64_t need);                  // write-back stages of >= need rows
+int32_t initial_stage_rows(const fc_cache* h);               // staging rows before any growth
+void engine_memory(const fc_cache* h, int64_t* out);          // engine + pipeline allocations (fc_memory_bytes)
 void engine_release(fc_cache* h);
 void engine_stats(fc_cache* h, double* out);                 // host scatter ms, jobs, rows, D2H bytes (then reset)
 // prefetch pipeline (fc_engine.cu)

@@ -298,7 +298,18 @@ __global__ void __launch_bounds__(kNT, 4) k_transfer_rows(RowCtx x, Units ud, Un
 
 static int rows_grid() { return kSMs * 8; }
 
+// engine 0's write-back stage (C rows): allocated the first time engine 0 evicts, so a
+// cache on the default async engine never holds it
+static int ensure_wb_stage(fc_cache* h) {
+  if (h->wb_stage) return FC_OK;
+  FC_CUDA(cudaMalloc(&h->wb_stage, (size_t)h->capacity * h->dim * 4));
+  if (h->sw) FC_CUDA(cudaMalloc(&h->wb_stage_state, (size_t)h->capacity * h->sw * 4));
+  return FC_OK;
+}
+
 int launch_evict_rows(fc_cache* h, cudaStream_t st) {
+  int rc = ensure_wb_stage(h);
+  if (rc) return rc;
   RowCtx x = row_ctx(h);
   const bool v = vec_ok(h);
   const Units ud = units_for(h->dim), us = units_for(h->sw ? h->sw : 4);
@@ -309,6 +320,8 @@ int launch_evict_rows(fc_cache* h, cudaStream_t st) {
 }
 
 int launch_transfer_rows(fc_cache* h, cudaStream_t st) {
+  int rc = ensure_wb_stage(h);
+  if (rc) return rc;
   RowCtx x = row_ctx(h);
   const bool v = vec_ok(h);
   const Units ud = units_for(h->dim), us = units_for(h->sw ? h->sw : 4);

@@ -324,6 +324,17 @@ class DeviceCache:
         u = int(info.unique)
         return info, buf[:u], buf[k:k + u], buf[2 * k:2 * k + u], buf[3 * k:3 * k + u], buf[4 * k:], d_ids
 
+    MEM_FIELDS = ("fast_rows_bytes", "id_space_bytes", "bitmap_bytes", "slot_space_bytes", "staging_bytes",
+                  "scratch_bytes", "device_total_bytes", "pinned_staging_bytes", "wb_stage_rows",
+                  "admission_stage_rows")
+
+    def memory(self) -> dict:
+        """Every device allocation of this cache by category (fc_memory_bytes), plus the
+        pinned host staging and the current staging row counts."""
+        out = (ctypes.c_int64 * len(self.MEM_FIELDS))()
+        check(self.lib.fc_memory_bytes(self.h, out, len(self.MEM_FIELDS)))
+        return {k: int(v) for k, v in zip(self.MEM_FIELDS, out)}
+
     def last_writebacks(self) -> int:
         """Rows written back by the last commit (waits for its kernels)."""
         v = ctypes.c_int64()

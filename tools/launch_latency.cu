@@ -23,7 +23,9 @@
 #include <chrono>
 #include <vector>
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
+namespace cg = cooperative_groups;
 
 #define CK(x)                                                                     \
   do {                                                                            \
@@ -83,6 +85,60 @@ __global__ void tma_gather(const char* __restrict__ host, char* __restrict__ dev
   asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// the same gather issued at a fixed rate: group k of block b no earlier than t0 + k * gap_ns
+__global__ void tma_paced(const char* __restrict__ host, char* __restrict__ dev, const int* __restrict__ idx,
+                          int nrows, unsigned gap_ns) {
+  constexpr int ST = 4;
+  extern __shared__ __align__(128) char ring[];
+  __shared__ uint64_t bar[ST];
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < ST; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&bar[s])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  const int ngroups = (nrows + 31) / 32;
+  const int mine = ngroups > (int)blockIdx.x ? (ngroups - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  unsigned ph = 0;
+  int issued = 0, retired = 0;
+  const unsigned long long t0 = gtimer() + (unsigned long long)blockIdx.x * gap_ns / gridDim.x;
+  while (retired < mine) {
+    if (issued < mine && issued - retired < ST && gtimer() >= t0 + (unsigned long long)issued * gap_ns) {
+      const int st = issued % ST;
+      if (issued >= ST) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      const int g = blockIdx.x + issued * gridDim.x;
+      const int r0 = g * 32, cnt = min(32, nrows - r0);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&bar[st])), "r"(cnt * 512)
+                   : "memory");
+      for (int r = 0; r < cnt; ++r)
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 512, [%2];" ::"r"(
+                su32(ring + (st * 32 + r) * 512)),
+            "l"(host + (long)idx[r0 + r] * 512), "r"(su32(&bar[st]))
+            : "memory");
+      ++issued;
+      continue;
+    }
+    if (issued == retired) continue;  // waiting for the pacing clock
+    const int st = retired % ST;
+    unsigned done = 0;
+    asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+                 : "=r"(done) : "r"(su32(&bar[st])), "r"((ph >> st) & 1u) : "memory");
+    if (!done) continue;
+    ph ^= 1u << st;
+    const int g = blockIdx.x + retired * gridDim.x;
+    const int r0 = g * 32, cnt = min(32, nrows - r0);
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dev + (long)r0 * 512),
+                 "r"(su32(ring + st * 32 * 512)), "r"(cnt * 512)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    ++retired;
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 __global__ void zc_gather(const float4* __restrict__ host, float4* __restrict__ dev, const int* __restrict__ idx,
                           int nrows) {
   const int lane = threadIdx.x & 31;
@@ -92,6 +148,49 @@ __global__ void zc_gather(const float4* __restrict__ host, float4* __restrict__ 
 }
 
 __global__ void tiny(int* c) { c[1] = c[0] + 1; }
+// 30 grid-wide barriers inside one cooperative kernel (one block per SM)
+__global__ void coop30(int* c) {
+  cg::grid_group g = cg::this_grid();
+  for (int i = 0; i < 30; ++i) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) c[1] = c[0] + i;
+    g.sync();
+  }
+}
+// 30 barriers of a hand-rolled flag barrier: one atomic + a spin on a generation word
+// mode 0: relaxed; 1: __threadfence() before arriving; 2: red.release.gpu arrive + ld.acquire.gpu spin
+__global__ void flagm(unsigned* bar, int mode) {
+  for (int i = 0; i < 30; ++i) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned target = (unsigned)(i + 1) * gridDim.x;
+      if (mode == 1) __threadfence();
+      if (mode == 2) {
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+        unsigned v;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+        } while (v < target);
+      } else {
+        atomicAdd(&bar[0], 1u);
+        while (atomicAdd(&bar[0], 0u) < target) {
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+__global__ void flag30(unsigned* bar) {
+  for (int i = 0; i < 30; ++i) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned target = (unsigned)(i + 1) * gridDim.x;
+      atomicAdd(&bar[0], 1u);
+      while (atomicAdd(&bar[0], 0u) < target) {
+      }
+    }
+    __syncthreads();
+  }
+}
 // one thread, 2000 dependent loads over an L2-resident ring: per-access latency
 __global__ void chase(const int* __restrict__ nxt, int* out) {
   int p = 0;
@@ -127,6 +226,10 @@ int main(int argc, char** argv) {
   float4 *ha, *hbuf;
   CK(cudaMalloc(&ha, hb));
   CK(cudaMalloc(&hbuf, hb));
+  unsigned* bar;
+  CK(cudaMalloc(&bar, 64));
+  char* dsrc;  // device-resident source for the control case (same random rows, 4 GiB)
+  CK(cudaMalloc(&dsrc, host_rows * 512));
   int* ctr;
   CK(cudaMalloc(&ctr, 64));
   char* dmem;
@@ -142,7 +245,11 @@ int main(int argc, char** argv) {
     CK(cudaMemcpy(dnext, nx.data(), n * 4, cudaMemcpyHostToDevice));
   }
   CK(cudaFuncSetAttribute(tma_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 512));
-  cudaStream_t bg, fg, gs;
+  CK(cudaFuncSetAttribute(tma_paced, cudaFuncAttributeMaxDynamicSharedMemorySize, 4 * 32 * 512));
+  cudaStream_t bg, fg, gs, bg2;
+  CK(cudaStreamCreateWithFlags(&bg2, cudaStreamNonBlocking));
+  char* hdst;  // pinned destination of the D2H background copies
+  CK(cudaHostAlloc(&hdst, (long)nrows * 512, cudaHostAllocDefault));
   CK(cudaStreamCreateWithFlags(&bg, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&fg, cudaStreamNonBlocking));
   CK(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
@@ -160,9 +267,20 @@ int main(int argc, char** argv) {
   CK(cudaGraphUpload(ge, fg));
   CK(cudaDeviceSynchronize());
 
-  auto launch_bg = [&](const std::string& kind, int blocks) {
+  auto launch_bg = [&](const std::string& kind0, int blocks) {
+    std::string kind = kind0;
+    if (kind.rfind("d2h", 0) == 0) {  // "d2h" alone, or "d2h+paced" with the paced gather beside it
+      for (int rep = 0; rep < 5; ++rep)
+        CK(cudaMemcpyAsync(hdst, dstage, (long)nrows * 512, cudaMemcpyDeviceToHost, bg2));
+      if (kind == "d2h") return;
+      kind = kind.substr(4);
+    }
     for (int rep = 0; rep < 5; ++rep) {
-      if (kind == "tma") tma_gather<<<blocks, 32, 4 * 32 * 512, bg>>>(hdev, dstage, didx, nrows);
+      if (kind == "paced") {  // 40 blocks, 16 KB groups: gap = 40 * 16 KB / rate
+        const unsigned gap = (unsigned)(40.0 * 16384.0 / blocks);  // ns (GB/s = B/ns)
+        tma_paced<<<40, 32, 4 * 32 * 512, bg>>>(hdev, dstage, didx, nrows, gap);
+      } else if (kind == "tmadev") tma_gather<<<blocks, 32, 4 * 32 * 512, bg>>>(dsrc, dstage, didx, nrows);
+      else if (kind == "tma") tma_gather<<<blocks, 32, 4 * 32 * 512, bg>>>(hdev, dstage, didx, nrows);
       else if (kind == "zc") zc_gather<<<blocks, 256, 0, bg>>>((const float4*)hdev, (float4*)dstage, didx, nrows);
       else if (kind == "dma") CK(cudaMemcpyAsync(dstage, host, (long)nrows * 512, cudaMemcpyHostToDevice, bg));
     }
@@ -184,7 +302,18 @@ int main(int argc, char** argv) {
       CK(cudaGraphLaunch(ge, fg));
     else if (c == "memset")
       for (int i = 0; i < 10; ++i) CK(cudaMemsetAsync(dmem, 0xff, 53 * 1024, fg));
-    else if (c == "chase")
+    else if (c == "coop30") {
+      void* a[] = {&ctr};
+      CK(cudaLaunchCooperativeKernel((const void*)coop30, 148, 256, a, 0, fg));
+    } else if (c == "flag30") {
+      CK(cudaMemsetAsync(bar, 0, 64, fg));
+      CK(cudaEventRecord(e0, fg));
+      flag30<<<148, 256, 0, fg>>>(bar);
+    } else if (c == "flagfence" || c == "flagrel") {
+      CK(cudaMemsetAsync(bar, 0, 64, fg));
+      CK(cudaEventRecord(e0, fg));
+      flagm<<<148, 256, 0, fg>>>(bar, c == "flagfence" ? 1 : 2);
+    } else if (c == "chase")
       chase<<<1, 1, 0, fg>>>(dnext, ctr + 4);
     else if (c == "hbm")
       hbm_copy<<<148 * 8, 256, 0, fg>>>(ha, hbuf, hb / 16);
@@ -194,11 +323,13 @@ int main(int argc, char** argv) {
     const char* kind;
     int blocks;
   };
-  const Bg bgs[] = {{"none", 0}, {"tma", 8}, {"tma", 16}, {"tma", 40}, {"tma", 148}, {"zc", 148}, {"dma", 0}};
-  const char* fgs[] = {"chain", "gated", "graph", "memset", "chase", "hbm"};
+  // paced: blocks = 40, the number is the target rate in GB/s
+  const Bg bgs[] = {{"none", 0}, {"paced", 30}, {"paced", 36}, {"d2h", 0}, {"d2h+paced", 20}, {"d2h+paced", 25},
+                    {"d2h+paced", 30}, {"d2h+paced", 36}, {"d2h+tma", 40}};
+  const char* fgs[] = {"chain", "flag30", "chase", "hbm"};
   // background throughput alone
   for (const Bg& b : bgs) {
-    if (std::string(b.kind) == "none") continue;
+    if (std::string(b.kind) == "none" || std::string(b.kind).rfind("d2h+", 0) == 0) continue;
     cudaEvent_t a0, a1;
     CK(cudaEventCreate(&a0));
     CK(cudaEventCreate(&a1));
