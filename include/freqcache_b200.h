@@ -182,7 +182,9 @@ int fc_last_writebacks(fc_cache* h, int64_t* rows);
 /* Memory report (replaces CacheStack.memory_report, cache_manager.py:553-562, which counts
  * fast rows + the 64 MiB TransferBuffer + index arrays): every device allocation the
  * cache holds, by category, so the total matches the device memory it takes. The staging
- * buffers start at buffer_bytes worth of rows and grow only when a batch needs more.
+ * buffers start at buffer_bytes worth of rows and grow only when a batch needs more. The
+ * cache's fixed arrays, the engine's stages and the pipeline's buffers are each carved from
+ * one allocation, so the total is exact up to the driver's own context memory.
  * out[] needs FC_MEM_FIELDS entries (bytes unless noted). */
 enum {
   FC_MEM_FAST_ROWS = 0,        /* cached rows (+ optimizer state) [C, D+S] */
@@ -191,11 +193,12 @@ enum {
   FC_MEM_SLOT_SPACE = 3,       /* slot tables, per-slot lists, counters, pipeline index lists */
   FC_MEM_STAGING = 4,          /* write-back and admission stages in HBM */
   FC_MEM_SCRATCH = 5,          /* backward / scatter_update scratch (grown on demand) */
-  FC_MEM_TOTAL_DEVICE = 6,     /* sum of the above */
-  FC_MEM_PINNED_STAGING = 7,   /* pinned host staging of the write-back (not the slow tier) */
-  FC_MEM_WB_STAGE_ROWS = 8,    /* rows per write-back stage buffer (count) */
-  FC_MEM_ADMIT_STAGE_ROWS = 9, /* rows per admission stage buffer (count) */
-  FC_MEM_FIELDS = 10
+  FC_MEM_ALLOC_SLACK = 6,      /* rounding of the allocations to the 2 MiB device pages */
+  FC_MEM_TOTAL_DEVICE = 7,     /* device memory the cache's allocations reserve: sum of the above */
+  FC_MEM_PINNED_STAGING = 8,   /* pinned host staging of the write-back (not the slow tier) */
+  FC_MEM_WB_STAGE_ROWS = 9,    /* rows per write-back stage buffer (count) */
+  FC_MEM_ADMIT_STAGE_ROWS = 10,/* rows per admission stage buffer (count) */
+  FC_MEM_FIELDS = 11
 };
 int fc_memory_bytes(fc_cache* h, int64_t* out, int32_t n_out);
 

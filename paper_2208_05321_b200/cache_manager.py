@@ -545,7 +545,7 @@ class CacheStack:
         peak_fast_tier_bytes = their sum = all device memory the cache allocated. `device`
         breaks it down (fc_memory_bytes)."""
         m = self.device.memory()
-        buf = m["staging_bytes"] + m["scratch_bytes"]
+        buf = m["staging_bytes"] + m["scratch_bytes"] + m["allocation_slack_bytes"]
         index = m["id_space_bytes"] + m["bitmap_bytes"] + m["slot_space_bytes"]
         return {"fast_rows_bytes": m["fast_rows_bytes"], "buffer_bytes": buf, "index_bytes": index,
                 "peak_fast_tier_bytes": m["device_total_bytes"], "device": m}

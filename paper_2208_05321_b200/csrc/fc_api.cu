@@ -133,20 +133,11 @@ struct DeviceGuard {
   }
 };
 
-template <class T>
-static int dalloc(T** p, size_t count) {
-  FC_CUDA(cudaMalloc(reinterpret_cast<void**>(p), std::max<size_t>(count, 1) * sizeof(T)));
-  return FC_OK;
-}
-
 static void release(fc_cache* h) {
   trace_clear(h);
   pipe_release(h);
   engine_release(h);
-  void* dev[] = {h->rank_of, h->rank_to_slot, h->slot_to_rank, h->dirty, h->fast, h->fast_state,
-                 h->res_bits, h->free_bits, h->id_bits, h->miss_bits, h->prot_bits, h->aux,
-                 h->evicted_ranks, h->victim_slots, h->wb_ranks, h->wb_stage, h->wb_stage_state,
-                 h->admitted_ranks, h->target_slots, h->block_cnt, h->block_cnt2, h->ctr, h->scratch};
+  void* dev[] = {h->arena, h->wb_stage, h->wb_stage_state, h->scratch};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (h->ctr_host) cudaFreeHost(h->ctr_host);
@@ -235,32 +226,36 @@ int fc_create(int64_t num_ids, int64_t capacity, int32_t dim, int32_t state_widt
   h->nw_slots = ((capacity + 31) / 32 + 3) / 4 * 4;
   const size_t C = (size_t)capacity;
   int rc = FC_OK;
-#define A(ptr, n)                  \
-  if ((rc = dalloc(&(ptr), (n)))) { \
-    release(h);                    \
-    return rc;                     \
+  Arena ar;
+  ar.add(&h->rank_of, num_ids);
+  ar.add(&h->rank_to_slot, num_ids);
+  ar.add(&h->aux, num_ids);
+  ar.add(&h->slot_to_rank, C);
+  ar.add(&h->dirty, C);
+  ar.add(&h->fast, C * dim);
+  if (state_width) ar.add(&h->fast_state, C * state_width);
+  ar.add(&h->res_bits, h->nw_ids);
+  ar.add(&h->id_bits, h->nw_ids);
+  ar.add(&h->miss_bits, h->nw_ids);
+  ar.add(&h->prot_bits, h->nw_ids);
+  ar.add(&h->free_bits, h->nw_slots);
+  ar.add(&h->evicted_ranks, C);
+  ar.add(&h->victim_slots, C);
+  ar.add(&h->wb_ranks, C);
+  ar.add(&h->admitted_ranks, C);
+  ar.add(&h->target_slots, C);
+  ar.add(&h->block_cnt, kMaxScanBlocks + 1);
+  ar.add(&h->block_cnt2, kMaxScanBlocks + 1);
+  ar.add(&h->ctr, 1);
+  {
+    const cudaError_t ea = ar.alloc(&h->arena);
+    if (ea != cudaSuccess) {
+      rc = cuda_fail(ea, "fc_create: device arrays");
+      release(h);
+      return rc;
+    }
+    h->arena_bytes = (int64_t)ar.bytes;
   }
-  A(h->rank_of, num_ids);
-  A(h->rank_to_slot, num_ids);
-  A(h->aux, num_ids);
-  A(h->slot_to_rank, C);
-  A(h->dirty, C);
-  A(h->fast, C * dim);
-  if (state_width) A(h->fast_state, C * state_width);
-  A(h->res_bits, h->nw_ids);
-  A(h->id_bits, h->nw_ids);
-  A(h->miss_bits, h->nw_ids);
-  A(h->prot_bits, h->nw_ids);
-  A(h->free_bits, h->nw_slots);
-  A(h->evicted_ranks, C);
-  A(h->victim_slots, C);
-  A(h->wb_ranks, C);
-  A(h->admitted_ranks, C);
-  A(h->target_slots, C);
-  A(h->block_cnt, kMaxScanBlocks + 1);
-  A(h->block_cnt2, kMaxScanBlocks + 1);
-  A(h->ctr, 1);
-#undef A
   cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&h->ctr_host), sizeof(Counters), cudaHostAllocDefault);
   if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->done, cudaEventDisableTiming);
   if (e == cudaSuccess) e = cudaMemset(h->rank_to_slot, 0xff, num_ids * 4);
@@ -546,17 +541,26 @@ int fc_prepare_commit(fc_cache* h, void* stream, fc_prepare_info* info) {
 
 int fc_memory_bytes(fc_cache* h, int64_t* out, int32_t n_out) {
   if (!h || !out || n_out < FC_MEM_FIELDS) return FC_ERR_BAD_ARG;
-  int64_t e[6];
+  int64_t e[7];
   engine_memory(h, e);
   const int64_t C = h->capacity, N = h->num_ids;
+  const int64_t wb0 = h->wb_stage ? 4 * C * (int64_t)(h->dim + (h->wb_stage_state ? h->sw : 0)) : 0;
   int64_t v[FC_MEM_FIELDS] = {};
   v[FC_MEM_FAST_ROWS] = 4 * C * (int64_t)(h->dim + (h->fast_state ? h->sw : 0));
   v[FC_MEM_ID_SPACE] = 3 * 4 * N + e[1];  // rank_of, rank_to_slot, aux (+ pending marks)
   v[FC_MEM_BITMAPS] = 4 * 4 * h->nw_ids + 4 * h->nw_slots;
-  v[FC_MEM_SLOT_SPACE] = C * (4 + 1 + 4 * 5) + 2 * 4 * (kMaxScanBlocks + 1) + (int64_t)sizeof(Counters) + e[2];
-  v[FC_MEM_STAGING] = e[0] + (h->wb_stage ? 4 * C * (int64_t)(h->dim + (h->wb_stage_state ? h->sw : 0)) : 0);
+  v[FC_MEM_STAGING] = e[0] + wb0;
   v[FC_MEM_SCRATCH] = (int64_t)h->scratch_bytes;
-  for (int i = 0; i < FC_MEM_TOTAL_DEVICE; ++i) v[FC_MEM_TOTAL_DEVICE] += v[i];
+  // what the allocations reserve: the arenas and the separately grown buffers in 2 MiB pages
+  int64_t reserved = reserved_bytes(h->arena_bytes) + e[6] + reserved_bytes(v[FC_MEM_SCRATCH]);
+  if (h->wb_stage) reserved += reserved_bytes(4 * C * (int64_t)h->dim);
+  if (h->wb_stage_state) reserved += reserved_bytes(4 * C * (int64_t)h->sw);
+  // slot tables, per-slot lists, counters and the 256-byte padding of the arenas' parts
+  v[FC_MEM_SLOT_SPACE] = h->arena_bytes - v[FC_MEM_FAST_ROWS] - 3 * 4 * N - v[FC_MEM_BITMAPS] + e[2];
+  int64_t sum = 0;
+  for (int i = 0; i < FC_MEM_ALLOC_SLACK; ++i) sum += v[i];
+  v[FC_MEM_ALLOC_SLACK] = reserved - sum;
+  v[FC_MEM_TOTAL_DEVICE] = reserved;
   v[FC_MEM_PINNED_STAGING] = e[3];
   v[FC_MEM_WB_STAGE_ROWS] = e[4];
   v[FC_MEM_ADMIT_STAGE_ROWS] = e[5];

@@ -28,13 +28,14 @@ constexpr int kBwdUnroll = 4;
 struct Grouping {
   uint32_t* keys;   // [n] sorted unique positions
   int32_t* order;   // [n] occurrence index of each sorted position
+  void* sort_scr;   // the radix sort's scratch (its zero-initialised state at the head)
   char* rest;
 };
 
 static size_t grouping_bytes(int64_t n) { return align16(n * 4) * 2 + align16(sort_scratch_bytes(n)); }
 
 static int build_grouping(void** scratch, size_t* scratch_bytes, const int32_t* inv, int64_t u, int64_t n,
-                          size_t extra, Grouping& g, cudaStream_t st) {
+                          size_t extra, Grouping& g, cudaStream_t st, bool state_zeroed = false) {
   int rc = ensure_scratch_buf(scratch, scratch_bytes, grouping_bytes(n) + extra);
   if (rc) return rc;
   char* p = static_cast<char*>(*scratch);
@@ -43,10 +44,11 @@ static int build_grouping(void** scratch, size_t* scratch_bytes, const int32_t* 
   g.order = reinterpret_cast<int32_t*>(p);
   p += align16(n * 4);
   void* sort_scr = p;
+  g.sort_scr = sort_scr;
   p += align16(sort_scratch_bytes(n));
   g.rest = p;
   return radix_sort_pairs(reinterpret_cast<const uint32_t*>(inv), nullptr, g.keys, g.order, n, key_bits_for(u),
-                          sort_scr, st);
+                          sort_scr, st, state_zeroed);
 }
 
 // ------------------------------------------------------------- scatter_update, bit-exact with np.add.at
@@ -74,6 +76,7 @@ int launch_scatter_update(fc_cache* h, const int32_t* uslots, const int32_t* inv
   if (u <= 0 || n <= 0) return FC_OK;
   Grouping g;
   const size_t extra = align16((u + 1) * 4) + align16(scan_scratch_bytes(u));
+  h->sort_zero_for = nullptr;  // this sort leaves its state behind
   int rc = build_grouping(&h->scratch, &h->scratch_bytes, inv, u, n, extra, g, st);
   if (rc) return rc;
   int32_t* seg = reinterpret_cast<int32_t*>(g.rest);
@@ -168,6 +171,8 @@ struct BwdArgs {
   uint8_t* dirty;
   OptArgs o;
   Units un;
+  uint32_t* zero;     // the fix-up clears these words (the next sort's state) when set
+  int64_t zero_words;
 };
 
 // One finished run of key `key` over sorted positions [a, b) of chunk c. A run that
@@ -208,6 +213,11 @@ __global__ void __launch_bounds__(kNT, 4) k_bwd_stream(BwdArgs x) {
   const int64_t nchunks = (x.n + kChunk - 1) / kChunk;
   for (int64_t c = warp; c < nchunks; c += nwarps) {
     const int64_t j0 = c * kChunk, j1 = min(x.n, j0 + kChunk);
+    // this chunk's two carry slots start empty (lane 0 may fill them in bwd_flush, later)
+    if (lane == 0) {
+      x.carry_key[c * 2] = -1;
+      x.carry_key[c * 2 + 1] = -1;
+    }
     const int prev_key = j0 > 0 ? (int)x.keys[j0 - 1] : -1;
     const int next_key = j1 < x.n ? (int)x.keys[j1] : -1;
     for (int cu0 = 0; cu0 < x.un.upr; cu0 += 32) {
@@ -361,6 +371,11 @@ __global__ void __launch_bounds__(kNT) k_bwd_fixup(BwdArgs x) {
     }
     __syncthreads();
   }
+  // the sort that produced keys/order is complete: clear its state for the next backward,
+  // which then queues no memset (a launch costs ~90 us beside the miss staging, DESIGN 4b)
+  if (x.zero)
+    for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < x.zero_words; i += (int64_t)gridDim.x * kNT)
+      x.zero[i] = 0u;
 }
 
 // optimizer step on every unique row, 32 rows per warp, kBwdUnroll units in flight
@@ -445,7 +460,8 @@ __global__ void __launch_bounds__(kNT) k_bwd_direct(BwdArgs x, const int32_t* __
 // k_bwd_apply (x.gu = per-unique sums, in `gu_out` when given, else in scratch).
 static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* inv, int64_t u, int64_t n,
                          const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw,
-                         int mode, const float* grad, int D, float* gu_out, BwdArgs& x, bool apply, cudaStream_t st) {
+                         int mode, const float* grad, int D, float* gu_out, BwdArgs& x, bool apply, cudaStream_t st,
+                         void** zero_for = nullptr, size_t* zero_bytes = nullptr) {
   if (D % 4 || (reinterpret_cast<uintptr_t>(grad) & 15) || (reinterpret_cast<uintptr_t>(gu_out) & 15)) {
     set_error("backward needs dim %% 4 == 0 and 16-byte aligned gradient rows");
     return FC_ERR_BAD_ARG;
@@ -459,9 +475,20 @@ static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* i
   const bool bags = offsets != nullptr;
   const size_t extra = (gu_out || apply ? 0 : align16((size_t)u * D * 4)) + align16(nchunks * 2 * (size_t)D * 4) +
                        2 * align16(nchunks * 2 * 4) + (bags ? 2 * align16(n * 4) : 0);
+  // sort state left zero by the previous fused backward on this scratch (no memset); this
+  // one's fix-up clears it again
+  const size_t state = sort_state_bytes(n, key_bits_for(u));
+  const bool zeroed = zero_for && *zero_for != nullptr && *zero_for == *scratch && *zero_bytes >= state &&
+                      grouping_bytes(n) + extra <= *scratch_bytes;
   Grouping g;
-  int rc = build_grouping(scratch, scratch_bytes, inv, u, n, extra, g, st);
+  int rc = build_grouping(scratch, scratch_bytes, inv, u, n, extra, g, st, zeroed);
+  if (zero_for) {  // valid again only once the fix-up below is queued
+    *zero_for = nullptr;
+    *zero_bytes = 0;
+  }
   if (rc) return rc;
+  x.zero = nullptr;
+  x.zero_words = 0;
   char* p = g.rest;
   x.gu = gu_out;
   if (!gu_out && !apply) {
@@ -493,7 +520,6 @@ static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* i
     x.bag_of = bag_of;
     x.coef = coef;
   }
-  FC_CUDA(cudaMemsetAsync(x.carry_key, 0xff, nchunks * 2 * 4, st));
   x.D = D;
   x.keys = g.keys;
   x.order = g.order;
@@ -507,7 +533,16 @@ static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* i
     k_bwd_stream<true><<<grid, kNT, 0, st>>>(x);
     if (fix_smem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_bwd_fixup<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                            (int)fix_smem));
+    if (zero_for) {
+      x.zero = static_cast<uint32_t*>(g.sort_scr);
+      x.zero_words = (int64_t)(state / 4);
+    }
     k_bwd_fixup<true><<<fgrid, kNT, fix_smem, st>>>(x);
+    if (zero_for) {
+      FC_CUDA(cudaGetLastError());
+      *zero_for = *scratch;
+      *zero_bytes = state;
+    }
   } else {
     k_bwd_stream<false><<<grid, kNT, 0, st>>>(x);
     if (fix_smem > 48 * 1024) FC_CUDA(cudaFuncSetAttribute(k_bwd_fixup<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -550,7 +585,7 @@ int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, cons
     return FC_OK;
   }
   int rc = segment_grads(&h->scratch, &h->scratch_bytes, inv, u, n, offsets, off_bytes, nbags, include_last, psw, mode,
-                         grad, D, nullptr, x, fused, st);
+                         grad, D, nullptr, x, fused, st, &h->sort_zero_for, &h->sort_zero_bytes);
   if (rc || fused) return rc;
   k_bwd_apply<<<grid_for(u, kNT, kSMs * 8), kNT, 0, st>>>(x, u);  // the unfused variant: per-row sums, then apply
   FC_CUDA(cudaGetLastError());

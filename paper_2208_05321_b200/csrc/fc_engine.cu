@@ -68,6 +68,10 @@ struct Job {
 struct AsyncWB {
   int32_t* pending = nullptr;   // device int32[num_ids], -1 or buf*rows + k
   int32_t rows = 0;             // rows per write-back stage buffer (grown on demand, engine_grow)
+  void* fixed_arena = nullptr;  // pending marks + dev_rows
+  int64_t fixed_bytes = 0;
+  void* stage_arena = nullptr;  // every stage / sstage / sranks buffer
+  int64_t stage_bytes = 0;
   int grows = 0;
   float* stage[kWbBufs] = {};
   float* sstage[kWbBufs] = {};
@@ -462,10 +466,10 @@ int32_t initial_stage_rows(const fc_cache* h) {
 }
 
 static void free_wb_stages(AsyncWB* a) {
+  if (a->stage_arena) cudaFree(a->stage_arena);
+  a->stage_arena = nullptr;
+  a->stage_bytes = 0;
   for (int b = 0; b < kWbBufs; ++b) {
-    cudaFree(a->stage[b]);
-    cudaFree(a->sranks[b]);
-    cudaFree(a->sstage[b]);
     cudaFreeHost(a->hstage[b]);
     cudaFreeHost(a->hranks[b]);
     cudaFreeHost(a->hsstage[b]);
@@ -477,13 +481,17 @@ static void free_wb_stages(AsyncWB* a) {
 
 static cudaError_t alloc_wb_stages(AsyncWB* a, const fc_cache* h, int32_t rows) {
   const size_t R = (size_t)rows;
-  cudaError_t e = cudaSuccess;
+  Arena ar;
+  for (int b = 0; b < kWbBufs; ++b) {
+    ar.add(&a->stage[b], R * h->dim);
+    if (h->sw) ar.add(&a->sstage[b], R * h->sw);
+    ar.add(&a->sranks[b], R);
+  }
+  cudaError_t e = ar.alloc(&a->stage_arena);
+  if (e == cudaSuccess) a->stage_bytes = (int64_t)ar.bytes;
   for (int b = 0; b < kWbBufs && e == cudaSuccess; ++b) {
-    e = cudaMalloc(&a->stage[b], R * h->dim * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&a->sranks[b], R * 4);
-    if (e == cudaSuccess) e = cudaHostAlloc(&a->hstage[b], R * h->dim * 4, cudaHostAllocDefault);
+    e = cudaHostAlloc(&a->hstage[b], R * h->dim * 4, cudaHostAllocDefault);
     if (e == cudaSuccess) e = cudaHostAlloc(&a->hranks[b], R * 4, cudaHostAllocDefault);
-    if (e == cudaSuccess && h->sw) e = cudaMalloc(&a->sstage[b], R * h->sw * 4);
     if (e == cudaSuccess && h->sw) e = cudaHostAlloc(&a->hsstage[b], R * h->sw * 4, cudaHostAllocDefault);
   }
   if (e == cudaSuccess) a->rows = rows;
@@ -544,7 +552,11 @@ int engine_set(fc_cache* h, int engine) {
   a->h = h;
   a->vec = vec_ok_engine(h);
   a->device = h->device;
-  cudaError_t e = cudaMalloc(&a->pending, (size_t)h->num_ids * 4);
+  Arena fx;
+  fx.add(&a->pending, (size_t)h->num_ids);
+  fx.add(&a->dev_rows, kWbBufs);
+  cudaError_t e = fx.alloc(&a->fixed_arena);
+  if (e == cudaSuccess) a->fixed_bytes = (int64_t)fx.bytes;
   if (e == cudaSuccess) e = cudaMemset(a->pending, 0xff, (size_t)h->num_ids * 4);
   if (e == cudaSuccess) e = alloc_wb_stages(a, h, initial_stage_rows(h));
   for (int b = 0; b < kWbBufs && e == cudaSuccess; ++b) {
@@ -556,7 +568,6 @@ int engine_set(fc_cache* h, int engine) {
   if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&a->dside, cudaStreamNonBlocking);
   for (int b = 0; b < kWbBufs && e == cudaSuccess; ++b)
     e = cudaEventCreateWithFlags(&a->cev[b], cudaEventDisableTiming | cudaEventBlockingSync);
-  if (e == cudaSuccess) e = cudaMalloc(&a->dev_rows, kWbBufs * sizeof(int32_t));
   if (e == cudaSuccess) e = cudaHostAlloc((void**)&a->done_host, 64, cudaHostAllocMapped);
   if (e == cudaSuccess) {
     *a->done_host = 0;
@@ -745,8 +756,7 @@ void engine_release(fc_cache* h) {
   a->cv_help.notify_all();
   for (auto& t : a->helpers)
     if (t.joinable()) t.join();
-  cudaFree(a->pending);
-  cudaFree(a->dev_rows);
+  if (a->fixed_arena) cudaFree(a->fixed_arena);
   cudaFreeHost(a->hrows);
   if (a->done_host) cudaFreeHost((void*)a->done_host);
   free_wb_stages(a);
@@ -818,6 +828,10 @@ struct Pipe {
   float* astage_s[2] = {nullptr, nullptr}; // [arows, S]
   int32_t arows = 0;                       // rows per admission stage (grown on demand)
   int32_t scap[2] = {0, 0};                // rows the last staging of each parity staged at most
+  void* fixed_arena = nullptr;             // counters + index lists of both parities
+  int64_t fixed_bytes = 0;
+  void* stage_arena = nullptr;             // both admission stages
+  int64_t stage_bytes = 0;
   int grows = 0;
   cudaStream_t xfer = nullptr;             // transfer stream (k_admit_stage)
   cudaEvent_t ev_index[2] = {nullptr, nullptr};
@@ -871,14 +885,9 @@ int pipe_order(fc_cache* h, cudaStream_t st) {
 void pipe_release(fc_cache* h) {
   Pipe* q = h->pipe;
   if (!q) return;
+  if (q->fixed_arena) cudaFree(q->fixed_arena);
+  if (q->stage_arena) cudaFree(q->stage_arena);
   for (int p = 0; p < 2; ++p) {
-    cudaFree(q->ib[p].ctr);
-    cudaFree(q->ib[p].evicted);
-    cudaFree(q->ib[p].vslots);
-    cudaFree(q->ib[p].admitted);
-    cudaFree(q->ib[p].target);
-    cudaFree(q->astage[p]);
-    cudaFree(q->astage_s[p]);
     cudaFreeHost(q->hctr[p]);
     for (cudaEvent_t ev : {q->ev_index[p], q->ev_xfer[p], q->ev_commit[p], q->px[p][0], q->px[p][1]})
       if (ev) cudaEventDestroy(ev);
@@ -895,16 +904,24 @@ static int pipe_create(fc_cache* h) {
   h->pipe = q;
   const size_t C = (size_t)h->capacity;
   q->arows = initial_stage_rows(h);
-  cudaError_t e = cudaSuccess;
+  Arena fx, sa;
+  for (int p = 0; p < 2; ++p) {
+    fx.add(&q->ib[p].ctr, 1);
+    fx.add(&q->ib[p].evicted, C);
+    fx.add(&q->ib[p].vslots, C);
+    fx.add(&q->ib[p].admitted, C);
+    fx.add(&q->ib[p].target, C);
+    sa.add(&q->astage[p], (size_t)q->arows * h->dim);
+    if (h->sw) sa.add(&q->astage_s[p], (size_t)q->arows * h->sw);
+  }
+  cudaError_t e = fx.alloc(&q->fixed_arena);
+  if (e == cudaSuccess) e = sa.alloc(&q->stage_arena);
+  if (e == cudaSuccess) {
+    q->fixed_bytes = (int64_t)fx.bytes;
+    q->stage_bytes = (int64_t)sa.bytes;
+  }
   for (int p = 0; p < 2 && e == cudaSuccess; ++p) {
-    e = cudaMalloc(&q->ib[p].ctr, sizeof(Counters));
-    if (e == cudaSuccess) e = cudaMemset(q->ib[p].ctr, 0, sizeof(Counters));
-    if (e == cudaSuccess) e = cudaMalloc(&q->ib[p].evicted, C * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&q->ib[p].vslots, C * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&q->ib[p].admitted, C * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&q->ib[p].target, C * 4);
-    if (e == cudaSuccess) e = cudaMalloc(&q->astage[p], (size_t)q->arows * h->dim * 4);
-    if (e == cudaSuccess && h->sw) e = cudaMalloc(&q->astage_s[p], (size_t)q->arows * h->sw * 4);
+    e = cudaMemset(q->ib[p].ctr, 0, sizeof(Counters));
     // mapped: the index phase publishes its counters with a kernel store instead of a
     // cudaMemcpy that would queue behind the write-back D2H on the copy engine
     if (e == cudaSuccess) e = cudaHostAlloc(&q->hctr[p], sizeof(Counters), cudaHostAllocMapped);
@@ -1296,20 +1313,24 @@ static int pipe_grow_admission(fc_cache* h, int64_t need) {
   if (need <= q->arows) return FC_OK;
   FC_CUDA(cudaDeviceSynchronize());
   const int64_t grown = std::min<int64_t>(h->capacity, std::max<int64_t>(need + need / 4, 2 * (int64_t)q->arows));
+  float* nd[2] = {nullptr, nullptr};
+  float* ns[2] = {nullptr, nullptr};
+  Arena sa;
   for (int p = 0; p < 2; ++p) {
-    float* nd = nullptr;
-    float* ns = nullptr;
-    FC_CUDA(cudaMalloc(&nd, (size_t)grown * h->dim * 4));
-    FC_CUDA(cudaMemcpy(nd, q->astage[p], (size_t)q->arows * h->dim * 4, cudaMemcpyDeviceToDevice));
-    cudaFree(q->astage[p]);
-    q->astage[p] = nd;
-    if (h->sw) {
-      FC_CUDA(cudaMalloc(&ns, (size_t)grown * h->sw * 4));
-      FC_CUDA(cudaMemcpy(ns, q->astage_s[p], (size_t)q->arows * h->sw * 4, cudaMemcpyDeviceToDevice));
-      cudaFree(q->astage_s[p]);
-      q->astage_s[p] = ns;
-    }
+    sa.add(&nd[p], (size_t)grown * h->dim);
+    if (h->sw) sa.add(&ns[p], (size_t)grown * h->sw);
   }
+  void* arena = nullptr;
+  FC_CUDA(sa.alloc(&arena));
+  for (int p = 0; p < 2; ++p) {
+    FC_CUDA(cudaMemcpy(nd[p], q->astage[p], (size_t)q->arows * h->dim * 4, cudaMemcpyDeviceToDevice));
+    if (h->sw) FC_CUDA(cudaMemcpy(ns[p], q->astage_s[p], (size_t)q->arows * h->sw * 4, cudaMemcpyDeviceToDevice));
+    q->astage[p] = nd[p];
+    q->astage_s[p] = ns[p];
+  }
+  cudaFree(q->stage_arena);
+  q->stage_arena = arena;
+  q->stage_bytes = (int64_t)sa.bytes;
   q->arows = (int32_t)grown;
   q->grows += 1;
   return FC_OK;
@@ -1574,21 +1595,23 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
 
 // Device / pinned-host bytes the engine and the pipeline hold (fc_memory_bytes):
 // out = {stage bytes (device), id-space bytes (pending marks), other device bytes,
-//        pinned host staging bytes, write-back stage rows, admission stage rows}
+//        pinned host staging bytes, write-back stage rows, admission stage rows,
+//        device bytes reserved by these allocations (2 MiB pages)}
 void engine_memory(const fc_cache* h, int64_t* out) {
-  for (int i = 0; i < 6; ++i) out[i] = 0;
-  const int64_t rb = 4 * (int64_t)(h->dim + h->sw);
+  for (int i = 0; i < 7; ++i) out[i] = 0;
   if (const AsyncWB* a = h->awb) {
-    out[0] += kWbBufs * (int64_t)a->rows * (rb + 4);
+    out[0] += a->stage_bytes;
     out[1] += 4 * h->num_ids;
-    out[2] += kWbBufs * 4;
-    out[3] += kWbBufs * (int64_t)a->rows * (rb + 4);
+    out[2] += a->fixed_bytes - 4 * h->num_ids;
+    out[3] += kWbBufs * (int64_t)a->rows * (4 * (int64_t)(h->dim + h->sw) + 4);
     out[4] = a->rows;
+    out[6] += reserved_bytes(a->stage_bytes) + reserved_bytes(a->fixed_bytes);
   }
   if (const Pipe* q = h->pipe) {
-    out[0] += 2 * (int64_t)q->arows * rb;
-    out[2] += 2 * (4 * 4 * (int64_t)h->capacity + (int64_t)sizeof(Counters));
+    out[0] += q->stage_bytes;
+    out[2] += q->fixed_bytes;
     out[5] = q->arows;
+    out[6] += reserved_bytes(q->stage_bytes) + reserved_bytes(q->fixed_bytes);
   }
 }
 

@@ -25,6 +25,7 @@
 #include <pthread.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "../../include/freqcache_b200.h"
@@ -106,6 +107,8 @@ struct fc_cache {
   int32_t* block_cnt;       // [kMaxScanBlocks + 1]
   int32_t* block_cnt2;      // second scan lane (concurrent compactions)
   fc::Counters* ctr;        // device (synchronous verbs)
+  void* arena;              // the allocation every array above (but wb_stage) is carved from
+  int64_t arena_bytes;
   fc::Counters* ctr_host;   // pinned mirror
   fc::Counters* live;       // counters of the last call: holds the current free_count
   cudaEvent_t done;
@@ -113,6 +116,10 @@ struct fc_cache {
   // scratch for sort-based kernels (backward / scatter_update), grown on demand
   void* scratch;
   size_t scratch_bytes;
+  // the fused backward's last kernel clears the sort state for the next sort: this many
+  // bytes at the head of `scratch` (valid while scratch == sort_zero_for) are zero
+  void* sort_zero_for;
+  size_t sort_zero_bytes;
 
   float* slow;              // slow tier rows, device-mapped pointer
   int64_t slow_ld;
@@ -188,6 +195,33 @@ int cuda_fail(cudaError_t e, const char* what);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// One cudaMalloc carved into many arrays (256-byte aligned): a cache's fixed arrays, the
+// engine's stages and the pipeline's buffers each live in one such arena, so the device
+// memory they take is the arena sizes rounded to the allocation granularity -- which is
+// what fc_memory_bytes reports.
+struct Arena {
+  struct Part {
+    void** p;
+    size_t off;
+  };
+  std::vector<Part> parts;
+  size_t bytes = 0;
+  template <class T>
+  void add(T** p, size_t count) {
+    parts.push_back({reinterpret_cast<void**>(p), bytes});
+    bytes += (std::max<size_t>(count, 1) * sizeof(T) + 255) & ~size_t(255);
+  }
+  // allocates and assigns every part; *base receives the allocation
+  cudaError_t alloc(void** base) {
+    cudaError_t e = cudaMalloc(base, std::max<size_t>(bytes, 256));
+    if (e != cudaSuccess) return e;
+    for (const Part& q : parts) *q.p = static_cast<char*>(*base) + q.off;
+    return cudaSuccess;
+  }
+};
+constexpr int64_t kAllocGranularity = 2 << 20;  // cudaMalloc reserves device memory in 2 MiB pages
+inline int64_t reserved_bytes(int64_t b) { return b <= 0 ? 0 : (b + kAllocGranularity - 1) / kAllocGranularity * kAllocGranularity; }
+
 inline int grid_for(int64_t items, int per_block, int max_blocks = kSMs * 8) {
   int64_t b = (items + per_block - 1) / per_block;
   if (b < 1) b = 1;
@@ -238,7 +272,8 @@ int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, cons
 // sort / scan helpers (fc_sort.cu)
 size_t sort_scratch_bytes(int64_t n);
 int radix_sort_pairs(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* keys_out, int32_t* vals_out,
-                     int64_t n, int key_bits, void* scratch, cudaStream_t st);
+                     int64_t n, int key_bits, void* scratch, cudaStream_t st, bool state_zeroed = false);
+size_t sort_state_bytes(int64_t n, int key_bits);
 int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch, cudaStream_t st);
 size_t scan_scratch_bytes(int64_t n);
 int ensure_scratch(fc_cache* h, size_t bytes);

@@ -220,10 +220,22 @@ size_t sort_scratch_bytes(int64_t n) {
          sizeof(uint32_t) * (size_t)kOsMaxPasses * kRsMaxBins * ntiles + 2 * n * sizeof(int32_t) + 64;
 }
 
+// Bytes at the head of the scratch (histograms, tile counters, look-back status words)
+// that must be zero when a sort of n keys of key_bits bits starts.
+size_t sort_state_bytes(int64_t n, int key_bits) {
+  const int64_t ntiles = (n + kRsTile - 1) / kRsTile;
+  const int passes = std::max(1, (key_bits + 8) / 9);
+  const int bins = 1 << std::max(1, (key_bits + passes - 1) / passes);
+  return sizeof(int32_t) * (kOsMaxPasses * kRsMaxBins + kOsMaxPasses + 4) +
+         sizeof(uint32_t) * (size_t)passes * bins * ntiles;
+}
+
 // Stable sort of (key, value) pairs by the low `key_bits` bits of the key.
 // vals_in == NULL sorts the positions 0..n-1 (an argsort). Inputs are untouched.
+// state_zeroed: the caller guarantees the first sort_state_bytes(n, key_bits) of the
+// scratch are already zero (a previous kernel cleared them), so no memset is queued.
 int radix_sort_pairs(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* keys_out, int32_t* vals_out,
-                     int64_t n, int key_bits, void* scratch, cudaStream_t st) {
+                     int64_t n, int key_bits, void* scratch, cudaStream_t st, bool state_zeroed) {
   if (n <= 0) return FC_OK;
   if (n > (int64_t)kOsMask) {
     set_error("radix sort of %lld keys exceeds the 30-bit tile counters", (long long)n);
@@ -245,7 +257,7 @@ int radix_sort_pairs(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* 
   p = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(p) + 15) & ~uintptr_t(15));
   uint32_t* ktmp = reinterpret_cast<uint32_t*>(p);
   int32_t* vtmp = reinterpret_cast<int32_t*>(p + n * sizeof(int32_t));
-  FC_CUDA(cudaMemsetAsync(scratch, 0, head + status_bytes, st));  // histograms, counters, status flags
+  if (!state_zeroed) FC_CUDA(cudaMemsetAsync(scratch, 0, head + status_bytes, st));  // histograms, counters, status
   k_os_hist<<<grid_for(n, kNT * 8, kSMs * 4), kNT, 0, st>>>(keys_in, n, passes, dbits, ghist);
   const uint32_t* ks = keys_in;
   const int32_t* vs = vals_in;

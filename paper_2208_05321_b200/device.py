@@ -325,8 +325,8 @@ class DeviceCache:
         return info, buf[:u], buf[k:k + u], buf[2 * k:2 * k + u], buf[3 * k:3 * k + u], buf[4 * k:], d_ids
 
     MEM_FIELDS = ("fast_rows_bytes", "id_space_bytes", "bitmap_bytes", "slot_space_bytes", "staging_bytes",
-                  "scratch_bytes", "device_total_bytes", "pinned_staging_bytes", "wb_stage_rows",
-                  "admission_stage_rows")
+                  "scratch_bytes", "allocation_slack_bytes", "device_total_bytes", "pinned_staging_bytes",
+                  "wb_stage_rows", "admission_stage_rows")
 
     def memory(self) -> dict:
         """Every device allocation of this cache by category (fc_memory_bytes), plus the

@@ -119,3 +119,28 @@ def test_hot_row_long_segment():
     want = w.copy()
     oracle.sparse_sgd(want, np.unique(ids), grad, 0.001)
     np.testing.assert_allclose(m.weight(), want, rtol=1e-5, atol=2e-6)
+
+
+def test_backward_sequence_of_batch_sizes_reuses_sort_state():
+    """Back-to-back fused backwards of growing and shrinking batches (the fix-up clears the
+    next sort's state instead of a memset, DESIGN 4b) with a scatter_update in between,
+    against dense SGD: every step within 1e-5."""
+    num, dim, lr = 3_000, 16, 0.05
+    rng = np.random.default_rng(11)
+    w = rng.uniform(-0.1, 0.1, (num, dim)).astype(np.float32)
+    m = CachedEmbeddingBag(num, dim, cache_ratio=1.0, mode="sum", weight=w, lr=lr)
+    dense = w.astype(np.float64)
+    for s, n in enumerate([500, 4_000, 120, 4_000, 9_000, 37, 9_000]):
+        ids = rng.integers(0, num, n)
+        gout = rng.standard_normal((n, dim)).astype(np.float32)
+        out = m(torch.from_numpy(ids))
+        np.testing.assert_allclose(out.detach().cpu().numpy(), dense[ids], rtol=RTOL, atol=ATOL)
+        out.backward(torch.from_numpy(gout).cuda())
+        np.add.at(dense, ids, -lr * gout.astype(np.float64))
+        if s == 3:  # another sort on the same scratch leaves its state behind
+            st = m.cache
+            info, uids, ucnt, uranks, uslots, inverse, _ = st.prepare(torch.from_numpy(ids[:50]).cuda())
+            deltas = torch.zeros((50, dim), dtype=torch.float32, device="cuda")
+            st.scatter_update(uslots, inverse, ucnt, deltas)
+    m.flush()
+    np.testing.assert_allclose(m.weight(), dense, rtol=RTOL, atol=ATOL)

@@ -72,6 +72,9 @@ def test_tiny_stages_grow_and_stay_exact(depth, monkeypatch):
 def _lib_bytes(fn):
     """Device bytes `fn` allocates outside torch's caching allocator (cudaMemGetInfo delta
     minus torch's reserved delta)."""
+    import gc
+
+    gc.collect()  # caches of earlier tests release their device memory first
     torch.cuda.synchronize()
     torch.cuda.empty_cache()
     f0, _ = torch.cuda.mem_get_info()
@@ -102,14 +105,21 @@ def test_memory_report_matches_device_allocations():
             out.backward(torch.ones_like(out))
         return m
 
-    build_and_run()  # loads every kernel the run uses (lazy module loading takes device memory once)
+    m0 = build_and_run()  # loads every kernel the run uses (lazy module loading takes device memory once)
+    m0.flush()
+    del m0
     used, m = _lib_bytes(build_and_run)
     rep = m.cache.memory()
     total = rep["device_total_bytes"]
     fast = rep["fast_rows_bytes"]
     print(f"cudaMemGetInfo delta (lib) {used / 2**20:.1f} MiB, reported {total / 2**20:.1f} MiB, "
           f"fast tier {fast / 2**20:.1f} MiB, staging {rep['staging_bytes'] / 2**20:.1f} MiB, {rep}")
-    assert abs(used - total) <= 0.01 * used, (used, total)
+    # what the report cannot see: the driver's GPU page tables for the pinned, device-mapped
+    # host memory the cache maps (slow tier + write-back staging), 8 B per 4 KiB page,
+    # allocated in 2 MiB pages
+    mapped = m.slow_rows.nbytes + rep["pinned_staging_bytes"]
+    page_tables = (mapped // 4096 * 8 + (2 << 20) - 1) // (2 << 20) * (2 << 20)
+    assert total <= used <= total + page_tables + 0.01 * used, (used, total, page_tables)
     # staging bounded by the 64 MiB buffer budget per stage, not by capacity
     row = 4 * dim
     assert rep["wb_stage_rows"] <= max(64 * 2**20 // row, 1024)
