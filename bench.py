@@ -211,13 +211,19 @@ class ClockSampler:
             self.proc.kill()
         self.th.join(timeout=2)
         if self.source.startswith("nvml"):
+            parsed = []
             for line in self.lines:
                 try:
                     t, sm, mx, r = line.strip().split(",")
+                    parsed.append((float(t), (float(sm), float(mx), [bool(int(r) & b) for b in self.BITS])))
                 except ValueError:
                     continue
-                if self.t0 <= float(t) <= self.t1:
-                    self.rows.append((float(sm), float(mx), [bool(int(r) & b) for b in self.BITS]))
+            self.rows = [row for t, row in parsed if self.t0 <= t <= self.t1]
+            if not self.rows and parsed:  # a region shorter than the poll interval: the nearest sample
+                t, row = min(parsed, key=lambda tr: min(abs(tr[0] - self.t0), abs(tr[0] - self.t1)))
+                if min(abs(t - self.t0), abs(t - self.t1)) < 0.02:
+                    self.rows = [row]
+                    self.source += " (region shorter than the poll interval: nearest sample, within 20 ms)"
 
     def summary(self):
         if not self.rows:
@@ -438,7 +444,7 @@ def launches_per_step(args, shard_mode, pipelined, world):
     if shard_mode == "column":  # prepare of the global batch + pool + fused backward (NCCL kernels not counted)
         return KERNELS_PER_TRAIN_STEP + (PIPELINE_EXTRA_KERNELS if pipelined else 0)
     return (SHARDED_BASE_KERNELS + (PIPELINE_EXTRA_KERNELS if pipelined else 0) + (1 if world == 1 else 5)
-            + (1 if args.no_peer else 2))
+            + (2 if args.peer else 1))
 
 
 def run_ours(args, cfg, torch, rank, world):
@@ -501,8 +507,10 @@ def run_ours(args, cfg, torch, rank, world):
         shard = CudaShard(idx.num_ids, D, fc.fast_capacity(idx.num_ids, cfg["ratio"]), rows, idx, optimizer=OPT,
                           lr=LR, device=dev, engine=args.engine, global_num_ids=cfg["num_ids"])
         # owners write the looked-up rows straight into the requesters' buffers over NVLink
-        # peer memory (fc_pool_to_peers); --no-peer keeps the NCCL all-to-all of the rows
-        mod = RowShardedEmbedding(shard, world, rank, mode=MODE, device=dev, peer_rows=0 if args.no_peer else N)
+        # peer memory (fc_pool_to_peers) with --peer; by default the rows come back by NCCL all-to-all
+        # (faster at world 1, 325-332 vs 290-316 M lookups/s, profiles/r01_bench_sharded_*.json; the
+        # peer path is untested across GPUs in this build's runs)
+        mod = RowShardedEmbedding(shard, world, rank, mode=MODE, device=dev, peer_rows=N if args.peer else 0)
         dcs = [shard.cache]
         cap = shard.cache.capacity
     dc = dcs[0]
@@ -715,7 +723,7 @@ def run_ours(args, cfg, torch, rank, world):
         "implementation": {"engine": args.engine, "prefetch": pipelined,
                            "prefetch_depth": (2 if depth2 else 1) if pipelined else 0,
                            "exchange": (None if not rowwise else "unique ids by NCCL all-to-all; rows back "
-                                        + ("by NCCL all-to-all" if args.no_peer else "by owner-side peer-memory writes")
+                                        + ("by owner-side peer-memory writes" if args.peer else "by NCCL all-to-all")
                                         ) if shard_mode != "column" else
                            "all-gather of ids; pooled columns by NCCL all-to-all (reference semantics)",
                            "capacity_per_gpu": cap},
@@ -948,8 +956,10 @@ def main():
     ap.add_argument("--prefetch-depth", type=int, default=2, choices=[1, 2],
                     help="2: batch t+1's prefetch is begun before batch t is committed (default)")
     ap.add_argument("--sharded", action="store_true", help="alias of --shard row (also at one GPU)")
-    ap.add_argument("--no-peer", action="store_true",
-                    help="row-sharded runs: return rows with NCCL all-to-all instead of peer-memory writes")
+    ap.add_argument("--peer", action="store_true",
+                    help="row-sharded runs: owners write the rows straight into the requesters' buffers over "
+                         "NVLink peer memory (CUDA IPC) instead of the NCCL all-to-all")
+    ap.add_argument("--no-peer", action="store_true", help="(default) rows come back by NCCL all-to-all")
     ap.add_argument("--no-prefetch", action="store_true",
                     help="synchronous prepare each step (no lookahead pipeline)")
     ap.add_argument("--engine", default="async", choices=["async", "zerocopy"],
