@@ -1433,7 +1433,11 @@ int pipe_launch_xfer(fc_cache* h, cudaStream_t after, bool from_update) {
   trace_mark(h, T_XFER_BEGIN, q->xfer);
   // FC_DEBUG_SKIP_STAGING=1: measurement only (admitted rows are NOT staged, results are
   // wrong) -- how long the rest of the pipelined step takes without host-link traffic
-  static const bool skip_staging = std::getenv("FC_DEBUG_SKIP_STAGING") != nullptr;
+  static const bool skip_staging = [] {
+    const bool on = std::getenv("FC_DEBUG_SKIP_STAGING") != nullptr;
+    if (on) std::fprintf(stderr, "[freqcache_b200] FC_DEBUG_SKIP_STAGING: admitted rows are NOT staged (timing only)\n");
+    return on;
+  }();
   if (skip_staging) {
   } else if (q->tma) {  // bulk-copy engine: rows are 16-byte multiples at 16-byte aligned addresses
     const int G = tma_group_rows((h->dim + h->sw) * 4);

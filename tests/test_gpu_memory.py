@@ -124,3 +124,37 @@ def test_memory_report_matches_device_allocations():
     row = 4 * dim
     assert rep["wb_stage_rows"] <= max(64 * 2**20 // row, 1024)
     assert rep["staging_bytes"] <= 5 * 64 * 2**20 + 5 * 4 * rep["wb_stage_rows"]
+
+
+@pytest.mark.parametrize("gbps", ["12", "40"])
+def test_paced_staging_stays_exact(gbps, monkeypatch):
+    """FC_XFER_GBPS paces the TMA miss staging (%globaltimer-spaced bulk copies); the
+    decisions and the post-flush table are unchanged."""
+    monkeypatch.setenv("FC_XFER_GBPS", gbps)
+    num_ids, cap, dim, nb, bsz = 30_000, 2_000, 32, 10, 2_500
+    rng = np.random.default_rng(9)
+    p = 1.0 / np.arange(1, num_ids + 1) ** 1.05
+    trace = rng.permutation(num_ids)[rng.choice(num_ids, size=(nb, bsz), p=p / p.sum())]
+    rank_of, id_of = oracle.rank_permutation(oracle.frequency_counts(trace, num_ids))
+    ref = oracle.init_rows(num_ids, dim, 2)
+    orc = oracle.OracleCache(rank_of, ref[id_of].copy(), cap)
+    st = fc.CacheStack(fc.IdxMap(rank_of, id_of), fc.SlowTierStore(ref[id_of].copy()),
+                       fc.FastTierStore(np.zeros((cap, dim), np.float32)), fc.Transmitter(), engine="async")
+    orc.warmup(cap)
+    st.warmup(cap)
+    colw = oracle.column_weights(dim, 3)
+    q = st.prepare(trace[0], 0)
+    for b in range(nb):
+        a = orc.prepare(trace[b], b)
+        assert np.array_equal(q.unique_slots, a["unique_slots"]), b
+        if b + 1 < nb:
+            st.prefetch(trace[b + 1], b + 1)
+        gs = oracle.row_scalars(a["unique_ids"], a["unique_counts"], b, 3)
+        orc.apply_unique_update(a, gs[:, None] * colw[None, :])
+        st.apply_synthetic_update(q, b, 3, colw)
+        if b + 1 < nb:
+            q = st.prepare(trace[b + 1], b + 1)
+    st.flush()
+    orc.flush()
+    torch.cuda.synchronize()
+    assert np.array_equal(st.slow.rows, orc.slow)
