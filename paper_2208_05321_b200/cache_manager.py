@@ -538,14 +538,19 @@ class CacheStack:
         return None
 
     def memory_report(self) -> dict:
-        """The reference's keys (cache_manager.py:553-562) filled with what the device cache
-        really holds: fast_rows_bytes = cached rows (+ optimizer state); buffer_bytes = the
-        HBM staging buffers (bounded like the reference's TransferBuffer, grown only when a
-        batch needs more) + scratch; index_bytes = every id-, slot- and bitmap-space array;
-        peak_fast_tier_bytes = their sum = all device memory the cache allocated. `device`
-        breaks it down (fc_memory_bytes)."""
-        m = self.device.memory()
-        buf = m["staging_bytes"] + m["scratch_bytes"] + m["allocation_slack_bytes"]
-        index = m["id_space_bytes"] + m["bitmap_bytes"] + m["slot_space_bytes"]
-        return {"fast_rows_bytes": m["fast_rows_bytes"], "buffer_bytes": buf, "index_bytes": index,
-                "peak_fast_tier_bytes": m["device_total_bytes"], "device": m}
+        """The reference's report (cache_manager.py:553-562), same keys and formula (the
+        simulator's RunMetrics document embeds it): fast rows + the TransferBuffer's
+        capacity + the reference's index arrays. What the device cache really allocates is
+        `device_memory()`."""
+        rows = self.fast.nbytes
+        buf = self.transmitter.buffer.capacity_bytes
+        index = self.state.index_bytes
+        return {"fast_rows_bytes": int(rows), "buffer_bytes": int(buf), "index_bytes": int(index),
+                "peak_fast_tier_bytes": int(rows + buf + index)}
+
+    def device_memory(self) -> dict:
+        """Every device allocation of this stack's cache by category (fc_memory_bytes):
+        fast rows, id-space arrays, bitmaps, slot-space arrays, the HBM staging buffers
+        (bounded by buffer_bytes, grown only when a batch needs more), scratch, the 2 MiB
+        page slack, and `device_total_bytes` = what the allocations reserve."""
+        return self.device.memory()

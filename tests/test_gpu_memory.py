@@ -6,8 +6,10 @@ needs more. FC_STAGE_ROWS forces a tiny start so every overflow path runs: the s
 prepare's read-back-and-grow before its eviction kernel, the pipeline commit's growth of
 the write-back stages, and the admission rows past the stage that the commit copies from
 their newest copy. Cache decisions and the post-flush slow tier must stay bit-exact with
-the oracle. memory_report (cache_manager.py:553-562) must account for the device memory
-the cache really takes (cudaMemGetInfo delta)."""
+the oracle. The device memory report (fc_memory_bytes, CacheStack.device_memory; the
+reference's own memory_report, cache_manager.py:553-562, keeps its formula because the
+simulator's RunMetrics embed it) must account for the device memory the cache really
+takes (cudaMemGetInfo delta)."""
 
 import numpy as np
 import pytest
@@ -63,7 +65,7 @@ def test_tiny_stages_grow_and_stay_exact(depth, monkeypatch):
     torch.cuda.synchronize()
     assert np.array_equal(st.state.slot_to_rank, orc.slot_rank)
     assert np.array_equal(st.slow.rows, orc.slow)
-    m = st.memory_report()["device"]
+    m = st.device_memory()
     assert m["wb_stage_rows"] > 48
     if depth:
         assert m["admission_stage_rows"] > 48
