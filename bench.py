@@ -69,9 +69,12 @@ METRIC = "cached-embedding lookups/sec"
 # sim update 1; backward = radix sort (histogram + 2 one-sweep passes) + fused stream + fix-up = 5
 KERNELS_PER_STEP = 17 + 1 + 1
 KERNELS_PER_TRAIN_STEP = 17 + 1 + 5
-# prefetch pipeline: + k_evict_state, k_admit_state, k_publish (index phase) and
-# k_admit_stage / k_evict_commit / k_admit_commit instead of k_evict_async / k_admit_async
-PIPELINE_EXTRA_KERNELS = 3 + 1
+# prefetch pipeline (round 2, fused index phase): 11 index kernels (k_begin, k_mark_ids, ids count +
+# emit, k_unique_info, k_inverse_plan, victims+misses count, victims emit with their slot-table
+# changes, misses emit + free-slot count, free-slot emit with the admissions' slot-table changes,
+# k_finish_publish) + k_admit_stage_tma + k_clear_pending, k_evict_commit, k_admit_commit = 15
+# instead of the synchronous prepare's 17
+PIPELINE_EXTRA_KERNELS = 15 - 17
 # row-sharded training step (profiles/r01_launches_sharded*): fc_route 6 (k_begin, k_route_mark,
 # count + emit, k_route_inverse, k_route_finish) + the owner's pipelined prepare 17 + 4 + the
 # requester's gradient reduction 5 + the owner's apply (k_bwd_direct when every received id is

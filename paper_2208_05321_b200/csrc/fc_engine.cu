@@ -984,14 +984,6 @@ struct PipeArgs {
   Units ud, us;
 };
 
-// counters -> pinned mapped host copy (system-scope stores, visible once the stream event fires)
-__global__ void k_publish(const Counters* __restrict__ c, Counters* host) {
-  const int* src = reinterpret_cast<const int*>(c);
-  int* dst = reinterpret_cast<int*>(host);
-  constexpr int kWords = (int)(sizeof(Counters) / sizeof(int));
-  for (int i = threadIdx.x; i < kWords; i += blockDim.x) dst[i] = src[i];
-  __threadfence_system();
-}
 
 // transfer stream: newest copy of each admitted rank -> admission stage (host link)
 template <bool VEC>
@@ -1371,10 +1363,8 @@ int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* 
   if (q->has_index[o]) FC_CUDA(cudaStreamWaitEvent(st, q->ev_index[o], 0));
   if (q->has_commit[p]) FC_CUDA(cudaStreamWaitEvent(st, q->ev_commit[p], 0));
   trace_mark(h, T_INDEX_BEGIN, st);
-  int rc = launch_index_phase(h, ids, ids_bytes, n, uids, ucnt, uranks, uslots, inverse, q->ib[p], st);
+  int rc = launch_index_phase(h, ids, ids_bytes, n, uids, ucnt, uranks, uslots, inverse, q->ib[p], q->hctr_dev[p], st);
   if (rc) return rc;
-  k_publish<<<1, 32, 0, st>>>(q->ib[p].ctr, q->hctr_dev[p]);
-  FC_CUDA(cudaGetLastError());
   trace_mark(h, T_INDEX_END, st);
   FC_CUDA(cudaEventRecord(q->ev_index[p], st));
   q->has_index[p] = true;
@@ -1417,7 +1407,10 @@ int pipe_launch_xfer(fc_cache* h, cudaStream_t after, bool from_update) {
   q->xfer_pending = false;
   q->xfer_behind = false;
   const int p = q->xfer_par, o = p ^ 1;
-  // stage(t+1) after index(t+1) and commit(t): pending marks and the stage's last reader
+  // stage(t+1) after index(t+1), after commit(t) (pending marks), and after commit(t-1),
+  // the last reader of this parity's admission stage. (Waiting only for commit(t)'s
+  // write-back marks lets the staging start ~20 us earlier, beside the admission copy and the
+  // pooled gather, and measured ~3% slower: profiles/r02_index_fusion_ab.txt.)
   FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_index[p], 0));
   if (q->has_commit[o]) FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_commit[o], 0));
   if (q->has_commit[p]) FC_CUDA(cudaStreamWaitEvent(q->xfer, q->ev_commit[p], 0));

@@ -41,17 +41,25 @@ struct CandWords {  // resident and not protected by the current batch
 };
 
 // ------------------------------------------------------------------ the primitive
+// (the bodies take the block index so that two passes can share one launch, see
+// launch_index_phase: every kernel boundary is expensive beside the miss staging)
 template <class WF>
-__global__ void __launch_bounds__(kNT) k_bits_count(WF wf, int64_t nwords, int64_t chunk, int32_t* cnt,
-                                                    const Counters* ctr, int gate) {
+__device__ __forceinline__ void bits_count_body(WF wf, int64_t nwords, int64_t chunk, int32_t* cnt,
+                                                const Counters* ctr, int gate, int blk) {
   __shared__ int sm[kNT / 32 + 1];
   if (!gate_open(ctr, gate)) return;
-  const int64_t b0 = (int64_t)blockIdx.x * chunk;
+  const int64_t b0 = (int64_t)blk * chunk;
   const int64_t b1 = min(nwords, b0 + chunk);
   int c = 0;
   for (int64_t w = b0 + threadIdx.x; w < b1; w += kNT) c += __popc(wf(w));
   c = block_sum<kNT>(c, sm);
-  if (threadIdx.x == 0) cnt[blockIdx.x] = c;
+  if (threadIdx.x == 0) cnt[blk] = c;
+}
+
+template <class WF>
+__global__ void __launch_bounds__(kNT) k_bits_count(WF wf, int64_t nwords, int64_t chunk, int32_t* cnt,
+                                                    const Counters* ctr, int gate) {
+  bits_count_body(wf, nwords, chunk, cnt, ctr, gate, blockIdx.x);
 }
 
 // Emit, with the block-offset scan folded in: every block sums the per-block counts
@@ -59,9 +67,9 @@ __global__ void __launch_bounds__(kNT) k_bits_count(WF wf, int64_t nwords, int64
 // runs the finisher on the total itself (the finishers only set counters, so the
 // blocks' identical writes are benign) and then emits its set bits in order.
 template <class WF, class EM, class FIN>
-__global__ void __launch_bounds__(kNT) k_bits_emit(WF wf, EM em, FIN fin, int64_t nwords, int64_t chunk,
-                                                   const int32_t* cnt, int nb, const int32_t* win, Counters* ctr,
-                                                   int gate) {
+__device__ __forceinline__ void bits_emit_body(WF wf, EM em, FIN fin, int64_t nwords, int64_t chunk,
+                                               const int32_t* cnt, int nb, const int32_t* win, Counters* ctr,
+                                               int gate, int blk) {
   __shared__ int sm[kNT / 32 + 1];
   __shared__ int s_base;
   __shared__ Counters lc;  // this block's view of the counters after the finisher
@@ -70,7 +78,7 @@ __global__ void __launch_bounds__(kNT) k_bits_emit(WF wf, EM em, FIN fin, int64_
   for (int b = threadIdx.x; b < nb; b += kNT) {
     const int v = cnt[b];
     all += v;
-    if (b < (int)blockIdx.x) pre += v;
+    if (b < blk) pre += v;
   }
   pre = block_sum<kNT>(pre, sm);
   all = block_sum<kNT>(all, sm);
@@ -81,7 +89,7 @@ __global__ void __launch_bounds__(kNT) k_bits_emit(WF wf, EM em, FIN fin, int64_
     // 1000+ blocks do not all write the same counters line
     lc = *ctr;
     fin(all, &lc);
-    if (blockIdx.x == 0) fin(all, ctr);
+    if (blk == 0) fin(all, ctr);
   }
   __syncthreads();
   if (!gate_open(&lc, gate)) return;  // the finisher may have raised an error
@@ -94,11 +102,11 @@ __global__ void __launch_bounds__(kNT) k_bits_emit(WF wf, EM em, FIN fin, int64_
     hi = lw[1];
   }
   const int base = s_base;
-  const int bend = base + cnt[blockIdx.x];
+  const int bend = base + cnt[blk];
   if (!EM::kVisitAll && (bend <= lo || base >= hi)) return;
   EM e = em;
   e.init(&lc);
-  const int64_t b0 = (int64_t)blockIdx.x * chunk;
+  const int64_t b0 = (int64_t)blk * chunk;
   const int64_t b1 = min(nwords, b0 + chunk);
   int run = base;
   int acc = 0;
@@ -120,6 +128,32 @@ __global__ void __launch_bounds__(kNT) k_bits_emit(WF wf, EM em, FIN fin, int64_
     acc = block_sum<kNT>(acc, sm);
     if (threadIdx.x == 0 && acc) atomicAdd(e.counter(ctr), acc);
   }
+}
+
+template <class WF, class EM, class FIN>
+__global__ void __launch_bounds__(kNT) k_bits_emit(WF wf, EM em, FIN fin, int64_t nwords, int64_t chunk,
+                                                   const int32_t* cnt, int nb, const int32_t* win, Counters* ctr,
+                                                   int gate) {
+  bits_emit_body(wf, em, fin, nwords, chunk, cnt, nb, win, ctr, gate, blockIdx.x);
+}
+
+// Two independent count passes in one launch (blocks [0, nb1) count the first bitmap).
+template <class WF1, class WF2>
+__global__ void __launch_bounds__(kNT) k_bits_count2(WF1 wf1, int64_t nw1, int64_t chunk1, int32_t* cnt1, int nb1,
+                                                     int gate1, WF2 wf2, int64_t nw2, int64_t chunk2, int32_t* cnt2,
+                                                     int gate2, const Counters* ctr) {
+  if ((int)blockIdx.x < nb1) bits_count_body(wf1, nw1, chunk1, cnt1, ctr, gate1, blockIdx.x);
+  else bits_count_body(wf2, nw2, chunk2, cnt2, ctr, gate2, blockIdx.x - nb1);
+}
+
+// An emit pass and an independent count pass in one launch (blocks [0, nb1) emit).
+template <class WF1, class EM, class FIN, class WF2>
+__global__ void __launch_bounds__(kNT) k_bits_emit_count(WF1 wf1, EM em, FIN fin, int64_t nw1, int64_t chunk1,
+                                                         const int32_t* cnt1, int nb1, const int32_t* win, int gate1,
+                                                         WF2 wf2, int64_t nw2, int64_t chunk2, int32_t* cnt2,
+                                                         int gate2, Counters* ctr) {
+  if ((int)blockIdx.x < nb1) bits_emit_body(wf1, em, fin, nw1, chunk1, cnt1, nb1, win, ctr, gate1, blockIdx.x);
+  else bits_count_body(wf2, nw2, chunk2, cnt2, ctr, gate2, blockIdx.x - nb1);
 }
 
 template <class WF, class FIN, class EM>
@@ -542,42 +576,136 @@ int launch_mark_dirty(fc_cache* h, const int64_t* slots, int64_t n, cudaStream_t
 // this phase may run while the previous batch's forward/backward still reads
 // and updates rows: those kernels address rows through their own unique_slots.
 
-// victims (descending ranks) -> slots; leave the slot tables; free their slots (:305-308)
-__global__ void k_evict_state(const int32_t* __restrict__ evicted, int32_t* __restrict__ vslots, int32_t* slot_to_rank,
-                              int32_t* rank_to_slot, uint32_t* res, uint32_t* freeb, Counters* c) {
-  if (!gate_open(c, G_EVICT)) return;
-  const int needed = c->needed;
-  for (int v = blockIdx.x * kNT + threadIdx.x; v < needed; v += gridDim.x * kNT) {
-    const int r = evicted[v];
+// The pipeline's index phase runs beside the previous batch's miss staging, where every
+// kernel boundary costs 60-100 us and the phase is on the critical path
+// (the next staging waits for it). So it fuses what round 1 ran as separate kernels:
+// the eviction count into k_inverse, the victims' and the admissions' slot-table updates
+// into their compactions' emit passes, two independent count passes into one launch each,
+// and the counters' publication into k_finish -- 11 launches instead of 17, same results.
+
+// victims -> slots as they are emitted (k_evict_state's work); free_count by the finisher
+struct EvictFinState {
+  __device__ void operator()(int total, Counters* c) const {
+    c->candidates = total;
+    const int need = c->needed;
+    if (need > total) {
+      c->err = FC_ERR_INSUFFICIENT_EVICTABLE;
+      return;
+    }
+    c->win_evict[0] = total - need;
+    c->win_evict[1] = total;
+    c->free_count += need;  // applied once, by block 0 on the shared counters (:305-308)
+  }
+};
+
+struct EvictEmitState {
+  static constexpr bool kVisitAll = false, kClear = false, kCount = false;
+  int32_t* evicted;
+  int32_t* vslots;
+  int32_t* slot_to_rank;
+  int32_t* rank_to_slot;
+  uint32_t* res;
+  uint32_t* freeb;
+  int total;
+  __device__ void init(const Counters* c) { total = c->candidates; }
+  __device__ int* counter(Counters*) const { return nullptr; }
+  __device__ __forceinline__ int operator()(int64_t r, int a) const {
+    const int v = total - 1 - a;  // descending, like np.sort(top)[::-1] (:75)
     const int s = rank_to_slot[r];
+    evicted[v] = (int32_t)r;
     vslots[v] = s;
     slot_to_rank[s] = -1;
     rank_to_slot[r] = -1;
+    // this thread read r's residency word already (each word is read by one thread)
     atomicAnd(&res[r >> 5], ~(1u << (r & 31)));
     atomicOr(&freeb[s >> 5], 1u << (s & 31));
+    return 0;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) c->free_count += needed;
+};
+
+// admitted ranks take the first free slots as the slots are emitted (k_admit_state's work)
+struct FreeFinState {
+  __device__ void operator()(int total, Counters* c) const {
+    if (total < c->misses) {
+      c->err = FC_ERR_INSUFFICIENT_FREE_SLOTS;
+      return;
+    }
+    c->free_count -= c->misses;  // applied once, by block 0 on the shared counters
+  }
+};
+
+struct FreeEmitState {
+  static constexpr bool kVisitAll = false, kClear = false, kCount = false;
+  int32_t* target;
+  const int32_t* admitted;
+  int32_t* slot_to_rank;
+  int32_t* rank_to_slot;
+  uint32_t* res;
+  uint32_t* freeb;
+  __device__ void init(const Counters*) {}
+  __device__ int* counter(Counters*) const { return nullptr; }
+  __device__ __forceinline__ int operator()(int64_t s, int a) const {
+    const int r = admitted[a];
+    target[a] = (int32_t)s;
+    slot_to_rank[s] = r;
+    rank_to_slot[r] = (int32_t)s;
+    atomicOr(&res[r >> 5], 1u << (r & 31));
+    atomicAnd(&freeb[s >> 5], ~(1u << (s & 31)));  // this thread read s's word already
+    return 0;
+  }
+};
+
+// k_inverse + the eviction count (k_plan, :293-296) by one thread of block 0
+template <typename IdT>
+__global__ void __launch_bounds__(kNT) k_inverse_plan(const IdT* __restrict__ ids, int64_t n,
+                                                      const int32_t* __restrict__ aux, int32_t* __restrict__ inv,
+                                                      Counters* c, int cap, int evict_mode) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && c->err == 0) {  // misses are final (k_unique_info)
+    const int m = c->misses, u = c->unique, fr = c->free_count;
+    const int needed = evict_mode == FC_EVICT_OCCUPANCY_AWARE ? max(0, m - fr) : max(0, u - cap);
+    c->needed = needed;
+    if (fr + needed < m) c->err = FC_ERR_INSUFFICIENT_FREE_SLOTS;  // paper_literal (:313-317)
+    c->win_admit[0] = 0;
+    c->win_admit[1] = m;
+  }
+  if (!c->emitted) return;
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT)
+    inv[i] = aux[(int64_t)ids[i]];
 }
 
-// admitted ranks (ascending) take the first free slots (ascending) (:310-323)
-__global__ void k_admit_state(const int32_t* __restrict__ admitted, const int32_t* __restrict__ target,
-                              int32_t* slot_to_rank, int32_t* rank_to_slot, uint32_t* res, uint32_t* freeb,
-                              Counters* c) {
-  if (!gate_open(c, G_ADMIT)) return;
-  const int m = c->misses;
-  for (int j = blockIdx.x * kNT + threadIdx.x; j < m; j += gridDim.x * kNT) {
-    const int r = admitted[j];
-    const int s = target[j];
-    slot_to_rank[s] = r;
-    rank_to_slot[r] = s;
-    atomicOr(&res[r >> 5], 1u << (r & 31));
-    atomicAnd(&freeb[s >> 5], ~(1u << (s & 31)));
+// k_finish + the counters' publication to the pinned mapped host copy (k_publish)
+__global__ void __launch_bounds__(kNT) k_finish_publish(const int32_t* __restrict__ uids,
+                                                        const int32_t* __restrict__ uranks,
+                                                        int32_t* __restrict__ uslots, int32_t* aux,
+                                                        const int32_t* __restrict__ rank_to_slot, uint32_t* prot,
+                                                        uint32_t* miss, const Counters* c, Counters* host) {
+  if (blockIdx.x == 0 && threadIdx.x < 32) {  // the counters do not change any more in this phase
+    const int* src = reinterpret_cast<const int*>(c);
+    int* dst = reinterpret_cast<int*>(host);
+    constexpr int kWords = (int)(sizeof(Counters) / sizeof(int));
+    for (int i = threadIdx.x; i < kWords; i += 32) dst[i] = src[i];
+    __threadfence_system();
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) c->free_count -= m;
+  if (!c->emitted) return;
+  const int u = c->unique;
+  const bool ok = c->err == 0;
+  for (int p = blockIdx.x * kNT + threadIdx.x; p < u; p += gridDim.x * kNT) {
+    aux[uids[p]] = 0;
+    const int r = uranks[p];
+    prot[r >> 5] = 0u;
+    miss[r >> 5] = 0u;
+    if (ok) uslots[p] = rank_to_slot[r];  // :325
+  }
+}
+
+static void compaction_shape(int64_t nwords, int& nb, int64_t& chunk) {
+  nb = grid_for(nwords, 128, kMaxScanBlocks);
+  chunk = (nwords + nb - 1) / nb;
 }
 
 int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt,
-                       int32_t* uranks, int32_t* uslots, int32_t* inverse, const IndexBufs& b, cudaStream_t st) {
+                       int32_t* uranks, int32_t* uslots, int32_t* inverse, const IndexBufs& b, Counters* publish,
+                       cudaStream_t st) {
   Counters* c = b.ctr;
   k_begin<<<1, 1, 0, st>>>(c, h->live);
   h->live = c;
@@ -591,25 +719,38 @@ int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, i
   trace_mark(h, 21, st);
   const int gu = grid_for(std::min<int64_t>(n, h->capacity), kNT, kSMs * 8);
   k_unique_info<<<grid_for(std::min<int64_t>(n, h->capacity), kNT * kUiIlp, kSMs * 8), kNT, 0, st>>>(
-      uids, h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, ucnt,
-                                    uranks, uslots, c);
-  if (ids_bytes == 8) k_inverse<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->aux, inverse, c);
-  else k_inverse<int><<<gn, kNT, 0, st>>>((const int*)ids, n, h->aux, inverse, c);
+      uids, h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, ucnt, uranks, uslots, c);
+  // (the pipeline requires a row to fit the buffer: no BufferTooSmall ordering here)
+  if (ids_bytes == 8)
+    k_inverse_plan<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->aux, inverse, c, h->capacity,
+                                                 h->evict_mode);
+  else
+    k_inverse_plan<int><<<gn, kNT, 0, st>>>((const int*)ids, n, h->aux, inverse, c, h->capacity, h->evict_mode);
   trace_mark(h, 22, st);
-  k_plan<<<1, 1, 0, st>>>(c, h->capacity, h->evict_mode);  // (the pipeline requires a row to fit the buffer)
-  compact(CandWords{h->res_bits, h->prot_bits}, EvictFin{}, EvictEmit{b.evicted, 0}, h->nw_ids, h->block_cnt,
-          win_evict(c), c, G_EVICT, st);
-  k_evict_state<<<grid_for(h->capacity, kNT, kSMs * 4), kNT, 0, st>>>(b.evicted, b.vslots, h->slot_to_rank,
-                                                                      h->rank_to_slot, h->res_bits, h->free_bits, c);
+  // victims' and misses' counts in one launch; the misses' emission shares a launch with the
+  // free slots' count (which needs the freed victim slots)
+  int nb_id, nb_sl;
+  int64_t ch_id, ch_sl;
+  compaction_shape(h->nw_ids, nb_id, ch_id);
+  compaction_shape(h->nw_slots, nb_sl, ch_sl);
+  const CandWords cand{h->res_bits, h->prot_bits};
+  k_bits_count2<CandWords, ArrWords><<<2 * nb_id, kNT, 0, st>>>(cand, h->nw_ids, ch_id, h->block_cnt, nb_id, G_EVICT,
+                                                              ArrWords{h->miss_bits}, h->nw_ids, ch_id, h->block_cnt2,
+                                                              G_ADMIT, c);
+  k_bits_emit<CandWords, EvictEmitState, EvictFinState><<<nb_id, kNT, 0, st>>>(
+      cand, EvictEmitState{b.evicted, b.vslots, h->slot_to_rank, h->rank_to_slot, h->res_bits, h->free_bits, 0},
+      EvictFinState{}, h->nw_ids, ch_id, h->block_cnt, nb_id, win_evict(c), c, G_EVICT);
   trace_mark(h, 23, st);
-  compact(ArrWords{h->miss_bits}, AdmitFin{}, RankEmit{b.admitted}, h->nw_ids, h->block_cnt, win_admit(c), c, G_ADMIT,
-          st);
-  compact(ArrWords{h->free_bits}, FreeFin{}, RankEmit{b.target}, h->nw_slots, h->block_cnt2, win_admit(c), c, G_ADMIT,
-          st);
-  k_admit_state<<<grid_for(h->capacity, kNT, kSMs * 4), kNT, 0, st>>>(b.admitted, b.target, h->slot_to_rank,
-                                                                      h->rank_to_slot, h->res_bits, h->free_bits, c);
+  k_bits_emit_count<ArrWords, RankEmit, AdmitFin, ArrWords><<<nb_id + nb_sl, kNT, 0, st>>>(
+      ArrWords{h->miss_bits}, RankEmit{b.admitted}, AdmitFin{}, h->nw_ids, ch_id, h->block_cnt2, nb_id, win_admit(c),
+      G_ADMIT, ArrWords{h->free_bits}, h->nw_slots, ch_sl, h->block_cnt, G_ADMIT, c);
+  k_bits_emit<ArrWords, FreeEmitState, FreeFinState><<<nb_sl, kNT, 0, st>>>(
+      ArrWords{h->free_bits}, FreeEmitState{b.target, b.admitted, h->slot_to_rank, h->rank_to_slot, h->res_bits,
+                                            h->free_bits},
+      FreeFinState{}, h->nw_slots, ch_sl, h->block_cnt, nb_sl, win_admit(c), c, G_ADMIT);
   trace_mark(h, 24, st);
-  k_finish<<<gu, kNT, 0, st>>>(uids, uranks, uslots, h->aux, h->rank_to_slot, h->prot_bits, h->miss_bits, c);
+  k_finish_publish<<<gu, kNT, 0, st>>>(uids, uranks, uslots, h->aux, h->rank_to_slot, h->prot_bits, h->miss_bits, c,
+                                       publish);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }

@@ -245,7 +245,8 @@ int launch_warmup_state(fc_cache* h, int64_t k, cudaStream_t st);
 int launch_mark_dirty(fc_cache* h, const int64_t* slots, int64_t n, cudaStream_t st);
 int launch_reset_counters(fc_cache* h, cudaStream_t st);
 int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt,
-                       int32_t* uranks, int32_t* uslots, int32_t* inverse, const IndexBufs& b, cudaStream_t st);
+                       int32_t* uranks, int32_t* uslots, int32_t* inverse, const IndexBufs& b, Counters* publish,
+                       cudaStream_t st);
 
 // row kernels (fc_rows.cu)
 int launch_evict_rows(fc_cache* h, cudaStream_t st);
