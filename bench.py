@@ -67,6 +67,7 @@ METRIC = "cached-embedding lookups/sec"
 # synchronous prepare = k_clear_pending + 16 (k_begin, k_mark_ids, 4 compactions x (count + emit),
 # k_unique_info, k_inverse, k_plan, k_evict_async, k_admit_async_tma, k_finish); pooled forward 1;
 # sim update 1; backward = radix sort (histogram + 2 one-sweep passes) + fused stream + fix-up = 5
+# (4 after a pipelined prepare: its index phase makes the histograms)
 KERNELS_PER_STEP = 17 + 1 + 1
 KERNELS_PER_TRAIN_STEP = 17 + 1 + 5
 # prefetch pipeline (round 2, fused index phase): 11 index kernels (k_begin, k_mark_ids, ids count +
@@ -74,7 +75,7 @@ KERNELS_PER_TRAIN_STEP = 17 + 1 + 5
 # changes, misses emit + free-slot count, free-slot emit with the admissions' slot-table changes,
 # k_finish_publish) + k_admit_stage_tma + k_clear_pending, k_evict_commit, k_admit_commit = 15
 # instead of the synchronous prepare's 17
-PIPELINE_EXTRA_KERNELS = 15 - 17
+PIPELINE_EXTRA_KERNELS = 15 - 17 - 1  # (- the backward's histogram kernel)
 # row-sharded training step (profiles/r01_launches_sharded*): fc_route 6 (k_begin, k_route_mark,
 # count + emit, k_route_inverse, k_route_finish) + the owner's pipelined prepare 17 + 4 + the
 # requester's gradient reduction 5 + the owner's apply (k_bwd_direct when every received id is

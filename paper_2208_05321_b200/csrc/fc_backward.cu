@@ -35,7 +35,8 @@ struct Grouping {
 static size_t grouping_bytes(int64_t n) { return align16(n * 4) * 2 + align16(sort_scratch_bytes(n)); }
 
 static int build_grouping(void** scratch, size_t* scratch_bytes, const int32_t* inv, int64_t u, int64_t n,
-                          size_t extra, Grouping& g, cudaStream_t st, bool state_zeroed = false) {
+                          size_t extra, Grouping& g, cudaStream_t st, bool state_zeroed = false,
+                          const int32_t* sort_hist = nullptr) {
   int rc = ensure_scratch_buf(scratch, scratch_bytes, grouping_bytes(n) + extra);
   if (rc) return rc;
   char* p = static_cast<char*>(*scratch);
@@ -48,7 +49,7 @@ static int build_grouping(void** scratch, size_t* scratch_bytes, const int32_t* 
   p += align16(sort_scratch_bytes(n));
   g.rest = p;
   return radix_sort_pairs(reinterpret_cast<const uint32_t*>(inv), nullptr, g.keys, g.order, n, key_bits_for(u),
-                          sort_scr, st, state_zeroed);
+                          sort_scr, st, state_zeroed, sort_hist);
 }
 
 // ------------------------------------------------------------- scatter_update, bit-exact with np.add.at
@@ -461,7 +462,8 @@ __global__ void __launch_bounds__(kNT) k_bwd_direct(BwdArgs x, const int32_t* __
 static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* inv, int64_t u, int64_t n,
                          const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw,
                          int mode, const float* grad, int D, float* gu_out, BwdArgs& x, bool apply, cudaStream_t st,
-                         void** zero_for = nullptr, size_t* zero_bytes = nullptr) {
+                         void** zero_for = nullptr, size_t* zero_bytes = nullptr,
+                         const int32_t* sort_hist = nullptr) {
   if (D % 4 || (reinterpret_cast<uintptr_t>(grad) & 15) || (reinterpret_cast<uintptr_t>(gu_out) & 15)) {
     set_error("backward needs dim %% 4 == 0 and 16-byte aligned gradient rows");
     return FC_ERR_BAD_ARG;
@@ -481,7 +483,7 @@ static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* i
   const bool zeroed = zero_for && *zero_for != nullptr && *zero_for == *scratch && *zero_bytes >= state &&
                       grouping_bytes(n) + extra <= *scratch_bytes;
   Grouping g;
-  int rc = build_grouping(scratch, scratch_bytes, inv, u, n, extra, g, st, zeroed);
+  int rc = build_grouping(scratch, scratch_bytes, inv, u, n, extra, g, st, zeroed, sort_hist);
   if (zero_for) {  // valid again only once the fix-up below is queued
     *zero_for = nullptr;
     *zero_bytes = 0;
@@ -584,8 +586,10 @@ int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, cons
     FC_CUDA(cudaGetLastError());
     return FC_OK;
   }
+  // the digit histograms of `inv`, when a pipeline index phase produced it (no histogram kernel)
+  const int32_t* sort_hist = pipe_take_sort_hist(h, inv, n);
   int rc = segment_grads(&h->scratch, &h->scratch_bytes, inv, u, n, offsets, off_bytes, nbags, include_last, psw, mode,
-                         grad, D, nullptr, x, fused, st, &h->sort_zero_for, &h->sort_zero_bytes);
+                         grad, D, nullptr, x, fused, st, &h->sort_zero_for, &h->sort_zero_bytes, sort_hist);
   if (rc || fused) return rc;
   k_bwd_apply<<<grid_for(u, kNT, kSMs * 8), kNT, 0, st>>>(x, u);  // the unfused variant: per-row sums, then apply
   FC_CUDA(cudaGetLastError());

@@ -828,6 +828,14 @@ struct Pipe {
   float* astage_s[2] = {nullptr, nullptr}; // [arows, S]
   int32_t arows = 0;                       // rows per admission stage (grown on demand)
   int32_t scap[2] = {0, 0};                // rows the last staging of each parity staged at most
+  // digit histograms of each begun batch's inverse for its backward's radix sort, in a ring
+  // deep enough that a batch's backward has run before its buffer is zeroed again (the index
+  // phase of batch t+4 follows commit(t+2), which follows backward(t+1) on the compute stream)
+  static constexpr int kHistRing = 4;
+  int32_t* sort_hist[kHistRing] = {};
+  const int32_t* hist_inv[kHistRing] = {};
+  int64_t hist_n[kHistRing] = {};
+  int hist_next = 0;
   void* fixed_arena = nullptr;             // counters + index lists of both parities
   int64_t fixed_bytes = 0;
   void* stage_arena = nullptr;             // both admission stages
@@ -905,6 +913,7 @@ static int pipe_create(fc_cache* h) {
   const size_t C = (size_t)h->capacity;
   q->arows = initial_stage_rows(h);
   Arena fx, sa;
+  for (int k = 0; k < Pipe::kHistRing; ++k) fx.add(&q->sort_hist[k], kSortHistInts);
   for (int p = 0; p < 2; ++p) {
     fx.add(&q->ib[p].ctr, 1);
     fx.add(&q->ib[p].evicted, C);
@@ -1328,6 +1337,19 @@ static int pipe_grow_admission(fc_cache* h, int64_t need) {
   return FC_OK;
 }
 
+const int32_t* pipe_take_sort_hist(fc_cache* h, const int32_t* inverse, int64_t n) {
+  Pipe* q = h->pipe;
+  if (!q || !inverse) return nullptr;
+  for (int k = 0; k < Pipe::kHistRing; ++k) {  // newest first
+    const int i = (q->hist_next + Pipe::kHistRing - 1 - k) % Pipe::kHistRing;
+    if (q->hist_inv[i] == inverse && q->hist_n[i] == n) {
+      q->hist_inv[i] = nullptr;  // one backward per prepare
+      return q->sort_hist[i];
+    }
+  }
+  return nullptr;
+}
+
 int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt, int32_t* uranks,
                int32_t* uslots, int32_t* inverse, cudaStream_t st) {
   if (h->engine != 1) {
@@ -1363,7 +1385,12 @@ int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* 
   if (q->has_index[o]) FC_CUDA(cudaStreamWaitEvent(st, q->ev_index[o], 0));
   if (q->has_commit[p]) FC_CUDA(cudaStreamWaitEvent(st, q->ev_commit[p], 0));
   trace_mark(h, T_INDEX_BEGIN, st);
-  int rc = launch_index_phase(h, ids, ids_bytes, n, uids, ucnt, uranks, uslots, inverse, q->ib[p], q->hctr_dev[p], st);
+  const int hs = q->hist_next;
+  q->hist_next = (hs + 1) % Pipe::kHistRing;
+  q->hist_inv[hs] = inverse;
+  q->hist_n[hs] = n;
+  int rc = launch_index_phase(h, ids, ids_bytes, n, uids, ucnt, uranks, uslots, inverse, q->ib[p], q->hctr_dev[p],
+                              q->sort_hist[hs], st);
   if (rc) return rc;
   trace_mark(h, T_INDEX_END, st);
   FC_CUDA(cudaEventRecord(q->ev_index[p], st));

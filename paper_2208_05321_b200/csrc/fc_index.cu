@@ -256,17 +256,32 @@ struct IdEmit {
 // works on kUiIlp ids at once so their loads overlap.
 constexpr int kUiIlp = 4;
 
+// sort_hist (pipeline only): also the digit histograms of the inverse this batch will have
+// -- unique position p occurs cnt times -- in the layout the backward's radix sort reads
+// ([passes][bins], digits of key_bits_for(u) bits), so the backward runs no histogram
+// kernel of its own (a launch costs ~100 us on the compute stream beside the staging).
 __global__ void __launch_bounds__(kNT) k_unique_info(const int32_t* __restrict__ uids, int32_t* aux,
                                                      const int32_t* __restrict__ rank_of,
                                                      const int32_t* __restrict__ rank_to_slot, uint32_t* prot,
                                                      uint32_t* miss, int32_t* __restrict__ ucnt,
                                                      int32_t* __restrict__ uranks, int32_t* __restrict__ uslots,
-                                                     Counters* c) {
+                                                     Counters* c, int32_t* sort_hist) {
+  __shared__ int sh[kSortHistInts];
   if (!c->emitted) return;
   const int u = c->unique;
   const int lane = threadIdx.x & 31;
   const int stride = gridDim.x * kNT;
   int misses = 0;
+  int passes = 0, dbits = 1, bins = 2;
+  if (sort_hist) {  // key_bits_for(u) and radix_sort_pairs' digit split, on device
+    int bits = 1;
+    while ((1 << bits) < u) ++bits;
+    passes = max(1, (bits + 8) / 9);
+    dbits = max(1, (bits + passes - 1) / passes);
+    bins = 1 << dbits;
+    for (int i = threadIdx.x; i < passes * bins; i += kNT) sh[i] = 0;
+    __syncthreads();
+  }
   for (int base = (blockIdx.x * kNT + threadIdx.x) & ~31; base < u; base += stride * kUiIlp) {
     int id[kUiIlp], cnt[kUiIlp], r[kUiIlp], sl[kUiIlp];
     bool in[kUiIlp];
@@ -295,11 +310,17 @@ __global__ void __launch_bounds__(kNT) k_unique_info(const int32_t* __restrict__
         atomicOr(&prot[r[k] >> 5], 1u << (r[k] & 31));
         m = sl[k] < 0;
         if (m) atomicOr(&miss[r[k] >> 5], 1u << (r[k] & 31));
+        for (int q = 0; q < passes; ++q) atomicAdd(&sh[q * bins + ((p >> (q * dbits)) & (bins - 1))], cnt[k]);
       }
       misses += __popc(__ballot_sync(FC_FULL, m));
     }
   }
   if (lane == 0 && misses) atomicAdd(&c->misses, misses);
+  if (sort_hist) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < passes * bins; i += kNT)
+      if (sh[i]) atomicAdd(&sort_hist[i], sh[i]);
+  }
 }
 
 template <typename IdT>
@@ -401,7 +422,9 @@ struct FreeFin {
 // Reset the per-call counters; the persistent free_count is carried over from the
 // counters of the last call (`src`), which may be another counters block (the
 // prefetch pipeline double-buffers its counters).
-__global__ void k_begin(Counters* c, const Counters* src) {
+__global__ void k_begin(Counters* c, const Counters* src, int32_t* zero = nullptr, int nzero = 0) {
+  for (int i = threadIdx.x; i < nzero; i += blockDim.x) zero[i] = 0;  // the sort histograms of this batch
+  if (threadIdx.x) return;
   if (src != c) c->free_count = src->free_count;
   c->err = 0;
   c->emitted = 0;
@@ -465,7 +488,7 @@ int launch_prepare(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32
   const int gu = grid_for(std::min<int64_t>(n, h->capacity), kNT, kSMs * 8);
   k_unique_info<<<grid_for(std::min<int64_t>(n, h->capacity), kNT * kUiIlp, kSMs * 8), kNT, 0, st>>>(
       uids, h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, ucnt,
-                                    uranks, uslots, c);
+                                    uranks, uslots, c, nullptr);
 
   if (ids_bytes == 8) k_inverse<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->aux, inverse, c);
   else k_inverse<int><<<gn, kNT, 0, st>>>((const int*)ids, n, h->aux, inverse, c);
@@ -705,9 +728,9 @@ static void compaction_shape(int64_t nwords, int& nb, int64_t& chunk) {
 
 int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt,
                        int32_t* uranks, int32_t* uslots, int32_t* inverse, const IndexBufs& b, Counters* publish,
-                       cudaStream_t st) {
+                       int32_t* sort_hist, cudaStream_t st) {
   Counters* c = b.ctr;
-  k_begin<<<1, 1, 0, st>>>(c, h->live);
+  k_begin<<<1, kNT, 0, st>>>(c, h->live, sort_hist, sort_hist ? kSortHistInts : 0);
   h->live = c;
   const int gn = grid_for(n, kNT, kSMs * 8);
   const int gm = grid_for(n, kMarkTile, kSMs * 6);
@@ -719,7 +742,7 @@ int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, i
   trace_mark(h, 21, st);
   const int gu = grid_for(std::min<int64_t>(n, h->capacity), kNT, kSMs * 8);
   k_unique_info<<<grid_for(std::min<int64_t>(n, h->capacity), kNT * kUiIlp, kSMs * 8), kNT, 0, st>>>(
-      uids, h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, ucnt, uranks, uslots, c);
+      uids, h->aux, h->rank_of, h->rank_to_slot, h->prot_bits, h->miss_bits, ucnt, uranks, uslots, c, sort_hist);
   // (the pipeline requires a row to fit the buffer: no BufferTooSmall ordering here)
   if (ids_bytes == 8)
     k_inverse_plan<long long><<<gn, kNT, 0, st>>>((const long long*)ids, n, h->aux, inverse, c, h->capacity,

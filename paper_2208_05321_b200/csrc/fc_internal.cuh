@@ -246,7 +246,9 @@ int launch_mark_dirty(fc_cache* h, const int64_t* slots, int64_t n, cudaStream_t
 int launch_reset_counters(fc_cache* h, cudaStream_t st);
 int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* uids, int32_t* ucnt,
                        int32_t* uranks, int32_t* uslots, int32_t* inverse, const IndexBufs& b, Counters* publish,
-                       cudaStream_t st);
+                       int32_t* sort_hist, cudaStream_t st);
+// the digit histograms a pipeline index phase made for this inverse (then forgotten), or NULL
+const int32_t* pipe_take_sort_hist(fc_cache* h, const int32_t* inverse, int64_t n);
 
 // row kernels (fc_rows.cu)
 int launch_evict_rows(fc_cache* h, cudaStream_t st);
@@ -273,7 +275,9 @@ int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, cons
 // sort / scan helpers (fc_sort.cu)
 size_t sort_scratch_bytes(int64_t n);
 int radix_sort_pairs(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* keys_out, int32_t* vals_out,
-                     int64_t n, int key_bits, void* scratch, cudaStream_t st, bool state_zeroed = false);
+                     int64_t n, int key_bits, void* scratch, cudaStream_t st, bool state_zeroed = false,
+                     const int32_t* ghist_pre = nullptr);
+constexpr int kSortHistInts = 4 * 512;  // digit histograms of up to 4 passes of <= 9-bit digits
 size_t sort_state_bytes(int64_t n, int key_bits);
 int exclusive_scan_i32(const int32_t* in, int32_t* out, int64_t n, void* scratch, cudaStream_t st);
 size_t scan_scratch_bytes(int64_t n);

@@ -208,8 +208,10 @@ __global__ void __launch_bounds__(kRsWarps * 32) k_os_scatter(const uint32_t* __
   for (int r = 0; r < kRsRounds; ++r) {
     if (dd[r] < kRsMaxBins) {
       const int64_t pos = (int64_t)base[dd[r]] + wc[w][dd[r]] + loc[r];
-      kout[pos] = kk[r];
-      vout[pos] = vv[r];
+      if (pos < n) {  // always, unless a precomputed histogram did not match the keys
+        kout[pos] = kk[r];
+        vout[pos] = vv[r];
+      }
     }
   }
 }
@@ -234,8 +236,11 @@ size_t sort_state_bytes(int64_t n, int key_bits) {
 // vals_in == NULL sorts the positions 0..n-1 (an argsort). Inputs are untouched.
 // state_zeroed: the caller guarantees the first sort_state_bytes(n, key_bits) of the
 // scratch are already zero (a previous kernel cleared them), so no memset is queued.
+// ghist_pre: the digit histograms of keys_in, already computed ([passes][bins], the layout
+// k_os_hist writes; the prefetch pipeline's index phase makes them for the backward's sort)
 int radix_sort_pairs(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* keys_out, int32_t* vals_out,
-                     int64_t n, int key_bits, void* scratch, cudaStream_t st, bool state_zeroed) {
+                     int64_t n, int key_bits, void* scratch, cudaStream_t st, bool state_zeroed,
+                     const int32_t* ghist_pre) {
   if (n <= 0) return FC_OK;
   if (n > (int64_t)kOsMask) {
     set_error("radix sort of %lld keys exceeds the 30-bit tile counters", (long long)n);
@@ -258,7 +263,8 @@ int radix_sort_pairs(const uint32_t* keys_in, const int32_t* vals_in, uint32_t* 
   uint32_t* ktmp = reinterpret_cast<uint32_t*>(p);
   int32_t* vtmp = reinterpret_cast<int32_t*>(p + n * sizeof(int32_t));
   if (!state_zeroed) FC_CUDA(cudaMemsetAsync(scratch, 0, head + status_bytes, st));  // histograms, counters, status
-  k_os_hist<<<grid_for(n, kNT * 8, kSMs * 4), kNT, 0, st>>>(keys_in, n, passes, dbits, ghist);
+  if (ghist_pre) ghist = const_cast<int32_t*>(ghist_pre);  // read only below
+  else k_os_hist<<<grid_for(n, kNT * 8, kSMs * 4), kNT, 0, st>>>(keys_in, n, passes, dbits, ghist);
   const uint32_t* ks = keys_in;
   const int32_t* vs = vals_in;
   for (int pass = 0; pass < passes; ++pass) {
