@@ -75,7 +75,8 @@ KERNELS_PER_TRAIN_STEP = 17 + 1 + 5
 # changes, misses emit + free-slot count, free-slot emit with the admissions' slot-table changes,
 # k_finish_publish) + k_admit_stage_tma + k_clear_pending, k_evict_commit, k_admit_commit = 15
 # instead of the synchronous prepare's 17
-PIPELINE_EXTRA_KERNELS = 15 - 17 - 1  # (- the backward's histogram kernel)
+PIPELINE_EXTRA_KERNELS = 15 - 17
+PIPELINE_BWD_SAVED = 1  # the fused backward after a pipelined prepare: no histogram kernel
 # row-sharded training step (profiles/r01_launches_sharded*): fc_route 6 (k_begin, k_route_mark,
 # count + emit, k_route_inverse, k_route_finish) + the owner's pipelined prepare 17 + 4 + the
 # requester's gradient reduction 5 + the owner's apply (k_bwd_direct when every received id is
@@ -443,10 +444,11 @@ def trace_batches(args, world):
 def launches_per_step(args, shard_mode, pipelined, world):
     """Our kernels launched per timed step (checked against the ncu launch lists in profiles/)."""
     if shard_mode is None:
-        return ((KERNELS_PER_STEP if args.step == "sim" else KERNELS_PER_TRAIN_STEP)
-                + (PIPELINE_EXTRA_KERNELS if pipelined else 0))
+        if args.step == "sim":
+            return KERNELS_PER_STEP + (PIPELINE_EXTRA_KERNELS if pipelined else 0)
+        return KERNELS_PER_TRAIN_STEP + (PIPELINE_EXTRA_KERNELS - PIPELINE_BWD_SAVED if pipelined else 0)
     if shard_mode == "column":  # prepare of the global batch + pool + fused backward (NCCL kernels not counted)
-        return KERNELS_PER_TRAIN_STEP + (PIPELINE_EXTRA_KERNELS if pipelined else 0)
+        return KERNELS_PER_TRAIN_STEP + (PIPELINE_EXTRA_KERNELS - PIPELINE_BWD_SAVED if pipelined else 0)
     return (SHARDED_BASE_KERNELS + (PIPELINE_EXTRA_KERNELS if pipelined else 0) + (1 if world == 1 else 5)
             + (2 if args.peer else 1))
 
