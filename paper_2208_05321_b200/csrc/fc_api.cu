@@ -445,6 +445,7 @@ int fc_prepare(fc_cache* h, const void* ids, int32_t ids_bytes, int64_t n, int64
   cudaStream_t st = as_stream(stream);
   FC_TRY(pipe_order(h, st));
   FC_TRY(engine_begin(h, st));
+  pipe_forget_sort_hist(h, inverse);  // this inverse buffer gets new contents, without histograms
   FC_TRY(launch_prepare(h, ids, ids_bytes, n, uids, ucnt, uranks, uslots, inverse, st));
   h->ev_src = h->evicted_ranks;
   h->ad_src = h->admitted_ranks;

@@ -1337,6 +1337,13 @@ static int pipe_grow_admission(fc_cache* h, int64_t need) {
   return FC_OK;
 }
 
+void pipe_forget_sort_hist(fc_cache* h, const int32_t* inverse) {
+  Pipe* q = h->pipe;
+  if (!q) return;
+  for (int k = 0; k < Pipe::kHistRing; ++k)
+    if (q->hist_inv[k] == inverse) q->hist_inv[k] = nullptr;
+}
+
 const int32_t* pipe_take_sort_hist(fc_cache* h, const int32_t* inverse, int64_t n) {
   Pipe* q = h->pipe;
   if (!q || !inverse) return nullptr;
@@ -1385,6 +1392,7 @@ int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* 
   if (q->has_index[o]) FC_CUDA(cudaStreamWaitEvent(st, q->ev_index[o], 0));
   if (q->has_commit[p]) FC_CUDA(cudaStreamWaitEvent(st, q->ev_commit[p], 0));
   trace_mark(h, T_INDEX_BEGIN, st);
+  pipe_forget_sort_hist(h, inverse);  // an older batch's histograms for this buffer are stale now
   const int hs = q->hist_next;
   q->hist_next = (hs + 1) % Pipe::kHistRing;
   q->hist_inv[hs] = inverse;

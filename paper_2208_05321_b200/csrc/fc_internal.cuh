@@ -249,6 +249,7 @@ int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, i
                        int32_t* sort_hist, cudaStream_t st);
 // the digit histograms a pipeline index phase made for this inverse (then forgotten), or NULL
 const int32_t* pipe_take_sort_hist(fc_cache* h, const int32_t* inverse, int64_t n);
+void pipe_forget_sort_hist(fc_cache* h, const int32_t* inverse);  // a synchronous prepare rewrites it
 
 // row kernels (fc_rows.cu)
 int launch_evict_rows(fc_cache* h, cudaStream_t st);

@@ -549,3 +549,38 @@ def test_prefetch_clean_victims_ship_exact_writebacks():
     ro = st[0]
     assert ro["writeback_rows"] > 0  # the first read-only steps still evict rows trained earlier
     assert ro["writeback_d2h_bytes"] < 0.5 * ro["victim_bytes"], ro
+
+
+def test_sync_prepare_into_a_prefetched_buffer_gets_its_own_sort():
+    """A pipelined prepare leaves the digit histograms of its inverse for that batch's
+    backward (keyed by the inverse buffer). A batch committed without a backward, whose
+    buffer a synchronous prepare of another batch then reuses, must not lend it its
+    histograms: the backward of the new batch is checked row by row."""
+    from paper_2208_05321_b200.device import DeviceCache
+
+    num, dim, cap, n, lr = 20_000, 32, 4_000, 6_000, 0.1
+    rng = np.random.default_rng(21)
+    rows = fc.store.pinned_empty((num, dim))
+    rows[...] = rng.uniform(-1, 1, (num, dim)).astype(np.float32)
+    dc = DeviceCache(num, cap, dim, device="cuda")
+    dc.set_idx_map(np.arange(num))
+    dc.attach_slow(rows)
+    dc.set_engine("async")
+    a = torch.from_numpy(rng.integers(0, num // 2, n).astype(np.int32)).cuda()
+    b = torch.from_numpy(rng.integers(num // 2, num, n).astype(np.int32)).cuda()
+    dc.prepare_begin(a)
+    res_a = dc.prepare_commit()  # committed, never backwarded
+    ptr_a = res_a[5].data_ptr()
+    del res_a
+    torch.cuda.synchronize()
+    info, uids, ucnt, uranks, uslots, inverse, _ = dc.prepare(b)
+    reused = inverse.data_ptr() == ptr_a
+    u = int(info.unique)
+    grad = torch.from_numpy(rng.standard_normal((n, dim)).astype(np.float32)).cuda()
+    before = dc.fast_rows[uslots.long()].double()
+    gsum = torch.zeros((u, dim), dtype=torch.float64, device="cuda").index_add_(0, inverse.long(), grad.double())
+    dc.backward_update(uslots, inverse, ucnt, None, n, False, None, "sum", grad, "sgd", lr, 1e-10)
+    torch.cuda.synchronize()
+    after = dc.fast_rows[uslots.long()].double()
+    np.testing.assert_allclose(after.cpu().numpy(), (before - lr * gsum).cpu().numpy(), rtol=1e-5, atol=1e-5)
+    print("inverse buffer reused:", reused)
