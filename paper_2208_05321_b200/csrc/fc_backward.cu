@@ -22,8 +22,18 @@
 
 namespace fc {
 
-constexpr int kChunk = 64;  // sorted occurrences per warp in the backward stream
-constexpr int kBwdUnroll = 4;
+// (overridable at build time for tuning sweeps: tools/build_bwd_variants.sh)
+#ifndef FC_BWD_CHUNK
+#define FC_BWD_CHUNK 64
+#endif
+#ifndef FC_BWD_UNROLL
+#define FC_BWD_UNROLL 4
+#endif
+#ifndef FC_BWD_MINBLOCKS
+#define FC_BWD_MINBLOCKS 4
+#endif
+constexpr int kChunk = FC_BWD_CHUNK;  // sorted occurrences per warp in the backward stream
+constexpr int kBwdUnroll = FC_BWD_UNROLL;
 
 struct Grouping {
   uint32_t* keys;   // [n] sorted unique positions
@@ -207,7 +217,7 @@ __device__ __forceinline__ void bwd_flush(const BwdArgs& x, int64_t c, int64_t j
 }
 
 template <bool APPLY>
-__global__ void __launch_bounds__(kNT, 4) k_bwd_stream(BwdArgs x) {
+__global__ void __launch_bounds__(kNT, FC_BWD_MINBLOCKS) k_bwd_stream(BwdArgs x) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
