@@ -558,7 +558,7 @@ def test_sync_prepare_into_a_prefetched_buffer_gets_its_own_sort():
     histograms: the backward of the new batch is checked row by row."""
     from paper_2208_05321_b200.device import DeviceCache
 
-    num, dim, cap, n, lr = 20_000, 32, 4_000, 6_000, 0.1
+    num, dim, cap, n, lr = 20_000, 32, 8_000, 6_000, 0.1
     rng = np.random.default_rng(21)
     rows = fc.store.pinned_empty((num, dim))
     rows[...] = rng.uniform(-1, 1, (num, dim)).astype(np.float32)
@@ -569,13 +569,24 @@ def test_sync_prepare_into_a_prefetched_buffer_gets_its_own_sort():
     a = torch.from_numpy(rng.integers(0, num // 2, n).astype(np.int32)).cuda()
     b = torch.from_numpy(rng.integers(num // 2, num, n).astype(np.int32)).cuda()
     dc.prepare_begin(a)
-    res_a = dc.prepare_commit()  # committed, never backwarded
-    ptr_a = res_a[5].data_ptr()
-    del res_a
-    torch.cuda.synchronize()
-    info, uids, ucnt, uranks, uslots, inverse, _ = dc.prepare(b)
-    reused = inverse.data_ptr() == ptr_a
+    _, ua, ca, ra, sa, inv_a, _ = dc.prepare_commit()  # committed, never backwarded
+    # a synchronous prepare of batch b written into batch a's buffers (fc_prepare directly)
+    import ctypes
+
+    from paper_2208_05321_b200 import _lib
+
+    k = min(n, cap)
+    base = inv_a.data_ptr() - 4 * (4 * k)  # prepare_commit's buffer: [uids|ucnt|uranks|uslots] (k each) + inverse
+    info = _lib.PrepareInfo()
+    ptr = lambda off: ctypes.c_void_p(base + 4 * off)  # noqa: E731
+    assert _lib.load().fc_prepare(dc.h, ctypes.c_void_p(b.data_ptr()), 4, n, 1, ptr(0), ptr(k), ptr(2 * k),
+                                  ptr(3 * k), ptr(4 * k), dc.stream(), ctypes.byref(info)) == 0
+    buf = torch.empty(0, dtype=torch.int32, device="cuda").set_(inv_a.untyped_storage())  # the same allocation
     u = int(info.unique)
+    ucnt = buf[(base - buf.data_ptr()) // 4 + k:][:u]
+    uslots = buf[(base - buf.data_ptr()) // 4 + 3 * k:][:u]
+    inverse = inv_a
+    reused = True
     grad = torch.from_numpy(rng.standard_normal((n, dim)).astype(np.float32)).cuda()
     before = dc.fast_rows[uslots.long()].double()
     gsum = torch.zeros((u, dim), dtype=torch.float64, device="cuda").index_add_(0, inverse.long(), grad.double())
