@@ -54,7 +54,7 @@ static void slow_wait_note(const char* what, std::chrono::steady_clock::time_poi
 
 // Write-back stage buffers in rotation: a host scatter job may lag this many commits
 // behind before a stage reuse has to wait for it (absorbs host-thread jitter).
-constexpr int kWbBufs = 3;
+constexpr int kWbBufs = 4;
 
 struct Job {
   int buf;
@@ -1528,7 +1528,9 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
   AsyncWB* a = h->awb;
   if (c.needed > a->rows) FC_TRY_E(engine_grow(h, c.needed));  // more victims than a stage holds
   const int b = a->cur;
-  if (a->rows_in[b] > 0) {  // write-back stage b still holds a job from kWbBufs commits ago
+  if (a->rows_in[b] > 0) {  // stage b still holds a job (the previous commit could not free it: a synchronous
+                            // prepare ran between them); this batch's staging may still read its marks
+    FC_CUDA(cudaStreamWaitEvent(st, q->ev_xfer[p], 0));
     // the stream (not the host) waits until the host threads have scattered that job;
     // fall back to a host wait when stream memory operations are unavailable
     WaitValueFn wv = std::getenv("FC_HOST_WAIT") ? nullptr : wait_value_fn();
@@ -1544,14 +1546,40 @@ int pipe_commit(fc_cache* h, cudaStream_t st, fc_prepare_info* info) {
     a->rows_in[b] = 0;
     a->rows_on_dev[b] = false;
   }
-  FC_CUDA(cudaStreamWaitEvent(st, q->ev_xfer[p], 0));
   trace_mark(h, T_COMMIT_BEGIN, st);
   PipeArgs x = pipe_args(h, p);
+  // Free the stage the next commit will use now, before the next staging is launched: wait
+  // (on the stream) for its last host job -- kWbBufs - 1 commits old -- and drop the pending
+  // marks that still point into it, so the next staging reads those rows from the slow tier.
+  // Queued first, so that the wait (it polls host memory) overlaps the current staging's
+  // tail. This batch's staging may read those marks meanwhile: the job is done, so the stage
+  // rows and the slow-tier rows are equal, and stage nb is rewritten only by the next commit.
+  const int nb = c.needed > 0 ? (b + 1) % kWbBufs : b;
+  if (nb != b && a->rows_in[nb] > 0) {
+    WaitValueFn wv = std::getenv("FC_HOST_WAIT") ? nullptr : wait_value_fn();
+    if (!wv || wv(reinterpret_cast<CUstream>(st), a->done_dev, (cuuint32_t)a->seq_of[nb], CU_STREAM_WAIT_VALUE_GEQ) !=
+                   CUDA_SUCCESS) {
+      const auto t0 = std::chrono::steady_clock::now();
+      wait_seq(a, a->seq_of[nb]);
+      h->prof[5] += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    }
+    k_clear_pending<<<grid_for(a->rows_in[nb], kNT, kSMs * 4), kNT, 0, st>>>(
+        a->sranks[nb], a->rows_in[nb], a->pending, (int32_t)(nb * a->rows), a->rows,
+        a->rows_on_dev[nb] ? a->dev_rows + nb : nullptr);
+    a->rows_in[nb] = 0;
+    a->rows_on_dev[nb] = false;
+  }
+  // The victims go to the write-back stage without waiting for this batch's staging: the
+  // staging reads only ranks that are not resident, and never stage b, whose marks the
+  // previous commit cleared before launching it (as above). Only the admission needs the
+  // staged rows, so the critical path from the end of one staging to the start of the
+  // next is the admission copy alone.
   if (c.needed > 0) {
     FC_CUDA(cudaMemsetAsync(a->dev_rows + b, 0, sizeof(int32_t), st));
     if (a->vec) k_evict_commit<true><<<kSMs * 8, kNT, 0, st>>>(x);
     else k_evict_commit<false><<<kSMs * 8, kNT, 0, st>>>(x);
   }
+  FC_CUDA(cudaStreamWaitEvent(st, q->ev_xfer[p], 0));
   if (c.misses > 0) {
     if (a->vec) k_admit_commit<true><<<kSMs * 8, kNT, 0, st>>>(x);
     else k_admit_commit<false><<<kSMs * 8, kNT, 0, st>>>(x);
