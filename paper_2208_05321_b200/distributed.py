@@ -557,7 +557,7 @@ class ColumnShardedEmbedding(torch.nn.Module):
         self.mode, self.group = mode, group
         self.device = device if device is not None else getattr(shard, "device", torch.device("cpu"))
         self._anchor = torch.nn.Parameter(torch.empty(0, device=self.device))
-        self._pfq = []  # prefetched batches, oldest first: dicts (src, ids, g_ids, counts, ev, begun)
+        self._pfq = []  # prefetched batches, oldest first: dicts (src, ids, counts, ev, begun)
         self._xstream = None
 
     # the two collectives of the column-wise exchange (overridable: the tests drive the module
