@@ -111,10 +111,14 @@ def _worker(rank, world, port, kind, mode, q, prefetch=False):
                 if r == rank:
                     want = oracle.pooled_bag(dense, ids, off, None, mode)
             ids, off, gout = step[rank]
-            t_ids = tids[si] if prefetch else torch.from_numpy(ids)
+            t_ids = tids[si] if prefetch is True else torch.from_numpy(ids)
             out = mod(t_ids, torch.from_numpy(off) if mode == "mean" else None)
             np.testing.assert_allclose(out.detach().numpy(), want, rtol=1e-5, atol=1e-6)
-            if prefetch and si + 1 < len(data):
+            if prefetch == "bypass" and si + 2 < len(data):
+                # a batch that the next forward does not ask for: that forward executes it
+                # first (FIFO), then prepares its own ids; outputs must not change
+                mod.prefetch(tids[si + 2])
+            elif prefetch and prefetch != "bypass" and si + 1 < len(data):
                 mod.prefetch(tids[si + 1])  # next batch's exchange + prepare start, before this backward
             out.backward(torch.from_numpy(gout))
             # dense SGD with every rank's batch (each rank owns its own bags' gradients)
@@ -139,7 +143,8 @@ def _worker(rank, world, port, kind, mode, q, prefetch=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,prefetch", [("row", False), ("row", True), ("column", False), ("column", True)])
+@pytest.mark.parametrize("kind,prefetch", [("row", False), ("row", True), ("row", "bypass"), ("column", False),
+                                            ("column", True), ("column", "bypass")])
 @pytest.mark.parametrize("mode", ["sum", "mean"])
 def test_two_rank_gloo_matches_dense(kind, mode, prefetch):
     ctx = mp.get_context("fork")
