@@ -66,6 +66,40 @@ def oracle_slot_tables(trace):
     return out
 
 
+def test_column_sharded_bypassed_prefetch_matches_dense():
+    """A prefetched batch that the next forward does not ask for is executed first (FIFO,
+    as the cache's own pipeline does); the outputs and the trained table stay those of
+    dense training."""
+    import torch.distributed as dist
+
+    from paper_2208_05321_b200.distributed import ColumnShardedEmbedding
+
+    trace, table, grads = workload()
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1)
+    try:
+        shard, idx, rows = build(0, 1, trace, table, "cuda")
+        mod = ColumnShardedEmbedding(shard, DIM, 1, 0, mode="sum", device=torch.device("cuda"))
+        dense = table.copy()
+        tids = [torch.from_numpy(trace[s]).cuda() for s in range(STEPS)]
+        for s in range(STEPS):
+            out = mod(tids[s])
+            want = oracle.pooled_bag(dense, trace[s], np.arange(B))
+            np.testing.assert_allclose(out.detach().cpu().numpy(), want, rtol=1e-5, atol=1e-6)
+            if s + 2 < STEPS:
+                mod.prefetch(tids[s + 2])  # not the next batch
+            out.backward(torch.from_numpy(grads[s]).cuda())
+            g = oracle.pooled_bag_backward_rows(grads[s], trace[s], np.arange(B), NUM)
+            oracle.sparse_sgd(dense, np.unique(trace[s]), g, LR)
+        mod.flush()
+        torch.cuda.synchronize()
+        got = np.empty_like(table)
+        got[idx.id_of] = rows
+        np.testing.assert_allclose(got, dense, rtol=1e-5, atol=1e-6)
+    finally:
+        dist.destroy_process_group()
+
+
 @pytest.mark.parametrize("prefetch", [False, True])
 def test_column_sharded_nccl_world1_matches_dense_and_oracle(prefetch):
     import torch.distributed as dist
