@@ -453,6 +453,23 @@ def launches_per_step(args, shard_mode, pipelined, world):
             + (2 if args.peer else 1))
 
 
+def table_placement(cfg, world):
+    """--shard table: one table per sparse feature, laid out contiguously -- Criteo Kaggle's own
+    26 cardinalities when the config has its 33,762,577 rows (sharding.py:26-30), else equal
+    tables -- placed by the reference's largest-first greedy (plan_tables_greedy,
+    sharding.py:158-172)."""
+    from paper_2208_05321_b200.distributed import TablePlacement
+    from paper_2208_05321_b200.sharding import CRITEO_KAGGLE_TABLE_SIZES
+
+    T = cfg["features"]
+    if sum(CRITEO_KAGGLE_TABLE_SIZES) == cfg["num_ids"]:
+        sizes = np.asarray(CRITEO_KAGGLE_TABLE_SIZES, dtype=np.int64)
+    else:
+        sizes = np.full(T, cfg["num_ids"] // T, dtype=np.int64)
+        sizes[:cfg["num_ids"] % T] += 1
+    return TablePlacement.balanced(sizes, world)
+
+
 def run_ours(args, cfg, torch, rank, world):
     import paper_2208_05321_b200 as fc
     from paper_2208_05321_b200.embedding import CachedEmbeddingBag
@@ -466,7 +483,7 @@ def run_ours(args, cfg, torch, rank, world):
     # global batch = world x B samples; this rank's slice is rows [rank*B, (rank+1)*B) of each global batch
     shard_mode = args.shard
     sharded = shard_mode is not None
-    rowwise = shard_mode == "row"
+    rowwise = shard_mode in ("row", "table")  # owner-local reorders need the id counts
     samples, rank_of, id_of, cap = make_workload(cfg, n_batches * world, device=dev, keep_counts=rowwise)
     counts = None
     if rowwise:
@@ -505,9 +522,12 @@ def run_ours(args, cfg, torch, rank, world):
         mod = ColumnShardedEmbedding(shard, D, world, rank, mode=MODE, device=dev)
         dcs = [shard.cache]
     else:
-        from paper_2208_05321_b200.distributed import CudaShard, RowShardedEmbedding, shard_rows_for_rank
+        from paper_2208_05321_b200.distributed import (CudaShard, RowShardedEmbedding, shard_rows_for_rank,
+                                                       shard_tables_for_rank)
 
-        idx = shard_rows_for_rank(counts, rank, world)
+        placement = table_placement(cfg, world) if shard_mode == "table" else None
+        idx = (shard_rows_for_rank(counts, rank, world) if placement is None
+               else shard_tables_for_rank(counts, placement, rank))
         rows = fc.store.pinned_empty((idx.num_ids, D))
         fill_pinned(torch, rows, dev, SEED + rank)
         shard = CudaShard(idx.num_ids, D, fc.fast_capacity(idx.num_ids, cfg["ratio"]), rows, idx, optimizer=OPT,
@@ -516,7 +536,8 @@ def run_ours(args, cfg, torch, rank, world):
         # peer memory (fc_pool_to_peers) with --peer; by default the rows come back by NCCL all-to-all
         # (faster at world 1, 325-332 vs 290-316 M lookups/s, profiles/r01_bench_sharded_*.json; the
         # peer path is untested across GPUs in this build's runs)
-        mod = RowShardedEmbedding(shard, world, rank, mode=MODE, device=dev, peer_rows=N if args.peer else 0)
+        mod = RowShardedEmbedding(shard, world, rank, mode=MODE, device=dev, peer_rows=N if args.peer else 0,
+                                  placement=placement)
         dcs = [shard.cache]
         cap = shard.cache.capacity
     dc = dcs[0]
@@ -882,6 +903,18 @@ def run_reference_arm(args, cfg, world, steps, warmup, time_budget_s=None):
                                                                      num_ids=len(counts[r::world])))))
         def parts(ids):
             return [(st, ids[m] // world, m, (0, D)) for st, m in zip(stacks, [ids % world == r for r in range(world)])]
+    elif shard == "table":  # one stack per rank over its whole tables, rank-local reorder
+        pl = table_placement(cfg, world)
+        stacks = []
+        for r in range(world):
+            g = pl.global_ids(r)
+            stacks.append(stack(g.size, D, rfs.build_reorder(rfs.FrequencyTable(counts=counts[g], num_ids=g.size))))
+        tstart = pl.starts
+
+        def parts(ids):
+            t = np.searchsorted(tstart, ids, side="right") - 1
+            own, loc = pl.owner[t], pl.lbase[t] + (ids - tstart[t])
+            return [(st, loc[own == r], own == r, (0, D)) for r, st in enumerate(stacks)]
     else:
         idx = rfs.build_reorder(rfs.FrequencyTable(counts=counts, num_ids=cfg["num_ids"]))
         plan = rsh.partition_columns(D, world if shard == "column" else 1)
@@ -953,9 +986,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="criteo_kaggle", choices=list(CONFIGS))
     ap.add_argument("--step", default="train", choices=["train", "sim"])
-    ap.add_argument("--shard", default=None, choices=["row", "column"],
-                    help="table split over the ranks: row (id %% N owners, the scaling variant; default at N>1) "
-                         "or column (the reference's column-wise split, sharding.py:46-118)")
+    ap.add_argument("--shard", default=None, choices=["row", "column", "table"],
+                    help="table split over the ranks: row (id %% N owners, the scaling variant; default at N>1), "
+                         "column (the reference's column-wise split, sharding.py:46-118) or table (one table per "
+                         "sparse feature, whole tables per rank)")
     ap.add_argument("--trace-batches", type=int, default=64)
     ap.add_argument("--cpu-baseline-s", type=float, default=20.0, help="time budget of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")

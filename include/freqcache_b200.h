@@ -273,6 +273,15 @@ int fc_backward_update(fc_cache* h, const int32_t* unique_slots, const int32_t* 
 typedef struct fc_router fc_router;  /* bitmap + scratch over a [world x S] routing key space */
 
 int fc_router_create(int64_t num_ids, int32_t world, int32_t device, fc_router** out);
+/* Table-wise placement (north star: tables sharded table-wise or column-wise): table t is the
+ * id range [table_starts[t], table_starts[t+1]) (table_starts[0] = 0, [num_tables] = num_ids)
+ * and belongs whole to rank table_owner[t]; an owner's local rows are its tables in table
+ * order. fc_route then groups ids by owner and returns owner-local ids, as for row-wise.
+ * Replaces the reference's table-wise placement, which it only plans and measures
+ * (plan_tables_greedy / tablewise_imbalance, sharding.py:158-193): here the owners come
+ * from that same greedy and the ids are actually routed to them. */
+int fc_router_create_tables(int64_t num_ids, int32_t world, int32_t num_tables, const int64_t* table_starts_host,
+                            const int32_t* table_owner_host, int32_t device, fc_router** out);
 int fc_router_destroy(fc_router* r);
 
 /* A requester's batch routed to row owners (owner = id % world, owner-local row =

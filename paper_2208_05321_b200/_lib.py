@@ -75,6 +75,7 @@ _SIGS = {
     "fc_build_reorder": (c_int32, [c_void_p, c_int32, c_int64, c_int64, c_void_p, c_void_p, c_void_p,
                                    POINTER(c_int64), c_void_p]),
     "fc_router_create": (c_int32, [c_int64, c_int32, c_int32, POINTER(c_void_p)]),
+    "fc_router_create_tables": (c_int32, [c_int64, c_int32, c_int32, c_void_p, c_void_p, c_int32, POINTER(c_void_p)]),
     "fc_router_destroy": (c_int32, [c_void_p]),
     "fc_route": (c_int32, [c_void_p, c_void_p, c_int32, c_int64, c_void_p, c_void_p, c_void_p, POINTER(c_int64),
                            c_void_p]),

@@ -784,11 +784,39 @@ int launch_index_phase(fc_cache* h, const void* ids, int ids_bytes, int64_t n, i
 // one ordered compaction of a bitmap over the key space key = owner * S + id / world —
 // plus every occurrence's position in that list (its inverse) and per-owner counts
 // for the all-to-all splits. Same machinery as prepare's dedup (k_mark_ids / IdEmit).
-template <typename IdT>
-__global__ void __launch_bounds__(kNT) k_route_mark(const IdT* __restrict__ ids, int64_t n, int64_t num_ids, int W,
-                                                    int64_t S, uint32_t* bits, Counters* c) {
+// Owner and owner-local row of a global id, as the routing key owner * S + local:
+//   RowMap   — row-wise: owner = id % W, local = id / W;
+//   TableMap — table-wise: whole tables (contiguous id ranges [starts[t], starts[t+1]))
+//              belong to owner[t] and sit at lbase[t] in that owner's local id space.
+struct RowMap {
+  uint32_t w, s;
+  __device__ __forceinline__ int key(long long id) const {
+    const uint32_t u = (uint32_t)id;
+    return (int)((u % w) * s + u / w);
+  }
+};
+
+struct TableMap {
+  const long long* starts;  // [T + 1]
+  const int* owner;         // [T]
+  const long long* lbase;   // [T]
+  int T;
+  long long S;
+  __device__ __forceinline__ int key(long long id) const {
+    int lo = 0, hi = T - 1;  // the last table whose start is <= id
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (starts[mid] <= id) lo = mid;
+      else hi = mid - 1;
+    }
+    return (int)(owner[lo] * S + lbase[lo] + (id - starts[lo]));
+  }
+};
+
+template <typename IdT, class Map>
+__global__ void __launch_bounds__(kNT) k_route_mark(const IdT* __restrict__ ids, int64_t n, int64_t num_ids, Map map,
+                                                    uint32_t* bits, Counters* c) {
   const int lane = threadIdx.x & 31;
-  const uint32_t w = (uint32_t)W, s32 = (uint32_t)S;  // key space < 2^31 (checked at create)
   for (int64_t base = (int64_t)blockIdx.x * kNT; base < n; base += (int64_t)gridDim.x * kNT) {
     const int64_t i = base + threadIdx.x;
     const bool valid = i < n;
@@ -798,8 +826,7 @@ __global__ void __launch_bounds__(kNT) k_route_mark(const IdT* __restrict__ ids,
       if (id < 0) atomicMin(&c->lo, id);
       else atomicMax(&c->hi, id);
     }
-    const uint32_t u = (uint32_t)id;
-    const int key = inr ? (int)((u % w) * s32 + u / w) : -1;
+    const int key = inr ? map.key(id) : -1;  // key space < 2^31 (checked at create)
     // one leader per distinct key of the warp; a read before the atomic skips the
     // bits already set (Zipf batches repeat head ids a lot)
     const unsigned peers = __match_any_sync(FC_FULL, key);
@@ -838,16 +865,13 @@ struct RouteEmit {
   }
 };
 
-template <typename IdT>
-__global__ void __launch_bounds__(kNT) k_route_inverse(const IdT* __restrict__ ids, int64_t n, int W, int64_t S,
+template <typename IdT, class Map>
+__global__ void __launch_bounds__(kNT) k_route_inverse(const IdT* __restrict__ ids, int64_t n, Map map,
                                                        const int32_t* __restrict__ aux, int32_t* __restrict__ inv,
                                                        const Counters* c) {
   if (!c->emitted) return;
-  const uint32_t w = (uint32_t)W, s32 = (uint32_t)S;
-  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT) {
-    const uint32_t u = (uint32_t)ids[i];
-    inv[i] = aux[(u % w) * s32 + u / w];
-  }
+  for (int64_t i = (int64_t)blockIdx.x * kNT + threadIdx.x; i < n; i += (int64_t)gridDim.x * kNT)
+    inv[i] = aux[map.key((long long)ids[i])];
 }
 
 // clears the key->position map for the next call; block 0 also writes the per-owner
@@ -893,12 +917,17 @@ struct fc_router {
   long long* owner_cnt_host;
   void* scratch;
   size_t scratch_bytes;
+  int32_t ntables;          // > 0: table-wise placement (fc_router_create_tables)
+  long long* t_starts;      // device [T + 1]
+  int* t_owner;             // device [T]
+  long long* t_lbase;       // device [T]
 };
 
 namespace fc {
 
 static void router_release(fc_router* r) {
-  void* dev[] = {r->bits, r->aux, r->ukeys, r->block_cnt, r->ctr, r->owner_cnt, r->scratch};
+  void* dev[] = {r->bits, r->aux, r->ukeys, r->block_cnt, r->ctr, r->owner_cnt, r->scratch, r->t_starts, r->t_owner,
+                 r->t_lbase};
   for (void* p : dev)
     if (p) cudaFree(p);
   if (r->ctr_host) cudaFreeHost(r->ctr_host);
@@ -910,8 +939,8 @@ static void router_release(fc_router* r) {
 
 using namespace fc;
 
-extern "C" int fc_router_create(int64_t num_ids, int32_t world, int32_t device, fc_router** out) {
-  if (!out || num_ids < 1 || world < 1 || world > 64) return FC_ERR_BAD_ARG;
+// keys per owner S: row-wise ceil(num_ids / world); table-wise the largest owner's rows
+static int router_create(int64_t num_ids, int32_t world, int64_t S_rows, int32_t device, fc_router** out) {
   *out = nullptr;
   int prev = 0;
   cudaGetDevice(&prev);
@@ -920,7 +949,7 @@ extern "C" int fc_router_create(int64_t num_ids, int32_t world, int32_t device, 
   std::memset(r, 0, sizeof(*r));
   r->num_ids = num_ids;
   r->world = world;
-  r->S = ((num_ids + world - 1) / world + 31) / 32 * 32;
+  r->S = (S_rows + 31) / 32 * 32;
   if (r->S * world > INT32_MAX - 64) {
     delete r;
     cudaSetDevice(prev);
@@ -944,6 +973,53 @@ extern "C" int fc_router_create(int64_t num_ids, int32_t world, int32_t device, 
     return cuda_fail(e, "fc_router_create");
   }
   *out = r;
+  return FC_OK;
+}
+
+extern "C" int fc_router_create(int64_t num_ids, int32_t world, int32_t device, fc_router** out) {
+  if (!out || num_ids < 1 || world < 1 || world > 64) return FC_ERR_BAD_ARG;
+  return router_create(num_ids, world, (num_ids + world - 1) / world, device, out);
+}
+
+extern "C" int fc_router_create_tables(int64_t num_ids, int32_t world, int32_t num_tables, const int64_t* table_starts,
+                                       const int32_t* table_owner, int32_t device, fc_router** out) {
+  if (!out || num_ids < 1 || world < 1 || world > 64 || num_tables < 1 || !table_starts || !table_owner)
+    return FC_ERR_BAD_ARG;
+  *out = nullptr;
+  if (table_starts[0] != 0 || table_starts[num_tables] != num_ids) {
+    set_error("table starts must run from 0 to num_ids");
+    return FC_ERR_BAD_ARG;
+  }
+  std::vector<long long> lbase(num_tables), load(world, 0);
+  for (int t = 0; t < num_tables; ++t) {
+    if (table_starts[t + 1] <= table_starts[t] || table_owner[t] < 0 || table_owner[t] >= world) {
+      set_error("table %d: empty, unordered or owned by a rank outside [0, %d)", t, world);
+      return FC_ERR_BAD_ARG;
+    }
+    lbase[t] = load[table_owner[t]];  // an owner's tables in table order
+    load[table_owner[t]] += table_starts[t + 1] - table_starts[t];
+  }
+  const long long S = *std::max_element(load.begin(), load.end());
+  int rc = router_create(num_ids, world, S, device, out);
+  if (rc) return rc;
+  fc_router* r = *out;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  cudaSetDevice(device);
+  r->ntables = num_tables;
+  cudaError_t e = cudaMalloc(&r->t_starts, (num_tables + 1) * sizeof(long long));
+  if (e == cudaSuccess) e = cudaMalloc(&r->t_owner, num_tables * sizeof(int));
+  if (e == cudaSuccess) e = cudaMalloc(&r->t_lbase, num_tables * sizeof(long long));
+  if (e == cudaSuccess)
+    e = cudaMemcpy(r->t_starts, table_starts, (num_tables + 1) * sizeof(long long), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(r->t_owner, table_owner, num_tables * sizeof(int), cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(r->t_lbase, lbase.data(), num_tables * sizeof(long long), cudaMemcpyHostToDevice);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) {
+    router_release(r);
+    *out = nullptr;
+    return cuda_fail(e, "fc_router_create_tables");
+  }
   return FC_OK;
 }
 
@@ -979,12 +1055,18 @@ extern "C" int fc_route(fc_router* r, const void* ids, int32_t ids_bytes, int64_
   Counters* c = r->ctr;
   k_begin<<<1, 1, 0, st>>>(c, c);
   const int g = grid_for(n, kNT, kSMs * 8);
-  if (ids_bytes == 8) k_route_mark<long long><<<g, kNT, 0, st>>>((const long long*)ids, n, r->num_ids, r->world, r->S, r->bits, c);
-  else k_route_mark<int><<<g, kNT, 0, st>>>((const int*)ids, n, r->num_ids, r->world, r->S, r->bits, c);
-  compact(ArrWords{r->bits}, RouteFin{}, RouteEmit{r->ukeys, local_ids, r->aux, r->S, 0}, r->nw, r->block_cnt, nullptr,
-          c, G_ALWAYS, st);
-  if (ids_bytes == 8) k_route_inverse<long long><<<g, kNT, 0, st>>>((const long long*)ids, n, r->world, r->S, r->aux, inverse, c);
-  else k_route_inverse<int><<<g, kNT, 0, st>>>((const int*)ids, n, r->world, r->S, r->aux, inverse, c);
+  auto run = [&](auto map) {
+    if (ids_bytes == 8)
+      k_route_mark<long long><<<g, kNT, 0, st>>>((const long long*)ids, n, r->num_ids, map, r->bits, c);
+    else k_route_mark<int><<<g, kNT, 0, st>>>((const int*)ids, n, r->num_ids, map, r->bits, c);
+    compact(ArrWords{r->bits}, RouteFin{}, RouteEmit{r->ukeys, local_ids, r->aux, r->S, 0}, r->nw, r->block_cnt,
+            nullptr, c, G_ALWAYS, st);
+    if (ids_bytes == 8)
+      k_route_inverse<long long><<<g, kNT, 0, st>>>((const long long*)ids, n, map, r->aux, inverse, c);
+    else k_route_inverse<int><<<g, kNT, 0, st>>>((const int*)ids, n, map, r->aux, inverse, c);
+  };
+  if (r->ntables > 0) run(TableMap{r->t_starts, r->t_owner, r->t_lbase, r->ntables, r->S});
+  else run(RowMap{(uint32_t)r->world, (uint32_t)r->S});
   k_route_finish<<<grid_for(n, kNT, kSMs * 4), kNT, 0, st>>>(r->ukeys, r->aux, r->S, r->world, c, r->owner_cnt);
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) e = cudaMemcpyAsync(r->ctr_host, c, sizeof(Counters), cudaMemcpyDeviceToHost, st);

@@ -80,13 +80,62 @@ class CudaShard:
         return self.cache.flush()
 
 
+class TablePlacement:
+    """Table-wise sharding (the other split `north_star` names besides column-wise): table t
+    is the global id range [starts[t], starts[t+1]) and belongs whole to rank owner[t]; an
+    owner's local rows are its tables in table order (fc_router_create_tables)."""
+
+    def __init__(self, starts, owner, world: int):
+        self.starts = np.asarray(starts, dtype=np.int64)
+        self.owner = np.asarray(owner, dtype=np.int32)
+        self.world = int(world)
+        sizes = np.diff(self.starts)
+        if self.starts[0] != 0 or (sizes <= 0).any() or self.owner.size != sizes.size:
+            raise ValueError("table starts must be strictly increasing from 0, one owner per table")
+        if (self.owner < 0).any() or (self.owner >= self.world).any():
+            raise ValueError(f"table owners must be ranks in [0, {self.world})")
+        self.lbase = np.zeros(sizes.size, dtype=np.int64)
+        load = np.zeros(self.world, dtype=np.int64)
+        for t, (o, sz) in enumerate(zip(self.owner, sizes)):
+            self.lbase[t] = load[o]
+            load[o] += sz
+        self.local_sizes = load
+        self.num_ids = int(self.starts[-1])
+
+    @classmethod
+    def balanced(cls, table_sizes, world: int) -> "TablePlacement":
+        """The reference's placement, plan_tables_greedy (sharding.py:158-172)."""
+        from .sharding import plan_tables_greedy
+
+        return cls.from_plan(plan_tables_greedy(table_sizes, world))
+
+    @classmethod
+    def from_plan(cls, plan) -> "TablePlacement":
+        """Tables laid out contiguously in table order; owners from a TableShardPlan."""
+        starts = np.concatenate([[0], np.cumsum(plan.table_sizes)])
+        return cls(starts, plan.assignment, plan.num_shards)
+
+    def owner_local(self, ids):
+        """(owner, owner-local id) of global ids (a torch tensor), as the router computes them."""
+        starts = torch.as_tensor(self.starts, device=ids.device)
+        t = torch.searchsorted(starts, ids.long(), right=True) - 1
+        owner = torch.as_tensor(self.owner, device=ids.device).long()[t]
+        local = torch.as_tensor(self.lbase, device=ids.device)[t] + (ids.long() - starts[t])
+        return owner, local
+
+    def global_ids(self, rank: int) -> np.ndarray:
+        """Global ids of rank's local rows, in local order."""
+        parts = [np.arange(self.starts[t], self.starts[t + 1]) for t in range(self.owner.size) if self.owner[t] == rank]
+        return np.concatenate(parts) if parts else np.zeros(0, dtype=np.int64)
+
+
 class Router:
     """libfreqcache_b200's row-sharded exchange planner (fc_route / fc_pool_rows /
     fc_route_grads): dedup + group-by-owner of a requester's ids with the same bitmap
     machinery as prepare, the pooled forward over the rows the owners send back, and
     its backward reduced to one deterministic gradient row per routed id."""
 
-    def __init__(self, num_ids: int, world: int, device):
+    def __init__(self, num_ids: int, world: int, device, placement=None):
         import ctypes
 
         from . import _lib
@@ -97,7 +146,15 @@ class Router:
         self.device = torch.device(device)
         self.world = int(world)
         h = ctypes.c_void_p()
-        check(self.lib.fc_router_create(int(num_ids), self.world, self.device.index or 0, ctypes.byref(h)))
+        if placement is None:  # row-wise: owner id % world
+            check(self.lib.fc_router_create(int(num_ids), self.world, self.device.index or 0, ctypes.byref(h)))
+        else:  # table-wise: whole tables per owner (TablePlacement)
+            starts = np.ascontiguousarray(placement.starts, dtype=np.int64)
+            owner = np.ascontiguousarray(placement.owner, dtype=np.int32)
+            check(self.lib.fc_router_create_tables(int(num_ids), self.world, int(owner.size),
+                                                   ctypes.c_void_p(starts.ctypes.data),
+                                                   ctypes.c_void_p(owner.ctypes.data), self.device.index or 0,
+                                                   ctypes.byref(h)))
         self.h = h
 
     def close(self):
@@ -344,9 +401,10 @@ class RowShardedEmbedding(torch.nn.Module):
     cache's prefetch pipeline; the next forward with the same ids commits it."""
 
     def __init__(self, shard, world: int, rank: int, mode: str = "sum", include_last_offset: bool = False,
-                 group=None, device=None, peer_rows: int = 0):
+                 group=None, device=None, peer_rows: int = 0, placement: TablePlacement | None = None):
         super().__init__()
         self.shard, self.world, self.rank = shard, world, rank
+        self.placement = placement  # None: row-wise (owner id % world); else table-wise
         self.mode, self.include_last_offset, self.group = mode, include_last_offset, group
         self.device = device if device is not None else getattr(shard, "device", torch.device("cpu"))
         self._anchor = torch.nn.Parameter(torch.empty(0, device=self.device))
@@ -362,7 +420,7 @@ class RowShardedEmbedding(torch.nn.Module):
             if num_ids is None:
                 raise ValueError("RowShardedEmbedding on CUDA needs shard.global_num_ids (the whole table's id "
                                  "space) for the libfreqcache_b200 router")
-            self.router = Router(num_ids, world, self.device)
+            self.router = Router(num_ids, world, self.device, placement)
             if peer_rows:  # fused return exchange over NVLink peer memory (PeerRows)
                 self.peer = PeerRows(shard, world, rank, int(peer_rows), group, self.device)
 
@@ -398,7 +456,7 @@ class RowShardedEmbedding(torch.nn.Module):
             send_counts = _upload(sc, ids.device)
         else:
             uniq, inv = torch.unique(ids.long(), sorted=True, return_inverse=True)
-            owner, local = self.owner_of(uniq, W)
+            owner, local = self.owner_of(uniq, W) if self.placement is None else self.placement.owner_local(uniq)
             order = torch.argsort(owner, stable=True)
             send_ids = local[order]
             send_counts = torch.bincount(owner, minlength=W)
@@ -709,6 +767,26 @@ def shard_rows_for_rank(counts: np.ndarray, rank: int, world: int):
     rank_of = np.empty_like(id_of)
     rank_of[id_of] = np.arange(id_of.size, dtype=np.int64)
     return IdxMap(rank_of=rank_of, id_of=id_of)
+
+
+def shard_tables_for_rank(counts: np.ndarray, placement: TablePlacement, rank: int):
+    """Local id space of a table shard (rank's tables in table order) and its frequency reorder."""
+    local_counts = counts[placement.global_ids(rank)]
+    id_of = np.argsort(-local_counts, kind="stable").astype(np.int64)
+    rank_of = np.empty_like(id_of)
+    rank_of[id_of] = np.arange(id_of.size, dtype=np.int64)
+    return IdxMap(rank_of=rank_of, id_of=id_of)
+
+
+def build_table_sharded(dim, cache_ratio, counts, placement: TablePlacement, rank, init_rows_fn, **kw):
+    """CudaShard for this rank's tables (table-wise split): its own frequency reorder over
+    its local rows; `init_rows_fn(global_ids) -> rows` seeds values."""
+    idx = shard_tables_for_rank(counts, placement, rank)
+    n_local = int(idx.id_of.size)
+    rows = pinned_empty((n_local, dim))
+    rows[...] = init_rows_fn(placement.global_ids(rank)[idx.id_of])
+    kw.setdefault("global_num_ids", placement.num_ids)
+    return CudaShard(n_local, dim, fast_capacity(n_local, cache_ratio), rows, idx, **kw)
 
 
 def build_row_sharded(num_ids, dim, cache_ratio, counts, rank, world, init_rows_fn, **kw):

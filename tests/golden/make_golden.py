@@ -407,7 +407,40 @@ def gen_csv():
         json.dump({"load_csv": out, "runs": runs, "trace_global_samples": tr.samples.tolist()}, fh, sort_keys=True)
 
 
+def gen_tablewise():
+    """Table-wise placement (plan_tables_greedy, sharding.py:158-172) and the load statistics
+    (tablewise_imbalance / columnwise_imbalance, :183-205) on the Criteo sizes, a scaled copy
+    and a tie-heavy random list, 1..8 shards."""
+    import json
+
+    from freqcache import sharding as sh
+
+    rng = np.random.default_rng(5)
+    lists = {"criteo": list(sh.CRITEO_KAGGLE_TABLE_SIZES), "criteo_div1000": sh.criteo_like_table_sizes(1000),
+             "ties": rng.integers(1, 6, 40).tolist()}
+    out = {}
+    for name, sizes in lists.items():
+        for w in range(1, 9):
+            plan = sh.plan_tables_greedy(sizes, w)
+            st = sh.tablewise_imbalance(plan)
+            out[f"{name}/{w}"] = {"sizes": [int(x) for x in sizes], "assignment": plan.assignment.tolist(),
+                                  "per_shard_rows": st.per_shard_rows.tolist(), "max_rows": st.max_rows,
+                                  "mean_rows": st.mean_rows, "imbalance_ratio": st.imbalance_ratio}
+    for dim in (128, 10):
+        for w in range(1, 9):
+            st = sh.columnwise_imbalance(sh.partition_columns(dim, w), 33_762_577)
+            out[f"column/{dim}/{w}"] = {"per_shard_rows": st.per_shard_rows.tolist(), "max_rows": st.max_rows,
+                                        "mean_rows": st.mean_rows, "imbalance_ratio": st.imbalance_ratio}
+    with open(os.path.join(OUT, "tablewise.json"), "w") as fh:
+        json.dump(out, fh, sort_keys=True)
+
+
 def main():
+    only = sys.argv[1:]  # e.g. `make_golden.py gen_tablewise`: regenerate just those
+    if only:
+        for name in only:
+            globals()[name]()
+        return
     gen_random_stream("stream_dirty_zipf", "dirty_only")
     gen_random_stream("stream_always_zipf", "always", seed=21, init_seed=3)
     gen_random_stream("stream_dirty_ident", "dirty_only", num_ids=48, cap=6, dim=10, nb=80, seed=6,
@@ -426,6 +459,7 @@ def main():
     gen_sim_metrics()
     gen_buffer_too_small()
     gen_csv()
+    gen_tablewise()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

@@ -13,10 +13,12 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import oracle
-from paper_2208_05321_b200.distributed import ColumnShardedEmbedding, RowShardedEmbedding, shard_rows_for_rank
+from paper_2208_05321_b200.distributed import (ColumnShardedEmbedding, RowShardedEmbedding, TablePlacement,
+                                               shard_rows_for_rank)
 from paper_2208_05321_b200.sharding import partition_columns
 
 NUM, DIM, BAGS, STEPS, LR = 400, 10, 24, 5, 0.1
+TABLES = [100, 50, 150, 60, 40]  # table-wise split: five tables over the 400 ids
 
 
 class OracleShard:
@@ -97,6 +99,12 @@ def _worker(rank, world, port, kind, mode, q, prefetch=False):
             local_rows = table[rank::world][idx.id_of].copy()
             shard = OracleShard(idx.rank_of, local_rows, max(1, idx.num_ids // 2), LR)
             mod = RowShardedEmbedding(shard, world, rank, mode=mode)
+        elif kind == "table":
+            pl = TablePlacement.balanced(TABLES, world)
+            gids = pl.global_ids(rank)
+            rank_of, id_of = oracle.rank_permutation(counts[gids])
+            shard = OracleShard(rank_of, table[gids][id_of].copy(), max(1, gids.size // 2), LR)
+            mod = RowShardedEmbedding(shard, world, rank, mode=mode, placement=pl)
         else:
             rank_of, id_of = oracle.rank_permutation(counts)
             a, b = partition_columns(DIM, world).ranges[rank]
@@ -131,6 +139,8 @@ def _worker(rank, world, port, kind, mode, q, prefetch=False):
         got = shard.table()
         if kind == "row":
             want_rows = dense[rank::world][idx.id_of]
+        elif kind == "table":
+            want_rows = dense[gids][id_of]
         else:
             want_rows = np.ascontiguousarray(dense[:, a:b])[id_of]
         np.testing.assert_allclose(got, want_rows, rtol=1e-5, atol=1e-6)
@@ -143,7 +153,8 @@ def _worker(rank, world, port, kind, mode, q, prefetch=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,prefetch", [("row", False), ("row", True), ("row", "bypass"), ("column", False),
+@pytest.mark.parametrize("kind,prefetch", [("row", False), ("row", True), ("row", "bypass"), ("table", False),
+                                            ("table", True), ("column", False),
                                             ("column", True), ("column", "bypass")])
 @pytest.mark.parametrize("mode", ["sum", "mean"])
 def test_two_rank_gloo_matches_dense(kind, mode, prefetch):

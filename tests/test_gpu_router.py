@@ -142,3 +142,102 @@ def test_row_sharded_on_cuda_requires_the_router():
 
     with pytest.raises(ValueError, match="global_num_ids"):
         RowShardedEmbedding(NoSpace(), 1, 0, device=torch.device("cuda"))
+
+
+@pytest.mark.parametrize("world,ntables", [(1, 3), (4, 26), (8, 26)])
+def test_route_tables_matches_numpy(world, ntables):
+    """Table-wise routing (fc_router_create_tables): whole tables per owner, owner-local ids
+    = the owner's tables in table order; output grouped by owner then owner-local id."""
+    from paper_2208_05321_b200.distributed import TablePlacement
+
+    rng = np.random.default_rng(world * 31 + ntables)
+    sizes = rng.integers(1_000, 60_000, ntables)
+    pl = TablePlacement.balanced(sizes, world)
+    num_ids, n = pl.num_ids, 150_000
+    p = 1.0 / np.arange(1, num_ids + 1) ** 1.05
+    ids = rng.permutation(num_ids)[rng.choice(num_ids, size=n, p=p / p.sum())]
+    r = Router(num_ids, world, "cuda", placement=pl)
+    local, inv, counts = r.route(torch.from_numpy(ids).cuda())
+    uniq = np.unique(ids)
+    t = np.searchsorted(pl.starts, uniq, side="right") - 1
+    own, loc = pl.owner[t], pl.lbase[t] + (uniq - pl.starts[t])
+    order = np.lexsort((loc, own))
+    assert counts == np.bincount(own, minlength=world).tolist()
+    assert np.array_equal(local.cpu().numpy(), loc[order])
+    o2, l2 = pl.owner_local(torch.from_numpy(uniq))  # the torch mirror agrees with the kernels
+    assert np.array_equal(o2.numpy(), own) and np.array_equal(l2.numpy(), loc)
+    pos = np.empty(num_ids, np.int64)
+    pos[uniq[order]] = np.arange(uniq.size)
+    assert np.array_equal(inv.cpu().numpy(), pos[ids])
+    # every owner-local id lies inside that owner's rows
+    for w in range(world):
+        mine = loc[own == w]
+        assert mine.size == 0 or mine.max() < pl.local_sizes[w]
+    with pytest.raises(ValueError, match="out of range"):
+        r.route(torch.tensor([0, num_ids], device="cuda"))
+
+
+def test_route_tables_rejects_bad_placements():
+    import ctypes
+
+    from paper_2208_05321_b200 import _lib
+    from paper_2208_05321_b200.errors import check
+
+    lib = _lib.load()
+    h = ctypes.c_void_p()
+
+    def create(starts, owner, world=2, num_ids=None):
+        s = np.asarray(starts, np.int64)
+        o = np.asarray(owner, np.int32)
+        return lib.fc_router_create_tables(int(s[-1] if num_ids is None else num_ids), world, int(o.size),
+                                           ctypes.c_void_p(s.ctypes.data), ctypes.c_void_p(o.ctypes.data), 0,
+                                           ctypes.byref(h))
+
+    for starts, owner, kw in [([0, 10, 10, 20], [0, 1, 0], {}),    # empty table
+                              ([1, 10, 20], [0, 1], {}),           # not starting at 0
+                              ([0, 10, 20], [0, 2], {}),           # owner out of range
+                              ([0, 10, 20], [0, 1], {"num_ids": 30})]:  # does not cover the ids
+        with pytest.raises(ValueError):
+            check(create(starts, owner, **kw))
+    check(create([0, 10, 20], [1, 0]))
+    lib.fc_router_destroy(h)
+
+
+def test_table_sharded_module_nccl_world1_matches_dense():
+    """build_table_sharded + RowShardedEmbedding(placement=...) through NCCL at world 1,
+    training against a dense EmbeddingBag + SGD."""
+    import torch.distributed as dist
+
+    from paper_2208_05321_b200.distributed import TablePlacement, build_table_sharded
+
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1)
+    sizes, dim, steps, B = [9_000, 4_000, 12_000, 5_000], 16, 5, 3_000
+    pl = TablePlacement.balanced(sizes, 1)
+    num_ids = pl.num_ids
+    rng = np.random.default_rng(8)
+    p = 1.0 / np.arange(1, num_ids + 1) ** 1.1
+    trace = rng.permutation(num_ids)[rng.choice(num_ids, size=(steps, B), p=p / p.sum())]
+    table = rng.uniform(-0.1, 0.1, (num_ids, dim)).astype(np.float32)
+    counts = np.bincount(trace.reshape(-1), minlength=num_ids)
+    shard = build_table_sharded(dim, 0.05, counts, pl, 0, lambda g: table[g], lr=0.1, device="cuda")
+    mod = RowShardedEmbedding(shard, 1, 0, mode="sum", device=torch.device("cuda"), placement=pl)
+    dense = torch.nn.EmbeddingBag(num_ids, dim, mode="sum", sparse=True)
+    dense.weight.data = torch.from_numpy(table.copy())
+    opt = torch.optim.SGD(dense.parameters(), lr=0.1)
+    for s in range(steps):
+        ids = torch.from_numpy(trace[s]).cuda()
+        out = mod(ids)
+        want = dense(torch.from_numpy(trace[s]), torch.arange(B))
+        np.testing.assert_allclose(out.detach().cpu().numpy(), want.detach().numpy(), rtol=1e-5, atol=5e-6)
+        g = np.random.default_rng(s).standard_normal((B, dim)).astype(np.float32)
+        out.backward(torch.from_numpy(g).cuda())
+        opt.zero_grad()
+        want.backward(torch.from_numpy(g))
+        opt.step()
+    mod.flush()
+    torch.cuda.synchronize()
+    got = np.empty_like(table)
+    got[pl.global_ids(0)[shard.idx_map.id_of]] = shard.rows
+    np.testing.assert_allclose(got, dense.weight.detach().numpy(), rtol=1e-5, atol=5e-6)
+    dist.destroy_process_group()
