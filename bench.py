@@ -419,8 +419,9 @@ def workload_config(args, cfg, world):
     """The workload both arms measure (identical dicts: the driver compares them)."""
     D, B, F = cfg["dim"], cfg["batch"], cfg["features"]
     shard = args.shard
-    return {"workload": args.config, "num_rows": cfg["num_ids"], "dim": D, "cache_ratio": cfg["ratio"],
-            "zipf_alpha": cfg["alpha"], "batch_per_gpu": B, "features": F, "lookups_per_step": B * F * world,
+    return {"workload": args.config if args.batch is None else f"{args.config}@batch{args.batch}", "num_rows": cfg["num_ids"], "dim": D, "cache_ratio": cfg["ratio"],
+            "zipf_alpha": cfg["alpha"], "batch_per_gpu": B, "global_batch": B * world, "features": F,
+            "lookups_per_step": B * F * world, "batch_scaling": args.batch_scaling if world > 1 else None,
             "pooling": cfg.get("mode", "sum") + (" with per-sample weights" if cfg.get("psw") else "") + ", bag size 1",
             "optimizer": cfg.get("optimizer", "sgd"), "ids": "uniform" if cfg["alpha"] is None else f"zipf({cfg['alpha']})",
             "step": ("forward (prepare + pooled gather) + backward/update" if args.step == "train"
@@ -431,6 +432,13 @@ def workload_config(args, cfg, world):
                   % (fc_capacity(cfg) * D * 4 >> 20, cfg["num_ids"] * 12 >> 20)}
 
 
+def scaling_kind(args, world):
+    """strong: the config's batch is the global batch, split over the N data-parallel ranks
+    (the reference's multi-GPU model, SURVEY 8e: every shard serves the one global batch);
+    weak: every rank takes the config's batch (global batch x N)."""
+    return "weak" if world == 1 else args.batch_scaling
+
+
 def fc_capacity(cfg):
     return max(1, int(cfg["ratio"] * cfg["num_ids"]))
 
@@ -438,7 +446,8 @@ def fc_capacity(cfg):
 def trace_batches(args, world):
     """Batches of B samples per rank in the generated trace (the frequency reorder scans all
     of them; both arms generate the same trace for the same --steps/--warmup/--gpus)."""
-    return max(args.trace_batches // world, args.warmup + 2 * args.steps + 2 * KSTEPS + 2)
+    per_rank = args.trace_batches // world if args.batch_scaling == "weak" else args.trace_batches
+    return max(per_rank, args.warmup + 2 * args.steps + 2 * KSTEPS + 2)
 
 
 def launches_per_step(args, shard_mode, pipelined, world):
@@ -743,7 +752,7 @@ def run_ours(args, cfg, torch, rank, world):
     lookups = N * world  # every rank processes its own B x F ids per step
     res = {
         "metric": METRIC, "value": lookups * K / (total_ms * 1e-3), "unit": "lookups/s", "n_gpus": world,
-        "steps": K, "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": "weak",
+        "steps": K, "warmup": W, "ms_per_step": total_ms / K, "higher_is_better": True, "scaling": scaling_kind(args, world),
         "vs_baseline": None, "dtype": "fp32 rows, int32 ids",
         "data": "synthetic: reference gen_zipf stream (seed 1), seeded rows",
         "config": workload_config(args, cfg, world),
@@ -991,6 +1000,12 @@ def main():
                          "column (the reference's column-wise split, sharding.py:46-118) or table (one table per "
                          "sparse feature, whole tables per rank)")
     ap.add_argument("--trace-batches", type=int, default=64)
+    ap.add_argument("--batch", type=int, default=None,
+                    help="override the config's (global) batch in samples, e.g. to time one rank's share")
+    ap.add_argument("--batch-scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1: strong = the config's batch is the global batch, B/N samples per rank (default; "
+                         "the reference's sharding serves one global batch); weak = B samples per rank. At 1.5%% "
+                         "cache weak is infeasible at N=8 on criteo_kaggle (2.4%% of the rows per global batch)")
     ap.add_argument("--cpu-baseline-s", type=float, default=20.0, help="time budget of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--prefetch-depth", type=int, default=2, choices=[1, 2],
@@ -1011,10 +1026,16 @@ def main():
         args.shard = "row"
     if args.gpus > 1 and args.shard is None:
         args.shard = "row"
-    cfg = CONFIGS[args.config]
+    cfg = dict(CONFIGS[args.config])
+    if args.batch is not None:
+        cfg["batch"] = args.batch
     rank = int(os.environ.get("RANK", 0))
     env_world = os.environ.get("WORLD_SIZE")
     world = int(env_world) if env_world is not None else args.gpus
+    if args.batch_scaling == "strong" and world > 1:  # the config's batch is the global batch
+        if cfg["batch"] % world:
+            raise SystemExit(f"bench.py: batch {cfg['batch']} does not split over {world} ranks")
+        cfg["batch"] //= world
     if env_world is not None and args.gpus != 1 and int(env_world) != args.gpus:
         raise SystemExit(f"bench.py --gpus {args.gpus} launched with WORLD_SIZE={env_world}")
 
@@ -1026,7 +1047,7 @@ def main():
         n = cfg["batch"] * cfg["features"] * world
         val = n / step_s
         emit({"metric": METRIC, "value": val, "unit": "lookups/s", "n_gpus": world, "steps": nsteps,
-              "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+              "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": scaling_kind(args, world),
               "vs_baseline": None, "dtype": "fp32 rows, int64 ids", "data": "synthetic: reference gen_zipf stream (seed 1)",
               "impl": "reference", "config": workload_config(args, cfg, world),
               "cpu_baseline": {"value": val, "unit": "lookups/s", "cores": 1, "kind": kind, "sample": note,
