@@ -419,7 +419,7 @@ def workload_config(args, cfg, world):
     """The workload both arms measure (identical dicts: the driver compares them)."""
     D, B, F = cfg["dim"], cfg["batch"], cfg["features"]
     shard = args.shard
-    return {"workload": args.config if args.batch is None else f"{args.config}@batch{args.batch}", "num_rows": cfg["num_ids"], "dim": D, "cache_ratio": cfg["ratio"],
+    return {"workload": args.config + (f"@batch{args.batch}" if args.batch else "") + (f"@dim{args.dim}" if args.dim else ""), "num_rows": cfg["num_ids"], "dim": D, "cache_ratio": cfg["ratio"],
             "zipf_alpha": cfg["alpha"], "batch_per_gpu": B, "global_batch": B * world, "features": F,
             "lookups_per_step": B * F * world, "batch_scaling": args.batch_scaling if world > 1 else None,
             "pooling": cfg.get("mode", "sum") + (" with per-sample weights" if cfg.get("psw") else "") + ", bag size 1",
@@ -566,8 +566,10 @@ def run_ours(args, cfg, torch, rank, world):
     def step(s, timed):
         ids = bview[s]
         if sharded:  # sharded training step: id exchange, this rank's cache, row/activation exchange
+            if pipelined and depth2:  # next batch's exchange + prepare begun before this batch is committed
+                mod.prefetch(bview[s + 1], ready=ids_ready)
             out = mod(ids, None, psw)
-            if pipelined:  # next batch's id exchange + owner prepare overlap this backward
+            if pipelined and not depth2:  # next batch's id exchange + owner prepare overlap this backward
                 mod.prefetch(bview[s + 1], ready=ids_ready)
             out.backward(gout)
             li = getattr(mod, "last_info", None)
@@ -600,8 +602,13 @@ def run_ours(args, cfg, torch, rank, world):
     # sharded modules prefetch through their own prefetch() (column-wise: all-gather of the next
     # batch's ids + prepare_begin of the global batch; row-wise: id exchange + the owner's prepare_begin)
     pipelined = args.engine == "async" and not args.no_prefetch
-    depth2 = args.prefetch_depth == 2 and not sharded and not os.environ.get("FC_XFER_AFTER_UPDATE")
-    if pipelined and not sharded:
+    # sharded modules default to depth 1: two batches in flight measured slower there (row-wise
+    # 1.48 vs 1.27-1.31 ms at cfg2, equal at the N=8 per-rank batch; profiles/r02_sharded_depth_ab.txt)
+    depth = args.prefetch_depth if args.prefetch_depth is not None else (1 if sharded else 2)
+    depth2 = depth == 2 and not os.environ.get("FC_XFER_AFTER_UPDATE")
+    if pipelined and sharded and depth2:
+        mod.prefetch(bview[0], ready=ids_ready)
+    elif pipelined and not sharded:
         dc.prepare_begin(bview[0], 0, ready=ids_ready)
     for s in range(W):
         step(s, False)
@@ -669,6 +676,8 @@ def run_ours(args, cfg, torch, rank, world):
     # ---- e2e: the public API (module forward+backward) from pinned host ids ----
     if pipelined and not sharded and dc.prefetch_outstanding:
         dc.prepare_commit()
+    if pipelined and sharded:
+        mod.flush()  # commits the timed loop's outstanding prefetches before the e2e loop primes its own
     ids_host = torch.from_numpy(samples).pin_memory()
     hb = [ids_host[local_batch(k)[0]:local_batch(k)[1]].reshape(-1) for k in range(n_batches)]
     # warm-up exactly like the timed loop (the first autograd backward starts torch's device
@@ -996,20 +1005,23 @@ def main():
     ap.add_argument("--config", default="criteo_kaggle", choices=list(CONFIGS))
     ap.add_argument("--step", default="train", choices=["train", "sim"])
     ap.add_argument("--shard", default=None, choices=["row", "column", "table"],
-                    help="table split over the ranks: row (id %% N owners, the scaling variant; default at N>1), "
-                         "column (the reference's column-wise split, sharding.py:46-118) or table (one table per "
-                         "sparse feature, whole tables per rank)")
+                    help="table split over the ranks: column (the reference's column-wise split, "
+                         "sharding.py:46-118; default at N>1), row (id %% N owners, index work sharded too) or table "
+                         "(whole tables per rank, the reference's greedy placement)")
     ap.add_argument("--trace-batches", type=int, default=64)
     ap.add_argument("--batch", type=int, default=None,
                     help="override the config's (global) batch in samples, e.g. to time one rank's share")
+    ap.add_argument("--dim", type=int, default=None,
+                    help="override the config's row width, e.g. to time one column shard's share at world 1")
     ap.add_argument("--batch-scaling", default="strong", choices=["strong", "weak"],
                     help="N>1: strong = the config's batch is the global batch, B/N samples per rank (default; "
                          "the reference's sharding serves one global batch); weak = B samples per rank. At 1.5%% "
                          "cache weak is infeasible at N=8 on criteo_kaggle (2.4%% of the rows per global batch)")
     ap.add_argument("--cpu-baseline-s", type=float, default=20.0, help="time budget of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--prefetch-depth", type=int, default=2, choices=[1, 2],
-                    help="2: batch t+1's prefetch is begun before batch t is committed (default)")
+    ap.add_argument("--prefetch-depth", type=int, default=None, choices=[1, 2],
+                    help="2: batch t+1's prefetch is begun before batch t is committed (default unsharded); "
+                         "1: after forward(t) (default for the sharded modules)")
     ap.add_argument("--sharded", action="store_true", help="alias of --shard row (also at one GPU)")
     ap.add_argument("--peer", action="store_true",
                     help="row-sharded runs: owners write the rows straight into the requesters' buffers over "
@@ -1025,10 +1037,15 @@ def main():
     if args.sharded and args.shard is None:
         args.shard = "row"
     if args.gpus > 1 and args.shard is None:
-        args.shard = "row"
+        # the reference's multi-GPU model: column shards serving one global batch (strong scaling).
+        # At the N=2/4/8 per-rank shares it is also the faster split on one GPU: 0.71 / 0.54 / 0.66 ms
+        # per step against row-wise 1.12 / 0.72 / 0.79 ms (profiles/r02_strong_scaling_shares.txt)
+        args.shard = "column"
     cfg = dict(CONFIGS[args.config])
     if args.batch is not None:
         cfg["batch"] = args.batch
+    if args.dim is not None:
+        cfg["dim"] = args.dim
     rank = int(os.environ.get("RANK", 0))
     env_world = os.environ.get("WORLD_SIZE")
     world = int(env_world) if env_world is not None else args.gpus

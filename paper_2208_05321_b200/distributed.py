@@ -409,7 +409,7 @@ class RowShardedEmbedding(torch.nn.Module):
         self.device = device if device is not None else getattr(shard, "device", torch.device("cpu"))
         self._anchor = torch.nn.Parameter(torch.empty(0, device=self.device))
         self.last_recv = 0
-        self._pf = None  # (ids, exchange) of a prefetched batch
+        self._pfq = []  # exchanges of prefetched batches, oldest first (at most two)
         # on a GPU the exchange planning, expansion and gradient reduction run in
         # libfreqcache_b200 (Router) -- there is no torch fallback there; the torch restatement
         # of the same steps below serves CPU process groups only (the gloo tests' oracle shards)
@@ -474,14 +474,16 @@ class RowShardedEmbedding(torch.nn.Module):
         kernels only, not for this batch's queued forward/backward. Host `ids` are
         copied there; device `ids` are read after the work queued on the current stream,
         or after `ready` (a torch.cuda.Event) when given."""
+        if len(self._pfq) >= 2:
+            raise RuntimeError("two prefetched batches are outstanding: run a forward first")
         if self.device.type != "cuda":
             dev_ids = ids.reshape(-1).to(self.device)
             x = self._exchange_ids(dev_ids)
             if hasattr(self.shard, "prepare_begin") and x["recv_ids"].numel() > 0:
                 self.shard.prepare_begin(x["recv_ids"])
                 x["begun"] = True
-            x["src"] = ids
-            self._pf = (dev_ids, x)
+            x["src"], x["ids"] = ids, dev_ids
+            self._pfq.append(x)
             return
         main = torch.cuda.current_stream(self.device)
         if getattr(self, "_xstream", None) is None:
@@ -505,21 +507,20 @@ class RowShardedEmbedding(torch.nn.Module):
             if isinstance(x.get(k), torch.Tensor):
                 x[k].record_stream(main)
         dev_ids.record_stream(main)
-        x["ev"], x["src"] = ev, ids
-        self._pf = (dev_ids, x)
+        x["ev"], x["src"], x["ids"] = ev, ids, dev_ids
+        self._pfq.append(x)
 
     def _forward(self, ids, offsets, n_bags, psw, src=None):
         x, h = None, None
-        if self._pf is not None:
-            pids, px = self._pf
-            self._pf = None
+        while self._pfq:  # prefetched batches are executed oldest first (FIFO) up to this one
+            px = self._pfq.pop(0)
+            pids = px["ids"]
             if px.get("ev") is not None:  # the side stream's exchange is ordered before anything below
                 torch.cuda.current_stream(self.device).wait_event(px["ev"])
-            if px.get("begun"):
-                hp = self.shard.prepare_commit()  # the prefetched batch is executed first
+            hp = self.shard.prepare_commit() if px.get("begun") else None
             if px["src"] is src or pids is ids or (pids.numel() == ids.numel() and bool(torch.equal(pids, ids))):
-                x = px
-                h = hp if px.get("begun") else None
+                x, h = px, hp
+                break
         if x is None:
             x = self._exchange_ids(ids)
         if h is None:
@@ -567,19 +568,21 @@ class RowShardedEmbedding(torch.nn.Module):
 
     def forward(self, ids, offsets=None, per_sample_weights=None):
         self._src = ids
-        if self._pf is not None and self._pf[1].get("src") is ids:
-            ids = self._pf[0]  # already on the device (prefetch copied it)
+        pf = next((p for p in self._pfq if p["src"] is ids), None)
+        if pf is not None:
+            ids = pf["ids"]  # already on the device (prefetch copied it)
         else:
             ids = ids.reshape(-1).to(self.device, non_blocking=True)
         n_bags = ids.numel() if offsets is None else offsets.numel() - (1 if self.include_last_offset else 0)
         return _RowShardFn.apply(self._anchor, self, ids, offsets, n_bags, per_sample_weights)
 
     def flush(self) -> int:
-        if self._pf is not None and self._pf[1].get("ev") is not None:
-            torch.cuda.current_stream(self.device).wait_event(self._pf[1]["ev"])
-        if self._pf is not None and self._pf[1].get("begun"):
-            self.shard.prepare_commit()
-        self._pf = None
+        while self._pfq:  # outstanding prefetches are committed first (their batches become resident)
+            px = self._pfq.pop(0)
+            if px.get("ev") is not None:
+                torch.cuda.current_stream(self.device).wait_event(px["ev"])
+            if px.get("begun"):
+                self.shard.prepare_commit()
         return self.shard.flush()
 
 

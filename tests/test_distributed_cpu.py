@@ -34,12 +34,12 @@ class OracleShard:
         p = self.c.prepare(ids.numpy())
         return {"p": p, "n": int(ids.numel()), "slots": self.c.occurrence_slots(p)}
 
-    # prefetch: the oracle executes the prepare at commit time (sequential semantics)
+    # prefetch: the oracle executes the prepare at commit time (sequential semantics), FIFO
     def prepare_begin(self, ids):
-        self._pending = ids
+        self._pending = getattr(self, "_pending", []) + [ids]
 
     def prepare_commit(self):
-        ids, self._pending = self._pending, None
+        ids = self._pending.pop(0)
         return self.prepare(ids)
 
     def pool(self, h, offsets=None, n_bags=None, include_last_offset=False, psw=None, mode="sum"):
@@ -113,20 +113,24 @@ def _worker(rank, world, port, kind, mode, q, prefetch=False):
         dense = table.copy()
         out = None
         tids = [torch.from_numpy(d[rank][0]) for d in data]
+        if prefetch == "depth2":
+            mod.prefetch(tids[0])
         for si, step in enumerate(data):
             for r in range(world):  # dense reference of every rank's batch
                 ids, off, gout = step[r]
                 if r == rank:
                     want = oracle.pooled_bag(dense, ids, off, None, mode)
             ids, off, gout = step[rank]
-            t_ids = tids[si] if prefetch is True else torch.from_numpy(ids)
+            t_ids = tids[si] if prefetch in (True, "depth2") else torch.from_numpy(ids)
+            if prefetch == "depth2" and si + 1 < len(data):
+                mod.prefetch(tids[si + 1])  # two batches in flight: batch si+1 begun before si is committed
             out = mod(t_ids, torch.from_numpy(off) if mode == "mean" else None)
             np.testing.assert_allclose(out.detach().numpy(), want, rtol=1e-5, atol=1e-6)
             if prefetch == "bypass" and si + 2 < len(data):
                 # a batch that the next forward does not ask for: that forward executes it
                 # first (FIFO), then prepares its own ids; outputs must not change
                 mod.prefetch(tids[si + 2])
-            elif prefetch and prefetch != "bypass" and si + 1 < len(data):
+            elif prefetch is True and si + 1 < len(data):
                 mod.prefetch(tids[si + 1])  # next batch's exchange + prepare start, before this backward
             out.backward(torch.from_numpy(gout))
             # dense SGD with every rank's batch (each rank owns its own bags' gradients)
@@ -153,8 +157,8 @@ def _worker(rank, world, port, kind, mode, q, prefetch=False):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("kind,prefetch", [("row", False), ("row", True), ("row", "bypass"), ("table", False),
-                                            ("table", True), ("column", False),
+@pytest.mark.parametrize("kind,prefetch", [("row", False), ("row", True), ("row", "bypass"), ("row", "depth2"),
+                                            ("table", False), ("table", True), ("column", "depth2"), ("column", False),
                                             ("column", True), ("column", "bypass")])
 @pytest.mark.parametrize("mode", ["sum", "mean"])
 def test_two_rank_gloo_matches_dense(kind, mode, prefetch):

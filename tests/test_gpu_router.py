@@ -48,10 +48,11 @@ def test_route_matches_numpy(world, num_ids, n):
     r.route(torch.from_numpy(ids[:10]).cuda())  # state is clean after an error
 
 
-@pytest.mark.parametrize("ids_on", ["cuda", "host", "cuda_ready"])
+@pytest.mark.parametrize("ids_on", ["cuda", "host", "cuda_ready", "cuda_depth2"])
 def test_row_sharded_module_nccl_world1_matches_dense(ids_on):
     """ids_on: device ids (the side-stream exchange waits for the current stream), pinned
-    host ids (copied on the side stream), device ids with a `ready` event."""
+    host ids (copied on the side stream), device ids with a `ready` event; cuda_depth2: two
+    batches in flight (batch s+1 prefetched before forward(s) commits s)."""
     import torch.distributed as dist
 
     if not dist.is_initialized():
@@ -74,19 +75,24 @@ def test_row_sharded_module_nccl_world1_matches_dense(ids_on):
     else:
         ids = [torch.from_numpy(trace[s]).cuda() for s in range(steps)]
     ready = None
-    if ids_on == "cuda_ready":
+    if ids_on in ("cuda_ready", "cuda_depth2"):
         ready = torch.cuda.Event()
         ready.record()
+    depth2 = ids_on == "cuda_depth2"
+    if depth2:
+        mod.prefetch(ids[0], ready=ready)
     dense = torch.nn.EmbeddingBag(num_ids, dim, mode="sum", sparse=True)
     dense.weight.data = torch.from_numpy(table.copy())
     opt = torch.optim.SGD(dense.parameters(), lr=0.1)
     for s in range(steps):
+        if depth2 and s + 1 < steps:
+            mod.prefetch(ids[s + 1], ready=ready)
         out = mod(ids[s])
         want = dense(torch.from_numpy(trace[s]), torch.arange(B))
         # fp32 sums of hot rows' gradients in a different order than torch's: 1e-5 of the
         # values' scale (|w| <~ 0.5) as the absolute floor
         np.testing.assert_allclose(out.detach().cpu().numpy(), want.detach().numpy(), rtol=1e-5, atol=5e-6)
-        if s + 1 < steps:
+        if s + 1 < steps and not depth2:
             mod.prefetch(ids[s + 1], ready=ready)
         out.backward(torch.from_numpy(grads[s]).cuda())
         opt.zero_grad()
