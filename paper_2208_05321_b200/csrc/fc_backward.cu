@@ -487,11 +487,13 @@ static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* i
   const bool bags = offsets != nullptr;
   const size_t extra = (gu_out || apply ? 0 : align16((size_t)u * D * 4)) + align16(nchunks * 2 * (size_t)D * 4) +
                        2 * align16(nchunks * 2 * 4) + (bags ? 2 * align16(n * 4) : 0);
-  // sort state left zero by the previous fused backward on this scratch (no memset); this
-  // one's fix-up clears it again
+  // sort state left zero by the previous fused backward (no memset); this one's fix-up clears
+  // it again. The state sits after the keys and order arrays, so its address moves with n:
+  // it counts as zero only where the previous fix-up cleared it (same address, no regrowth)
   const size_t state = sort_state_bytes(n, key_bits_for(u));
-  const bool zeroed = zero_for && *zero_for != nullptr && *zero_for == *scratch && *zero_bytes >= state &&
-                      grouping_bytes(n) + extra <= *scratch_bytes;
+  const bool fits = *scratch != nullptr && grouping_bytes(n) + extra <= *scratch_bytes;
+  const void* sort_at = fits ? static_cast<const void*>(static_cast<char*>(*scratch) + 2 * align16(n * 4)) : nullptr;
+  const bool zeroed = zero_for && *zero_for != nullptr && fits && *zero_for == sort_at && *zero_bytes >= state;
   Grouping g;
   int rc = build_grouping(scratch, scratch_bytes, inv, u, n, extra, g, st, zeroed, sort_hist);
   if (zero_for) {  // valid again only once the fix-up below is queued
@@ -552,7 +554,7 @@ static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* i
     k_bwd_fixup<true><<<fgrid, kNT, fix_smem, st>>>(x);
     if (zero_for) {
       FC_CUDA(cudaGetLastError());
-      *zero_for = *scratch;
+      *zero_for = g.sort_scr;  // the address the fix-up cleared
       *zero_bytes = state;
     }
   } else {

@@ -117,7 +117,8 @@ struct fc_cache {
   void* scratch;
   size_t scratch_bytes;
   // the fused backward's last kernel clears the sort state for the next sort: this many
-  // bytes at the head of `scratch` (valid while scratch == sort_zero_for) are zero
+  // bytes from sort_zero_for (inside `scratch`; the state's offset depends on the batch size)
+  // are zero
   void* sort_zero_for;
   size_t sort_zero_bytes;
 

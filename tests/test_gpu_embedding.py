@@ -121,16 +121,20 @@ def test_hot_row_long_segment():
     np.testing.assert_allclose(m.weight(), want, rtol=1e-5, atol=2e-6)
 
 
-def test_backward_sequence_of_batch_sizes_reuses_sort_state():
+@pytest.mark.parametrize("num,sizes", [(3_000, [500, 4_000, 120, 4_000, 9_000, 37, 9_000]),
+                                       (200, [4_000, 120, 4_000, 500, 9_000, 300, 2_000, 9_000])])
+def test_backward_sequence_of_batch_sizes_reuses_sort_state(num, sizes):
     """Back-to-back fused backwards of growing and shrinking batches (the fix-up clears the
     next sort's state instead of a memset, DESIGN 4b) with a scatter_update in between,
-    against dense SGD: every step within 1e-5."""
-    num, dim, lr = 3_000, 16, 0.05
+    against dense SGD: every step within 1e-5. The second case draws from 200 ids, so every
+    batch has duplicates (the radix-grouped path, never the all-distinct direct one) and the
+    sort state's address moves with n on a scratch that does not grow."""
+    dim, lr = 16, 0.05
     rng = np.random.default_rng(11)
     w = rng.uniform(-0.1, 0.1, (num, dim)).astype(np.float32)
     m = CachedEmbeddingBag(num, dim, cache_ratio=1.0, mode="sum", weight=w, lr=lr)
     dense = w.astype(np.float64)
-    for s, n in enumerate([500, 4_000, 120, 4_000, 9_000, 37, 9_000]):
+    for s, n in enumerate(sizes):
         ids = rng.integers(0, num, n)
         gout = rng.standard_normal((n, dim)).astype(np.float32)
         out = m(torch.from_numpy(ids))
