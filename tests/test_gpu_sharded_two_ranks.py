@@ -32,7 +32,27 @@ def workload():
     return trace, table, grads
 
 
-def _rank_main(rank, world, port, kind, prefetch, q):
+BAGS = 1_500  # per rank per step (mean mode: bags of 0-3 ids)
+
+
+def workload_bags():
+    """Per step and rank: (ids, offsets, bag gradients) with bag lengths 0..3."""
+    rng = np.random.default_rng(33)
+    p = 1.0 / np.arange(1, NUM + 1) ** 1.1
+    perm = rng.permutation(NUM)
+    steps = []
+    for _ in range(STEPS):
+        per = []
+        for _r in range(2):
+            lens = rng.integers(0, 4, BAGS)
+            ids = perm[rng.choice(NUM, size=int(lens.sum()), p=p / p.sum())]
+            off = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.int64)
+            per.append((ids, off, rng.standard_normal((BAGS, DIM)).astype(np.float32)))
+        steps.append(per)
+    return steps
+
+
+def _rank_main(rank, world, port, kind, prefetch, q, mode="sum"):
     import torch.distributed as dist
 
     import paper_2208_05321_b200.distributed as D
@@ -51,7 +71,11 @@ def _rank_main(rank, world, port, kind, prefetch, q):
 
         D._a2a = staged_a2a
         trace, table, grads = workload()
-        counts = np.bincount(trace.reshape(-1), minlength=NUM)
+        bags = workload_bags() if mode == "mean" else None
+        if bags is None:
+            counts = np.bincount(trace.reshape(-1), minlength=NUM)
+        else:
+            counts = np.bincount(np.concatenate([b[r][0] for b in bags for r in range(world)]), minlength=NUM)
         placement = None
         if kind == "row":
             idx = D.shard_rows_for_rank(counts, rank, world)
@@ -65,17 +89,24 @@ def _rank_main(rank, world, port, kind, prefetch, q):
         rows[...] = table[gids[idx.id_of]]
         shard = D.CudaShard(n_local, DIM, fast_capacity(n_local, 0.05), rows, idx, lr=LR, device="cuda:0",
                             global_num_ids=NUM)
-        mod = D.RowShardedEmbedding(shard, world, rank, mode="sum", device=torch.device("cuda", 0),
+        mod = D.RowShardedEmbedding(shard, world, rank, mode=mode, device=torch.device("cuda", 0),
                                     placement=placement)
         per = B // world
-        tids = [torch.from_numpy(trace[s, rank * per:(rank + 1) * per]).cuda() for s in range(STEPS)]
+        if bags is None:
+            tids = [torch.from_numpy(trace[s, rank * per:(rank + 1) * per]).cuda() for s in range(STEPS)]
+            toff = [None] * STEPS
+            tg = [torch.from_numpy(grads[s, rank * per:(rank + 1) * per]).cuda() for s in range(STEPS)]
+        else:
+            tids = [torch.from_numpy(b[rank][0]).cuda() for b in bags]
+            toff = [torch.from_numpy(b[rank][1]).cuda() for b in bags]
+            tg = [torch.from_numpy(b[rank][2]).cuda() for b in bags]
         outs = []
         for s in range(STEPS):
-            out = mod(tids[s])
+            out = mod(tids[s], toff[s])
             outs.append(out.detach().cpu().numpy())
             if prefetch and s + 1 < STEPS:
                 mod.prefetch(tids[s + 1])
-            out.backward(torch.from_numpy(grads[s, rank * per:(rank + 1) * per]).cuda())
+            out.backward(tg[s])
         mod.flush()
         torch.cuda.synchronize()
         got = np.empty((n_local, DIM), np.float32)
@@ -128,4 +159,42 @@ def test_two_ranks_match_dense(kind, prefetch):
     for r in range(world):
         got[res[r][0]] = res[r][1]
     assert not np.isnan(got).any()  # the two owners hold every row exactly once
+    np.testing.assert_allclose(got, dense.weight.detach().numpy(), rtol=1e-5, atol=5e-6)
+
+
+def test_two_ranks_mean_bags_match_dense():
+    """Row-wise, mean pooling over bags of 0-3 ids (empty bags included), prefetching."""
+    import torch.multiprocessing as mp
+
+    _, table, _ = workload()
+    bags = workload_bags()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, "row", True, q, "mean")) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = {r: (g, rows, outs) for r, g, rows, outs in (q.get(timeout=600) for _ in range(world))}
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert isinstance(res[r][1], np.ndarray), res[r][0]
+    dense = torch.nn.EmbeddingBag(NUM, DIM, mode="mean", sparse=True)
+    dense.weight.data = torch.from_numpy(table.copy())
+    opt = torch.optim.SGD(dense.parameters(), lr=LR)
+    for s, step in enumerate(bags):
+        ids = np.concatenate([step[r][0] for r in range(world)])
+        off = np.concatenate([step[0][1], step[1][1] + step[0][0].size])
+        want = dense(torch.from_numpy(ids), torch.from_numpy(off))
+        for r in range(world):
+            np.testing.assert_allclose(res[r][2][s], want.detach().numpy()[r * BAGS:(r + 1) * BAGS], rtol=1e-5,
+                                       atol=5e-6)
+        opt.zero_grad()
+        want.backward(torch.from_numpy(np.concatenate([step[r][2] for r in range(world)])))
+        opt.step()
+    got = np.full_like(table, np.nan)
+    for r in range(world):
+        got[res[r][0]] = res[r][1]
+    assert not np.isnan(got).any()
     np.testing.assert_allclose(got, dense.weight.detach().numpy(), rtol=1e-5, atol=5e-6)
