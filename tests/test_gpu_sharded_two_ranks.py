@@ -87,8 +87,8 @@ def _rank_main(rank, world, port, kind, prefetch, q, mode="sum"):
         n_local = int(gids.size)
         rows = pinned_empty((n_local, DIM))
         rows[...] = table[gids[idx.id_of]]
-        shard = D.CudaShard(n_local, DIM, fast_capacity(n_local, 0.05), rows, idx, lr=LR, device="cuda:0",
-                            global_num_ids=NUM)
+        cap = fast_capacity(n_local, 0.05 if mode == "sum" else 0.15)  # mean bags: more unique ids per batch
+        shard = D.CudaShard(n_local, DIM, cap, rows, idx, lr=LR, device="cuda:0", global_num_ids=NUM)
         mod = D.RowShardedEmbedding(shard, world, rank, mode=mode, device=torch.device("cuda", 0),
                                     placement=placement)
         per = B // world
