@@ -567,6 +567,8 @@ static int segment_grads(void** scratch, size_t* scratch_bytes, const int32_t* i
   return FC_OK;
 }
 
+__global__ void k_noop() {}
+
 int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, const int32_t* ucnt, int64_t u, int64_t n,
                     const void* offsets, int off_bytes, int64_t nbags, int include_last, const float* psw, int mode,
                     const float* grad, int optim, float lr, float eps, cudaStream_t st) {
@@ -600,6 +602,14 @@ int launch_backward(fc_cache* h, const int32_t* uslots, const int32_t* inv, cons
   }
   // the digit histograms of `inv`, when a pipeline index phase produced it (no histogram kernel)
   const int32_t* sort_hist = pipe_take_sort_hist(h, inv, n);
+  // FC_DEBUG_NOOP_LAUNCHES=k: measurement only -- k empty kernels on the compute stream before a
+  // pipelined backward, to price a kernel boundary inside the step (results unchanged)
+  static const int noop_launches = [] {
+    const char* e = std::getenv("FC_DEBUG_NOOP_LAUNCHES");
+    return e ? std::max(0, std::atoi(e)) : 0;
+  }();
+  if (sort_hist)
+    for (int k = 0; k < noop_launches; ++k) k_noop<<<1, 32, 0, st>>>();
   int rc = segment_grads(&h->scratch, &h->scratch_bytes, inv, u, n, offsets, off_bytes, nbags, include_last, psw, mode,
                          grad, D, nullptr, x, fused, st, &h->sort_zero_for, &h->sort_zero_bytes, sort_hist);
   if (rc || fused) return rc;
