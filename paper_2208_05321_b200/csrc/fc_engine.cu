@@ -869,6 +869,14 @@ struct Pipe {
     if (rc__) return rc__; \
   } while (0)
 
+// FC_DEBUG_NOOP_INDEX / FC_DEBUG_NOOP_XFER=k: measurement only -- k empty kernels at the end of
+// every pipelined index phase / before every staging, to price a kernel boundary on that chain
+__global__ void k_noop_e() {}
+static int debug_noops(const char* name) {
+  const char* e = std::getenv(name);
+  return e ? std::max(0, std::atoi(e)) : 0;
+}
+
 bool pipe_outstanding(const fc_cache* h) { return h->pipe && h->pipe->nout > 0; }
 
 // Host wait for every recorded pipeline commit (their kernels have finished).
@@ -1400,6 +1408,7 @@ int pipe_begin(fc_cache* h, const void* ids, int ids_bytes, int64_t n, int32_t* 
   int rc = launch_index_phase(h, ids, ids_bytes, n, uids, ucnt, uranks, uslots, inverse, q->ib[p], q->hctr_dev[p],
                               q->sort_hist[hs], st);
   if (rc) return rc;
+  for (int k = 0; k < debug_noops("FC_DEBUG_NOOP_INDEX"); ++k) k_noop_e<<<1, 32, 0, st>>>();
   trace_mark(h, T_INDEX_END, st);
   FC_CUDA(cudaEventRecord(q->ev_index[p], st));
   q->has_index[p] = true;
@@ -1458,6 +1467,7 @@ int pipe_launch_xfer(fc_cache* h, cudaStream_t after, bool from_update) {
   harvest_xfer_time(h, p, true);  // this parity's previous staging (long finished) before its events are reused
   q->timed[p] = h->profile != 0;
   if (q->timed[p]) FC_CUDA(cudaEventRecord(q->px[p][0], q->xfer));
+  for (int k = 0; k < debug_noops("FC_DEBUG_NOOP_XFER"); ++k) k_noop_e<<<1, 32, 0, q->xfer>>>();
   trace_mark(h, T_XFER_BEGIN, q->xfer);
   // FC_DEBUG_SKIP_STAGING=1: measurement only (admitted rows are NOT staged, results are
   // wrong) -- how long the rest of the pipelined step takes without host-link traffic
