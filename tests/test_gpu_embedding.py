@@ -121,9 +121,10 @@ def test_hot_row_long_segment():
     np.testing.assert_allclose(m.weight(), want, rtol=1e-5, atol=2e-6)
 
 
-@pytest.mark.parametrize("num,sizes", [(3_000, [500, 4_000, 120, 4_000, 9_000, 37, 9_000]),
-                                       (200, [4_000, 120, 4_000, 500, 9_000, 300, 2_000, 9_000])])
-def test_backward_sequence_of_batch_sizes_reuses_sort_state(num, sizes):
+@pytest.mark.parametrize("num,sizes,prefetch", [(3_000, [500, 4_000, 120, 4_000, 9_000, 37, 9_000], False),
+                                                (200, [4_000, 120, 4_000, 500, 9_000, 300, 2_000, 9_000], False),
+                                                (200, [4_000, 120, 4_000, 500, 9_000, 300, 2_000, 9_000], True)])
+def test_backward_sequence_of_batch_sizes_reuses_sort_state(num, sizes, prefetch):
     """Back-to-back fused backwards of growing and shrinking batches (the fix-up clears the
     next sort's state instead of a memset, DESIGN 4b) with a scatter_update in between,
     against dense SGD: every step within 1e-5. The second case draws from 200 ids, so every
@@ -134,10 +135,15 @@ def test_backward_sequence_of_batch_sizes_reuses_sort_state(num, sizes):
     w = rng.uniform(-0.1, 0.1, (num, dim)).astype(np.float32)
     m = CachedEmbeddingBag(num, dim, cache_ratio=1.0, mode="sum", weight=w, lr=lr)
     dense = w.astype(np.float64)
+    batches = [torch.from_numpy(rng.integers(0, num, n)) for n in sizes]
+    if prefetch:  # pipelined: the index phase makes the sort histograms, sizes still change
+        m.prefetch(batches[0])
     for s, n in enumerate(sizes):
-        ids = rng.integers(0, num, n)
+        ids = batches[s].numpy()
         gout = rng.standard_normal((n, dim)).astype(np.float32)
-        out = m(torch.from_numpy(ids))
+        out = m(batches[s])
+        if prefetch and s + 1 < len(sizes) and s != 3:
+            m.prefetch(batches[s + 1])
         np.testing.assert_allclose(out.detach().cpu().numpy(), dense[ids], rtol=RTOL, atol=ATOL)
         out.backward(torch.from_numpy(gout).cuda())
         np.add.at(dense, ids, -lr * gout.astype(np.float64))
