@@ -26,6 +26,19 @@ class _CudaArray:
                                          "data": (int(ptr), False), "version": 3, "strides": None}
 
 
+_RAW_STREAM = None
+
+
+def _raw_stream(index: int) -> int:
+    global _RAW_STREAM
+    if _RAW_STREAM is None:
+        import torch
+
+        _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None) or (
+            lambda i: torch.cuda.current_stream(i).cuda_stream)  # older torch: the public (slower) path
+    return _RAW_STREAM(index)
+
+
 def _ptr(t) -> int:
     return 0 if t is None else int(t.data_ptr())
 
@@ -79,7 +92,9 @@ class DeviceCache:
 
     # ------------------------------------------------------------------ plumbing
     def stream(self):
-        return ctypes.c_void_p(self.torch.cuda.current_stream(self.device).cuda_stream)
+        # the raw handle of the current stream (torch.cuda.current_stream builds a Stream object
+        # and re-parses the device on every call: ~10 us of host time per call on this path)
+        return ctypes.c_void_p(_raw_stream(self.device.index))
 
     def close(self):
         if getattr(self, "h", None) is not None and self.h.value:
@@ -238,7 +253,7 @@ class DeviceCache:
             # highest priority: the index phase is short but on the pipeline's critical
             # path, and must not queue behind the previous batch's backward blocks
             self.index_stream = torch.cuda.Stream(self.device, priority=-100)
-        main = torch.cuda.current_stream(self.device)  # orders device ids
+        main = torch.cuda.current_stream(self.device.index)  # orders device ids
         consumer = main if consumer is None else consumer
         if index_on_main is None:
             index_on_main = self.index_on_main

@@ -25,7 +25,7 @@ import numpy as np
 import torch
 import torch.distributed as dist
 
-from .device import DeviceCache
+from .device import DeviceCache, _raw_stream
 from .freq_stats import IdxMap
 from .sharding import partition_columns
 from .store import fast_capacity, pinned_empty
@@ -169,7 +169,7 @@ class Router:
             pass
 
     def _stream(self):
-        return self._ct.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        return self._ct.c_void_p(_raw_stream(self.device.index))
 
     def route(self, ids):
         """-> (owner-local unique ids grouped by owner, inverse, per-owner counts)"""
@@ -328,7 +328,7 @@ class PeerRows:
     def pool_to_peers(self, shard, h, x):
         ct = self._ct
         seg, off = self._segments(x)
-        stream = ct.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        stream = ct.c_void_p(torch.cuda.current_stream(self.device.index).cuda_stream)
         self._check(self.lib.fc_pool_to_peers(shard.cache.h, ct.c_void_p(h["uslots"].data_ptr()),
                                               ct.c_void_p(h["inverse"].data_ptr()), int(h["n"]),
                                               ct.c_void_p(seg.data_ptr()), self.world, ct.c_void_p(self.dst.data_ptr()),
@@ -368,7 +368,7 @@ class PeerRows:
         seg, off = self._segments(x)
         n = int(sum(x["rc"]))
         g_recv = torch.empty((n, self.dim), dtype=torch.float32, device=self.device)
-        stream = ct.c_void_p(torch.cuda.current_stream(self.device).cuda_stream)
+        stream = ct.c_void_p(torch.cuda.current_stream(self.device.index).cuda_stream)
         self._check(self.lib.fc_gather_from_peers(ct.c_void_p(self.gsrc.data_ptr()), ct.c_void_p(off.data_ptr()),
                                                   ct.c_void_p(seg.data_ptr()), self.world, n, self.dim,
                                                   ct.c_void_p(g_recv.data_ptr()), stream))
@@ -485,7 +485,7 @@ class RowShardedEmbedding(torch.nn.Module):
             x["src"], x["ids"] = ids, dev_ids
             self._pfq.append(x)
             return
-        main = torch.cuda.current_stream(self.device)
+        main = torch.cuda.current_stream(self.device.index)
         if getattr(self, "_xstream", None) is None:
             self._xstream = torch.cuda.Stream(self.device, priority=-100)
         xs = self._xstream
@@ -516,7 +516,7 @@ class RowShardedEmbedding(torch.nn.Module):
             px = self._pfq.pop(0)
             pids = px["ids"]
             if px.get("ev") is not None:  # the side stream's exchange is ordered before anything below
-                torch.cuda.current_stream(self.device).wait_event(px["ev"])
+                torch.cuda.current_stream(self.device.index).wait_event(px["ev"])
             hp = self.shard.prepare_commit() if px.get("begun") else None
             if px["src"] is src or pids is ids or (pids.numel() == ids.numel() and bool(torch.equal(pids, ids))):
                 x, h = px, hp
@@ -580,7 +580,7 @@ class RowShardedEmbedding(torch.nn.Module):
         while self._pfq:  # outstanding prefetches are committed first (their batches become resident)
             px = self._pfq.pop(0)
             if px.get("ev") is not None:
-                torch.cuda.current_stream(self.device).wait_event(px["ev"])
+                torch.cuda.current_stream(self.device.index).wait_event(px["ev"])
             if px.get("begun"):
                 self.shard.prepare_commit()
         return self.shard.flush()
@@ -669,7 +669,7 @@ class ColumnShardedEmbedding(torch.nn.Module):
                 self.shard.prepare_begin(g_ids)
             self._pfq.append({"src": ids, "ids": dev_ids, "counts": counts, "ev": None, "begun": can_begin})
             return
-        main = torch.cuda.current_stream(self.device)
+        main = torch.cuda.current_stream(self.device.index)
         if self._xstream is None:
             self._xstream = torch.cuda.Stream(self.device, priority=-100)
         xs = self._xstream
@@ -696,7 +696,7 @@ class ColumnShardedEmbedding(torch.nn.Module):
         while self._pfq:
             pf = self._pfq.pop(0)
             if pf["ev"] is not None:
-                torch.cuda.current_stream(self.device).wait_event(pf["ev"])
+                torch.cuda.current_stream(self.device.index).wait_event(pf["ev"])
             h = self.shard.prepare_commit() if pf["begun"] else None
             same = pf["src"] is src or pf["ids"] is ids or (
                 pf["ids"].numel() == ids.numel() and bool(torch.equal(pf["ids"], ids)))
@@ -756,7 +756,7 @@ class ColumnShardedEmbedding(torch.nn.Module):
         while self._pfq:
             pf = self._pfq.pop(0)
             if pf["ev"] is not None:
-                torch.cuda.current_stream(self.device).wait_event(pf["ev"])
+                torch.cuda.current_stream(self.device.index).wait_event(pf["ev"])
             if pf["begun"]:
                 self.shard.prepare_commit()
         return self.shard.flush()
