@@ -29,13 +29,18 @@ class _CudaArray:
 _RAW_STREAM = None
 
 
-def _raw_stream(index: int) -> int:
+def _raw_stream(index) -> int:
+    """Raw handle of the current CUDA stream of device `index` (None: the current device)."""
     global _RAW_STREAM
     if _RAW_STREAM is None:
         import torch
 
         _RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None) or (
             lambda i: torch.cuda.current_stream(i).cuda_stream)  # older torch: the public (slower) path
+    if index is None:
+        import torch
+
+        index = torch.cuda.current_device()
     return _RAW_STREAM(index)
 
 
