@@ -161,6 +161,17 @@ def test_bench_reference_arm_and_gpu_count_check():
     assert doc["cpu_baseline"]["kind"] in ("reference", "port") and doc["cpu_baseline"]["cores"] == 1
     assert doc["config"]["workload"] == "small" and doc["config"]["parallelism"] == "single"
     assert doc["e2e"]["h2d_bytes_per_step"] == 0
+    # rank 0 of a 2-rank launch: the config's batch is the global batch (strong scaling), split in
+    # two, and the reference's column-wise stacks serve it
+    env = dict(os.environ, WORLD_SIZE="2", RANK="0")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--config", "small",
+                        "--gpus", "2", "--shard", "column", "--steps", "1", "--warmup", "3", "--trace-batches", "12"],
+                       capture_output=True, text=True, timeout=300, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    doc = json.loads([ln for ln in r.stdout.splitlines() if ln.strip()][0])
+    assert doc["scaling"] == "strong" and doc["n_gpus"] == 2
+    assert doc["config"]["global_batch"] == 1024 and doc["config"]["batch_per_gpu"] == 512
+    assert doc["config"]["parallelism"] == "columnwise2" and doc["config"]["lookups_per_step"] == 1024 * 26
     import torch
 
     if torch.cuda.device_count() < 2:
