@@ -149,6 +149,9 @@ class Router:
         if placement is None:  # row-wise: owner id % world
             check(self.lib.fc_router_create(int(num_ids), self.world, self.device.index or 0, ctypes.byref(h)))
         else:  # table-wise: whole tables per owner (TablePlacement)
+            if placement.world != self.world or placement.num_ids != int(num_ids):
+                raise ValueError(f"placement is for {placement.world} ranks over {placement.num_ids} ids, the router "
+                                 f"for {self.world} over {int(num_ids)}")
             starts = np.ascontiguousarray(placement.starts, dtype=np.int64)
             owner = np.ascontiguousarray(placement.owner, dtype=np.int32)
             check(self.lib.fc_router_create_tables(int(num_ids), self.world, int(owner.size),

@@ -207,6 +207,10 @@ def test_route_tables_rejects_bad_placements():
             check(create(starts, owner, **kw))
     check(create([0, 10, 20], [1, 0]))
     lib.fc_router_destroy(h)
+    from paper_2208_05321_b200.distributed import TablePlacement
+
+    with pytest.raises(ValueError, match="placement is for"):
+        Router(20, 3, "cuda", placement=TablePlacement([0, 10, 20], [1, 0], 2))
 
 
 def test_table_sharded_module_nccl_world1_matches_dense():
