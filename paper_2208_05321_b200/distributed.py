@@ -407,6 +407,8 @@ class RowShardedEmbedding(torch.nn.Module):
                  group=None, device=None, peer_rows: int = 0, placement: TablePlacement | None = None):
         super().__init__()
         self.shard, self.world, self.rank = shard, world, rank
+        if placement is not None and placement.world != world:
+            raise ValueError(f"table placement is for {placement.world} ranks, the module has {world}")
         self.placement = placement  # None: row-wise (owner id % world); else table-wise
         self.mode, self.include_last_offset, self.group = mode, include_last_offset, group
         self.device = device if device is not None else getattr(shard, "device", torch.device("cpu"))
