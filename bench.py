@@ -528,7 +528,9 @@ def run_ours(args, cfg, torch, rank, world):
         fill_pinned(torch, rows, dev, SEED + rank)
         shard = CudaShard(cfg["num_ids"], hi_c - lo_c, cap, rows, fc.IdxMap(rank_of, id_of), optimizer=OPT, lr=LR,
                           device=dev, engine=args.engine)
-        mod = ColumnShardedEmbedding(shard, D, world, rank, mode=MODE, device=dev)
+        # --peer: the pooled-columns all-to-all and its backward mirror fused into the gather /
+        # gradient-pull kernels over NVLink peer memory (PeerColumns) instead of NCCL
+        mod = ColumnShardedEmbedding(shard, D, world, rank, mode=MODE, device=dev, peer_rows=N if args.peer else 0)
         dcs = [shard.cache]
     else:
         from paper_2208_05321_b200.distributed import (CudaShard, RowShardedEmbedding, shard_rows_for_rank,
@@ -770,7 +772,9 @@ def run_ours(args, cfg, torch, rank, world):
                            "exchange": (None if not rowwise else "unique ids by NCCL all-to-all; rows back "
                                         + ("by owner-side peer-memory writes" if args.peer else "by NCCL all-to-all")
                                         ) if shard_mode != "column" else
-                           "all-gather of ids; pooled columns by NCCL all-to-all (reference semantics)",
+                           ("all-gather of ids; pooled columns written into the requesters' outputs over peer memory "
+                            "(fc_pool_cols_to_peers), gradient columns pulled back (fc_gather_cols_from_peers)"
+                            if args.peer else "all-gather of ids; pooled columns by NCCL all-to-all (reference semantics)"),
                            "capacity_per_gpu": cap},
         "step_latency_ms": {"p50": float(np.percentile(step_ms, 50)), "p99": float(np.percentile(step_ms, 99)),
                             "prepare_avg": (None if pipelined else prof["prepare_ms"] / max(prof["calls"], 1)),
@@ -1024,8 +1028,9 @@ def main():
                          "1: after forward(t) (default for the sharded modules)")
     ap.add_argument("--sharded", action="store_true", help="alias of --shard row (also at one GPU)")
     ap.add_argument("--peer", action="store_true",
-                    help="row-sharded runs: owners write the rows straight into the requesters' buffers over "
-                         "NVLink peer memory (CUDA IPC) instead of the NCCL all-to-all")
+                    help="sharded runs: the return exchange fused into the owners' kernels over NVLink peer memory "
+                         "(CUDA IPC) instead of the NCCL all-to-all (row-wise: looked-up rows; column-wise: pooled "
+                         "column slices and the gradients' columns)")
     ap.add_argument("--no-peer", action="store_true", help="(default) rows come back by NCCL all-to-all")
     ap.add_argument("--no-prefetch", action="store_true",
                     help="synchronous prepare each step (no lookahead pipeline)")

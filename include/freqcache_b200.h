@@ -320,6 +320,22 @@ int fc_pool_to_peers(fc_cache* h, const int32_t* unique_slots, const int32_t* in
  * requesters' writes. */
 int fc_gather_from_peers(const float* const* src_ptrs_dev, const int64_t* src_off_dev, const int64_t* seg_dev,
                          int32_t world, int64_t n, int32_t dim, float* out, void* stream);
+/* Column-wise split (the reference's sharding.py:62-118), forward fused with its all-to-all
+ * (the exchange sharding.py:133-146 only accounts for): this rank's pooled column slice of
+ * global occurrence i (bag size 1; requester r = the segment of i in seg_dev[0..world]) is
+ * written straight into requester r's output dst_ptrs_dev[r] (peer pointer over NVLink) at
+ * row dst_off_dev[r] + (i - seg[r]), columns [col, col + dim) of rows ld floats wide; psw
+ * (optional, per global occurrence) scales the row. dim, ld and col multiples of 4. */
+int fc_pool_cols_to_peers(fc_cache* h, const int32_t* unique_slots, const int32_t* inverse, int64_t n,
+                          const int64_t* seg_dev, int32_t world, float* const* dst_ptrs_dev,
+                          const int64_t* dst_off_dev, int64_t ld, int64_t col, const float* per_sample_weights,
+                          void* stream);
+/* Its backward mirror: columns [col, col + dim) of every requester's gradient rows
+ * (src_ptrs_dev[r], rows ld floats wide, from row src_off_dev[r]) gathered over peer memory
+ * into out [n, dim] in global occurrence order, ready for fc_backward_update. */
+int fc_gather_cols_from_peers(const float* const* src_ptrs_dev, const int64_t* src_off_dev, const int64_t* seg_dev,
+                              int32_t world, int64_t n, int32_t dim, int64_t ld, int64_t col, float* out,
+                              void* stream);
 /* CUDA IPC plumbing for the peer pointers. handle_out: FC_IPC_HANDLE_BYTES opaque bytes
  * (the allocation's cudaIpcMemHandle_t + the pointer's offset inside it, so pointers into a
  * caching allocator's segment export correctly); fc_ipc_open returns the same address in

@@ -86,6 +86,10 @@ _SIGS = {
     "fc_pool_to_peers": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
                                    c_void_p]),
     "fc_gather_from_peers": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_int32, c_void_p, c_void_p]),
+    "fc_pool_cols_to_peers": (c_int32, [c_void_p, c_void_p, c_void_p, c_int64, c_void_p, c_int32, c_void_p, c_void_p,
+                                        c_int64, c_int64, c_void_p, c_void_p]),
+    "fc_gather_cols_from_peers": (c_int32, [c_void_p, c_void_p, c_void_p, c_int32, c_int64, c_int32, c_int64, c_int64,
+                                            c_void_p, c_void_p]),
     "fc_ipc_handle": (c_int32, [c_void_p, c_void_p]),
     "fc_ipc_open": (c_int32, [c_void_p, c_int32, POINTER(c_void_p)]),
     "fc_ipc_close": (c_int32, [c_void_p]),

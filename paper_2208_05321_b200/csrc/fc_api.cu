@@ -728,6 +728,23 @@ int fc_gather_from_peers(const float* const* src_ptrs_dev, const int64_t* src_of
   return launch_gather_from_peers(src_ptrs_dev, src_off_dev, seg_dev, world, n, dim, out, as_stream(stream));
 }
 
+int fc_pool_cols_to_peers(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const int64_t* seg_dev,
+                          int32_t world, float* const* dst_ptrs_dev, const int64_t* dst_off_dev, int64_t ld,
+                          int64_t col, const float* psw, void* stream) {
+  if (!h || world < 1 || world > 64 || n < 0 || ld < 1 || col < 0) return FC_ERR_BAD_ARG;
+  DeviceGuard dg(h->device);
+  return launch_pool_cols_to_peers(h, uslots, inv, n, seg_dev, world, dst_ptrs_dev, dst_off_dev, ld, col, psw,
+                                   as_stream(stream));
+}
+
+int fc_gather_cols_from_peers(const float* const* src_ptrs_dev, const int64_t* src_off_dev, const int64_t* seg_dev,
+                              int32_t world, int64_t n, int32_t dim, int64_t ld, int64_t col, float* out,
+                              void* stream) {
+  if (world < 1 || world > 64 || n < 0 || dim < 1 || ld < 1 || col < 0) return FC_ERR_BAD_ARG;
+  return launch_gather_cols_from_peers(src_ptrs_dev, src_off_dev, seg_dev, world, n, dim, ld, col, out,
+                                       as_stream(stream));
+}
+
 // A CUDA IPC handle names a whole cudaMalloc allocation and cudaIpcOpenMemHandle maps its
 // BASE; a pointer inside a caching allocator's segment (torch) sits at an offset from it.
 // The exported handle therefore carries that offset, and the importer adds it back.

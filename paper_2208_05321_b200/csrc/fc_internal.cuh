@@ -262,6 +262,11 @@ int launch_pool(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t 
 int launch_gather_rows(fc_cache* h, const int32_t* slots, int64_t n, float* out, cudaStream_t st);
 int launch_gather_from_peers(const float* const* src, const int64_t* src_off, const int64_t* seg, int W, int64_t n,
                              int D, float* out, cudaStream_t st);
+int launch_pool_cols_to_peers(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const int64_t* seg,
+                              int W, float* const* dst, const int64_t* dst_off, int64_t ld, int64_t col,
+                              const float* psw, cudaStream_t st);
+int launch_gather_cols_from_peers(const float* const* src, const int64_t* src_off, const int64_t* seg, int W,
+                                  int64_t n, int D, int64_t ld, int64_t col, float* out, cudaStream_t st);
 int launch_pool_to_peers(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const int64_t* seg, int W,
                          float* const* dst, const int64_t* dst_off, cudaStream_t st);
 int launch_unique_add(fc_cache* h, const int32_t* uslots, int64_t u, const float* add, cudaStream_t st);

@@ -568,12 +568,15 @@ int launch_pool_rows(const float* rows, int D, const int32_t* uslots, const int3
 // written directly into requester r's receive buffer over NVLink peer memory (CUDA IPC /
 // symmetric pointers), at row dst_off[r] + (i - seg[r]). Replaces "pool into a local
 // buffer, then all-to-all". The caller orders it before a stream-ordered barrier.
+// Column-wise split (fc_pool_cols_to_peers): the destination rows are ld floats wide and this
+// rank's slice starts at column col; psw (optional) scales occurrence i's row.
 __global__ void __launch_bounds__(kNT) k_pool_to_peers(const float* __restrict__ fast, int D,
                                                        const int32_t* __restrict__ uslots,
                                                        const int32_t* __restrict__ inv, int64_t n,
                                                        const int64_t* __restrict__ seg, int W,
                                                        float* const* __restrict__ dst, const int64_t* __restrict__ dst_off,
-                                                       Units un) {
+                                                       Units un, int64_t ld, int64_t col,
+                                                       const float* __restrict__ psw) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
@@ -582,11 +585,13 @@ __global__ void __launch_bounds__(kNT) k_pool_to_peers(const float* __restrict__
     const bool act = i < n;
     const float* src = nullptr;
     float* out = nullptr;
+    float w = 1.f;
     if (act) {
       int r = 0;
       while (r + 1 < W && seg[r + 1] <= i) ++r;  // W <= 64: a short scan
       src = fast + (int64_t)uslots[inv[i]] * D;
-      out = dst[r] + (dst_off[r] + (i - seg[r])) * (int64_t)D;
+      out = dst[r] + (dst_off[r] + (i - seg[r])) * ld + col;
+      if (psw) w = psw[i];
     }
     // lanes sweep the 32 rows' 16-byte units (4 in flight), writing to each row's owner
     const int total = 32 * un.upr;
@@ -602,7 +607,12 @@ __global__ void __launch_bounds__(kNT) k_pool_to_peers(const float* __restrict__
         const float* sp = reinterpret_cast<const float*>(__shfl_sync(FC_FULL, reinterpret_cast<long long>(src), rr));
         d[q] = reinterpret_cast<float*>(__shfl_sync(FC_FULL, reinterpret_cast<long long>(out), rr)) + c;
         a[q] = __shfl_sync(FC_FULL, (int)act, rr) && u < total;
-        if (a[q]) v[q] = ld4(sp + c);
+        const float wq = __shfl_sync(FC_FULL, w, rr);
+        if (a[q]) {
+          v[q] = ld4(sp + c);
+          if (psw) v[q] = make_float4(__fmul_rn(v[q].x, wq), __fmul_rn(v[q].y, wq), __fmul_rn(v[q].z, wq),
+                                      __fmul_rn(v[q].w, wq));
+        }
       }
 #pragma unroll
       for (int q = 0; q < 4; ++q)
@@ -620,7 +630,22 @@ int launch_pool_to_peers(fc_cache* h, const int32_t* uslots, const int32_t* inv,
     return FC_ERR_BAD_ARG;
   }
   k_pool_to_peers<<<grid_for(n, kNT, kSMs * 8), kNT, 0, st>>>(h->fast, h->dim, uslots, inv, n, seg, W, dst, dst_off,
-                                                              units_for(h->dim));
+                                                              units_for(h->dim), h->dim, 0, nullptr);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+int launch_pool_cols_to_peers(fc_cache* h, const int32_t* uslots, const int32_t* inv, int64_t n, const int64_t* seg,
+                              int W, float* const* dst, const int64_t* dst_off, int64_t ld, int64_t col,
+                              const float* psw, cudaStream_t st) {
+  if (n <= 0) return FC_OK;
+  if (h->dim % 4 || ld % 4 || col % 4 || col + h->dim > ld) {
+    set_error("pool_cols_to_peers needs 16-byte aligned column slices (dim %d, ld %lld, col %lld)", h->dim,
+              (long long)ld, (long long)col);
+    return FC_ERR_BAD_ARG;
+  }
+  k_pool_to_peers<<<grid_for(n, kNT, kSMs * 8), kNT, 0, st>>>(h->fast, h->dim, uslots, inv, n, seg, W, dst, dst_off,
+                                                              units_for(h->dim), ld, col, psw);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }
@@ -631,7 +656,7 @@ int launch_pool_to_peers(fc_cache* h, const int32_t* uslots, const int32_t* inv,
 __global__ void __launch_bounds__(kNT) k_gather_from_peers(const float* const* __restrict__ src,
                                                            const int64_t* __restrict__ src_off,
                                                            const int64_t* __restrict__ seg, int W, int64_t n, int D,
-                                                           float* __restrict__ out, Units un) {
+                                                           float* __restrict__ out, Units un, int64_t ld, int64_t col) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = ((int64_t)blockIdx.x * kNT + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * kNT) >> 5;
@@ -642,7 +667,7 @@ __global__ void __launch_bounds__(kNT) k_gather_from_peers(const float* const* _
     if (act) {
       int r = 0;
       while (r + 1 < W && seg[r + 1] <= i) ++r;
-      sp = src[r] + (src_off[r] + (i - seg[r])) * (int64_t)D;
+      sp = src[r] + (src_off[r] + (i - seg[r])) * ld + col;
     }
     const int total = 32 * un.upr;
     for (int u0 = 0; u0 < total; u0 += 32 * 4) {
@@ -669,7 +694,21 @@ __global__ void __launch_bounds__(kNT) k_gather_from_peers(const float* const* _
 int launch_gather_from_peers(const float* const* src, const int64_t* src_off, const int64_t* seg, int W, int64_t n,
                              int D, float* out, cudaStream_t st) {
   if (n <= 0) return FC_OK;
-  k_gather_from_peers<<<grid_for(n, kNT, kSMs * 8), kNT, 0, st>>>(src, src_off, seg, W, n, D, out, units_for(D));
+  k_gather_from_peers<<<grid_for(n, kNT, kSMs * 8), kNT, 0, st>>>(src, src_off, seg, W, n, D, out, units_for(D), D, 0);
+  FC_CUDA(cudaGetLastError());
+  return FC_OK;
+}
+
+int launch_gather_cols_from_peers(const float* const* src, const int64_t* src_off, const int64_t* seg, int W,
+                                  int64_t n, int D, int64_t ld, int64_t col, float* out, cudaStream_t st) {
+  if (n <= 0) return FC_OK;
+  if (D % 4 || ld % 4 || col % 4 || col + D > ld) {
+    set_error("gather_cols_from_peers needs 16-byte aligned column slices (dim %d, ld %lld, col %lld)", D,
+              (long long)ld, (long long)col);
+    return FC_ERR_BAD_ARG;
+  }
+  k_gather_from_peers<<<grid_for(n, kNT, kSMs * 8), kNT, 0, st>>>(src, src_off, seg, W, n, D, out, units_for(D), ld,
+                                                                  col);
   FC_CUDA(cudaGetLastError());
   return FC_OK;
 }

@@ -220,6 +220,17 @@ def _upload(vals, device):
     return t.pin_memory().to(device, non_blocking=True)
 
 
+def _peer_barrier(flag, group=None):
+    """Stream-ordered barrier after peer-memory writes: a one-element NCCL all-reduce on the
+    current stream (every rank's earlier kernels finish before it completes anywhere). A
+    CPU-only group (gloo: the single-GPU multi-process tests) waits on the host instead."""
+    if dist.get_backend(group) == "nccl":
+        dist.all_reduce(flag, group=group)
+    else:
+        torch.cuda.current_stream(flag.device.index).synchronize()
+        dist.barrier(group=group)
+
+
 def _a2a(out, inp, out_splits, in_splits, group=None):
     dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
     return out
@@ -337,7 +348,7 @@ class PeerRows:
                                               ct.c_void_p(seg.data_ptr()), self.world, ct.c_void_p(self.dst.data_ptr()),
                                               ct.c_void_p(off.data_ptr()), stream))
         if self.world > 1:  # every owner's writes land before anyone reads (one rank: stream order suffices)
-            dist.all_reduce(self.flag, group=self.group)
+            _peer_barrier(self.flag, self.group)
         return self.rbuf[:x["u"]]
 
     def segments(self, x):
@@ -367,7 +378,7 @@ class PeerRows:
         router.grads(x["inv"], x["u"], grad_out, offsets, n_bags, include_last_offset, psw, mode,
                      out=self.gbuf[:x["u"]])
         if self.world > 1:  # every requester's gradients are in place
-            dist.all_reduce(self.flag, group=self.group)
+            _peer_barrier(self.flag, self.group)
         seg, off = self._segments(x)
         n = int(sum(x["rc"]))
         g_recv = torch.empty((n, self.dim), dtype=torch.float32, device=self.device)
@@ -376,6 +387,69 @@ class PeerRows:
                                                   ct.c_void_p(seg.data_ptr()), self.world, n, self.dim,
                                                   ct.c_void_p(g_recv.data_ptr()), stream))
         return g_recv
+
+
+class PeerColumns(PeerRows):
+    """The column-wise exchange fused into the kernels over peer memory (bag size 1): every
+    rank exposes two output buffers [max_rows, D] (alternating per step, so a forward's
+    output stays valid through the next forward) and one gradient buffer [max_rows, D].
+    Forward: `fc_pool_cols_to_peers` writes this rank's column slice of every global
+    occurrence straight into its requester's output (replacing the pooled-columns NCCL
+    all-to-all); a one-element all-reduce orders the writes before anyone reads. Backward:
+    each requester copies its upstream gradient into its shared buffer, a barrier, then
+    `fc_gather_cols_from_peers` pulls this rank's columns of every requester's rows."""
+
+    def __init__(self, dim: int, width: int, col: int, world: int, rank: int, max_rows: int, group, device):
+        import ctypes
+
+        from . import _lib
+        from .errors import check
+
+        self._ct, self._check, self.lib = ctypes, check, _lib.load()
+        self.world, self.rank, self.group, self.device = world, rank, group, torch.device(device)
+        self.max_rows, self.dim, self.width, self.col = int(max_rows), int(dim), int(width), int(col)
+        if self.dim % 4 or self.width % 4 or self.col % 4:
+            raise ValueError("peer column exchange needs column slices in multiples of 4 floats")
+        self._opened = []
+        self.obufs = [torch.empty((self.max_rows, self.dim), dtype=torch.float32, device=self.device)
+                      for _ in range(2)]
+        self.gbuf = torch.empty((self.max_rows, self.dim), dtype=torch.float32, device=self.device)
+        self.dsts = [self._share(b) for b in self.obufs]
+        self.gsrc = self._share(self.gbuf)
+        self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
+        self.zero_off = torch.zeros(world, dtype=torch.int64, device=self.device)
+        self._step = 0
+
+    def pool_cols(self, shard, h, counts, psw):
+        """Forward: returns this rank's [n_local, D] output (a view of a shared buffer)."""
+        ct = self._ct
+        if max(counts) > self.max_rows:
+            raise RuntimeError(f"PeerColumns buffers hold {self.max_rows} rows, a rank sends {max(counts)}")
+        seg = _upload([0] + np.cumsum(counts).tolist(), self.device)
+        dst = self.dsts[self._step & 1]
+        buf = self.obufs[self._step & 1]
+        self._step += 1
+        self._check(self.lib.fc_pool_cols_to_peers(
+            shard.cache.h, ct.c_void_p(h["uslots"].data_ptr()), ct.c_void_p(h["inverse"].data_ptr()), int(h["n"]),
+            ct.c_void_p(seg.data_ptr()), self.world, ct.c_void_p(dst.data_ptr()), ct.c_void_p(self.zero_off.data_ptr()),
+            self.dim, self.col, ct.c_void_p(0 if psw is None else psw.data_ptr()),
+            ct.c_void_p(_raw_stream(self.device.index))))
+        if self.world > 1:  # every rank's column writes land before anyone reads its output
+            _peer_barrier(self.flag, self.group)
+        return buf[:counts[self.rank]], seg
+
+    def grads_cols(self, grad_out, seg, n_global):
+        """Backward: this rank's columns of every requester's gradient rows, [n_global, width]."""
+        ct = self._ct
+        self.gbuf[:grad_out.shape[0]].copy_(grad_out)
+        if self.world > 1:  # every requester's gradient rows are in place
+            _peer_barrier(self.flag, self.group)
+        out = torch.empty((n_global, self.width), dtype=torch.float32, device=self.device)
+        self._check(self.lib.fc_gather_cols_from_peers(
+            ct.c_void_p(self.gsrc.data_ptr()), ct.c_void_p(self.zero_off.data_ptr()), ct.c_void_p(seg.data_ptr()),
+            self.world, int(n_global), self.width, self.dim, self.col, ct.c_void_p(out.data_ptr()),
+            ct.c_void_p(_raw_stream(self.device.index))))
+        return out
 
 
 # ----------------------------------------------------------------------------- row-wise (scaling)
@@ -615,7 +689,8 @@ class ColumnShardedEmbedding(torch.nn.Module):
     miss staging overlap backward(t). The next forward with the same ids commits it.
     Decisions are identical with and without prefetching (the commits are FIFO)."""
 
-    def __init__(self, shard, dim: int, world: int, rank: int, mode: str = "sum", group=None, device=None):
+    def __init__(self, shard, dim: int, world: int, rank: int, mode: str = "sum", group=None, device=None,
+                 peer_rows: int = 0):
         super().__init__()
         self.shard, self.dim, self.world, self.rank = shard, dim, world, rank
         self.plan = partition_columns(dim, world)
@@ -625,6 +700,13 @@ class ColumnShardedEmbedding(torch.nn.Module):
         self._anchor = torch.nn.Parameter(torch.empty(0, device=self.device))
         self._pfq = []  # prefetched batches, oldest first: dicts (src, ids, counts, ev, begun)
         self._xstream = None
+        # peer_rows > 0 (CUDA, bag size 1): the pooled-columns all-to-all and its backward mirror
+        # fused into the kernels over NVLink peer memory (PeerColumns); peer_rows bounds the ids
+        # one rank sends per batch
+        self.peer = None
+        if peer_rows and self.device.type == "cuda":
+            a, b = self.plan.ranges[rank]
+            self.peer = PeerColumns(dim, b - a, a, world, rank, int(peer_rows), group, self.device)
 
     # the two collectives of the column-wise exchange (overridable: the tests drive the module
     # over a CPU-only process group by staging these through host memory)
@@ -727,19 +809,26 @@ class ColumnShardedEmbedding(torch.nn.Module):
         if psw is not None:
             g_psw = self._gather_var(psw.contiguous(), counts, max(counts))
         self.last_info = h.get("info") if isinstance(h, dict) else None
+        if self.peer is not None and offsets is None:  # bag size 1: the all-to-all fused into the gather
+            out, seg = self.peer.pool_cols(self.shard, h, counts, g_psw)
+            return out, (h, None, n_bags, g_psw, seg, int(sum(counts)))
         pooled = self.shard.pool(h, g_off, W * n_bags, False, g_psw, self.mode)  # [W*n_bags, w_r]
         if W == 1:
-            return pooled, (h, g_off, n_bags, g_psw)
+            return pooled, (h, g_off, n_bags, g_psw, None, None)
         w_r = self.widths[self.rank]
         recv = torch.empty(sum(n_bags * w for w in self.widths), dtype=pooled.dtype, device=pooled.device)
         self._alltoall(recv, pooled.reshape(-1).contiguous(), [n_bags * w for w in self.widths], [n_bags * w_r] * W)
         parts = torch.split(recv, [n_bags * w for w in self.widths])
         out = torch.cat([p.reshape(n_bags, w) for p, w in zip(parts, self.widths)], dim=1)
-        return out, (h, g_off, n_bags, g_psw)
+        return out, (h, g_off, n_bags, g_psw, None, None)
 
     def _backward(self, saved, grad_out):
-        h, g_off, n_bags, g_psw = saved
+        h, g_off, n_bags, g_psw, seg, n_global = saved
         W, w_r = self.world, self.widths[self.rank]
+        if seg is not None:  # fused peer-memory path: this rank's columns of every requester's rows
+            recv = self.peer.grads_cols(grad_out.contiguous(), seg, n_global)
+            self.shard.backward(h, recv, None, n_global, False, g_psw, self.mode)
+            return
         if W == 1:
             recv = grad_out.contiguous()
         else:

@@ -100,8 +100,10 @@ def test_column_sharded_bypassed_prefetch_matches_dense():
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("prefetch", [False, True])
-def test_column_sharded_nccl_world1_matches_dense_and_oracle(prefetch):
+@pytest.mark.parametrize("prefetch,peer", [(False, False), (True, False), (True, True)])
+def test_column_sharded_nccl_world1_matches_dense_and_oracle(prefetch, peer):
+    """peer: the pooled columns written by fc_pool_cols_to_peers and the gradients pulled by
+    fc_gather_cols_from_peers (PeerColumns) instead of the NCCL all-to-alls."""
     import torch.distributed as dist
 
     from paper_2208_05321_b200.distributed import ColumnShardedEmbedding
@@ -111,7 +113,9 @@ def test_column_sharded_nccl_world1_matches_dense_and_oracle(prefetch):
         dist.init_process_group("nccl", store=dist.HashStore(), rank=0, world_size=1)
     try:
         shard, idx, rows = build(0, 1, trace, table, "cuda")
-        mod = ColumnShardedEmbedding(shard, DIM, 1, 0, mode="sum", device=torch.device("cuda"))
+        mod = ColumnShardedEmbedding(shard, DIM, 1, 0, mode="sum", device=torch.device("cuda"),
+                                     peer_rows=B if peer else 0)
+        assert (mod.peer is not None) == peer
         dense = table.copy()  # the oracle restatement of torch EmbeddingBag + SGD (float64 gradients)
         slots = oracle_slot_tables(trace)
         moved = 0
@@ -158,7 +162,7 @@ def _staged_module():
     return Staged
 
 
-def _rank_main(rank, world, port, q, prefetch=False):
+def _rank_main(rank, world, port, q, prefetch=False, peer=False):
     import torch.distributed as dist
 
     try:
@@ -167,8 +171,12 @@ def _rank_main(rank, world, port, q, prefetch=False):
         torch.cuda.set_device(0)
         trace, table, grads = workload()
         shard, idx, rows = build(rank, world, trace, table, "cuda:0")
-        mod = _staged_module()(shard, DIM, world, rank, mode="sum", device=torch.device("cuda", 0))
         per = B // world  # this rank's slice of every global batch
+        # peer: pooled columns / gradient columns through CUDA IPC peer pointers between the
+        # two processes (PeerColumns) instead of the staged all-to-all
+        mod = _staged_module()(shard, DIM, world, rank, mode="sum", device=torch.device("cuda", 0),
+                               peer_rows=per if peer else 0)
+        assert (mod.peer is not None) == peer
         slot_tables = []
         outs = []
         tids = [torch.from_numpy(trace[s, rank * per:(rank + 1) * per]).cuda() for s in range(STEPS)]
@@ -193,8 +201,8 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("prefetch", [False, True])
-def test_column_sharded_two_ranks_equal_world1_bitwise(prefetch):
+@pytest.mark.parametrize("prefetch,peer", [(False, False), (True, False), (True, True)])
+def test_column_sharded_two_ranks_equal_world1_bitwise(prefetch, peer):
     import torch.multiprocessing as mp
 
     import paper_2208_05321_b200 as fc
@@ -204,7 +212,7 @@ def test_column_sharded_two_ranks_equal_world1_bitwise(prefetch):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, prefetch)) for r in range(world)]
+    procs = [ctx.Process(target=_rank_main, args=(r, world, port, q, prefetch, peer)) for r in range(world)]
     for p in procs:
         p.start()
     res = dict((r, (rows, st, outs)) for r, rows, st, outs in (q.get(timeout=300) for _ in range(world)))
@@ -230,3 +238,58 @@ def test_column_sharded_two_ranks_equal_world1_bitwise(prefetch):
     torch.cuda.synchronize()
     cat = np.concatenate([res[r][0] for r in range(world)], axis=1)  # column slices, rank order
     assert np.array_equal(cat, m.slow_rows)  # bitwise
+
+
+def test_pool_cols_to_peers_addressing():
+    """fc_pool_cols_to_peers / fc_gather_cols_from_peers with local buffers standing in for
+    three requesters: occurrence i of the global batch (requester r = its segment) lands
+    in r's output row i - seg[r], columns [col, col + width) of ld-wide rows, scaled by psw;
+    the gather reads the same columns back in global order."""
+    import ctypes
+
+    import paper_2208_05321_b200 as fc
+    from paper_2208_05321_b200 import _lib
+
+    lib = _lib.load()
+    num, width, ld, col = 4000, 8, 24, 12
+    idx = fc.IdxMap(np.arange(num), np.arange(num))
+    rows = np.random.default_rng(3).standard_normal((num, width)).astype(np.float32)
+    st = fc.CacheStack(idx, fc.SlowTierStore(rows.copy()), fc.FastTierStore(np.zeros((900, width), np.float32)),
+                       fc.Transmitter())
+    ids = np.random.default_rng(4).integers(0, num, 800)
+    p = st.prepare(ids, 0)
+    seg = np.array([0, 300, 300, 800], dtype=np.int64)  # requester 1 sends nothing
+    W = 3
+    psw = torch.rand(800, device="cuda")
+    outs = [torch.zeros((seg[r + 1] - seg[r] + 2, ld), device="cuda") for r in range(W)]
+    dst = torch.tensor([o.data_ptr() for o in outs], dtype=torch.int64, device="cuda")
+    zero = torch.zeros(W, dtype=torch.int64, device="cuda")
+    seg_d = torch.from_numpy(seg).cuda()
+    dc = st.device
+    rc = lib.fc_pool_cols_to_peers(dc.h, ctypes.c_void_p(p.d_unique_slots.data_ptr()),
+                                   ctypes.c_void_p(p.d_inverse.data_ptr()), 800, ctypes.c_void_p(seg_d.data_ptr()), W,
+                                   ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(zero.data_ptr()), ld, col,
+                                   ctypes.c_void_p(psw.data_ptr()), dc.stream())
+    assert rc == _lib.OK
+    torch.cuda.synchronize()
+    w = psw.cpu().numpy()
+    for r in range(W):
+        got = outs[r].cpu().numpy()
+        a, b = seg[r], seg[r + 1]
+        want = rows[ids[a:b]] * w[a:b, None]
+        assert np.array_equal(got[:b - a, col:col + width], want), r
+        assert not got[:, :col].any() and not got[:, col + width:].any() and not got[b - a:].any(), r
+    # gather the same slice back: global order, [800, width]
+    back = torch.empty((800, width), device="cuda")
+    rc = lib.fc_gather_cols_from_peers(ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(zero.data_ptr()),
+                                       ctypes.c_void_p(seg_d.data_ptr()), W, 800, width, ld, col,
+                                       ctypes.c_void_p(back.data_ptr()), dc.stream())
+    assert rc == _lib.OK
+    torch.cuda.synchronize()
+    assert np.array_equal(back.cpu().numpy(), rows[ids] * w[:, None])
+    # misaligned column slices are refused
+    rc = lib.fc_pool_cols_to_peers(dc.h, ctypes.c_void_p(p.d_unique_slots.data_ptr()),
+                                   ctypes.c_void_p(p.d_inverse.data_ptr()), 800, ctypes.c_void_p(seg_d.data_ptr()), W,
+                                   ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(zero.data_ptr()), ld, 6,
+                                   ctypes.c_void_p(0), dc.stream())
+    assert rc == _lib.ERR_BAD_ARG
