@@ -457,7 +457,8 @@ def launches_per_step(args, shard_mode, pipelined, world):
             return KERNELS_PER_STEP + (PIPELINE_EXTRA_KERNELS if pipelined else 0)
         return KERNELS_PER_TRAIN_STEP + (PIPELINE_EXTRA_KERNELS - PIPELINE_BWD_SAVED if pipelined else 0)
     if shard_mode == "column":  # prepare of the global batch + pool + fused backward (NCCL kernels not counted)
-        return KERNELS_PER_TRAIN_STEP + (PIPELINE_EXTRA_KERNELS - PIPELINE_BWD_SAVED if pipelined else 0)
+        peer = args.peer or (world > 1 and not args.no_peer)  # + the gradient-column gather over peer memory
+        return KERNELS_PER_TRAIN_STEP + (PIPELINE_EXTRA_KERNELS - PIPELINE_BWD_SAVED if pipelined else 0) + int(peer)
     return (SHARDED_BASE_KERNELS + (PIPELINE_EXTRA_KERNELS if pipelined else 0) + (1 if world == 1 else 5)
             + (2 if args.peer else 1))
 
@@ -521,6 +522,9 @@ def run_ours(args, cfg, torch, rank, world):
     elif shard_mode == "column":
         from paper_2208_05321_b200.distributed import ColumnShardedEmbedding, CudaShard
 
+        # the fused peer-memory exchange is the column split's default at N>1 (--no-peer: NCCL)
+        col_peer = args.peer or (world > 1 and not args.no_peer)
+
         # the reference's column-wise split (sharding.py:46-118): every rank caches all rows of its
         # column slice over the GLOBAL batch (identical decisions on every rank)
         lo_c, hi_c = fc.partition_columns(D, world).ranges[rank]
@@ -530,7 +534,9 @@ def run_ours(args, cfg, torch, rank, world):
                           device=dev, engine=args.engine)
         # --peer: the pooled-columns all-to-all and its backward mirror fused into the gather /
         # gradient-pull kernels over NVLink peer memory (PeerColumns) instead of NCCL
-        mod = ColumnShardedEmbedding(shard, D, world, rank, mode=MODE, device=dev, peer_rows=N if args.peer else 0)
+        mod = ColumnShardedEmbedding(shard, D, world, rank, mode=MODE, device=dev, peer_rows=N if col_peer else 0)
+        if col_peer and mod.peer is None:
+            log(f"[bench] rank {rank}: {mod.peer_error}")
         dcs = [shard.cache]
     else:
         from paper_2208_05321_b200.distributed import (CudaShard, RowShardedEmbedding, shard_rows_for_rank,
@@ -774,7 +780,8 @@ def run_ours(args, cfg, torch, rank, world):
                                         ) if shard_mode != "column" else
                            ("all-gather of ids; pooled columns written into the requesters' outputs over peer memory "
                             "(fc_pool_cols_to_peers), gradient columns pulled back (fc_gather_cols_from_peers)"
-                            if args.peer else "all-gather of ids; pooled columns by NCCL all-to-all (reference semantics)"),
+                            if getattr(mod, "peer", None) is not None
+                            else "all-gather of ids; pooled columns by NCCL all-to-all (reference semantics)"),
                            "capacity_per_gpu": cap},
         "step_latency_ms": {"p50": float(np.percentile(step_ms, 50)), "p99": float(np.percentile(step_ms, 99)),
                             "prepare_avg": (None if pipelined else prof["prepare_ms"] / max(prof["calls"], 1)),
@@ -1031,7 +1038,9 @@ def main():
                     help="sharded runs: the return exchange fused into the owners' kernels over NVLink peer memory "
                          "(CUDA IPC) instead of the NCCL all-to-all (row-wise: looked-up rows; column-wise: pooled "
                          "column slices and the gradients' columns)")
-    ap.add_argument("--no-peer", action="store_true", help="(default) rows come back by NCCL all-to-all")
+    ap.add_argument("--no-peer", action="store_true",
+                    help="column-wise at N>1: the NCCL all-to-alls instead of the fused peer-memory exchange "
+                         "(row-wise always uses NCCL unless --peer)")
     ap.add_argument("--no-prefetch", action="store_true",
                     help="synchronous prepare each step (no lookahead pipeline)")
     ap.add_argument("--engine", default="async", choices=["async", "zerocopy"],

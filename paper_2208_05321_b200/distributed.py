@@ -220,6 +220,28 @@ def _upload(vals, device):
     return t.pin_memory().to(device, non_blocking=True)
 
 
+def _agreed_peer(make, world, group, device):
+    """Build a peer-memory exchange on every rank, or on none: a rank whose setup fails (an
+    IPC mapping refused, buffers that do not fit) reports it, all ranks agree with a MIN
+    all-reduce, and the modules then keep their NCCL path."""
+    peer, ok = None, 1
+    try:
+        peer = make()
+    except (RuntimeError, ValueError) as e:
+        ok = 0
+        import warnings
+
+        warnings.warn(f"peer-memory exchange not set up: {e}")
+    if world > 1:
+        t = torch.tensor([ok], dtype=torch.int32, device=device if dist.get_backend(group) == "nccl" else "cpu")
+        dist.all_reduce(t, op=dist.ReduceOp.MIN, group=group)
+        ok = int(t.item())
+    if not ok and peer is not None:
+        peer.close()
+        peer = None
+    return peer
+
+
 def _peer_barrier(flag, group=None):
     """Stream-ordered barrier after peer-memory writes: a one-element NCCL all-reduce on the
     current stream (every rank's earlier kernels finish before it completes anywhere). A
@@ -305,17 +327,22 @@ class PeerRows:
         self.gbuf = torch.empty((self.max_rows, self.dim), dtype=torch.float32, device=self.device)
         self.dst = self._share(self.rbuf)
         self.gsrc = self._share(self.gbuf)
+        self._raise_if_failed()
         self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
 
     def _share(self, buf):
-        """Every rank's pointer to its peers' copy of `buf` (CUDA IPC), as a device array."""
+        """Every rank's pointer to its peers' copy of `buf` (CUDA IPC), as a device array.
+        A rank that cannot export its handle still joins the exchange (sending None), so
+        every rank raises together instead of leaving the others in the collective."""
         from . import _lib
 
         ct = self._ct
         hd = (ct.c_ubyte * _lib.IPC_HANDLE_BYTES)()
-        self._check(self.lib.fc_ipc_handle(ct.c_void_p(buf.data_ptr()), hd))
+        mine = bytes(hd) if self.lib.fc_ipc_handle(ct.c_void_p(buf.data_ptr()), hd) == _lib.OK else None
         handles = [None] * self.world
-        dist.all_gather_object(handles, bytes(hd), group=self.group)
+        dist.all_gather_object(handles, mine, group=self.group)
+        if any(h is None for h in handles):
+            raise RuntimeError("a rank could not export a CUDA IPC handle for the peer exchange")
         ptrs = []
         for r in range(self.world):
             if r == self.rank:
@@ -323,10 +350,18 @@ class PeerRows:
                 continue
             p = ct.c_void_p()
             hb = (ct.c_ubyte * _lib.IPC_HANDLE_BYTES).from_buffer_copy(handles[r])
-            self._check(self.lib.fc_ipc_open(hb, self.device.index or 0, ct.byref(p)))
+            if self.lib.fc_ipc_open(hb, self.device.index or 0, ct.byref(p)) != _lib.OK:
+                self._failed = True  # raised after every exchange, so no rank leaves a collective early
+                ptrs.append(0)
+                continue
             self._opened.append(p)
             ptrs.append(p.value)
         return torch.tensor(ptrs, dtype=torch.int64, device=self.device)
+
+    def _raise_if_failed(self):
+        if getattr(self, "_failed", False):
+            self.close()
+            raise RuntimeError("could not map a peer's buffer (CUDA IPC)")
 
     def close(self):
         for p in getattr(self, "_opened", []):
@@ -416,6 +451,7 @@ class PeerColumns(PeerRows):
         self.gbuf = torch.empty((self.max_rows, self.dim), dtype=torch.float32, device=self.device)
         self.dsts = [self._share(b) for b in self.obufs]
         self.gsrc = self._share(self.gbuf)
+        self._raise_if_failed()
         self.flag = torch.zeros(1, dtype=torch.int32, device=self.device)
         self.zero_off = torch.zeros(world, dtype=torch.int64, device=self.device)
         self._step = 0
@@ -704,9 +740,13 @@ class ColumnShardedEmbedding(torch.nn.Module):
         # fused into the kernels over NVLink peer memory (PeerColumns); peer_rows bounds the ids
         # one rank sends per batch
         self.peer = None
+        self.peer_error = None
         if peer_rows and self.device.type == "cuda":
             a, b = self.plan.ranges[rank]
-            self.peer = PeerColumns(dim, b - a, a, world, rank, int(peer_rows), group, self.device)
+            self.peer = _agreed_peer(lambda: PeerColumns(dim, b - a, a, world, rank, int(peer_rows), group,
+                                                         self.device), world, group, self.device)
+            if self.peer is None:
+                self.peer_error = "peer exchange unavailable on some rank; NCCL all-to-all used"
 
     # the two collectives of the column-wise exchange (overridable: the tests drive the module
     # over a CPU-only process group by staging these through host memory)

@@ -293,3 +293,26 @@ def test_pool_cols_to_peers_addressing():
                                    ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(zero.data_ptr()), ld, 6,
                                    ctypes.c_void_p(0), dc.stream())
     assert rc == _lib.ERR_BAD_ARG
+
+
+def test_column_peer_falls_back_to_nccl_on_unaligned_slices():
+    """A column slice that is not a multiple of 4 floats cannot use the peer kernels: the
+    module warns and keeps the NCCL all-to-all path (forward only here: the CUDA backward
+    itself needs rows of a multiple of 4 floats)."""
+    import warnings
+
+    import paper_2208_05321_b200 as fc
+    from paper_2208_05321_b200.distributed import ColumnShardedEmbedding, CudaShard
+    from paper_2208_05321_b200.store import pinned_empty
+
+    num, dim = 2_000, 10
+    rows = pinned_empty((num, dim))
+    rows[...] = np.random.default_rng(0).standard_normal((num, dim)).astype(np.float32)
+    shard = CudaShard(num, dim, 500, rows, fc.IdxMap(np.arange(num), np.arange(num)), lr=0.1, device="cuda")
+    with warnings.catch_warnings(record=True) as w:
+        warnings.simplefilter("always")
+        mod = ColumnShardedEmbedding(shard, dim, 1, 0, device=torch.device("cuda"), peer_rows=256)
+    assert mod.peer is None and mod.peer_error and any("peer-memory exchange" in str(x.message) for x in w)
+    ids = torch.arange(0, 200, device="cuda")
+    out = mod(ids)
+    np.testing.assert_array_equal(out.detach().cpu().numpy(), rows[:200])
