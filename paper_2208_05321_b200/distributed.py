@@ -536,8 +536,9 @@ class RowShardedEmbedding(torch.nn.Module):
                 raise ValueError("RowShardedEmbedding on CUDA needs shard.global_num_ids (the whole table's id "
                                  "space) for the libfreqcache_b200 router")
             self.router = Router(num_ids, world, self.device, placement)
-            if peer_rows:  # fused return exchange over NVLink peer memory (PeerRows)
-                self.peer = PeerRows(shard, world, rank, int(peer_rows), group, self.device)
+            if peer_rows:  # fused return exchange over NVLink peer memory (PeerRows); all ranks or none
+                self.peer = _agreed_peer(lambda: PeerRows(shard, world, rank, int(peer_rows), group, self.device),
+                                         world, group, self.device)
 
     @staticmethod
     def owner_of(ids, world):
