@@ -477,9 +477,10 @@ class PeerColumns(PeerRows):
     def grads_cols(self, grad_out, seg, n_global):
         """Backward: this rank's columns of every requester's gradient rows, [n_global, width]."""
         ct = self._ct
+        if self.world == 1:  # one rank holds every column of every row: the gradient is its own
+            return grad_out
         self.gbuf[:grad_out.shape[0]].copy_(grad_out)
-        if self.world > 1:  # every requester's gradient rows are in place
-            _peer_barrier(self.flag, self.group)
+        _peer_barrier(self.flag, self.group)  # every requester's gradient rows are in place
         out = torch.empty((n_global, self.width), dtype=torch.float32, device=self.device)
         self._check(self.lib.fc_gather_cols_from_peers(
             ct.c_void_p(self.gsrc.data_ptr()), ct.c_void_p(self.zero_off.data_ptr()), ct.c_void_p(seg.data_ptr()),
