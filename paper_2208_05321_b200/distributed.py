@@ -339,8 +339,10 @@ class PeerRows:
         ct = self._ct
         hd = (ct.c_ubyte * _lib.IPC_HANDLE_BYTES)()
         mine = bytes(hd) if self.lib.fc_ipc_handle(ct.c_void_p(buf.data_ptr()), hd) == _lib.OK else None
-        handles = [None] * self.world
-        dist.all_gather_object(handles, mine, group=self.group)
+        handles = [mine]
+        if self.world > 1:
+            handles = [None] * self.world
+            dist.all_gather_object(handles, mine, group=self.group)
         if any(h is None for h in handles):
             raise RuntimeError("a rank could not export a CUDA IPC handle for the peer exchange")
         ptrs = []
